@@ -1,0 +1,321 @@
+/*
+ * pfs_oracle.c — CPU restatement of the reference's bulk Pauli-frame sampler.
+ *
+ * TEST INFRASTRUCTURE / CPU BASELINE ONLY.  Only tests/, __graft_entry__.smoke()
+ * and bench.py's cpu_baseline / --impl reference legs may load this library;
+ * the product path (paper_2103_02202_b200/) never links or calls it.
+ *
+ * It restates, over uint32 shot words instead of Python ints:
+ *   FrameBatch.__init__            stabsim/frame_sim.py:29-40   (x = 0, z = coins)
+ *   _apply_plan per frame rule     stabsim/frame_sim.py:64-72   + gates.py:326-348
+ *   measure / reset / measure_reset stabsim/frame_sim.py:74-90
+ *   apply_noise geometric walk     stabsim/frame_sim.py:92-153  + entropy.py:65-88
+ *   _run_batch opcode loop         stabsim/frame_sim.py:192-205
+ *   detector_events                stabsim/io_formats.py:208-227
+ *   transposed + write_b8          stabsim/bitvec.py:193-209, io_formats.py:94-96
+ *
+ * Randomness comes from one of two sources:
+ *   - injected rows (coins + noise masks) — bit-exact
+ *     against the reference's own FrameBatch (tests/golden/inject_*.npz);
+ *   - counter-based Philox4x32-10 with the chunked geometric walk documented in
+ *     the same draws the CUDA kernels make, so the GPU's sampled
+ *     mode is bit-exact against this file as well as statistically matched to the
+ *     reference (tests/golden/stats_*.npz).
+ *
+ * Parity pinned by: tests/golden/{inject,noiseless,stats,exact}_* generated from
+ * the reference itself (tests/golden/make_golden.py).
+ */
+#include <math.h>
+#include <pthread.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+enum { K_GATE = 0, K_M = 1, K_R = 2, K_MR = 3, K_NOISE = 4, K_DET = 5, K_OBS = 6 };
+enum { R_NONE = 0, R_SWAPXZ = 1, R_ZXORX = 2, R_XXORZ = 3, R_CX = 4, R_CZ = 5, R_CY = 6, R_SWAP = 7 };
+enum { CH_XERR = 0, CH_YERR = 1, CH_ZERR = 2, CH_DEP1 = 3, CH_DEP2 = 4 };
+
+typedef struct {
+    int32_t kind, code, n_targets, tgt_off, rec_base, coin_base, noise_row_base, aux;
+} orc_instr;
+
+/* ---------------- Philox4x32-10 (Salmon et al., SC'11) ---------------- */
+static inline void philox_round(uint32_t c[4], const uint32_t k[2]) {
+    uint64_t p0 = (uint64_t)0xD2511F53u * c[0];
+    uint64_t p1 = (uint64_t)0xCD9E8D57u * c[2];
+    uint32_t hi0 = (uint32_t)(p0 >> 32), lo0 = (uint32_t)p0;
+    uint32_t hi1 = (uint32_t)(p1 >> 32), lo1 = (uint32_t)p1;
+    uint32_t n0 = hi1 ^ c[1] ^ k[0];
+    uint32_t n2 = hi0 ^ c[3] ^ k[1];
+    c[0] = n0; c[1] = lo1; c[2] = n2; c[3] = lo0;
+}
+
+void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    uint32_t k[2] = {key[0], key[1]};
+    for (int r = 0; r < 10; r++) {
+        philox_round(c, k);
+        if (r < 9) { k[0] += 0x9E3779B9u; k[1] += 0xBB67AE85u; }
+    }
+    out[0] = c[0]; out[1] = c[1]; out[2] = c[2]; out[3] = c[3];
+}
+
+#define DOMAIN_COIN 0x40000000u
+#define DOMAIN_NOISE 0x80000000u
+
+typedef struct {
+    const orc_instr* ins; int64_t n_ins;
+    const int32_t* targets;
+    const double* noise_p; const double* noise_log1m; const int32_t* noise_k;
+    int32_t num_qubits; int64_t num_meas;
+    const int64_t* det_ptr; const int64_t* det_idx; int64_t num_cols;
+    int64_t num_shots; int32_t T; uint64_t seed; uint64_t tile_offset;
+    const uint32_t* coins; const uint32_t* masks; int64_t inject_words;
+    uint32_t* flips; uint32_t* events; int64_t out_words;
+    int64_t n_tiles; int nthreads;
+} orc_job;
+
+typedef struct { const orc_job* job; int tid; int rc; } orc_worker;
+
+static const uint8_t DEP1_X[3] = {1, 1, 0}, DEP1_Z[3] = {0, 1, 1};
+
+static inline void pattern_of(int ch, uint32_t pick, uint32_t* xm, uint32_t* zm) {
+    switch (ch) {
+        case CH_XERR: *xm = 1; *zm = 0; return;
+        case CH_YERR: *xm = 1; *zm = 1; return;
+        case CH_ZERR: *xm = 0; *zm = 1; return;
+        case CH_DEP1: *xm = DEP1_X[pick]; *zm = DEP1_Z[pick]; return;
+        default: {  /* DEPOLARIZE2 code = pick + 1, gates.py:354-360 */
+            uint32_t code = pick + 1;
+            *xm = (code & 1) | (((code >> 2) & 1) << 1);
+            *zm = ((code >> 1) & 1) | (((code >> 3) & 1) << 1);
+        }
+    }
+}
+
+/* coin word w (32 shots) of coin row e for global tile g */
+static inline void coin_words(const orc_job* jb, int64_t e, uint64_t g, int64_t local_tile,
+                              int nw, uint32_t* dst) {
+    if (jb->coins) {
+        const uint32_t* src = jb->coins + e * jb->inject_words + local_tile * nw;
+        memcpy(dst, src, sizeof(uint32_t) * nw);
+        return;
+    }
+    uint32_t key[2] = {(uint32_t)jb->seed, (uint32_t)(jb->seed >> 32)};
+    for (int c = 0; c * 4 < nw; c++) {
+        uint32_t ctr[4] = {(uint32_t)e, (uint32_t)c, (uint32_t)g, DOMAIN_COIN};
+        uint32_t o[4];
+        orc_philox4x32_10(ctr, key, o);
+        for (int j = 0; j < 4 && c * 4 + j < nw; j++) dst[c * 4 + j] = o[j];
+    }
+}
+
+static void run_tile(const orc_job* jb, int64_t t, uint32_t* x, uint32_t* z, uint32_t* rec,
+                     uint32_t* tmp) {
+    const int nw = jb->T / 32;
+    const int n = jb->num_qubits;
+    const uint64_t g = jb->tile_offset + (uint64_t)t;
+    /* FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39) */
+    memset(x, 0, sizeof(uint32_t) * (size_t)n * nw);
+    for (int q = 0; q < n; q++) coin_words(jb, q, g, t, nw, z + (size_t)q * nw);
+    const uint32_t key[2] = {(uint32_t)jb->seed, (uint32_t)(jb->seed >> 32)};
+
+    for (int64_t i = 0; i < jb->n_ins; i++) {
+        const orc_instr* in = &jb->ins[i];
+        const int32_t* tg = jb->targets + in->tgt_off;
+        switch (in->kind) {
+        case K_GATE: {
+            int ar = (in->code >= R_CX) ? 2 : 1;
+            for (int a = 0; a + ar <= in->n_targets; a += ar) {
+                uint32_t* x0 = x + (size_t)tg[a] * nw; uint32_t* z0 = z + (size_t)tg[a] * nw;
+                uint32_t* x1 = ar == 2 ? x + (size_t)tg[a + 1] * nw : NULL;
+                uint32_t* z1 = ar == 2 ? z + (size_t)tg[a + 1] * nw : NULL;
+                switch (in->code) {
+                case R_SWAPXZ: for (int w = 0; w < nw; w++) { uint32_t v = x0[w]; x0[w] = z0[w]; z0[w] = v; } break;
+                case R_ZXORX: for (int w = 0; w < nw; w++) z0[w] ^= x0[w]; break;
+                case R_XXORZ: for (int w = 0; w < nw; w++) x0[w] ^= z0[w]; break;
+                case R_CX: for (int w = 0; w < nw; w++) { x1[w] ^= x0[w]; z0[w] ^= z1[w]; } break;
+                case R_CZ: for (int w = 0; w < nw; w++) { uint32_t a0 = x0[w], a1 = x1[w]; z0[w] ^= a1; z1[w] ^= a0; } break;
+                case R_CY: for (int w = 0; w < nw; w++) {
+                        uint32_t ox0 = x0[w], ox1 = x1[w], oz1 = z1[w];
+                        z0[w] ^= ox1 ^ oz1; z1[w] = oz1 ^ ox0; x1[w] = ox1 ^ ox0; } break;
+                case R_SWAP: for (int w = 0; w < nw; w++) {
+                        uint32_t v = x0[w]; x0[w] = x1[w]; x1[w] = v;
+                        v = z0[w]; z0[w] = z1[w]; z1[w] = v; } break;
+                default: break;
+                }
+            }
+            break;
+        }
+        case K_M: case K_R: case K_MR: {
+            for (int j = 0; j < in->n_targets; j++) {
+                uint32_t* xq = x + (size_t)tg[j] * nw; uint32_t* zq = z + (size_t)tg[j] * nw;
+                if (in->kind == K_M) {
+                    memcpy(rec + (size_t)(in->rec_base + j) * nw, xq, sizeof(uint32_t) * nw);
+                    coin_words(jb, (int64_t)in->coin_base + j, g, t, nw, tmp);
+                    for (int w = 0; w < nw; w++) zq[w] ^= tmp[w];
+                } else if (in->kind == K_R) {
+                    memset(xq, 0, sizeof(uint32_t) * nw);
+                    coin_words(jb, (int64_t)in->coin_base + j, g, t, nw, zq);
+                } else {
+                    memcpy(rec + (size_t)(in->rec_base + j) * nw, xq, sizeof(uint32_t) * nw);
+                    /* the measure's coin row (coin_base + 2j) is overwritten by the reset's */
+                    memset(xq, 0, sizeof(uint32_t) * nw);
+                    coin_words(jb, (int64_t)in->coin_base + 2 * j + 1, g, t, nw, zq);
+                }
+            }
+            break;
+        }
+        case K_NOISE: {
+            const int ar = in->code == CH_DEP2 ? 2 : 1;
+            const int64_t nid = in->aux;
+            if (jb->masks) {
+                for (int j = 0; j < in->n_targets; j++) {
+                    const uint32_t* mx = jb->masks + ((int64_t)in->noise_row_base + 2 * j) * jb->inject_words + t * nw;
+                    const uint32_t* mz = mx + jb->inject_words;
+                    uint32_t* xq = x + (size_t)tg[j] * nw; uint32_t* zq = z + (size_t)tg[j] * nw;
+                    for (int w = 0; w < nw; w++) { xq[w] ^= mx[w]; zq[w] ^= mz[w]; }
+                }
+                break;
+            }
+            const double p = jb->noise_p[nid];
+            if (p <= 0.0) break;
+            const double log1m = jb->noise_log1m[nid];
+            const int64_t A = in->n_targets / ar;
+            const int64_t k = jb->noise_k[nid];
+            const int64_t T = jb->T;
+            const uint32_t npat = in->code == CH_DEP1 ? 3u : (in->code == CH_DEP2 ? 15u : 1u);
+            for (int64_t r = 0; r * k < A; r++) {
+                const int64_t a0 = r * k;
+                const int64_t apps = (A - a0) < k ? (A - a0) : k;
+                const int64_t len = apps * T;
+                int64_t pos = -1;
+                for (uint32_t j = 0;; j++) {
+                    uint32_t ctr[4] = {j, (uint32_t)r, (uint32_t)g, DOMAIN_NOISE | (uint32_t)nid};
+                    uint32_t o[4];
+                    orc_philox4x32_10(ctr, key, o);
+                    /* u in (0, 1]; gap as in sample_hits_geometric (entropy.py:82-85) */
+                    uint64_t m53 = ((uint64_t)o[0] << 21) | (o[1] >> 11);
+                    double u = (double)(m53 + 1) * 0x1.0p-53;
+                    double gap = p >= 1.0 ? 0.0 : floor(log(u) / log1m);
+                    if (gap >= (double)(len - 1 - pos)) break;
+                    pos += (int64_t)gap + 1;
+                    uint32_t pick = (uint32_t)(((uint64_t)o[2] * npat) >> 32);
+                    uint32_t xm, zm;
+                    pattern_of(in->code, pick, &xm, &zm);
+                    const int64_t app = a0 + pos / T;
+                    const int64_t s = pos % T;
+                    const uint32_t bit = 1u << (s & 31);
+                    const int64_t w = s >> 5;
+                    for (int sl = 0; sl < ar; sl++) {
+                        int32_t q = tg[app * ar + sl];
+                        if ((xm >> sl) & 1) x[(size_t)q * nw + w] ^= bit;
+                        if ((zm >> sl) & 1) z[(size_t)q * nw + w] ^= bit;
+                    }
+                }
+            }
+            break;
+        }
+        default: break;  /* K_DET / K_OBS evaluated below from the full record */
+        }
+    }
+
+    /* tail mask for shots past num_shots in the last tile */
+    int64_t first_shot = t * (int64_t)jb->T;
+    for (int w = 0; w < nw; w++) {
+        int64_t s0 = first_shot + 32 * (int64_t)w;
+        uint32_t m = s0 >= jb->num_shots ? 0u
+                   : (jb->num_shots - s0 >= 32 ? 0xFFFFFFFFu : ((1u << (jb->num_shots - s0)) - 1u));
+        tmp[w] = m;
+    }
+    if (jb->flips) {
+        for (int64_t m = 0; m < jb->num_meas; m++)
+            for (int w = 0; w < nw; w++)
+                jb->flips[m * jb->out_words + t * nw + w] = rec[(size_t)m * nw + w] & tmp[w];
+    }
+    if (jb->events) {
+        /* detector_events: XOR of flip bits per detector (io_formats.py:208-227) */
+        for (int64_t d = 0; d < jb->num_cols; d++) {
+            uint32_t* dst = jb->events + d * jb->out_words + t * nw;
+            for (int w = 0; w < nw; w++) dst[w] = 0;
+            for (int64_t e = jb->det_ptr[d]; e < jb->det_ptr[d + 1]; e++) {
+                const uint32_t* src = rec + (size_t)jb->det_idx[e] * nw;
+                for (int w = 0; w < nw; w++) dst[w] ^= src[w];
+            }
+            for (int w = 0; w < nw; w++) dst[w] &= tmp[w];
+        }
+    }
+}
+
+static void* worker_main(void* arg) {
+    orc_worker* wk = (orc_worker*)arg;
+    const orc_job* jb = wk->job;
+    const int nw = jb->T / 32;
+    size_t nq = (size_t)jb->num_qubits * nw;
+    uint32_t* x = (uint32_t*)malloc(sizeof(uint32_t) * (nq + 1));
+    uint32_t* z = (uint32_t*)malloc(sizeof(uint32_t) * (nq + 1));
+    uint32_t* rec = (uint32_t*)malloc(sizeof(uint32_t) * ((size_t)jb->num_meas * nw + 1));
+    uint32_t* tmp = (uint32_t*)malloc(sizeof(uint32_t) * (nw + 4));
+    if (!x || !z || !rec || !tmp) { wk->rc = -2; free(x); free(z); free(rec); free(tmp); return NULL; }
+    for (int64_t t = wk->tid; t < jb->n_tiles; t += jb->nthreads) run_tile(jb, t, x, z, rec, tmp);
+    free(x); free(z); free(rec); free(tmp);
+    wk->rc = 0;
+    return NULL;
+}
+
+/*
+ * Sample num_shots shots.  Outputs are row-major bit tables [rows][out_words]
+ * (shot s = bit s%32 of word s/32) for measurement flips and/or detection events
+ * (detector columns then observables).  Returns 0 or a negative error code.
+ */
+int orc_sample(const orc_instr* ins, int64_t n_ins, const int32_t* targets,
+               const double* noise_p, const double* noise_log1m, const int32_t* noise_k,
+               int32_t num_qubits, int64_t num_meas,
+               const int64_t* det_ptr, const int64_t* det_idx, int64_t num_cols,
+               int64_t num_shots, int32_t tile_shots, uint64_t seed, uint64_t tile_offset,
+               const uint32_t* coins, const uint32_t* masks, int64_t inject_words,
+               uint32_t* flips, uint32_t* events, int64_t out_words, int nthreads) {
+    if (tile_shots <= 0 || tile_shots % 32) return -1;
+    if (num_shots < 1) return -1;
+    orc_job jb = {ins, n_ins, targets, noise_p, noise_log1m, noise_k, num_qubits, num_meas,
+                  det_ptr, det_idx, num_cols, num_shots, tile_shots, seed, tile_offset,
+                  coins, masks, inject_words, flips, events, out_words,
+                  (num_shots + tile_shots - 1) / tile_shots, nthreads < 1 ? 1 : nthreads};
+    if (out_words < jb.n_tiles * (tile_shots / 32)) return -3;
+    if ((coins || masks) && inject_words < jb.n_tiles * (tile_shots / 32)) return -4;
+    int nth = jb.nthreads;
+    if (nth > jb.n_tiles) { nth = (int)jb.n_tiles; jb.nthreads = nth; }
+    orc_worker* wk = (orc_worker*)calloc((size_t)nth, sizeof(orc_worker));
+    pthread_t* th = (pthread_t*)calloc((size_t)nth, sizeof(pthread_t));
+    if (!wk || !th) { free(wk); free(th); return -2; }
+    for (int i = 0; i < nth; i++) {
+        wk[i].job = &jb; wk[i].tid = i; wk[i].rc = -5;
+        if (nth == 1) worker_main(&wk[i]);
+        else pthread_create(&th[i], NULL, worker_main, &wk[i]);
+    }
+    int rc = 0;
+    for (int i = 0; i < nth; i++) {
+        if (nth > 1) pthread_join(th[i], NULL);
+        if (wk[i].rc) rc = wk[i].rc;
+    }
+    free(wk); free(th);
+    return rc;
+}
+
+/*
+ * Row-major bit table -> shot-major b8 bytes (bitvec.transposed + write_b8):
+ * out[s * pitch + r/8] bit r%8 = rows[r][s] ^ xor_bits[r] (xor_bits may be NULL).
+ */
+void orc_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t num_shots, int64_t row_words,
+                    const uint8_t* xor_bits, uint8_t* out, int64_t pitch) {
+    int64_t nb = (num_rows + 7) / 8;
+    for (int64_t s = 0; s < num_shots; s++) memset(out + s * pitch, 0, (size_t)nb);
+    for (int64_t r = 0; r < num_rows; r++) {
+        const uint32_t* row = rows + r * row_words;
+        uint8_t flip = xor_bits ? (xor_bits[r] & 1) : 0;
+        for (int64_t s = 0; s < num_shots; s++) {
+            uint8_t b = (uint8_t)(((row[s >> 5] >> (s & 31)) & 1) ^ flip);
+            out[s * pitch + (r >> 3)] |= (uint8_t)(b << (r & 7));
+        }
+    }
+}
