@@ -1,0 +1,139 @@
+/*
+ * pfs.h — C-ABI of the B200 bulk Pauli-frame sampler (libpfs.so).
+ *
+ * The reference (stabsim, pure Python) has no native FFI; this ABI is what its
+ * Python entry points would bind through ctypes to replace the hot path:
+ *
+ *   pfs_program_create   replaces  compile_frame_program     stabsim/frame_sim.py:170-189
+ *                        (plus the record/detector bookkeeping of circuit.detector_sets,
+ *                         stabsim/circuit.py:247-256)
+ *   pfs_run (FLIPS)      replaces  collect_flips             stabsim/frame_sim.py:208-229
+ *                        (FrameBatch + _run_batch + _transpose_flips, frame_sim.py:26-239)
+ *   pfs_run (SAMPLES)    replaces  sample_batch              stabsim/frame_sim.py:242-258
+ *   pfs_run (DETECTORS)  replaces  collect_flips + detector_events
+ *                                                            stabsim/io_formats.py:208-227
+ *   pfs_run (COUNTS)     new: per-column event counts (no output I/O; BASELINE config 3)
+ *   pfs_last_error       error text (the reference raises ValueError, frame_sim.py:30-31,
+ *                        211-212, 247-250; the ctypes shim re-raises it)
+ *
+ * All arguments are plain pointers and sizes.  Return value: 0 on success, a
+ * negative PFS_E* code on failure with a thread-local message in pfs_last_error().
+ * Threading: a program handle is bound to one device; do not run one handle on two
+ * streams concurrently.  Ownership: the caller owns every input and output buffer;
+ * the handle owns its device copies.
+ */
+#ifndef PFS_H
+#define PFS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Flat instruction row (int32 x 8), produced by paper_2103_02202_b200/program.py.
+ * kind: 0 gate (code = frame rule), 1 M, 2 R, 3 MR, 4 noise (code = channel),
+ *       5 DETECTOR (aux = column), 6 OBSERVABLE_INCLUDE (aux = column,
+ *       targets = absolute record indices). */
+typedef struct pfs_instr {
+    int32_t kind, code, n_targets, tgt_off, rec_base, coin_base, noise_row_base, aux;
+} pfs_instr;
+
+typedef struct pfs_options {
+    int32_t words_per_tile;   /* W: 32-shot words per CTA tile (0 = auto)          */
+    int32_t ring_in_smem;     /* -1 auto, 0 global-memory record ring, 1 shared     */
+    int32_t threads;          /* threads per CTA (0 = auto)                         */
+    int32_t ctas_per_sm;      /* persistent grid = SMs x this (0 = auto)            */
+    double noise_target_hits; /* expected hits per geometric-walk chunk (0 = 1.0)   */
+    int32_t timing;           /* 1: record per-kernel CUDA-event times in pfs_run  */
+    int32_t reserved[7];
+} pfs_options;
+
+typedef struct pfs_info {
+    int32_t num_qubits;
+    int32_t words_per_tile;   /* W */
+    int32_t tile_shots;       /* T = 32 W */
+    int32_t threads;
+    int32_t ring_in_smem;
+    int32_t smem_bytes;       /* dynamic shared memory per CTA */
+    int64_t num_measurements;
+    int64_t num_columns;      /* detectors + observables */
+    int64_t num_observables;
+    int64_t num_ops;          /* device ops after splitting/merging */
+    int64_t num_barriers;     /* __syncthreads between ops per tile */
+    int64_t num_slots;        /* record ring slots (incl. observable accumulators) */
+    int64_t num_noise;
+    int64_t bframe_bits;      /* algorithmic frame bits per shot */
+    int64_t num_coin_rows;
+    int64_t num_noise_rows;
+    int64_t reserved[6];
+} pfs_info;
+
+enum pfs_mode {
+    PFS_MODE_FLIPS = 0,          /* shot-major b8 measurement flips                 */
+    PFS_MODE_SAMPLES = 1,        /* shot-major b8 flips XOR reference sample         */
+    PFS_MODE_DETECTORS = 2,      /* shot-major b8 detection events (+ observables)  */
+    PFS_MODE_COUNTS = 3,         /* uint64 event count per column                   */
+    PFS_MODE_FLIPS_ROWS = 4,     /* measurement-major uint32 rows [M][ceil(S/32)]   */
+    PFS_MODE_DETECTORS_ROWS = 5  /* column-major uint32 rows [D][ceil(S/32)]        */
+};
+
+enum pfs_error {
+    PFS_OK = 0,
+    PFS_E_INVALID = -1,   /* bad argument (maps to ValueError)   */
+    PFS_E_CUDA = -2,      /* CUDA runtime failure                */
+    PFS_E_NOMEM = -3,     /* host/device allocation failure      */
+    PFS_E_NODEVICE = -4   /* no CUDA device / extension unusable */
+};
+
+int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs,
+                       const int32_t* targets, int64_t n_targets,
+                       const double* noise_p, int64_t n_noise,
+                       const int64_t* det_ptr, const int64_t* det_idx,
+                       int64_t n_columns, int64_t n_observables,
+                       int32_t num_qubits, int64_t num_measurements,
+                       int64_t num_coin_rows, int64_t num_noise_rows,
+                       const pfs_options* options_or_null, struct pfs_program** out);
+
+int pfs_program_info(const struct pfs_program* prog, pfs_info* out);
+
+/* Apps per geometric-walk chunk for each noise instruction (n = num_noise). */
+int pfs_program_noise_chunks(const struct pfs_program* prog, int32_t* out, int64_t n);
+
+/*
+ * Sample num_shots shots [shot_offset, shot_offset + num_shots) on `device`.
+ * shot_offset must be a multiple of the tile size T (pfs_info.tile_shots); the
+ * counter-based RNG is keyed by (seed, global tile, event), so results do not
+ * depend on how a shot range is split across calls or GPUs.
+ *
+ * ref_bits: uint8[num_measurements] reference sample (SAMPLES only).
+ * inject_coins / inject_noise: both NULL (Philox mode) or both set (injected
+ * mode): uint32 rows [num_coin_rows | num_noise_rows][inject_row_words], shot s
+ * of a row at bit s%32 of word s/32.
+ * out: host or device pointer (detected).  b8 modes write num_shots rows of
+ * out_pitch bytes (out_pitch >= ceil(R/8); 0 = exactly ceil(R/8));
+ * COUNTS writes uint64[num_columns]; *_ROWS write rows of ceil(num_shots/32) words.
+ * stream: cudaStream_t (NULL = legacy default stream).  Host outputs are complete
+ * when pfs_run returns; device outputs are complete in stream order.
+ */
+int pfs_run(struct pfs_program* prog, int device, uint64_t seed, uint64_t shot_offset,
+            int64_t num_shots, int mode, const uint8_t* ref_bits,
+            const uint32_t* inject_coins, const uint32_t* inject_noise,
+            int64_t inject_row_words, void* out, int64_t out_bytes, int64_t out_pitch,
+            void* stream);
+
+/* Per-kernel times (ms) of the last pfs_run when options.timing = 1:
+ * [0] frame program kernel, [1] transpose kernel, [2] H2D, [3] D2H, [4] total. */
+int pfs_program_last_timing(const struct pfs_program* prog, double* ms, int n);
+
+/* Number of this library's kernel launches made by the last pfs_run. */
+int64_t pfs_program_last_launches(const struct pfs_program* prog);
+
+void pfs_program_destroy(struct pfs_program* prog);
+const char* pfs_last_error(void);
+int pfs_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PFS_H */

@@ -53,7 +53,7 @@ def _ptr(a):
 
 def sample(prog: FlatProgram, num_shots: int, tile_shots: int, seed: int = 0,
            tile_offset: int = 0, coins=None, masks=None, flips: bool = True,
-           events: bool = True, nthreads: int = 1):
+           events: bool = True, nthreads: int = 1, noise_k=None):
     """Run the oracle; returns (flip_rows, event_rows), uint32 [rows, words]."""
     L = lib()
     n_tiles = -(-num_shots // tile_shots)
@@ -63,7 +63,8 @@ def sample(prog: FlatProgram, num_shots: int, tile_shots: int, seed: int = 0,
     p = np.ascontiguousarray(prog.noise_p, dtype=np.float64)
     with np.errstate(divide="ignore"):
         log1m = np.log1p(-p)
-    k = noise_chunks(prog, tile_shots)
+    k = (noise_chunks(prog, tile_shots) if noise_k is None
+         else np.ascontiguousarray(noise_k, dtype=np.int32))
     inject_words = 0
     if coins is not None or masks is not None:
         if coins is None or masks is None:

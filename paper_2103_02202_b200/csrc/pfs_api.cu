@@ -1,0 +1,498 @@
+// C-ABI of libpfs.so (include/pfs.h): program handles, device upload, the
+// sampling driver (chunked, double-buffered D2H pipeline for host outputs).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <new>
+#include <stdexcept>
+#include <string>
+
+#include "pfs_internal.h"
+
+using namespace pfs;
+
+namespace {
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+    g_last_error = msg;
+    return code;
+}
+
+#define CUDA_TRY(expr)                                                                     \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess)                                                             \
+            return fail(PFS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));   \
+    } while (0)
+
+constexpr size_t kSmemBudget = 227 * 1024;  // B200 opt-in max dynamic shared memory / CTA
+
+template <typename T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t n = 0;
+    cudaError_t reserve(size_t count) {
+        if (count <= n && p) return cudaSuccess;
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+        cudaError_t e = cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T));
+        if (e == cudaSuccess) n = count;
+        return e;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        n = 0;
+    }
+};
+}  // namespace
+
+struct pfs_program {
+    HostProgram hp;
+    pfs_options opts{};
+    LaunchCfg cfg{};
+    int device = -1;
+    int num_sms = 0;
+    size_t smem_optin = kSmemBudget;
+    DevBuf<DOp> d_ops;
+    DevBuf<uint32_t> d_targets, d_det_ptr, d_det_terms, d_ring;
+    DevBuf<double> d_p, d_log1m;
+    DevBuf<int32_t> d_k;
+    DevBuf<uint32_t> d_rows[2];
+    DevBuf<uint8_t> d_b8[2];
+    DevBuf<uint32_t> d_coins, d_masks;
+    DevBuf<uint8_t> d_ref;
+    DevBuf<unsigned long long> d_counts;
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t ev[8] = {};
+    double last_ms[5] = {0, 0, 0, 0, 0};
+    int64_t last_launches = 0;
+};
+
+static void choose_layout(pfs_program* pg) {
+    const HostProgram& hp = pg->hp;
+    const pfs_options& o = pg->opts;
+    const size_t budget = pg->smem_optin;
+    auto frame = [&](int W) { return frame_smem_bytes(hp.num_qubits, W); };
+    auto ring = [&](int W) { return (size_t)hp.num_slots * W * 4; };
+    int Ws = 0, Wg = 0;
+    for (int W = 32; W >= 1; W >>= 1)
+        if (frame(W) + ring(W) <= budget) { Ws = W; break; }
+    for (int W = 32; W >= 1; W >>= 1)
+        if (frame(W) <= budget) { Wg = W; break; }
+    int W;
+    bool rs;
+    if (o.words_per_tile > 0) {
+        W = o.words_per_tile;
+        if (o.ring_in_smem == 1) rs = true;
+        else if (o.ring_in_smem == 0) rs = false;
+        else rs = frame(W) + ring(W) <= budget;
+    } else if (o.ring_in_smem == 1) {
+        W = Ws; rs = true;
+    } else if (o.ring_in_smem == 0) {
+        W = Wg; rs = false;
+    } else if (Ws > 0 && Ws >= std::min(Wg, 8)) {
+        W = Ws; rs = true;
+    } else {
+        W = Wg; rs = false;
+    }
+    pg->cfg.W = W;
+    pg->cfg.ring_smem = rs;
+    pg->cfg.smem_bytes = frame(W) + (rs ? ring(W) : 0);
+    int threads = o.threads > 0 ? o.threads : 512;
+    pg->cfg.threads = threads;
+}
+
+extern "C" {
+
+int pfs_version(void) { return 1; }
+const char* pfs_last_error(void) { return g_last_error.c_str(); }
+
+int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t* targets,
+                       int64_t n_targets, const double* noise_p, int64_t n_noise,
+                       const int64_t* det_ptr, const int64_t* det_idx, int64_t n_columns,
+                       int64_t n_observables, int32_t num_qubits, int64_t num_measurements,
+                       int64_t num_coin_rows, int64_t num_noise_rows,
+                       const pfs_options* options_or_null, pfs_program** out) {
+    if (!out) return fail(PFS_E_INVALID, "out is null");
+    *out = nullptr;
+    pfs_program* pg = new (std::nothrow) pfs_program();
+    if (!pg) return fail(PFS_E_NOMEM, "out of host memory");
+    if (options_or_null) pg->opts = *options_or_null;
+    try {
+        pg->hp = compile_program(instrs, n_instrs, targets, n_targets, noise_p, n_noise, det_ptr,
+                                 det_idx, n_columns, n_observables, num_qubits, num_measurements,
+                                 num_coin_rows, num_noise_rows);
+    } catch (const std::invalid_argument& e) {
+        delete pg;
+        return fail(PFS_E_INVALID, e.what());
+    } catch (const std::bad_alloc&) {
+        delete pg;
+        return fail(PFS_E_NOMEM, "out of host memory");
+    }
+    choose_layout(pg);
+    if (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget) {
+        delete pg;
+        return fail(PFS_E_INVALID, "frame table of " + std::to_string(num_qubits) +
+                                       " qubits does not fit one CTA's shared memory");
+    }
+    const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 1.0;
+    assign_noise_chunks(pg->hp, 32 * pg->cfg.W, th);
+    *out = pg;
+    return PFS_OK;
+}
+
+int pfs_program_info(const pfs_program* pg, pfs_info* o) {
+    if (!pg || !o) return fail(PFS_E_INVALID, "null argument");
+    std::memset(o, 0, sizeof(*o));
+    const HostProgram& hp = pg->hp;
+    o->num_qubits = hp.num_qubits;
+    o->words_per_tile = pg->cfg.W;
+    o->tile_shots = 32 * pg->cfg.W;
+    o->threads = pg->cfg.threads;
+    o->ring_in_smem = pg->cfg.ring_smem ? 1 : 0;
+    o->smem_bytes = (int32_t)pg->cfg.smem_bytes;
+    o->num_measurements = hp.num_meas;
+    o->num_columns = hp.num_cols;
+    o->num_observables = hp.num_obs;
+    o->num_ops = (int64_t)hp.ops.size();
+    o->num_barriers = hp.num_barriers;
+    o->num_slots = hp.num_slots;
+    o->num_noise = hp.num_noise;
+    o->bframe_bits = hp.bframe_bits;
+    o->num_coin_rows = hp.num_coin_rows;
+    o->num_noise_rows = hp.num_noise_rows;
+    return PFS_OK;
+}
+
+int pfs_program_noise_chunks(const pfs_program* pg, int32_t* out, int64_t n) {
+    if (!pg || (!out && n)) return fail(PFS_E_INVALID, "null argument");
+    if (n != pg->hp.num_noise) return fail(PFS_E_INVALID, "size mismatch");
+    std::copy(pg->hp.noise_k.begin(), pg->hp.noise_k.end(), out);
+    return PFS_OK;
+}
+
+int pfs_program_last_timing(const pfs_program* pg, double* ms, int n) {
+    if (!pg || !ms) return fail(PFS_E_INVALID, "null argument");
+    for (int i = 0; i < n && i < 5; i++) ms[i] = pg->last_ms[i];
+    return PFS_OK;
+}
+
+int64_t pfs_program_last_launches(const pfs_program* pg) { return pg ? pg->last_launches : -1; }
+
+void pfs_program_destroy(pfs_program* pg) {
+    if (!pg) return;
+    if (pg->device >= 0) {
+        int prev = -1;
+        cudaGetDevice(&prev);
+        cudaSetDevice(pg->device);
+        pg->d_ops.release(); pg->d_targets.release(); pg->d_det_ptr.release();
+        pg->d_det_terms.release(); pg->d_ring.release(); pg->d_p.release();
+        pg->d_log1m.release(); pg->d_k.release();
+        for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
+        pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
+        if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
+        for (auto& e : pg->ev) if (e) cudaEventDestroy(e);
+        if (prev >= 0) cudaSetDevice(prev);
+    }
+    delete pg;
+}
+
+}  // extern "C"
+
+template <typename T>
+static cudaError_t upload(DevBuf<T>& b, const std::vector<T>& v) {
+    cudaError_t e = b.reserve(v.size());
+    if (e != cudaSuccess || v.empty()) return e;
+    return cudaMemcpy(b.p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice);
+}
+
+static int ensure_device(pfs_program* pg, int device) {
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(PFS_E_NODEVICE, "no CUDA device available");
+    if (device < 0 || device >= ndev) return fail(PFS_E_INVALID, "bad device index");
+    CUDA_TRY(cudaSetDevice(device));
+    if (pg->device == device) return PFS_OK;
+    if (pg->device >= 0) return fail(PFS_E_INVALID, "program is bound to another device");
+    cudaDeviceProp prop;
+    CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+    if (prop.major != 10) return fail(PFS_E_NODEVICE, "libpfs is built for sm_100a (B200) only");
+    pg->num_sms = prop.multiProcessorCount;
+    pg->smem_optin = prop.sharedMemPerBlockOptin;
+    if (pg->cfg.smem_bytes > pg->smem_optin)
+        return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory");
+    const HostProgram& hp = pg->hp;
+    CUDA_TRY(upload(pg->d_ops, hp.ops));
+    CUDA_TRY(upload(pg->d_targets, hp.targets));
+    CUDA_TRY(upload(pg->d_det_ptr, hp.det_ptr));
+    CUDA_TRY(upload(pg->d_det_terms, hp.det_terms));
+    CUDA_TRY(upload(pg->d_p, hp.noise_p));
+    CUDA_TRY(upload(pg->d_log1m, hp.noise_log1m));
+    CUDA_TRY(upload(pg->d_k, hp.noise_k));
+    CUDA_TRY(set_frame_kernel_smem(pg->cfg));
+    int per_sm = pg->opts.ctas_per_sm;
+    if (per_sm <= 0) {
+        size_t per = pg->cfg.smem_bytes + 1024;
+        per_sm = (int)std::max<size_t>(1, (prop.sharedMemPerMultiprocessor) / per);
+        per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / pg->cfg.threads));
+    }
+    pg->cfg.grid = pg->num_sms * per_sm;
+    CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
+    for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
+    pg->device = device;
+    return PFS_OK;
+}
+
+static bool is_device_ptr(const void* p) {
+    cudaPointerAttributes a;
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot_offset,
+                       int64_t num_shots, int mode, const uint8_t* ref_bits,
+                       const uint32_t* inject_coins, const uint32_t* inject_noise,
+                       int64_t inject_row_words, void* out, int64_t out_bytes,
+                       int64_t out_pitch, void* stream_v) {
+    if (!pg) return fail(PFS_E_INVALID, "program is null");
+    if (num_shots < 1) return fail(PFS_E_INVALID, "num_shots must be >= 1");
+    if (mode < PFS_MODE_FLIPS || mode > PFS_MODE_DETECTORS_ROWS) return fail(PFS_E_INVALID, "bad mode");
+    if (!out) return fail(PFS_E_INVALID, "out is null");
+    const HostProgram& hp = pg->hp;
+    const int W = pg->cfg.W;
+    const int64_t T = 32 * W;
+    if (shot_offset % T) return fail(PFS_E_INVALID, "shot_offset must be a multiple of the tile size " + std::to_string(T));
+    if ((inject_coins == nullptr) != (inject_noise == nullptr))
+        return fail(PFS_E_INVALID, "injected mode needs both coin and noise-mask rows");
+    const bool injected = inject_coins != nullptr;
+    if (injected && inject_row_words < (num_shots + 31) / 32)
+        return fail(PFS_E_INVALID, "inject_row_words smaller than ceil(num_shots/32)");
+    if (mode == PFS_MODE_SAMPLES && !ref_bits && hp.num_meas > 0)
+        return fail(PFS_E_INVALID, "SAMPLES mode needs the reference sample");
+    const bool rows_meas = mode == PFS_MODE_FLIPS || mode == PFS_MODE_SAMPLES || mode == PFS_MODE_FLIPS_ROWS;
+    const bool b8 = mode <= PFS_MODE_DETECTORS;
+    const int64_t R = rows_meas ? hp.num_meas : hp.num_cols;
+    const int64_t nbytes = (R + 7) / 8;
+    if (out_pitch == 0) out_pitch = nbytes;
+    if (b8 && out_pitch < nbytes) return fail(PFS_E_INVALID, "out_pitch smaller than ceil(R/8)");
+    const int64_t used_words = (num_shots + 31) / 32;
+    int64_t need;
+    if (b8) need = (num_shots - 1) * out_pitch + nbytes;
+    else if (mode == PFS_MODE_COUNTS) need = hp.num_cols * 8;
+    else need = R * used_words * 4;
+    if (out_bytes < need) return fail(PFS_E_INVALID, "output buffer too small: need " + std::to_string(need) + " bytes");
+
+    int rc = ensure_device(pg, device);
+    if (rc) return rc;
+    cudaStream_t st = (cudaStream_t)stream_v;
+    const bool dev_out = is_device_ptr(out);
+    const bool timing = pg->opts.timing != 0;
+    pg->last_launches = 0;
+    for (double& m : pg->last_ms) m = 0;
+    if (timing) CUDA_TRY(cudaEventRecord(pg->ev[0], st));
+
+    // ---- inputs: injected rows and reference bits (H2D) ----
+    const int64_t n_tiles_all = (num_shots + T - 1) / T;
+    const int64_t words_all = n_tiles_all * W;
+    if (injected) {
+        // rows padded to whole tiles
+        auto up_rows = [&](DevBuf<uint32_t>& b, const uint32_t* src, int64_t rows) -> cudaError_t {
+            cudaError_t e = b.reserve((size_t)std::max<int64_t>(rows, 1) * words_all);
+            if (e != cudaSuccess || rows == 0) return e;
+            if (is_device_ptr(src)) {
+                e = cudaMemsetAsync(b.p, 0, (size_t)rows * words_all * 4, st);
+                if (e != cudaSuccess) return e;
+                return cudaMemcpy2DAsync(b.p, words_all * 4, src, inject_row_words * 4, used_words * 4,
+                                         rows, cudaMemcpyDeviceToDevice, st);
+            }
+            e = cudaMemsetAsync(b.p, 0, (size_t)rows * words_all * 4, st);
+            if (e != cudaSuccess) return e;
+            return cudaMemcpy2DAsync(b.p, words_all * 4, src, inject_row_words * 4, used_words * 4,
+                                     rows, cudaMemcpyHostToDevice, st);
+        };
+        CUDA_TRY(up_rows(pg->d_coins, inject_coins, hp.num_coin_rows));
+        CUDA_TRY(up_rows(pg->d_masks, inject_noise, hp.num_noise_rows));
+    }
+    const uint8_t* d_ref = nullptr;
+    if (mode == PFS_MODE_SAMPLES && hp.num_meas > 0) {
+        CUDA_TRY(pg->d_ref.reserve(hp.num_meas));
+        CUDA_TRY(cudaMemcpyAsync(pg->d_ref.p, ref_bits, hp.num_meas,
+                                 is_device_ptr(ref_bits) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+        d_ref = pg->d_ref.p;
+    }
+    if (timing) CUDA_TRY(cudaEventRecord(pg->ev[1], st));
+
+    KParams kp{};
+    kp.ops = pg->d_ops.p;
+    kp.targets = pg->d_targets.p;
+    kp.det_ptr = pg->d_det_ptr.p;
+    kp.det_terms = pg->d_det_terms.p;
+    kp.noise_p = pg->d_p.p;
+    kp.noise_log1m = pg->d_log1m.p;
+    kp.noise_k = pg->d_k.p;
+    kp.coins = injected ? pg->d_coins.p : nullptr;
+    kp.masks = injected ? pg->d_masks.p : nullptr;
+    kp.inject_words = words_all;
+    kp.seed = seed;
+    kp.n_ops = (int32_t)hp.ops.size();
+    kp.num_qubits = hp.num_qubits;
+    kp.num_slots = (int32_t)hp.num_slots;
+    kp.num_obs = (int32_t)hp.num_obs;
+    kp.num_cols = (int32_t)hp.num_cols;
+    kp.do_dets = rows_meas ? 0 : 1;
+
+    LaunchCfg cfg = pg->cfg;
+    if (!cfg.ring_smem) {
+        CUDA_TRY(pg->d_ring.reserve((size_t)std::max<int64_t>(hp.num_slots, 1) * W * cfg.grid));
+        kp.ring_global = pg->d_ring.p;
+    }
+
+    if (mode == PFS_MODE_COUNTS) {
+        unsigned long long* cptr;
+        if (dev_out) cptr = (unsigned long long*)out;
+        else { CUDA_TRY(pg->d_counts.reserve(std::max<int64_t>(hp.num_cols, 1))); cptr = pg->d_counts.p; }
+        if (hp.num_cols > 0) CUDA_TRY(cudaMemsetAsync(cptr, 0, hp.num_cols * 8, st));
+        kp.counts = cptr;
+        const size_t extra = (size_t)hp.num_cols * 4;
+        kp.counts_in_smem = (cfg.smem_bytes + extra <= pg->smem_optin) ? 1 : 0;
+        if (kp.counts_in_smem) {
+            cfg.smem_bytes += extra;
+            CUDA_TRY(set_frame_kernel_smem(cfg));
+        }
+        // per-CTA u32 counters: bound shots per launch so no counter can overflow
+        const int64_t max_tiles = std::max<int64_t>(1, ((int64_t)1 << 30) / T) * cfg.grid;
+        for (int64_t t0 = 0; t0 < n_tiles_all; t0 += max_tiles) {
+            const int64_t nt = std::min(max_tiles, n_tiles_all - t0);
+            kp.n_tiles = nt;
+            kp.tile_offset = shot_offset / T + t0;
+            kp.num_shots = std::min<int64_t>(num_shots - t0 * T, nt * T);
+            if (injected) { kp.coins = pg->d_coins.p + t0 * W; kp.masks = pg->d_masks.p + t0 * W; }
+            LaunchCfg lc = cfg;
+            lc.grid = (int)std::min<int64_t>(cfg.grid, nt);
+            CUDA_TRY(launch_frame_kernel(lc, kp, st));
+            pg->last_launches++;
+        }
+        if (timing) CUDA_TRY(cudaEventRecord(pg->ev[2], st));
+        if (!dev_out && hp.num_cols > 0)
+            CUDA_TRY(cudaMemcpyAsync(out, cptr, hp.num_cols * 8, cudaMemcpyDeviceToHost, st));
+        if (timing) CUDA_TRY(cudaEventRecord(pg->ev[4], st));
+        if (!dev_out || timing) CUDA_TRY(cudaStreamSynchronize(st));
+        if (timing) {
+            float a = 0, b = 0, c = 0;
+            cudaEventElapsedTime(&a, pg->ev[1], pg->ev[2]);
+            cudaEventElapsedTime(&b, pg->ev[0], pg->ev[1]);
+            cudaEventElapsedTime(&c, pg->ev[0], pg->ev[4]);
+            pg->last_ms[0] = a; pg->last_ms[2] = b; pg->last_ms[4] = c;
+        }
+        return PFS_OK;
+    }
+
+    // ---- row-producing modes ----
+    // Device output: one pass straight into the caller's buffer when possible.
+    // Host output: chunks of tiles, kernels on `st`, D2H on copy_stream, double-buffered.
+    const int64_t dev_pitch = b8 ? ((nbytes + 31) / 32) * 32 : 0;
+    int64_t chunk_tiles = n_tiles_all;
+    if (!dev_out) {
+        const int64_t bytes_per_tile = R * W * 4 + (b8 ? T * dev_pitch : 0);
+        const int64_t target = (int64_t)256 << 20;
+        chunk_tiles = std::max<int64_t>(1, target / std::max<int64_t>(bytes_per_tile, 1));
+        chunk_tiles = std::max<int64_t>(chunk_tiles, cfg.grid);  // keep every SM busy
+        chunk_tiles = std::min(chunk_tiles, n_tiles_all);
+    }
+    const bool direct_rows = dev_out && !b8;  // *_ROWS into the caller's buffer
+    const int n_chunks = (int)((n_tiles_all + chunk_tiles - 1) / chunk_tiles);
+    const int nbuf = dev_out ? 1 : std::min(2, n_chunks);
+    const int64_t chunk_words = chunk_tiles * W;
+    for (int b = 0; b < nbuf; b++) {
+        if (!direct_rows) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * chunk_words));
+        if (b8 && !dev_out) CUDA_TRY(pg->d_b8[b].reserve((size_t)chunk_tiles * T * dev_pitch));
+    }
+    if (timing) CUDA_TRY(cudaEventRecord(pg->ev[1], st));
+    float frame_ms = 0, tr_ms = 0;
+    for (int ci = 0; ci < n_chunks; ci++) {
+        const int b = ci % nbuf;
+        const int64_t t0 = (int64_t)ci * chunk_tiles;
+        const int64_t nt = std::min(chunk_tiles, n_tiles_all - t0);
+        const int64_t shots0 = t0 * T;
+        const int64_t nshots = std::min<int64_t>(num_shots - shots0, nt * T);
+        if (!dev_out && ci >= 2) CUDA_TRY(cudaStreamWaitEvent(st, pg->ev[6 + b], 0));  // buffer free
+        uint32_t* rows = direct_rows ? (uint32_t*)out : pg->d_rows[b].p;
+        const int64_t row_words = direct_rows ? used_words : chunk_words;
+        kp.out_words = row_words;
+        kp.rec_out = rows_meas ? rows : nullptr;
+        kp.ev_out = rows_meas ? nullptr : rows;
+        kp.n_tiles = nt;
+        kp.tile_offset = shot_offset / T + t0;
+        kp.num_shots = nshots;
+        if (injected) { kp.coins = pg->d_coins.p + t0 * W; kp.masks = pg->d_masks.p + t0 * W; }
+        if (direct_rows && (used_words % W) != 0) {
+            // the last tile would write past the caller's rows: stage through scratch
+            CUDA_TRY(pg->d_rows[0].reserve((size_t)std::max<int64_t>(R, 1) * chunk_words));
+            rows = pg->d_rows[0].p;
+            kp.out_words = chunk_words;
+            kp.rec_out = rows_meas ? rows : nullptr;
+            kp.ev_out = rows_meas ? nullptr : rows;
+        }
+        LaunchCfg lc = cfg;
+        lc.grid = (int)std::min<int64_t>(cfg.grid, nt);
+        if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[2], st));
+        CUDA_TRY(launch_frame_kernel(lc, kp, st));
+        pg->last_launches++;
+        if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[3], st));
+        if (b8) {
+            uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
+            const int64_t pitch = dev_out ? out_pitch : dev_pitch;
+            CUDA_TRY(launch_rows_to_b8(rows, R, kp.out_words, nshots,
+                                       mode == PFS_MODE_SAMPLES ? d_ref : nullptr, dst, pitch, st));
+            pg->last_launches++;
+            if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
+        } else if (direct_rows && rows != (uint32_t*)out) {
+            CUDA_TRY(cudaMemcpy2DAsync(out, used_words * 4, rows, kp.out_words * 4, used_words * 4, R,
+                                       cudaMemcpyDeviceToDevice, st));
+        }
+        if (timing && ci == 0) {
+            CUDA_TRY(cudaStreamSynchronize(st));
+            cudaEventElapsedTime(&frame_ms, pg->ev[2], pg->ev[3]);
+            if (b8) cudaEventElapsedTime(&tr_ms, pg->ev[3], pg->ev[5]);
+        }
+        if (!dev_out) {
+            CUDA_TRY(cudaEventRecord(pg->ev[4], st));
+            CUDA_TRY(cudaStreamWaitEvent(pg->copy_stream, pg->ev[4], 0));
+            if (b8) {
+                CUDA_TRY(cudaMemcpy2DAsync((uint8_t*)out + shots0 * out_pitch, out_pitch, pg->d_b8[b].p,
+                                           dev_pitch, nbytes, nshots, cudaMemcpyDeviceToHost,
+                                           pg->copy_stream));
+            } else {
+                const int64_t cw = (nshots + 31) / 32;
+                CUDA_TRY(cudaMemcpy2DAsync((uint32_t*)out + shots0 / 32, used_words * 4, rows,
+                                           chunk_words * 4, cw * 4, R, cudaMemcpyDeviceToHost,
+                                           pg->copy_stream));
+            }
+            CUDA_TRY(cudaEventRecord(pg->ev[6 + b], pg->copy_stream));
+        }
+    }
+    if (!dev_out) {
+        CUDA_TRY(cudaStreamSynchronize(pg->copy_stream));
+        CUDA_TRY(cudaStreamSynchronize(st));
+    }
+    if (timing) {
+        CUDA_TRY(cudaEventRecord(pg->ev[4], st));
+        CUDA_TRY(cudaStreamSynchronize(st));
+        float h2d = 0, tot = 0;
+        cudaEventElapsedTime(&h2d, pg->ev[0], pg->ev[1]);
+        cudaEventElapsedTime(&tot, pg->ev[0], pg->ev[4]);
+        pg->last_ms[0] = frame_ms;
+        pg->last_ms[1] = tr_ms;
+        pg->last_ms[2] = h2d;
+        pg->last_ms[4] = tot;
+    }
+    return PFS_OK;
+}

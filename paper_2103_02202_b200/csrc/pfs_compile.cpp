@@ -1,0 +1,336 @@
+// Host-side circuit compiler: flat frame program -> device op list.
+//
+// Replaces the per-call `compile_frame_program` (stabsim/frame_sim.py:170-189)
+// with a one-time native pass that prepares the op stream the persistent CUDA
+// kernel interprets:
+//   * split every instruction at the first repeated qubit, so each device op is
+//     a set of independent applications (the reference applies an
+//     instruction's applications sequentially, frame_sim.py:61-62, 196-197 —
+//     `CX 0 1 1 2` must stay two steps);
+//   * merge consecutive instructions of the same frame rule / collapse kind
+//     when they touch disjoint qubits (fewer ops, fewer barriers);
+//   * allocate measurement-record ring slots by liveness: a record lives from
+//     its M until the last DETECTOR / OBSERVABLE_INCLUDE that reads it
+//     (detector sets: stabsim/circuit.py:247-256);
+//   * schedule __syncthreads: a barrier goes before an op only if it touches a
+//     qubit row or record slot already touched since the previous barrier.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+
+#include "pfs_internal.h"
+
+namespace pfs {
+
+namespace {
+
+int rule_arity(int32_t rule) { return rule >= R_CX ? 2 : 1; }
+
+int64_t rule_bits(int32_t rule) {
+    switch (rule) {
+        case R_SWAPXZ: return 4;
+        case R_ZXORX: case R_XXORZ: return 3;
+        case R_CX: case R_CZ: return 6;
+        case R_CY: return 7;
+        case R_SWAP: return 8;
+        default: return 0;
+    }
+}
+
+[[noreturn]] void bad(const std::string& msg) { throw std::invalid_argument(msg); }
+
+}  // namespace
+
+HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* targets,
+                            int64_t n_targets, const double* noise_p, int64_t n_noise,
+                            const int64_t* det_ptr, const int64_t* det_idx, int64_t n_cols,
+                            int64_t n_obs, int32_t num_qubits, int64_t num_meas,
+                            int64_t num_coin_rows, int64_t num_noise_rows) {
+    if (num_qubits < 0 || num_meas < 0 || n_cols < 0 || n_obs < 0 || n_obs > n_cols)
+        bad("negative sizes");
+    if (n_ins > 0 && (!ins || (n_targets > 0 && !targets))) bad("null instruction arrays");
+    if (n_cols > 0 && (!det_ptr)) bad("null detector arrays");
+    const int64_t n_det = n_cols - n_obs;
+    HostProgram hp;
+    hp.num_qubits = num_qubits;
+    hp.num_meas = num_meas;
+    hp.num_cols = n_cols;
+    hp.num_obs = n_obs;
+    hp.num_noise = n_noise;
+    hp.num_coin_rows = num_coin_rows;
+    hp.num_noise_rows = num_noise_rows;
+    hp.noise_p.assign(noise_p, noise_p + n_noise);
+    hp.noise_log1m.resize(n_noise);
+    hp.noise_apps.assign(n_noise, 0);
+    for (int64_t i = 0; i < n_noise; i++) {
+        double p = noise_p[i];
+        if (!(p >= 0.0 && p <= 1.0)) bad("noise probability must be in [0, 1], got " + std::to_string(p));
+        hp.noise_log1m[i] = std::log1p(-p);
+    }
+
+    // ---- pass 1: validate and compute record liveness ----
+    std::vector<int64_t> last_use(num_meas, -1);
+    {
+        int64_t rec = 0, coin = num_qubits, nrow = 0, col = 0;
+        for (int64_t i = 0; i < n_ins; i++) {
+            const pfs_instr& in = ins[i];
+            if (in.n_targets < 0 || in.tgt_off < 0 || (int64_t)in.tgt_off + in.n_targets > n_targets)
+                bad("instruction " + std::to_string(i) + ": target range out of bounds");
+            const int32_t* tg = targets + in.tgt_off;
+            switch (in.kind) {
+            case K_GATE:
+                if (in.code <= R_NONE || in.code > R_SWAP) bad("unknown frame rule");
+                if (in.n_targets % rule_arity(in.code)) bad("gate target count not a multiple of arity");
+                for (int j = 0; j < in.n_targets; j++)
+                    if (tg[j] < 0 || tg[j] >= num_qubits)
+                        bad("qubit " + std::to_string(tg[j]) + " out of range [0, " + std::to_string(num_qubits) + ")");
+                for (int j = 0; j + 1 < in.n_targets && rule_arity(in.code) == 2; j += 2)
+                    if (tg[j] == tg[j + 1]) bad("two-qubit gate targets a qubit pair twice");
+                hp.bframe_bits += rule_bits(in.code) * (in.n_targets / rule_arity(in.code));
+                break;
+            case K_M: case K_R: case K_MR:
+                for (int j = 0; j < in.n_targets; j++)
+                    if (tg[j] < 0 || tg[j] >= num_qubits)
+                        bad("qubit " + std::to_string(tg[j]) + " out of range [0, " + std::to_string(num_qubits) + ")");
+                if (in.kind != K_R && in.rec_base != rec) bad("record numbering is not contiguous");
+                if (in.coin_base != coin) bad("coin row numbering is not contiguous");
+                if (in.kind != K_R) rec += in.n_targets;
+                coin += (int64_t)in.n_targets * (in.kind == K_MR ? 2 : 1);
+                hp.bframe_bits += (in.kind == K_R ? 2 : 4) * (int64_t)in.n_targets;
+                break;
+            case K_NOISE: {
+                if (in.code < CH_XERR || in.code > CH_DEP2) bad("unknown noise channel");
+                int ar = in.code == CH_DEP2 ? 2 : 1;
+                if (in.n_targets % ar) bad("noise target count not a multiple of arity");
+                for (int j = 0; j < in.n_targets; j++)
+                    if (tg[j] < 0 || tg[j] >= num_qubits)
+                        bad("qubit " + std::to_string(tg[j]) + " out of range [0, " + std::to_string(num_qubits) + ")");
+                if (in.aux < 0 || in.aux >= n_noise) bad("noise ordinal out of range");
+                if (in.noise_row_base != nrow) bad("noise row numbering is not contiguous");
+                hp.noise_apps[in.aux] = (uint32_t)(in.n_targets / ar);
+                nrow += 2 * (int64_t)in.n_targets;
+                break;
+            }
+            case K_DET: {
+                if (in.aux != col || col >= n_det) bad("detector columns out of order");
+                for (int64_t e = det_ptr[col]; e < det_ptr[col + 1]; e++) {
+                    int64_t m = det_idx[e];
+                    if (m < 0 || m >= rec)
+                        bad("detector " + std::to_string(col) + " references measurement " +
+                            std::to_string(m) + ", have " + std::to_string(rec));
+                    last_use[m] = i;
+                }
+                col++;
+                break;
+            }
+            case K_OBS:
+                if (in.aux < n_det || in.aux >= n_cols) bad("observable column out of range");
+                for (int j = 0; j < in.n_targets; j++) {
+                    int64_t m = tg[j];
+                    if (m < 0 || m >= rec) bad("observable references a future measurement");
+                    last_use[m] = i;
+                }
+                break;
+            default:
+                bad("unknown instruction kind " + std::to_string(in.kind));
+            }
+        }
+        if (rec != num_meas) bad("measurement count mismatch");
+        if (col != n_det) bad("detector count mismatch");
+        if (coin != num_coin_rows) bad("coin row count mismatch");
+        if (nrow != num_noise_rows) bad("noise row count mismatch");
+    }
+
+    // ---- pass 2: emit device ops, allocating record slots ----
+    std::vector<uint32_t> slot_of(num_meas, NO_SLOT);
+    std::vector<uint32_t> free_slots;
+    uint32_t next_slot = (uint32_t)n_obs;  // [0, n_obs) = observable accumulators
+    std::vector<int64_t> stamp(num_qubits, -1);
+    int64_t cur = -1;  // open (mergeable) op index
+    auto open_op = [&](uint32_t kind, uint32_t code) {
+        DOp op{};
+        op.kcf = kind | (code << 8);
+        op.off = (uint32_t)hp.targets.size();
+        hp.ops.push_back(op);
+        cur = (int64_t)hp.ops.size() - 1;
+    };
+    auto kind_of = [&](int64_t k) { return hp.ops[k].kcf & 0xFF; };
+    auto code_of = [&](int64_t k) { return (hp.ops[k].kcf >> 8) & 0xFF; };
+    auto alloc = [&]() -> uint32_t {
+        if (!free_slots.empty()) { uint32_t s = free_slots.back(); free_slots.pop_back(); return s; }
+        return next_slot++;
+    };
+    hp.det_ptr.assign(1, 0);
+    auto release_after = [&](int64_t i, int64_t m) {
+        if (last_use[m] == i && slot_of[m] != NO_SLOT) { free_slots.push_back(slot_of[m]); slot_of[m] = NO_SLOT; }
+    };
+
+    for (int64_t i = 0; i < n_ins; i++) {
+        const pfs_instr& in = ins[i];
+        const int32_t* tg = targets + in.tgt_off;
+        switch (in.kind) {
+        case K_GATE: {
+            const int ar = rule_arity(in.code);
+            for (int j = 0; j < in.n_targets; j += ar) {
+                bool conflict = cur < 0 || kind_of(cur) != K_GATE || code_of(cur) != (uint32_t)in.code;
+                for (int s = 0; s < ar && !conflict; s++) conflict = stamp[tg[j + s]] == cur;
+                if (conflict) open_op(K_GATE, in.code);
+                for (int s = 0; s < ar; s++) { hp.targets.push_back((uint32_t)tg[j + s]); stamp[tg[j + s]] = cur; }
+                hp.ops[cur].count++;
+            }
+            break;
+        }
+        case K_M: case K_MR: case K_R: {
+            const bool records = in.kind != K_R;
+            const int coin_per = in.kind == K_MR ? 2 : 1;
+            for (int j = 0; j < in.n_targets; j++) {
+                const int64_t q = tg[j];
+                const uint32_t rec = (uint32_t)(in.rec_base + j);
+                const uint32_t coin = (uint32_t)(in.coin_base + (int64_t)coin_per * j);
+                bool conflict = cur < 0 || kind_of(cur) != in.kind || stamp[q] == cur;
+                if (!conflict) {
+                    const DOp& o = hp.ops[cur];
+                    if (records && o.a + o.count != rec) conflict = true;
+                    if (o.b + (uint32_t)coin_per * o.count != coin) conflict = true;
+                }
+                if (conflict) {
+                    open_op(in.kind, 0);
+                    hp.ops[cur].a = records ? rec : 0;
+                    hp.ops[cur].b = coin;
+                }
+                hp.targets.push_back((uint32_t)q);
+                if (records) {
+                    uint32_t s = NO_SLOT;
+                    if (last_use[rec] >= 0) { s = alloc(); slot_of[rec] = s; }
+                    hp.targets.push_back(s);
+                }
+                stamp[q] = cur;
+                hp.ops[cur].count++;
+            }
+            break;
+        }
+        case K_NOISE: {
+            const int ar = in.code == CH_DEP2 ? 2 : 1;
+            open_op(K_NOISE, in.code);
+            DOp& o = hp.ops[cur];
+            o.count = (uint32_t)(in.n_targets / ar);
+            o.a = (uint32_t)in.noise_row_base;
+            o.b = (uint32_t)in.aux;
+            bool dup = false;
+            for (int j = 0; j < in.n_targets; j++) {
+                if (stamp[tg[j]] == cur) dup = true;
+                stamp[tg[j]] = cur;
+                hp.targets.push_back((uint32_t)tg[j]);
+            }
+            if (dup) o.kcf |= F_DUP << 16;
+            cur = -1;  // never merge noise ops (one RNG domain per instruction)
+            break;
+        }
+        case K_DET: {
+            const int64_t col = in.aux;
+            if (cur < 0 || kind_of(cur) != K_DET || hp.ops[cur].a + hp.ops[cur].count != (uint32_t)col) {
+                open_op(K_DET, 0);
+                hp.ops[cur].a = (uint32_t)col;
+            }
+            hp.ops[cur].count++;
+            for (int64_t e = det_ptr[col]; e < det_ptr[col + 1]; e++) hp.det_terms.push_back(slot_of[det_idx[e]]);
+            hp.det_ptr.push_back((uint32_t)hp.det_terms.size());
+            for (int64_t e = det_ptr[col]; e < det_ptr[col + 1]; e++) release_after(i, det_idx[e]);
+            break;
+        }
+        case K_OBS: {
+            open_op(K_OBS, 0);
+            DOp& o = hp.ops[cur];
+            o.count = (uint32_t)in.n_targets;
+            o.a = (uint32_t)(in.aux - n_det);  // accumulator slot
+            for (int j = 0; j < in.n_targets; j++) hp.targets.push_back(slot_of[tg[j]]);
+            for (int j = 0; j < in.n_targets; j++) release_after(i, tg[j]);
+            cur = -1;
+            break;
+        }
+        }
+    }
+    // observable columns: one term each, the accumulator slot
+    if (n_obs > 0) {
+        open_op(K_DET, 0);
+        hp.ops[cur].a = (uint32_t)n_det;
+        hp.ops[cur].count = (uint32_t)n_obs;
+        for (int64_t k = 0; k < n_obs; k++) {
+            hp.det_terms.push_back((uint32_t)k);
+            hp.det_ptr.push_back((uint32_t)hp.det_terms.size());
+        }
+    }
+    hp.num_slots = next_slot;
+
+    // ---- pass 3: barrier scheduling over qubit rows + record slots ----
+    const int64_t nres = (int64_t)num_qubits + hp.num_slots;
+    std::vector<int64_t> rstamp(nres, -1);
+    int64_t seg = 0;
+    std::vector<int64_t> res;
+    for (size_t k = 0; k < hp.ops.size(); k++) {
+        DOp& o = hp.ops[k];
+        const uint32_t kind = o.kcf & 0xFF;
+        res.clear();
+        switch (kind) {
+        case K_GATE: {
+            int ar = rule_arity((o.kcf >> 8) & 0xFF);
+            for (uint32_t j = 0; j < o.count * ar; j++) res.push_back(hp.targets[o.off + j]);
+            break;
+        }
+        case K_M: case K_MR:
+            for (uint32_t j = 0; j < o.count; j++) {
+                res.push_back(hp.targets[o.off + 2 * j]);
+                uint32_t s = hp.targets[o.off + 2 * j + 1];
+                if (s != NO_SLOT) res.push_back(num_qubits + (int64_t)s);
+            }
+            break;
+        case K_R:
+            for (uint32_t j = 0; j < o.count; j++) res.push_back(hp.targets[o.off + j]);
+            break;
+        case K_NOISE: {
+            int ar = ((o.kcf >> 8) & 0xFF) == CH_DEP2 ? 2 : 1;
+            for (uint32_t j = 0; j < o.count * ar; j++) res.push_back(hp.targets[o.off + j]);
+            break;
+        }
+        case K_DET:
+            for (uint32_t c = o.a; c < o.a + o.count; c++)
+                for (uint32_t e = hp.det_ptr[c]; e < hp.det_ptr[c + 1]; e++)
+                    if (hp.det_terms[e] != NO_SLOT) res.push_back(num_qubits + (int64_t)hp.det_terms[e]);
+            break;
+        case K_OBS:
+            res.push_back(num_qubits + (int64_t)o.a);
+            for (uint32_t j = 0; j < o.count; j++)
+                if (hp.targets[o.off + j] != NO_SLOT) res.push_back(num_qubits + (int64_t)hp.targets[o.off + j]);
+            break;
+        }
+        bool conflict = false;
+        for (int64_t r : res) if (rstamp[r] == seg) { conflict = true; break; }
+        if (conflict && k > 0) { seg++; o.kcf |= F_BARRIER << 16; }
+        for (int64_t r : res) rstamp[r] = seg;
+    }
+    hp.num_barriers = seg;
+    return hp;
+}
+
+void assign_noise_chunks(HostProgram& hp, int tile_shots, double target_hits) {
+    hp.noise_k.assign(hp.num_noise, 1);
+    for (int64_t i = 0; i < hp.num_noise; i++) {
+        const int64_t A = hp.noise_apps[i];
+        const double p = hp.noise_p[i];
+        int64_t k;
+        if (A <= 0) k = 1;
+        else if (p <= 0.0) k = A;
+        else {
+            double x = target_hits / (p * (double)tile_shots);
+            k = x >= (double)A ? A : (int64_t)x;
+            if (k < 1) k = 1;
+            if (k > A) k = A;
+        }
+        hp.noise_k[i] = (int32_t)k;
+    }
+}
+
+}  // namespace pfs

@@ -1,0 +1,120 @@
+// Internal declarations shared by the host compiler (pfs_compile.cpp), the
+// kernels (pfs_kernels.cu) and the C-ABI (pfs_api.cu).
+#pragma once
+#include <cstdint>
+#include <string>
+#include <vector>
+
+#include "../../include/pfs.h"
+
+namespace pfs {
+
+enum Kind : uint32_t { K_GATE = 0, K_M = 1, K_R = 2, K_MR = 3, K_NOISE = 4, K_DET = 5, K_OBS = 6 };
+enum Rule : uint32_t { R_NONE = 0, R_SWAPXZ = 1, R_ZXORX = 2, R_XXORZ = 3, R_CX = 4, R_CZ = 5,
+                       R_CY = 6, R_SWAP = 7 };
+enum Channel : uint32_t { CH_XERR = 0, CH_YERR = 1, CH_ZERR = 2, CH_DEP1 = 3, CH_DEP2 = 4 };
+
+// Device op flags
+constexpr uint32_t F_BARRIER = 1u;   // __syncthreads() before this op
+constexpr uint32_t F_DUP = 2u;       // noise op with repeated targets: atomic XOR
+constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
+
+constexpr uint32_t DOMAIN_COIN = 0x40000000u;
+constexpr uint32_t DOMAIN_NOISE = 0x80000000u;
+
+// One device op (32 bytes).  See DESIGN.md §3.
+//   GATE : count = apps, off -> targets (1 or 2 per app)
+//   M/MR : count = targets, off -> (qubit, slot) pairs, a = rec_base, b = coin_base
+//   R    : count = targets, off -> qubits, b = coin_base
+//   NOISE: count = apps, off -> targets, a = noise_row_base, b = noise ordinal
+//   DET  : count = columns, a = first column (terms via det_ptr/det_terms)
+//   OBS  : count = terms, off -> record slots, a = accumulator slot
+struct DOp {
+    uint32_t kcf;  // kind | code << 8 | flags << 16
+    uint32_t count;
+    uint32_t off;
+    uint32_t a;
+    uint32_t b;
+    uint32_t c;
+    uint32_t d;
+    uint32_t e;
+};
+static_assert(sizeof(DOp) == 32, "DOp is 32 bytes");
+
+struct HostProgram {
+    int32_t num_qubits = 0;
+    int64_t num_meas = 0;
+    int64_t num_cols = 0;
+    int64_t num_obs = 0;
+    int64_t num_noise = 0;
+    int64_t num_coin_rows = 0;
+    int64_t num_noise_rows = 0;
+    int64_t bframe_bits = 0;
+    int64_t num_slots = 0;
+    int64_t num_barriers = 0;
+    std::vector<DOp> ops;
+    std::vector<uint32_t> targets;
+    std::vector<uint32_t> det_ptr;    // [num_cols + 1] into det_terms
+    std::vector<uint32_t> det_terms;  // slots
+    std::vector<double> noise_p;
+    std::vector<double> noise_log1m;
+    std::vector<int32_t> noise_k;     // filled once T is known
+    std::vector<uint32_t> noise_apps; // apps per noise ordinal
+};
+
+// Host compiler: flat program -> device ops (splitting, merging, record-slot
+// liveness allocation, barrier scheduling).  Throws std::invalid_argument.
+HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int32_t* targets,
+                            int64_t n_targets, const double* noise_p, int64_t n_noise,
+                            const int64_t* det_ptr, const int64_t* det_idx, int64_t n_cols,
+                            int64_t n_obs, int32_t num_qubits, int64_t num_meas,
+                            int64_t num_coin_rows, int64_t num_noise_rows);
+
+void assign_noise_chunks(HostProgram& hp, int tile_shots, double target_hits);
+
+// Kernel launch plumbing (pfs_kernels.cu)
+struct KParams {
+    const DOp* ops;
+    const uint32_t* targets;
+    const uint32_t* det_ptr;
+    const uint32_t* det_terms;
+    const double* noise_p;
+    const double* noise_log1m;
+    const int32_t* noise_k;
+    const uint32_t* coins;       // injected: [rows][inject_words]
+    const uint32_t* masks;
+    uint32_t* rec_out;           // [M][out_words] (flips rows) or null
+    uint32_t* ev_out;            // [cols][out_words] or null
+    unsigned long long* counts;  // [cols] or null
+    uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
+    int64_t inject_words;
+    int64_t out_words;
+    int64_t n_tiles;
+    int64_t num_shots;           // shots of this launch (for tail masking)
+    uint64_t seed;
+    uint64_t tile_offset;        // global index of local tile 0
+    int32_t n_ops;
+    int32_t num_qubits;
+    int32_t num_slots;
+    int32_t num_obs;
+    int32_t num_cols;
+    int32_t counts_in_smem;
+    int32_t do_dets;             // evaluate DET/OBS ops
+};
+
+struct LaunchCfg {
+    int W;
+    bool ring_smem;
+    int threads;
+    int grid;
+    size_t smem_bytes;
+};
+
+size_t frame_smem_bytes(int num_qubits, int W);
+cudaError_t launch_frame_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStream_t stream);
+cudaError_t set_frame_kernel_smem(const LaunchCfg& cfg);
+cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t row_words,
+                              int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
+                              int64_t pitch, cudaStream_t stream);
+
+}  // namespace pfs

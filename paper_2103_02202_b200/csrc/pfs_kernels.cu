@@ -1,0 +1,477 @@
+// sm_100a kernels of the bulk Pauli-frame sampler.
+//
+// frame_kernel  — persistent program interpreter.  Each CTA owns a tile of
+//                 T = 32 W shots and keeps the whole frame table of that tile
+//                 (x and z bit-planes, qubit-major, shots packed in uint32
+//                 words: SURVEY.md Appendix D) resident in shared memory for the
+//                 entire circuit.  Reference semantics per op:
+//                   gate rules      stabsim/frame_sim.py:64-72 (gates.py:326-348)
+//                   M / R / MR      stabsim/frame_sim.py:74-90
+//                   noise           stabsim/frame_sim.py:92-167, entropy.py:65-88
+//                   detectors       stabsim/io_formats.py:208-227
+// rows_to_b8    — 32x32 warp-shuffle bit transpose of row-major bit tables to
+//                 shot-major b8 (stabsim/bitvec.py:193-209, io_formats.py:94-96).
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "pfs_internal.h"
+
+namespace pfs {
+
+// ---------------------------------------------------------------- Philox
+__device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32_t& c2,
+                                              uint32_t& c3, uint32_t k0, uint32_t k1) {
+#pragma unroll
+    for (int r = 0; r < 10; r++) {
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+        const uint32_t n0 = hi1 ^ c1 ^ k0;
+        const uint32_t n2 = hi0 ^ c3 ^ k1;
+        c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+        k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
+    }
+}
+
+// ---------------------------------------------------------------- vectors
+template <int V> struct VW { uint32_t w[V]; };
+
+template <int V> __device__ __forceinline__ VW<V> vld(const uint32_t* p);
+template <> __device__ __forceinline__ VW<4> vld<4>(const uint32_t* p) {
+    uint4 v = *reinterpret_cast<const uint4*>(p); return VW<4>{{v.x, v.y, v.z, v.w}};
+}
+template <> __device__ __forceinline__ VW<2> vld<2>(const uint32_t* p) {
+    uint2 v = *reinterpret_cast<const uint2*>(p); return VW<2>{{v.x, v.y}};
+}
+template <> __device__ __forceinline__ VW<1> vld<1>(const uint32_t* p) { return VW<1>{{*p}}; }
+
+template <int V> __device__ __forceinline__ void vst(uint32_t* p, const VW<V>& v);
+template <> __device__ __forceinline__ void vst<4>(uint32_t* p, const VW<4>& v) {
+    *reinterpret_cast<uint4*>(p) = make_uint4(v.w[0], v.w[1], v.w[2], v.w[3]);
+}
+template <> __device__ __forceinline__ void vst<2>(uint32_t* p, const VW<2>& v) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(v.w[0], v.w[1]);
+}
+template <> __device__ __forceinline__ void vst<1>(uint32_t* p, const VW<1>& v) { *p = v.w[0]; }
+
+template <int V> __device__ __forceinline__ VW<V> vxor(const VW<V>& a, const VW<V>& b) {
+    VW<V> r;
+#pragma unroll
+    for (int j = 0; j < V; j++) r.w[j] = a.w[j] ^ b.w[j];
+    return r;
+}
+template <int V> __device__ __forceinline__ VW<V> vzero() {
+    VW<V> r;
+#pragma unroll
+    for (int j = 0; j < V; j++) r.w[j] = 0u;
+    return r;
+}
+
+// global-memory loads through the read-only path for immutable inputs
+template <int V> __device__ __forceinline__ VW<V> vldg(const uint32_t* p);
+template <> __device__ __forceinline__ VW<4> vldg<4>(const uint32_t* p) {
+    uint4 v = __ldg(reinterpret_cast<const uint4*>(p)); return VW<4>{{v.x, v.y, v.z, v.w}};
+}
+template <> __device__ __forceinline__ VW<2> vldg<2>(const uint32_t* p) {
+    uint2 v = __ldg(reinterpret_cast<const uint2*>(p)); return VW<2>{{v.x, v.y}};
+}
+template <> __device__ __forceinline__ VW<1> vldg<1>(const uint32_t* p) { return VW<1>{{__ldg(p)}}; }
+
+// coin words c*V .. c*V+V-1 of coin row e for global tile g
+template <int W, int V>
+__device__ __forceinline__ VW<V> coin_words(const KParams& kp, uint32_t e, int c, uint32_t g,
+                                            int64_t tile) {
+    if (kp.coins != nullptr)
+        return vldg<V>(kp.coins + (int64_t)e * kp.inject_words + tile * W + c * V);
+    const int word = c * V;
+    uint32_t c0 = e, c1 = (uint32_t)(word >> 2), c2 = g, c3 = DOMAIN_COIN;
+    philox4x32_10(c0, c1, c2, c3, (uint32_t)kp.seed, (uint32_t)(kp.seed >> 32));
+    const uint32_t o[4] = {c0, c1, c2, c3};
+    VW<V> r;
+#pragma unroll
+    for (int j = 0; j < V; j++) r.w[j] = o[(word & 3) + j];
+    return r;
+}
+
+__device__ __forceinline__ void pattern_of(uint32_t ch, uint32_t pick, uint32_t& xm, uint32_t& zm) {
+    switch (ch) {
+        case CH_XERR: xm = 1; zm = 0; return;
+        case CH_YERR: xm = 1; zm = 1; return;
+        case CH_ZERR: xm = 0; zm = 1; return;
+        case CH_DEP1: xm = (pick <= 1u) ? 1u : 0u; zm = (pick >= 1u) ? 1u : 0u; return;
+        default: {
+            const uint32_t code = pick + 1u;  // DEPOLARIZE2 codes 1..15 (gates.py:354-360)
+            xm = (code & 1u) | (((code >> 2) & 1u) << 1);
+            zm = ((code >> 1) & 1u) | (((code >> 3) & 1u) << 1);
+        }
+    }
+}
+
+template <int C> struct Log2;
+template <> struct Log2<1> { static constexpr int v = 0; };
+template <> struct Log2<2> { static constexpr int v = 1; };
+template <> struct Log2<4> { static constexpr int v = 2; };
+template <> struct Log2<8> { static constexpr int v = 3; };
+
+// ------------------------------------------------------------ frame kernel
+template <int W, bool RING_SMEM>
+__global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ KParams kp) {
+    constexpr int V = W >= 4 ? 4 : W;  // words per vector access
+    constexpr int C = W / V;           // vector chunks per row
+    constexpr int LC = Log2<C>::v;
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int n = kp.num_qubits;
+    uint32_t* const X = smem;
+    uint32_t* const Z = smem + (size_t)n * W;
+    uint32_t* const ring = RING_SMEM ? (smem + (size_t)2 * n * W)
+                                     : (kp.ring_global + (size_t)blockIdx.x * kp.num_slots * W);
+    uint32_t* const cnt = smem + (size_t)2 * n * W + (RING_SMEM ? (size_t)kp.num_slots * W : 0);
+    const int tid = threadIdx.x;
+    const int nth = blockDim.x;
+    const uint32_t key0 = (uint32_t)kp.seed, key1 = (uint32_t)(kp.seed >> 32);
+
+    if (kp.counts_in_smem) {
+        for (int i = tid; i < kp.num_cols; i += nth) cnt[i] = 0u;
+    }
+
+    for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x) {
+        const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
+        // FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39)
+        for (int i = tid; i < (n << LC); i += nth) {
+            const int q = i >> LC, c = i & (C - 1);
+            vst<V>(X + (size_t)q * W + c * V, vzero<V>());
+            vst<V>(Z + (size_t)q * W + c * V, coin_words<W, V>(kp, (uint32_t)q, c, g, tile));
+        }
+        for (int i = tid; i < (kp.num_obs << LC); i += nth) {
+            const int k = i >> LC, c = i & (C - 1);
+            vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
+        }
+        __syncthreads();
+
+        for (int oi = 0; oi < kp.n_ops; oi++) {
+            const uint4 h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi));
+            const uint4 h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi) + 1);
+            const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
+            const uint32_t count = h0.y, off = h0.z, oa = h0.w, ob = h1.x;
+            if (flags & F_BARRIER) __syncthreads();
+            const uint32_t* tg = kp.targets + off;
+            switch (kind) {
+            case K_GATE: {
+                const int items = (int)(count << LC);
+                switch (code) {
+                case R_SWAPXZ:
+                    for (int i = tid; i < items; i += nth) {
+                        const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                        const VW<V> a = vld<V>(X + p), b = vld<V>(Z + p);
+                        vst<V>(X + p, b); vst<V>(Z + p, a);
+                    }
+                    break;
+                case R_ZXORX:
+                    for (int i = tid; i < items; i += nth) {
+                        const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                        vst<V>(Z + p, vxor<V>(vld<V>(Z + p), vld<V>(X + p)));
+                    }
+                    break;
+                case R_XXORZ:
+                    for (int i = tid; i < items; i += nth) {
+                        const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                        vst<V>(X + p, vxor<V>(vld<V>(X + p), vld<V>(Z + p)));
+                    }
+                    break;
+                default: {  // two-qubit rules
+                    for (int i = tid; i < items; i += nth) {
+                        const uint2 qq = __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC));
+                        const int cv = (i & (C - 1)) * V;
+                        const size_t p0 = (size_t)qq.x * W + cv, p1 = (size_t)qq.y * W + cv;
+                        const VW<V> x0 = vld<V>(X + p0), x1 = vld<V>(X + p1);
+                        const VW<V> z0 = vld<V>(Z + p0), z1 = vld<V>(Z + p1);
+                        switch (code) {
+                        case R_CX:
+                            vst<V>(X + p1, vxor<V>(x1, x0)); vst<V>(Z + p0, vxor<V>(z0, z1)); break;
+                        case R_CZ:
+                            vst<V>(Z + p0, vxor<V>(z0, x1)); vst<V>(Z + p1, vxor<V>(z1, x0)); break;
+                        case R_CY:
+                            vst<V>(X + p1, vxor<V>(x1, x0));
+                            vst<V>(Z + p0, vxor<V>(z0, vxor<V>(x1, z1)));
+                            vst<V>(Z + p1, vxor<V>(z1, x0)); break;
+                        default:  // SWAP
+                            vst<V>(X + p0, x1); vst<V>(X + p1, x0);
+                            vst<V>(Z + p0, z1); vst<V>(Z + p1, z0); break;
+                        }
+                    }
+                }
+                }
+                break;
+            }
+            case K_M: case K_MR: {
+                const int items = (int)(count << LC);
+                for (int i = tid; i < items; i += nth) {
+                    const int j = i >> LC, c = i & (C - 1);
+                    const uint2 qs = __ldg(reinterpret_cast<const uint2*>(tg) + j);
+                    const size_t p = (size_t)qs.x * W + c * V;
+                    const VW<V> xv = vld<V>(X + p);
+                    if (kp.do_dets && qs.y != NO_SLOT) vst<V>(ring + (size_t)qs.y * W + c * V, xv);
+                    if (kp.rec_out != nullptr)
+                        vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_words + tile * W + c * V, xv);
+                    if (kind == K_M) {
+                        vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_words<W, V>(kp, ob + j, c, g, tile)));
+                    } else {
+                        vst<V>(X + p, vzero<V>());
+                        vst<V>(Z + p, coin_words<W, V>(kp, ob + 2 * j + 1, c, g, tile));
+                    }
+                }
+                break;
+            }
+            case K_R: {
+                const int items = (int)(count << LC);
+                for (int i = tid; i < items; i += nth) {
+                    const int j = i >> LC, c = i & (C - 1);
+                    const size_t p = (size_t)__ldg(tg + j) * W + c * V;
+                    vst<V>(X + p, vzero<V>());
+                    vst<V>(Z + p, coin_words<W, V>(kp, ob + j, c, g, tile));
+                }
+                break;
+            }
+            case K_NOISE: {
+                const int ar = code == CH_DEP2 ? 2 : 1;
+                if (kp.masks != nullptr) {
+                    // injected masks: per target, x row then z row
+                    const int items = (int)((count * ar) << LC);
+                    for (int i = tid; i < items; i += nth) {
+                        const int j = i >> LC, c = i & (C - 1);
+                        const size_t p = (size_t)__ldg(tg + j) * W + c * V;
+                        const uint32_t* mrow = kp.masks + (int64_t)(oa + 2 * j) * kp.inject_words + tile * W + c * V;
+                        const VW<V> mx = vldg<V>(mrow), mz = vldg<V>(mrow + kp.inject_words);
+                        if (flags & F_DUP) {
+#pragma unroll
+                            for (int k = 0; k < V; k++) {
+                                if (mx.w[k]) atomicXor(X + p + k, mx.w[k]);
+                                if (mz.w[k]) atomicXor(Z + p + k, mz.w[k]);
+                            }
+                        } else {
+                            vst<V>(X + p, vxor<V>(vld<V>(X + p), mx));
+                            vst<V>(Z + p, vxor<V>(vld<V>(Z + p), mz));
+                        }
+                    }
+                    break;
+                }
+                const double prob = __ldg(kp.noise_p + ob);
+                if (!(prob > 0.0)) break;
+                const double log1m = __ldg(kp.noise_log1m + ob);
+                const int64_t k = __ldg(kp.noise_k + ob);
+                const int64_t A = count;
+                const int64_t n_chunks = (A + k - 1) / k;
+                const uint32_t npat = code == CH_DEP1 ? 3u : (code == CH_DEP2 ? 15u : 1u);
+                constexpr int64_t T = 32 * W;
+                for (int64_t r = tid; r < n_chunks; r += nth) {
+                    const int64_t a0 = r * k;
+                    const int64_t apps = (A - a0) < k ? (A - a0) : k;
+                    const int64_t len = apps * T;
+                    int64_t pos = -1;
+                    for (uint32_t j = 0;; j++) {
+                        uint32_t c0 = j, c1 = (uint32_t)r, c2 = g, c3 = DOMAIN_NOISE | ob;
+                        philox4x32_10(c0, c1, c2, c3, key0, key1);
+                        const uint64_t m53 = ((uint64_t)c0 << 21) | (c1 >> 11);
+                        const double u = (double)(m53 + 1ull) * 0x1.0p-53;
+                        const double gap = prob >= 1.0 ? 0.0 : floor(log(u) / log1m);
+                        if (gap >= (double)(len - 1 - pos)) break;
+                        pos += (int64_t)gap + 1;
+                        const uint32_t pick = (uint32_t)(((uint64_t)c2 * npat) >> 32);
+                        uint32_t xm, zm;
+                        pattern_of(code, pick, xm, zm);
+                        const int64_t app = a0 + pos / T;
+                        const int s = (int)(pos % T);
+                        const uint32_t bit = 1u << (s & 31);
+                        const int w = s >> 5;
+                        for (int sl = 0; sl < ar; sl++) {
+                            const size_t qrow = (size_t)__ldg(tg + app * ar + sl) * W + w;
+                            if (flags & F_DUP) {
+                                if ((xm >> sl) & 1u) atomicXor(X + qrow, bit);
+                                if ((zm >> sl) & 1u) atomicXor(Z + qrow, bit);
+                            } else {
+                                if ((xm >> sl) & 1u) X[qrow] ^= bit;
+                                if ((zm >> sl) & 1u) Z[qrow] ^= bit;
+                            }
+                        }
+                    }
+                }
+                break;
+            }
+            case K_DET: {
+                if (!kp.do_dets) break;
+                const int items = (int)(count << LC);
+                for (int i = tid; i < items; i += nth) {
+                    const uint32_t col = oa + (uint32_t)(i >> LC);
+                    const int c = i & (C - 1);
+                    VW<V> acc = vzero<V>();
+                    const uint32_t e0 = __ldg(kp.det_ptr + col), e1 = __ldg(kp.det_ptr + col + 1);
+                    for (uint32_t e = e0; e < e1; e++) {
+                        const uint32_t s = __ldg(kp.det_terms + e);
+                        acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
+                    }
+                    if (kp.ev_out != nullptr)
+                        vst<V>(kp.ev_out + (int64_t)col * kp.out_words + tile * W + c * V, acc);
+                    if (kp.counts != nullptr) {
+                        uint32_t tot = 0;
+#pragma unroll
+                        for (int jw = 0; jw < V; jw++) {
+                            const int64_t s0 = tile * (int64_t)(32 * W) + 32 * (c * V + jw);
+                            const int64_t rem = kp.num_shots - s0;
+                            const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+                            tot += __popc(acc.w[jw] & m);
+                        }
+                        if (tot) {
+                            if (kp.counts_in_smem) atomicAdd(cnt + col, tot);
+                            else atomicAdd(kp.counts + col, (unsigned long long)tot);
+                        }
+                    }
+                }
+                break;
+            }
+            case K_OBS: {
+                if (!kp.do_dets) break;
+                for (int c = tid; c < C; c += nth) {
+                    VW<V> acc = vld<V>(ring + (size_t)oa * W + c * V);
+                    for (uint32_t j = 0; j < count; j++) {
+                        const uint32_t s = __ldg(tg + j);
+                        acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
+                    }
+                    vst<V>(ring + (size_t)oa * W + c * V, acc);
+                }
+                break;
+            }
+            default: break;
+            }
+        }
+        __syncthreads();
+    }
+    if (kp.counts_in_smem) {
+        __syncthreads();
+        for (int i = tid; i < kp.num_cols; i += nth)
+            if (cnt[i]) atomicAdd(kp.counts + i, (unsigned long long)cnt[i]);
+    }
+}
+
+size_t frame_smem_bytes(int num_qubits, int W) { return (size_t)2 * num_qubits * W * 4; }
+
+template <int W, bool RS>
+static cudaError_t launch_t(const LaunchCfg& cfg, const KParams& kp, cudaStream_t st) {
+    frame_kernel<W, RS><<<cfg.grid, cfg.threads, cfg.smem_bytes, st>>>(kp);
+    return cudaGetLastError();
+}
+template <int W, bool RS>
+static cudaError_t smem_t(const LaunchCfg& cfg) {
+    return cudaFuncSetAttribute(frame_kernel<W, RS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)cfg.smem_bytes);
+}
+
+#define PFS_DISPATCH(FN, ...)                                                        \
+    switch (cfg.W) {                                                                 \
+        case 1: return cfg.ring_smem ? FN<1, true>(__VA_ARGS__) : FN<1, false>(__VA_ARGS__);   \
+        case 2: return cfg.ring_smem ? FN<2, true>(__VA_ARGS__) : FN<2, false>(__VA_ARGS__);   \
+        case 4: return cfg.ring_smem ? FN<4, true>(__VA_ARGS__) : FN<4, false>(__VA_ARGS__);   \
+        case 8: return cfg.ring_smem ? FN<8, true>(__VA_ARGS__) : FN<8, false>(__VA_ARGS__);   \
+        case 16: return cfg.ring_smem ? FN<16, true>(__VA_ARGS__) : FN<16, false>(__VA_ARGS__); \
+        case 32: return cfg.ring_smem ? FN<32, true>(__VA_ARGS__) : FN<32, false>(__VA_ARGS__); \
+        default: return cudaErrorInvalidValue;                                       \
+    }
+
+cudaError_t launch_frame_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStream_t stream) {
+    PFS_DISPATCH(launch_t, cfg, kp, stream)
+}
+cudaError_t set_frame_kernel_smem(const LaunchCfg& cfg) { PFS_DISPATCH(smem_t, cfg) }
+
+// ------------------------------------------------------------ transpose
+// Tile: 256 rows x 512 shots.  Block of 256 threads (8 warps).
+constexpr int TR_ROWS = 256;
+constexpr int TR_WORDS = 16;  // 512 shots
+
+__device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
+    // lane l holds row l (bit b = column b); afterwards lane l holds column l.
+#pragma unroll
+    for (int j = 16; j > 0; j >>= 1) {
+        const uint32_t mlo = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
+                           : j == 2 ? 0x33333333u : 0x55555555u;
+        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+        if (lane & j) v = (v & ~mlo) | ((other >> j) & mlo);
+        else v = (v & mlo) | ((other & mlo) << j);
+    }
+    return v;
+}
+
+__global__ void __launch_bounds__(256) rows_to_b8_kernel(const uint32_t* __restrict__ rows,
+                                                         int64_t num_rows, int64_t row_words,
+                                                         int64_t num_shots,
+                                                         const uint8_t* __restrict__ xor_bits,
+                                                         uint8_t* __restrict__ out, int64_t pitch) {
+    __shared__ uint32_t tin[TR_ROWS][TR_WORDS + 1];
+    __shared__ uint32_t tout[TR_WORDS * 32][TR_ROWS / 32 + 1];
+    const int t = threadIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.y * TR_ROWS;
+    const int64_t w0 = (int64_t)blockIdx.x * TR_WORDS;
+    {
+        const int64_t r = r0 + t;
+        uint32_t v[TR_WORDS];
+        if (r < num_rows) {
+            const uint32_t* src = rows + r * row_words + w0;
+            if (w0 + TR_WORDS <= row_words && (row_words & 3) == 0) {
+#pragma unroll
+                for (int k = 0; k < TR_WORDS / 4; k++) {
+                    const uint4 q = __ldg(reinterpret_cast<const uint4*>(src) + k);
+                    v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+                }
+            } else {
+#pragma unroll
+                for (int k = 0; k < TR_WORDS; k++) v[k] = (w0 + k < row_words) ? __ldg(src + k) : 0u;
+            }
+            if (xor_bits != nullptr && (__ldg(xor_bits + r) & 1u)) {
+#pragma unroll
+                for (int k = 0; k < TR_WORDS; k++) v[k] = ~v[k];
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < TR_WORDS; k++) v[k] = 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < TR_WORDS; k++) tin[t][k] = v[k];
+    }
+    __syncthreads();
+    const int warp = t >> 5, lane = t & 31;
+    for (int pair = warp; pair < (TR_ROWS / 32) * TR_WORDS; pair += 8) {
+        const int rb = pair / TR_WORDS, w = pair % TR_WORDS;
+        uint32_t v = tin[rb * 32 + lane][w];
+        v = transpose32_lane(v, lane);
+        tout[w * 32 + lane][rb] = v;
+    }
+    __syncthreads();
+    const int64_t nbytes = (num_rows + 7) >> 3;
+    const int64_t b0 = r0 >> 3;
+    const int64_t span = (nbytes - b0) < 32 ? (nbytes - b0) : 32;
+    const bool full = (pitch & 15) == 0 && ((uintptr_t)out & 15) == 0 && b0 + 32 <= pitch;
+    for (int sl = t; sl < TR_WORDS * 32; sl += 256) {
+        const int64_t s = w0 * 32 + sl;
+        if (s >= num_shots) break;
+        uint8_t* dst = out + s * pitch + b0;
+        if (full) {
+            reinterpret_cast<uint4*>(dst)[0] = make_uint4(tout[sl][0], tout[sl][1], tout[sl][2], tout[sl][3]);
+            reinterpret_cast<uint4*>(dst)[1] = make_uint4(tout[sl][4], tout[sl][5], tout[sl][6], tout[sl][7]);
+        } else {
+            for (int b = 0; b < span; b++) dst[b] = (uint8_t)(tout[sl][b >> 2] >> ((b & 3) * 8));
+        }
+    }
+}
+
+cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t row_words,
+                              int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
+                              int64_t pitch, cudaStream_t stream) {
+    if (num_rows <= 0 || num_shots <= 0) return cudaSuccess;
+    const int64_t used_words = (num_shots + 31) / 32;
+    dim3 grid((unsigned)((used_words + TR_WORDS - 1) / TR_WORDS),
+              (unsigned)((num_rows + TR_ROWS - 1) / TR_ROWS));
+    if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
+    rows_to_b8_kernel<<<grid, 256, 0, stream>>>(rows, num_rows, row_words, num_shots, xor_bits,
+                                                out, pitch);
+    return cudaGetLastError();
+}
+
+}  // namespace pfs

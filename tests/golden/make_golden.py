@@ -290,7 +290,7 @@ def make_pairs(num_det: int, per_round: int, seed: int, n_random: int = 4000):
     return np.array(pairs, dtype=np.int64).reshape(-1, 2)
 
 
-def gen_stats(procs: int):
+def gen_stats(procs: int, only=None):
     cases = [
         ("d3", gen.surface_code_memory(3, 3, 1e-2), 1 << 16, 1024, 8),
         ("d5", gen.surface_code_memory(5, 5, 5e-3), 1 << 16, 4096, 24),
@@ -298,13 +298,15 @@ def gen_stats(procs: int):
         ("d25", gen.surface_code_memory(25, 25, 1e-3), 1 << 16, 8192, 624),
     ]
     for name, text, shots, B, per_round in cases:
+        if only and name not in only:
+            continue
         t0 = time.time()
         c = mc.parse(text)
         nd = len(mc.detector_and_observable_sets(c))
         pairs = make_pairs(nd, per_round, 3)
         per = shots // procs
         jobs = [(text, per, 1000 + i, B, pairs) for i in range(procs)]
-        with mp.Pool(procs) as pool:
+        with mp.get_context("spawn").Pool(procs) as pool:
             res = pool.map(_stat_worker, jobs)
         counts = sum(r[0] for r in res)
         pc = sum(r[1] for r in res)
@@ -349,3 +351,6 @@ if __name__ == "__main__":
         gen_noiseless()
     if "stats" in which:
         gen_stats(min(8, os.cpu_count() or 1))
+    for w in which:
+        if w.startswith("stats_"):
+            gen_stats(min(8, os.cpu_count() or 1), only={w[6:]})

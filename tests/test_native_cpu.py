@@ -1,0 +1,95 @@
+"""libpfs.so on the CPU side: it loads, exports every symbol include/pfs.h
+declares, and its host compiler (no GPU needed) behaves.  No compute calls."""
+
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+from paper_2103_02202_b200 import _native as N
+from paper_2103_02202_b200 import generators as gen
+from paper_2103_02202_b200.program import flatten, noise_chunks
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module", autouse=True)
+def built():
+    from paper_2103_02202_b200.build import build
+    build()
+
+
+def test_exports_match_header():
+    with open(os.path.join(REPO, "include", "pfs.h")) as f:
+        hdr = f.read()
+    declared = set(re.findall(r"\b(pfs_[a-z_]+)\s*\(", hdr))
+    assert declared == set(N.EXPORTS)
+    L = ctypes.CDLL(N.LIB_PATH)
+    for name in declared:
+        assert hasattr(L, name), name
+    assert N.lib().pfs_version() == 1
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 3])
+def test_program_info_matches_survey_counts(cfg):
+    f = flatten(gen.config_circuit(cfg))
+    p = N.NativeProgram(f)
+    info = p.info
+    assert info["bframe_bits"] == {0: 708, 1: 75181, 3: 3700}[cfg]
+    assert info["num_measurements"] == f.num_measurements
+    assert info["num_columns"] == f.num_columns
+    assert info["tile_shots"] == 32 * info["words_per_tile"]
+    assert np.array_equal(p.noise_chunks(), noise_chunks(f, p.tile_shots))
+
+
+def test_d25_layout():
+    f = flatten(gen.surface_code_memory(25, 25, 1e-3))
+    p = N.NativeProgram(f)
+    assert p.info["bframe_bits"] == 518500
+    assert p.info["smem_bytes"] <= 227 * 1024
+    for W in (1, 2, 4, 8, 16):
+        q = N.NativeProgram(f, words_per_tile=W, ring_in_smem=0)
+        assert q.info["tile_shots"] == 32 * W and q.info["ring_in_smem"] == 0
+
+
+def test_conflicting_instruction_is_split():
+    # CX 0 1 1 2 must stay two sequential steps (frame_sim.py:61-62)
+    f = flatten("CX 0 1 1 2\nM 0 1 2\n")
+    p = N.NativeProgram(f)
+    assert p.info["num_ops"] == 3
+    f2 = flatten("CX 0 1 2 3\nCX 4 5\nM 0 1 2 3 4 5\n")
+    assert N.NativeProgram(f2).info["num_ops"] == 2  # merged CX, one M
+
+
+def test_errors_are_value_errors():
+    f = flatten("H 0\nM 0\nDETECTOR rec[-1]\n")
+    bad = flatten("H 0\nM 0\nDETECTOR rec[-1]\n")
+    bad.instrs = bad.instrs.copy()
+    bad.instrs[0, 2] = 5  # target range past the end
+    with pytest.raises(ValueError):
+        N.NativeProgram(bad)
+    bad2 = flatten("X_ERROR(0.1) 0\n")
+    bad2.noise_p = np.array([1.5])
+    with pytest.raises(ValueError, match="noise probability"):
+        N.NativeProgram(bad2)
+    # a program whose frame table can never fit one CTA
+    big = flatten("H 40000\n")
+    with pytest.raises(ValueError, match="does not fit"):
+        N.NativeProgram(big)
+    p = N.NativeProgram(f)
+    with pytest.raises(ValueError, match="num_shots must be >= 1"):
+        p.run(N.MODE_DETECTORS, 0, 1, np.zeros(8, np.uint8), 8)
+
+
+def test_oracle_not_reachable_from_product():
+    """The product package must not import the oracle (it is the checker)."""
+    pkg = os.path.join(REPO, "paper_2103_02202_b200")
+    for root, _, files in os.walk(pkg):
+        for fn in files:
+            if fn.endswith((".py", ".cu", ".cpp", ".h")):
+                with open(os.path.join(root, fn)) as f:
+                    src = f.read()
+                assert "import oracle" not in src and "from oracle" not in src, fn
+                assert "pfs_oracle" not in src, fn
