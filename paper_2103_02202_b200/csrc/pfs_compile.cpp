@@ -151,6 +151,9 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     std::vector<int64_t> stamp(num_qubits, -1);
     int64_t cur = -1;  // open (mergeable) op index
     auto open_op = [&](uint32_t kind, uint32_t code) {
+        // ops read their targets as uint2 pairs (two-qubit rules, (qubit, slot)
+        // pairs of M/MR): keep every op's target list 8-byte aligned
+        if (hp.targets.size() & 1) hp.targets.push_back(0u);
         DOp op{};
         op.kcf = kind | (code << 8);
         op.off = (uint32_t)hp.targets.size();
