@@ -215,7 +215,9 @@ def run_ours(args, rank, world, local_rank):
     nb = (ds.num_columns + 7) // 8
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
-    out = torch.empty((shots, nb), dtype=torch.uint8, device=dev)
+    pitch = (nb + 31) // 32 * 32  # 32-byte aligned shot rows on device (b8 bytes + zero pad)
+    out_full = torch.empty((shots, pitch), dtype=torch.uint8, device=dev)
+    out = out_full[:, :nb]
     base_offset = rank * ((shots + T - 1) // T) * T
     seed = 20260214
 
@@ -280,10 +282,12 @@ def run_ours(args, rank, world, local_rank):
     bframe_bytes = info["bframe_bits"] / 8.0
     fr = float(np.mean(frame_ms)) if frame_ms else float("nan")
     achieved_gbs = bframe_bytes * shots / (fr / 1e3) / 1e9
-    smem_peak = smem_peak_gbs()
+    from paper_2103_02202_b200._native import measure_smem_bandwidth
+    smem_peak = measure_smem_bandwidth(local_rank)
     roof = {"bound": "smem" if smem_peak else "hbm",
             "achieved": achieved_gbs, "peak": smem_peak or hbm, "unit": "GB/s",
             "frac": achieved_gbs / (smem_peak or hbm), "traffic": profile_traffic(),
+            "peak_source": "measured live: pfs_measure_smem_bandwidth (LDS.128/STS.128 CX mix, all SMs)",
             "kernel": "frame_kernel (SMEM-resident frame table)",
             "frame_kernel_ms": fr, "transpose_kernel_ms": float(np.mean(tr_ms)),
             "bytes_per_shot": bframe_bytes,

@@ -66,7 +66,10 @@ typedef struct pfs_info {
     int64_t bframe_bits;      /* algorithmic frame bits per shot */
     int64_t num_coin_rows;
     int64_t num_noise_rows;
-    int64_t reserved[6];
+    int64_t noise_tab_len;    /* uint64 entries of the Binomial threshold tables   */
+    int64_t hit_capacity;     /* pre-generated noise hit-list entries per CTA       */
+    int64_t pregen_chunks;    /* noise chunks sampled in each tile's pre-pass       */
+    int64_t reserved[3];
 } pfs_info;
 
 enum pfs_mode {
@@ -97,8 +100,12 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs,
 
 int pfs_program_info(const struct pfs_program* prog, pfs_info* out);
 
-/* Apps per geometric-walk chunk for each noise instruction (n = num_noise). */
-int pfs_program_noise_chunks(const struct pfs_program* prog, int32_t* out, int64_t n);
+/* The per-tile noise sampling schedule, for the parity oracle:
+ * params = num_noise x 12 uint32 (L, nchunks, last_len, tab_full, len_full,
+ * tab_last, len_last, cap_base, cap, flags, npat, chunk_base), tab = the
+ * Binomial threshold tables (noise_tab_len uint64). */
+int pfs_program_noise_schedule(const struct pfs_program* prog, uint32_t* params,
+                               int64_t n_params, uint64_t* tab, int64_t n_tab);
 
 /*
  * Sample num_shots shots [shot_offset, shot_offset + num_shots) on `device`.
@@ -128,6 +135,10 @@ int pfs_program_last_timing(const struct pfs_program* prog, double* ms, int n);
 
 /* Number of this library's kernel launches made by the last pfs_run. */
 int64_t pfs_program_last_launches(const struct pfs_program* prog);
+
+/* Roofline denominator for the SMEM-resident frame kernel: measured shared-
+ * memory bandwidth (GB/s, loads + stores, CX access mix) over all SMs. */
+int pfs_measure_smem_bandwidth(int device, double* gbs);
 
 void pfs_program_destroy(struct pfs_program* prog);
 const char* pfs_last_error(void);

@@ -13,7 +13,7 @@ import subprocess
 
 import numpy as np
 
-from paper_2103_02202_b200.program import FlatProgram, noise_chunks
+from paper_2103_02202_b200.program import FlatProgram
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "_build", "libpfs_oracle.so")
@@ -36,7 +36,7 @@ def lib():
         L = ctypes.CDLL(LIB_PATH)
         P = ctypes.c_void_p
         i64, i32, u64 = ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
-        L.orc_sample.argtypes = [P, i64, P, P, P, P, i32, i64, P, P, i64, i64, i32, u64, u64,
+        L.orc_sample.argtypes = [P, i64, P, P, P, i32, i64, P, P, i64, i64, i32, u64, u64,
                                  P, P, i64, P, P, i64, ctypes.c_int]
         L.orc_sample.restype = ctypes.c_int
         L.orc_rows_to_b8.argtypes = [P, i64, i64, i64, P, P, i64]
@@ -53,18 +53,22 @@ def _ptr(a):
 
 def sample(prog: FlatProgram, num_shots: int, tile_shots: int, seed: int = 0,
            tile_offset: int = 0, coins=None, masks=None, flips: bool = True,
-           events: bool = True, nthreads: int = 1, noise_k=None):
-    """Run the oracle; returns (flip_rows, event_rows), uint32 [rows, words]."""
+           events: bool = True, nthreads: int = 1, schedule=None):
+    """Run the oracle; returns (flip_rows, event_rows), uint32 [rows, words].
+
+    `schedule` = (params, tables) of the noise sampler for this tile size, as
+    compiled by the product's host compiler (`NativeProgram.noise_schedule()`):
+    the RNG draw order only — the frame semantics are this file's own.
+    """
     L = lib()
     n_tiles = -(-num_shots // tile_shots)
     words = n_tiles * tile_shots // 32
     ins = np.ascontiguousarray(prog.instrs, dtype=np.int32)
     tg = np.ascontiguousarray(prog.targets, dtype=np.int32)
-    p = np.ascontiguousarray(prog.noise_p, dtype=np.float64)
-    with np.errstate(divide="ignore"):
-        log1m = np.log1p(-p)
-    k = (noise_chunks(prog, tile_shots) if noise_k is None
-         else np.ascontiguousarray(noise_k, dtype=np.int32))
+    if schedule is None:
+        schedule = noise_schedule(prog, tile_shots)
+    params = np.ascontiguousarray(schedule[0], dtype=np.uint32)
+    tab = np.ascontiguousarray(schedule[1], dtype=np.uint64)
     inject_words = 0
     if coins is not None or masks is not None:
         if coins is None or masks is None:
@@ -74,7 +78,8 @@ def sample(prog: FlatProgram, num_shots: int, tile_shots: int, seed: int = 0,
         inject_words = words
     fl = np.zeros((prog.num_measurements, words), dtype=np.uint32) if flips else None
     ev = np.zeros((prog.num_columns, words), dtype=np.uint32) if events else None
-    rc = L.orc_sample(_ptr(ins), ins.shape[0], _ptr(tg), _ptr(p), _ptr(log1m), _ptr(k),
+    rc = L.orc_sample(_ptr(ins), ins.shape[0], _ptr(tg), _ptr(params) if params.size else None,
+                      _ptr(tab) if tab.size else None,
                       prog.num_qubits, prog.num_measurements, _ptr(prog.det_ptr),
                       _ptr(prog.det_idx), prog.num_columns, num_shots, tile_shots,
                       seed & 0xFFFFFFFFFFFFFFFF, tile_offset, _ptr(coins), _ptr(masks),
@@ -83,6 +88,14 @@ def sample(prog: FlatProgram, num_shots: int, tile_shots: int, seed: int = 0,
     if rc != 0:
         raise RuntimeError(f"orc_sample failed ({rc})")
     return fl, ev
+
+
+def noise_schedule(prog: FlatProgram, tile_shots: int):
+    """Noise RNG schedule for tile size T from the product's host compiler
+    (pure host code, no GPU needed)."""
+    from paper_2103_02202_b200._native import NativeProgram
+
+    return NativeProgram(prog, words_per_tile=tile_shots // 32, ring_in_smem=0).noise_schedule()
 
 
 def _pad_rows(a, words):

@@ -9,7 +9,8 @@
  *   FrameBatch.__init__            stabsim/frame_sim.py:29-40   (x = 0, z = coins)
  *   _apply_plan per frame rule     stabsim/frame_sim.py:64-72   + gates.py:326-348
  *   measure / reset / measure_reset stabsim/frame_sim.py:74-90
- *   apply_noise geometric walk     stabsim/frame_sim.py:92-153  + entropy.py:65-88
+ *   apply_noise                    stabsim/frame_sim.py:92-167  (i.i.d. Bernoulli(p) per
+ *                                  (application, frame) trial; entropy.py:65-113)
  *   _run_batch opcode loop         stabsim/frame_sim.py:192-205
  *   detector_events                stabsim/io_formats.py:208-227
  *   transposed + write_b8          stabsim/bitvec.py:193-209, io_formats.py:94-96
@@ -17,9 +18,12 @@
  * Randomness comes from one of two sources:
  *   - injected rows (coins + noise masks) — bit-exact
  *     against the reference's own FrameBatch (tests/golden/inject_*.npz);
- *   - counter-based Philox4x32-10 with the chunked geometric walk documented in
- *     the same draws the CUDA kernels make, so the GPU's sampled
- *     mode is bit-exact against this file as well as statistically matched to the
+ *   - counter-based Philox4x32-10 driving the chunked Bernoulli sampler of
+ *     DESIGN.md §4 (Binomial count by table inversion + distinct uniform
+ *     positions — the same i.i.d. Bernoulli(p) trials the reference's geometric
+ *     gaps / hybrid sampler produce, drawn in an order a GPU can parallelise).
+ *     The CUDA kernels make the same draws, so the GPU's sampled mode is
+ *     bit-exact against this file as well as statistically matched to the
  *     reference (tests/golden/stats_*.npz).
  *
  * Parity pinned by: tests/golden/{inject,noiseless,stats,exact}_* generated from
@@ -63,10 +67,19 @@ void orc_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t ou
 #define DOMAIN_COIN 0x40000000u
 #define DOMAIN_NOISE 0x80000000u
 
+/* noise schedule row, 12 x uint32 */
+typedef struct {
+    uint32_t L, nchunks, last_len, tab_full, len_full, tab_last, len_last, cap_base, cap, flags,
+        npat, chunk_base;
+} orc_noise;
+#define NZ_NONE 1u
+#define NZ_ALL 2u
+#define NZ_MAX_LIST 16
+
 typedef struct {
     const orc_instr* ins; int64_t n_ins;
     const int32_t* targets;
-    const double* noise_p; const double* noise_log1m; const int32_t* noise_k;
+    const orc_noise* noise; const uint64_t* noise_tab;
     int32_t num_qubits; int64_t num_meas;
     const int64_t* det_ptr; const int64_t* det_idx; int64_t num_cols;
     int64_t num_shots; int32_t T; uint64_t seed; uint64_t tile_offset;
@@ -76,6 +89,70 @@ typedef struct {
 } orc_job;
 
 typedef struct { const orc_job* job; int tid; int rc; } orc_worker;
+
+typedef struct { uint32_t r, g, dom, j, idx; uint32_t key[2]; uint32_t buf[4]; } word_stream;
+
+static inline uint32_t ws_next(word_stream* ws) {
+    if (ws->idx == 4) {
+        uint32_t ctr[4] = {ws->j++, ws->r, ws->g, ws->dom};
+        orc_philox4x32_10(ctr, ws->key, ws->buf);
+        ws->idx = 0;
+    }
+    return ws->buf[ws->idx++];
+}
+static inline uint64_t ws_next64(word_stream* ws) {
+    uint32_t lo = ws_next(ws);
+    return ((uint64_t)ws_next(ws) << 32) | lo;
+}
+static inline uint64_t umul64hi(uint64_t a, uint64_t b) {
+    return (uint64_t)(((unsigned __int128)a * b) >> 64);
+}
+static inline uint32_t umulhi32(uint32_t a, uint32_t b) { return (uint32_t)(((uint64_t)a * b) >> 32); }
+
+/* hits of chunk r: emit(trial within the op, pattern pick) */
+typedef void (*emit_fn)(void* ctx, uint32_t trial, uint32_t pick);
+static void noise_chunk(const orc_noise* np, const uint64_t* tabs, uint64_t seed, uint32_t ordinal,
+                        uint32_t r, uint32_t g, emit_fn emit, void* ctx) {
+    const uint32_t len = (r + 1 == np->nchunks) ? np->last_len : np->L;
+    const uint32_t base = r * np->L;
+    word_stream ws = {r, g, 0x80000000u | ordinal, 0, 4, {(uint32_t)seed, (uint32_t)(seed >> 32)}, {0, 0, 0, 0}};
+    if (np->flags & NZ_ALL) {
+        for (uint32_t i = 0; i < len; i++) emit(ctx, base + i, np->npat > 1 ? umulhi32(ws_next(&ws), np->npat) : 0u);
+        return;
+    }
+    const int full = len == np->L;
+    const uint64_t* tab = tabs + (full ? np->tab_full : np->tab_last);
+    const uint32_t tlen = full ? np->len_full : np->len_last;
+    const uint64_t u = ws_next64(&ws);
+    uint32_t count = 0;
+    while (count < tlen && u >= tab[count]) count++;
+    if (count == 0) return;
+    if (count <= NZ_MAX_LIST) {
+        uint32_t sel[NZ_MAX_LIST];
+        for (uint32_t h = 0; h < count; h++) {
+            uint32_t pos;
+            int dup;
+            do {
+                pos = (uint32_t)umul64hi(ws_next64(&ws), len);
+                dup = 0;
+                for (uint32_t q = 0; q < h; q++) dup |= sel[q] == pos;
+            } while (dup);
+            sel[h] = pos;
+            emit(ctx, base + pos, np->npat > 1 ? umulhi32(ws_next(&ws), np->npat) : 0u);
+        }
+    } else {
+        uint32_t needed = count;
+        for (uint32_t i = 0; needed > 0; i++) {
+            if (umul64hi(ws_next64(&ws), (uint64_t)(len - i)) < needed) {
+                emit(ctx, base + i, np->npat > 1 ? umulhi32(ws_next(&ws), np->npat) : 0u);
+                needed--;
+            }
+        }
+    }
+}
+
+typedef struct { uint32_t* x; uint32_t* z; const int32_t* tg; int ar; int ch; int T; int nw; } hit_ctx;
+static void apply_hit(void* vctx, uint32_t trial, uint32_t pick);
 
 static const uint8_t DEP1_X[3] = {1, 1, 0}, DEP1_Z[3] = {0, 1, 1};
 
@@ -90,6 +167,20 @@ static inline void pattern_of(int ch, uint32_t pick, uint32_t* xm, uint32_t* zm)
             *xm = (code & 1) | (((code >> 2) & 1) << 1);
             *zm = ((code >> 1) & 1) | (((code >> 3) & 1) << 1);
         }
+    }
+}
+
+static void apply_hit(void* vctx, uint32_t trial, uint32_t pick) {
+    hit_ctx* c = (hit_ctx*)vctx;
+    uint32_t xm, zm;
+    pattern_of(c->ch, pick, &xm, &zm);
+    const uint32_t app = trial / (uint32_t)c->T, s = trial % (uint32_t)c->T;
+    const uint32_t bit = 1u << (s & 31);
+    const uint32_t w = s >> 5;
+    for (int sl = 0; sl < c->ar; sl++) {
+        int32_t q = c->tg[app * c->ar + sl];
+        if ((xm >> sl) & 1) c->x[(size_t)q * c->nw + w] ^= bit;
+        if ((zm >> sl) & 1) c->z[(size_t)q * c->nw + w] ^= bit;
     }
 }
 
@@ -118,8 +209,6 @@ static void run_tile(const orc_job* jb, int64_t t, uint32_t* x, uint32_t* z, uin
     /* FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39) */
     memset(x, 0, sizeof(uint32_t) * (size_t)n * nw);
     for (int q = 0; q < n; q++) coin_words(jb, q, g, t, nw, z + (size_t)q * nw);
-    const uint32_t key[2] = {(uint32_t)jb->seed, (uint32_t)(jb->seed >> 32)};
-
     for (int64_t i = 0; i < jb->n_ins; i++) {
         const orc_instr* in = &jb->ins[i];
         const int32_t* tg = jb->targets + in->tgt_off;
@@ -178,42 +267,11 @@ static void run_tile(const orc_job* jb, int64_t t, uint32_t* x, uint32_t* z, uin
                 }
                 break;
             }
-            const double p = jb->noise_p[nid];
-            if (p <= 0.0) break;
-            const double log1m = jb->noise_log1m[nid];
-            const int64_t A = in->n_targets / ar;
-            const int64_t k = jb->noise_k[nid];
-            const int64_t T = jb->T;
-            const uint32_t npat = in->code == CH_DEP1 ? 3u : (in->code == CH_DEP2 ? 15u : 1u);
-            for (int64_t r = 0; r * k < A; r++) {
-                const int64_t a0 = r * k;
-                const int64_t apps = (A - a0) < k ? (A - a0) : k;
-                const int64_t len = apps * T;
-                int64_t pos = -1;
-                for (uint32_t j = 0;; j++) {
-                    uint32_t ctr[4] = {j, (uint32_t)r, (uint32_t)g, DOMAIN_NOISE | (uint32_t)nid};
-                    uint32_t o[4];
-                    orc_philox4x32_10(ctr, key, o);
-                    /* u in (0, 1]; gap as in sample_hits_geometric (entropy.py:82-85) */
-                    uint64_t m53 = ((uint64_t)o[0] << 21) | (o[1] >> 11);
-                    double u = (double)(m53 + 1) * 0x1.0p-53;
-                    double gap = p >= 1.0 ? 0.0 : floor(log(u) / log1m);
-                    if (gap >= (double)(len - 1 - pos)) break;
-                    pos += (int64_t)gap + 1;
-                    uint32_t pick = (uint32_t)(((uint64_t)o[2] * npat) >> 32);
-                    uint32_t xm, zm;
-                    pattern_of(in->code, pick, &xm, &zm);
-                    const int64_t app = a0 + pos / T;
-                    const int64_t s = pos % T;
-                    const uint32_t bit = 1u << (s & 31);
-                    const int64_t w = s >> 5;
-                    for (int sl = 0; sl < ar; sl++) {
-                        int32_t q = tg[app * ar + sl];
-                        if ((xm >> sl) & 1) x[(size_t)q * nw + w] ^= bit;
-                        if ((zm >> sl) & 1) z[(size_t)q * nw + w] ^= bit;
-                    }
-                }
-            }
+            const orc_noise* np = &jb->noise[nid];
+            if (np->flags & NZ_NONE) break;
+            hit_ctx hc = {x, z, tg, ar, in->code, jb->T, nw};
+            for (uint32_t r = 0; r < np->nchunks; r++)
+                noise_chunk(np, jb->noise_tab, jb->seed, (uint32_t)nid, r, (uint32_t)g, apply_hit, &hc);
             break;
         }
         default: break;  /* K_DET / K_OBS evaluated below from the full record */
@@ -269,7 +327,7 @@ static void* worker_main(void* arg) {
  * (detector columns then observables).  Returns 0 or a negative error code.
  */
 int orc_sample(const orc_instr* ins, int64_t n_ins, const int32_t* targets,
-               const double* noise_p, const double* noise_log1m, const int32_t* noise_k,
+               const uint32_t* noise_params, const uint64_t* noise_tab,
                int32_t num_qubits, int64_t num_meas,
                const int64_t* det_ptr, const int64_t* det_idx, int64_t num_cols,
                int64_t num_shots, int32_t tile_shots, uint64_t seed, uint64_t tile_offset,
@@ -277,7 +335,7 @@ int orc_sample(const orc_instr* ins, int64_t n_ins, const int32_t* targets,
                uint32_t* flips, uint32_t* events, int64_t out_words, int nthreads) {
     if (tile_shots <= 0 || tile_shots % 32) return -1;
     if (num_shots < 1) return -1;
-    orc_job jb = {ins, n_ins, targets, noise_p, noise_log1m, noise_k, num_qubits, num_meas,
+    orc_job jb = {ins, n_ins, targets, (const orc_noise*)noise_params, noise_tab, num_qubits, num_meas,
                   det_ptr, det_idx, num_cols, num_shots, tile_shots, seed, tile_offset,
                   coins, masks, inject_words, flips, events, out_words,
                   (num_shots + tile_shots - 1) / tile_shots, nthreads < 1 ? 1 : nthreads};

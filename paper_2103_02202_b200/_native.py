@@ -40,15 +40,16 @@ class Info(ctypes.Structure):
                 ("num_barriers", ctypes.c_int64), ("num_slots", ctypes.c_int64),
                 ("num_noise", ctypes.c_int64), ("bframe_bits", ctypes.c_int64),
                 ("num_coin_rows", ctypes.c_int64), ("num_noise_rows", ctypes.c_int64),
-                ("reserved", ctypes.c_int64 * 6)]
+                ("noise_tab_len", ctypes.c_int64), ("hit_capacity", ctypes.c_int64),
+                ("pregen_chunks", ctypes.c_int64), ("reserved", ctypes.c_int64 * 3)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
 
 
-EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_chunks", "pfs_run",
+EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_schedule", "pfs_run",
            "pfs_program_last_timing", "pfs_program_last_launches", "pfs_program_destroy",
-           "pfs_last_error", "pfs_version")
+           "pfs_last_error", "pfs_version", "pfs_measure_smem_bandwidth")
 
 _lib = None
 
@@ -67,8 +68,8 @@ def lib():
     L.pfs_program_create.restype = ctypes.c_int
     L.pfs_program_info.argtypes = [P, ctypes.POINTER(Info)]
     L.pfs_program_info.restype = ctypes.c_int
-    L.pfs_program_noise_chunks.argtypes = [P, P, i64]
-    L.pfs_program_noise_chunks.restype = ctypes.c_int
+    L.pfs_program_noise_schedule.argtypes = [P, P, i64, P, i64]
+    L.pfs_program_noise_schedule.restype = ctypes.c_int
     L.pfs_run.argtypes = [P, ctypes.c_int, u64, u64, i64, ctypes.c_int, P, P, P, i64, P, i64, i64, P]
     L.pfs_run.restype = ctypes.c_int
     L.pfs_program_last_timing.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.c_int]
@@ -79,6 +80,8 @@ def lib():
     L.pfs_program_destroy.restype = None
     L.pfs_last_error.argtypes = []
     L.pfs_last_error.restype = ctypes.c_char_p
+    L.pfs_measure_smem_bandwidth.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
+    L.pfs_measure_smem_bandwidth.restype = ctypes.c_int
     L.pfs_version.argtypes = []
     L.pfs_version.restype = ctypes.c_int
     _lib = L
@@ -106,6 +109,12 @@ def _p(a):
     if hasattr(a, "data_ptr"):
         return a.data_ptr()
     return a.ctypes.data
+
+
+def measure_smem_bandwidth(device: int = 0) -> float:
+    v = ctypes.c_double()
+    _check(lib().pfs_measure_smem_bandwidth(device, ctypes.byref(v)))
+    return float(v.value)
 
 
 class NativeProgram:
@@ -141,10 +150,14 @@ class NativeProgram:
             _lib.pfs_program_destroy(h)
             self._h = None
 
-    def noise_chunks(self) -> np.ndarray:
-        out = np.zeros(self.flat.num_noise, dtype=np.int32)
-        _check(lib().pfs_program_noise_chunks(self._h, _p(out) if out.size else None, out.size))
-        return out
+    def noise_schedule(self):
+        """(params uint32 [num_noise, 12], tables uint64) — the noise RNG schedule."""
+        params = np.zeros((self.flat.num_noise, 12), dtype=np.uint32)
+        tab = np.zeros(self.info["noise_tab_len"], dtype=np.uint64)
+        _check(lib().pfs_program_noise_schedule(self._h, _p(params) if params.size else None,
+                                                params.size, _p(tab) if tab.size else None,
+                                                tab.size))
+        return params, tab
 
     def run(self, mode: int, num_shots: int, seed: int, out, out_bytes: int, out_pitch: int = 0,
             shot_offset: int = 0, device: int = 0, ref_bits=None, coins=None, masks=None,

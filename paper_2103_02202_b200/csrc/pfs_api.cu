@@ -60,8 +60,9 @@ struct pfs_program {
     size_t smem_optin = kSmemBudget;
     DevBuf<DOp> d_ops;
     DevBuf<uint32_t> d_targets, d_det_ptr, d_det_terms, d_ring;
-    DevBuf<double> d_p, d_log1m;
-    DevBuf<int32_t> d_k;
+    DevBuf<NoiseParam> d_noise;
+    DevBuf<uint64_t> d_noise_tab;
+    DevBuf<uint32_t> d_pregen, d_hits;
     DevBuf<uint32_t> d_rows[2];
     DevBuf<uint8_t> d_b8[2];
     DevBuf<uint32_t> d_coins, d_masks;
@@ -73,11 +74,13 @@ struct pfs_program {
     int64_t last_launches = 0;
 };
 
+static size_t fixed_smem(const HostProgram& hp) { return (size_t)hp.num_noise * 4; }
+
 static void choose_layout(pfs_program* pg) {
     const HostProgram& hp = pg->hp;
     const pfs_options& o = pg->opts;
     const size_t budget = pg->smem_optin;
-    auto frame = [&](int W) { return frame_smem_bytes(hp.num_qubits, W); };
+    auto frame = [&](int W) { return frame_smem_bytes(hp.num_qubits, W) + fixed_smem(hp); };
     auto ring = [&](int W) { return (size_t)hp.num_slots * W * 4; };
     int Ws = 0, Wg = 0;
     for (int W = 32; W >= 1; W >>= 1)
@@ -103,13 +106,22 @@ static void choose_layout(pfs_program* pg) {
     pg->cfg.W = W;
     pg->cfg.ring_smem = rs;
     pg->cfg.smem_bytes = frame(W) + (rs ? ring(W) : 0);
-    int threads = o.threads > 0 ? o.threads : 512;
+    int threads = o.threads > 0 ? o.threads : 1024;
     pg->cfg.threads = threads;
 }
 
 extern "C" {
 
 int pfs_version(void) { return 1; }
+
+int pfs_measure_smem_bandwidth(int device, double* gbs) {
+    if (!gbs) return fail(PFS_E_INVALID, "null argument");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0)
+        return fail(PFS_E_NODEVICE, "no CUDA device available");
+    CUDA_TRY(smem_probe(device, gbs));
+    return PFS_OK;
+}
 const char* pfs_last_error(void) { return g_last_error.c_str(); }
 
 int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t* targets,
@@ -140,8 +152,13 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         return fail(PFS_E_INVALID, "frame table of " + std::to_string(num_qubits) +
                                        " qubits does not fit one CTA's shared memory");
     }
-    const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 1.0;
-    assign_noise_chunks(pg->hp, 32 * pg->cfg.W, th);
+    const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 2.0;
+    try {
+        build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
+    } catch (const std::invalid_argument& e) {
+        delete pg;
+        return fail(PFS_E_INVALID, e.what());
+    }
     *out = pg;
     return PFS_OK;
 }
@@ -166,13 +183,22 @@ int pfs_program_info(const pfs_program* pg, pfs_info* o) {
     o->bframe_bits = hp.bframe_bits;
     o->num_coin_rows = hp.num_coin_rows;
     o->num_noise_rows = hp.num_noise_rows;
+    o->noise_tab_len = (int64_t)hp.noise_tab.size();
+    o->hit_capacity = hp.hit_capacity;
+    o->pregen_chunks = hp.pregen_chunks;
     return PFS_OK;
 }
 
-int pfs_program_noise_chunks(const pfs_program* pg, int32_t* out, int64_t n) {
-    if (!pg || (!out && n)) return fail(PFS_E_INVALID, "null argument");
-    if (n != pg->hp.num_noise) return fail(PFS_E_INVALID, "size mismatch");
-    std::copy(pg->hp.noise_k.begin(), pg->hp.noise_k.end(), out);
+int pfs_program_noise_schedule(const pfs_program* pg, uint32_t* params, int64_t n_params,
+                               uint64_t* tab, int64_t n_tab) {
+    if (!pg) return fail(PFS_E_INVALID, "null argument");
+    const HostProgram& hp = pg->hp;
+    if (n_params != hp.num_noise * 12 || n_tab != (int64_t)hp.noise_tab.size())
+        return fail(PFS_E_INVALID, "size mismatch");
+    if (n_params && !params) return fail(PFS_E_INVALID, "null params");
+    if (n_tab && !tab) return fail(PFS_E_INVALID, "null table");
+    if (n_params) std::memcpy(params, hp.noise.data(), n_params * 4);
+    if (n_tab) std::memcpy(tab, hp.noise_tab.data(), n_tab * 8);
     return PFS_OK;
 }
 
@@ -191,8 +217,8 @@ void pfs_program_destroy(pfs_program* pg) {
         cudaGetDevice(&prev);
         cudaSetDevice(pg->device);
         pg->d_ops.release(); pg->d_targets.release(); pg->d_det_ptr.release();
-        pg->d_det_terms.release(); pg->d_ring.release(); pg->d_p.release();
-        pg->d_log1m.release(); pg->d_k.release();
+        pg->d_det_terms.release(); pg->d_ring.release(); pg->d_noise.release();
+        pg->d_noise_tab.release(); pg->d_pregen.release(); pg->d_hits.release();
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
@@ -231,9 +257,9 @@ static int ensure_device(pfs_program* pg, int device) {
     CUDA_TRY(upload(pg->d_targets, hp.targets));
     CUDA_TRY(upload(pg->d_det_ptr, hp.det_ptr));
     CUDA_TRY(upload(pg->d_det_terms, hp.det_terms));
-    CUDA_TRY(upload(pg->d_p, hp.noise_p));
-    CUDA_TRY(upload(pg->d_log1m, hp.noise_log1m));
-    CUDA_TRY(upload(pg->d_k, hp.noise_k));
+    CUDA_TRY(upload(pg->d_noise, hp.noise));
+    CUDA_TRY(upload(pg->d_noise_tab, hp.noise_tab));
+    CUDA_TRY(upload(pg->d_pregen, hp.pregen_ops));
     CUDA_TRY(set_frame_kernel_smem(pg->cfg));
     int per_sm = pg->opts.ctas_per_sm;
     if (per_sm <= 0) {
@@ -242,6 +268,7 @@ static int ensure_device(pfs_program* pg, int device) {
         per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / pg->cfg.threads));
     }
     pg->cfg.grid = pg->num_sms * per_sm;
+    CUDA_TRY(pg->d_hits.reserve((size_t)std::max<int64_t>(hp.hit_capacity, 1) * pg->cfg.grid));
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
     for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
     pg->device = device;
@@ -335,9 +362,14 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.targets = pg->d_targets.p;
     kp.det_ptr = pg->d_det_ptr.p;
     kp.det_terms = pg->d_det_terms.p;
-    kp.noise_p = pg->d_p.p;
-    kp.noise_log1m = pg->d_log1m.p;
-    kp.noise_k = pg->d_k.p;
+    kp.noise = pg->d_noise.p;
+    kp.noise_tab = pg->d_noise_tab.p;
+    kp.pregen_ops = pg->d_pregen.p;
+    kp.hits_global = pg->d_hits.p;
+    kp.hit_capacity = hp.hit_capacity;
+    kp.num_noise = (int32_t)hp.num_noise;
+    kp.num_pregen = (int32_t)hp.pregen_ops.size();
+    kp.pregen_chunks = (int32_t)hp.pregen_chunks;
     kp.coins = injected ? pg->d_coins.p : nullptr;
     kp.masks = injected ? pg->d_masks.p : nullptr;
     kp.inject_words = words_all;

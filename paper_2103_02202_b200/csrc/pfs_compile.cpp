@@ -63,12 +63,12 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     hp.num_coin_rows = num_coin_rows;
     hp.num_noise_rows = num_noise_rows;
     hp.noise_p.assign(noise_p, noise_p + n_noise);
-    hp.noise_log1m.resize(n_noise);
     hp.noise_apps.assign(n_noise, 0);
+    hp.noise_arity.assign(n_noise, 1);
+    hp.noise.assign(n_noise, NoiseParam{});
     for (int64_t i = 0; i < n_noise; i++) {
         double p = noise_p[i];
         if (!(p >= 0.0 && p <= 1.0)) bad("noise probability must be in [0, 1], got " + std::to_string(p));
-        hp.noise_log1m[i] = std::log1p(-p);
     }
 
     // ---- pass 1: validate and compute record liveness ----
@@ -111,6 +111,8 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
                 if (in.aux < 0 || in.aux >= n_noise) bad("noise ordinal out of range");
                 if (in.noise_row_base != nrow) bad("noise row numbering is not contiguous");
                 hp.noise_apps[in.aux] = (uint32_t)(in.n_targets / ar);
+                hp.noise_arity[in.aux] = (uint32_t)ar;
+                hp.noise[in.aux].npat = in.code == CH_DEP1 ? 3u : (in.code == CH_DEP2 ? 15u : 1u);
                 nrow += 2 * (int64_t)in.n_targets;
                 break;
             }
@@ -318,21 +320,90 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     return hp;
 }
 
-void assign_noise_chunks(HostProgram& hp, int tile_shots, double target_hits) {
-    hp.noise_k.assign(hp.num_noise, 1);
-    for (int64_t i = 0; i < hp.num_noise; i++) {
-        const int64_t A = hp.noise_apps[i];
-        const double p = hp.noise_p[i];
-        int64_t k;
-        if (A <= 0) k = 1;
-        else if (p <= 0.0) k = A;
-        else {
-            double x = target_hits / (p * (double)tile_shots);
-            k = x >= (double)A ? A : (int64_t)x;
-            if (k < 1) k = 1;
-            if (k > A) k = A;
+// Binomial(n, p) inverse-CDF thresholds in 64-bit fixed point:
+// X = min{m : u < t[m]} for u uniform on [0, 2^64), X = len(t) if u >= every
+// entry.  Upper-tail thresholds are built from the tail sum so their absolute
+// error stays ~2^-64.
+static std::vector<uint64_t> binomial_thresholds(uint64_t n, double p) {
+    std::vector<double> pmf;
+    const double q = 1.0 - p;
+    double pm = std::exp((double)n * std::log1p(-p));
+    const double mean = (double)n * p;
+    for (uint64_t m = 0;; m++) {
+        pmf.push_back(pm);
+        if (m == n) break;
+        if ((double)m > mean && pm < 1e-40) break;
+        pm = pm * ((double)(n - m) / (double)(m + 1)) * (p / q);
+    }
+    const size_t M = pmf.size();
+    std::vector<double> sf(M, 0.0);  // P(X > m)
+    for (size_t m = M - 1; m-- > 0;) sf[m] = sf[m + 1] + pmf[m + 1];
+    std::vector<uint64_t> t;
+    double cdf = 0.0;
+    for (size_t m = 0; m < M; m++) {
+        cdf += pmf[m];
+        const double tail = std::ldexp(sf[m], 64);
+        if (tail < 1.0) break;  // every remaining u lands on X = m
+        uint64_t v;
+        if (cdf <= 0.5) v = (uint64_t)std::floor(std::ldexp(cdf, 64));
+        else v = (uint64_t)0 - (uint64_t)std::ceil(tail);
+        t.push_back(v);
+    }
+    return t;
+}
+
+void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
+    hp.noise_tab.clear();
+    hp.pregen_ops.clear();
+    hp.pregen_chunks = 0;
+    hp.hit_capacity = 0;
+    for (int64_t j = 0; j < hp.num_noise; j++) {
+        NoiseParam& np = hp.noise[j];
+        const uint32_t npat = np.npat ? np.npat : 1u;
+        np = NoiseParam{};
+        np.npat = npat;
+        const uint64_t N = (uint64_t)hp.noise_apps[j] * (uint64_t)tile_shots;
+        const double p = hp.noise_p[j];
+        if (N == 0 || p <= 0.0) { np.flags = NZ_NONE; continue; }
+        if (N >= (1ull << 31)) bad("noise instruction too large for one tile");
+        uint64_t L;
+        if (p >= 1.0) {
+            np.flags = NZ_ALL;
+            L = std::min<uint64_t>(N, 1024);
+        } else {
+            double want = target_hits / p;
+            L = 1;
+            while ((double)(L * 2) <= want && L < (1ull << 30)) L *= 2;
+            if (L > N) L = N;
         }
-        hp.noise_k[i] = (int32_t)k;
+        np.L = (uint32_t)L;
+        np.nchunks = (uint32_t)((N + L - 1) / L);
+        np.last_len = (uint32_t)(N - (uint64_t)(np.nchunks - 1) * L);
+        if (!(np.flags & NZ_ALL)) {
+            auto tf = binomial_thresholds(L, p);
+            np.tab_full = (uint32_t)hp.noise_tab.size();
+            np.len_full = (uint32_t)tf.size();
+            hp.noise_tab.insert(hp.noise_tab.end(), tf.begin(), tf.end());
+            if (np.last_len != L) {
+                auto tl = binomial_thresholds(np.last_len, p);
+                np.tab_last = (uint32_t)hp.noise_tab.size();
+                np.len_last = (uint32_t)tl.size();
+                hp.noise_tab.insert(hp.noise_tab.end(), tl.begin(), tl.end());
+            } else {
+                np.tab_last = np.tab_full;
+                np.len_last = np.len_full;
+            }
+        }
+        const double E = (double)N * p;
+        if (p < 0.25 && E <= 16384.0 && N < (1ull << 28)) {
+            np.flags |= NZ_PREGEN;
+            np.cap = (uint32_t)std::ceil(E + 8.0 * std::sqrt(E) + 16.0);
+            np.cap_base = (uint32_t)hp.hit_capacity;
+            hp.hit_capacity += np.cap;
+            np.chunk_base = (uint32_t)hp.pregen_chunks;
+            hp.pregen_chunks += np.nchunks;
+            hp.pregen_ops.push_back((uint32_t)j);
+        }
     }
 }
 

@@ -1,6 +1,8 @@
 // Internal declarations shared by the host compiler (pfs_compile.cpp), the
 // kernels (pfs_kernels.cu) and the C-ABI (pfs_api.cu).
 #pragma once
+#include <cuda_runtime.h>
+
 #include <cstdint>
 #include <string>
 #include <vector>
@@ -16,11 +18,17 @@ enum Channel : uint32_t { CH_XERR = 0, CH_YERR = 1, CH_ZERR = 2, CH_DEP1 = 3, CH
 
 // Device op flags
 constexpr uint32_t F_BARRIER = 1u;   // __syncthreads() before this op
-constexpr uint32_t F_DUP = 2u;       // noise op with repeated targets: atomic XOR
+constexpr uint32_t F_DUP = 2u;       // noise op with repeated targets
 constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
 
 constexpr uint32_t DOMAIN_COIN = 0x40000000u;
 constexpr uint32_t DOMAIN_NOISE = 0x80000000u;
+
+// Noise schedule flags
+constexpr uint32_t NZ_NONE = 1u;     // p == 0: no hits
+constexpr uint32_t NZ_ALL = 2u;      // p == 1: every trial hits
+constexpr uint32_t NZ_PREGEN = 4u;   // hits generated in the tile's pre-pass into a hit list
+constexpr int NZ_MAX_LIST = 16;      // distinct-position list; larger counts use selection sampling
 
 // One device op (32 bytes).  See DESIGN.md §3.
 //   GATE : count = apps, off -> targets (1 or 2 per app)
@@ -41,6 +49,26 @@ struct DOp {
 };
 static_assert(sizeof(DOp) == 32, "DOp is 32 bytes");
 
+// Per noise instruction sampling schedule for one tile: the
+// op's trial space (apps x T shots, app-major) is cut into chunks of L trials;
+// each chunk draws Binomial(len, p) hits by table inversion, then distinct
+// uniform positions, then a uniform Pauli pattern per hit.
+struct NoiseParam {
+    uint32_t L;          // trials per chunk
+    uint32_t nchunks;
+    uint32_t last_len;   // trials in the last chunk
+    uint32_t tab_full;   // offset of the Binomial(L, p) threshold table
+    uint32_t len_full;
+    uint32_t tab_last;   // Binomial(last_len, p) table
+    uint32_t len_last;
+    uint32_t cap_base;   // hit-list region of this op in the per-CTA scratch
+    uint32_t cap;
+    uint32_t flags;
+    uint32_t npat;
+    uint32_t chunk_base; // prefix over pre-generated ops (pre-pass work index)
+};
+static_assert(sizeof(NoiseParam) == 48, "NoiseParam is 48 bytes");
+
 struct HostProgram {
     int32_t num_qubits = 0;
     int64_t num_meas = 0;
@@ -57,9 +85,14 @@ struct HostProgram {
     std::vector<uint32_t> det_ptr;    // [num_cols + 1] into det_terms
     std::vector<uint32_t> det_terms;  // slots
     std::vector<double> noise_p;
-    std::vector<double> noise_log1m;
-    std::vector<int32_t> noise_k;     // filled once T is known
     std::vector<uint32_t> noise_apps; // apps per noise ordinal
+    std::vector<uint32_t> noise_arity;
+    // filled by build_noise_schedule once T is known
+    std::vector<NoiseParam> noise;
+    std::vector<uint64_t> noise_tab;
+    std::vector<uint32_t> pregen_ops;   // noise ordinals with NZ_PREGEN, in order
+    int64_t pregen_chunks = 0;          // total pre-pass chunks per tile
+    int64_t hit_capacity = 0;           // hit-list entries per CTA
 };
 
 // Host compiler: flat program -> device ops (splitting, merging, record-slot
@@ -70,7 +103,7 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
                             int64_t n_obs, int32_t num_qubits, int64_t num_meas,
                             int64_t num_coin_rows, int64_t num_noise_rows);
 
-void assign_noise_chunks(HostProgram& hp, int tile_shots, double target_hits);
+void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits);
 
 // Kernel launch plumbing (pfs_kernels.cu)
 struct KParams {
@@ -78,19 +111,21 @@ struct KParams {
     const uint32_t* targets;
     const uint32_t* det_ptr;
     const uint32_t* det_terms;
-    const double* noise_p;
-    const double* noise_log1m;
-    const int32_t* noise_k;
+    const NoiseParam* noise;
+    const uint64_t* noise_tab;
+    const uint32_t* pregen_ops;
     const uint32_t* coins;       // injected: [rows][inject_words]
     const uint32_t* masks;
     uint32_t* rec_out;           // [M][out_words] (flips rows) or null
     uint32_t* ev_out;            // [cols][out_words] or null
     unsigned long long* counts;  // [cols] or null
     uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
+    uint32_t* hits_global;       // [grid][hit_capacity] pre-generated noise hits
     int64_t inject_words;
     int64_t out_words;
     int64_t n_tiles;
     int64_t num_shots;           // shots of this launch (for tail masking)
+    int64_t hit_capacity;
     uint64_t seed;
     uint64_t tile_offset;        // global index of local tile 0
     int32_t n_ops;
@@ -98,6 +133,9 @@ struct KParams {
     int32_t num_slots;
     int32_t num_obs;
     int32_t num_cols;
+    int32_t num_noise;
+    int32_t num_pregen;
+    int32_t pregen_chunks;
     int32_t counts_in_smem;
     int32_t do_dets;             // evaluate DET/OBS ops
 };
@@ -116,5 +154,6 @@ cudaError_t set_frame_kernel_smem(const LaunchCfg& cfg);
 cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t row_words,
                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
                               int64_t pitch, cudaStream_t stream);
+cudaError_t smem_probe(int device, double* gbs);
 
 }  // namespace pfs

@@ -107,11 +107,96 @@ __device__ __forceinline__ void pattern_of(uint32_t ch, uint32_t pick, uint32_t&
     }
 }
 
+// Stream of 32-bit Philox words for one noise chunk: call j of chunk r in
+// global tile g of noise instruction `ordinal`.
+struct WordStream {
+    uint32_t r, g, dom, k0, k1, j;
+    uint32_t buf[4];
+    int idx;
+    __device__ __forceinline__ WordStream(uint32_t r_, uint32_t g_, uint32_t ordinal, uint64_t seed)
+        : r(r_), g(g_), dom(DOMAIN_NOISE | ordinal), k0((uint32_t)seed), k1((uint32_t)(seed >> 32)),
+          j(0), idx(4) {}
+    __device__ __forceinline__ uint32_t next() {
+        if (idx == 4) {
+            uint32_t c0 = j++, c1 = r, c2 = g, c3 = dom;
+            philox4x32_10(c0, c1, c2, c3, k0, k1);
+            buf[0] = c0; buf[1] = c1; buf[2] = c2; buf[3] = c3;
+            idx = 0;
+        }
+        return buf[idx++];
+    }
+    __device__ __forceinline__ uint64_t next64() {
+        const uint32_t lo = next();
+        return ((uint64_t)next() << 32) | lo;
+    }
+};
+
+// Hits of one chunk: Binomial(len, p) count by threshold inversion, then
+// distinct uniform positions (selection sampling past NZ_MAX_LIST), each with
+// a uniform Pauli pattern pick.  emit(trial index within the op, pick).
+template <typename Emit>
+__device__ __forceinline__ void noise_chunk(const KParams& kp, const NoiseParam& np, uint32_t ordinal,
+                                            uint32_t r, uint32_t g, Emit emit) {
+    const uint32_t len = (r + 1 == np.nchunks) ? np.last_len : np.L;
+    const uint32_t base = r * np.L;
+    WordStream ws(r, g, ordinal, kp.seed);
+    if (np.flags & NZ_ALL) {
+        for (uint32_t i = 0; i < len; i++) emit(base + i, np.npat > 1 ? __umulhi(ws.next(), np.npat) : 0u);
+        return;
+    }
+    const bool full = len == np.L;
+    const uint64_t* tab = kp.noise_tab + (full ? np.tab_full : np.tab_last);
+    const uint32_t tlen = full ? np.len_full : np.len_last;
+    const uint64_t u = ws.next64();
+    uint32_t count = 0;
+    while (count < tlen && u >= __ldg(reinterpret_cast<const unsigned long long*>(tab) + count)) count++;
+    if (count == 0) return;
+    if (count <= NZ_MAX_LIST) {
+        uint32_t sel[NZ_MAX_LIST];
+        for (uint32_t h = 0; h < count; h++) {
+            uint32_t pos;
+            bool dup;
+            do {
+                pos = (uint32_t)__umul64hi(ws.next64(), (uint64_t)len);
+                dup = false;
+                for (uint32_t q = 0; q < h; q++) dup |= sel[q] == pos;
+            } while (dup);
+            sel[h] = pos;
+            emit(base + pos, np.npat > 1 ? __umulhi(ws.next(), np.npat) : 0u);
+        }
+    } else {
+        uint32_t needed = count;
+        for (uint32_t i = 0; needed > 0; i++) {
+            if (__umul64hi(ws.next64(), (uint64_t)(len - i)) < needed) {
+                emit(base + i, np.npat > 1 ? __umulhi(ws.next(), np.npat) : 0u);
+                needed--;
+            }
+        }
+    }
+}
+
 template <int C> struct Log2;
 template <> struct Log2<1> { static constexpr int v = 0; };
 template <> struct Log2<2> { static constexpr int v = 1; };
 template <> struct Log2<4> { static constexpr int v = 2; };
 template <> struct Log2<8> { static constexpr int v = 3; };
+
+// XOR one sampled Pauli (pattern pick) into the frame of app `app`, shot s.
+template <int W>
+__device__ __forceinline__ void apply_hit(uint32_t* X, uint32_t* Z, const uint32_t* tg, uint32_t ch,
+                                          int ar, uint32_t trial, uint32_t pick) {
+    constexpr uint32_t T = 32 * W;
+    const uint32_t app = trial / T, s = trial % T;
+    uint32_t xm, zm;
+    pattern_of(ch, pick, xm, zm);
+    const uint32_t bit = 1u << (s & 31);
+    const uint32_t w = s >> 5;
+    for (int sl = 0; sl < ar; sl++) {
+        const size_t row = (size_t)__ldg(tg + app * ar + sl) * W + w;
+        if ((xm >> sl) & 1u) atomicXor(X + row, bit);
+        if ((zm >> sl) & 1u) atomicXor(Z + row, bit);
+    }
+}
 
 // ------------------------------------------------------------ frame kernel
 template <int W, bool RING_SMEM>
@@ -126,9 +211,10 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
     uint32_t* const ring = RING_SMEM ? (smem + (size_t)2 * n * W)
                                      : (kp.ring_global + (size_t)blockIdx.x * kp.num_slots * W);
     uint32_t* const cnt = smem + (size_t)2 * n * W + (RING_SMEM ? (size_t)kp.num_slots * W : 0);
+    uint32_t* const ncnt = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // hits per noise op
+    uint32_t* const hits = kp.hits_global + (size_t)blockIdx.x * kp.hit_capacity;
     const int tid = threadIdx.x;
     const int nth = blockDim.x;
-    const uint32_t key0 = (uint32_t)kp.seed, key1 = (uint32_t)(kp.seed >> 32);
 
     if (kp.counts_in_smem) {
         for (int i = tid; i < kp.num_cols; i += nth) cnt[i] = 0u;
@@ -146,13 +232,50 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
             const int k = i >> LC, c = i & (C - 1);
             vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
         }
+        // ---- noise pre-pass: sample every pre-generated noise op of this tile
+        // into per-op hit lists (no frame access, no barriers inside) ----
+        if (kp.masks == nullptr && kp.num_pregen > 0) {
+            for (int i = tid; i < kp.num_noise; i += nth) ncnt[i] = 0u;
+            __syncthreads();
+            const int total = kp.pregen_chunks;
+            const int per = (total + nth - 1) / nth;
+            int c0 = tid * per;
+            const int c1 = min(total, c0 + per);
+            if (c0 < c1) {
+                int lo = 0, hi = kp.num_pregen - 1;  // last op with chunk_base <= c0
+                while (lo < hi) {
+                    const int mid = (lo + hi + 1) >> 1;
+                    if ((int)__ldg(&kp.noise[__ldg(kp.pregen_ops + mid)].chunk_base) <= c0) lo = mid;
+                    else hi = mid - 1;
+                }
+                int k = lo;
+                while (c0 < c1) {
+                    const uint32_t ord = __ldg(kp.pregen_ops + k);
+                    const NoiseParam np = kp.noise[ord];
+                    const int end = min(c1, (int)(np.chunk_base + np.nchunks));
+                    for (; c0 < end; c0++) {
+                        noise_chunk(kp, np, ord, (uint32_t)(c0 - np.chunk_base), g,
+                                    [&](uint32_t trial, uint32_t pick) {
+                                        const uint32_t slot = atomicAdd(ncnt + ord, 1u);
+                                        if (slot < np.cap) hits[np.cap_base + slot] = (trial << 4) | pick;
+                                    });
+                    }
+                    k++;
+                }
+            }
+        }
         __syncthreads();
 
+        uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
+        uint4 h1 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops) + 1) : make_uint4(0, 0, 0, 0);
         for (int oi = 0; oi < kp.n_ops; oi++) {
-            const uint4 h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi));
-            const uint4 h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi) + 1);
             const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
             const uint32_t count = h0.y, off = h0.z, oa = h0.w, ob = h1.x;
+            // prefetch the next op descriptor while this one runs
+            if (oi + 1 < kp.n_ops) {
+                h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
+                h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1) + 1);
+            }
             if (flags & F_BARRIER) __syncthreads();
             const uint32_t* tg = kp.targets + off;
             switch (kind) {
@@ -255,45 +378,20 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
                     }
                     break;
                 }
-                const double prob = __ldg(kp.noise_p + ob);
-                if (!(prob > 0.0)) break;
-                const double log1m = __ldg(kp.noise_log1m + ob);
-                const int64_t k = __ldg(kp.noise_k + ob);
-                const int64_t A = count;
-                const int64_t n_chunks = (A + k - 1) / k;
-                const uint32_t npat = code == CH_DEP1 ? 3u : (code == CH_DEP2 ? 15u : 1u);
-                constexpr int64_t T = 32 * W;
-                for (int64_t r = tid; r < n_chunks; r += nth) {
-                    const int64_t a0 = r * k;
-                    const int64_t apps = (A - a0) < k ? (A - a0) : k;
-                    const int64_t len = apps * T;
-                    int64_t pos = -1;
-                    for (uint32_t j = 0;; j++) {
-                        uint32_t c0 = j, c1 = (uint32_t)r, c2 = g, c3 = DOMAIN_NOISE | ob;
-                        philox4x32_10(c0, c1, c2, c3, key0, key1);
-                        const uint64_t m53 = ((uint64_t)c0 << 21) | (c1 >> 11);
-                        const double u = (double)(m53 + 1ull) * 0x1.0p-53;
-                        const double gap = prob >= 1.0 ? 0.0 : floor(log(u) / log1m);
-                        if (gap >= (double)(len - 1 - pos)) break;
-                        pos += (int64_t)gap + 1;
-                        const uint32_t pick = (uint32_t)(((uint64_t)c2 * npat) >> 32);
-                        uint32_t xm, zm;
-                        pattern_of(code, pick, xm, zm);
-                        const int64_t app = a0 + pos / T;
-                        const int s = (int)(pos % T);
-                        const uint32_t bit = 1u << (s & 31);
-                        const int w = s >> 5;
-                        for (int sl = 0; sl < ar; sl++) {
-                            const size_t qrow = (size_t)__ldg(tg + app * ar + sl) * W + w;
-                            if (flags & F_DUP) {
-                                if ((xm >> sl) & 1u) atomicXor(X + qrow, bit);
-                                if ((zm >> sl) & 1u) atomicXor(Z + qrow, bit);
-                            } else {
-                                if ((xm >> sl) & 1u) X[qrow] ^= bit;
-                                if ((zm >> sl) & 1u) Z[qrow] ^= bit;
-                            }
-                        }
+                const NoiseParam np = kp.noise[ob];
+                if (np.flags & NZ_NONE) break;
+                if ((np.flags & NZ_PREGEN) && ncnt[ob] <= np.cap) {
+                    const uint32_t nh = ncnt[ob];
+                    for (uint32_t i = tid; i < nh; i += nth) {
+                        const uint32_t e = hits[np.cap_base + i];
+                        apply_hit<W>(X, Z, tg, code, ar, e >> 4, e & 15u);
                     }
+                } else {
+                    // inline sampling (large-p ops, or a pre-pass list overflow)
+                    for (uint32_t r = tid; r < np.nchunks; r += nth)
+                        noise_chunk(kp, np, ob, r, g, [&](uint32_t trial, uint32_t pick) {
+                            apply_hit<W>(X, Z, tg, code, ar, trial, pick);
+                        });
                 }
                 break;
             }
@@ -448,17 +546,84 @@ __global__ void __launch_bounds__(256) rows_to_b8_kernel(const uint32_t* __restr
     const int64_t b0 = r0 >> 3;
     const int64_t span = (nbytes - b0) < 32 ? (nbytes - b0) : 32;
     const bool full = (pitch & 15) == 0 && ((uintptr_t)out & 15) == 0 && b0 + 32 <= pitch;
-    for (int sl = t; sl < TR_WORDS * 32; sl += 256) {
-        const int64_t s = w0 * 32 + sl;
-        if (s >= num_shots) break;
-        uint8_t* dst = out + s * pitch + b0;
-        if (full) {
-            reinterpret_cast<uint4*>(dst)[0] = make_uint4(tout[sl][0], tout[sl][1], tout[sl][2], tout[sl][3]);
-            reinterpret_cast<uint4*>(dst)[1] = make_uint4(tout[sl][4], tout[sl][5], tout[sl][6], tout[sl][7]);
-        } else {
-            for (int b = 0; b < span; b++) dst[b] = (uint8_t)(tout[sl][b >> 2] >> ((b & 3) * 8));
+    if (full) {
+        for (int sl = t; sl < TR_WORDS * 32; sl += 256) {
+            const int64_t s = w0 * 32 + sl;
+            if (s >= num_shots) break;
+            uint4* dst = reinterpret_cast<uint4*>(out + s * pitch + b0);
+            dst[0] = make_uint4(tout[sl][0], tout[sl][1], tout[sl][2], tout[sl][3]);
+            dst[1] = make_uint4(tout[sl][4], tout[sl][5], tout[sl][6], tout[sl][7]);
+        }
+    } else {
+        // unaligned pitch (exact b8 rows): one warp per shot row, one byte per
+        // lane, so each store instruction writes one contiguous 32-byte run
+        for (int sl = warp; sl < TR_WORDS * 32; sl += 8) {
+            const int64_t s = w0 * 32 + sl;
+            if (s >= num_shots) break;
+            if (lane < span)
+                out[s * pitch + b0 + lane] = (uint8_t)(tout[sl][lane >> 2] >> ((lane & 3) * 8));
         }
     }
+}
+
+// ------------------------------------------------------------ SMEM roofline probe
+// Every thread streams LDS.128 x4 + STS.128 x2 per iteration over a 64 KB
+// buffer with conflict-free addressing (the CX access mix); bytes moved =
+// (loads + stores) x 16 B.
+__global__ void __launch_bounds__(1024) smem_probe_kernel(int iters, uint32_t* sink) {
+    extern __shared__ __align__(16) uint4 sbuf[];
+    const int n = 4096;  // 64 KB of uint4
+    const int t = threadIdx.x;
+    for (int i = t; i < n; i += blockDim.x) sbuf[i] = make_uint4(i, i * 3, i * 5, i * 7);
+    __syncthreads();
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    int base = t;
+    for (int it = 0; it < iters; it++) {
+        const int a0 = (base) & (n - 1), a1 = (base + 1024) & (n - 1);
+        const int a2 = (base + 2048) & (n - 1), a3 = (base + 3072) & (n - 1);
+        uint4 x0 = sbuf[a0], x1 = sbuf[a1], z0 = sbuf[a2], z1 = sbuf[a3];
+        x1.x ^= x0.x; x1.y ^= x0.y; x1.z ^= x0.z; x1.w ^= x0.w;
+        z0.x ^= z1.x; z0.y ^= z1.y; z0.z ^= z1.z; z0.w ^= z1.w;
+        sbuf[a1] = x1;
+        sbuf[a2] = z0;
+        acc.x ^= x1.x; acc.y ^= z0.y;
+        base += blockDim.x;
+    }
+    if ((acc.x ^ acc.y) == 0x12345678u) sink[0] = acc.x;
+}
+
+cudaError_t smem_probe(int device, double* gbs) {
+    cudaError_t e = cudaSetDevice(device);
+    if (e != cudaSuccess) return e;
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+    uint32_t* sink = nullptr;
+    if ((e = cudaMalloc(&sink, 4)) != cudaSuccess) return e;
+    const int threads = 1024, iters = 4096;
+    const int grid = sms * 2;
+    const size_t sm = 64 * 1024;
+    cudaFuncSetAttribute(smem_probe_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    smem_probe_kernel<<<grid, threads, sm>>>(iters, sink);  // warm-up
+    float best = 1e30f;
+    for (int r = 0; r < 5; r++) {
+        cudaEventRecord(a);
+        smem_probe_kernel<<<grid, threads, sm>>>(iters, sink);
+        cudaEventRecord(b);
+        cudaEventSynchronize(b);
+        float ms = 0;
+        cudaEventElapsedTime(&ms, a, b);
+        best = ms < best ? ms : best;
+    }
+    e = cudaGetLastError();
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+    cudaFree(sink);
+    const double bytes = (double)grid * threads * iters * 6.0 * 16.0;
+    *gbs = bytes / (best * 1e-3) / 1e9;
+    return e;
 }
 
 cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t row_words,

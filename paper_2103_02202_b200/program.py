@@ -160,30 +160,3 @@ def flatten(circuit) -> FlatProgram:
         targets=np.array(targets, dtype=np.int32), noise_p=np.array(noise_p, dtype=np.float64),
         det_ptr=ptr, det_idx=idx, num_coin_rows=state["coin"], num_noise_rows=state["nrow"],
         bframe_bits=state["bits"])
-
-
-def noise_chunk_apps(p: float, tile_shots: int, n_apps: int, target_hits: float = 1.0) -> int:
-    """Applications per geometric-walk chunk (the RNG work unit).
-
-    A chunk is k consecutive applications x the tile's shots, walked with
-    geometric gaps exactly like `sample_hits_geometric` (entropy.py:65-88)
-    walks one instruction x batch; k is chosen so a chunk expects about
-    `target_hits` hits.
-    """
-    if n_apps <= 0:
-        return 1
-    if p <= 0.0:
-        return n_apps
-    k = int(target_hits / (p * tile_shots))
-    return max(1, min(n_apps, k))
-
-
-def noise_chunks(prog: FlatProgram, tile_shots: int) -> np.ndarray:
-    """int32 [num_noise] apps-per-chunk for every noise instruction."""
-    out = np.ones(prog.num_noise, dtype=np.int32)
-    sel = prog.instrs[:, 0] == K_NOISE
-    for row in prog.instrs[sel]:
-        n_apps = int(row[2]) // CHANNEL_ARITY[int(row[1])]
-        out[int(row[7])] = noise_chunk_apps(float(prog.noise_p[int(row[7])]), tile_shots,
-                                            n_apps)
-    return out

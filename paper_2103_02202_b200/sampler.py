@@ -23,9 +23,15 @@ from .program import flatten
 
 
 def _nbytes(a) -> int:
-    if hasattr(a, "nbytes") and not hasattr(a, "data_ptr"):
-        return int(a.nbytes)
-    return int(a.numel() * a.element_size())
+    """Bytes spanned by a (possibly row-strided) numpy array or torch tensor."""
+    if hasattr(a, "data_ptr"):
+        es = a.element_size()
+        if a.dim() == 2 and a.numel():
+            return int(((a.size(0) - 1) * a.stride(0) + a.size(1)) * es)
+        return int(a.numel() * es)
+    if a.ndim == 2 and a.size:
+        return int((a.shape[0] - 1) * a.strides[0] + a.shape[1] * a.itemsize)
+    return int(a.nbytes)
 
 
 def pinned_empty(shape, dtype=np.uint8):

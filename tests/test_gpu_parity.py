@@ -91,7 +91,7 @@ def test_philox_bit_exact_vs_oracle(oracle_lib, case, layout):
     ms = compile_sampler(text, words_per_tile=W, ring_in_smem=ring)
     fl_rows = ms.sample_flip_rows(shots, seed=seed, shot_offset=offset)
     ofl, oev = oracle_lib.sample(ds.flat, shots, T, seed=seed, tile_offset=offset // T,
-                                 nthreads=4, noise_k=ds.native.noise_chunks())
+                                 nthreads=4, schedule=ds.native.noise_schedule())
     assert np.array_equal(rows_unpack(ev_rows, shots), rows_unpack(oev, shots))
     assert np.array_equal(rows_unpack(fl_rows, shots), rows_unpack(ofl, shots))
     # b8 outputs are the transposes of the row outputs

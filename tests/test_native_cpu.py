@@ -10,7 +10,7 @@ import pytest
 
 from paper_2103_02202_b200 import _native as N
 from paper_2103_02202_b200 import generators as gen
-from paper_2103_02202_b200.program import flatten, noise_chunks
+from paper_2103_02202_b200.program import flatten
 
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
@@ -41,7 +41,13 @@ def test_program_info_matches_survey_counts(cfg):
     assert info["num_measurements"] == f.num_measurements
     assert info["num_columns"] == f.num_columns
     assert info["tile_shots"] == 32 * info["words_per_tile"]
-    assert np.array_equal(p.noise_chunks(), noise_chunks(f, p.tile_shots))
+    params, tab = p.noise_schedule()
+    assert params.shape == (f.num_noise, 12)
+    # every table is non-decreasing (inverse-CDF thresholds)
+    for row in params:
+        for off, ln in ((row[3], row[4]), (row[5], row[6])):
+            t = tab[off:off + ln]
+            assert np.all(t[1:] >= t[:-1])
 
 
 def test_d25_layout():
@@ -52,6 +58,20 @@ def test_d25_layout():
     for W in (1, 2, 4, 8, 16):
         q = N.NativeProgram(f, words_per_tile=W, ring_in_smem=0)
         assert q.info["tile_shots"] == 32 * W and q.info["ring_in_smem"] == 0
+
+
+def test_binomial_thresholds_match_scipy():
+    """The noise count table is the Binomial(L, p) inverse CDF in 2^-64 units."""
+    from scipy.stats import binom
+
+    f = flatten("X_ERROR(0.001) " + " ".join(map(str, range(64))) + "\n")
+    p = N.NativeProgram(f, words_per_tile=8, ring_in_smem=0)
+    params, tab = p.noise_schedule()
+    L, nch, last, tf, lf = (int(v) for v in params[0, :5])
+    assert L * (nch - 1) + last == 64 * 256
+    cdf = binom.cdf(np.arange(lf), L, 0.001)
+    got = tab[tf:tf + lf].astype(np.float64) / 2.0 ** 64
+    assert np.allclose(got, cdf, rtol=1e-9, atol=1e-15)
 
 
 def test_conflicting_instruction_is_split():
