@@ -46,7 +46,11 @@ typedef struct pfs_options {
     int32_t ctas_per_sm;      /* persistent grid = SMs x this (0 = auto)            */
     double noise_target_hits; /* expected hits per geometric-walk chunk (0 = 1.0)   */
     int32_t timing;           /* 1: record per-kernel CUDA-event times in pfs_run  */
-    int32_t reserved[7];
+    int32_t debug_skip;       /* profiling ablations only (wrong results!): bit0 noise
+                                 apply, bit1 noise pre-pass, bit2 coin RNG, bit3 detectors,
+                                 bit4 gates, bit5 collapses */
+    int32_t producer_threads; /* threads sampling the next tile's noise (0 = auto)   */
+    int32_t reserved[5];
 } pfs_options;
 
 typedef struct pfs_info {

@@ -62,7 +62,8 @@ struct pfs_program {
     DevBuf<uint32_t> d_targets, d_det_ptr, d_det_terms, d_ring;
     DevBuf<NoiseParam> d_noise;
     DevBuf<uint64_t> d_noise_tab;
-    DevBuf<uint32_t> d_pregen, d_hits;
+    DevBuf<uint32_t> d_pregen, d_noise_off, d_noise_ch;
+    DevBuf<uint64_t> d_hits;
     DevBuf<uint32_t> d_rows[2];
     DevBuf<uint8_t> d_b8[2];
     DevBuf<uint32_t> d_coins, d_masks;
@@ -74,7 +75,7 @@ struct pfs_program {
     int64_t last_launches = 0;
 };
 
-static size_t fixed_smem(const HostProgram& hp) { return (size_t)hp.num_noise * 4; }
+static size_t fixed_smem(const HostProgram& hp) { return (size_t)hp.num_noise * 8; }
 
 static void choose_layout(pfs_program* pg) {
     const HostProgram& hp = pg->hp;
@@ -98,7 +99,7 @@ static void choose_layout(pfs_program* pg) {
         W = Ws; rs = true;
     } else if (o.ring_in_smem == 0) {
         W = Wg; rs = false;
-    } else if (Ws > 0 && Ws >= std::min(Wg, 8)) {
+    } else if (Ws > 0 && Ws >= Wg) {
         W = Ws; rs = true;
     } else {
         W = Wg; rs = false;
@@ -219,6 +220,7 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_ops.release(); pg->d_targets.release(); pg->d_det_ptr.release();
         pg->d_det_terms.release(); pg->d_ring.release(); pg->d_noise.release();
         pg->d_noise_tab.release(); pg->d_pregen.release(); pg->d_hits.release();
+        pg->d_noise_off.release(); pg->d_noise_ch.release();
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
@@ -260,6 +262,8 @@ static int ensure_device(pfs_program* pg, int device) {
     CUDA_TRY(upload(pg->d_noise, hp.noise));
     CUDA_TRY(upload(pg->d_noise_tab, hp.noise_tab));
     CUDA_TRY(upload(pg->d_pregen, hp.pregen_ops));
+    CUDA_TRY(upload(pg->d_noise_off, hp.noise_off));
+    CUDA_TRY(upload(pg->d_noise_ch, hp.noise_ch));
     CUDA_TRY(set_frame_kernel_smem(pg->cfg));
     int per_sm = pg->opts.ctas_per_sm;
     if (per_sm <= 0) {
@@ -268,7 +272,7 @@ static int ensure_device(pfs_program* pg, int device) {
         per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / pg->cfg.threads));
     }
     pg->cfg.grid = pg->num_sms * per_sm;
-    CUDA_TRY(pg->d_hits.reserve((size_t)std::max<int64_t>(hp.hit_capacity, 1) * pg->cfg.grid));
+    CUDA_TRY(pg->d_hits.reserve((size_t)std::max<int64_t>(hp.hit_capacity, 1) * 2 * pg->cfg.grid));
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
     for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
     pg->device = device;
@@ -370,6 +374,12 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.num_noise = (int32_t)hp.num_noise;
     kp.num_pregen = (int32_t)hp.pregen_ops.size();
     kp.pregen_chunks = (int32_t)hp.pregen_chunks;
+    kp.noise_off = pg->d_noise_off.p;
+    kp.noise_ch = pg->d_noise_ch.p;
+    kp.first_pregen = hp.first_pregen;
+    kp.first_cap_base = hp.first_cap_base;
+    kp.producers = hp.pregen_ops.empty() ? 0 : (pg->opts.producer_threads > 0 ? pg->opts.producer_threads : 256);
+    if (kp.producers >= pg->cfg.threads) kp.producers = pg->cfg.threads / 4;
     kp.coins = injected ? pg->d_coins.p : nullptr;
     kp.masks = injected ? pg->d_masks.p : nullptr;
     kp.inject_words = words_all;
@@ -380,6 +390,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.num_obs = (int32_t)hp.num_obs;
     kp.num_cols = (int32_t)hp.num_cols;
     kp.do_dets = rows_meas ? 0 : 1;
+    kp.debug_skip = pg->opts.debug_skip;
 
     LaunchCfg cfg = pg->cfg;
     if (!cfg.ring_smem) {

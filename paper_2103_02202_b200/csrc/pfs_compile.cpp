@@ -65,6 +65,8 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     hp.noise_p.assign(noise_p, noise_p + n_noise);
     hp.noise_apps.assign(n_noise, 0);
     hp.noise_arity.assign(n_noise, 1);
+    hp.noise_off.assign(n_noise, 0);
+    hp.noise_ch.assign(n_noise, 0);
     hp.noise.assign(n_noise, NoiseParam{});
     for (int64_t i = 0; i < n_noise; i++) {
         double p = noise_p[i];
@@ -224,6 +226,8 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
             o.count = (uint32_t)(in.n_targets / ar);
             o.a = (uint32_t)in.noise_row_base;
             o.b = (uint32_t)in.aux;
+            hp.noise_off[in.aux] = o.off;
+            hp.noise_ch[in.aux] = (uint32_t)in.code;
             bool dup = false;
             for (int j = 0; j < in.n_targets; j++) {
                 if (stamp[tg[j]] == cur) dup = true;
@@ -404,6 +408,27 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
             hp.pregen_chunks += np.nchunks;
             hp.pregen_ops.push_back((uint32_t)j);
         }
+    }
+    // noise ops learn their hit-list base and the next pre-generated op, so
+    // consumer threads can prefetch the next op's hits while other ops run
+    std::vector<uint32_t> next_of(hp.num_noise, NO_SLOT);
+    for (size_t k = 0; k + 1 < hp.pregen_ops.size(); k++) next_of[hp.pregen_ops[k]] = hp.pregen_ops[k + 1];
+    hp.first_pregen = hp.pregen_ops.empty() ? NO_SLOT : hp.pregen_ops[0];
+    hp.first_cap_base = hp.pregen_ops.empty() ? 0 : hp.noise[hp.pregen_ops[0]].cap_base;
+    for (DOp& o : hp.ops) {
+        if ((o.kcf & 0xFF) != K_NOISE) continue;
+        const NoiseParam& np = hp.noise[o.b];
+        o.kcf &= ~(F_PREGEN << 16);
+        if (np.flags & NZ_PREGEN) o.kcf |= F_PREGEN << 16;
+        o.c = np.cap_base;
+        // the next pre-generated op after this one in program order
+        uint32_t nx = NO_SLOT;
+        if (np.flags & NZ_PREGEN) nx = next_of[o.b];
+        else {
+            for (uint32_t q : hp.pregen_ops) if (q > o.b) { nx = q; break; }
+        }
+        o.d = nx;
+        o.e = nx == NO_SLOT ? 0u : hp.noise[nx].cap_base;
     }
 }
 

@@ -19,6 +19,7 @@ enum Channel : uint32_t { CH_XERR = 0, CH_YERR = 1, CH_ZERR = 2, CH_DEP1 = 3, CH
 // Device op flags
 constexpr uint32_t F_BARRIER = 1u;   // __syncthreads() before this op
 constexpr uint32_t F_DUP = 2u;       // noise op with repeated targets
+constexpr uint32_t F_PREGEN = 4u;    // noise op whose hits come from the producer warps
 constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
 
 constexpr uint32_t DOMAIN_COIN = 0x40000000u;
@@ -34,7 +35,9 @@ constexpr int NZ_MAX_LIST = 16;      // distinct-position list; larger counts us
 //   GATE : count = apps, off -> targets (1 or 2 per app)
 //   M/MR : count = targets, off -> (qubit, slot) pairs, a = rec_base, b = coin_base
 //   R    : count = targets, off -> qubits, b = coin_base
-//   NOISE: count = apps, off -> targets, a = noise_row_base, b = noise ordinal
+//   NOISE: count = apps, off -> targets, a = noise_row_base, b = noise ordinal,
+//          c = hit-list base, d = next pre-generated ordinal (NO_SLOT: none),
+//          e = that op's hit-list base (consumers prefetch its first hits)
 //   DET  : count = columns, a = first column (terms via det_ptr/det_terms)
 //   OBS  : count = terms, off -> record slots, a = accumulator slot
 struct DOp {
@@ -87,12 +90,16 @@ struct HostProgram {
     std::vector<double> noise_p;
     std::vector<uint32_t> noise_apps; // apps per noise ordinal
     std::vector<uint32_t> noise_arity;
+    std::vector<uint32_t> noise_off;  // per ordinal: device target offset
+    std::vector<uint32_t> noise_ch;   // per ordinal: channel
     // filled by build_noise_schedule once T is known
     std::vector<NoiseParam> noise;
     std::vector<uint64_t> noise_tab;
     std::vector<uint32_t> pregen_ops;   // noise ordinals with NZ_PREGEN, in order
     int64_t pregen_chunks = 0;          // total pre-pass chunks per tile
-    int64_t hit_capacity = 0;           // hit-list entries per CTA
+    int64_t hit_capacity = 0;           // hit-list entries per CTA (per buffer)
+    uint32_t first_pregen = NO_SLOT;
+    uint32_t first_cap_base = 0;
 };
 
 // Host compiler: flat program -> device ops (splitting, merging, record-slot
@@ -114,13 +121,15 @@ struct KParams {
     const NoiseParam* noise;
     const uint64_t* noise_tab;
     const uint32_t* pregen_ops;
+    const uint32_t* noise_off;   // per noise ordinal: offset of its targets
+    const uint32_t* noise_ch;    // per noise ordinal: channel
     const uint32_t* coins;       // injected: [rows][inject_words]
     const uint32_t* masks;
     uint32_t* rec_out;           // [M][out_words] (flips rows) or null
     uint32_t* ev_out;            // [cols][out_words] or null
     unsigned long long* counts;  // [cols] or null
     uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
-    uint32_t* hits_global;       // [grid][hit_capacity] pre-generated noise hits
+    uint64_t* hits_global;       // [grid][2][hit_capacity] pre-generated noise hits
     int64_t inject_words;
     int64_t out_words;
     int64_t n_tiles;
@@ -138,6 +147,10 @@ struct KParams {
     int32_t pregen_chunks;
     int32_t counts_in_smem;
     int32_t do_dets;             // evaluate DET/OBS ops
+    int32_t debug_skip;          // profiling ablations (pfs_options.debug_skip)
+    int32_t producers;           // threads sampling the next tile's noise (warp-specialised)
+    uint32_t first_pregen;       // first pre-generated noise ordinal (NO_SLOT: none)
+    uint32_t first_cap_base;
 };
 
 struct LaunchCfg {

@@ -83,6 +83,7 @@ __device__ __forceinline__ VW<V> coin_words(const KParams& kp, uint32_t e, int c
                                             int64_t tile) {
     if (kp.coins != nullptr)
         return vldg<V>(kp.coins + (int64_t)e * kp.inject_words + tile * W + c * V);
+    if (kp.debug_skip & 4) return vzero<V>();
     const int word = c * V;
     uint32_t c0 = e, c1 = (uint32_t)(word >> 2), c2 = g, c3 = DOMAIN_COIN;
     philox4x32_10(c0, c1, c2, c3, (uint32_t)kp.seed, (uint32_t)(kp.seed >> 32));
@@ -198,7 +199,76 @@ __device__ __forceinline__ void apply_hit(uint32_t* X, uint32_t* Z, const uint32
     }
 }
 
+// Pre-generated hit entry (u64): q0 (20 bits) | q1 (20) | word (5) | bit (5) |
+// x mask (2) | z mask (2).  Resolved to frame rows by the producer warps, so
+// applying a hit is just one or two shared-memory atomics.
+__device__ __forceinline__ uint64_t make_hit(uint32_t q0, uint32_t q1, uint32_t w, uint32_t bit,
+                                             uint32_t xm, uint32_t zm) {
+    return (uint64_t)q0 | ((uint64_t)q1 << 20) | ((uint64_t)w << 40) | ((uint64_t)bit << 45) |
+           ((uint64_t)xm << 50) | ((uint64_t)zm << 52);
+}
+
+template <int W>
+__device__ __forceinline__ void apply_entry(uint32_t* X, uint32_t* Z, uint64_t e) {
+    const uint32_t q0 = (uint32_t)e & 0xFFFFFu, q1 = (uint32_t)(e >> 20) & 0xFFFFFu;
+    const uint32_t w = (uint32_t)(e >> 40) & 31u, bit = 1u << ((uint32_t)(e >> 45) & 31u);
+    const uint32_t xm = (uint32_t)(e >> 50) & 3u, zm = (uint32_t)(e >> 52) & 3u;
+    if (xm & 1u) atomicXor(X + (size_t)q0 * W + w, bit);
+    if (zm & 1u) atomicXor(Z + (size_t)q0 * W + w, bit);
+    if (xm & 2u) atomicXor(X + (size_t)q1 * W + w, bit);
+    if (zm & 2u) atomicXor(Z + (size_t)q1 * W + w, bit);
+}
+
+__device__ __forceinline__ void consumer_sync(int nthreads) {
+    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
+}
+
+// Sample the pre-generated noise ops of global tile g into hit lists
+// (threads [t0, t0 + nthr) of the CTA).
+template <int W>
+__device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uint32_t* ncnt,
+                                              uint64_t* hits, int t, int nthr) {
+    constexpr uint32_t T = 32 * W;
+    const int total = kp.pregen_chunks;
+    const int per = (total + nthr - 1) / nthr;
+    int c0 = t * per;
+    const int c1 = min(total, c0 + per);
+    if (c0 >= c1) return;
+    int lo = 0, hi = kp.num_pregen - 1;  // last op with chunk_base <= c0
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if ((int)__ldg(&kp.noise[__ldg(kp.pregen_ops + mid)].chunk_base) <= c0) lo = mid;
+        else hi = mid - 1;
+    }
+    for (int k = lo; c0 < c1; k++) {
+        const uint32_t ord = __ldg(kp.pregen_ops + k);
+        const NoiseParam np = kp.noise[ord];
+        const uint32_t* tg = kp.targets + __ldg(&kp.noise_off[ord]);
+        const uint32_t ch = __ldg(&kp.noise_ch[ord]);
+        const int ar = ch == CH_DEP2 ? 2 : 1;
+        const int end = min(c1, (int)(np.chunk_base + np.nchunks));
+        for (; c0 < end; c0++) {
+            noise_chunk(kp, np, ord, (uint32_t)(c0 - np.chunk_base), g,
+                        [&](uint32_t trial, uint32_t pick) {
+                            const uint32_t app = trial / T, s = trial % T;
+                            uint32_t xm, zm;
+                            pattern_of(ch, pick, xm, zm);
+                            const uint32_t q0 = __ldg(tg + app * ar);
+                            const uint32_t q1 = ar == 2 ? __ldg(tg + app * ar + 1) : 0u;
+                            const uint32_t slot = atomicAdd(ncnt + ord, 1u);
+                            if (slot < np.cap)
+                                hits[np.cap_base + slot] = make_hit(q0, q1, s >> 5, s & 31, xm, zm);
+                        });
+        }
+    }
+}
+
 // ------------------------------------------------------------ frame kernel
+// Warp-specialised persistent kernel.  Threads [0, nc) are consumers: they
+// run the op stream of tile i on the frame in shared memory, synchronising on
+// named barrier 1.  Threads [nc, blockDim) are producers: meanwhile they
+// sample the noise of tile i+1 into the other hit-list buffer.  One full
+// __syncthreads per tile hands the buffers over.
 template <int W, bool RING_SMEM>
 __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ KParams kp) {
     constexpr int V = W >= 4 ? 4 : W;  // words per vector access
@@ -211,241 +281,258 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
     uint32_t* const ring = RING_SMEM ? (smem + (size_t)2 * n * W)
                                      : (kp.ring_global + (size_t)blockIdx.x * kp.num_slots * W);
     uint32_t* const cnt = smem + (size_t)2 * n * W + (RING_SMEM ? (size_t)kp.num_slots * W : 0);
-    uint32_t* const ncnt = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // hits per noise op
-    uint32_t* const hits = kp.hits_global + (size_t)blockIdx.x * kp.hit_capacity;
+    uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // [2][num_noise]
+    uint64_t* const hits0 = kp.hits_global + (size_t)blockIdx.x * 2 * kp.hit_capacity;
     const int tid = threadIdx.x;
-    const int nth = blockDim.x;
+    const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
+    const int nprod = pregen ? kp.producers : 0;
+    const int nth = blockDim.x - nprod;  // consumer threads
+    const bool is_consumer = tid < nth;
 
     if (kp.counts_in_smem) {
-        for (int i = tid; i < kp.num_cols; i += nth) cnt[i] = 0u;
+        for (int i = tid; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
     }
-
-    for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x) {
-        const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
-        // FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39)
-        for (int i = tid; i < (n << LC); i += nth) {
-            const int q = i >> LC, c = i & (C - 1);
-            vst<V>(X + (size_t)q * W + c * V, vzero<V>());
-            vst<V>(Z + (size_t)q * W + c * V, coin_words<W, V>(kp, (uint32_t)q, c, g, tile));
-        }
-        for (int i = tid; i < (kp.num_obs << LC); i += nth) {
-            const int k = i >> LC, c = i & (C - 1);
-            vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
-        }
-        // ---- noise pre-pass: sample every pre-generated noise op of this tile
-        // into per-op hit lists (no frame access, no barriers inside) ----
-        if (kp.masks == nullptr && kp.num_pregen > 0) {
-            for (int i = tid; i < kp.num_noise; i += nth) ncnt[i] = 0u;
-            __syncthreads();
-            const int total = kp.pregen_chunks;
-            const int per = (total + nth - 1) / nth;
-            int c0 = tid * per;
-            const int c1 = min(total, c0 + per);
-            if (c0 < c1) {
-                int lo = 0, hi = kp.num_pregen - 1;  // last op with chunk_base <= c0
-                while (lo < hi) {
-                    const int mid = (lo + hi + 1) >> 1;
-                    if ((int)__ldg(&kp.noise[__ldg(kp.pregen_ops + mid)].chunk_base) <= c0) lo = mid;
-                    else hi = mid - 1;
-                }
-                int k = lo;
-                while (c0 < c1) {
-                    const uint32_t ord = __ldg(kp.pregen_ops + k);
-                    const NoiseParam np = kp.noise[ord];
-                    const int end = min(c1, (int)(np.chunk_base + np.nchunks));
-                    for (; c0 < end; c0++) {
-                        noise_chunk(kp, np, ord, (uint32_t)(c0 - np.chunk_base), g,
-                                    [&](uint32_t trial, uint32_t pick) {
-                                        const uint32_t slot = atomicAdd(ncnt + ord, 1u);
-                                        if (slot < np.cap) hits[np.cap_base + slot] = (trial << 4) | pick;
-                                    });
-                    }
-                    k++;
-                }
-            }
-        }
+    // prologue: every thread samples the first tile's noise into buffer 0
+    if (pregen && (int64_t)blockIdx.x < kp.n_tiles) {
+        for (int i = tid; i < kp.num_noise; i += blockDim.x) ncnt0[i] = 0u;
         __syncthreads();
+        noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid, blockDim.x);
+    }
+    __syncthreads();
 
-        uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
-        uint4 h1 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops) + 1) : make_uint4(0, 0, 0, 0);
-        for (int oi = 0; oi < kp.n_ops; oi++) {
-            const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
-            const uint32_t count = h0.y, off = h0.z, oa = h0.w, ob = h1.x;
-            // prefetch the next op descriptor while this one runs
-            if (oi + 1 < kp.n_ops) {
-                h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
-                h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1) + 1);
+    int it = 0;
+    for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x, it++) {
+        const int buf = it & 1;
+        uint32_t* const ncnt = ncnt0 + buf * kp.num_noise;
+        uint64_t* const hits = hits0 + (size_t)buf * kp.hit_capacity;
+        const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
+        if (!is_consumer) {
+            // ---- producers: noise of this CTA's next tile into the other buffer ----
+            const int64_t nt = tile + gridDim.x;
+            if (nt < kp.n_tiles) {
+                uint32_t* const ncn = ncnt0 + (buf ^ 1) * kp.num_noise;
+                const int pt = tid - nth;
+                for (int i = pt; i < kp.num_noise; i += nprod) ncn[i] = 0u;
+                asm volatile("bar.sync 2, %0;" ::"r"(nprod) : "memory");
+                noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + (uint64_t)nt), ncn,
+                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt, nprod);
             }
-            if (flags & F_BARRIER) __syncthreads();
-            const uint32_t* tg = kp.targets + off;
-            switch (kind) {
-            case K_GATE: {
-                const int items = (int)(count << LC);
-                switch (code) {
-                case R_SWAPXZ:
-                    for (int i = tid; i < items; i += nth) {
-                        const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
-                        const VW<V> a = vld<V>(X + p), b = vld<V>(Z + p);
-                        vst<V>(X + p, b); vst<V>(Z + p, a);
-                    }
-                    break;
-                case R_ZXORX:
-                    for (int i = tid; i < items; i += nth) {
-                        const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
-                        vst<V>(Z + p, vxor<V>(vld<V>(Z + p), vld<V>(X + p)));
-                    }
-                    break;
-                case R_XXORZ:
-                    for (int i = tid; i < items; i += nth) {
-                        const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
-                        vst<V>(X + p, vxor<V>(vld<V>(X + p), vld<V>(Z + p)));
-                    }
-                    break;
-                default: {  // two-qubit rules
-                    for (int i = tid; i < items; i += nth) {
-                        const uint2 qq = __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC));
-                        const int cv = (i & (C - 1)) * V;
-                        const size_t p0 = (size_t)qq.x * W + cv, p1 = (size_t)qq.y * W + cv;
-                        const VW<V> x0 = vld<V>(X + p0), x1 = vld<V>(X + p1);
-                        const VW<V> z0 = vld<V>(Z + p0), z1 = vld<V>(Z + p1);
-                        switch (code) {
-                        case R_CX:
-                            vst<V>(X + p1, vxor<V>(x1, x0)); vst<V>(Z + p0, vxor<V>(z0, z1)); break;
-                        case R_CZ:
-                            vst<V>(Z + p0, vxor<V>(z0, x1)); vst<V>(Z + p1, vxor<V>(z1, x0)); break;
-                        case R_CY:
-                            vst<V>(X + p1, vxor<V>(x1, x0));
-                            vst<V>(Z + p0, vxor<V>(z0, vxor<V>(x1, z1)));
-                            vst<V>(Z + p1, vxor<V>(z1, x0)); break;
-                        default:  // SWAP
-                            vst<V>(X + p0, x1); vst<V>(X + p1, x0);
-                            vst<V>(Z + p0, z1); vst<V>(Z + p1, z0); break;
+        } else {
+            // ---- consumers: FrameBatch.__init__: x = 0, z = coins (frame_sim.py:36-39) ----
+            for (int i = tid; i < (n << LC); i += nth) {
+                const int q = i >> LC, c = i & (C - 1);
+                vst<V>(X + (size_t)q * W + c * V, vzero<V>());
+                vst<V>(Z + (size_t)q * W + c * V, coin_words<W, V>(kp, (uint32_t)q, c, g, tile));
+            }
+            for (int i = tid; i < (kp.num_obs << LC); i += nth) {
+                const int k = i >> LC, c = i & (C - 1);
+                vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
+            }
+            // register prefetch of the first pre-generated noise op's hit `tid`
+            uint32_t pf_ord = pregen ? kp.first_pregen : NO_SLOT;
+            uint64_t pf_hit = 0;
+            if (pf_ord != NO_SLOT && (uint32_t)tid < ncnt[pf_ord]) pf_hit = hits[kp.first_cap_base + tid];
+            consumer_sync(nth);
+
+            uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
+            uint4 h1 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops) + 1) : make_uint4(0, 0, 0, 0);
+            for (int oi = 0; oi < kp.n_ops; oi++) {
+                const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
+                const uint32_t count = h0.y, off = h0.z, oa = h0.w, ob = h1.x;
+                const uint32_t oc = h1.y, od = h1.z, oe = h1.w;
+                // prefetch the next op descriptor while this one runs
+                if (oi + 1 < kp.n_ops) {
+                    h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
+                    h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1) + 1);
+                }
+                if (flags & F_BARRIER) consumer_sync(nth);
+                const uint32_t* tg = kp.targets + off;
+                if (kp.debug_skip) {
+                    const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
+                                       : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
+                    if (kp.debug_skip & bit) continue;
+                }
+                switch (kind) {
+                case K_GATE: {
+                    const int items = (int)(count << LC);
+                    switch (code) {
+                    case R_SWAPXZ:
+                        for (int i = tid; i < items; i += nth) {
+                            const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                            const VW<V> a = vld<V>(X + p), b = vld<V>(Z + p);
+                            vst<V>(X + p, b); vst<V>(Z + p, a);
+                        }
+                        break;
+                    case R_ZXORX:
+                        for (int i = tid; i < items; i += nth) {
+                            const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                            vst<V>(Z + p, vxor<V>(vld<V>(Z + p), vld<V>(X + p)));
+                        }
+                        break;
+                    case R_XXORZ:
+                        for (int i = tid; i < items; i += nth) {
+                            const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                            vst<V>(X + p, vxor<V>(vld<V>(X + p), vld<V>(Z + p)));
+                        }
+                        break;
+                    default: {  // two-qubit rules
+                        for (int i = tid; i < items; i += nth) {
+                            const uint2 qq = __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC));
+                            const int cv = (i & (C - 1)) * V;
+                            const size_t p0 = (size_t)qq.x * W + cv, p1 = (size_t)qq.y * W + cv;
+                            const VW<V> x0 = vld<V>(X + p0), x1 = vld<V>(X + p1);
+                            const VW<V> z0 = vld<V>(Z + p0), z1 = vld<V>(Z + p1);
+                            switch (code) {
+                            case R_CX:
+                                vst<V>(X + p1, vxor<V>(x1, x0)); vst<V>(Z + p0, vxor<V>(z0, z1)); break;
+                            case R_CZ:
+                                vst<V>(Z + p0, vxor<V>(z0, x1)); vst<V>(Z + p1, vxor<V>(z1, x0)); break;
+                            case R_CY:
+                                vst<V>(X + p1, vxor<V>(x1, x0));
+                                vst<V>(Z + p0, vxor<V>(z0, vxor<V>(x1, z1)));
+                                vst<V>(Z + p1, vxor<V>(z1, x0)); break;
+                            default:  // SWAP
+                                vst<V>(X + p0, x1); vst<V>(X + p1, x0);
+                                vst<V>(Z + p0, z1); vst<V>(Z + p1, z0); break;
+                            }
                         }
                     }
-                }
-                }
-                break;
-            }
-            case K_M: case K_MR: {
-                const int items = (int)(count << LC);
-                for (int i = tid; i < items; i += nth) {
-                    const int j = i >> LC, c = i & (C - 1);
-                    const uint2 qs = __ldg(reinterpret_cast<const uint2*>(tg) + j);
-                    const size_t p = (size_t)qs.x * W + c * V;
-                    const VW<V> xv = vld<V>(X + p);
-                    if (kp.do_dets && qs.y != NO_SLOT) vst<V>(ring + (size_t)qs.y * W + c * V, xv);
-                    if (kp.rec_out != nullptr)
-                        vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_words + tile * W + c * V, xv);
-                    if (kind == K_M) {
-                        vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_words<W, V>(kp, ob + j, c, g, tile)));
-                    } else {
-                        vst<V>(X + p, vzero<V>());
-                        vst<V>(Z + p, coin_words<W, V>(kp, ob + 2 * j + 1, c, g, tile));
                     }
+                    break;
                 }
-                break;
-            }
-            case K_R: {
-                const int items = (int)(count << LC);
-                for (int i = tid; i < items; i += nth) {
-                    const int j = i >> LC, c = i & (C - 1);
-                    const size_t p = (size_t)__ldg(tg + j) * W + c * V;
-                    vst<V>(X + p, vzero<V>());
-                    vst<V>(Z + p, coin_words<W, V>(kp, ob + j, c, g, tile));
+                case K_M: case K_MR: {
+                    const int items = (int)(count << LC);
+                    for (int i = tid; i < items; i += nth) {
+                        const int j = i >> LC, c = i & (C - 1);
+                        const uint2 qs = __ldg(reinterpret_cast<const uint2*>(tg) + j);
+                        const size_t p = (size_t)qs.x * W + c * V;
+                        const VW<V> xv = vld<V>(X + p);
+                        if (kp.do_dets && qs.y != NO_SLOT) vst<V>(ring + (size_t)qs.y * W + c * V, xv);
+                        if (kp.rec_out != nullptr)
+                            vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_words + tile * W + c * V, xv);
+                        if (kind == K_M) {
+                            vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_words<W, V>(kp, ob + j, c, g, tile)));
+                        } else {
+                            vst<V>(X + p, vzero<V>());
+                            vst<V>(Z + p, coin_words<W, V>(kp, ob + 2 * j + 1, c, g, tile));
+                        }
+                    }
+                    break;
                 }
-                break;
-            }
-            case K_NOISE: {
-                const int ar = code == CH_DEP2 ? 2 : 1;
-                if (kp.masks != nullptr) {
-                    // injected masks: per target, x row then z row
-                    const int items = (int)((count * ar) << LC);
+                case K_R: {
+                    const int items = (int)(count << LC);
                     for (int i = tid; i < items; i += nth) {
                         const int j = i >> LC, c = i & (C - 1);
                         const size_t p = (size_t)__ldg(tg + j) * W + c * V;
-                        const uint32_t* mrow = kp.masks + (int64_t)(oa + 2 * j) * kp.inject_words + tile * W + c * V;
-                        const VW<V> mx = vldg<V>(mrow), mz = vldg<V>(mrow + kp.inject_words);
-                        if (flags & F_DUP) {
-#pragma unroll
-                            for (int k = 0; k < V; k++) {
-                                if (mx.w[k]) atomicXor(X + p + k, mx.w[k]);
-                                if (mz.w[k]) atomicXor(Z + p + k, mz.w[k]);
-                            }
-                        } else {
-                            vst<V>(X + p, vxor<V>(vld<V>(X + p), mx));
-                            vst<V>(Z + p, vxor<V>(vld<V>(Z + p), mz));
-                        }
+                        vst<V>(X + p, vzero<V>());
+                        vst<V>(Z + p, coin_words<W, V>(kp, ob + j, c, g, tile));
                     }
                     break;
                 }
-                const NoiseParam np = kp.noise[ob];
-                if (np.flags & NZ_NONE) break;
-                if ((np.flags & NZ_PREGEN) && ncnt[ob] <= np.cap) {
-                    const uint32_t nh = ncnt[ob];
-                    for (uint32_t i = tid; i < nh; i += nth) {
-                        const uint32_t e = hits[np.cap_base + i];
-                        apply_hit<W>(X, Z, tg, code, ar, e >> 4, e & 15u);
+                case K_NOISE: {
+                    const int ar = code == CH_DEP2 ? 2 : 1;
+                    if (kp.masks != nullptr) {
+                        // injected masks: per target, x row then z row
+                        const int items = (int)((count * ar) << LC);
+                        for (int i = tid; i < items; i += nth) {
+                            const int j = i >> LC, c = i & (C - 1);
+                            const size_t p = (size_t)__ldg(tg + j) * W + c * V;
+                            const uint32_t* mrow = kp.masks + (int64_t)(oa + 2 * j) * kp.inject_words + tile * W + c * V;
+                            const VW<V> mx = vldg<V>(mrow), mz = vldg<V>(mrow + kp.inject_words);
+                            if (flags & F_DUP) {
+#pragma unroll
+                                for (int k = 0; k < V; k++) {
+                                    if (mx.w[k]) atomicXor(X + p + k, mx.w[k]);
+                                    if (mz.w[k]) atomicXor(Z + p + k, mz.w[k]);
+                                }
+                            } else {
+                                vst<V>(X + p, vxor<V>(vld<V>(X + p), mx));
+                                vst<V>(Z + p, vxor<V>(vld<V>(Z + p), mz));
+                            }
+                        }
+                        break;
                     }
-                } else {
-                    // inline sampling (large-p ops, or a pre-pass list overflow)
+                    if ((flags & F_PREGEN) && pregen) {
+                        const NoiseParam* npp = kp.noise + ob;
+                        const uint32_t nh = ncnt[ob];
+                        if (nh <= __ldg(&npp->cap)) {
+                            // hit `tid` was prefetched into a register
+                            if ((uint32_t)tid < nh && pf_ord == ob) apply_entry<W>(X, Z, pf_hit);
+                            for (uint32_t i = (pf_ord == ob ? nth : 0) + tid; i < nh; i += nth)
+                                apply_entry<W>(X, Z, hits[oc + i]);
+                        } else {
+                            for (uint32_t r = tid; r < __ldg(&npp->nchunks); r += nth)
+                                noise_chunk(kp, *npp, ob, r, g, [&](uint32_t trial, uint32_t pick) {
+                                    apply_hit<W>(X, Z, tg, code, ar, trial, pick);
+                                });
+                        }
+                        // prefetch the next pre-generated op's hit `tid`
+                        pf_ord = od;
+                        if (od != NO_SLOT && (uint32_t)tid < ncnt[od]) pf_hit = hits[oe + tid];
+                        break;
+                    }
+                    if (kp.debug_skip & 2) break;
+                    const NoiseParam np = kp.noise[ob];
+                    if (np.flags & NZ_NONE) break;
+                    // inline sampling (large-p ops)
                     for (uint32_t r = tid; r < np.nchunks; r += nth)
                         noise_chunk(kp, np, ob, r, g, [&](uint32_t trial, uint32_t pick) {
                             apply_hit<W>(X, Z, tg, code, ar, trial, pick);
                         });
+                    break;
                 }
-                break;
-            }
-            case K_DET: {
-                if (!kp.do_dets) break;
-                const int items = (int)(count << LC);
-                for (int i = tid; i < items; i += nth) {
-                    const uint32_t col = oa + (uint32_t)(i >> LC);
-                    const int c = i & (C - 1);
-                    VW<V> acc = vzero<V>();
-                    const uint32_t e0 = __ldg(kp.det_ptr + col), e1 = __ldg(kp.det_ptr + col + 1);
-                    for (uint32_t e = e0; e < e1; e++) {
-                        const uint32_t s = __ldg(kp.det_terms + e);
-                        acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
-                    }
-                    if (kp.ev_out != nullptr)
-                        vst<V>(kp.ev_out + (int64_t)col * kp.out_words + tile * W + c * V, acc);
-                    if (kp.counts != nullptr) {
-                        uint32_t tot = 0;
+                case K_DET: {
+                    if (!kp.do_dets) break;
+                    const int items = (int)(count << LC);
+                    for (int i = tid; i < items; i += nth) {
+                        const uint32_t col = oa + (uint32_t)(i >> LC);
+                        const int c = i & (C - 1);
+                        VW<V> acc = vzero<V>();
+                        const uint32_t e0 = __ldg(kp.det_ptr + col), e1 = __ldg(kp.det_ptr + col + 1);
+                        for (uint32_t e = e0; e < e1; e++) {
+                            const uint32_t s = __ldg(kp.det_terms + e);
+                            acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
+                        }
+                        if (kp.ev_out != nullptr)
+                            vst<V>(kp.ev_out + (int64_t)col * kp.out_words + tile * W + c * V, acc);
+                        if (kp.counts != nullptr) {
+                            uint32_t tot = 0;
 #pragma unroll
-                        for (int jw = 0; jw < V; jw++) {
-                            const int64_t s0 = tile * (int64_t)(32 * W) + 32 * (c * V + jw);
-                            const int64_t rem = kp.num_shots - s0;
-                            const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-                            tot += __popc(acc.w[jw] & m);
-                        }
-                        if (tot) {
-                            if (kp.counts_in_smem) atomicAdd(cnt + col, tot);
-                            else atomicAdd(kp.counts + col, (unsigned long long)tot);
+                            for (int jw = 0; jw < V; jw++) {
+                                const int64_t s0 = tile * (int64_t)(32 * W) + 32 * (c * V + jw);
+                                const int64_t rem = kp.num_shots - s0;
+                                const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+                                tot += __popc(acc.w[jw] & m);
+                            }
+                            if (tot) {
+                                if (kp.counts_in_smem) atomicAdd(cnt + col, tot);
+                                else atomicAdd(kp.counts + col, (unsigned long long)tot);
+                            }
                         }
                     }
+                    break;
                 }
-                break;
-            }
-            case K_OBS: {
-                if (!kp.do_dets) break;
-                for (int c = tid; c < C; c += nth) {
-                    VW<V> acc = vld<V>(ring + (size_t)oa * W + c * V);
-                    for (uint32_t j = 0; j < count; j++) {
-                        const uint32_t s = __ldg(tg + j);
-                        acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
+                case K_OBS: {
+                    if (!kp.do_dets) break;
+                    for (int c = tid; c < C; c += nth) {
+                        VW<V> acc = vld<V>(ring + (size_t)oa * W + c * V);
+                        for (uint32_t j = 0; j < count; j++) {
+                            const uint32_t s = __ldg(tg + j);
+                            acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
+                        }
+                        vst<V>(ring + (size_t)oa * W + c * V, acc);
                     }
-                    vst<V>(ring + (size_t)oa * W + c * V, acc);
+                    break;
                 }
-                break;
-            }
-            default: break;
+                default: break;
+                }
             }
         }
         __syncthreads();
     }
     if (kp.counts_in_smem) {
         __syncthreads();
-        for (int i = tid; i < kp.num_cols; i += nth)
+        for (int i = tid; i < kp.num_cols; i += blockDim.x)
             if (cnt[i]) atomicAdd(kp.counts + i, (unsigned long long)cnt[i]);
     }
 }

@@ -290,6 +290,20 @@ def make_pairs(num_det: int, per_round: int, seed: int, n_random: int = 4000):
     return np.array(pairs, dtype=np.int64).reshape(-1, 2)
 
 
+def _stat_subprocess(job):
+    """Run one stats shard in a fresh interpreter (fork/spawn pools hang here)."""
+    import pickle
+    import subprocess
+    import tempfile
+
+    with tempfile.NamedTemporaryFile(suffix=".pkl", delete=False) as f:
+        pickle.dump(job, f)
+        path = f.name
+    subprocess.run([sys.executable, os.path.abspath(__file__), "_statjob", path], check=True)
+    with open(path + ".out", "rb") as f:
+        return pickle.load(f)
+
+
 def gen_stats(procs: int, only=None):
     cases = [
         ("d3", gen.surface_code_memory(3, 3, 1e-2), 1 << 16, 1024, 8),
@@ -306,8 +320,9 @@ def gen_stats(procs: int, only=None):
         pairs = make_pairs(nd, per_round, 3)
         per = shots // procs
         jobs = [(text, per, 1000 + i, B, pairs) for i in range(procs)]
-        with mp.get_context("spawn").Pool(procs) as pool:
-            res = pool.map(_stat_worker, jobs)
+        from concurrent.futures import ThreadPoolExecutor
+        with ThreadPoolExecutor(procs) as pool:
+            res = list(pool.map(_stat_subprocess, jobs))
         counts = sum(r[0] for r in res)
         pc = sum(r[1] for r in res)
         np.savez_compressed(os.path.join(HERE, f"stats_{name}.npz"), text=np.array(text),
@@ -340,6 +355,13 @@ def gen_exact():
 
 
 if __name__ == "__main__":
+    if len(sys.argv) == 3 and sys.argv[1] == "_statjob":
+        import pickle
+        with open(sys.argv[2], "rb") as f:
+            job = pickle.load(f)
+        with open(sys.argv[2] + ".out", "wb") as f:
+            pickle.dump(_stat_worker(job), f)
+        sys.exit(0)
     which = set(sys.argv[1:]) or {"plans", "inject", "noiseless", "stats", "exact"}
     if "plans" in which:
         gen_frame_plans()
