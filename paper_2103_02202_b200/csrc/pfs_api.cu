@@ -155,6 +155,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
     }
     const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 2.0;
     try {
+        reorder_for_banks(pg->hp, pg->cfg.W);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
     } catch (const std::invalid_argument& e) {
         delete pg;
@@ -378,8 +379,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.noise_ch = pg->d_noise_ch.p;
     kp.first_pregen = hp.first_pregen;
     kp.first_cap_base = hp.first_cap_base;
-    kp.producers = hp.pregen_ops.empty() ? 0 : (pg->opts.producer_threads > 0 ? pg->opts.producer_threads : 256);
-    if (kp.producers >= pg->cfg.threads) kp.producers = pg->cfg.threads / 4;
+    kp.producers = hp.pregen_ops.empty() ? 0 : (pg->opts.producer_threads > 0 ? pg->opts.producer_threads : 512);
+    if (kp.producers >= pg->cfg.threads) kp.producers = pg->cfg.threads / 2;
     kp.coins = injected ? pg->d_coins.p : nullptr;
     kp.masks = injected ? pg->d_masks.p : nullptr;
     kp.inject_words = words_all;

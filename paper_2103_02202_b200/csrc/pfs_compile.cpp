@@ -324,6 +324,51 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     return hp;
 }
 
+// Reorder the applications of every gate op so each aligned group of G
+// consecutive applications (the apps one shared-memory wavefront serves: G =
+// 128 B / row bytes) touches G distinct bank groups per operand.  Apps of one
+// op are independent by construction, so any order is the same circuit.
+void reorder_for_banks(HostProgram& hp, int W) {
+    const int G = W >= 32 ? 1 : 128 / (W * 4);
+    if (G <= 1) return;
+    std::vector<uint32_t> scratch;
+    for (DOp& o : hp.ops) {
+        if ((o.kcf & 0xFF) != K_GATE || o.count < 2) continue;
+        const int ar = rule_arity((o.kcf >> 8) & 0xFF);
+        const uint32_t A = o.count;
+        uint32_t* tg = hp.targets.data() + o.off;
+        // buckets of app indices by first-operand residue
+        std::vector<std::vector<uint32_t>> bucket(G);
+        for (uint32_t a = 0; a < A; a++) bucket[tg[a * ar] % G].push_back(a);
+        std::vector<size_t> head(G, 0);
+        scratch.clear();
+        scratch.reserve((size_t)A * ar);
+        uint32_t left = A;
+        std::vector<char> used1(G);
+        while (left) {
+            std::fill(used1.begin(), used1.end(), 0);
+            int taken = 0;
+            for (int r = 0; r < G && left; r++) {
+                auto& b = bucket[r];
+                if (head[r] >= b.size()) continue;
+                size_t pick = head[r];
+                if (ar == 2) {  // prefer an app whose second operand residue is unused
+                    for (size_t k = head[r]; k < b.size() && k < head[r] + 8; k++)
+                        if (!used1[tg[b[k] * 2 + 1] % G]) { pick = k; break; }
+                    std::swap(b[head[r]], b[pick]);
+                    used1[tg[b[head[r]] * 2 + 1] % G] = 1;
+                }
+                const uint32_t a = b[head[r]++];
+                for (int s2 = 0; s2 < ar; s2++) scratch.push_back(tg[a * ar + s2]);
+                left--;
+                taken++;
+            }
+            (void)taken;
+        }
+        std::copy(scratch.begin(), scratch.end(), tg);
+    }
+}
+
 // Binomial(n, p) inverse-CDF thresholds in 64-bit fixed point:
 // X = min{m : u < t[m]} for u uniform on [0, 2^64), X = len(t) if u >= every
 // entry.  Upper-tail thresholds are built from the tail sum so their absolute
@@ -375,9 +420,10 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
             np.flags = NZ_ALL;
             L = std::min<uint64_t>(N, 1024);
         } else {
+            // power of two nearest (in ratio) to target_hits / p trials
             double want = target_hits / p;
             L = 1;
-            while ((double)(L * 2) <= want && L < (1ull << 30)) L *= 2;
+            while ((double)(L * 2) <= want * 1.41421356 && L < (1ull << 30)) L *= 2;
             if (L > N) L = N;
         }
         np.L = (uint32_t)L;

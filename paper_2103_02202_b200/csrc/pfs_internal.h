@@ -29,7 +29,7 @@ constexpr uint32_t DOMAIN_NOISE = 0x80000000u;
 constexpr uint32_t NZ_NONE = 1u;     // p == 0: no hits
 constexpr uint32_t NZ_ALL = 2u;      // p == 1: every trial hits
 constexpr uint32_t NZ_PREGEN = 4u;   // hits generated in the tile's pre-pass into a hit list
-constexpr int NZ_MAX_LIST = 16;      // distinct-position list; larger counts use selection sampling
+constexpr int NZ_MAX_LIST = 8;      // distinct-position list; larger counts use selection sampling
 
 // One device op (32 bytes).  See DESIGN.md §3.
 //   GATE : count = apps, off -> targets (1 or 2 per app)
@@ -111,6 +111,7 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
                             int64_t num_coin_rows, int64_t num_noise_rows);
 
 void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits);
+void reorder_for_banks(HostProgram& hp, int W);
 
 // Kernel launch plumbing (pfs_kernels.cu)
 struct KParams {

@@ -109,22 +109,24 @@ __device__ __forceinline__ void pattern_of(uint32_t ch, uint32_t pick, uint32_t&
 }
 
 // Stream of 32-bit Philox words for one noise chunk: call j of chunk r in
-// global tile g of noise instruction `ordinal`.
+// global tile g of noise instruction `ordinal`.  The 4-word
+// buffer lives in registers (constant-index selects, no local memory).
 struct WordStream {
     uint32_t r, g, dom, k0, k1, j;
-    uint32_t buf[4];
+    uint32_t b0, b1, b2, b3;
     int idx;
     __device__ __forceinline__ WordStream(uint32_t r_, uint32_t g_, uint32_t ordinal, uint64_t seed)
         : r(r_), g(g_), dom(DOMAIN_NOISE | ordinal), k0((uint32_t)seed), k1((uint32_t)(seed >> 32)),
-          j(0), idx(4) {}
+          j(0), b0(0), b1(0), b2(0), b3(0), idx(4) {}
     __device__ __forceinline__ uint32_t next() {
         if (idx == 4) {
-            uint32_t c0 = j++, c1 = r, c2 = g, c3 = dom;
-            philox4x32_10(c0, c1, c2, c3, k0, k1);
-            buf[0] = c0; buf[1] = c1; buf[2] = c2; buf[3] = c3;
+            b0 = j++; b1 = r; b2 = g; b3 = dom;
+            philox4x32_10(b0, b1, b2, b3, k0, k1);
             idx = 0;
         }
-        return buf[idx++];
+        const uint32_t v = idx == 0 ? b0 : idx == 1 ? b1 : idx == 2 ? b2 : b3;
+        idx++;
+        return v;
     }
     __device__ __forceinline__ uint64_t next64() {
         const uint32_t lo = next();
@@ -146,23 +148,27 @@ __device__ __forceinline__ void noise_chunk(const KParams& kp, const NoiseParam&
         return;
     }
     const bool full = len == np.L;
-    const uint64_t* tab = kp.noise_tab + (full ? np.tab_full : np.tab_last);
+    const unsigned long long* tab =
+        reinterpret_cast<const unsigned long long*>(kp.noise_tab) + (full ? np.tab_full : np.tab_last);
     const uint32_t tlen = full ? np.len_full : np.len_last;
     const uint64_t u = ws.next64();
     uint32_t count = 0;
-    while (count < tlen && u >= __ldg(reinterpret_cast<const unsigned long long*>(tab) + count)) count++;
+    while (count < tlen && u >= __ldg(tab + count)) count++;
     if (count == 0) return;
     if (count <= NZ_MAX_LIST) {
-        uint32_t sel[NZ_MAX_LIST];
+        uint32_t sel[NZ_MAX_LIST];  // constant-indexed only: stays in registers
         for (uint32_t h = 0; h < count; h++) {
             uint32_t pos;
             bool dup;
             do {
                 pos = (uint32_t)__umul64hi(ws.next64(), (uint64_t)len);
                 dup = false;
-                for (uint32_t q = 0; q < h; q++) dup |= sel[q] == pos;
+#pragma unroll
+                for (uint32_t q = 0; q < NZ_MAX_LIST; q++) dup |= (q < h) && sel[q] == pos;
             } while (dup);
-            sel[h] = pos;
+#pragma unroll
+            for (uint32_t q = 0; q < NZ_MAX_LIST; q++)
+                if (q == h) sel[q] = pos;
             emit(base + pos, np.npat > 1 ? __umulhi(ws.next(), np.npat) : 0u);
         }
     } else {

@@ -43,6 +43,12 @@ def main():
         ("W16_no_noise", {"words_per_tile": 16, "ring_in_smem": 0, "debug_skip": 3}),
         ("W16_no_gates", {"words_per_tile": 16, "ring_in_smem": 0, "debug_skip": 16}),
         ("W16_no_dets", {"words_per_tile": 16, "ring_in_smem": 0, "debug_skip": 8}),
+        ("nn_no_gates", {"debug_skip": 3 | 16}),
+        ("nn_no_dets", {"debug_skip": 3 | 8}),
+        ("nn_no_collapse", {"debug_skip": 3 | 32}),
+        ("nn_no_coins", {"debug_skip": 3 | 4}),
+        ("producers_only", {"debug_skip": 1 | 4 | 8 | 16 | 32}),
+        ("producers_only_p512", {"debug_skip": 1 | 4 | 8 | 16 | 32, "producer_threads": 512}),
     ]
     if a.variants:
         keep = set(a.variants.split(","))
