@@ -90,24 +90,19 @@ typedef struct {
 
 typedef struct { const orc_job* job; int tid; int rc; } orc_worker;
 
-typedef struct { uint32_t r, g, dom, j, idx; uint32_t key[2]; uint32_t buf[4]; } word_stream;
-
-static inline uint32_t ws_next(word_stream* ws) {
-    if (ws->idx == 4) {
-        uint32_t ctr[4] = {ws->j++, ws->r, ws->g, ws->dom};
-        orc_philox4x32_10(ctr, ws->key, ws->buf);
-        ws->idx = 0;
-    }
-    return ws->buf[ws->idx++];
-}
-static inline uint64_t ws_next64(word_stream* ws) {
-    uint32_t lo = ws_next(ws);
-    return ((uint64_t)ws_next(ws) << 32) | lo;
-}
 static inline uint64_t umul64hi(uint64_t a, uint64_t b) {
     return (uint64_t)(((unsigned __int128)a * b) >> 64);
 }
 static inline uint32_t umulhi32(uint32_t a, uint32_t b) { return (uint32_t)(((uint64_t)a * b) >> 32); }
+
+/* Philox block j of chunk r: j = 0 count, j = 1 + h + 8*attempt
+ * hit h, j = 2^31 + i selection sampling / p == 1 trials. */
+static inline void noise_block(uint32_t j, uint32_t r, uint32_t g, uint32_t ordinal, uint64_t seed,
+                               uint32_t w[4]) {
+    uint32_t ctr[4] = {j, r, g, 0x80000000u | ordinal};
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    orc_philox4x32_10(ctr, key, w);
+}
 
 /* hits of chunk r: emit(trial within the op, pattern pick) */
 typedef void (*emit_fn)(void* ctx, uint32_t trial, uint32_t pick);
@@ -115,36 +110,42 @@ static void noise_chunk(const orc_noise* np, const uint64_t* tabs, uint64_t seed
                         uint32_t r, uint32_t g, emit_fn emit, void* ctx) {
     const uint32_t len = (r + 1 == np->nchunks) ? np->last_len : np->L;
     const uint32_t base = r * np->L;
-    word_stream ws = {r, g, 0x80000000u | ordinal, 0, 4, {(uint32_t)seed, (uint32_t)(seed >> 32)}, {0, 0, 0, 0}};
+    uint32_t w[4];
     if (np->flags & NZ_ALL) {
-        for (uint32_t i = 0; i < len; i++) emit(ctx, base + i, np->npat > 1 ? umulhi32(ws_next(&ws), np->npat) : 0u);
+        for (uint32_t i = 0; i < len; i++) {
+            noise_block(0x80000000u + i, r, g, ordinal, seed, w);
+            emit(ctx, base + i, np->npat > 1 ? umulhi32(w[2], np->npat) : 0u);
+        }
         return;
     }
     const int full = len == np->L;
     const uint64_t* tab = tabs + (full ? np->tab_full : np->tab_last);
     const uint32_t tlen = full ? np->len_full : np->len_last;
-    const uint64_t u = ws_next64(&ws);
+    noise_block(0u, r, g, ordinal, seed, w);
+    const uint64_t u = ((uint64_t)w[1] << 32) | w[0];
     uint32_t count = 0;
     while (count < tlen && u >= tab[count]) count++;
     if (count == 0) return;
     if (count <= NZ_MAX_LIST) {
-        uint32_t sel[NZ_MAX_LIST];
-        for (uint32_t h = 0; h < count; h++) {
-            uint32_t pos;
-            int dup;
-            do {
-                pos = (uint32_t)umul64hi(ws_next64(&ws), len);
-                dup = 0;
-                for (uint32_t q = 0; q < h; q++) dup |= sel[q] == pos;
-            } while (dup);
-            sel[h] = pos;
-            emit(ctx, base + pos, np->npat > 1 ? umulhi32(ws_next(&ws), np->npat) : 0u);
+        uint32_t pos[NZ_MAX_LIST], pick[NZ_MAX_LIST];
+        for (uint32_t attempt = 0;; attempt++) {
+            for (uint32_t h = 0; h < count; h++) {
+                noise_block(1u + h + NZ_MAX_LIST * attempt, r, g, ordinal, seed, w);
+                pos[h] = (uint32_t)umul64hi(((uint64_t)w[1] << 32) | w[0], len);
+                pick[h] = np->npat > 1 ? umulhi32(w[2], np->npat) : 0u;
+            }
+            int dup = 0;
+            for (uint32_t h = 1; h < count; h++)
+                for (uint32_t q = 0; q < h; q++) dup |= pos[h] == pos[q];
+            if (!dup) break;
         }
+        for (uint32_t h = 0; h < count; h++) emit(ctx, base + pos[h], pick[h]);
     } else {
         uint32_t needed = count;
         for (uint32_t i = 0; needed > 0; i++) {
-            if (umul64hi(ws_next64(&ws), (uint64_t)(len - i)) < needed) {
-                emit(ctx, base + i, np->npat > 1 ? umulhi32(ws_next(&ws), np->npat) : 0u);
+            noise_block(0x80000000u + i, r, g, ordinal, seed, w);
+            if (umul64hi(((uint64_t)w[1] << 32) | w[0], (uint64_t)(len - i)) < needed) {
+                emit(ctx, base + i, np->npat > 1 ? umulhi32(w[2], np->npat) : 0u);
                 needed--;
             }
         }

@@ -75,7 +75,10 @@ struct pfs_program {
     int64_t last_launches = 0;
 };
 
-static size_t fixed_smem(const HostProgram& hp) { return (size_t)hp.num_noise * 8; }
+// noise counters (2 buffers) + the sampler's per-thread duplicate-check scratch
+static size_t fixed_smem(const HostProgram& hp) {
+    return (size_t)hp.num_noise * 8 + (size_t)NZ_MAX_LIST * FRAME_MAX_THREADS * 4;
+}
 
 static void choose_layout(pfs_program* pg) {
     const HostProgram& hp = pg->hp;
@@ -107,7 +110,7 @@ static void choose_layout(pfs_program* pg) {
     pg->cfg.W = W;
     pg->cfg.ring_smem = rs;
     pg->cfg.smem_bytes = frame(W) + (rs ? ring(W) : 0);
-    int threads = o.threads > 0 ? o.threads : 1024;
+    int threads = o.threads > 0 ? std::min(o.threads, FRAME_MAX_THREADS) : FRAME_MAX_THREADS;
     pg->cfg.threads = threads;
 }
 
@@ -379,7 +382,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.noise_ch = pg->d_noise_ch.p;
     kp.first_pregen = hp.first_pregen;
     kp.first_cap_base = hp.first_cap_base;
-    kp.producers = hp.pregen_ops.empty() ? 0 : (pg->opts.producer_threads > 0 ? pg->opts.producer_threads : 512);
+    kp.producers = hp.pregen_ops.empty() ? 0 : (pg->opts.producer_threads > 0 ? pg->opts.producer_threads : 256);
     if (kp.producers >= pg->cfg.threads) kp.producers = pg->cfg.threads / 2;
     kp.coins = injected ? pg->d_coins.p : nullptr;
     kp.masks = injected ? pg->d_masks.p : nullptr;

@@ -418,12 +418,12 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
         uint64_t L;
         if (p >= 1.0) {
             np.flags = NZ_ALL;
-            L = std::min<uint64_t>(N, 1024);
+            L = std::min<uint64_t>(N, 1024);  // positions must stay below 2^28
         } else {
             // power of two nearest (in ratio) to target_hits / p trials
             double want = target_hits / p;
             L = 1;
-            while ((double)(L * 2) <= want * 1.41421356 && L < (1ull << 30)) L *= 2;
+            while ((double)(L * 2) <= want * 1.41421356 && L < (1ull << 27)) L *= 2;
             if (L > N) L = N;
         }
         np.L = (uint32_t)L;

@@ -29,7 +29,10 @@ constexpr uint32_t DOMAIN_NOISE = 0x80000000u;
 constexpr uint32_t NZ_NONE = 1u;     // p == 0: no hits
 constexpr uint32_t NZ_ALL = 2u;      // p == 1: every trial hits
 constexpr uint32_t NZ_PREGEN = 4u;   // hits generated in the tile's pre-pass into a hit list
-constexpr int NZ_MAX_LIST = 8;      // distinct-position list; larger counts use selection sampling
+constexpr int NZ_MAX_LIST = 8;
+// frame kernel CTA size cap (launch bounds): 768 threads leaves 85 registers per
+// thread, enough for the noise sampler without spills
+constexpr int FRAME_MAX_THREADS = 768;      // distinct-position list; larger counts use selection sampling
 
 // One device op (32 bytes).  See DESIGN.md §3.
 //   GATE : count = apps, off -> targets (1 or 2 per app)

@@ -108,74 +108,66 @@ __device__ __forceinline__ void pattern_of(uint32_t ch, uint32_t pick, uint32_t&
     }
 }
 
-// Stream of 32-bit Philox words for one noise chunk: call j of chunk r in
-// global tile g of noise instruction `ordinal`.  The 4-word
-// buffer lives in registers (constant-index selects, no local memory).
-struct WordStream {
-    uint32_t r, g, dom, k0, k1, j;
-    uint32_t b0, b1, b2, b3;
-    int idx;
-    __device__ __forceinline__ WordStream(uint32_t r_, uint32_t g_, uint32_t ordinal, uint64_t seed)
-        : r(r_), g(g_), dom(DOMAIN_NOISE | ordinal), k0((uint32_t)seed), k1((uint32_t)(seed >> 32)),
-          j(0), b0(0), b1(0), b2(0), b3(0), idx(4) {}
-    __device__ __forceinline__ uint32_t next() {
-        if (idx == 4) {
-            b0 = j++; b1 = r; b2 = g; b3 = dom;
-            philox4x32_10(b0, b1, b2, b3, k0, k1);
-            idx = 0;
-        }
-        const uint32_t v = idx == 0 ? b0 : idx == 1 ? b1 : idx == 2 ? b2 : b3;
-        idx++;
-        return v;
-    }
-    __device__ __forceinline__ uint64_t next64() {
-        const uint32_t lo = next();
-        return ((uint64_t)next() << 32) | lo;
-    }
-};
+// Noise draws.  Every Philox block of a chunk has a fixed
+// counter (j, r, g, DOMAIN_NOISE | ordinal): j = 0 gives the chunk's hit count,
+// j = 1 + h + NZ_MAX_LIST * attempt gives hit h's position and Pauli pick, and
+// selection sampling (count > NZ_MAX_LIST, ~never) uses j = 2^31 + trial.  With
+// fixed counters all lanes of a warp run their Philox rounds converged.
+__device__ __forceinline__ void noise_block(uint32_t j, uint32_t r, uint32_t g, uint32_t ordinal,
+                                            uint64_t seed, uint32_t& w0, uint32_t& w1, uint32_t& w2,
+                                            uint32_t& w3) {
+    w0 = j; w1 = r; w2 = g; w3 = DOMAIN_NOISE | ordinal;
+    philox4x32_10(w0, w1, w2, w3, (uint32_t)seed, (uint32_t)(seed >> 32));
+}
 
 // Hits of one chunk: Binomial(len, p) count by threshold inversion, then
-// distinct uniform positions (selection sampling past NZ_MAX_LIST), each with
-// a uniform Pauli pattern pick.  emit(trial index within the op, pick).
+// distinct uniform positions (all positions redrawn while any two collide),
+// each with a uniform Pauli pattern pick.  emit(trial index within op, pick).
+// `sl` is this thread's NZ_MAX_LIST-entry scratch in shared memory (stride
+// `ss` words) holding (position << 4 | pick) while duplicates are checked.
 template <typename Emit>
 __device__ __forceinline__ void noise_chunk(const KParams& kp, const NoiseParam& np, uint32_t ordinal,
-                                            uint32_t r, uint32_t g, Emit emit) {
+                                            uint32_t r, uint32_t g, uint32_t* sl, int ss, Emit emit) {
     const uint32_t len = (r + 1 == np.nchunks) ? np.last_len : np.L;
     const uint32_t base = r * np.L;
-    WordStream ws(r, g, ordinal, kp.seed);
+    uint32_t w0, w1, w2, w3;
     if (np.flags & NZ_ALL) {
-        for (uint32_t i = 0; i < len; i++) emit(base + i, np.npat > 1 ? __umulhi(ws.next(), np.npat) : 0u);
+        for (uint32_t i = 0; i < len; i++) {
+            noise_block(0x80000000u + i, r, g, ordinal, kp.seed, w0, w1, w2, w3);
+            emit(base + i, np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
+        }
         return;
     }
     const bool full = len == np.L;
     const unsigned long long* tab =
         reinterpret_cast<const unsigned long long*>(kp.noise_tab) + (full ? np.tab_full : np.tab_last);
     const uint32_t tlen = full ? np.len_full : np.len_last;
-    const uint64_t u = ws.next64();
+    noise_block(0u, r, g, ordinal, kp.seed, w0, w1, w2, w3);
+    const uint64_t u = ((uint64_t)w1 << 32) | w0;
     uint32_t count = 0;
     while (count < tlen && u >= __ldg(tab + count)) count++;
     if (count == 0) return;
     if (count <= NZ_MAX_LIST) {
-        uint32_t sel[NZ_MAX_LIST];  // constant-indexed only: stays in registers
+        for (uint32_t attempt = 0;; attempt++) {
+            bool dup = false;
+            for (uint32_t h = 0; h < count; h++) {
+                noise_block(1u + h + NZ_MAX_LIST * attempt, r, g, ordinal, kp.seed, w0, w1, w2, w3);
+                const uint32_t pos = (uint32_t)__umul64hi(((uint64_t)w1 << 32) | w0, (uint64_t)len);
+                for (uint32_t q = 0; q < h; q++) dup |= (sl[q * ss] >> 4) == pos;
+                sl[h * ss] = (pos << 4) | (np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
+            }
+            if (!dup) break;
+        }
         for (uint32_t h = 0; h < count; h++) {
-            uint32_t pos;
-            bool dup;
-            do {
-                pos = (uint32_t)__umul64hi(ws.next64(), (uint64_t)len);
-                dup = false;
-#pragma unroll
-                for (uint32_t q = 0; q < NZ_MAX_LIST; q++) dup |= (q < h) && sel[q] == pos;
-            } while (dup);
-#pragma unroll
-            for (uint32_t q = 0; q < NZ_MAX_LIST; q++)
-                if (q == h) sel[q] = pos;
-            emit(base + pos, np.npat > 1 ? __umulhi(ws.next(), np.npat) : 0u);
+            const uint32_t e = sl[h * ss];
+            emit(base + (e >> 4), e & 15u);
         }
     } else {
         uint32_t needed = count;
         for (uint32_t i = 0; needed > 0; i++) {
-            if (__umul64hi(ws.next64(), (uint64_t)(len - i)) < needed) {
-                emit(base + i, np.npat > 1 ? __umulhi(ws.next(), np.npat) : 0u);
+            noise_block(0x80000000u + i, r, g, ordinal, kp.seed, w0, w1, w2, w3);
+            if (__umul64hi(((uint64_t)w1 << 32) | w0, (uint64_t)(len - i)) < needed) {
+                emit(base + i, np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
                 needed--;
             }
         }
@@ -233,7 +225,7 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 // (threads [t0, t0 + nthr) of the CTA).
 template <int W>
 __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uint32_t* ncnt,
-                                              uint64_t* hits, int t, int nthr) {
+                                              uint64_t* hits, int t, int nthr, uint32_t* sl, int ss) {
     constexpr uint32_t T = 32 * W;
     const int total = kp.pregen_chunks;
     const int per = (total + nthr - 1) / nthr;
@@ -254,7 +246,7 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
         const int ar = ch == CH_DEP2 ? 2 : 1;
         const int end = min(c1, (int)(np.chunk_base + np.nchunks));
         for (; c0 < end; c0++) {
-            noise_chunk(kp, np, ord, (uint32_t)(c0 - np.chunk_base), g,
+            noise_chunk(kp, np, ord, (uint32_t)(c0 - np.chunk_base), g, sl, ss,
                         [&](uint32_t trial, uint32_t pick) {
                             const uint32_t app = trial / T, s = trial % T;
                             uint32_t xm, zm;
@@ -276,7 +268,7 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
 // sample the noise of tile i+1 into the other hit-list buffer.  One full
 // __syncthreads per tile hands the buffers over.
 template <int W, bool RING_SMEM>
-__global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __grid_constant__ KParams kp) {
     constexpr int V = W >= 4 ? 4 : W;  // words per vector access
     constexpr int C = W / V;           // vector chunks per row
     constexpr int LC = Log2<C>::v;
@@ -290,6 +282,10 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
     uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // [2][num_noise]
     uint64_t* const hits0 = kp.hits_global + (size_t)blockIdx.x * 2 * kp.hit_capacity;
     const int tid = threadIdx.x;
+    // per-thread duplicate-check scratch of the noise sampler: [NZ_MAX_LIST][blockDim]
+    uint32_t* const nscr = ncnt0 + 2 * kp.num_noise;
+    uint32_t* const sl = nscr + tid;
+    const int ss = blockDim.x;
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
     const int nprod = pregen ? kp.producers : 0;
     const int nth = blockDim.x - nprod;  // consumer threads
@@ -302,7 +298,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
     if (pregen && (int64_t)blockIdx.x < kp.n_tiles) {
         for (int i = tid; i < kp.num_noise; i += blockDim.x) ncnt0[i] = 0u;
         __syncthreads();
-        noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid, blockDim.x);
+        noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid, blockDim.x, sl, ss);
     }
     __syncthreads();
 
@@ -321,7 +317,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
                 for (int i = pt; i < kp.num_noise; i += nprod) ncn[i] = 0u;
                 asm volatile("bar.sync 2, %0;" ::"r"(nprod) : "memory");
                 noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + (uint64_t)nt), ncn,
-                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt, nprod);
+                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt, nprod, sl, ss);
             }
         } else {
             // ---- consumers: FrameBatch.__init__: x = 0, z = coins (frame_sim.py:36-39) ----
@@ -468,7 +464,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
                                 apply_entry<W>(X, Z, hits[oc + i]);
                         } else {
                             for (uint32_t r = tid; r < __ldg(&npp->nchunks); r += nth)
-                                noise_chunk(kp, *npp, ob, r, g, [&](uint32_t trial, uint32_t pick) {
+                                noise_chunk(kp, *npp, ob, r, g, sl, ss, [&](uint32_t trial, uint32_t pick) {
                                     apply_hit<W>(X, Z, tg, code, ar, trial, pick);
                                 });
                         }
@@ -482,7 +478,7 @@ __global__ void __launch_bounds__(1024, 1) frame_kernel(const __grid_constant__ 
                     if (np.flags & NZ_NONE) break;
                     // inline sampling (large-p ops)
                     for (uint32_t r = tid; r < np.nchunks; r += nth)
-                        noise_chunk(kp, np, ob, r, g, [&](uint32_t trial, uint32_t pick) {
+                        noise_chunk(kp, np, ob, r, g, sl, ss, [&](uint32_t trial, uint32_t pick) {
                             apply_hit<W>(X, Z, tg, code, ar, trial, pick);
                         });
                     break;

@@ -49,6 +49,9 @@ def main():
         ("nn_no_coins", {"debug_skip": 3 | 4}),
         ("producers_only", {"debug_skip": 1 | 4 | 8 | 16 | 32}),
         ("producers_only_p512", {"debug_skip": 1 | 4 | 8 | 16 | 32, "producer_threads": 512}),
+        ("prod128", {"producer_threads": 128}),
+        ("prod384", {"producer_threads": 384}),
+        ("thr512_prod128", {"threads": 512, "producer_threads": 128}),
     ]
     if a.variants:
         keep = set(a.variants.split(","))

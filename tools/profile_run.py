@@ -18,6 +18,8 @@ def main():
     ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--mode", default="b8")
     ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--debug-skip", type=int, default=0)
+    ap.add_argument("--producers", type=int, default=0)
     a = ap.parse_args()
     import torch
 
@@ -25,7 +27,8 @@ def main():
     from paper_2103_02202_b200.sampler import compile_detector_sampler
 
     ds = compile_detector_sampler(gen.config_circuit(a.config), words_per_tile=a.words,
-                                  ring_in_smem=a.ring, threads=a.threads)
+                                  ring_in_smem=a.ring, threads=a.threads,
+                                  debug_skip=a.debug_skip, producer_threads=a.producers)
     nb = (ds.num_columns + 7) // 8
     pitch = (nb + 31) // 32 * 32
     if a.mode == "b8":
