@@ -95,8 +95,7 @@ static inline uint64_t umul64hi(uint64_t a, uint64_t b) {
 }
 static inline uint32_t umulhi32(uint32_t a, uint32_t b) { return (uint32_t)(((uint64_t)a * b) >> 32); }
 
-/* Philox block j of chunk r: j = 0 count, j = 1 + h + 8*attempt
- * hit h, j = 2^31 + i selection sampling / p == 1 trials. */
+/* Philox block j of chunk r. */
 static inline void noise_block(uint32_t j, uint32_t r, uint32_t g, uint32_t ordinal, uint64_t seed,
                                uint32_t w[4]) {
     uint32_t ctr[4] = {j, r, g, 0x80000000u | ordinal};
@@ -104,48 +103,61 @@ static inline void noise_block(uint32_t j, uint32_t r, uint32_t g, uint32_t ordi
     orc_philox4x32_10(ctr, key, w);
 }
 
+/* Word pair k of chunk r: pair 0 = block 0 (w2, w3); pair k >= 1 = block
+ * (k+1)/2, (w0, w1) for odd k, (w2, w3) for even k. */
+static inline void noise_pair(uint32_t k, uint32_t r, uint32_t g, uint32_t ordinal, uint64_t seed,
+                              uint32_t* a, uint32_t* b) {
+    uint32_t w[4];
+    noise_block(k == 0 ? 0u : (k + 1) >> 1, r, g, ordinal, seed, w);
+    if (k == 0 || !(k & 1u)) { *a = w[2]; *b = w[3]; }
+    else { *a = w[0]; *b = w[1]; }
+}
+
 /* hits of chunk r: emit(trial within the op, pattern pick) */
 typedef void (*emit_fn)(void* ctx, uint32_t trial, uint32_t pick);
 static void noise_chunk(const orc_noise* np, const uint64_t* tabs, uint64_t seed, uint32_t ordinal,
                         uint32_t r, uint32_t g, emit_fn emit, void* ctx) {
-    const uint32_t len = (r + 1 == np->nchunks) ? np->last_len : np->L;
-    const uint32_t base = r * np->L;
+    const uint32_t L = np->L;
+    uint32_t lg = 0;
+    while ((1u << lg) < L) lg++;
+    const uint32_t base = r * L;
+    const uint32_t valid = (r + 1 == np->nchunks) ? np->last_len : L;
     uint32_t w[4];
     if (np->flags & NZ_ALL) {
-        for (uint32_t i = 0; i < len; i++) {
+        for (uint32_t i = 0; i < valid; i++) {
             noise_block(0x80000000u + i, r, g, ordinal, seed, w);
             emit(ctx, base + i, np->npat > 1 ? umulhi32(w[2], np->npat) : 0u);
         }
         return;
     }
-    const int full = len == np->L;
-    const uint64_t* tab = tabs + (full ? np->tab_full : np->tab_last);
-    const uint32_t tlen = full ? np->len_full : np->len_last;
+    const uint64_t* tab = tabs + np->tab_full;
     noise_block(0u, r, g, ordinal, seed, w);
     const uint64_t u = ((uint64_t)w[1] << 32) | w[0];
     uint32_t count = 0;
-    while (count < tlen && u >= tab[count]) count++;
+    while (count < np->len_full && u >= tab[count]) count++;
     if (count == 0) return;
     if (count <= NZ_MAX_LIST) {
         uint32_t pos[NZ_MAX_LIST], pick[NZ_MAX_LIST];
         for (uint32_t attempt = 0;; attempt++) {
             for (uint32_t h = 0; h < count; h++) {
-                noise_block(1u + h + NZ_MAX_LIST * attempt, r, g, ordinal, seed, w);
-                pos[h] = (uint32_t)umul64hi(((uint64_t)w[1] << 32) | w[0], len);
-                pick[h] = np->npat > 1 ? umulhi32(w[2], np->npat) : 0u;
+                uint32_t a, b;
+                noise_pair(attempt * NZ_MAX_LIST + h, r, g, ordinal, seed, &a, &b);
+                pos[h] = lg ? (a >> (32 - lg)) : 0u;
+                pick[h] = np->npat > 1 ? umulhi32(b, np->npat) : 0u;
             }
             int dup = 0;
             for (uint32_t h = 1; h < count; h++)
                 for (uint32_t q = 0; q < h; q++) dup |= pos[h] == pos[q];
             if (!dup) break;
         }
-        for (uint32_t h = 0; h < count; h++) emit(ctx, base + pos[h], pick[h]);
+        for (uint32_t h = 0; h < count; h++)
+            if (pos[h] < valid) emit(ctx, base + pos[h], pick[h]);
     } else {
         uint32_t needed = count;
         for (uint32_t i = 0; needed > 0; i++) {
             noise_block(0x80000000u + i, r, g, ordinal, seed, w);
-            if (umul64hi(((uint64_t)w[1] << 32) | w[0], (uint64_t)(len - i)) < needed) {
-                emit(ctx, base + i, np->npat > 1 ? umulhi32(w[2], np->npat) : 0u);
+            if (umul64hi(((uint64_t)w[1] << 32) | w[0], (uint64_t)(L - i)) < needed) {
+                if (i < valid) emit(ctx, base + i, np->npat > 1 ? umulhi32(w[2], np->npat) : 0u);
                 needed--;
             }
         }

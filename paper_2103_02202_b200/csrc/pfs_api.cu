@@ -156,7 +156,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         return fail(PFS_E_INVALID, "frame table of " + std::to_string(num_qubits) +
                                        " qubits does not fit one CTA's shared memory");
     }
-    const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 2.0;
+    const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 1.0;
     try {
         reorder_for_banks(pg->hp, pg->cfg.W);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);

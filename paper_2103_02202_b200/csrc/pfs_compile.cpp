@@ -418,31 +418,26 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
         uint64_t L;
         if (p >= 1.0) {
             np.flags = NZ_ALL;
-            L = std::min<uint64_t>(N, 1024);  // positions must stay below 2^28
+            L = 1;
+            while (L < N && L < 1024) L *= 2;  // power of two; positions stay below 2^28
         } else {
             // power of two nearest (in ratio) to target_hits / p trials
             double want = target_hits / p;
             L = 1;
             while ((double)(L * 2) <= want * 1.41421356 && L < (1ull << 27)) L *= 2;
-            if (L > N) L = N;
+            while (L > 1 && L / 2 >= N) L /= 2;  // no chunk longer than needed
         }
         np.L = (uint32_t)L;
         np.nchunks = (uint32_t)((N + L - 1) / L);
-        np.last_len = (uint32_t)(N - (uint64_t)(np.nchunks - 1) * L);
+        np.last_len = (uint32_t)(N - (uint64_t)(np.nchunks - 1) * L);  // real trials in the last chunk
         if (!(np.flags & NZ_ALL)) {
+            // every chunk draws from Binomial(L, p): trials past N are virtual and dropped
             auto tf = binomial_thresholds(L, p);
             np.tab_full = (uint32_t)hp.noise_tab.size();
             np.len_full = (uint32_t)tf.size();
+            np.tab_last = np.tab_full;
+            np.len_last = np.len_full;
             hp.noise_tab.insert(hp.noise_tab.end(), tf.begin(), tf.end());
-            if (np.last_len != L) {
-                auto tl = binomial_thresholds(np.last_len, p);
-                np.tab_last = (uint32_t)hp.noise_tab.size();
-                np.len_last = (uint32_t)tl.size();
-                hp.noise_tab.insert(hp.noise_tab.end(), tl.begin(), tl.end());
-            } else {
-                np.tab_last = np.tab_full;
-                np.len_last = np.len_full;
-            }
         }
         const double E = (double)N * p;
         if (p < 0.25 && E <= 16384.0 && N < (1ull << 28)) {

@@ -108,11 +108,17 @@ __device__ __forceinline__ void pattern_of(uint32_t ch, uint32_t pick, uint32_t&
     }
 }
 
-// Noise draws.  Every Philox block of a chunk has a fixed
-// counter (j, r, g, DOMAIN_NOISE | ordinal): j = 0 gives the chunk's hit count,
-// j = 1 + h + NZ_MAX_LIST * attempt gives hit h's position and Pauli pick, and
-// selection sampling (count > NZ_MAX_LIST, ~never) uses j = 2^31 + trial.  With
-// fixed counters all lanes of a warp run their Philox rounds converged.
+// Noise draws.  A chunk is L = 2^lg consecutive trials of the
+// op (trials past the op's end are virtual and dropped).  Philox block j of
+// chunk r has counter (j, r, g, DOMAIN_NOISE | ordinal):
+//   block 0        : w0,w1 -> 64-bit uniform for the Binomial(L, p) count,
+//                    w2,w3 -> word pair 0;
+//   block b >= 1   : word pairs 2b-1 (w0,w1) and 2b (w2,w3).
+// Hit h of attempt a uses pair a*NZ_MAX_LIST + h: position = top lg bits of the
+// first word (exactly uniform), Pauli pick = mulhi(second word, npat).  All
+// positions are redrawn (next attempt) while any two coincide.  Counts above
+// NZ_MAX_LIST (~1e-6 per chunk) use selection sampling with block 2^31 + i per
+// trial, as does p == 1.  In the common case a chunk costs one Philox block.
 __device__ __forceinline__ void noise_block(uint32_t j, uint32_t r, uint32_t g, uint32_t ordinal,
                                             uint64_t seed, uint32_t& w0, uint32_t& w1, uint32_t& w2,
                                             uint32_t& w3) {
@@ -120,54 +126,63 @@ __device__ __forceinline__ void noise_block(uint32_t j, uint32_t r, uint32_t g, 
     philox4x32_10(w0, w1, w2, w3, (uint32_t)seed, (uint32_t)(seed >> 32));
 }
 
-// Hits of one chunk: Binomial(len, p) count by threshold inversion, then
-// distinct uniform positions (all positions redrawn while any two collide),
-// each with a uniform Pauli pattern pick.  emit(trial index within op, pick).
-// `sl` is this thread's NZ_MAX_LIST-entry scratch in shared memory (stride
-// `ss` words) holding (position << 4 | pick) while duplicates are checked.
 template <typename Emit>
 __device__ __forceinline__ void noise_chunk(const KParams& kp, const NoiseParam& np, uint32_t ordinal,
                                             uint32_t r, uint32_t g, uint32_t* sl, int ss, Emit emit) {
-    const uint32_t len = (r + 1 == np.nchunks) ? np.last_len : np.L;
-    const uint32_t base = r * np.L;
+    const uint32_t L = np.L;
+    const uint32_t lg = 31u - __clz(L);
+    const uint32_t base = r * L;
+    const uint32_t valid = (r + 1 == np.nchunks) ? np.last_len : L;  // real trials in this chunk
     uint32_t w0, w1, w2, w3;
     if (np.flags & NZ_ALL) {
-        for (uint32_t i = 0; i < len; i++) {
+        for (uint32_t i = 0; i < valid; i++) {
             noise_block(0x80000000u + i, r, g, ordinal, kp.seed, w0, w1, w2, w3);
             emit(base + i, np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
         }
         return;
     }
-    const bool full = len == np.L;
-    const unsigned long long* tab =
-        reinterpret_cast<const unsigned long long*>(kp.noise_tab) + (full ? np.tab_full : np.tab_last);
-    const uint32_t tlen = full ? np.len_full : np.len_last;
+    const unsigned long long* tab = reinterpret_cast<const unsigned long long*>(kp.noise_tab) + np.tab_full;
     noise_block(0u, r, g, ordinal, kp.seed, w0, w1, w2, w3);
     const uint64_t u = ((uint64_t)w1 << 32) | w0;
     uint32_t count = 0;
-    while (count < tlen && u >= __ldg(tab + count)) count++;
+    while (count < np.len_full && u >= __ldg(tab + count)) count++;
     if (count == 0) return;
+    const uint32_t sh = 32u - lg;
+    if (count == 1) {  // the common case: block 0 already holds the hit
+        const uint32_t pos = lg ? (w2 >> sh) : 0u;
+        if (pos < valid) emit(base + pos, np.npat > 1 ? __umulhi(w3, np.npat) : 0u);
+        return;
+    }
     if (count <= NZ_MAX_LIST) {
         for (uint32_t attempt = 0;; attempt++) {
             bool dup = false;
+            uint32_t blk = 0xFFFFFFFFu;
             for (uint32_t h = 0; h < count; h++) {
-                noise_block(1u + h + NZ_MAX_LIST * attempt, r, g, ordinal, kp.seed, w0, w1, w2, w3);
-                const uint32_t pos = (uint32_t)__umul64hi(((uint64_t)w1 << 32) | w0, (uint64_t)len);
+                const uint32_t k = attempt * NZ_MAX_LIST + h;
+                uint32_t a, b;
+                if (k == 0) { a = w2; b = w3; }
+                else {
+                    const uint32_t need = (k + 1) >> 1;
+                    if (need != blk) { noise_block(need, r, g, ordinal, kp.seed, w0, w1, w2, w3); blk = need; }
+                    if (k & 1u) { a = w0; b = w1; } else { a = w2; b = w3; }
+                }
+                const uint32_t pos = lg ? (a >> sh) : 0u;
                 for (uint32_t q = 0; q < h; q++) dup |= (sl[q * ss] >> 4) == pos;
-                sl[h * ss] = (pos << 4) | (np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
+                sl[h * ss] = (pos << 4) | (np.npat > 1 ? __umulhi(b, np.npat) : 0u);
             }
             if (!dup) break;
+            // block 0's pair must be recomputed for nothing: attempts > 0 never use pair 0
         }
         for (uint32_t h = 0; h < count; h++) {
             const uint32_t e = sl[h * ss];
-            emit(base + (e >> 4), e & 15u);
+            if ((e >> 4) < valid) emit(base + (e >> 4), e & 15u);
         }
     } else {
         uint32_t needed = count;
         for (uint32_t i = 0; needed > 0; i++) {
             noise_block(0x80000000u + i, r, g, ordinal, kp.seed, w0, w1, w2, w3);
-            if (__umul64hi(((uint64_t)w1 << 32) | w0, (uint64_t)(len - i)) < needed) {
-                emit(base + i, np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
+            if (__umul64hi(((uint64_t)w1 << 32) | w0, (uint64_t)(L - i)) < needed) {
+                if (i < valid) emit(base + i, np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
                 needed--;
             }
         }

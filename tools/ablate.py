@@ -36,7 +36,8 @@ def main():
         ("W8_global", {"words_per_tile": 8, "ring_in_smem": 0}),
         ("W8_512thr", {"threads": 512}),
         ("W4_smem", {"words_per_tile": 4, "ring_in_smem": 1}),
-        ("hits4", {"noise_target_hits": 4.0}),
+        ("hits2", {"noise_target_hits": 2.0}),
+        ("hits05", {"noise_target_hits": 0.5}),
         ("W16_prod128", {"words_per_tile": 16, "ring_in_smem": 0, "producer_threads": 128}),
         ("W16_prod384", {"words_per_tile": 16, "ring_in_smem": 0, "producer_threads": 384}),
         ("W16_hits4", {"words_per_tile": 16, "ring_in_smem": 0, "noise_target_hits": 4.0}),
