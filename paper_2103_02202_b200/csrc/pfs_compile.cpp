@@ -445,8 +445,9 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
             np.cap = (uint32_t)std::ceil(E + 8.0 * std::sqrt(E) + 16.0);
             np.cap_base = (uint32_t)hp.hit_capacity;
             hp.hit_capacity += np.cap;
+            // pre-pass work items are 32-chunk blocks (one warp each)
             np.chunk_base = (uint32_t)hp.pregen_chunks;
-            hp.pregen_chunks += np.nchunks;
+            hp.pregen_chunks += (np.nchunks + 31) / 32;
             hp.pregen_ops.push_back((uint32_t)j);
         }
     }

@@ -71,7 +71,7 @@ struct NoiseParam {
     uint32_t cap;
     uint32_t flags;
     uint32_t npat;
-    uint32_t chunk_base; // prefix over pre-generated ops (pre-pass work index)
+    uint32_t chunk_base; // first pre-pass work item (32-chunk block) of this op
 };
 static_assert(sizeof(NoiseParam) == 48, "NoiseParam is 48 bytes");
 
@@ -99,7 +99,7 @@ struct HostProgram {
     std::vector<NoiseParam> noise;
     std::vector<uint64_t> noise_tab;
     std::vector<uint32_t> pregen_ops;   // noise ordinals with NZ_PREGEN, in order
-    int64_t pregen_chunks = 0;          // total pre-pass chunks per tile
+    int64_t pregen_chunks = 0;          // total pre-pass work items (32-chunk blocks) per tile
     int64_t hit_capacity = 0;           // hit-list entries per CTA (per buffer)
     uint32_t first_pregen = NO_SLOT;
     uint32_t first_cap_base = 0;

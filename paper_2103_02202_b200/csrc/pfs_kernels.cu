@@ -236,42 +236,134 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
     asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
 }
 
-// Sample the pre-generated noise ops of global tile g into hit lists
-// (threads [t0, t0 + nthr) of the CTA).
+// Sample the pre-generated noise ops of global tile g into hit lists.
+// Warp-cooperative: a work item is 32 consecutive chunks of one op, lane l
+// owns chunk 32*item + l, so the Philox block-0 draw (count + first hit) runs
+// converged across the warp; hit-list slots are reserved with one atomic per
+// warp.  Same draws as noise_chunk.
 template <int W>
 __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uint32_t* ncnt,
-                                              uint64_t* hits, int t, int nthr, uint32_t* sl, int ss) {
+                                              uint64_t* hits, int warp, int nwarps, uint32_t* sl,
+                                              int ss) {
     constexpr uint32_t T = 32 * W;
-    const int total = kp.pregen_chunks;
-    const int per = (total + nthr - 1) / nthr;
-    int c0 = t * per;
-    const int c1 = min(total, c0 + per);
-    if (c0 >= c1) return;
-    int lo = 0, hi = kp.num_pregen - 1;  // last op with chunk_base <= c0
-    while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if ((int)__ldg(&kp.noise[__ldg(kp.pregen_ops + mid)].chunk_base) <= c0) lo = mid;
-        else hi = mid - 1;
-    }
-    for (int k = lo; c0 < c1; k++) {
-        const uint32_t ord = __ldg(kp.pregen_ops + k);
-        const NoiseParam np = kp.noise[ord];
-        const uint32_t* tg = kp.targets + __ldg(&kp.noise_off[ord]);
-        const uint32_t ch = __ldg(&kp.noise_ch[ord]);
-        const int ar = ch == CH_DEP2 ? 2 : 1;
-        const int end = min(c1, (int)(np.chunk_base + np.nchunks));
-        for (; c0 < end; c0++) {
-            noise_chunk(kp, np, ord, (uint32_t)(c0 - np.chunk_base), g, sl, ss,
-                        [&](uint32_t trial, uint32_t pick) {
-                            const uint32_t app = trial / T, s = trial % T;
-                            uint32_t xm, zm;
-                            pattern_of(ch, pick, xm, zm);
-                            const uint32_t q0 = __ldg(tg + app * ar);
-                            const uint32_t q1 = ar == 2 ? __ldg(tg + app * ar + 1) : 0u;
-                            const uint32_t slot = atomicAdd(ncnt + ord, 1u);
-                            if (slot < np.cap)
-                                hits[np.cap_base + slot] = make_hit(q0, q1, s >> 5, s & 31, xm, zm);
-                        });
+    const int lane = threadIdx.x & 31;
+    const int total = kp.pregen_chunks;  // work items (32-chunk blocks) per tile
+    int k = 0;
+    uint32_t ord = 0, item_base = 0, next_base = 0, ch = 0, tab0 = 0;
+    NoiseParam np{};
+    unsigned long long t0 = 0, t1 = 0;
+    const uint32_t* tg = nullptr;
+    int ar = 1;
+    bool loaded = false;
+    for (int item = warp; item < total; item += nwarps) {
+        // advance the op cursor (items visit ops in increasing order)
+        while (!loaded || (uint32_t)item >= next_base) {
+            if (loaded) k++;
+            ord = __ldg(kp.pregen_ops + k);
+            np = kp.noise[ord];
+            item_base = np.chunk_base;
+            next_base = item_base + ((np.nchunks + 31u) >> 5);
+            ch = __ldg(&kp.noise_ch[ord]);
+            ar = ch == CH_DEP2 ? 2 : 1;
+            tg = kp.targets + __ldg(&kp.noise_off[ord]);
+            const unsigned long long* tab = reinterpret_cast<const unsigned long long*>(kp.noise_tab) + np.tab_full;
+            t0 = np.len_full > 0 ? __ldg(tab) : ~0ull;
+            t1 = np.len_full > 1 ? __ldg(tab + 1) : ~0ull;
+            loaded = true;
+        }
+        (void)tab0;
+        const uint32_t r = ((uint32_t)item - item_base) * 32u + (uint32_t)lane;
+        const bool valid = r < np.nchunks;
+        const uint32_t L = np.L;
+        const uint32_t lg = 31u - __clz(L);
+        const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
+        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
+        uint32_t count = 0;
+        if (valid) {
+            noise_block(0u, r, g, ord, kp.seed, w0, w1, w2, w3);
+            const unsigned long long u = ((unsigned long long)w1 << 32) | w0;
+            if (u >= t0) {
+                count = 1;
+                if (u >= t1) {
+                    count = 2;
+                    const unsigned long long* tab =
+                        reinterpret_cast<const unsigned long long*>(kp.noise_tab) + np.tab_full;
+                    while (count < np.len_full && u >= __ldg(tab + count)) count++;
+                }
+            }
+        }
+        // positions/picks: count 1 straight from block 0; more hits via pairs
+        uint32_t e0 = 0;
+        uint32_t nreal = 0;
+        const uint32_t sh = 32u - lg;
+        if (count == 1) {
+            const uint32_t pos = lg ? (w2 >> sh) : 0u;
+            e0 = (pos << 4) | (np.npat > 1 ? __umulhi(w3, np.npat) : 0u);
+            nreal = pos < vlen ? 1u : 0u;
+        } else if (count > 1 && count <= (uint32_t)NZ_MAX_LIST) {
+            for (uint32_t attempt = 0;; attempt++) {
+                bool dup = false;
+                uint32_t blk = 0xFFFFFFFFu;
+                uint32_t b0 = w0, b1 = w1, b2 = w2, b3 = w3;
+                for (uint32_t h = 0; h < count; h++) {
+                    const uint32_t kk = attempt * NZ_MAX_LIST + h;
+                    uint32_t x, y;
+                    if (kk == 0) { x = w2; y = w3; }
+                    else {
+                        const uint32_t need = (kk + 1) >> 1;
+                        if (need != blk) { noise_block(need, r, g, ord, kp.seed, b0, b1, b2, b3); blk = need; }
+                        if (kk & 1u) { x = b0; y = b1; } else { x = b2; y = b3; }
+                    }
+                    const uint32_t pos = lg ? (x >> sh) : 0u;
+                    for (uint32_t q = 0; q < h; q++) dup |= (sl[q * ss] >> 4) == pos;
+                    sl[h * ss] = (pos << 4) | (np.npat > 1 ? __umulhi(y, np.npat) : 0u);
+                }
+                if (!dup) break;
+            }
+            for (uint32_t h = 0; h < count; h++) nreal += (sl[h * ss] >> 4) < vlen ? 1u : 0u;
+        }
+        // rare: count > NZ_MAX_LIST -> selection sampling, emitted directly below
+        const bool big = count > (uint32_t)NZ_MAX_LIST;
+        // warp-aggregated slot reservation
+        uint32_t pre = nreal;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+            if (lane >= d) pre += v;
+        }
+        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, pre, 31);
+        uint32_t base = 0;
+        if (lane == 0 && tot) base = atomicAdd(ncnt + ord, tot);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0) + pre - nreal;
+        auto write = [&](uint32_t slot, uint32_t trial, uint32_t pick) {
+            if (slot >= np.cap) return;
+            const uint32_t app = trial / T, s = trial % T;
+            uint32_t xm, zm;
+            pattern_of(ch, pick, xm, zm);
+            const uint32_t q0 = __ldg(tg + app * ar);
+            const uint32_t q1 = ar == 2 ? __ldg(tg + app * ar + 1) : 0u;
+            hits[np.cap_base + slot] = make_hit(q0, q1, s >> 5, s & 31, xm, zm);
+        };
+        if (count == 1) {
+            if (nreal) write(base, r * L + (e0 >> 4), e0 & 15u);
+        } else if (count > 1 && !big) {
+            uint32_t o = 0;
+            for (uint32_t h = 0; h < count; h++) {
+                const uint32_t e = sl[h * ss];
+                if ((e >> 4) < vlen) write(base + o++, r * L + (e >> 4), e & 15u);
+            }
+        } else if (big) {
+            uint32_t needed = count;
+            for (uint32_t i = 0; needed > 0; i++) {
+                noise_block(0x80000000u + i, r, g, ord, kp.seed, w0, w1, w2, w3);
+                if (__umul64hi(((uint64_t)w1 << 32) | w0, (uint64_t)(L - i)) < needed) {
+                    if (i < vlen) {
+                        const uint32_t slot = atomicAdd(ncnt + ord, 1u);
+                        write(slot, r * L + i, np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
+                    }
+                    needed--;
+                }
+            }
         }
     }
 }
@@ -313,7 +405,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     if (pregen && (int64_t)blockIdx.x < kp.n_tiles) {
         for (int i = tid; i < kp.num_noise; i += blockDim.x) ncnt0[i] = 0u;
         __syncthreads();
-        noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid, blockDim.x, sl, ss);
+        noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid >> 5,
+                         blockDim.x >> 5, sl, ss);
     }
     __syncthreads();
 
@@ -332,7 +425,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 for (int i = pt; i < kp.num_noise; i += nprod) ncn[i] = 0u;
                 asm volatile("bar.sync 2, %0;" ::"r"(nprod) : "memory");
                 noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + (uint64_t)nt), ncn,
-                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt, nprod, sl, ss);
+                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt >> 5, nprod >> 5, sl, ss);
             }
         } else {
             // ---- consumers: FrameBatch.__init__: x = 0, z = coins (frame_sim.py:36-39) ----
