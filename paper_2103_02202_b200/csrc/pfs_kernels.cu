@@ -244,7 +244,7 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 template <int W>
 __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uint32_t* ncnt,
                                               uint64_t* hits, int warp, int nwarps, uint32_t* sl,
-                                              int ss) {
+                                              int ss, uint32_t* wscr) {
     constexpr uint32_t T = 32 * W;
     const int lane = threadIdx.x & 31;
     const int total = kp.pregen_chunks;  // work items (32-chunk blocks) per tile
@@ -292,7 +292,8 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
                 }
             }
         }
-        // positions/picks: count 1 straight from block 0; more hits via pairs
+        // positions/picks: count 1 straight from block 0; lanes with 2..NZ_MAX_LIST
+        // hits need blocks 1..count/2, computed cooperatively by the whole warp
         uint32_t e0 = 0;
         uint32_t nreal = 0;
         const uint32_t sh = 32u - lg;
@@ -300,27 +301,73 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
             const uint32_t pos = lg ? (w2 >> sh) : 0u;
             e0 = (pos << 4) | (np.npat > 1 ? __umulhi(w3, np.npat) : 0u);
             nreal = pos < vlen ? 1u : 0u;
-        } else if (count > 1 && count <= (uint32_t)NZ_MAX_LIST) {
-            for (uint32_t attempt = 0;; attempt++) {
+        }
+        {
+            const uint32_t nb = (count > 1 && count <= (uint32_t)NZ_MAX_LIST) ? (count >> 1) : 0u;
+            uint32_t pb = nb;  // inclusive prefix of extra blocks
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pb, d);
+                if (lane >= d) pb += v;
+            }
+            const uint32_t ntask = __shfl_sync(0xFFFFFFFFu, pb, 31);
+            const uint32_t first = pb - nb;
+            for (uint32_t t0 = 0; t0 < ntask; t0 += 32) {
+                const uint32_t task = t0 + lane;
+                // owner lane of this task: largest lane with first(lane) <= task
+                uint32_t owner = 0;
+#pragma unroll
+                for (int q = 0; q < 32; q++) {
+                    const uint32_t fq = __shfl_sync(0xFFFFFFFFu, first, q);
+                    const uint32_t nq = __shfl_sync(0xFFFFFFFFu, nb, q);
+                    if (nq && task >= fq) owner = q;
+                }
+                const uint32_t of = __shfl_sync(0xFFFFFFFFu, first, owner);
+                if (task < ntask) {
+                    const uint32_t orr = ((uint32_t)item - item_base) * 32u + owner;
+                    uint32_t b0, b1, b2, b3;
+                    noise_block(1u + (task - of), orr, g, ord, kp.seed, b0, b1, b2, b3);
+                    uint4* ws = reinterpret_cast<uint4*>(wscr) + (task & 31u);
+                    *ws = make_uint4(b0, b1, b2, b3);
+                }
+                __syncwarp();
+                // owners consume the blocks of this round that belong to them
+                if (nb) {
+                    for (uint32_t bi = 0; bi < nb; bi++) {
+                        const uint32_t tk = first + bi;
+                        if (tk < t0 || tk >= t0 + 32) continue;
+                        const uint4 blk = reinterpret_cast<const uint4*>(wscr)[tk & 31u];
+                        // block bi+1 holds pairs 2bi+1 (x,y) and 2bi+2 (z,w)
+                        const uint32_t h1 = 2 * bi + 1, h2 = 2 * bi + 2;
+                        if (h1 < count) sl[h1 * ss] = ((lg ? (blk.x >> sh) : 0u) << 4) |
+                                                      (np.npat > 1 ? __umulhi(blk.y, np.npat) : 0u);
+                        if (h2 < count) sl[h2 * ss] = ((lg ? (blk.z >> sh) : 0u) << 4) |
+                                                      (np.npat > 1 ? __umulhi(blk.w, np.npat) : 0u);
+                    }
+                }
+                __syncwarp();
+            }
+            if (nb) {
+                sl[0] = ((lg ? (w2 >> sh) : 0u) << 4) | (np.npat > 1 ? __umulhi(w3, np.npat) : 0u);
                 bool dup = false;
-                uint32_t blk = 0xFFFFFFFFu;
-                uint32_t b0 = w0, b1 = w1, b2 = w2, b3 = w3;
-                for (uint32_t h = 0; h < count; h++) {
-                    const uint32_t kk = attempt * NZ_MAX_LIST + h;
-                    uint32_t x, y;
-                    if (kk == 0) { x = w2; y = w3; }
-                    else {
+                for (uint32_t h = 1; h < count; h++)
+                    for (uint32_t q = 0; q < h; q++) dup |= (sl[h * ss] >> 4) == (sl[q * ss] >> 4);
+                for (uint32_t attempt = 1; dup; attempt++) {  // rare: redraw every position
+                    dup = false;
+                    uint32_t blk = 0xFFFFFFFFu;
+                    uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+                    for (uint32_t h = 0; h < count; h++) {
+                        const uint32_t kk = attempt * NZ_MAX_LIST + h;
                         const uint32_t need = (kk + 1) >> 1;
                         if (need != blk) { noise_block(need, r, g, ord, kp.seed, b0, b1, b2, b3); blk = need; }
-                        if (kk & 1u) { x = b0; y = b1; } else { x = b2; y = b3; }
+                        const uint32_t x = (kk & 1u) ? b0 : b2, y = (kk & 1u) ? b1 : b3;
+                        const uint32_t pos = lg ? (x >> sh) : 0u;
+                        for (uint32_t q = 0; q < h; q++) dup |= (sl[q * ss] >> 4) == pos;
+                        sl[h * ss] = (pos << 4) | (np.npat > 1 ? __umulhi(y, np.npat) : 0u);
                     }
-                    const uint32_t pos = lg ? (x >> sh) : 0u;
-                    for (uint32_t q = 0; q < h; q++) dup |= (sl[q * ss] >> 4) == pos;
-                    sl[h * ss] = (pos << 4) | (np.npat > 1 ? __umulhi(y, np.npat) : 0u);
                 }
-                if (!dup) break;
+                for (uint32_t h = 0; h < count; h++) nreal += (sl[h * ss] >> 4) < vlen ? 1u : 0u;
             }
-            for (uint32_t h = 0; h < count; h++) nreal += (sl[h * ss] >> 4) < vlen ? 1u : 0u;
         }
         // rare: count > NZ_MAX_LIST -> selection sampling, emitted directly below
         const bool big = count > (uint32_t)NZ_MAX_LIST;
@@ -393,6 +440,9 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     uint32_t* const nscr = ncnt0 + 2 * kp.num_noise;
     uint32_t* const sl = nscr + tid;
     const int ss = blockDim.x;
+    // per-warp scratch (32 Philox blocks) of the cooperative noise pre-pass, 16-byte aligned
+    uint32_t* const wscr = reinterpret_cast<uint32_t*>(
+        (reinterpret_cast<uintptr_t>(nscr + NZ_MAX_LIST * blockDim.x) + 15) & ~(uintptr_t)15) + ((tid >> 5) << 7);
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
     const int nprod = pregen ? kp.producers : 0;
     const int nth = blockDim.x - nprod;  // consumer threads
@@ -406,7 +456,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
         for (int i = tid; i < kp.num_noise; i += blockDim.x) ncnt0[i] = 0u;
         __syncthreads();
         noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid >> 5,
-                         blockDim.x >> 5, sl, ss);
+                         blockDim.x >> 5, sl, ss, wscr);
     }
     __syncthreads();
 
@@ -425,7 +475,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 for (int i = pt; i < kp.num_noise; i += nprod) ncn[i] = 0u;
                 asm volatile("bar.sync 2, %0;" ::"r"(nprod) : "memory");
                 noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + (uint64_t)nt), ncn,
-                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt >> 5, nprod >> 5, sl, ss);
+                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt >> 5, nprod >> 5, sl, ss,
+                                 wscr);
             }
         } else {
             // ---- consumers: FrameBatch.__init__: x = 0, z = coins (frame_sim.py:36-39) ----
