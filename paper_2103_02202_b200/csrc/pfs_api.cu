@@ -77,8 +77,7 @@ struct pfs_program {
 
 // noise counters (2 buffers) + the sampler's per-thread duplicate-check scratch
 static size_t fixed_smem(const HostProgram& hp) {
-    return (size_t)hp.num_noise * 8 + (size_t)NZ_MAX_LIST * FRAME_MAX_THREADS * 4 +
-           (size_t)(FRAME_MAX_THREADS / 32) * 512 + 16;
+    return (size_t)hp.num_noise * 8 + (size_t)(FRAME_MAX_THREADS / 32) * (256 + 32 * NZ_MAX_LIST) * 4;
 }
 
 static void choose_layout(pfs_program* pg) {

@@ -237,28 +237,41 @@ __device__ __forceinline__ void consumer_sync(int nthreads) {
 }
 
 // Sample the pre-generated noise ops of global tile g into hit lists.
-// Warp-cooperative: a work item is 32 consecutive chunks of one op, lane l
-// owns chunk 32*item + l, so the Philox block-0 draw (count + first hit) runs
-// converged across the warp; hit-list slots are reserved with one atomic per
-// warp.  Same draws as noise_chunk.
+// Data-parallel per warp: a work item is 32 consecutive chunks of one op (lane
+// l owns chunk 32*item + l).  (1) every lane draws its chunk's Philox block 0
+// (count + first hit), converged; (2) the item's hits are compacted across the
+// warp and each lane produces one hit per round: its pair, position, pick,
+// target rows and hit-list entry (one atomic per item reserves the slots);
+// (3) duplicate positions inside a chunk are detected afterwards and, rarely,
+// redrawn serially.  The draws equal noise_chunk's; virtual
+// trials past the op's end become no-op entries.
+template <int W>
+__device__ __forceinline__ uint64_t hit_entry(const uint32_t* tg, int ar, uint32_t ch, uint32_t trial,
+                                              uint32_t pick, bool real) {
+    constexpr uint32_t T = 32 * W;
+    if (!real) return 0ull;  // xm = zm = 0: applies nothing
+    const uint32_t app = trial / T, s = trial % T;
+    uint32_t xm, zm;
+    pattern_of(ch, pick, xm, zm);
+    const uint32_t q0 = __ldg(tg + app * ar);
+    const uint32_t q1 = ar == 2 ? __ldg(tg + app * ar + 1) : 0u;
+    return make_hit(q0, q1, s >> 5, s & 31, xm, zm);
+}
+
 template <int W>
 __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uint32_t* ncnt,
-                                              uint64_t* hits, int warp, int nwarps, uint32_t* sl,
-                                              int ss, uint32_t* wscr) {
-    constexpr uint32_t T = 32 * W;
+                                              uint64_t* hits, int warp, int nwarps, uint32_t* wscr) {
     const int lane = threadIdx.x & 31;
     const int total = kp.pregen_chunks;  // work items (32-chunk blocks) per tile
-    int k = 0;
-    uint32_t ord = 0, item_base = 0, next_base = 0, ch = 0, tab0 = 0;
+    int k = -1;
+    uint32_t ord = 0, item_base = 0, next_base = 0, ch = 0;
     NoiseParam np{};
     unsigned long long t0 = 0, t1 = 0;
     const uint32_t* tg = nullptr;
     int ar = 1;
-    bool loaded = false;
     for (int item = warp; item < total; item += nwarps) {
-        // advance the op cursor (items visit ops in increasing order)
-        while (!loaded || (uint32_t)item >= next_base) {
-            if (loaded) k++;
+        while (k < 0 || (uint32_t)item >= next_base) {  // op cursor (monotone)
+            k++;
             ord = __ldg(kp.pregen_ops + k);
             np = kp.noise[ord];
             item_base = np.chunk_base;
@@ -269,16 +282,14 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
             const unsigned long long* tab = reinterpret_cast<const unsigned long long*>(kp.noise_tab) + np.tab_full;
             t0 = np.len_full > 0 ? __ldg(tab) : ~0ull;
             t1 = np.len_full > 1 ? __ldg(tab + 1) : ~0ull;
-            loaded = true;
         }
-        (void)tab0;
-        const uint32_t r = ((uint32_t)item - item_base) * 32u + (uint32_t)lane;
-        const bool valid = r < np.nchunks;
         const uint32_t L = np.L;
         const uint32_t lg = 31u - __clz(L);
-        const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
-        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0;
-        uint32_t count = 0;
+        const uint32_t sh = 32u - lg;
+        const uint32_t r0 = ((uint32_t)item - item_base) * 32u;
+        const uint32_t r = r0 + (uint32_t)lane;
+        const bool valid = r < np.nchunks;
+        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, count = 0;
         if (valid) {
             noise_block(0u, r, g, ord, kp.seed, w0, w1, w2, w3);
             const unsigned long long u = ((unsigned long long)w1 << 32) | w0;
@@ -292,126 +303,98 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
                 }
             }
         }
-        // positions/picks: count 1 straight from block 0; lanes with 2..NZ_MAX_LIST
-        // hits need blocks 1..count/2, computed cooperatively by the whole warp
-        uint32_t e0 = 0;
-        uint32_t nreal = 0;
-        const uint32_t sh = 32u - lg;
-        if (count == 1) {
-            const uint32_t pos = lg ? (w2 >> sh) : 0u;
-            e0 = (pos << 4) | (np.npat > 1 ? __umulhi(w3, np.npat) : 0u);
-            nreal = pos < vlen ? 1u : 0u;
-        }
-        {
-            const uint32_t nb = (count > 1 && count <= (uint32_t)NZ_MAX_LIST) ? (count >> 1) : 0u;
-            uint32_t pb = nb;  // inclusive prefix of extra blocks
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pb, d);
-                if (lane >= d) pb += v;
-            }
-            const uint32_t ntask = __shfl_sync(0xFFFFFFFFu, pb, 31);
-            const uint32_t first = pb - nb;
-            for (uint32_t t0 = 0; t0 < ntask; t0 += 32) {
-                const uint32_t task = t0 + lane;
-                // owner lane of this task: largest lane with first(lane) <= task
-                uint32_t owner = 0;
-#pragma unroll
-                for (int q = 0; q < 32; q++) {
-                    const uint32_t fq = __shfl_sync(0xFFFFFFFFu, first, q);
-                    const uint32_t nq = __shfl_sync(0xFFFFFFFFu, nb, q);
-                    if (nq && task >= fq) owner = q;
-                }
-                const uint32_t of = __shfl_sync(0xFFFFFFFFu, first, owner);
-                if (task < ntask) {
-                    const uint32_t orr = ((uint32_t)item - item_base) * 32u + owner;
-                    uint32_t b0, b1, b2, b3;
-                    noise_block(1u + (task - of), orr, g, ord, kp.seed, b0, b1, b2, b3);
-                    uint4* ws = reinterpret_cast<uint4*>(wscr) + (task & 31u);
-                    *ws = make_uint4(b0, b1, b2, b3);
-                }
-                __syncwarp();
-                // owners consume the blocks of this round that belong to them
-                if (nb) {
-                    for (uint32_t bi = 0; bi < nb; bi++) {
-                        const uint32_t tk = first + bi;
-                        if (tk < t0 || tk >= t0 + 32) continue;
-                        const uint4 blk = reinterpret_cast<const uint4*>(wscr)[tk & 31u];
-                        // block bi+1 holds pairs 2bi+1 (x,y) and 2bi+2 (z,w)
-                        const uint32_t h1 = 2 * bi + 1, h2 = 2 * bi + 2;
-                        if (h1 < count) sl[h1 * ss] = ((lg ? (blk.x >> sh) : 0u) << 4) |
-                                                      (np.npat > 1 ? __umulhi(blk.y, np.npat) : 0u);
-                        if (h2 < count) sl[h2 * ss] = ((lg ? (blk.z >> sh) : 0u) << 4) |
-                                                      (np.npat > 1 ? __umulhi(blk.w, np.npat) : 0u);
-                    }
-                }
-                __syncwarp();
-            }
-            if (nb) {
-                sl[0] = ((lg ? (w2 >> sh) : 0u) << 4) | (np.npat > 1 ? __umulhi(w3, np.npat) : 0u);
-                bool dup = false;
-                for (uint32_t h = 1; h < count; h++)
-                    for (uint32_t q = 0; q < h; q++) dup |= (sl[h * ss] >> 4) == (sl[q * ss] >> 4);
-                for (uint32_t attempt = 1; dup; attempt++) {  // rare: redraw every position
-                    dup = false;
-                    uint32_t blk = 0xFFFFFFFFu;
-                    uint32_t b0 = 0, b1 = 0, b2 = 0, b3 = 0;
-                    for (uint32_t h = 0; h < count; h++) {
-                        const uint32_t kk = attempt * NZ_MAX_LIST + h;
-                        const uint32_t need = (kk + 1) >> 1;
-                        if (need != blk) { noise_block(need, r, g, ord, kp.seed, b0, b1, b2, b3); blk = need; }
-                        const uint32_t x = (kk & 1u) ? b0 : b2, y = (kk & 1u) ? b1 : b3;
-                        const uint32_t pos = lg ? (x >> sh) : 0u;
-                        for (uint32_t q = 0; q < h; q++) dup |= (sl[q * ss] >> 4) == pos;
-                        sl[h * ss] = (pos << 4) | (np.npat > 1 ? __umulhi(y, np.npat) : 0u);
-                    }
-                }
-                for (uint32_t h = 0; h < count; h++) nreal += (sl[h * ss] >> 4) < vlen ? 1u : 0u;
-            }
-        }
-        // rare: count > NZ_MAX_LIST -> selection sampling, emitted directly below
         const bool big = count > (uint32_t)NZ_MAX_LIST;
-        // warp-aggregated slot reservation
-        uint32_t pre = nreal;
+        const uint32_t c = big ? 0u : count;
+        uint32_t pre = c;  // inclusive prefix
 #pragma unroll
         for (int d = 1; d < 32; d <<= 1) {
             const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pre, d);
             if (lane >= d) pre += v;
         }
-        const uint32_t tot = __shfl_sync(0xFFFFFFFFu, pre, 31);
-        uint32_t base = 0;
-        if (lane == 0 && tot) base = atomicAdd(ncnt + ord, tot);
-        base = __shfl_sync(0xFFFFFFFFu, base, 0) + pre - nreal;
-        auto write = [&](uint32_t slot, uint32_t trial, uint32_t pick) {
-            if (slot >= np.cap) return;
-            const uint32_t app = trial / T, s = trial % T;
-            uint32_t xm, zm;
-            pattern_of(ch, pick, xm, zm);
-            const uint32_t q0 = __ldg(tg + app * ar);
-            const uint32_t q1 = ar == 2 ? __ldg(tg + app * ar + 1) : 0u;
-            hits[np.cap_base + slot] = make_hit(q0, q1, s >> 5, s & 31, xm, zm);
-        };
-        if (count == 1) {
-            if (nreal) write(base, r * L + (e0 >> 4), e0 & 15u);
-        } else if (count > 1 && !big) {
-            uint32_t o = 0;
-            for (uint32_t h = 0; h < count; h++) {
-                const uint32_t e = sl[h * ss];
-                if ((e >> 4) < vlen) write(base + o++, r * L + (e >> 4), e & 15u);
+        const uint32_t H = __shfl_sync(0xFFFFFFFFu, pre, 31);
+        const uint32_t excl = pre - c;
+        uint32_t sbase = 0;
+        if (lane == 0 && H) sbase = atomicAdd(ncnt + ord, H);
+        sbase = __shfl_sync(0xFFFFFFFFu, sbase, 0);
+        for (uint32_t j0 = 0; j0 < H; j0 += 32) {
+            const uint32_t j = j0 + (uint32_t)lane;
+            // owner chunk: smallest lane q with pre[q] > j
+            uint32_t lo = 0;
+#pragma unroll
+            for (int st = 16; st > 0; st >>= 1) {
+                const uint32_t pv = __shfl_sync(0xFFFFFFFFu, pre, (int)(lo + st - 1));
+                if (pv <= j) lo += st;
             }
-        } else if (big) {
+            const uint32_t owner = lo > 31u ? 31u : lo;
+            const uint32_t oexcl = __shfl_sync(0xFFFFFFFFu, excl, (int)owner);
+            uint32_t x = __shfl_sync(0xFFFFFFFFu, w2, (int)owner);
+            uint32_t y = __shfl_sync(0xFFFFFFFFu, w3, (int)owner);
+            if (j < H) {
+                const uint32_t h = j - oexcl;
+                const uint32_t rr = r0 + owner;
+                if (h > 0) {
+                    uint32_t b0, b1, b2, b3;
+                    noise_block((h + 1) >> 1, rr, g, ord, kp.seed, b0, b1, b2, b3);
+                    x = (h & 1u) ? b0 : b2;
+                    y = (h & 1u) ? b1 : b3;
+                }
+                const uint32_t pos = lg ? (x >> sh) : 0u;
+                const uint32_t pick = np.npat > 1 ? __umulhi(y, np.npat) : 0u;
+                const uint32_t vlen = (rr + 1 == np.nchunks) ? np.last_len : L;
+                wscr[j] = pos;
+                const uint32_t slot = sbase + j;
+                if (slot < np.cap)
+                    hits[np.cap_base + slot] = hit_entry<W>(tg, ar, ch, rr * L + pos, pick, pos < vlen);
+            }
+        }
+        __syncwarp();
+        // duplicate positions within a chunk (probability ~count^2 / 2L)
+        bool dup = false;
+        if (c > 1) {
+            for (uint32_t h = 1; h < c; h++)
+                for (uint32_t q = 0; q < h; q++) dup |= wscr[excl + h] == wscr[excl + q];
+        }
+        __syncwarp();
+        if (dup) {  // redraw every position of this chunk (attempts >= 1), same slots
+            const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
+            uint32_t* sl = wscr + 256 + lane * NZ_MAX_LIST;
+            for (uint32_t attempt = 1; dup; attempt++) {
+                dup = false;
+                uint32_t blk = 0xFFFFFFFFu, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
+                for (uint32_t h = 0; h < c; h++) {
+                    const uint32_t kk = attempt * NZ_MAX_LIST + h;
+                    const uint32_t need = (kk + 1) >> 1;
+                    if (need != blk) { noise_block(need, r, g, ord, kp.seed, b0, b1, b2, b3); blk = need; }
+                    const uint32_t x = (kk & 1u) ? b0 : b2, y = (kk & 1u) ? b1 : b3;
+                    const uint32_t pos = lg ? (x >> sh) : 0u;
+                    for (uint32_t q = 0; q < h; q++) dup |= (sl[q] >> 4) == pos;
+                    sl[h] = (pos << 4) | (np.npat > 1 ? __umulhi(y, np.npat) : 0u);
+                }
+            }
+            for (uint32_t h = 0; h < c; h++) {
+                const uint32_t slot = sbase + excl + h;
+                const uint32_t pos = sl[h] >> 4;
+                if (slot < np.cap)
+                    hits[np.cap_base + slot] = hit_entry<W>(tg, ar, ch, r * L + pos, sl[h] & 15u, pos < vlen);
+            }
+        }
+        if (big) {  // selection sampling, ~1e-6 of chunks
+            const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
             uint32_t needed = count;
             for (uint32_t i = 0; needed > 0; i++) {
                 noise_block(0x80000000u + i, r, g, ord, kp.seed, w0, w1, w2, w3);
                 if (__umul64hi(((uint64_t)w1 << 32) | w0, (uint64_t)(L - i)) < needed) {
                     if (i < vlen) {
                         const uint32_t slot = atomicAdd(ncnt + ord, 1u);
-                        write(slot, r * L + i, np.npat > 1 ? __umulhi(w2, np.npat) : 0u);
+                        if (slot < np.cap)
+                            hits[np.cap_base + slot] = hit_entry<W>(tg, ar, ch, r * L + i,
+                                                                    np.npat > 1 ? __umulhi(w2, np.npat) : 0u, true);
                     }
                     needed--;
                 }
             }
         }
+        __syncwarp();
     }
 }
 
@@ -436,13 +419,12 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // [2][num_noise]
     uint64_t* const hits0 = kp.hits_global + (size_t)blockIdx.x * 2 * kp.hit_capacity;
     const int tid = threadIdx.x;
-    // per-thread duplicate-check scratch of the noise sampler: [NZ_MAX_LIST][blockDim]
+    // per-warp scratch of the noise sampler: 256 positions + 32 x NZ_MAX_LIST
+    // per-lane duplicate-check slots (also used by the consumers' inline path)
     uint32_t* const nscr = ncnt0 + 2 * kp.num_noise;
-    uint32_t* const sl = nscr + tid;
-    const int ss = blockDim.x;
-    // per-warp scratch (32 Philox blocks) of the cooperative noise pre-pass, 16-byte aligned
-    uint32_t* const wscr = reinterpret_cast<uint32_t*>(
-        (reinterpret_cast<uintptr_t>(nscr + NZ_MAX_LIST * blockDim.x) + 15) & ~(uintptr_t)15) + ((tid >> 5) << 7);
+    uint32_t* const wscr = nscr + (tid >> 5) * (256 + 32 * NZ_MAX_LIST);
+    uint32_t* const sl = wscr + 256 + (tid & 31) * NZ_MAX_LIST;
+    const int ss = 1;
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
     const int nprod = pregen ? kp.producers : 0;
     const int nth = blockDim.x - nprod;  // consumer threads
@@ -456,7 +438,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
         for (int i = tid; i < kp.num_noise; i += blockDim.x) ncnt0[i] = 0u;
         __syncthreads();
         noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid >> 5,
-                         blockDim.x >> 5, sl, ss, wscr);
+                         blockDim.x >> 5, wscr);
     }
     __syncthreads();
 
@@ -475,8 +457,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 for (int i = pt; i < kp.num_noise; i += nprod) ncn[i] = 0u;
                 asm volatile("bar.sync 2, %0;" ::"r"(nprod) : "memory");
                 noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + (uint64_t)nt), ncn,
-                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt >> 5, nprod >> 5, sl, ss,
-                                 wscr);
+                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt >> 5, nprod >> 5, wscr);
             }
         } else {
             // ---- consumers: FrameBatch.__init__: x = 0, z = coins (frame_sim.py:36-39) ----
