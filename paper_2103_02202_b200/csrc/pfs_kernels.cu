@@ -398,6 +398,25 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
     }
 }
 
+// Items of one op, U per thread per batch: all U operand loads (L2-resident
+// target indices) are issued before any of the dependent shared-memory work.
+template <int U, typename Load, typename Work>
+__device__ __forceinline__ void batched_items(int tid, int nth, int items, Load load, Work work) {
+    for (int i0 = tid; i0 < items; i0 += U * nth) {
+        decltype(load(0)) v[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = i0 + u * nth;
+            v[u] = i < items ? load(i) : decltype(load(0)){};
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const int i = i0 + u * nth;
+            if (i < items) work(i, v[u]);
+        }
+    }
+}
+
 // ------------------------------------------------------------ frame kernel
 // Warp-specialised persistent kernel.  Threads [0, nc) are consumers: they
 // run the op stream of tile i on the frame in shared memory, synchronising on
@@ -497,29 +516,30 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 switch (kind) {
                 case K_GATE: {
                     const int items = (int)(count << LC);
+                    auto q1 = [&](int i) { return __ldg(tg + (i >> LC)); };
+                    auto q2 = [&](int i) { return __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC)); };
                     switch (code) {
                     case R_SWAPXZ:
-                        for (int i = tid; i < items; i += nth) {
-                            const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                        batched_items<4>(tid, nth, items, q1, [&](int i, uint32_t q) {
+                            const size_t p = (size_t)q * W + (i & (C - 1)) * V;
                             const VW<V> a = vld<V>(X + p), b = vld<V>(Z + p);
                             vst<V>(X + p, b); vst<V>(Z + p, a);
-                        }
+                        });
                         break;
                     case R_ZXORX:
-                        for (int i = tid; i < items; i += nth) {
-                            const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                        batched_items<4>(tid, nth, items, q1, [&](int i, uint32_t q) {
+                            const size_t p = (size_t)q * W + (i & (C - 1)) * V;
                             vst<V>(Z + p, vxor<V>(vld<V>(Z + p), vld<V>(X + p)));
-                        }
+                        });
                         break;
                     case R_XXORZ:
-                        for (int i = tid; i < items; i += nth) {
-                            const size_t p = (size_t)__ldg(tg + (i >> LC)) * W + (i & (C - 1)) * V;
+                        batched_items<4>(tid, nth, items, q1, [&](int i, uint32_t q) {
+                            const size_t p = (size_t)q * W + (i & (C - 1)) * V;
                             vst<V>(X + p, vxor<V>(vld<V>(X + p), vld<V>(Z + p)));
-                        }
+                        });
                         break;
-                    default: {  // two-qubit rules
-                        for (int i = tid; i < items; i += nth) {
-                            const uint2 qq = __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC));
+                    default:  // two-qubit rules
+                        batched_items<4>(tid, nth, items, q2, [&](int i, uint2 qq) {
                             const int cv = (i & (C - 1)) * V;
                             const size_t p0 = (size_t)qq.x * W + cv, p1 = (size_t)qq.y * W + cv;
                             const VW<V> x0 = vld<V>(X + p0), x1 = vld<V>(X + p1);
@@ -537,38 +557,39 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                                 vst<V>(X + p0, x1); vst<V>(X + p1, x0);
                                 vst<V>(Z + p0, z1); vst<V>(Z + p1, z0); break;
                             }
-                        }
-                    }
+                        });
                     }
                     break;
                 }
                 case K_M: case K_MR: {
                     const int items = (int)(count << LC);
-                    for (int i = tid; i < items; i += nth) {
-                        const int j = i >> LC, c = i & (C - 1);
-                        const uint2 qs = __ldg(reinterpret_cast<const uint2*>(tg) + j);
-                        const size_t p = (size_t)qs.x * W + c * V;
-                        const VW<V> xv = vld<V>(X + p);
-                        if (kp.do_dets && qs.y != NO_SLOT) vst<V>(ring + (size_t)qs.y * W + c * V, xv);
-                        if (kp.rec_out != nullptr)
-                            vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_words + tile * W + c * V, xv);
-                        if (kind == K_M) {
-                            vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_words<W, V>(kp, ob + j, c, g, tile)));
-                        } else {
-                            vst<V>(X + p, vzero<V>());
-                            vst<V>(Z + p, coin_words<W, V>(kp, ob + 2 * j + 1, c, g, tile));
-                        }
-                    }
+                    batched_items<4>(tid, nth, items,
+                        [&](int i) { return __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC)); },
+                        [&](int i, uint2 qs) {
+                            const int j = i >> LC, c = i & (C - 1);
+                            const size_t p = (size_t)qs.x * W + c * V;
+                            const VW<V> xv = vld<V>(X + p);
+                            if (kp.do_dets && qs.y != NO_SLOT) vst<V>(ring + (size_t)qs.y * W + c * V, xv);
+                            if (kp.rec_out != nullptr)
+                                vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_words + tile * W + c * V, xv);
+                            if (kind == K_M) {
+                                vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_words<W, V>(kp, ob + j, c, g, tile)));
+                            } else {
+                                vst<V>(X + p, vzero<V>());
+                                vst<V>(Z + p, coin_words<W, V>(kp, ob + 2 * j + 1, c, g, tile));
+                            }
+                        });
                     break;
                 }
                 case K_R: {
                     const int items = (int)(count << LC);
-                    for (int i = tid; i < items; i += nth) {
-                        const int j = i >> LC, c = i & (C - 1);
-                        const size_t p = (size_t)__ldg(tg + j) * W + c * V;
-                        vst<V>(X + p, vzero<V>());
-                        vst<V>(Z + p, coin_words<W, V>(kp, ob + j, c, g, tile));
-                    }
+                    batched_items<4>(tid, nth, items, [&](int i) { return __ldg(tg + (i >> LC)); },
+                        [&](int i, uint32_t q) {
+                            const int j = i >> LC, c = i & (C - 1);
+                            const size_t p = (size_t)q * W + c * V;
+                            vst<V>(X + p, vzero<V>());
+                            vst<V>(Z + p, coin_words<W, V>(kp, ob + j, c, g, tile));
+                        });
                     break;
                 }
                 case K_NOISE: {
@@ -626,32 +647,42 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 case K_DET: {
                     if (!kp.do_dets) break;
                     const int items = (int)(count << LC);
-                    for (int i = tid; i < items; i += nth) {
-                        const uint32_t col = oa + (uint32_t)(i >> LC);
-                        const int c = i & (C - 1);
-                        VW<V> acc = vzero<V>();
-                        const uint32_t e0 = __ldg(kp.det_ptr + col), e1 = __ldg(kp.det_ptr + col + 1);
-                        for (uint32_t e = e0; e < e1; e++) {
-                            const uint32_t s = __ldg(kp.det_terms + e);
-                            acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
-                        }
-                        if (kp.ev_out != nullptr)
-                            vst<V>(kp.ev_out + (int64_t)col * kp.out_words + tile * W + c * V, acc);
-                        if (kp.counts != nullptr) {
-                            uint32_t tot = 0;
+                    // prefetch each column's term range and first two record slots
+                    batched_items<4>(tid, nth, items,
+                        [&](int i) {
+                            const uint32_t col = oa + (uint32_t)(i >> LC);
+                            const uint32_t e0 = __ldg(kp.det_ptr + col), e1 = __ldg(kp.det_ptr + col + 1);
+                            const uint32_t s0 = e0 < e1 ? __ldg(kp.det_terms + e0) : NO_SLOT;
+                            const uint32_t s1 = e0 + 1 < e1 ? __ldg(kp.det_terms + e0 + 1) : NO_SLOT;
+                            return make_uint4(e0, e1, s0, s1);
+                        },
+                        [&](int i, uint4 d) {
+                            const uint32_t col = oa + (uint32_t)(i >> LC);
+                            const int c = i & (C - 1);
+                            VW<V> acc = vzero<V>();
+                            if (d.z != NO_SLOT) acc = vld<V>(ring + (size_t)d.z * W + c * V);
+                            if (d.w != NO_SLOT) acc = vxor<V>(acc, vld<V>(ring + (size_t)d.w * W + c * V));
+                            for (uint32_t e = d.x + 2; e < d.y; e++) {
+                                const uint32_t s = __ldg(kp.det_terms + e);
+                                acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
+                            }
+                            if (kp.ev_out != nullptr)
+                                vst<V>(kp.ev_out + (int64_t)col * kp.out_words + tile * W + c * V, acc);
+                            if (kp.counts != nullptr) {
+                                uint32_t tot = 0;
 #pragma unroll
-                            for (int jw = 0; jw < V; jw++) {
-                                const int64_t s0 = tile * (int64_t)(32 * W) + 32 * (c * V + jw);
-                                const int64_t rem = kp.num_shots - s0;
-                                const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-                                tot += __popc(acc.w[jw] & m);
+                                for (int jw = 0; jw < V; jw++) {
+                                    const int64_t s0 = tile * (int64_t)(32 * W) + 32 * (c * V + jw);
+                                    const int64_t rem = kp.num_shots - s0;
+                                    const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+                                    tot += __popc(acc.w[jw] & m);
+                                }
+                                if (tot) {
+                                    if (kp.counts_in_smem) atomicAdd(cnt + col, tot);
+                                    else atomicAdd(kp.counts + col, (unsigned long long)tot);
+                                }
                             }
-                            if (tot) {
-                                if (kp.counts_in_smem) atomicAdd(cnt + col, tot);
-                                else atomicAdd(kp.counts + col, (unsigned long long)tot);
-                            }
-                        }
-                    }
+                        });
                     break;
                 }
                 case K_OBS: {
