@@ -563,7 +563,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 }
                 case K_M: case K_MR: {
                     const int items = (int)(count << LC);
-                    batched_items<4>(tid, nth, items,
+                    batched_items<2>(tid, nth, items,
                         [&](int i) { return __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC)); },
                         [&](int i, uint2 qs) {
                             const int j = i >> LC, c = i & (C - 1);
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     if (!kp.do_dets) break;
                     const int items = (int)(count << LC);
                     // prefetch each column's term range and first two record slots
-                    batched_items<4>(tid, nth, items,
+                    batched_items<2>(tid, nth, items,
                         [&](int i) {
                             const uint32_t col = oa + (uint32_t)(i >> LC);
                             const uint32_t e0 = __ldg(kp.det_ptr + col), e1 = __ldg(kp.det_ptr + col + 1);
