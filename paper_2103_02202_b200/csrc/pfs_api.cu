@@ -473,7 +473,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (!dev_out && ci >= 2) CUDA_TRY(cudaStreamWaitEvent(st, pg->ev[6 + b], 0));  // buffer free
         uint32_t* rows = direct_rows ? (uint32_t*)out : pg->d_rows[b].p;
         const int64_t row_words = direct_rows ? used_words : chunk_words;
-        kp.out_words = row_words;
+        kp.out_row_stride = b8 ? W : row_words;         // b8: tile-major scratch
+        kp.out_tile_stride = b8 ? R * W : W;
         kp.rec_out = rows_meas ? rows : nullptr;
         kp.ev_out = rows_meas ? nullptr : rows;
         kp.n_tiles = nt;
@@ -484,7 +485,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             // the last tile would write past the caller's rows: stage through scratch
             CUDA_TRY(pg->d_rows[0].reserve((size_t)std::max<int64_t>(R, 1) * chunk_words));
             rows = pg->d_rows[0].p;
-            kp.out_words = chunk_words;
+            kp.out_row_stride = chunk_words;
+            kp.out_tile_stride = W;
             kp.rec_out = rows_meas ? rows : nullptr;
             kp.ev_out = rows_meas ? nullptr : rows;
         }
@@ -497,12 +499,12 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (b8) {
             uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
             const int64_t pitch = dev_out ? out_pitch : dev_pitch;
-            CUDA_TRY(launch_rows_to_b8(rows, R, kp.out_words, nshots,
-                                       mode == PFS_MODE_SAMPLES ? d_ref : nullptr, dst, pitch, st));
+            CUDA_TRY(launch_tiles_to_b8(rows, R, W, nt, nshots,
+                                        mode == PFS_MODE_SAMPLES ? d_ref : nullptr, dst, pitch, st));
             pg->last_launches++;
             if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
         } else if (direct_rows && rows != (uint32_t*)out) {
-            CUDA_TRY(cudaMemcpy2DAsync(out, used_words * 4, rows, kp.out_words * 4, used_words * 4, R,
+            CUDA_TRY(cudaMemcpy2DAsync(out, used_words * 4, rows, kp.out_row_stride * 4, used_words * 4, R,
                                        cudaMemcpyDeviceToDevice, st));
         }
         if (timing && ci == 0) {

@@ -135,7 +135,8 @@ struct KParams {
     uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
     uint64_t* hits_global;       // [grid][2][hit_capacity] pre-generated noise hits
     int64_t inject_words;
-    int64_t out_words;
+    int64_t out_row_stride;      // output word address = row * out_row_stride
+    int64_t out_tile_stride;     //                     + tile * out_tile_stride + word
     int64_t n_tiles;
     int64_t num_shots;           // shots of this launch (for tail masking)
     int64_t hit_capacity;
@@ -172,5 +173,9 @@ cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t ro
                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
                               int64_t pitch, cudaStream_t stream);
 cudaError_t smem_probe(int device, double* gbs);
+// tile-major [tile][row][W] bit tables -> shot-major b8 rows of `pitch` bytes
+cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, int64_t n_tiles,
+                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
+                               int64_t pitch, cudaStream_t stream);
 
 }  // namespace pfs

@@ -496,16 +496,14 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             consumer_sync(nth);
 
             uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
-            uint4 h1 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops) + 1) : make_uint4(0, 0, 0, 0);
             for (int oi = 0; oi < kp.n_ops; oi++) {
                 const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
-                const uint32_t count = h0.y, off = h0.z, oa = h0.w, ob = h1.x;
-                const uint32_t oc = h1.y, od = h1.z, oe = h1.w;
-                // prefetch the next op descriptor while this one runs
-                if (oi + 1 < kp.n_ops) {
-                    h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
-                    h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1) + 1);
-                }
+                const uint32_t count = h0.y, off = h0.z, oa = h0.w;
+                // second half of the descriptor: its load overlaps the barrier wait
+                const uint4 h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi) + 1);
+                // prefetch the next op's first half while this one runs
+                if (oi + 1 < kp.n_ops) h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
+                const uint32_t ob = h1.x, oc = h1.y, od = h1.z, oe = h1.w;
                 if (flags & F_BARRIER) consumer_sync(nth);
                 const uint32_t* tg = kp.targets + off;
                 if (kp.debug_skip) {
@@ -571,7 +569,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                             const VW<V> xv = vld<V>(X + p);
                             if (kp.do_dets && qs.y != NO_SLOT) vst<V>(ring + (size_t)qs.y * W + c * V, xv);
                             if (kp.rec_out != nullptr)
-                                vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_words + tile * W + c * V, xv);
+                                vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_row_stride +
+                                           tile * kp.out_tile_stride + c * V, xv);
                             if (kind == K_M) {
                                 vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_words<W, V>(kp, ob + j, c, g, tile)));
                             } else {
@@ -667,7 +666,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                                 acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
                             }
                             if (kp.ev_out != nullptr)
-                                vst<V>(kp.ev_out + (int64_t)col * kp.out_words + tile * W + c * V, acc);
+                                vst<V>(kp.ev_out + (int64_t)col * kp.out_row_stride +
+                                           tile * kp.out_tile_stride + c * V, acc);
                             if (kp.counts != nullptr) {
                                 uint32_t tot = 0;
 #pragma unroll
@@ -824,6 +824,80 @@ __global__ void __launch_bounds__(256) rows_to_b8_kernel(const uint32_t* __restr
                 out[s * pitch + b0 + lane] = (uint8_t)(tout[sl][lane >> 2] >> ((lane & 3) * 8));
         }
     }
+}
+
+// Tile-major input: block (tile t, rows r0..r0+255) is one contiguous run of
+// 256 W words, so loads are fully coalesced; each shot's 32 output bytes are
+// one aligned sector when the pitch allows.
+__global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __restrict__ tiles,
+                                                          int64_t num_rows, int W,
+                                                          int64_t num_shots,
+                                                          const uint8_t* __restrict__ xor_bits,
+                                                          uint8_t* __restrict__ out, int64_t pitch) {
+    extern __shared__ uint32_t tsm[];
+    const int Wp = W + 1;
+    uint32_t* tin = tsm;                      // [256][W+1]
+    uint32_t* tout = tsm + 256 * Wp;          // [32W][9]
+    const int t = threadIdx.x;
+    const int64_t tile = blockIdx.x;
+    const int64_t r0 = (int64_t)blockIdx.y * 256;
+    const int rows = (int)((num_rows - r0) < 256 ? (num_rows - r0) : 256);
+    const uint32_t* src = tiles + tile * num_rows * W + r0 * W;
+    for (int i = t; i < 256 * W; i += 256) {
+        const int r = i / W, w = i - r * W;
+        uint32_t v = 0u;
+        if (r < rows) {
+            v = __ldg(src + i);
+            if (xor_bits != nullptr && (__ldg(xor_bits + r0 + r) & 1u)) v = ~v;
+        }
+        tin[r * Wp + w] = v;
+    }
+    __syncthreads();
+    const int warp = t >> 5, lane = t & 31;
+    for (int pair = warp; pair < 8 * W; pair += 8) {
+        const int rb = pair / W, w = pair - rb * W;
+        uint32_t v = tin[(rb * 32 + lane) * Wp + w];
+        v = transpose32_lane(v, lane);
+        tout[(w * 32 + lane) * 9 + rb] = v;
+    }
+    __syncthreads();
+    const int64_t nbytes = (num_rows + 7) >> 3;
+    const int64_t b0 = r0 >> 3;
+    const int64_t span = (nbytes - b0) < 32 ? (nbytes - b0) : 32;
+    const int64_t s0 = tile * 32 * W;
+    const bool full = (pitch & 15) == 0 && ((uintptr_t)out & 15) == 0 && b0 + 32 <= pitch;
+    if (full) {
+        for (int sl = t; sl < 32 * W; sl += 256) {
+            const int64_t s = s0 + sl;
+            if (s >= num_shots) break;
+            const uint32_t* o = tout + sl * 9;
+            uint4* dst = reinterpret_cast<uint4*>(out + s * pitch + b0);
+            dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
+            dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+        }
+    } else {
+        for (int sl = warp; sl < 32 * W; sl += 8) {
+            const int64_t s = s0 + sl;
+            if (s >= num_shots) break;
+            if (lane < span) out[s * pitch + b0 + lane] = (uint8_t)(tout[sl * 9 + (lane >> 2)] >> ((lane & 3) * 8));
+        }
+    }
+}
+
+cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, int64_t n_tiles,
+                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
+                               int64_t pitch, cudaStream_t stream) {
+    if (num_rows <= 0 || num_shots <= 0 || n_tiles <= 0) return cudaSuccess;
+    dim3 grid((unsigned)n_tiles, (unsigned)((num_rows + 255) / 256));
+    if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
+    const size_t sm = ((size_t)256 * (W + 1) + (size_t)32 * W * 9) * 4;
+    if (sm > 48 * 1024) {
+        cudaError_t e = cudaFuncSetAttribute(tiles_to_b8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)sm);
+        if (e != cudaSuccess) return e;
+    }
+    tiles_to_b8_kernel<<<grid, 256, sm, stream>>>(tiles, num_rows, W, num_shots, xor_bits, out, pitch);
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ SMEM roofline probe
