@@ -829,42 +829,52 @@ __global__ void __launch_bounds__(256) rows_to_b8_kernel(const uint32_t* __restr
 // Tile-major input: block (tile t, rows r0..r0+255) is one contiguous run of
 // 256 W words, so loads are fully coalesced; each shot's 32 output bytes are
 // one aligned sector when the pitch allows.
+// TW = tile words, W = words handled per CTA (TW > 16 splits a tile in parts)
+template <int TW, int W>
 __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __restrict__ tiles,
-                                                          int64_t num_rows, int W,
-                                                          int64_t num_shots,
+                                                          int64_t num_rows, int64_t num_shots,
                                                           const uint8_t* __restrict__ xor_bits,
                                                           uint8_t* __restrict__ out, int64_t pitch) {
-    extern __shared__ uint32_t tsm[];
-    const int Wp = W + 1;
-    uint32_t* tin = tsm;                      // [256][W+1]
-    uint32_t* tout = tsm + 256 * Wp;          // [32W][9]
+    constexpr int Wp = W + 1;
+    constexpr int PARTS = TW / W;
+    __shared__ uint32_t tin[256 * Wp];
+    __shared__ uint32_t tout[32 * W * 9];
     const int t = threadIdx.x;
-    const int64_t tile = blockIdx.x;
+    const int64_t tile = blockIdx.x / PARTS;
+    const int part = (int)(blockIdx.x % PARTS);
     const int64_t r0 = (int64_t)blockIdx.y * 256;
     const int rows = (int)((num_rows - r0) < 256 ? (num_rows - r0) : 256);
-    const uint32_t* src = tiles + tile * num_rows * W + r0 * W;
-    for (int i = t; i < 256 * W; i += 256) {
-        const int r = i / W, w = i - r * W;
-        uint32_t v = 0u;
-        if (r < rows) {
-            v = __ldg(src + i);
-            if (xor_bits != nullptr && (__ldg(xor_bits + r0 + r) & 1u)) v = ~v;
-        }
-        tin[r * Wp + w] = v;
+    const uint32_t* src = tiles + tile * num_rows * TW + r0 * TW + part * W;
+    // all W loads of a thread are issued before any is used
+    uint32_t v[W];
+#pragma unroll
+    for (int k = 0; k < W; k++) {
+        const int i = t + 256 * k;
+        const int r = i / W, w = i % W;
+        v[k] = (r < rows) ? __ldg(src + r * TW + w) : 0u;
+    }
+#pragma unroll
+    for (int k = 0; k < W; k++) {
+        const int i = t + 256 * k;
+        const int r = i / W, w = i % W;
+        uint32_t x = v[k];
+        if (xor_bits != nullptr && r < rows && (__ldg(xor_bits + r0 + r) & 1u)) x = ~x;
+        tin[r * Wp + w] = x;
     }
     __syncthreads();
     const int warp = t >> 5, lane = t & 31;
+#pragma unroll
     for (int pair = warp; pair < 8 * W; pair += 8) {
-        const int rb = pair / W, w = pair - rb * W;
-        uint32_t v = tin[(rb * 32 + lane) * Wp + w];
-        v = transpose32_lane(v, lane);
-        tout[(w * 32 + lane) * 9 + rb] = v;
+        const int rb = pair / W, w = pair % W;
+        uint32_t x = tin[(rb * 32 + lane) * Wp + w];
+        x = transpose32_lane(x, lane);
+        tout[(w * 32 + lane) * 9 + rb] = x;
     }
     __syncthreads();
     const int64_t nbytes = (num_rows + 7) >> 3;
     const int64_t b0 = r0 >> 3;
     const int64_t span = (nbytes - b0) < 32 ? (nbytes - b0) : 32;
-    const int64_t s0 = tile * 32 * W;
+    const int64_t s0 = tile * 32 * TW + part * 32 * W;
     const bool full = (pitch & 15) == 0 && ((uintptr_t)out & 15) == 0 && b0 + 32 <= pitch;
     if (full) {
         for (int sl = t; sl < 32 * W; sl += 256) {
@@ -888,15 +898,18 @@ cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, i
                                int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
                                int64_t pitch, cudaStream_t stream) {
     if (num_rows <= 0 || num_shots <= 0 || n_tiles <= 0) return cudaSuccess;
-    dim3 grid((unsigned)n_tiles, (unsigned)((num_rows + 255) / 256));
+    const unsigned parts = W > 16 ? (unsigned)(W / 16) : 1u;
+    dim3 grid((unsigned)n_tiles * parts, (unsigned)((num_rows + 255) / 256));
     if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
-    const size_t sm = ((size_t)256 * (W + 1) + (size_t)32 * W * 9) * 4;
-    if (sm > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(tiles_to_b8_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)sm);
-        if (e != cudaSuccess) return e;
+    switch (W) {
+        case 1: tiles_to_b8_kernel<1, 1><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 2: tiles_to_b8_kernel<2, 2><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 4: tiles_to_b8_kernel<4, 4><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 8: tiles_to_b8_kernel<8, 8><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 16: tiles_to_b8_kernel<16, 16><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 32: tiles_to_b8_kernel<32, 16><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        default: return cudaErrorInvalidValue;
     }
-    tiles_to_b8_kernel<<<grid, 256, sm, stream>>>(tiles, num_rows, W, num_shots, xor_bits, out, pitch);
     return cudaGetLastError();
 }
 
