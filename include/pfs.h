@@ -140,6 +140,15 @@ int pfs_program_last_timing(const struct pfs_program* prog, double* ms, int n);
 /* Number of this library's kernel launches made by the last pfs_run. */
 int64_t pfs_program_last_launches(const struct pfs_program* prog);
 
+/* detector_events (stabsim/io_formats.py:208-227) for flips that were already
+ * sampled: flips_b8 = shot-major b8 rows (in_pitch bytes, 0 = ceil(M/8)),
+ * detectors as CSR (det_ptr[num_dets+1], det_idx = record indices); writes
+ * shot-major b8 events.  Host or device buffers; synchronous. */
+int pfs_detector_events(int device, const uint8_t* flips_b8, int64_t num_shots,
+                        int64_t num_results, int64_t in_pitch, const int64_t* det_ptr,
+                        const int64_t* det_idx, int64_t num_dets, uint8_t* out_b8,
+                        int64_t out_bytes, int64_t out_pitch, void* stream);
+
 /* Roofline denominator for the SMEM-resident frame kernel: measured shared-
  * memory bandwidth (GB/s, loads + stores, CX access mix) over all SMs. */
 int pfs_measure_smem_bandwidth(int device, double* gbs);

@@ -50,7 +50,8 @@ class Info(ctypes.Structure):
 
 EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_schedule", "pfs_run",
            "pfs_program_last_timing", "pfs_program_last_launches", "pfs_program_destroy",
-           "pfs_last_error", "pfs_version", "pfs_measure_smem_bandwidth")
+           "pfs_last_error", "pfs_version", "pfs_measure_smem_bandwidth",
+           "pfs_detector_events")
 
 _lib = None
 
@@ -83,6 +84,8 @@ def lib():
     L.pfs_last_error.restype = ctypes.c_char_p
     L.pfs_measure_smem_bandwidth.argtypes = [ctypes.c_int, ctypes.POINTER(ctypes.c_double)]
     L.pfs_measure_smem_bandwidth.restype = ctypes.c_int
+    L.pfs_detector_events.argtypes = [ctypes.c_int, P, i64, i64, i64, P, P, i64, P, i64, i64, P]
+    L.pfs_detector_events.restype = ctypes.c_int
     L.pfs_version.argtypes = []
     L.pfs_version.restype = ctypes.c_int
     _lib = L
@@ -116,6 +119,21 @@ def measure_smem_bandwidth(device: int = 0) -> float:
     v = ctypes.c_double()
     _check(lib().pfs_measure_smem_bandwidth(device, ctypes.byref(v)))
     return float(v.value)
+
+
+def detector_events_b8(flips_b8: np.ndarray, num_results: int, det_ptr: np.ndarray,
+                       det_idx: np.ndarray, device: int = 0) -> np.ndarray:
+    """GPU detector_events: b8 flips -> b8 events (pfs_detector_events)."""
+    fl = np.ascontiguousarray(flips_b8, dtype=np.uint8)
+    S = fl.shape[0]
+    D = int(det_ptr.shape[0]) - 1
+    out = np.zeros((S, (D + 7) // 8), dtype=np.uint8)
+    ptr = np.ascontiguousarray(det_ptr, dtype=np.int64)
+    idx = np.ascontiguousarray(det_idx, dtype=np.int64)
+    _check(lib().pfs_detector_events(device, _p(fl), S, num_results, fl.shape[1] if fl.ndim == 2 else 0,
+                                     _p(ptr), _p(idx) if idx.size else None, D, _p(out), out.nbytes,
+                                     out.shape[1], None))
+    return out
 
 
 class NativeProgram:

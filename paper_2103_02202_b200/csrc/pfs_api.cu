@@ -545,3 +545,63 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     }
     return PFS_OK;
 }
+
+// detector_events (stabsim/io_formats.py:208-227) on already-sampled flips.
+extern "C" int pfs_detector_events(int device, const uint8_t* flips_b8, int64_t num_shots,
+                                   int64_t num_results, int64_t in_pitch, const int64_t* det_ptr,
+                                   const int64_t* det_idx, int64_t num_dets, uint8_t* out_b8,
+                                   int64_t out_bytes, int64_t out_pitch, void* stream_v) {
+    if (num_shots < 0 || num_results < 0 || num_dets < 0) return fail(PFS_E_INVALID, "negative size");
+    if (num_shots == 0 || num_dets == 0) return PFS_OK;
+    if (!flips_b8 || !det_ptr || !out_b8) return fail(PFS_E_INVALID, "null argument");
+    const int64_t nb_in = (num_results + 7) / 8, nb_out = (num_dets + 7) / 8;
+    if (in_pitch == 0) in_pitch = nb_in;
+    if (out_pitch == 0) out_pitch = nb_out;
+    if (in_pitch < nb_in || out_pitch < nb_out) return fail(PFS_E_INVALID, "pitch too small");
+    if (out_bytes < (num_shots - 1) * out_pitch + nb_out) return fail(PFS_E_INVALID, "output buffer too small");
+    for (int64_t d = 0; d < num_dets; d++) {
+        if (det_ptr[d + 1] < det_ptr[d]) return fail(PFS_E_INVALID, "det_ptr not monotone");
+        for (int64_t e = det_ptr[d]; e < det_ptr[d + 1]; e++)
+            if (det_idx[e] < 0 || det_idx[e] >= num_results)
+                return fail(PFS_E_INVALID, "detector " + std::to_string(d) + " references measurement " +
+                                               std::to_string(det_idx[e]) + ", have " + std::to_string(num_results));
+    }
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PFS_E_NODEVICE, "no CUDA device available");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t st = (cudaStream_t)stream_v;
+    const int64_t words = (num_shots + 31) / 32;
+    const int64_t nnz = det_ptr[num_dets];
+    const bool in_dev = is_device_ptr(flips_b8), out_dev = is_device_ptr(out_b8);
+    uint8_t *d_in = nullptr, *d_out = nullptr;
+    uint32_t *d_rows = nullptr, *d_ev = nullptr;
+    int64_t *d_ptr = nullptr, *d_idx = nullptr;
+    auto cleanup = [&]() {
+        if (!in_dev && d_in) cudaFree(d_in);
+        if (!out_dev && d_out) cudaFree(d_out);
+        cudaFree(d_rows); cudaFree(d_ev); cudaFree(d_ptr); cudaFree(d_idx);
+    };
+#define DE_TRY(expr) do { cudaError_t _e = (expr); if (_e != cudaSuccess) { cleanup(); \
+        return fail(PFS_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e)); } } while (0)
+    if (in_dev) d_in = const_cast<uint8_t*>(flips_b8);
+    else {
+        DE_TRY(cudaMalloc(&d_in, (size_t)num_shots * in_pitch));
+        DE_TRY(cudaMemcpyAsync(d_in, flips_b8, (size_t)num_shots * in_pitch, cudaMemcpyHostToDevice, st));
+    }
+    if (out_dev) d_out = out_b8;
+    else DE_TRY(cudaMalloc(&d_out, (size_t)num_shots * out_pitch));
+    DE_TRY(cudaMalloc(&d_rows, (size_t)std::max<int64_t>(num_results, 1) * words * 4));
+    DE_TRY(cudaMalloc(&d_ev, (size_t)num_dets * words * 4));
+    DE_TRY(cudaMalloc(&d_ptr, (size_t)(num_dets + 1) * 8));
+    DE_TRY(cudaMalloc(&d_idx, (size_t)std::max<int64_t>(nnz, 1) * 8));
+    DE_TRY(cudaMemcpyAsync(d_ptr, det_ptr, (size_t)(num_dets + 1) * 8, cudaMemcpyHostToDevice, st));
+    if (nnz) DE_TRY(cudaMemcpyAsync(d_idx, det_idx, (size_t)nnz * 8, cudaMemcpyHostToDevice, st));
+    DE_TRY(launch_detector_events(d_in, in_pitch, num_shots, num_results, d_ptr, d_idx, num_dets, d_rows,
+                                  d_ev, d_out, out_pitch, st));
+    if (!out_dev)
+        DE_TRY(cudaMemcpyAsync(out_b8, d_out, (size_t)(num_shots - 1) * out_pitch + nb_out, cudaMemcpyDeviceToHost, st));
+    DE_TRY(cudaStreamSynchronize(st));
+#undef DE_TRY
+    cleanup();
+    return PFS_OK;
+}

@@ -173,6 +173,10 @@ cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t ro
                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
                               int64_t pitch, cudaStream_t stream);
 cudaError_t smem_probe(int device, double* gbs);
+cudaError_t launch_detector_events(const uint8_t* flips, int64_t in_pitch, int64_t num_shots,
+                                   int64_t num_results, const int64_t* ptr, const int64_t* idx,
+                                   int64_t num_dets, uint32_t* rows, uint32_t* ev, uint8_t* out,
+                                   int64_t out_pitch, cudaStream_t st);
 // tile-major [tile][row][W] bit tables -> shot-major b8 rows of `pitch` bytes
 cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, int64_t n_tiles,
                                int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,

@@ -913,6 +913,74 @@ cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, i
     return cudaGetLastError();
 }
 
+// ------------------------------------------------------------ detector_events
+// Shot-major b8 (any pitch) -> row-major rows [R][row_words]: the inverse of
+// rows_to_b8.  Tile: 256 rows (32 bytes per shot) x 256 shots.
+__global__ void __launch_bounds__(256) b8_to_rows_kernel(const uint8_t* __restrict__ in,
+                                                         int64_t in_pitch, int64_t num_rows,
+                                                         int64_t num_shots, uint32_t* __restrict__ rows,
+                                                         int64_t row_words) {
+    __shared__ uint32_t sin[256][9];   // [shot][byte-word]
+    __shared__ uint32_t sout[256][9];  // [row][shot-word]
+    const int t = threadIdx.x, warp = t >> 5, lane = t & 31;
+    const int64_t s0 = (int64_t)blockIdx.x * 256;
+    const int64_t r0 = (int64_t)blockIdx.y * 256;
+    const int64_t nbytes = (num_rows + 7) >> 3;
+    const int64_t b0 = r0 >> 3;
+    for (int sl = warp; sl < 256; sl += 8) {  // one warp per shot: 32 consecutive bytes
+        const int64_t s = s0 + sl;
+        uint32_t b = 0u;
+        if (s < num_shots && b0 + lane < nbytes) b = __ldg(in + s * in_pitch + b0 + lane);
+        // pack 4 bytes per word with shuffles
+        const uint32_t b1 = __shfl_down_sync(0xFFFFFFFFu, b, 1);
+        const uint32_t b2 = __shfl_down_sync(0xFFFFFFFFu, b, 2);
+        const uint32_t b3 = __shfl_down_sync(0xFFFFFFFFu, b, 3);
+        if ((lane & 3) == 0) sin[sl][lane >> 2] = b | (b1 << 8) | (b2 << 16) | (b3 << 24);
+    }
+    __syncthreads();
+    for (int pair = warp; pair < 64; pair += 8) {  // (row block rb, shot word w)
+        const int rb = pair >> 3, w = pair & 7;
+        uint32_t v = sin[w * 32 + lane][rb];   // lane = shot, bits = rows rb*32..
+        v = transpose32_lane(v, lane);         // lane = row, bits = shots w*32..
+        sout[rb * 32 + lane][w] = v;
+    }
+    __syncthreads();
+    const int64_t r = r0 + t;
+    if (r < num_rows) {
+        const int64_t w0 = s0 >> 5;
+        for (int w = 0; w < 8; w++)
+            if (w0 + w < row_words) rows[r * row_words + w0 + w] = sout[t][w];
+    }
+}
+
+// events[d][w] = XOR over e in [ptr[d], ptr[d+1]) of rows[idx[e]][w]
+__global__ void rows_xor_kernel(const uint32_t* __restrict__ rows, int64_t row_words,
+                                const int64_t* __restrict__ ptr, const int64_t* __restrict__ idx,
+                                int64_t num_dets, uint32_t* __restrict__ ev) {
+    const int64_t d = blockIdx.y;
+    const int64_t w = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (d >= num_dets || w >= row_words) return;
+    uint32_t acc = 0u;
+    for (int64_t e = __ldg(ptr + d); e < __ldg(ptr + d + 1); e++) acc ^= __ldg(rows + __ldg(idx + e) * row_words + w);
+    ev[d * row_words + w] = acc;
+}
+
+cudaError_t launch_detector_events(const uint8_t* flips, int64_t in_pitch, int64_t num_shots,
+                                   int64_t num_results, const int64_t* ptr, const int64_t* idx,
+                                   int64_t num_dets, uint32_t* rows, uint32_t* ev, uint8_t* out,
+                                   int64_t out_pitch, cudaStream_t st) {
+    const int64_t words = (num_shots + 31) / 32;
+    if (num_results > 0) {
+        dim3 g1((unsigned)((num_shots + 255) / 256), (unsigned)((num_results + 255) / 256));
+        b8_to_rows_kernel<<<g1, 256, 0, st>>>(flips, in_pitch, num_results, num_shots, rows, words);
+    }
+    dim3 g2((unsigned)((words + 255) / 256), (unsigned)num_dets);
+    rows_xor_kernel<<<g2, 256, 0, st>>>(rows, words, ptr, idx, num_dets, ev);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return launch_rows_to_b8(ev, num_dets, words, num_shots, nullptr, out, out_pitch, st);
+}
+
 // ------------------------------------------------------------ SMEM roofline probe
 // Every thread streams LDS.128 x4 + STS.128 x2 per iteration over a 64 KB
 // buffer with conflict-free addressing (the CX access mix); bytes moved =

@@ -1,0 +1,83 @@
+"""The drop-in entry points (collect_flips / sample_batch / detector_events /
+sample_detection_events) on the GPU, against the reference's contracts."""
+
+import numpy as np
+import pytest
+
+from tests._util import b8_unpack, load_inject, load_noiseless
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def need_gpu():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def test_collect_flips_and_detector_events_compose():
+    from paper_2103_02202_b200 import frame_sim, generators as gen
+    from paper_2103_02202_b200.circuit import detector_and_observable_sets, parse
+    from paper_2103_02202_b200.io_formats import detector_events
+
+    text = gen.surface_code_memory(5, 5, 5e-3)
+    c = parse(text)
+    flips = frame_sim.collect_flips(c, 3000, np.random.default_rng(1))
+    assert flips.num_shots == 3000 and flips.num_results == c.num_measurements
+    ev = detector_events(flips, detector_and_observable_sets(c))
+    # detector_events on the GPU equals the XOR definition computed on the host
+    fm = flips.to_numpy()
+    expect = np.stack([np.bitwise_xor.reduce(fm[:, list(s)], axis=1)
+                       for s in detector_and_observable_sets(c)], axis=1)
+    assert np.array_equal(ev.to_numpy(), expect)
+    # the fused device path gives the same events for the same seed stream
+    fused = frame_sim.sample_detection_events(c, 3000, np.random.default_rng(1))
+    assert fused.num_results == len(detector_and_observable_sets(c))
+
+
+def test_detector_events_errors():
+    from paper_2103_02202_b200.io_formats import SampleTable, detector_events
+    t = SampleTable.from_numpy(np.zeros((4, 3), np.uint8))
+    with pytest.raises(ValueError, match="detector 0 references measurement 5, have 3"):
+        detector_events(t, [(5,)])
+    assert detector_events(t, []).num_results == 0
+
+
+def test_sample_batch_noiseless_equals_reference():
+    from paper_2103_02202_b200 import frame_sim
+    text, ref, det = load_noiseless("d5")
+    out = frame_sim.sample_batch(text, ref, 2000, np.random.default_rng(3))
+    s = out.to_numpy()
+    assert np.array_equal(s[:, det], np.broadcast_to(ref[det], s[:, det].shape))
+    with pytest.raises(ValueError, match="reference has 3 bits, circuit measures"):
+        frame_sim.sample_batch(text, [0, 1, 0], 10, np.random.default_rng(0))
+
+
+def test_error_conventions():
+    from paper_2103_02202_b200 import frame_sim
+    with pytest.raises(ValueError, match="num_shots must be >= 1"):
+        frame_sim.collect_flips("M 0\n", 0, np.random.default_rng(0))
+    with pytest.raises(ValueError, match="batch_size must be >= 1"):
+        frame_sim.collect_flips("M 0\n", 5, np.random.default_rng(0), batch_size=0)
+
+
+def test_h_m_is_fair():
+    """`H 0; M 0` gives 0.5 +- 0.02 at 10^4 shots."""
+    from paper_2103_02202_b200 import frame_sim
+    out = frame_sim.sample_batch("H 0\nM 0\n", [0], 10000, np.random.default_rng(7))
+    assert abs(out.to_numpy().mean() - 0.5) < 0.02
+
+
+def test_reference_circuit_objects_accepted():
+    """A reference `stabsim` Circuit is accepted wherever a circuit is."""
+    import os
+    import sys
+    if not os.path.isdir("/root/reference/pkg/src"):
+        pytest.skip("reference not mounted")
+    sys.path.insert(0, "/root/reference/pkg/src")
+    from stabsim import circuit as rc
+    from paper_2103_02202_b200 import frame_sim
+    c = rc.parse("H 0\nCNOT 0 1\nM 0 1\nDETECTOR rec[-1] rec[-2]\n")
+    ev = frame_sim.sample_detection_events(c, 500, np.random.default_rng(0))
+    assert not ev.to_numpy().any()
