@@ -46,7 +46,7 @@ def parse_args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
-    ap.add_argument("--extra-d100", action="store_true", help="also time config 4 (d=100)")
+    ap.add_argument("--no-d100", action="store_true", help="skip the config 4 (d=100) extra line")
     return ap.parse_args()
 
 
@@ -193,25 +193,31 @@ def run_reference(args, rank, world):
 
 
 # ----------------------------------------------------------------- our arm
-def run_ours(args, rank, world, local_rank):
+def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, world: int,
+            local_rank: int, e2e_steps: int):
+    """Time `steps` sampling steps of config `cfg` (device-resident b8 output),
+    then the per-kernel durations (CUDA events inside pfs_run), then e2e."""
     import torch
 
-    from paper_2103_02202_b200.sampler import compile_detector_sampler, pinned_empty
+    from paper_2103_02202_b200 import _native as N
+    from paper_2103_02202_b200.program import flatten
+    from paper_2103_02202_b200.sampler import DetectorSampler, pinned_empty
 
     dist = world > 1
     if dist:
         import torch.distributed as tdist
-    torch.cuda.set_device(local_rank)
     dev = torch.device("cuda", local_rank)
-    text = config_text(args.config)
-    from paper_2103_02202_b200 import generators as gen
-    shots = args.shots or gen.CONFIGS[args.config]["shots"]
-    ds = compile_detector_sampler(text, device=local_rank, words_per_tile=args.words,
-                                  ring_in_smem=args.ring, threads=args.threads,
-                                  noise_target_hits=args.target_hits, timing=True)
+    t0 = time.perf_counter()
+    flat = flatten(config_text(cfg))
+    compile_s = time.perf_counter() - t0
+    kw = dict(words_per_tile=args.words, ring_in_smem=args.ring, threads=args.threads,
+              noise_target_hits=args.target_hits)
+    ds = DetectorSampler.__new__(DetectorSampler)
+    ds.circuit, ds.flat, ds.device = None, flat, local_rank
+    ds._seeds = np.random.default_rng(0)
+    ds.native = N.NativeProgram(flat, **kw)
     info = ds.info
     T = ds.tile_shots
-    shots = max(T, (shots // T) * T) if args.shots else shots
     nb = (ds.num_columns + 7) // 8
     stream = torch.cuda.current_stream(dev)
     sp = stream.cuda_stream
@@ -221,26 +227,22 @@ def run_ours(args, rank, world, local_rank):
     base_offset = rank * ((shots + T - 1) // T) * T
     seed = 20260214
 
-    def step(i):
-        ds.sample(shots, seed=seed + i, out=out, shot_offset=base_offset, stream=sp)
+    def step(sampler, i):
+        sampler.sample(shots, seed=seed + i, out=out, shot_offset=base_offset, stream=sp)
 
-    for i in range(args.warmup):
-        step(i)
+    for i in range(warmup):
+        step(ds, i)
     torch.cuda.synchronize()
     if dist:
         tdist.barrier()
     torch.cuda.synchronize()
-    frame_ms, tr_ms = [], []
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     launches = 0
     with ClockSampler(local_rank) as clk:
         ev0.record(stream)
-        for i in range(args.steps):
-            step(args.warmup + i)
-            t = ds.native.last_timing()
-            frame_ms.append(t[0])
-            tr_ms.append(t[1])
+        for i in range(steps):
+            step(ds, warmup + i)
             launches += ds.native.last_launches()
         ev1.record(stream)
         torch.cuda.synchronize()
@@ -249,20 +251,34 @@ def run_ours(args, rank, world, local_rank):
         tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
         tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
         elapsed = float(tt.item())
-    total_shots = shots * world * args.steps
-    value = total_shots / elapsed
-    clocks = clk.summary()
+    res = {"cfg": cfg, "shots": shots, "steps": steps, "elapsed": elapsed,
+           "value": shots * world * steps / elapsed, "clocks": clk.summary(),
+           "launches": launches, "info": info, "nb": nb, "compile_s": compile_s}
 
-    # e2e: the public API with a pinned HOST output buffer (D2H inside the step)
-    e2e = None
-    if not args.no_e2e:
+    # per-kernel durations: CUDA events recorded on the launching stream inside pfs_run
+    dt = DetectorSampler.__new__(DetectorSampler)
+    dt.circuit, dt.flat, dt.device = None, flat, local_rank
+    dt._seeds = np.random.default_rng(0)
+    dt.native = N.NativeProgram(flat, timing=True, **kw)
+    fr, tr = [], []
+    for i in range(max(3, min(steps, 10))):
+        step(dt, i)
+        t = dt.native.last_timing()
+        if i:
+            fr.append(t[0])
+            tr.append(t[1])
+    res["frame_ms"] = float(np.mean(fr))
+    res["transpose_ms"] = float(np.mean(tr))
+    del dt
+
+    if e2e_steps > 0:
         host, _keep = pinned_empty((shots, nb), np.uint8)
         ds.sample(shots, seed=1, out=host, shot_offset=base_offset)
         torch.cuda.synchronize()
         if dist:
             tdist.barrier()
         t0 = time.perf_counter()
-        for i in range(args.steps):
+        for i in range(e2e_steps):
             ds.sample(shots, seed=seed + i, out=host, shot_offset=base_offset)
         torch.cuda.synchronize()
         e_el = time.perf_counter() - t0
@@ -270,58 +286,99 @@ def run_ours(args, rank, world, local_rank):
             tt = torch.tensor([e_el], device=dev, dtype=torch.float64)
             tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
             e_el = float(tt.item())
-        e2e = {"value": total_shots / e_el, "unit": "shots/s", "h2d_bytes_per_step": 0,
-               "d2h_bytes_per_step": int(shots * nb * world),
-               "note": "public API DetectorSampler.sample(out=pinned host array); per step the "
-                       "inputs are (seed, shot range) only - the compiled program is resident"}
+        res["e2e"] = {"value": shots * world * e2e_steps / e_el, "unit": "shots/s",
+                      "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(shots * nb * world),
+                      "steps": e2e_steps,
+                      "note": "public API DetectorSampler.sample(out=pinned host ndarray): frame "
+                              "kernel + transpose + D2H of the b8 events in a double-buffered "
+                              "chunk pipeline; per-step inputs are (seed, shot range) only"}
+        del host, _keep
+    del out_full, out
+    torch.cuda.empty_cache()
+    return res
 
+
+def roofline_of(res, smem_peak, hbm):
+    info = res["info"]
+    bframe_bytes = info["bframe_bits"] / 8.0
+    fr = res["frame_ms"]
+    achieved = bframe_bytes * res["shots"] / (fr / 1e3) / 1e9
+    return {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+            "frac": achieved / smem_peak, "traffic": profile_traffic(),
+            "peak_source": "measured live: pfs_measure_smem_bandwidth (LDS.128/STS.128 CX mix, "
+                           "all SMs)",
+            "kernel": "frame_kernel (frame table resident in shared memory)",
+            "frame_kernel_ms": fr, "transpose_kernel_ms": res["transpose_ms"],
+            "bytes_per_shot": bframe_bytes,
+            "hbm_equiv": {"achieved_gbs": achieved, "peak_gbs": hbm, "frac": achieved / hbm,
+                          "note": "frame-update GB/s vs measured HBM copy peak (BASELINE.json "
+                                  "metric wording); the frame table never streams through HBM"}}
+
+
+def run_ours(args, rank, world, local_rank):
+    import torch
+
+    from paper_2103_02202_b200 import generators as gen
+    from paper_2103_02202_b200._native import measure_smem_bandwidth
+
+    torch.cuda.set_device(local_rank)
+    shots = args.shots or gen.CONFIGS[args.config]["shots"]
+    main = measure(args, args.config, shots, args.steps, args.warmup, rank, world, local_rank,
+                   0 if args.no_e2e else max(2, args.steps // 4))
+    extra = None
+    if args.config == 2 and not args.no_d100:
+        s4 = gen.CONFIGS[4]["shots"]
+        extra = measure(args, 4, s4, max(3, args.steps // 4), 3, rank, world, local_rank,
+                        0 if args.no_e2e else 2)
     if rank != 0:
         return
     peaks = measured_peaks()
     hbm = float(peaks.get("hbm_gbs", 6469.6))
-    bframe_bytes = info["bframe_bits"] / 8.0
-    fr = float(np.mean(frame_ms)) if frame_ms else float("nan")
-    achieved_gbs = bframe_bytes * shots / (fr / 1e3) / 1e9
-    from paper_2103_02202_b200._native import measure_smem_bandwidth
     smem_peak = measure_smem_bandwidth(local_rank)
-    roof = {"bound": "smem" if smem_peak else "hbm",
-            "achieved": achieved_gbs, "peak": smem_peak or hbm, "unit": "GB/s",
-            "frac": achieved_gbs / (smem_peak or hbm), "traffic": profile_traffic(),
-            "peak_source": "measured live: pfs_measure_smem_bandwidth (LDS.128/STS.128 CX mix, all SMs)",
-            "kernel": "frame_kernel (SMEM-resident frame table)",
-            "frame_kernel_ms": fr, "transpose_kernel_ms": float(np.mean(tr_ms)),
-            "bytes_per_shot": bframe_bytes,
-            "hbm_equiv": {"achieved_gbs": achieved_gbs, "peak_gbs": hbm,
-                          "frac": achieved_gbs / hbm,
-                          "note": "frame-update GB/s vs measured HBM copy peak "
-                                  "(BASELINE.json metric); >1 because the frame table is "
-                                  "SMEM-resident, never streamed from HBM"}}
+    info = main["info"]
+    T = info["tile_shots"]
+    workloads = {2: "config2: rotated surface code Z-memory d=25 r=25 p=1e-3",
+                 4: "config4: rotated surface code Z-memory d=100 r=100 p=1e-3",
+                 0: "config0: d=3 r=3 p=1e-3", 1: "config1: random Clifford n=64 x200 layers",
+                 3: "config3: d=5 r=5 p=5e-3"}
     line = {
-        "metric": "surface-code detection-event shots/sec (d=25, 25 rounds, p=1e-3)",
-        "value": value, "unit": "shots/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * elapsed / args.steps,
+        "metric": "surface-code detection-event shots/sec (d=25 & d=100, p=1e-3); frame-update "
+                  "GB/s vs peak",
+        "value": main["value"], "unit": "shots/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * main["elapsed"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded circuit-level noise, counter-based Philox)",
-        "config": {"workload": f"config{args.config}: rotated surface code Z-memory d=25 r=25 "
-                               "p=1e-3, detection events + observable, shot-major b8 in HBM",
-                   "shots_per_gpu_per_step": shots, "columns": ds.num_columns,
+        "config": {"workload": workloads.get(args.config, f"config{args.config}") +
+                   ", detection events + observable, shot-major b8 in HBM",
+                   "shots_per_gpu_per_step": main["shots"], "columns": info["num_columns"],
                    "W": info["words_per_tile"], "tile_shots": T,
                    "ring_in_smem": info["ring_in_smem"], "threads": info["threads"],
-                   "l2": f"outputs {shots * nb / 1e9:.2f} GB/step > 126 MB L2 (no flush needed)",
-                   "parallelism": f"shots sharded x{world}"},
-        "roofline": roof,
-        "clocks": clocks,
-        "gpu_launches": launches,
+                   "l2": f"outputs {main['shots'] * main['nb'] / 1e9:.2f} GB/step > 126 MB L2 "
+                         "(no flush needed)",
+                   "parallelism": f"shots sharded x{world} (global shot offsets)"},
+        "roofline": roofline_of(main, smem_peak, hbm),
+        "clocks": main["clocks"],
+        "gpu_launches": main["launches"],
     }
-    if e2e:
-        line["e2e"] = e2e
+    if "e2e" in main:
+        line["e2e"] = main["e2e"]
+    if extra is not None:
+        x = {"workload": workloads[4] + ", detection events + observable, shot-major b8 in HBM",
+             "value": extra["value"], "unit": "shots/s", "shots_per_gpu_per_step": extra["shots"],
+             "ms_per_step": 1e3 * extra["elapsed"] / extra["steps"], "steps": extra["steps"],
+             "host_compile_s": extra["compile_s"],
+             "roofline": roofline_of(extra, smem_peak, hbm), "clocks": extra["clocks"],
+             "W": extra["info"]["words_per_tile"], "gpu_launches": extra["launches"]}
+        if "e2e" in extra:
+            x["e2e"] = extra["e2e"]
+        line["d100"] = x
     if not args.no_cpu_baseline:
         cores = host_cores()
-        rate, s_shots, dt = cpu_port_rate(text, args.cpu_seconds, cores)
+        rate, s_shots, dt = cpu_port_rate(config_text(args.config), args.cpu_seconds, cores)
         line["cpu_baseline"] = {"value": rate, "unit": "shots/s", "cores": cores, "kind": "port",
                                 "sample": f"{s_shots} shots of config {args.config} in "
                                           f"{dt:.1f}s on {cores} threads ({cpu_model()}); C "
-                                          "restatement of stabsim frame_sim+detector_events"}
+                                          "restatement of stabsim frame_sim+detector_events+b8"}
     print(json.dumps(line), flush=True)
 
 

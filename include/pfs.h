@@ -50,7 +50,9 @@ typedef struct pfs_options {
                                  apply, bit1 noise pre-pass, bit2 coin RNG, bit3 detectors,
                                  bit4 gates, bit5 collapses */
     int32_t producer_threads; /* threads sampling the next tile's noise (0 = auto)   */
-    int32_t reserved[5];
+    int32_t schedule_only;    /* 1: compile without the shared-memory fit check (the
+                                 program exposes info / noise schedule, cannot run)  */
+    int32_t reserved[4];
 } pfs_options;
 
 typedef struct pfs_info {

@@ -95,7 +95,8 @@ def noise_schedule(prog: FlatProgram, tile_shots: int):
     (pure host code, no GPU needed)."""
     from paper_2103_02202_b200._native import NativeProgram
 
-    return NativeProgram(prog, words_per_tile=tile_shots // 32, ring_in_smem=0).noise_schedule()
+    return NativeProgram(prog, words_per_tile=tile_shots // 32, ring_in_smem=0,
+                         schedule_only=True).noise_schedule()
 
 
 def _pad_rows(a, words):

@@ -151,7 +151,8 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         return fail(PFS_E_NOMEM, "out of host memory");
     }
     choose_layout(pg);
-    if (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget) {
+    if (pg->opts.schedule_only && pg->cfg.W < 1) pg->cfg.W = pg->opts.words_per_tile > 0 ? pg->opts.words_per_tile : 1;
+    if (!pg->opts.schedule_only && (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget)) {
         delete pg;
         return fail(PFS_E_INVALID, "frame table of " + std::to_string(num_qubits) +
                                        " qubits does not fit one CTA's shared memory");
@@ -256,8 +257,8 @@ static int ensure_device(pfs_program* pg, int device) {
     if (prop.major != 10) return fail(PFS_E_NODEVICE, "libpfs is built for sm_100a (B200) only");
     pg->num_sms = prop.multiProcessorCount;
     pg->smem_optin = prop.sharedMemPerBlockOptin;
-    if (pg->cfg.smem_bytes > pg->smem_optin)
-        return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory");
+    if (pg->cfg.smem_bytes > pg->smem_optin || pg->opts.schedule_only)
+        return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory (or schedule-only program)");
     const HostProgram& hp = pg->hp;
     CUDA_TRY(upload(pg->d_ops, hp.ops));
     CUDA_TRY(upload(pg->d_targets, hp.targets));
