@@ -304,7 +304,9 @@ def roofline_of(res, smem_peak, hbm):
     fr = res["frame_ms"]
     achieved = bframe_bytes * res["shots"] / (fr / 1e3) / 1e9
     return {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-            "frac": achieved / smem_peak, "traffic": profile_traffic(),
+            "frac": achieved / smem_peak,
+            "traffic": profile_traffic(res["shots"]) if res["cfg"] == 2 else None,
+            "traffic_source": "profiles/frame_kernel_traffic.json (ncu --set full, per shot)",
             "peak_source": "measured live: pfs_measure_smem_bandwidth (LDS.128/STS.128 CX mix, "
                            "all SMs)",
             "kernel": "frame_kernel (frame table resident in shared memory)",
@@ -391,11 +393,14 @@ def smem_peak_gbs():
         return None
 
 
-def profile_traffic():
+def profile_traffic(shots=None):
+    """DRAM bytes per frame-kernel launch from the committed ncu capture
+    (profiles/frame_kernel_traffic.json, per shot x this launch's shots)."""
     p = os.path.join(REPO, "profiles", "frame_kernel_traffic.json")
     try:
         with open(p) as f:
-            return json.load(f).get("dram_bytes_per_launch")
+            d = json.load(f)
+        return float(d["dram_bytes_per_shot"]) * shots if shots else None
     except Exception:
         return None
 
