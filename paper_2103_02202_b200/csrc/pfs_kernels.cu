@@ -269,8 +269,20 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
     unsigned long long t0 = 0, t1 = 0;
     const uint32_t* tg = nullptr;
     int ar = 1;
-    for (int item = warp; item < total; item += nwarps) {
-        while (k < 0 || (uint32_t)item >= next_base) {  // op cursor (monotone)
+    // contiguous item ranges per warp: a warp crosses few op boundaries
+    const int per = (total + nwarps - 1) / nwarps;
+    const int item_end = min(total, (warp + 1) * per);
+    if (warp * per < item_end) {  // first op: binary search on item bases
+        int lo = 0, hi = kp.num_pregen - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if ((int)__ldg(&kp.noise[__ldg(kp.pregen_ops + mid)].chunk_base) <= warp * per) lo = mid;
+            else hi = mid - 1;
+        }
+        k = lo - 1;
+    }
+    for (int item = warp * per; item < item_end; item++) {
+        while (next_base == 0 || (uint32_t)item >= next_base) {  // op cursor (monotone)
             k++;
             ord = __ldg(kp.pregen_ops + k);
             np = kp.noise[ord];
