@@ -260,15 +260,17 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     dt.circuit, dt.flat, dt.device = None, flat, local_rank
     dt._seeds = np.random.default_rng(0)
     dt.native = N.NativeProgram(flat, timing=True, **kw)
-    fr, tr = [], []
+    fr, tr, nz = [], [], []
     for i in range(max(3, min(steps, 10))):
         step(dt, i)
         t = dt.native.last_timing()
         if i:
             fr.append(t[0])
             tr.append(t[1])
+            nz.append(t[5])
     res["frame_ms"] = float(np.mean(fr))
     res["transpose_ms"] = float(np.mean(tr))
+    res["noise_ms"] = float(np.mean(nz))
     del dt
 
     if e2e_steps > 0:
@@ -311,6 +313,7 @@ def roofline_of(res, smem_peak, hbm):
                            "all SMs)",
             "kernel": "frame_kernel (frame table resident in shared memory)",
             "frame_kernel_ms": fr, "transpose_kernel_ms": res["transpose_ms"],
+            "noise_kernel_ms": res["noise_ms"],
             "bytes_per_shot": bframe_bytes,
             "hbm_equiv": {"achieved_gbs": achieved, "peak_gbs": hbm, "frac": achieved / hbm,
                           "note": "frame-update GB/s vs measured HBM copy peak (BASELINE.json "

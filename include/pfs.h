@@ -135,8 +135,9 @@ int pfs_run(struct pfs_program* prog, int device, uint64_t seed, uint64_t shot_o
             int64_t inject_row_words, void* out, int64_t out_bytes, int64_t out_pitch,
             void* stream);
 
-/* Per-kernel times (ms) of the last pfs_run when options.timing = 1:
- * [0] frame program kernel, [1] transpose kernel, [2] H2D, [3] D2H, [4] total. */
+/* Per-kernel times (ms) of the last pfs_run when options.timing = 1 (first
+ * chunk): [0] frame program kernel, [1] transpose kernel, [2] H2D, [3] D2H,
+ * [4] total, [5] noise sampling kernel. */
 int pfs_program_last_timing(const struct pfs_program* prog, double* ms, int n);
 
 /* Number of this library's kernel launches made by the last pfs_run. */

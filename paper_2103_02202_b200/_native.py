@@ -187,8 +187,8 @@ class NativeProgram:
                              out_bytes, out_pitch, stream or None))
 
     def last_timing(self) -> list:
-        arr = (ctypes.c_double * 5)()
-        _check(lib().pfs_program_last_timing(self._h, arr, 5))
+        arr = (ctypes.c_double * 6)()
+        _check(lib().pfs_program_last_timing(self._h, arr, 6))
         return list(arr)
 
     def last_launches(self) -> int:

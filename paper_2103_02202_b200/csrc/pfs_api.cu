@@ -64,20 +64,21 @@ struct pfs_program {
     DevBuf<uint64_t> d_noise_tab;
     DevBuf<uint32_t> d_pregen, d_noise_off, d_noise_ch;
     DevBuf<uint64_t> d_hits;
+    DevBuf<uint32_t> d_ncnt;
     DevBuf<uint32_t> d_rows[2];
     DevBuf<uint8_t> d_b8[2];
     DevBuf<uint32_t> d_coins, d_masks;
     DevBuf<uint8_t> d_ref;
     DevBuf<unsigned long long> d_counts;
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t ev[8] = {};
-    double last_ms[5] = {0, 0, 0, 0, 0};
+    cudaEvent_t ev[10] = {};
+    double last_ms[6] = {0, 0, 0, 0, 0, 0};
     int64_t last_launches = 0;
 };
 
-// noise counters (2 buffers) + the sampler's per-thread duplicate-check scratch
+// this tile's per-op hit counts + the inline sampler's per-lane scratch
 static size_t fixed_smem(const HostProgram& hp) {
-    return (size_t)hp.num_noise * 8 + (size_t)(FRAME_MAX_THREADS / 32) * (256 + 32 * NZ_MAX_LIST) * 4;
+    return (size_t)hp.num_noise * 4 + (size_t)(FRAME_MAX_THREADS / 32) * (32 * NZ_MAX_LIST) * 4;
 }
 
 static void choose_layout(pfs_program* pg) {
@@ -210,7 +211,7 @@ int pfs_program_noise_schedule(const pfs_program* pg, uint32_t* params, int64_t 
 
 int pfs_program_last_timing(const pfs_program* pg, double* ms, int n) {
     if (!pg || !ms) return fail(PFS_E_INVALID, "null argument");
-    for (int i = 0; i < n && i < 5; i++) ms[i] = pg->last_ms[i];
+    for (int i = 0; i < n && i < 6; i++) ms[i] = pg->last_ms[i];
     return PFS_OK;
 }
 
@@ -225,7 +226,7 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_ops.release(); pg->d_targets.release(); pg->d_det_ptr.release();
         pg->d_det_terms.release(); pg->d_ring.release(); pg->d_noise.release();
         pg->d_noise_tab.release(); pg->d_pregen.release(); pg->d_hits.release();
-        pg->d_noise_off.release(); pg->d_noise_ch.release();
+        pg->d_noise_off.release(); pg->d_noise_ch.release(); pg->d_ncnt.release();
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
@@ -277,7 +278,6 @@ static int ensure_device(pfs_program* pg, int device) {
         per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / pg->cfg.threads));
     }
     pg->cfg.grid = pg->num_sms * per_sm;
-    CUDA_TRY(pg->d_hits.reserve((size_t)std::max<int64_t>(hp.hit_capacity, 1) * 2 * pg->cfg.grid));
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
     for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
     pg->device = device;
@@ -291,6 +291,51 @@ static bool is_device_ptr(const void* p) {
         return false;
     }
     return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// Run nt tiles: noise_kernel (per-tile hit lists) then frame_kernel, in
+// sub-chunks bounded by the hit-list buffer budget.  kp describes tile 0 of
+// the range (tile_offset, output and inject pointers, num_shots).
+static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64_t nt, bool injected,
+                        cudaStream_t st, bool time_noise) {
+    const HostProgram& hp = pg->hp;
+    const int W = cfg.W;
+    const int64_t T = 32 * W;
+    const bool pregen = !injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2);
+    int64_t sub = nt;
+    if (pregen) {
+        const int64_t per_tile = hp.hit_capacity * 8 + hp.num_noise * 4;
+        const int64_t budget = (int64_t)1536 << 20;
+        sub = std::max<int64_t>(cfg.grid, budget / std::max<int64_t>(per_tile, 1));
+        sub = std::min(sub, nt);
+        CUDA_TRY(pg->d_hits.reserve((size_t)std::max<int64_t>(hp.hit_capacity, 1) * sub));
+        CUDA_TRY(pg->d_ncnt.reserve((size_t)std::max<int64_t>(hp.num_noise, 1) * sub));
+    }
+    for (int64_t s0 = 0; s0 < nt; s0 += sub) {
+        const int64_t ns = std::min(sub, nt - s0);
+        KParams k2 = kp;
+        k2.n_tiles = ns;
+        k2.tile_offset = kp.tile_offset + (uint64_t)s0;
+        k2.num_shots = std::min<int64_t>(kp.num_shots - s0 * T, ns * T);
+        if (k2.rec_out) k2.rec_out += s0 * kp.out_tile_stride;
+        if (k2.ev_out) k2.ev_out += s0 * kp.out_tile_stride;
+        if (k2.coins) k2.coins += s0 * W;
+        if (k2.masks) k2.masks += s0 * W;
+        if (pregen) {
+            k2.hits_global = pg->d_hits.p;
+            k2.ncnt_global = pg->d_ncnt.p;
+            CUDA_TRY(cudaMemsetAsync(pg->d_ncnt.p, 0, (size_t)hp.num_noise * ns * 4, st));
+            if (time_noise && s0 == 0) CUDA_TRY(cudaEventRecord(pg->ev[8], st));
+            CUDA_TRY(launch_noise_kernel(W, k2, ns, st));
+            if (time_noise && s0 == 0) CUDA_TRY(cudaEventRecord(pg->ev[9], st));
+            pg->last_launches++;
+        }
+        LaunchCfg lc = cfg;
+        lc.grid = (int)std::min<int64_t>(cfg.grid, ns);
+        CUDA_TRY(launch_frame_kernel(lc, k2, st));
+        pg->last_launches++;
+    }
+    return PFS_OK;
 }
 
 extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot_offset,
@@ -374,7 +419,6 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.noise = pg->d_noise.p;
     kp.noise_tab = pg->d_noise_tab.p;
     kp.pregen_ops = pg->d_pregen.p;
-    kp.hits_global = pg->d_hits.p;
     kp.hit_capacity = hp.hit_capacity;
     kp.num_noise = (int32_t)hp.num_noise;
     kp.num_pregen = (int32_t)hp.pregen_ops.size();
@@ -383,8 +427,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.noise_ch = pg->d_noise_ch.p;
     kp.first_pregen = hp.first_pregen;
     kp.first_cap_base = hp.first_cap_base;
-    kp.producers = hp.pregen_ops.empty() ? 0 : (pg->opts.producer_threads > 0 ? pg->opts.producer_threads : 256);
-    if (kp.producers >= pg->cfg.threads) kp.producers = pg->cfg.threads / 2;
+
     kp.coins = injected ? pg->d_coins.p : nullptr;
     kp.masks = injected ? pg->d_masks.p : nullptr;
     kp.inject_words = words_all;
@@ -423,10 +466,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             kp.tile_offset = shot_offset / T + t0;
             kp.num_shots = std::min<int64_t>(num_shots - t0 * T, nt * T);
             if (injected) { kp.coins = pg->d_coins.p + t0 * W; kp.masks = pg->d_masks.p + t0 * W; }
-            LaunchCfg lc = cfg;
-            lc.grid = (int)std::min<int64_t>(cfg.grid, nt);
-            CUDA_TRY(launch_frame_kernel(lc, kp, st));
-            pg->last_launches++;
+            int rc2 = launch_tiles(pg, kp, cfg, nt, injected, st, false);
+            if (rc2) return rc2;
         }
         if (timing) CUDA_TRY(cudaEventRecord(pg->ev[2], st));
         if (!dev_out && hp.num_cols > 0)
@@ -491,11 +532,11 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             kp.rec_out = rows_meas ? rows : nullptr;
             kp.ev_out = rows_meas ? nullptr : rows;
         }
-        LaunchCfg lc = cfg;
-        lc.grid = (int)std::min<int64_t>(cfg.grid, nt);
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[2], st));
-        CUDA_TRY(launch_frame_kernel(lc, kp, st));
-        pg->last_launches++;
+        {
+            int rc2 = launch_tiles(pg, kp, cfg, nt, injected, st, timing && ci == 0);
+            if (rc2) return rc2;
+        }
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[3], st));
         if (b8) {
             uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
@@ -511,6 +552,12 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (timing && ci == 0) {
             CUDA_TRY(cudaStreamSynchronize(st));
             cudaEventElapsedTime(&frame_ms, pg->ev[2], pg->ev[3]);
+            if (!injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2)) {
+                float nz = 0;
+                cudaEventElapsedTime(&nz, pg->ev[8], pg->ev[9]);
+                pg->last_ms[5] = nz;
+                frame_ms -= nz;  // [0] = frame kernel alone, [5] = noise kernel
+            }
             if (b8) cudaEventElapsedTime(&tr_ms, pg->ev[3], pg->ev[5]);
         }
         if (!dev_out) {

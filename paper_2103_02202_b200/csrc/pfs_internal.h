@@ -133,7 +133,8 @@ struct KParams {
     uint32_t* ev_out;            // [cols][out_words] or null
     unsigned long long* counts;  // [cols] or null
     uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
-    uint64_t* hits_global;       // [grid][2][hit_capacity] pre-generated noise hits
+    uint64_t* hits_global;       // [tiles][hit_capacity] pre-sampled noise hits (noise_kernel)
+    uint32_t* ncnt_global;       // [tiles][num_noise] hits per noise op
     int64_t inject_words;
     int64_t out_row_stride;      // output word address = row * out_row_stride
     int64_t out_tile_stride;     //                     + tile * out_tile_stride + word
@@ -168,6 +169,7 @@ struct LaunchCfg {
 
 size_t frame_smem_bytes(int num_qubits, int W);
 cudaError_t launch_frame_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStream_t stream);
+cudaError_t launch_noise_kernel(int W, const KParams& kp, int64_t n_tiles, cudaStream_t stream);
 cudaError_t set_frame_kernel_smem(const LaunchCfg& cfg);
 cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t row_words,
                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,

@@ -260,28 +260,25 @@ __device__ __forceinline__ uint64_t hit_entry(const uint32_t* tg, int ar, uint32
 
 template <int W>
 __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uint32_t* ncnt,
-                                              uint64_t* hits, int warp, int nwarps, uint32_t* wscr) {
+                                              uint64_t* hits, int item_begin, int item_end,
+                                              uint32_t* wscr) {
     const int lane = threadIdx.x & 31;
-    const int total = kp.pregen_chunks;  // work items (32-chunk blocks) per tile
     int k = -1;
     uint32_t ord = 0, item_base = 0, next_base = 0, ch = 0;
     NoiseParam np{};
     unsigned long long t0 = 0, t1 = 0;
     const uint32_t* tg = nullptr;
     int ar = 1;
-    // contiguous item ranges per warp: a warp crosses few op boundaries
-    const int per = (total + nwarps - 1) / nwarps;
-    const int item_end = min(total, (warp + 1) * per);
-    if (warp * per < item_end) {  // first op: binary search on item bases
+    if (item_begin < item_end) {  // first op: binary search on item bases
         int lo = 0, hi = kp.num_pregen - 1;
         while (lo < hi) {
             const int mid = (lo + hi + 1) >> 1;
-            if ((int)__ldg(&kp.noise[__ldg(kp.pregen_ops + mid)].chunk_base) <= warp * per) lo = mid;
+            if ((int)__ldg(&kp.noise[__ldg(kp.pregen_ops + mid)].chunk_base) <= item_begin) lo = mid;
             else hi = mid - 1;
         }
         k = lo - 1;
     }
-    for (int item = warp * per; item < item_end; item++) {
+    for (int item = item_begin; item < item_end; item++) {
         while (next_base == 0 || (uint32_t)item >= next_base) {  // op cursor (monotone)
             k++;
             ord = __ldg(kp.pregen_ops + k);
@@ -410,6 +407,24 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
     }
 }
 
+// Noise sampling kernel: runs before the frame kernel over every tile of the
+// launch at full occupancy (no shared-memory frame), writing each tile's hit
+// lists and per-op hit counts to global memory (L2-resident for a chunk).
+// grid = (ceil(items / (8 * NZ_ITEMS_PER_WARP)), tiles), 256 threads.
+constexpr int NZ_ITEMS_PER_WARP = 4;
+template <int W>
+__global__ void __launch_bounds__(256) noise_kernel(const __grid_constant__ KParams kp) {
+    __shared__ uint32_t wscr_all[8][256 + 32 * NZ_MAX_LIST];
+    const int warp = threadIdx.x >> 5;
+    const int64_t tile = blockIdx.y;
+    const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
+    const int wi = blockIdx.x * 8 + warp;
+    const int b = wi * NZ_ITEMS_PER_WARP;
+    const int e = min(kp.pregen_chunks, b + NZ_ITEMS_PER_WARP);
+    noise_prepass<W>(kp, g, kp.ncnt_global + tile * kp.num_noise,
+                     kp.hits_global + tile * kp.hit_capacity, b, e, wscr_all[warp]);
+}
+
 // Items of one op, U per thread per batch: all U operand loads (L2-resident
 // target indices) are issued before any of the dependent shared-memory work.
 template <int U, typename Load, typename Work>
@@ -430,11 +445,9 @@ __device__ __forceinline__ void batched_items(int tid, int nth, int items, Load 
 }
 
 // ------------------------------------------------------------ frame kernel
-// Warp-specialised persistent kernel.  Threads [0, nc) are consumers: they
-// run the op stream of tile i on the frame in shared memory, synchronising on
-// named barrier 1.  Threads [nc, blockDim) are producers: meanwhile they
-// sample the noise of tile i+1 into the other hit-list buffer.  One full
-// __syncthreads per tile hands the buffers over.
+// Persistent kernel: each CTA runs the op stream over its tiles with the frame
+// in shared memory; noise comes pre-sampled per tile from noise_kernel (hit
+// lists in global memory), applied with shared-memory atomics.
 template <int W, bool RING_SMEM>
 __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __grid_constant__ KParams kp) {
     constexpr int V = W >= 4 ? 4 : W;  // words per vector access
@@ -447,51 +460,24 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     uint32_t* const ring = RING_SMEM ? (smem + (size_t)2 * n * W)
                                      : (kp.ring_global + (size_t)blockIdx.x * kp.num_slots * W);
     uint32_t* const cnt = smem + (size_t)2 * n * W + (RING_SMEM ? (size_t)kp.num_slots * W : 0);
-    uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // [2][num_noise]
-    uint64_t* const hits0 = kp.hits_global + (size_t)blockIdx.x * 2 * kp.hit_capacity;
+    uint32_t* const ncnt = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // this tile's hits per op
     const int tid = threadIdx.x;
-    // per-warp scratch of the noise sampler: 256 positions + 32 x NZ_MAX_LIST
-    // per-lane duplicate-check slots (also used by the consumers' inline path)
-    uint32_t* const nscr = ncnt0 + 2 * kp.num_noise;
-    uint32_t* const wscr = nscr + (tid >> 5) * (256 + 32 * NZ_MAX_LIST);
-    uint32_t* const sl = wscr + 256 + (tid & 31) * NZ_MAX_LIST;
+    // per-warp scratch of the inline noise sampler (large-p ops / list overflow)
+    uint32_t* const nscr = ncnt + kp.num_noise;
+    uint32_t* const sl = nscr + (tid >> 5) * (32 * NZ_MAX_LIST) + (tid & 31) * NZ_MAX_LIST;
     const int ss = 1;
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
-    const int nprod = pregen ? kp.producers : 0;
-    const int nth = blockDim.x - nprod;  // consumer threads
-    const bool is_consumer = tid < nth;
+    const int nth = blockDim.x;
 
     if (kp.counts_in_smem) {
-        for (int i = tid; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
+        for (int i = tid; i < kp.num_cols; i += nth) cnt[i] = 0u;
     }
-    // prologue: every thread samples the first tile's noise into buffer 0
-    if (pregen && (int64_t)blockIdx.x < kp.n_tiles) {
-        for (int i = tid; i < kp.num_noise; i += blockDim.x) ncnt0[i] = 0u;
-        __syncthreads();
-        noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + blockIdx.x), ncnt0, hits0, tid >> 5,
-                         blockDim.x >> 5, wscr);
-    }
-    __syncthreads();
 
-    int it = 0;
-    for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x, it++) {
-        const int buf = it & 1;
-        uint32_t* const ncnt = ncnt0 + buf * kp.num_noise;
-        uint64_t* const hits = hits0 + (size_t)buf * kp.hit_capacity;
+    for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x) {
         const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
-        if (!is_consumer) {
-            // ---- producers: noise of this CTA's next tile into the other buffer ----
-            const int64_t nt = tile + gridDim.x;
-            if (nt < kp.n_tiles) {
-                uint32_t* const ncn = ncnt0 + (buf ^ 1) * kp.num_noise;
-                const int pt = tid - nth;
-                for (int i = pt; i < kp.num_noise; i += nprod) ncn[i] = 0u;
-                asm volatile("bar.sync 2, %0;" ::"r"(nprod) : "memory");
-                noise_prepass<W>(kp, (uint32_t)(kp.tile_offset + (uint64_t)nt), ncn,
-                                 hits0 + (size_t)(buf ^ 1) * kp.hit_capacity, pt >> 5, nprod >> 5, wscr);
-            }
-        } else {
-            // ---- consumers: FrameBatch.__init__: x = 0, z = coins (frame_sim.py:36-39) ----
+        const uint64_t* const hits = kp.hits_global + tile * kp.hit_capacity;
+        {
+            // ---- FrameBatch.__init__: x = 0, z = coins (frame_sim.py:36-39) ----
             for (int i = tid; i < (n << LC); i += nth) {
                 const int q = i >> LC, c = i & (C - 1);
                 vst<V>(X + (size_t)q * W + c * V, vzero<V>());
@@ -501,11 +487,14 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 const int k = i >> LC, c = i & (C - 1);
                 vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
             }
+            if (pregen)
+                for (int i = tid; i < kp.num_noise; i += nth) ncnt[i] = kp.ncnt_global[tile * kp.num_noise + i];
             // register prefetch of the first pre-generated noise op's hit `tid`
             uint32_t pf_ord = pregen ? kp.first_pregen : NO_SLOT;
             uint64_t pf_hit = 0;
-            if (pf_ord != NO_SLOT && (uint32_t)tid < ncnt[pf_ord]) pf_hit = hits[kp.first_cap_base + tid];
-            consumer_sync(nth);
+            if (pf_ord != NO_SLOT && (uint32_t)tid < kp.ncnt_global[tile * kp.num_noise + pf_ord])
+                pf_hit = hits[kp.first_cap_base + tid];
+            __syncthreads();
 
             uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
             for (int oi = 0; oi < kp.n_ops; oi++) {
@@ -516,7 +505,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 // prefetch the next op's first half while this one runs
                 if (oi + 1 < kp.n_ops) h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
                 const uint32_t ob = h1.x, oc = h1.y, od = h1.z, oe = h1.w;
-                if (flags & F_BARRIER) consumer_sync(nth);
+                if (flags & F_BARRIER) __syncthreads();
                 const uint32_t* tg = kp.targets + off;
                 if (kp.debug_skip) {
                     const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
@@ -750,6 +739,23 @@ cudaError_t launch_frame_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStr
     PFS_DISPATCH(launch_t, cfg, kp, stream)
 }
 cudaError_t set_frame_kernel_smem(const LaunchCfg& cfg) { PFS_DISPATCH(smem_t, cfg) }
+
+cudaError_t launch_noise_kernel(int W, const KParams& kp, int64_t n_tiles, cudaStream_t st) {
+    if (n_tiles <= 0 || kp.pregen_chunks <= 0) return cudaSuccess;
+    dim3 grid((unsigned)((kp.pregen_chunks + 8 * NZ_ITEMS_PER_WARP - 1) / (8 * NZ_ITEMS_PER_WARP)),
+              (unsigned)n_tiles);
+    if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
+    switch (W) {
+        case 1: noise_kernel<1><<<grid, 256, 0, st>>>(kp); break;
+        case 2: noise_kernel<2><<<grid, 256, 0, st>>>(kp); break;
+        case 4: noise_kernel<4><<<grid, 256, 0, st>>>(kp); break;
+        case 8: noise_kernel<8><<<grid, 256, 0, st>>>(kp); break;
+        case 16: noise_kernel<16><<<grid, 256, 0, st>>>(kp); break;
+        case 32: noise_kernel<32><<<grid, 256, 0, st>>>(kp); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
+}
 
 // ------------------------------------------------------------ transpose
 // Tile: 256 rows x 512 shots.  Block of 256 threads (8 warps).
