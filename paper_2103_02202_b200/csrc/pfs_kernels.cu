@@ -488,7 +488,18 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
             }
             if (pregen)
-                for (int i = tid; i < kp.num_noise; i += nth) ncnt[i] = kp.ncnt_global[tile * kp.num_noise + i];
+                for (int i = tid; i < kp.num_noise; i += nth) {
+                    const uint32_t c = kp.ncnt_global[tile * kp.num_noise + i];
+                    ncnt[i] = c;
+                    // pull this op's hit list into L2 ahead of use (TMA bulk prefetch)
+                    const NoiseParam* np = kp.noise + i;
+                    const uint32_t nb = min(c, __ldg(&np->cap)) * 8u;
+                    if ((__ldg(&np->flags) & NZ_PREGEN) && nb) {
+                        const uint64_t* src = hits + __ldg(&np->cap_base);
+                        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
+                                     ::"l"(src), "r"((nb + 15u) & ~15u) : "memory");
+                    }
+                }
             // register prefetch of the first pre-generated noise op's hit `tid`
             uint32_t pf_ord = pregen ? kp.first_pregen : NO_SLOT;
             uint64_t pf_hit = 0;
