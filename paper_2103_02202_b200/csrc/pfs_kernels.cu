@@ -495,9 +495,12 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     const NoiseParam* np = kp.noise + i;
                     const uint32_t nb = min(c, __ldg(&np->cap)) * 8u;
                     if ((__ldg(&np->flags) & NZ_PREGEN) && nb) {
-                        const uint64_t* src = hits + __ldg(&np->cap_base);
+                        // bulk copies need 16-byte aligned addresses and sizes
+                        const uintptr_t a0 = reinterpret_cast<uintptr_t>(hits + __ldg(&np->cap_base));
+                        const uintptr_t lo = a0 & ~(uintptr_t)15;
+                        const uint32_t sz = (uint32_t)(((a0 + nb) - lo + 15) & ~(uintptr_t)15);
                         asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;"
-                                     ::"l"(src), "r"((nb + 15u) & ~15u) : "memory");
+                                     ::"l"(lo), "r"(sz) : "memory");
                     }
                 }
             // register prefetch of the first pre-generated noise op's hit `tid`
