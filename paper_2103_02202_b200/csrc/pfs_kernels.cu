@@ -490,10 +490,11 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             if (pregen)
                 for (int i = tid; i < kp.num_noise; i += nth) {
                     const uint32_t c = kp.ncnt_global[tile * kp.num_noise + i];
-                    ncnt[i] = c;
-                    // pull this op's hit list into L2 ahead of use (TMA bulk prefetch)
                     const NoiseParam* np = kp.noise + i;
-                    const uint32_t nb = min(c, __ldg(&np->cap)) * 8u;
+                    const uint32_t cap = __ldg(&np->cap);
+                    ncnt[i] = c <= cap ? c : NO_SLOT;  // overflow -> inline resampling
+                    // pull this op's hit list into L2 ahead of use (TMA bulk prefetch)
+                    const uint32_t nb = min(c, cap) * 8u;
                     if ((__ldg(&np->flags) & NZ_PREGEN) && nb) {
                         // bulk copies need 16-byte aligned addresses and sizes
                         const uintptr_t a0 = reinterpret_cast<uintptr_t>(hits + __ldg(&np->cap_base));
@@ -506,8 +507,10 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             // register prefetch of the first pre-generated noise op's hit `tid`
             uint32_t pf_ord = pregen ? kp.first_pregen : NO_SLOT;
             uint64_t pf_hit = 0;
-            if (pf_ord != NO_SLOT && (uint32_t)tid < kp.ncnt_global[tile * kp.num_noise + pf_ord])
-                pf_hit = hits[kp.first_cap_base + tid];
+            if (pf_ord != NO_SLOT) {
+                const uint32_t c0 = kp.ncnt_global[tile * kp.num_noise + pf_ord];
+                if ((uint32_t)tid < c0 && c0 <= __ldg(&kp.noise[pf_ord].cap)) pf_hit = hits[kp.first_cap_base + tid];
+            }
             __syncthreads();
 
             uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
@@ -630,14 +633,14 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                         break;
                     }
                     if ((flags & F_PREGEN) && pregen) {
-                        const NoiseParam* npp = kp.noise + ob;
-                        const uint32_t nh = ncnt[ob];
-                        if (nh <= __ldg(&npp->cap)) {
+                        const uint32_t nh = ncnt[ob];  // NO_SLOT: the hit list overflowed
+                        if (nh != NO_SLOT) {
                             // hit `tid` was prefetched into a register
                             if ((uint32_t)tid < nh && pf_ord == ob) apply_entry<W>(X, Z, pf_hit);
                             for (uint32_t i = (pf_ord == ob ? nth : 0) + tid; i < nh; i += nth)
                                 apply_entry<W>(X, Z, hits[oc + i]);
                         } else {
+                            const NoiseParam* npp = kp.noise + ob;
                             for (uint32_t r = tid; r < __ldg(&npp->nchunks); r += nth)
                                 noise_chunk(kp, *npp, ob, r, g, sl, ss, [&](uint32_t trial, uint32_t pick) {
                                     apply_hit<W>(X, Z, tg, code, ar, trial, pick);
@@ -645,7 +648,10 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                         }
                         // prefetch the next pre-generated op's hit `tid`
                         pf_ord = od;
-                        if (od != NO_SLOT && (uint32_t)tid < ncnt[od]) pf_hit = hits[oe + tid];
+                        if (od != NO_SLOT) {
+                            const uint32_t nn = ncnt[od];
+                            if (nn != NO_SLOT && (uint32_t)tid < nn) pf_hit = hits[oe + tid];
+                        }
                         break;
                     }
                     if (kp.debug_skip & 2) break;
