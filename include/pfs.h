@@ -52,7 +52,8 @@ typedef struct pfs_options {
     int32_t producer_threads; /* threads sampling the next tile's noise (0 = auto)   */
     int32_t schedule_only;    /* 1: compile without the shared-memory fit check (the
                                  program exposes info / noise schedule, cannot run)  */
-    int32_t reserved[4];
+    int32_t groups;           /* independent tiles in flight per CTA (0 = auto)     */
+    int32_t reserved[3];
 } pfs_options;
 
 typedef struct pfs_info {
@@ -74,8 +75,9 @@ typedef struct pfs_info {
     int64_t num_noise_rows;
     int64_t noise_tab_len;    /* uint64 entries of the Binomial threshold tables   */
     int64_t hit_capacity;     /* pre-generated noise hit-list entries per CTA       */
-    int64_t pregen_chunks;    /* noise chunks sampled in each tile's pre-pass       */
-    int64_t reserved[3];
+    int64_t pregen_chunks;    /* noise work items (32 chunks each) per tile         */
+    int64_t groups;           /* independent tiles in flight per CTA                */
+    int64_t reserved[2];
 } pfs_info;
 
 enum pfs_mode {

@@ -29,7 +29,8 @@ class Options(ctypes.Structure):
                 ("threads", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("noise_target_hits", ctypes.c_double), ("timing", ctypes.c_int32),
                 ("debug_skip", ctypes.c_int32), ("producer_threads", ctypes.c_int32),
-                ("schedule_only", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
+                ("schedule_only", ctypes.c_int32), ("groups", ctypes.c_int32),
+                ("reserved", ctypes.c_int32 * 3)]
 
 
 class Info(ctypes.Structure):
@@ -42,7 +43,8 @@ class Info(ctypes.Structure):
                 ("num_noise", ctypes.c_int64), ("bframe_bits", ctypes.c_int64),
                 ("num_coin_rows", ctypes.c_int64), ("num_noise_rows", ctypes.c_int64),
                 ("noise_tab_len", ctypes.c_int64), ("hit_capacity", ctypes.c_int64),
-                ("pregen_chunks", ctypes.c_int64), ("reserved", ctypes.c_int64 * 3)]
+                ("pregen_chunks", ctypes.c_int64), ("groups", ctypes.c_int64),
+                ("reserved", ctypes.c_int64 * 2)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -142,7 +144,7 @@ class NativeProgram:
     def __init__(self, prog: FlatProgram, words_per_tile: int = 0, ring_in_smem: int = -1,
                  threads: int = 0, ctas_per_sm: int = 0, noise_target_hits: float = 0.0,
                  timing: bool = False, debug_skip: int = 0, producer_threads: int = 0,
-                 schedule_only: bool = False):
+                 schedule_only: bool = False, groups: int = 0):
         L = lib()
         self.flat = prog
         self._keep = [np.ascontiguousarray(prog.instrs, dtype=np.int32),
@@ -152,7 +154,8 @@ class NativeProgram:
                       np.ascontiguousarray(prog.det_idx, dtype=np.int64)]
         ins, tg, p, dp, di = self._keep
         opts = Options(words_per_tile, ring_in_smem, threads, ctas_per_sm, noise_target_hits,
-                       1 if timing else 0, debug_skip, producer_threads, 1 if schedule_only else 0)
+                       1 if timing else 0, debug_skip, producer_threads, 1 if schedule_only else 0,
+                       groups)
         h = ctypes.c_void_p()
         _check(L.pfs_program_create(_p(ins), ins.shape[0], _p(tg), tg.shape[0], _p(p), p.shape[0],
                                     _p(dp), _p(di), prog.num_columns, prog.num_observables,

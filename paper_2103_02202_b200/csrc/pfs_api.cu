@@ -76,42 +76,52 @@ struct pfs_program {
     int64_t last_launches = 0;
 };
 
-// this tile's per-op hit counts + the inline sampler's per-lane scratch
-static size_t fixed_smem(const HostProgram& hp) {
-    return (size_t)hp.num_noise * 4 + (size_t)(FRAME_MAX_THREADS / 32) * (32 * NZ_MAX_LIST) * 4;
+// per-group per-op hit counts + the inline sampler's per-lane scratch
+static size_t fixed_smem(const HostProgram& hp, int groups) {
+    return (size_t)hp.num_noise * 4 * groups + (size_t)(FRAME_MAX_THREADS / 32) * (32 * NZ_MAX_LIST) * 4;
 }
 
 static void choose_layout(pfs_program* pg) {
     const HostProgram& hp = pg->hp;
     const pfs_options& o = pg->opts;
     const size_t budget = pg->smem_optin;
-    auto frame = [&](int W) { return frame_smem_bytes(hp.num_qubits, W) + fixed_smem(hp); };
+    const size_t fixed1 = fixed_smem(hp, 1), fixed2 = fixed_smem(hp, 2);
+    auto frame = [&](int W) { return frame_smem_bytes(hp.num_qubits, W); };
     auto ring = [&](int W) { return (size_t)hp.num_slots * W * 4; };
-    int Ws = 0, Wg = 0;
-    for (int W = 32; W >= 1; W >>= 1)
-        if (frame(W) + ring(W) <= budget) { Ws = W; break; }
-    for (int W = 32; W >= 1; W >>= 1)
-        if (frame(W) <= budget) { Wg = W; break; }
-    int W;
-    bool rs;
+    auto fits = [&](int W, int G, bool rs) {
+        return G * (frame(W) + (rs ? ring(W) : 0)) + (G == 1 ? fixed1 : fixed2) <= budget;
+    };
+    int W = 0, G = 1;
+    bool rs = false;
     if (o.words_per_tile > 0) {
         W = o.words_per_tile;
+        G = o.groups > 0 ? o.groups : (fits(W, 2, false) ? 2 : 1);
         if (o.ring_in_smem == 1) rs = true;
         else if (o.ring_in_smem == 0) rs = false;
-        else rs = frame(W) + ring(W) <= budget;
-    } else if (o.ring_in_smem == 1) {
-        W = Ws; rs = true;
-    } else if (o.ring_in_smem == 0) {
-        W = Wg; rs = false;
-    } else if (Ws > 0 && Ws >= Wg) {
-        W = Ws; rs = true;
+        else rs = fits(W, G, true);
     } else {
-        W = Wg; rs = false;
+        // candidates: (W, groups, ring placement); prefer more shots in flight
+        // per SM (G*W), then two groups (latency overlap), then a shared-memory ring
+        int best_score = -1;
+        for (int g = 1; g <= 2; g++) {
+            if (o.groups > 0 && g != o.groups) continue;
+            for (int w = 32; w >= 1; w >>= 1) {
+                for (int r = 1; r >= 0; r--) {
+                    if (o.ring_in_smem == 0 && r) continue;
+                    if (o.ring_in_smem == 1 && !r) continue;
+                    if (!fits(w, g, r)) continue;
+                    const int score = (g * w) * 4 + (g == 2 ? 2 : 0) + r;
+                    if (score > best_score) { best_score = score; W = w; G = g; rs = r; }
+                }
+            }
+        }
     }
     pg->cfg.W = W;
+    pg->cfg.groups = G;
     pg->cfg.ring_smem = rs;
-    pg->cfg.smem_bytes = frame(W) + (rs ? ring(W) : 0);
+    pg->cfg.smem_bytes = W > 0 ? G * (frame(W) + (rs ? ring(W) : 0)) + (G == 1 ? fixed1 : fixed2) : 0;
     int threads = o.threads > 0 ? std::min(o.threads, FRAME_MAX_THREADS) : FRAME_MAX_THREADS;
+    threads = (threads / (32 * G)) * 32 * G;  // whole warps per group
     pg->cfg.threads = threads;
 }
 
@@ -176,6 +186,7 @@ int pfs_program_info(const pfs_program* pg, pfs_info* o) {
     const HostProgram& hp = pg->hp;
     o->num_qubits = hp.num_qubits;
     o->words_per_tile = pg->cfg.W;
+    o->groups = pg->cfg.groups;
     o->tile_shots = 32 * pg->cfg.W;
     o->threads = pg->cfg.threads;
     o->ring_in_smem = pg->cfg.ring_smem ? 1 : 0;
@@ -331,7 +342,8 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
             pg->last_launches++;
         }
         LaunchCfg lc = cfg;
-        lc.grid = (int)std::min<int64_t>(cfg.grid, ns);
+        lc.grid = (int)std::min<int64_t>(cfg.grid, (ns + cfg.groups - 1) / cfg.groups);
+        k2.groups = cfg.groups;
         CUDA_TRY(launch_frame_kernel(lc, k2, st));
         pg->last_launches++;
     }
@@ -442,7 +454,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
 
     LaunchCfg cfg = pg->cfg;
     if (!cfg.ring_smem) {
-        CUDA_TRY(pg->d_ring.reserve((size_t)std::max<int64_t>(hp.num_slots, 1) * W * cfg.grid));
+        CUDA_TRY(pg->d_ring.reserve((size_t)std::max<int64_t>(hp.num_slots, 1) * W * cfg.grid * cfg.groups));
         kp.ring_global = pg->d_ring.p;
     }
 

@@ -154,13 +154,14 @@ struct KParams {
     int32_t counts_in_smem;
     int32_t do_dets;             // evaluate DET/OBS ops
     int32_t debug_skip;          // profiling ablations (pfs_options.debug_skip)
-    int32_t producers;           // threads sampling the next tile's noise (warp-specialised)
+    int32_t groups;              // independent thread groups (tiles in flight) per CTA
     uint32_t first_pregen;       // first pre-generated noise ordinal (NO_SLOT: none)
     uint32_t first_cap_base;
 };
 
 struct LaunchCfg {
     int W;
+    int groups;
     bool ring_smem;
     int threads;
     int grid;

@@ -455,25 +455,36 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     constexpr int LC = Log2<C>::v;
     extern __shared__ __align__(16) uint32_t smem[];
     const int n = kp.num_qubits;
-    uint32_t* const X = smem;
-    uint32_t* const Z = smem + (size_t)n * W;
-    uint32_t* const ring = RING_SMEM ? (smem + (size_t)2 * n * W)
-                                     : (kp.ring_global + (size_t)blockIdx.x * kp.num_slots * W);
-    uint32_t* const cnt = smem + (size_t)2 * n * W + (RING_SMEM ? (size_t)kp.num_slots * W : 0);
-    uint32_t* const ncnt = cnt + (kp.counts_in_smem ? kp.num_cols : 0);  // this tile's hits per op
-    const int tid = threadIdx.x;
+    // kp.groups independent thread groups per CTA, each with its own tile,
+    // frame, record ring and named barrier: one group's op latency overlaps
+    // the other group's work
+    const int G = kp.groups;
+    const int gsz = blockDim.x / G;
+    const int grp = threadIdx.x / gsz;
+    const int tid = threadIdx.x - grp * gsz;  // thread index within the group
+    const int nth = gsz;
+    const size_t fw = (size_t)2 * n * W;      // frame words per group
+    uint32_t* const X = smem + grp * fw;
+    uint32_t* const Z = X + (size_t)n * W;
+    uint32_t* const ring = RING_SMEM ? (smem + G * fw + (size_t)grp * kp.num_slots * W)
+                                     : (kp.ring_global + ((size_t)blockIdx.x * G + grp) * kp.num_slots * W);
+    uint32_t* const cnt = smem + G * fw + (RING_SMEM ? (size_t)G * kp.num_slots * W : 0);
+    uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);
+    uint32_t* const ncnt = ncnt0 + grp * kp.num_noise;  // this tile's hits per op
     // per-warp scratch of the inline noise sampler (large-p ops / list overflow)
-    uint32_t* const nscr = ncnt + kp.num_noise;
-    uint32_t* const sl = nscr + (tid >> 5) * (32 * NZ_MAX_LIST) + (tid & 31) * NZ_MAX_LIST;
+    uint32_t* const nscr = ncnt0 + G * kp.num_noise;
+    uint32_t* const sl = nscr + (threadIdx.x >> 5) * (32 * NZ_MAX_LIST) + (threadIdx.x & 31) * NZ_MAX_LIST;
     const int ss = 1;
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
-    const int nth = blockDim.x;
+    const uint32_t bar_id = 1u + (uint32_t)grp;
+    auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gsz) : "memory"); };
 
     if (kp.counts_in_smem) {
-        for (int i = tid; i < kp.num_cols; i += nth) cnt[i] = 0u;
+        for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
+        __syncthreads();
     }
 
-    for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x) {
+    for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
         const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
         const uint64_t* const hits = kp.hits_global + tile * kp.hit_capacity;
         {
@@ -511,7 +522,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 const uint32_t c0 = kp.ncnt_global[tile * kp.num_noise + pf_ord];
                 if ((uint32_t)tid < c0 && c0 <= __ldg(&kp.noise[pf_ord].cap)) pf_hit = hits[kp.first_cap_base + tid];
             }
-            __syncthreads();
+            group_sync();
 
             uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
             for (int oi = 0; oi < kp.n_ops; oi++) {
@@ -522,7 +533,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 // prefetch the next op's first half while this one runs
                 if (oi + 1 < kp.n_ops) h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
                 const uint32_t ob = h1.x, oc = h1.y, od = h1.z, oe = h1.w;
-                if (flags & F_BARRIER) __syncthreads();
+                if (flags & F_BARRIER) group_sync();
                 const uint32_t* tg = kp.targets + off;
                 if (kp.debug_skip) {
                     const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
@@ -722,11 +733,11 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 }
             }
         }
-        __syncthreads();
+        group_sync();  // the group's frame is reused by its next tile
     }
     if (kp.counts_in_smem) {
         __syncthreads();
-        for (int i = tid; i < kp.num_cols; i += blockDim.x)
+        for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x)
             if (cnt[i]) atomicAdd(kp.counts + i, (unsigned long long)cnt[i]);
     }
 }

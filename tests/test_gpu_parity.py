@@ -27,15 +27,17 @@ def need_gpu():
     build()
 
 
-# (words_per_tile, ring_in_smem) layouts exercising every kernel instantiation
-LAYOUTS = [(0, -1), (1, 0), (2, 1), (4, 0), (8, 1), (16, 0), (32, 1)]
+# (words_per_tile, ring_in_smem, groups) layouts exercising every kernel
+# instantiation, one and two tiles in flight per CTA
+LAYOUTS = [(0, -1, 0), (1, 0, 1), (2, 1, 2), (4, 0, 0), (8, 1, 1), (16, 0, 2), (32, 1, 0),
+           (16, 0, 1)]
 
 
-def _fits(text, W, ring):
+def _fits(text, W, ring, groups=0):
     from paper_2103_02202_b200._native import NativeProgram
     from paper_2103_02202_b200.program import flatten
     try:
-        NativeProgram(flatten(text), words_per_tile=W, ring_in_smem=ring)
+        NativeProgram(flatten(text), words_per_tile=W, ring_in_smem=ring, groups=groups)
         return True
     except ValueError:
         return False
@@ -47,13 +49,13 @@ def test_injected_bit_exact_vs_reference(name, layout):
     from paper_2103_02202_b200.sampler import compile_detector_sampler, compile_sampler
 
     text, B, coins, masks, flips_ref, events_ref = load_inject(name)
-    W, ring = layout
-    if not _fits(text, W, ring):
+    W, ring, groups = layout
+    if not _fits(text, W, ring, groups):
         pytest.skip("layout does not fit")
-    ds = compile_detector_sampler(text, words_per_tile=W, ring_in_smem=ring)
+    ds = compile_detector_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
     ev = ds.sample(B, coins=coins, masks=masks)
     assert np.array_equal(ev, events_ref)
-    ms = compile_sampler(text, words_per_tile=W, ring_in_smem=ring)
+    ms = compile_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
     fl = ms.sample_flips(B, coins=coins, masks=masks)
     assert np.array_equal(fl, flips_ref)
     # counts mode sees the same events
@@ -74,21 +76,21 @@ def _philox_cases():
 
 
 @pytest.mark.parametrize("case", list(_philox_cases()))
-@pytest.mark.parametrize("layout", [(0, -1), (1, 1), (4, 0), (16, 1)])
+@pytest.mark.parametrize("layout", [(0, -1, 0), (1, 1, 1), (4, 0, 2), (16, 1, 1), (8, 0, 2)])
 def test_philox_bit_exact_vs_oracle(oracle_lib, case, layout):
     from paper_2103_02202_b200.sampler import compile_detector_sampler, compile_sampler
 
     text = _philox_cases()[case]
-    W, ring = layout
-    if not _fits(text, W, ring):
+    W, ring, groups = layout
+    if not _fits(text, W, ring, groups):
         pytest.skip("layout does not fit")
-    ds = compile_detector_sampler(text, words_per_tile=W, ring_in_smem=ring)
+    ds = compile_detector_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
     T = ds.tile_shots
     shots = 3 * T + 37
     seed = 0xC0FFEE
     offset = 5 * T
     ev_rows = ds.sample_rows(shots, seed=seed, shot_offset=offset)
-    ms = compile_sampler(text, words_per_tile=W, ring_in_smem=ring)
+    ms = compile_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
     fl_rows = ms.sample_flip_rows(shots, seed=seed, shot_offset=offset)
     ofl, oev = oracle_lib.sample(ds.flat, shots, T, seed=seed, tile_offset=offset // T,
                                  nthreads=4, schedule=ds.native.noise_schedule())
