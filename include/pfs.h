@@ -158,6 +158,11 @@ int pfs_detector_events(int device, const uint8_t* flips_b8, int64_t num_shots,
  * memory bandwidth (GB/s, loads + stores, CX access mix) over all SMs. */
 int pfs_measure_smem_bandwidth(int device, double* gbs);
 
+/* Profiling helpers: per-op clock64 trace (debug_skip bit 6) and the device op
+ * list as (kind|code<<8|flags<<16, count) pairs. */
+int pfs_program_op_clock(struct pfs_program* prog, long long* out, int64_t n);
+int pfs_program_ops(const struct pfs_program* prog, uint32_t* out, int64_t n);
+
 void pfs_program_destroy(struct pfs_program* prog);
 const char* pfs_last_error(void);
 int pfs_version(void);

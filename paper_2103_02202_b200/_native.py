@@ -53,7 +53,7 @@ class Info(ctypes.Structure):
 EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_schedule", "pfs_run",
            "pfs_program_last_timing", "pfs_program_last_launches", "pfs_program_destroy",
            "pfs_last_error", "pfs_version", "pfs_measure_smem_bandwidth",
-           "pfs_detector_events")
+           "pfs_detector_events", "pfs_program_op_clock", "pfs_program_ops")
 
 _lib = None
 
@@ -88,6 +88,10 @@ def lib():
     L.pfs_measure_smem_bandwidth.restype = ctypes.c_int
     L.pfs_detector_events.argtypes = [ctypes.c_int, P, i64, i64, i64, P, P, i64, P, i64, i64, P]
     L.pfs_detector_events.restype = ctypes.c_int
+    L.pfs_program_op_clock.argtypes = [P, P, i64]
+    L.pfs_program_op_clock.restype = ctypes.c_int
+    L.pfs_program_ops.argtypes = [P, P, i64]
+    L.pfs_program_ops.restype = ctypes.c_int
     L.pfs_version.argtypes = []
     L.pfs_version.restype = ctypes.c_int
     _lib = L
@@ -193,6 +197,16 @@ class NativeProgram:
         arr = (ctypes.c_double * 6)()
         _check(lib().pfs_program_last_timing(self._h, arr, 6))
         return list(arr)
+
+    def op_clock(self) -> np.ndarray:
+        out = np.zeros(self.info["num_ops"], dtype=np.int64)
+        _check(lib().pfs_program_op_clock(self._h, _p(out), out.size))
+        return out
+
+    def ops(self) -> np.ndarray:
+        out = np.zeros((self.info["num_ops"], 2), dtype=np.uint32)
+        _check(lib().pfs_program_ops(self._h, _p(out), self.info["num_ops"]))
+        return out
 
     def last_launches(self) -> int:
         return int(lib().pfs_program_last_launches(self._h))

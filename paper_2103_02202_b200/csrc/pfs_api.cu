@@ -65,6 +65,7 @@ struct pfs_program {
     DevBuf<uint32_t> d_pregen, d_noise_off, d_noise_ch;
     DevBuf<uint64_t> d_hits;
     DevBuf<uint32_t> d_ncnt;
+    DevBuf<long long> d_clock;
     DevBuf<uint32_t> d_rows[2];
     DevBuf<uint8_t> d_b8[2];
     DevBuf<uint32_t> d_coins, d_masks;
@@ -451,6 +452,10 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.num_cols = (int32_t)hp.num_cols;
     kp.do_dets = rows_meas ? 0 : 1;
     kp.debug_skip = pg->opts.debug_skip;
+    if (pg->opts.debug_skip & 64) {  // op-boundary clock trace of the first tile
+        CUDA_TRY(pg->d_clock.reserve(hp.ops.size() + 1));
+        kp.op_clock = pg->d_clock.p;
+    }
 
     LaunchCfg cfg = pg->cfg;
     if (!cfg.ring_smem) {
@@ -663,5 +668,23 @@ extern "C" int pfs_detector_events(int device, const uint8_t* flips_b8, int64_t 
     DE_TRY(cudaStreamSynchronize(st));
 #undef DE_TRY
     cleanup();
+    return PFS_OK;
+}
+
+// Profiling: the per-op clock64 trace recorded by the last pfs_run with
+// options.debug_skip bit 6 (CTA 0, group 0, first tile).
+extern "C" int pfs_program_op_clock(pfs_program* pg, long long* out, int64_t n) {
+    if (!pg || !out) return fail(PFS_E_INVALID, "null argument");
+    if (!pg->d_clock.p) return fail(PFS_E_INVALID, "no clock trace (set debug_skip bit 6)");
+    const int64_t m = std::min<int64_t>(n, (int64_t)pg->hp.ops.size());
+    CUDA_TRY(cudaMemcpy(out, pg->d_clock.p, m * sizeof(long long), cudaMemcpyDeviceToHost));
+    return PFS_OK;
+}
+
+// Profiling: the device op list (kind|code|flags, count) for interpreting traces.
+extern "C" int pfs_program_ops(const pfs_program* pg, uint32_t* out, int64_t n) {
+    if (!pg || !out) return fail(PFS_E_INVALID, "null argument");
+    const int64_t m = std::min<int64_t>(n, (int64_t)pg->hp.ops.size());
+    for (int64_t i = 0; i < m; i++) { out[2 * i] = pg->hp.ops[i].kcf; out[2 * i + 1] = pg->hp.ops[i].count; }
     return PFS_OK;
 }

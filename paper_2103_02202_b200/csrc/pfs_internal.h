@@ -133,6 +133,7 @@ struct KParams {
     uint32_t* ev_out;            // [cols][out_words] or null
     unsigned long long* counts;  // [cols] or null
     uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
+    long long* op_clock;         // profiling: per-op clock64 of CTA 0's first tile, or null
     uint64_t* hits_global;       // [tiles][hit_capacity] pre-sampled noise hits (noise_kernel)
     uint32_t* ncnt_global;       // [tiles][num_noise] hits per noise op
     int64_t inject_words;

@@ -534,6 +534,9 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 if (oi + 1 < kp.n_ops) h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
                 const uint32_t ob = h1.x, oc = h1.y, od = h1.z, oe = h1.w;
                 if (flags & F_BARRIER) group_sync();
+                if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
+                    tile == 0)  // profiling: op-boundary timestamps of the first tile
+                    kp.op_clock[oi] = clock64();
                 const uint32_t* tg = kp.targets + off;
                 if (kp.debug_skip) {
                     const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u

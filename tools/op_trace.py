@@ -1,0 +1,54 @@
+"""Per-op time of the frame kernel from clock64 traces (profiling only).
+
+    python tools/op_trace.py [--config 2] [--shots N]
+Prints the cycle share per op kind (and the costliest ops)."""
+import argparse
+import collections
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--shots", type=int, default=1 << 16)
+    ap.add_argument("--groups", type=int, default=0)
+    ap.add_argument("--words", type=int, default=0)
+    a = ap.parse_args()
+    import numpy as np
+    import torch
+
+    from paper_2103_02202_b200 import generators as gen
+    from paper_2103_02202_b200.sampler import compile_detector_sampler
+
+    ds = compile_detector_sampler(gen.config_circuit(a.config), debug_skip=64, groups=a.groups,
+                                  words_per_tile=a.words)
+    out = torch.empty((ds.num_columns, (a.shots + 31) // 32), dtype=torch.int32, device="cuda")
+    for i in range(3):
+        ds.sample_rows(a.shots, seed=i, out=out)
+    torch.cuda.synchronize()
+    clk = ds.native.op_clock()
+    ops = ds.native.ops()
+    dt = np.diff(clk)
+    names = {0: "GATE", 1: "M", 2: "R", 3: "MR", 4: "NOISE", 5: "DET", 6: "OBS"}
+    agg = collections.defaultdict(lambda: [0, 0])
+    for i, d in enumerate(dt):
+        k = int(ops[i, 0] & 0xFF)
+        key = names.get(k, str(k)) + ("/bar" if (ops[i + 1, 0] >> 16) & 1 else "")
+        agg[key][0] += 1
+        agg[key][1] += int(d)
+    tot = int(dt.sum())
+    print(ds.info)
+    print(f"first tile: {tot} cycles over {len(dt)} ops")
+    for k, (n, c) in sorted(agg.items(), key=lambda x: -x[1][1]):
+        print(f"  {k:12s} n={n:4d} cycles={c:9d} ({100 * c / tot:5.1f}%)  avg={c / n:8.0f}")
+    top = np.argsort(dt)[::-1][:15]
+    for i in top:
+        print(f"  op {i:4d} kind={names.get(int(ops[i, 0] & 0xFF))} code={(ops[i, 0] >> 8) & 0xFF} "
+              f"count={ops[i, 1]} cycles={dt[i]}")
+
+
+if __name__ == "__main__":
+    main()
