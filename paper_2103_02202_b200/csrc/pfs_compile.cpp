@@ -274,6 +274,20 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     }
     hp.num_slots = next_slot;
 
+    // DET ops whose columns all have the same term count k get direct term
+    // addressing: terms of column a+i at det_terms[off + i*k] (off = term base,
+    // code = k), one dependent load fewer in the kernel
+    for (DOp& o : hp.ops) {
+        if ((o.kcf & 0xFF) != K_DET || o.count == 0) continue;
+        const uint32_t base = hp.det_ptr[o.a];
+        const uint32_t k = hp.det_ptr[o.a + 1] - base;
+        bool uniform = k >= 1 && k <= 255;
+        for (uint32_t c = o.a; uniform && c < o.a + o.count; c++)
+            uniform = hp.det_ptr[c + 1] - hp.det_ptr[c] == k;
+        o.off = base;
+        if (uniform) o.kcf = (o.kcf & ~0xFF00u) | (k << 8);
+    }
+
     // ---- pass 3: barrier scheduling over qubit rows + record slots ----
     const int64_t nres = (int64_t)num_qubits + hp.num_slots;
     std::vector<int64_t> rstamp(nres, -1);

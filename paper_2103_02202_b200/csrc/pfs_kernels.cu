@@ -222,10 +222,17 @@ __device__ __forceinline__ uint64_t make_hit(uint32_t q0, uint32_t q1, uint32_t 
 }
 
 template <int W>
-__device__ __forceinline__ void apply_entry(uint32_t* X, uint32_t* Z, uint64_t e) {
+__device__ __forceinline__ void apply_entry(uint32_t* X, uint32_t* Z, uint64_t e, bool plain = false) {
     const uint32_t q0 = (uint32_t)e & 0xFFFFFu, q1 = (uint32_t)(e >> 20) & 0xFFFFFu;
     const uint32_t w = (uint32_t)(e >> 40) & 31u, bit = 1u << ((uint32_t)(e >> 45) & 31u);
     const uint32_t xm = (uint32_t)(e >> 50) & 3u, zm = (uint32_t)(e >> 52) & 3u;
+    if (plain) {  // profiling ablation only (racy)
+        if (xm & 1u) X[(size_t)q0 * W + w] ^= bit;
+        if (zm & 1u) Z[(size_t)q0 * W + w] ^= bit;
+        if (xm & 2u) X[(size_t)q1 * W + w] ^= bit;
+        if (zm & 2u) Z[(size_t)q1 * W + w] ^= bit;
+        return;
+    }
     if (xm & 1u) atomicXor(X + (size_t)q0 * W + w, bit);
     if (zm & 1u) atomicXor(Z + (size_t)q0 * W + w, bit);
     if (xm & 2u) atomicXor(X + (size_t)q1 * W + w, bit);
@@ -515,13 +522,9 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                                      ::"l"(lo), "r"(sz) : "memory");
                     }
                 }
-            // register prefetch of the first pre-generated noise op's hit `tid`
+            // the next pre-generated noise op (its hit list is L1-prefetched one op ahead)
             uint32_t pf_ord = pregen ? kp.first_pregen : NO_SLOT;
-            uint64_t pf_hit = 0;
-            if (pf_ord != NO_SLOT) {
-                const uint32_t c0 = kp.ncnt_global[tile * kp.num_noise + pf_ord];
-                if ((uint32_t)tid < c0 && c0 <= __ldg(&kp.noise[pf_ord].cap)) pf_hit = hits[kp.first_cap_base + tid];
-            }
+            uint32_t pf_base = kp.first_cap_base;
             group_sync();
 
             uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
@@ -534,6 +537,32 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 if (oi + 1 < kp.n_ops) h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
                 const uint32_t ob = h1.x, oc = h1.y, od = h1.z, oe = h1.w;
                 if (flags & F_BARRIER) group_sync();
+                if (oi + 1 < kp.n_ops) {
+                    // pull the next op's operand block into L1 while this op runs
+                    // (h0 already holds the next op's first descriptor half)
+                    const uint32_t nk = h0.x & 0xFFu, ncode = (h0.x >> 8) & 0xFFu;
+                    const char* base = nullptr;
+                    uint32_t bytes = 0;
+                    switch (nk) {
+                        case K_GATE: base = (const char*)(kp.targets + h0.z); bytes = h0.y * (ncode >= R_CX ? 8u : 4u); break;
+                        case K_M: case K_MR: base = (const char*)(kp.targets + h0.z); bytes = h0.y * 8u; break;
+                        case K_R: base = (const char*)(kp.targets + h0.z); bytes = h0.y * 4u; break;
+                        case K_DET: if (ncode) { base = (const char*)(kp.det_terms + h0.z); bytes = h0.y * ncode * 4u; } break;
+                        case K_NOISE:
+                            if (pregen && pf_ord != NO_SLOT) {
+                                const uint32_t nn = ncnt[pf_ord];
+                                if (nn != NO_SLOT) { base = (const char*)(hits + pf_base); bytes = nn * 8u; }
+                            }
+                            break;
+                        default: break;
+                    }
+                    if (base != nullptr) {
+                        const uintptr_t b0 = reinterpret_cast<uintptr_t>(base) & ~(uintptr_t)127;
+                        const uint32_t lines = (uint32_t)((reinterpret_cast<uintptr_t>(base) + bytes - b0 + 127) >> 7);
+                        for (uint32_t l = tid; l < lines; l += nth)
+                            asm volatile("prefetch.global.L1 [%0];" ::"l"(b0 + ((uintptr_t)l << 7)));
+                    }
+                }
                 if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
                     tile == 0)  // profiling: op-boundary timestamps of the first tile
                     kp.op_clock[oi] = clock64();
@@ -649,10 +678,9 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     if ((flags & F_PREGEN) && pregen) {
                         const uint32_t nh = ncnt[ob];  // NO_SLOT: the hit list overflowed
                         if (nh != NO_SLOT) {
-                            // hit `tid` was prefetched into a register
-                            if ((uint32_t)tid < nh && pf_ord == ob) apply_entry<W>(X, Z, pf_hit);
-                            for (uint32_t i = (pf_ord == ob ? nth : 0) + tid; i < nh; i += nth)
-                                apply_entry<W>(X, Z, hits[oc + i]);
+                            if (!(kp.debug_skip & 256))
+                                for (uint32_t i = tid; i < nh; i += nth)
+                                    apply_entry<W>(X, Z, hits[oc + i], (kp.debug_skip & 128) != 0);
                         } else {
                             const NoiseParam* npp = kp.noise + ob;
                             for (uint32_t r = tid; r < __ldg(&npp->nchunks); r += nth)
@@ -660,12 +688,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                                     apply_hit<W>(X, Z, tg, code, ar, trial, pick);
                                 });
                         }
-                        // prefetch the next pre-generated op's hit `tid`
-                        pf_ord = od;
-                        if (od != NO_SLOT) {
-                            const uint32_t nn = ncnt[od];
-                            if (nn != NO_SLOT && (uint32_t)tid < nn) pf_hit = hits[oe + tid];
-                        }
+                        pf_ord = od;  // the next pre-generated op and its hit-list base
+                        pf_base = oe;
                         break;
                     }
                     if (kp.debug_skip & 2) break;
@@ -681,11 +705,15 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 case K_DET: {
                     if (!kp.do_dets) break;
                     const int items = (int)(count << LC);
-                    // prefetch each column's term range and first two record slots
+                    // prefetch each column's term range and first two record slots;
+                    // uniform ops (code = terms per column) address terms directly
                     batched_items<2>(tid, nth, items,
                         [&](int i) {
-                            const uint32_t col = oa + (uint32_t)(i >> LC);
-                            const uint32_t e0 = __ldg(kp.det_ptr + col), e1 = __ldg(kp.det_ptr + col + 1);
+                            const uint32_t ci = (uint32_t)(i >> LC);
+                            const uint32_t col = oa + ci;
+                            uint32_t e0, e1;
+                            if (code) { e0 = off + ci * code; e1 = e0 + code; }
+                            else { e0 = __ldg(kp.det_ptr + col); e1 = __ldg(kp.det_ptr + col + 1); }
                             const uint32_t s0 = e0 < e1 ? __ldg(kp.det_terms + e0) : NO_SLOT;
                             const uint32_t s1 = e0 + 1 < e1 ? __ldg(kp.det_terms + e0 + 1) : NO_SLOT;
                             return make_uint4(e0, e1, s0, s1);

@@ -16,6 +16,7 @@ def main():
     ap.add_argument("--shots", type=int, default=1 << 16)
     ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--words", type=int, default=0)
+    ap.add_argument("--debug", type=int, default=0)
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -23,7 +24,7 @@ def main():
     from paper_2103_02202_b200 import generators as gen
     from paper_2103_02202_b200.sampler import compile_detector_sampler
 
-    ds = compile_detector_sampler(gen.config_circuit(a.config), debug_skip=64, groups=a.groups,
+    ds = compile_detector_sampler(gen.config_circuit(a.config), debug_skip=64 | a.debug, groups=a.groups,
                                   words_per_tile=a.words)
     out = torch.empty((ds.num_columns, (a.shots + 31) // 32), dtype=torch.int32, device="cuda")
     for i in range(3):
@@ -44,6 +45,16 @@ def main():
     print(f"first tile: {tot} cycles over {len(dt)} ops")
     for k, (n, c) in sorted(agg.items(), key=lambda x: -x[1][1]):
         print(f"  {k:12s} n={n:4d} cycles={c:9d} ({100 * c / tot:5.1f}%)  avg={c / n:8.0f}")
+    # per (kind, code) breakdown
+    agg2 = collections.defaultdict(lambda: [0, 0, 0])
+    for i, d in enumerate(dt):
+        k = int(ops[i, 0] & 0xFF)
+        key = (names.get(k, str(k)), int((ops[i, 0] >> 8) & 0xFF))
+        agg2[key][0] += 1
+        agg2[key][1] += int(d)
+        agg2[key][2] += int(ops[i, 1])
+    for k, (n, c, cnt) in sorted(agg2.items(), key=lambda x: -x[1][1]):
+        print(f"  {k[0]:6s} code={k[1]} n={n:4d} avg_cycles={c / n:8.0f} avg_count={cnt / n:8.1f}")
     top = np.argsort(dt)[::-1][:15]
     for i in top:
         print(f"  op {i:4d} kind={names.get(int(ops[i, 0] & 0xFF))} code={(ops[i, 0] >> 8) & 0xFF} "
