@@ -66,6 +66,7 @@ struct pfs_program {
     DevBuf<uint64_t> d_hits;
     DevBuf<uint32_t> d_ncnt;
     DevBuf<long long> d_clock;
+    DevBuf<uint32_t> d_nscratch;
     DevBuf<uint32_t> d_rows[2];
     DevBuf<uint8_t> d_b8[2];
     DevBuf<uint32_t> d_coins, d_masks;
@@ -77,9 +78,12 @@ struct pfs_program {
     int64_t last_launches = 0;
 };
 
-// per-group per-op hit counts + the inline sampler's per-lane scratch
+static bool desc_fits(const HostProgram& hp) { return hp.ops.size() * sizeof(DOp) <= (size_t)DESC_SMEM_MAX; }
+
+// per-group hit counts, TMA staging buffers + mbarriers, descriptor copy
 static size_t fixed_smem(const HostProgram& hp, int groups) {
-    return (size_t)hp.num_noise * 4 * groups + (size_t)(FRAME_MAX_THREADS / 32) * (32 * NZ_MAX_LIST) * 4;
+    return (size_t)hp.num_noise * 4 * groups + 16 + (size_t)groups * 2 * STAGE_BYTES + groups * 16 +
+           (desc_fits(hp) ? hp.ops.size() * sizeof(DOp) : 0);
 }
 
 static void choose_layout(pfs_program* pg) {
@@ -239,6 +243,7 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_det_terms.release(); pg->d_ring.release(); pg->d_noise.release();
         pg->d_noise_tab.release(); pg->d_pregen.release(); pg->d_hits.release();
         pg->d_noise_off.release(); pg->d_noise_ch.release(); pg->d_ncnt.release();
+        pg->d_nscratch.release(); pg->d_clock.release();
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
@@ -452,6 +457,10 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.num_cols = (int32_t)hp.num_cols;
     kp.do_dets = rows_meas ? 0 : 1;
     kp.debug_skip = pg->opts.debug_skip;
+    kp.stage = (pg->opts.debug_skip & 1024) ? 0 : 1;  // bit 10: profiling ablation, no staging
+    kp.desc_in_smem = desc_fits(hp) ? 1 : 0;
+    CUDA_TRY(pg->d_nscratch.reserve((size_t)pg->cfg.grid * pg->cfg.threads * NZ_MAX_LIST));
+    kp.noise_scratch = pg->d_nscratch.p;
     if (pg->opts.debug_skip & 64) {  // op-boundary clock trace of the first tile
         CUDA_TRY(pg->d_clock.reserve(hp.ops.size() + 1));
         kp.op_clock = pg->d_clock.p;

@@ -32,7 +32,11 @@ constexpr uint32_t NZ_PREGEN = 4u;   // hits generated in the tile's pre-pass in
 constexpr int NZ_MAX_LIST = 8;
 // frame kernel CTA size cap (launch bounds): 768 threads leaves 85 registers per
 // thread, enough for the noise sampler without spills
-constexpr int FRAME_MAX_THREADS = 768;      // distinct-position list; larger counts use selection sampling
+constexpr int FRAME_MAX_THREADS = 768;
+// per-group TMA staging buffer (x2, double-buffered) for an op's operand block
+constexpr int STAGE_BYTES = 8192;
+// op descriptors are copied to shared memory when they take at most this much
+constexpr int DESC_SMEM_MAX = 16384;      // distinct-position list; larger counts use selection sampling
 
 // One device op (32 bytes).  See DESIGN.md §3.
 //   GATE : count = apps, off -> targets (1 or 2 per app)
@@ -134,6 +138,7 @@ struct KParams {
     unsigned long long* counts;  // [cols] or null
     uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
     long long* op_clock;         // profiling: per-op clock64 of CTA 0's first tile, or null
+    uint32_t* noise_scratch;     // [grid][threads][NZ_MAX_LIST] inline noise sampler scratch
     uint64_t* hits_global;       // [tiles][hit_capacity] pre-sampled noise hits (noise_kernel)
     uint32_t* ncnt_global;       // [tiles][num_noise] hits per noise op
     int64_t inject_words;
@@ -156,6 +161,8 @@ struct KParams {
     int32_t do_dets;             // evaluate DET/OBS ops
     int32_t debug_skip;          // profiling ablations (pfs_options.debug_skip)
     int32_t groups;              // independent thread groups (tiles in flight) per CTA
+    int32_t stage;               // stage operand blocks through shared memory (TMA)
+    int32_t desc_in_smem;        // op descriptors copied to shared memory
     uint32_t first_pregen;       // first pre-generated noise ordinal (NO_SLOT: none)
     uint32_t first_cap_base;
 };

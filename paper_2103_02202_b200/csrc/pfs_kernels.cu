@@ -432,6 +432,66 @@ __global__ void __launch_bounds__(256) noise_kernel(const __grid_constant__ KPar
                      kp.hits_global + tile * kp.hit_capacity, b, e, wscr_all[warp]);
 }
 
+// ---------------------------------------------------------------- TMA staging
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(mbar)), "r"(count) : "memory");
+}
+// one elected thread: expect `bytes` and start a bulk global->shared copy that
+// completes the transaction on `mbar`
+__device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t bytes, uint64_t* mbar) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;"
+                 ::"r"(smem_addr(mbar)), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                 ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mbar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_addr(mbar)), "r"(parity) : "memory");
+    }
+}
+
+// Operand block of an op (descriptor halves h0/h1): the contiguous global range
+// its items read — targets, uniform detector terms, or (pre-sampled noise) the
+// tile's hit list.  Returns the 16-byte aligned source, its size, and the word
+// offset of the first operand inside it; size 0 = not staged.
+struct StageBlock { const char* src; uint32_t bytes; uint32_t woff; };
+__device__ __forceinline__ StageBlock stage_block(const KParams& kp, uint4 h0, uint4 h1, bool pregen,
+                                                  const uint32_t* ncnt, const uint64_t* hits) {
+    const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
+    const char* src = nullptr;
+    uint32_t bytes = 0;
+    switch (kind) {
+        case K_GATE: src = (const char*)(kp.targets + h0.z); bytes = h0.y * (code >= R_CX ? 8u : 4u); break;
+        case K_M: case K_MR: src = (const char*)(kp.targets + h0.z); bytes = h0.y * 8u; break;
+        case K_R: case K_OBS: src = (const char*)(kp.targets + h0.z); bytes = h0.y * 4u; break;
+        case K_DET: if (code) { src = (const char*)(kp.det_terms + h0.z); bytes = h0.y * code * 4u; } break;
+        case K_NOISE:
+            if (pregen && (flags & F_PREGEN)) {
+                const uint32_t nh = ncnt[h1.x];
+                if (nh != NO_SLOT) { src = (const char*)(hits + h1.y); bytes = nh * 8u; }
+            }
+            break;
+        default: break;
+    }
+    StageBlock b{nullptr, 0u, 0u};
+    if (src == nullptr || bytes == 0) return b;
+    const uintptr_t lo = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
+    const uint32_t sz = (uint32_t)((reinterpret_cast<uintptr_t>(src) + bytes - lo + 15) & ~(uintptr_t)15);
+    if (sz > (uint32_t)STAGE_BYTES) return b;
+    b.src = reinterpret_cast<const char*>(lo);
+    b.bytes = sz;
+    b.woff = (uint32_t)((reinterpret_cast<uintptr_t>(src) - lo) >> 2);
+    return b;
+}
+
 // Items of one op, U per thread per batch: all U operand loads (L2-resident
 // target indices) are issued before any of the dependent shared-memory work.
 template <int U, typename Load, typename Work>
@@ -478,18 +538,37 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     uint32_t* const cnt = smem + G * fw + (RING_SMEM ? (size_t)G * kp.num_slots * W : 0);
     uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);
     uint32_t* const ncnt = ncnt0 + grp * kp.num_noise;  // this tile's hits per op
-    // per-warp scratch of the inline noise sampler (large-p ops / list overflow)
-    uint32_t* const nscr = ncnt0 + G * kp.num_noise;
-    uint32_t* const sl = nscr + (threadIdx.x >> 5) * (32 * NZ_MAX_LIST) + (threadIdx.x & 31) * NZ_MAX_LIST;
+    // 16-byte aligned tail: per-group TMA staging buffers, mbarriers, descriptors
+    char* const tail = reinterpret_cast<char*>(
+        (reinterpret_cast<uintptr_t>(ncnt0 + G * kp.num_noise) + 15) & ~(uintptr_t)15);
+    uint32_t* const stg = reinterpret_cast<uint32_t*>(tail) + (size_t)grp * 2 * (STAGE_BYTES / 4);
+    uint64_t* const mbar = reinterpret_cast<uint64_t*>(tail + (size_t)G * 2 * STAGE_BYTES) + grp * 2;
+    const uint4* const dsc = kp.desc_in_smem
+        ? reinterpret_cast<const uint4*>(tail + (size_t)G * 2 * STAGE_BYTES + G * 16)
+        : reinterpret_cast<const uint4*>(kp.ops);
+    // per-lane scratch of the inline noise sampler (large-p ops / list overflow), global
+    uint32_t* const sl = kp.noise_scratch +
+                         ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
     const int ss = 1;
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
+    const bool staging = kp.stage != 0;
     const uint32_t bar_id = 1u + (uint32_t)grp;
     auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gsz) : "memory"); };
 
-    if (kp.counts_in_smem) {
+    if (kp.counts_in_smem)
         for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
-        __syncthreads();
+    if (kp.desc_in_smem) {
+        uint4* d = const_cast<uint4*>(dsc);
+        for (int i = threadIdx.x; i < 2 * kp.n_ops; i += blockDim.x)
+            d[i] = __ldg(reinterpret_cast<const uint4*>(kp.ops) + i);
     }
+    if (staging && tid == 0) {
+        mbar_init(mbar, 1);
+        mbar_init(mbar + 1, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    uint32_t phase = 0;  // parity bit per staging buffer
 
     for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
         const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
@@ -522,51 +601,44 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                                      ::"l"(lo), "r"(sz) : "memory");
                     }
                 }
-            // the next pre-generated noise op (its hit list is L1-prefetched one op ahead)
-            uint32_t pf_ord = pregen ? kp.first_pregen : NO_SLOT;
-            uint32_t pf_base = kp.first_cap_base;
-            group_sync();
+            group_sync();  // counts visible, previous tile's staging buffers free
+            if (staging && tid == 0 && kp.n_ops > 0) {
+                const StageBlock b = stage_block(kp, dsc[0], dsc[1], pregen, ncnt, hits);
+                if (b.bytes) bulk_load(stg, b.src, b.bytes, mbar);
+            }
 
-            uint4 h0 = kp.n_ops > 0 ? __ldg(reinterpret_cast<const uint4*>(kp.ops)) : make_uint4(0, 0, 0, 0);
+            uint4 h0 = kp.n_ops > 0 ? dsc[0] : make_uint4(0, 0, 0, 0);
             for (int oi = 0; oi < kp.n_ops; oi++) {
                 const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
                 const uint32_t count = h0.y, off = h0.z, oa = h0.w;
-                // second half of the descriptor: its load overlaps the barrier wait
-                const uint4 h1 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi) + 1);
-                // prefetch the next op's first half while this one runs
-                if (oi + 1 < kp.n_ops) h0 = __ldg(reinterpret_cast<const uint4*>(kp.ops + oi + 1));
-                const uint32_t ob = h1.x, oc = h1.y, od = h1.z, oe = h1.w;
-                if (flags & F_BARRIER) group_sync();
-                if (oi + 1 < kp.n_ops) {
-                    // pull the next op's operand block into L1 while this op runs
-                    // (h0 already holds the next op's first descriptor half)
-                    const uint32_t nk = h0.x & 0xFFu, ncode = (h0.x >> 8) & 0xFFu;
-                    const char* base = nullptr;
-                    uint32_t bytes = 0;
-                    switch (nk) {
-                        case K_GATE: base = (const char*)(kp.targets + h0.z); bytes = h0.y * (ncode >= R_CX ? 8u : 4u); break;
-                        case K_M: case K_MR: base = (const char*)(kp.targets + h0.z); bytes = h0.y * 8u; break;
-                        case K_R: base = (const char*)(kp.targets + h0.z); bytes = h0.y * 4u; break;
-                        case K_DET: if (ncode) { base = (const char*)(kp.det_terms + h0.z); bytes = h0.y * ncode * 4u; } break;
-                        case K_NOISE:
-                            if (pregen && pf_ord != NO_SLOT) {
-                                const uint32_t nn = ncnt[pf_ord];
-                                if (nn != NO_SLOT) { base = (const char*)(hits + pf_base); bytes = nn * 8u; }
-                            }
-                            break;
-                        default: break;
-                    }
-                    if (base != nullptr) {
-                        const uintptr_t b0 = reinterpret_cast<uintptr_t>(base) & ~(uintptr_t)127;
-                        const uint32_t lines = (uint32_t)((reinterpret_cast<uintptr_t>(base) + bytes - b0 + 127) >> 7);
-                        for (uint32_t l = tid; l < lines; l += nth)
-                            asm volatile("prefetch.global.L1 [%0];" ::"l"(b0 + ((uintptr_t)l << 7)));
+                const uint4 h1 = dsc[2 * oi + 1];
+                // the next op's first half (an L1/L2 load when descriptors stay global)
+                if (oi + 1 < kp.n_ops) h0 = dsc[2 * oi + 2];
+                const uint32_t ob = h1.x, oc = h1.y;
+                if ((flags & F_BARRIER) || staging) group_sync();
+                const uint32_t buf = (uint32_t)oi & 1u;
+                // TMA: stage the next op's operand block into the other buffer
+                // (free: every thread has passed this op's barrier)
+                if (staging && tid == 0 && oi + 1 < kp.n_ops) {
+                    const StageBlock b = stage_block(kp, h0, dsc[2 * oi + 3], pregen, ncnt, hits);
+                    if (b.bytes) bulk_load(stg + (buf ^ 1u) * (STAGE_BYTES / 4), b.src, b.bytes, mbar + (buf ^ 1u));
+                }
+                // this op's operands: staged copy (wait for its bulk transaction) or global
+                const uint32_t* ops32 = nullptr;
+                if (staging) {
+                    const StageBlock b = stage_block(kp, make_uint4(kind | (code << 8) | (flags << 16), count, off, oa),
+                                                     h1, pregen, ncnt, hits);
+                    if (b.bytes) {
+                        mbar_wait(mbar + buf, (phase >> buf) & 1u);
+                        phase ^= 1u << buf;
+                        ops32 = stg + buf * (STAGE_BYTES / 4) + b.woff;
                     }
                 }
                 if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
                     tile == 0)  // profiling: op-boundary timestamps of the first tile
                     kp.op_clock[oi] = clock64();
-                const uint32_t* tg = kp.targets + off;
+                const uint32_t* const tgg = kp.targets + off;  // global targets
+                const uint32_t* const tg = (ops32 != nullptr && kind != K_NOISE && kind != K_DET) ? ops32 : tgg;
                 if (kp.debug_skip) {
                     const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
                                        : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
@@ -575,8 +647,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 switch (kind) {
                 case K_GATE: {
                     const int items = (int)(count << LC);
-                    auto q1 = [&](int i) { return __ldg(tg + (i >> LC)); };
-                    auto q2 = [&](int i) { return __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC)); };
+                    auto q1 = [&](int i) { return tg[i >> LC]; };
+                    auto q2 = [&](int i) { return reinterpret_cast<const uint2*>(tg)[i >> LC]; };
                     switch (code) {
                     case R_SWAPXZ:
                         batched_items<4>(tid, nth, items, q1, [&](int i, uint32_t q) {
@@ -623,7 +695,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 case K_M: case K_MR: {
                     const int items = (int)(count << LC);
                     batched_items<2>(tid, nth, items,
-                        [&](int i) { return __ldg(reinterpret_cast<const uint2*>(tg) + (i >> LC)); },
+                        [&](int i) { return reinterpret_cast<const uint2*>(tg)[i >> LC]; },
                         [&](int i, uint2 qs) {
                             const int j = i >> LC, c = i & (C - 1);
                             const size_t p = (size_t)qs.x * W + c * V;
@@ -643,7 +715,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 }
                 case K_R: {
                     const int items = (int)(count << LC);
-                    batched_items<4>(tid, nth, items, [&](int i) { return __ldg(tg + (i >> LC)); },
+                    batched_items<4>(tid, nth, items, [&](int i) { return tg[i >> LC]; },
                         [&](int i, uint32_t q) {
                             const int j = i >> LC, c = i & (C - 1);
                             const size_t p = (size_t)q * W + c * V;
@@ -659,7 +731,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                         const int items = (int)((count * ar) << LC);
                         for (int i = tid; i < items; i += nth) {
                             const int j = i >> LC, c = i & (C - 1);
-                            const size_t p = (size_t)__ldg(tg + j) * W + c * V;
+                            const size_t p = (size_t)__ldg(tgg + j) * W + c * V;
                             const uint32_t* mrow = kp.masks + (int64_t)(oa + 2 * j) * kp.inject_words + tile * W + c * V;
                             const VW<V> mx = vldg<V>(mrow), mz = vldg<V>(mrow + kp.inject_words);
                             if (flags & F_DUP) {
@@ -678,18 +750,23 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     if ((flags & F_PREGEN) && pregen) {
                         const uint32_t nh = ncnt[ob];  // NO_SLOT: the hit list overflowed
                         if (nh != NO_SLOT) {
-                            if (!(kp.debug_skip & 256))
+                            if (kp.debug_skip & 512) {  // profiling: loads only
+                                uint64_t acc = 0;
+                                for (uint32_t i = tid; i < nh; i += nth) acc ^= hits[oc + i];
+                                if (acc == 0x123456789ull) X[0] ^= 1u;
+                            } else if (!(kp.debug_skip & 256)) {
+                                const uint64_t* hl = ops32 != nullptr ? reinterpret_cast<const uint64_t*>(ops32)
+                                                                      : hits + oc;
                                 for (uint32_t i = tid; i < nh; i += nth)
-                                    apply_entry<W>(X, Z, hits[oc + i], (kp.debug_skip & 128) != 0);
+                                    apply_entry<W>(X, Z, hl[i], (kp.debug_skip & 128) != 0);
+                            }
                         } else {
                             const NoiseParam* npp = kp.noise + ob;
                             for (uint32_t r = tid; r < __ldg(&npp->nchunks); r += nth)
                                 noise_chunk(kp, *npp, ob, r, g, sl, ss, [&](uint32_t trial, uint32_t pick) {
-                                    apply_hit<W>(X, Z, tg, code, ar, trial, pick);
+                                    apply_hit<W>(X, Z, tgg, code, ar, trial, pick);
                                 });
                         }
-                        pf_ord = od;  // the next pre-generated op and its hit-list base
-                        pf_base = oe;
                         break;
                     }
                     if (kp.debug_skip & 2) break;
@@ -698,7 +775,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     // inline sampling (large-p ops)
                     for (uint32_t r = tid; r < np.nchunks; r += nth)
                         noise_chunk(kp, np, ob, r, g, sl, ss, [&](uint32_t trial, uint32_t pick) {
-                            apply_hit<W>(X, Z, tg, code, ar, trial, pick);
+                            apply_hit<W>(X, Z, tgg, code, ar, trial, pick);
                         });
                     break;
                 }
@@ -714,8 +791,10 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                             uint32_t e0, e1;
                             if (code) { e0 = off + ci * code; e1 = e0 + code; }
                             else { e0 = __ldg(kp.det_ptr + col); e1 = __ldg(kp.det_ptr + col + 1); }
-                            const uint32_t s0 = e0 < e1 ? __ldg(kp.det_terms + e0) : NO_SLOT;
-                            const uint32_t s1 = e0 + 1 < e1 ? __ldg(kp.det_terms + e0 + 1) : NO_SLOT;
+                            // staged uniform terms live at ops32[e - off]
+                            const uint32_t* tb = (code && ops32 != nullptr) ? ops32 - off : kp.det_terms;
+                            const uint32_t s0 = e0 < e1 ? tb[e0] : NO_SLOT;
+                            const uint32_t s1 = e0 + 1 < e1 ? tb[e0 + 1] : NO_SLOT;
                             return make_uint4(e0, e1, s0, s1);
                         },
                         [&](int i, uint4 d) {
@@ -753,7 +832,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     for (int c = tid; c < C; c += nth) {
                         VW<V> acc = vld<V>(ring + (size_t)oa * W + c * V);
                         for (uint32_t j = 0; j < count; j++) {
-                            const uint32_t s = __ldg(tg + j);
+                            const uint32_t s = tg[j];
                             acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
                         }
                         vst<V>(ring + (size_t)oa * W + c * V, acc);
