@@ -462,7 +462,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     CUDA_TRY(pg->d_nscratch.reserve((size_t)pg->cfg.grid * pg->cfg.threads * NZ_MAX_LIST));
     kp.noise_scratch = pg->d_nscratch.p;
     if (pg->opts.debug_skip & 64) {  // op-boundary clock trace of the first tile
-        CUDA_TRY(pg->d_clock.reserve(hp.ops.size() + 1));
+        CUDA_TRY(pg->d_clock.reserve(hp.ops.size() * 9 + 1));
         kp.op_clock = pg->d_clock.p;
     }
 
@@ -685,7 +685,7 @@ extern "C" int pfs_detector_events(int device, const uint8_t* flips_b8, int64_t 
 extern "C" int pfs_program_op_clock(pfs_program* pg, long long* out, int64_t n) {
     if (!pg || !out) return fail(PFS_E_INVALID, "null argument");
     if (!pg->d_clock.p) return fail(PFS_E_INVALID, "no clock trace (set debug_skip bit 6)");
-    const int64_t m = std::min<int64_t>(n, (int64_t)pg->hp.ops.size());
+    const int64_t m = std::min<int64_t>(n, (int64_t)pg->hp.ops.size() * 9);
     CUDA_TRY(cudaMemcpy(out, pg->d_clock.p, m * sizeof(long long), cudaMemcpyDeviceToHost));
     return PFS_OK;
 }

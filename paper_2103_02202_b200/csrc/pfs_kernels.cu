@@ -552,6 +552,10 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     const int ss = 1;
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
     const bool staging = kp.stage != 0;
+    // with staging, the group's last warp is a dedicated TMA issuer: it only
+    // issues the next op's bulk copy, so its latency never delays item work
+    const int nthw = (staging && gsz >= 64) ? gsz - 32 : gsz;  // item workers
+    const int issuer = staging ? (gsz >= 64 ? gsz - 32 : 0) : -1;
     const uint32_t bar_id = 1u + (uint32_t)grp;
     auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gsz) : "memory"); };
 
@@ -602,7 +606,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     }
                 }
             group_sync();  // counts visible, previous tile's staging buffers free
-            if (staging && tid == 0 && kp.n_ops > 0) {
+            if (tid == issuer && kp.n_ops > 0) {
                 const StageBlock b = stage_block(kp, dsc[0], dsc[1], pregen, ncnt, hits);
                 if (b.bytes) bulk_load(stg, b.src, b.bytes, mbar);
             }
@@ -619,7 +623,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 const uint32_t buf = (uint32_t)oi & 1u;
                 // TMA: stage the next op's operand block into the other buffer
                 // (free: every thread has passed this op's barrier)
-                if (staging && tid == 0 && oi + 1 < kp.n_ops) {
+                if (tid == issuer && oi + 1 < kp.n_ops) {
                     const StageBlock b = stage_block(kp, h0, dsc[2 * oi + 3], pregen, ncnt, hits);
                     if (b.bytes) bulk_load(stg + (buf ^ 1u) * (STAGE_BYTES / 4), b.src, b.bytes, mbar + (buf ^ 1u));
                 }
@@ -629,7 +633,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     const StageBlock b = stage_block(kp, make_uint4(kind | (code << 8) | (flags << 16), count, off, oa),
                                                      h1, pregen, ncnt, hits);
                     if (b.bytes) {
-                        mbar_wait(mbar + buf, (phase >> buf) & 1u);
+                        if (tid < nthw) mbar_wait(mbar + buf, (phase >> buf) & 1u);
                         phase ^= 1u << buf;
                         ops32 = stg + buf * (STAGE_BYTES / 4) + b.woff;
                     }
@@ -644,6 +648,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                                        : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
                     if (kp.debug_skip & bit) continue;
                 }
+                if (tid >= nthw) continue;  // the issuer warp does no item work
+                const int nth = nthw;       // items are spread over the worker threads
                 switch (kind) {
                 case K_GATE: {
                     const int items = (int)(count << LC);
@@ -841,6 +847,9 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 }
                 default: break;
                 }
+                if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tile == 0 &&
+                    (tid & 31) == 0 && (tid >> 5) < 8)  // profiling: per-warp end of op work
+                    kp.op_clock[(size_t)kp.n_ops * (1 + (tid >> 5)) + oi] = clock64();
             }
         }
         group_sync();  // the group's frame is reused by its next tile

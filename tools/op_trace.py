@@ -30,9 +30,12 @@ def main():
     for i in range(3):
         ds.sample_rows(a.shots, seed=i, out=out)
     torch.cuda.synchronize()
-    clk = ds.native.op_clock()
+    clk9 = ds.native.op_clock()
+    clk = clk9[0]
+    ends = clk9[1:]  # per-warp (warps 0..7) end of each op's work
     ops = ds.native.ops()
     dt = np.diff(clk)
+    work = ends[:, :-1] - clk[None, :-1]  # per warp: op start (barrier exit) -> own work done
     names = {0: "GATE", 1: "M", 2: "R", 3: "MR", 4: "NOISE", 5: "DET", 6: "OBS"}
     agg = collections.defaultdict(lambda: [0, 0])
     for i, d in enumerate(dt):
@@ -53,8 +56,15 @@ def main():
         agg2[key][0] += 1
         agg2[key][1] += int(d)
         agg2[key][2] += int(ops[i, 1])
+    wk = collections.defaultdict(list)
+    for i in range(len(dt)):
+        k = int(ops[i, 0] & 0xFF)
+        wk[(names.get(k, str(k)), int((ops[i, 0] >> 8) & 0xFF))].append(work[:, i])
     for k, (n, c, cnt) in sorted(agg2.items(), key=lambda x: -x[1][1]):
-        print(f"  {k[0]:6s} code={k[1]} n={n:4d} avg_cycles={c / n:8.0f} avg_count={cnt / n:8.1f}")
+        w = np.array(wk[k])
+        print(f"  {k[0]:6s} code={k[1]} n={n:4d} avg_cycles={c / n:8.0f} avg_count={cnt / n:8.1f} "
+              f"warp0_work={w[:, 0].mean():7.0f} warpmax_work={w.max(axis=1).mean():7.0f} "
+              f"warpmin_work={w.min(axis=1).mean():7.0f}")
     top = np.argsort(dt)[::-1][:15]
     for i in top:
         print(f"  op {i:4d} kind={names.get(int(ops[i, 0] & 0xFF))} code={(ops[i, 0] >> 8) & 0xFF} "
