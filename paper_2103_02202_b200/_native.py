@@ -14,7 +14,9 @@ import numpy as np
 from .program import FlatProgram
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "_lib", "libpfs.so")
+# PFS_PROFILE=1 selects the profiling build (op clock traces, ablations; tools/ only)
+LIB_PATH = os.path.join(_PKG, "_lib", "libpfs_profile.so" if os.environ.get("PFS_PROFILE") == "1"
+                        else "libpfs.so")
 
 MODE_FLIPS, MODE_SAMPLES, MODE_DETECTORS, MODE_COUNTS, MODE_FLIPS_ROWS, MODE_DETECTORS_ROWS = range(6)
 E_INVALID, E_CUDA, E_NOMEM, E_NODEVICE = -1, -2, -3, -4

@@ -177,6 +177,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
     try {
         reorder_for_banks(pg->hp, pg->cfg.W);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
+        assign_staging(pg->hp);
     } catch (const std::invalid_argument& e) {
         delete pg;
         return fail(PFS_E_INVALID, e.what());

@@ -477,14 +477,32 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
         o.kcf &= ~(F_PREGEN << 16);
         if (np.flags & NZ_PREGEN) o.kcf |= F_PREGEN << 16;
         o.c = np.cap_base;
-        // the next pre-generated op after this one in program order
-        uint32_t nx = NO_SLOT;
-        if (np.flags & NZ_PREGEN) nx = next_of[o.b];
-        else {
-            for (uint32_t q : hp.pregen_ops) if (q > o.b) { nx = q; break; }
+    }
+}
+
+// Static operand blocks (targets, uniform detector terms) staged by TMA:
+// d = 16-byte aligned word offset of the block in its array, e = valid | array |
+// first-operand word offset | size in 16-byte units.
+void assign_staging(HostProgram& hp) {
+    for (DOp& o : hp.ops) {
+        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
+        uint64_t words = 0;
+        uint32_t arr = 0;
+        switch (kind) {
+            case K_GATE: words = (uint64_t)o.count * (rule_arity(code) == 2 ? 2 : 1); break;
+            case K_M: case K_MR: words = 2ull * o.count; break;
+            case K_R: case K_OBS: words = o.count; break;
+            case K_DET: if (code) { words = (uint64_t)o.count * code; arr = 1; } break;
+            default: break;
         }
-        o.d = nx;
-        o.e = nx == NO_SLOT ? 0u : hp.noise[nx].cap_base;
+        o.d = 0;
+        o.e = 0;
+        if (kind == K_NOISE || words == 0) continue;
+        const uint64_t lo = o.off & ~3u;
+        const uint64_t bytes = ((o.off + words - lo) * 4 + 15) & ~15ull;
+        if (bytes > (uint64_t)STAGE_BYTES) continue;
+        o.d = (uint32_t)lo;
+        o.e = 0x80000000u | (arr << 30) | ((o.off - (uint32_t)lo) << 16) | (uint32_t)(bytes / 16);
     }
 }
 

@@ -43,8 +43,8 @@ constexpr int DESC_SMEM_MAX = 16384;      // distinct-position list; larger coun
 //   M/MR : count = targets, off -> (qubit, slot) pairs, a = rec_base, b = coin_base
 //   R    : count = targets, off -> qubits, b = coin_base
 //   NOISE: count = apps, off -> targets, a = noise_row_base, b = noise ordinal,
-//          c = hit-list base, d = next pre-generated ordinal (NO_SLOT: none),
-//          e = that op's hit-list base (consumers prefetch its first hits)
+//          c = hit-list base
+//   all but NOISE: d/e = TMA staging block of the op's operands (assign_staging)
 //   DET  : count = columns, a = first column (terms via det_ptr/det_terms)
 //   OBS  : count = terms, off -> record slots, a = accumulator slot
 struct DOp {
@@ -119,6 +119,7 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
 
 void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits);
 void reorder_for_banks(HostProgram& hp, int W);
+void assign_staging(HostProgram& hp);
 
 // Kernel launch plumbing (pfs_kernels.cu)
 struct KParams {

@@ -17,6 +17,12 @@
 
 #include "pfs_internal.h"
 
+// PFS_PROFILE=1 builds the profiling library (op clock traces, ablations);
+// the production kernels carry none of it.
+#ifndef PFS_PROFILE
+#define PFS_PROFILE 0
+#endif
+
 namespace pfs {
 
 // ---------------------------------------------------------------- Philox
@@ -83,7 +89,9 @@ __device__ __forceinline__ VW<V> coin_words(const KParams& kp, uint32_t e, int c
                                             int64_t tile) {
     if (kp.coins != nullptr)
         return vldg<V>(kp.coins + (int64_t)e * kp.inject_words + tile * W + c * V);
+#if PFS_PROFILE
     if (kp.debug_skip & 4) return vzero<V>();
+#endif
     const int word = c * V;
     uint32_t c0 = e, c1 = (uint32_t)(word >> 2), c2 = g, c3 = DOMAIN_COIN;
     philox4x32_10(c0, c1, c2, c3, (uint32_t)kp.seed, (uint32_t)(kp.seed >> 32));
@@ -458,37 +466,37 @@ __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     }
 }
 
-// Operand block of an op (descriptor halves h0/h1): the contiguous global range
-// its items read — targets, uniform detector terms, or (pre-sampled noise) the
-// tile's hit list.  Returns the 16-byte aligned source, its size, and the word
-// offset of the first operand inside it; size 0 = not staged.
+// Operand block of an op: static blocks (targets, uniform detector terms) come
+// precomputed in the descriptor (h1.z = aligned word offset, h1.w = valid |
+// array | word offset | 16-byte units); a pre-sampled noise op's block is this
+// tile's hit list, sized at run time.  bytes 0 = read from global memory.
 struct StageBlock { const char* src; uint32_t bytes; uint32_t woff; };
-__device__ __forceinline__ StageBlock stage_block(const KParams& kp, uint4 h0, uint4 h1, bool pregen,
+__device__ __forceinline__ StageBlock stage_block(const KParams& kp, uint32_t kcf, uint4 h1, bool pregen,
                                                   const uint32_t* ncnt, const uint64_t* hits) {
-    const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
-    const char* src = nullptr;
-    uint32_t bytes = 0;
-    switch (kind) {
-        case K_GATE: src = (const char*)(kp.targets + h0.z); bytes = h0.y * (code >= R_CX ? 8u : 4u); break;
-        case K_M: case K_MR: src = (const char*)(kp.targets + h0.z); bytes = h0.y * 8u; break;
-        case K_R: case K_OBS: src = (const char*)(kp.targets + h0.z); bytes = h0.y * 4u; break;
-        case K_DET: if (code) { src = (const char*)(kp.det_terms + h0.z); bytes = h0.y * code * 4u; } break;
-        case K_NOISE:
-            if (pregen && (flags & F_PREGEN)) {
-                const uint32_t nh = ncnt[h1.x];
-                if (nh != NO_SLOT) { src = (const char*)(hits + h1.y); bytes = nh * 8u; }
-            }
-            break;
-        default: break;
-    }
     StageBlock b{nullptr, 0u, 0u};
-    if (src == nullptr || bytes == 0) return b;
-    const uintptr_t lo = reinterpret_cast<uintptr_t>(src) & ~(uintptr_t)15;
-    const uint32_t sz = (uint32_t)((reinterpret_cast<uintptr_t>(src) + bytes - lo + 15) & ~(uintptr_t)15);
-    if (sz > (uint32_t)STAGE_BYTES) return b;
-    b.src = reinterpret_cast<const char*>(lo);
-    b.bytes = sz;
-    b.woff = (uint32_t)((reinterpret_cast<uintptr_t>(src) - lo) >> 2);
+    if ((kcf & 0xFFu) == K_NOISE) {
+        if (pregen && ((kcf >> 16) & F_PREGEN)) {
+            const uint32_t nh = ncnt[h1.x];
+            if (nh != NO_SLOT && nh) {
+                const uintptr_t src = reinterpret_cast<uintptr_t>(hits + h1.y);
+                const uintptr_t lo = src & ~(uintptr_t)15;
+                const uint32_t sz = (uint32_t)((src + nh * 8u - lo + 15) & ~(uintptr_t)15);
+                if (sz <= (uint32_t)STAGE_BYTES) {
+                    b.src = reinterpret_cast<const char*>(lo);
+                    b.bytes = sz;
+                    b.woff = (uint32_t)((src - lo) >> 2);
+                }
+            }
+        }
+        return b;
+    }
+    const uint32_t e = h1.w;
+    if (e >> 31) {
+        const uint32_t* arr = (e & 0x40000000u) ? kp.det_terms : kp.targets;
+        b.src = reinterpret_cast<const char*>(arr + h1.z);
+        b.bytes = (e & 0xFFFFu) * 16u;
+        b.woff = (e >> 16) & 3u;
+    }
     return b;
 }
 
@@ -607,7 +615,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 }
             group_sync();  // counts visible, previous tile's staging buffers free
             if (tid == issuer && kp.n_ops > 0) {
-                const StageBlock b = stage_block(kp, dsc[0], dsc[1], pregen, ncnt, hits);
+                const StageBlock b = stage_block(kp, dsc[0].x, dsc[1], pregen, ncnt, hits);
                 if (b.bytes) bulk_load(stg, b.src, b.bytes, mbar);
             }
 
@@ -624,30 +632,33 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 // TMA: stage the next op's operand block into the other buffer
                 // (free: every thread has passed this op's barrier)
                 if (tid == issuer && oi + 1 < kp.n_ops) {
-                    const StageBlock b = stage_block(kp, h0, dsc[2 * oi + 3], pregen, ncnt, hits);
+                    const StageBlock b = stage_block(kp, h0.x, dsc[2 * oi + 3], pregen, ncnt, hits);
                     if (b.bytes) bulk_load(stg + (buf ^ 1u) * (STAGE_BYTES / 4), b.src, b.bytes, mbar + (buf ^ 1u));
                 }
                 // this op's operands: staged copy (wait for its bulk transaction) or global
                 const uint32_t* ops32 = nullptr;
                 if (staging) {
-                    const StageBlock b = stage_block(kp, make_uint4(kind | (code << 8) | (flags << 16), count, off, oa),
-                                                     h1, pregen, ncnt, hits);
+                    const StageBlock b = stage_block(kp, kind | (code << 8) | (flags << 16), h1, pregen, ncnt, hits);
                     if (b.bytes) {
                         if (tid < nthw) mbar_wait(mbar + buf, (phase >> buf) & 1u);
                         phase ^= 1u << buf;
                         ops32 = stg + buf * (STAGE_BYTES / 4) + b.woff;
                     }
                 }
+#if PFS_PROFILE
                 if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
                     tile == 0)  // profiling: op-boundary timestamps of the first tile
                     kp.op_clock[oi] = clock64();
+#endif
                 const uint32_t* const tgg = kp.targets + off;  // global targets
                 const uint32_t* const tg = (ops32 != nullptr && kind != K_NOISE && kind != K_DET) ? ops32 : tgg;
+#if PFS_PROFILE
                 if (kp.debug_skip) {
                     const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
                                        : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
                     if (kp.debug_skip & bit) continue;
                 }
+#endif
                 if (tid >= nthw) continue;  // the issuer warp does no item work
                 const int nth = nthw;       // items are spread over the worker threads
                 switch (kind) {
@@ -756,16 +767,9 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     if ((flags & F_PREGEN) && pregen) {
                         const uint32_t nh = ncnt[ob];  // NO_SLOT: the hit list overflowed
                         if (nh != NO_SLOT) {
-                            if (kp.debug_skip & 512) {  // profiling: loads only
-                                uint64_t acc = 0;
-                                for (uint32_t i = tid; i < nh; i += nth) acc ^= hits[oc + i];
-                                if (acc == 0x123456789ull) X[0] ^= 1u;
-                            } else if (!(kp.debug_skip & 256)) {
-                                const uint64_t* hl = ops32 != nullptr ? reinterpret_cast<const uint64_t*>(ops32)
-                                                                      : hits + oc;
-                                for (uint32_t i = tid; i < nh; i += nth)
-                                    apply_entry<W>(X, Z, hl[i], (kp.debug_skip & 128) != 0);
-                            }
+                            const uint64_t* hl = ops32 != nullptr ? reinterpret_cast<const uint64_t*>(ops32)
+                                                                  : hits + oc;
+                            for (uint32_t i = tid; i < nh; i += nth) apply_entry<W>(X, Z, hl[i]);
                         } else {
                             const NoiseParam* npp = kp.noise + ob;
                             for (uint32_t r = tid; r < __ldg(&npp->nchunks); r += nth)
@@ -847,9 +851,11 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 }
                 default: break;
                 }
+#if PFS_PROFILE
                 if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tile == 0 &&
                     (tid & 31) == 0 && (tid >> 5) < 8)  // profiling: per-warp end of op work
                     kp.op_clock[(size_t)kp.n_ops * (1 + (tid >> 5)) + oi] = clock64();
+#endif
             }
         }
         group_sync();  // the group's frame is reused by its next tile
