@@ -1019,22 +1019,32 @@ __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __rest
     const int64_t r0 = (int64_t)blockIdx.y * 256;
     const int rows = (int)((num_rows - r0) < 256 ? (num_rows - r0) : 256);
     const uint32_t* src = tiles + tile * num_rows * TW + r0 * TW + part * W;
-    // all W loads of a thread are issued before any is used
+    // thread t owns row t of the block: its W words are contiguous (16-byte
+    // vector loads when W >= 4), all issued before use
+    const int r = t;
     uint32_t v[W];
+    if (r < rows) {
+        const uint32_t* rp = src + (size_t)r * TW;
+        if constexpr (W >= 4) {
 #pragma unroll
-    for (int k = 0; k < W; k++) {
-        const int i = t + 256 * k;
-        const int r = i / W, w = i % W;
-        v[k] = (r < rows) ? __ldg(src + r * TW + w) : 0u;
+            for (int k = 0; k < W / 4; k++) {
+                const uint4 q = __ldg(reinterpret_cast<const uint4*>(rp) + k);
+                v[4 * k] = q.x; v[4 * k + 1] = q.y; v[4 * k + 2] = q.z; v[4 * k + 3] = q.w;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < W; k++) v[k] = __ldg(rp + k);
+        }
+        if (xor_bits != nullptr && (__ldg(xor_bits + r0 + r) & 1u)) {
+#pragma unroll
+            for (int k = 0; k < W; k++) v[k] = ~v[k];
+        }
+    } else {
+#pragma unroll
+        for (int k = 0; k < W; k++) v[k] = 0u;
     }
 #pragma unroll
-    for (int k = 0; k < W; k++) {
-        const int i = t + 256 * k;
-        const int r = i / W, w = i % W;
-        uint32_t x = v[k];
-        if (xor_bits != nullptr && r < rows && (__ldg(xor_bits + r0 + r) & 1u)) x = ~x;
-        tin[r * Wp + w] = x;
-    }
+    for (int k = 0; k < W; k++) tin[r * Wp + k] = v[k];
     __syncthreads();
     const int warp = t >> 5, lane = t & 31;
 #pragma unroll

@@ -39,6 +39,9 @@ def main():
         ("G2_W8", {"words_per_tile": 8, "ring_in_smem": 0, "groups": 2}),
         ("G2_W4", {"words_per_tile": 4, "ring_in_smem": 0, "groups": 2}),
         ("G2_W8_512", {"words_per_tile": 8, "ring_in_smem": 0, "groups": 2, "threads": 512}),
+        ("G1_W8_rs", {"words_per_tile": 8, "ring_in_smem": 1, "groups": 1}),
+        ("G2_W4_rs", {"words_per_tile": 4, "ring_in_smem": 1, "groups": 2}),
+        ("G1_W16_640", {"words_per_tile": 16, "ring_in_smem": 0, "groups": 1, "threads": 640}),
         ("W8_512thr", {"threads": 512}),
         ("W4_smem", {"words_per_tile": 4, "ring_in_smem": 1}),
         ("hits2", {"noise_target_hits": 2.0}),
