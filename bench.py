@@ -42,6 +42,7 @@ def parse_args():
     ap.add_argument("--words", type=int, default=0, help="override W (32-shot words per tile)")
     ap.add_argument("--ring", type=int, default=-1)
     ap.add_argument("--threads", type=int, default=0)
+    ap.add_argument("--kernel", type=int, default=0, help="frame kernel: 0 auto, 1 cooperative, 2 warp-private")
     ap.add_argument("--target-hits", type=float, default=0.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
@@ -211,7 +212,7 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     flat = flatten(config_text(cfg))
     compile_s = time.perf_counter() - t0
     kw = dict(words_per_tile=args.words, ring_in_smem=args.ring, threads=args.threads,
-              noise_target_hits=args.target_hits)
+              noise_target_hits=args.target_hits, kernel=args.kernel)
     ds = DetectorSampler.__new__(DetectorSampler)
     ds.circuit, ds.flat, ds.device = None, flat, local_rank
     ds._seeds = np.random.default_rng(0)

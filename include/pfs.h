@@ -53,7 +53,10 @@ typedef struct pfs_options {
     int32_t schedule_only;    /* 1: compile without the shared-memory fit check (the
                                  program exposes info / noise schedule, cannot run)  */
     int32_t groups;           /* independent tiles in flight per CTA (0 = auto)     */
-    int32_t reserved[3];
+    int32_t kernel;           /* frame kernel: 0 auto, 1 cooperative (a CTA's threads
+                                 share one tile), 2 warp-private (a warp owns one
+                                 32-shot word column, no CTA barriers)               */
+    int32_t reserved[2];
 } pfs_options;
 
 typedef struct pfs_info {
@@ -77,7 +80,8 @@ typedef struct pfs_info {
     int64_t hit_capacity;     /* pre-generated noise hit-list entries per CTA       */
     int64_t pregen_chunks;    /* noise work items (32 chunks each) per tile         */
     int64_t groups;           /* independent tiles in flight per CTA                */
-    int64_t reserved[2];
+    int64_t kernel;           /* frame kernel of row-producing modes: 1 cooperative, 2 warp */
+    int64_t warps_per_cta;    /* warp-private kernel: word columns per CTA (0: unused) */
 } pfs_info;
 
 enum pfs_mode {

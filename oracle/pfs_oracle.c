@@ -205,12 +205,14 @@ static inline void coin_words(const orc_job* jb, int64_t e, uint64_t g, int64_t 
         memcpy(dst, src, sizeof(uint32_t) * nw);
         return;
     }
+    /* windows of 128 rows: row e of word w is word (e >> 5) & 3 of the block with
+       counter (((e >> 7) << 5) | (e & 31), w, g, DOMAIN_COIN) */
     uint32_t key[2] = {(uint32_t)jb->seed, (uint32_t)(jb->seed >> 32)};
-    for (int c = 0; c * 4 < nw; c++) {
-        uint32_t ctr[4] = {(uint32_t)e, (uint32_t)c, (uint32_t)g, DOMAIN_COIN};
+    for (int w = 0; w < nw; w++) {
+        uint32_t ctr[4] = {(uint32_t)(((e >> 7) << 5) | (e & 31)), (uint32_t)w, (uint32_t)g, DOMAIN_COIN};
         uint32_t o[4];
         orc_philox4x32_10(ctr, key, o);
-        for (int j = 0; j < 4 && c * 4 + j < nw; j++) dst[c * 4 + j] = o[j];
+        dst[w] = o[(e >> 5) & 3];
     }
 }
 

@@ -15,8 +15,9 @@ from .program import FlatProgram
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
 # PFS_PROFILE=1 selects the profiling build (op clock traces, ablations; tools/ only)
-LIB_PATH = os.path.join(_PKG, "_lib", "libpfs_profile.so" if os.environ.get("PFS_PROFILE") == "1"
-                        else "libpfs.so")
+# PFS_LIB=<path> loads an experimental build instead (A/B timing in tools/ only)
+LIB_PATH = os.environ.get("PFS_LIB") or os.path.join(
+    _PKG, "_lib", "libpfs_profile.so" if os.environ.get("PFS_PROFILE") == "1" else "libpfs.so")
 
 MODE_FLIPS, MODE_SAMPLES, MODE_DETECTORS, MODE_COUNTS, MODE_FLIPS_ROWS, MODE_DETECTORS_ROWS = range(6)
 E_INVALID, E_CUDA, E_NOMEM, E_NODEVICE = -1, -2, -3, -4
@@ -32,7 +33,7 @@ class Options(ctypes.Structure):
                 ("noise_target_hits", ctypes.c_double), ("timing", ctypes.c_int32),
                 ("debug_skip", ctypes.c_int32), ("producer_threads", ctypes.c_int32),
                 ("schedule_only", ctypes.c_int32), ("groups", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 3)]
+                ("kernel", ctypes.c_int32), ("reserved", ctypes.c_int32 * 2)]
 
 
 class Info(ctypes.Structure):
@@ -46,7 +47,7 @@ class Info(ctypes.Structure):
                 ("num_coin_rows", ctypes.c_int64), ("num_noise_rows", ctypes.c_int64),
                 ("noise_tab_len", ctypes.c_int64), ("hit_capacity", ctypes.c_int64),
                 ("pregen_chunks", ctypes.c_int64), ("groups", ctypes.c_int64),
-                ("reserved", ctypes.c_int64 * 2)]
+                ("kernel", ctypes.c_int64), ("warps_per_cta", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
         return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
@@ -150,7 +151,7 @@ class NativeProgram:
     def __init__(self, prog: FlatProgram, words_per_tile: int = 0, ring_in_smem: int = -1,
                  threads: int = 0, ctas_per_sm: int = 0, noise_target_hits: float = 0.0,
                  timing: bool = False, debug_skip: int = 0, producer_threads: int = 0,
-                 schedule_only: bool = False, groups: int = 0):
+                 schedule_only: bool = False, groups: int = 0, kernel: int = 0):
         L = lib()
         self.flat = prog
         self._keep = [np.ascontiguousarray(prog.instrs, dtype=np.int32),
@@ -161,7 +162,7 @@ class NativeProgram:
         ins, tg, p, dp, di = self._keep
         opts = Options(words_per_tile, ring_in_smem, threads, ctas_per_sm, noise_target_hits,
                        1 if timing else 0, debug_skip, producer_threads, 1 if schedule_only else 0,
-                       groups)
+                       groups, kernel)
         h = ctypes.c_void_p()
         _check(L.pfs_program_create(_p(ins), ins.shape[0], _p(tg), tg.shape[0], _p(p), p.shape[0],
                                     _p(dp), _p(di), prog.num_columns, prog.num_observables,

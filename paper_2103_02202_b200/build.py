@@ -20,6 +20,7 @@ LIB = os.path.join(LIB_DIR, "libpfs.so")
 PROFILE_LIB = os.path.join(LIB_DIR, "libpfs_profile.so")  # PFS_PROFILE=1: traces, ablations
 SOURCES = ["pfs_compile.cpp", "pfs_kernels.cu", "pfs_api.cu"]
 HEADERS = ["pfs_internal.h", os.path.join("..", "..", "include", "pfs.h")]
+INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 
@@ -40,19 +41,22 @@ def _stale(lib=LIB) -> bool:
     return False
 
 
-def build(force: bool = False, verbose: bool = False, profile: bool = False) -> str:
-    lib = PROFILE_LIB if profile else LIB
-    if not force and not _stale(lib):
+def build(force: bool = False, verbose: bool = False, profile: bool = False,
+          out: str | None = None, csrc: str = CSRC, defines: tuple = ()) -> str:
+    """out/csrc/defines: experimental builds for A/B timing (tools only)."""
+    lib = out or (PROFILE_LIB if profile else LIB)
+    if not force and out is None and not _stale(lib):
         return lib
     os.makedirs(LIB_DIR, exist_ok=True)
     tmp = lib + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--threads", "0",
-           "-Xcompiler", "-fPIC,-O3", "-shared", "-o", tmp]
+           "-Xcompiler", "-fPIC,-O3", "-shared", "-I", INCLUDE, "-o", tmp]
     if profile:
         cmd += ["-DPFS_PROFILE=1"]
+    cmd += [f"-D{d}" for d in defines]
     if verbose:
         cmd += ["-Xptxas", "-v"]
-    cmd += [os.path.join(CSRC, f) for f in SOURCES]
+    cmd += [os.path.join(csrc, f) for f in SOURCES]
     cmd += ["-lcudart"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
@@ -64,4 +68,13 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False) -> 
 
 
 if __name__ == "__main__":
-    print(build(force=True, verbose="--verbose" in sys.argv, profile="--profile" in sys.argv))
+    import argparse
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--profile", action="store_true")
+    ap.add_argument("--out", default=None, help="experimental build path (load with PFS_LIB=)")
+    ap.add_argument("--csrc", default=CSRC)
+    ap.add_argument("-D", dest="defines", action="append", default=[])
+    a = ap.parse_args()
+    print(build(force=True, verbose=a.verbose, profile=a.profile, out=a.out, csrc=a.csrc,
+                defines=tuple(a.defines)))

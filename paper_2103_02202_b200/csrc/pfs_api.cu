@@ -54,7 +54,9 @@ struct DevBuf {
 struct pfs_program {
     HostProgram hp;
     pfs_options opts{};
-    LaunchCfg cfg{};
+    LaunchCfg cfg{};   // frame_kernel (cooperative); cfg.W is the program's tile width
+    LaunchCfg wcfg{};  // frame_warp_kernel (wcfg.kernel == 0: not eligible)
+    int warp_desc_smem = 0;
     int device = -1;
     int num_sms = 0;
     size_t smem_optin = kSmemBudget;
@@ -86,9 +88,38 @@ static size_t fixed_smem(const HostProgram& hp, int groups) {
            (desc_fits(hp) ? hp.ops.size() * sizeof(DOp) : 0);
 }
 
+// Warp-private kernel: a warp's word column (x/z per qubit, record ring, hit
+// counts) must fit shared memory several times over; descriptors join it when
+// they fit without costing a warp.
+static void choose_warp_layout(pfs_program* pg) {
+    const HostProgram& hp = pg->hp;
+    const size_t budget = pg->smem_optin;
+    const size_t per = warp_kernel_smem_per_warp(hp.num_qubits, hp.num_slots, hp.num_noise);
+    const size_t desc = hp.ops.size() * sizeof(DOp);
+    const int max_w = WARP_KERNEL_MAX_THREADS / 32;
+    int nw_g = (int)std::min<size_t>(max_w, budget / per);
+    int nw_s = desc <= budget ? (int)std::min<size_t>(max_w, (budget - desc) / per) : 0;
+    pg->wcfg = LaunchCfg{};
+    // opt-in (pfs_options.kernel = 2): measured slower than the cooperative
+    // kernel on the d=25 headline circuit
+    if (pg->opts.kernel != KERNEL_WARP || std::max(nw_g, nw_s) < 4) return;
+    const bool ds = nw_s >= nw_g;
+    const int nw = ds ? nw_s : nw_g;
+    pg->warp_desc_smem = ds ? 1 : 0;
+    pg->wcfg.kernel = KERNEL_WARP;
+    pg->wcfg.threads = 32 * nw;
+    pg->wcfg.groups = 1;
+    pg->wcfg.ring_smem = true;
+    pg->wcfg.smem_bytes = (ds ? desc : 0) + (size_t)nw * per;
+}
+
 static void choose_layout(pfs_program* pg) {
     const HostProgram& hp = pg->hp;
-    const pfs_options& o = pg->opts;
+    pfs_options o = pg->opts;
+    choose_warp_layout(pg);
+    // the warp-private kernel takes 8-word tiles (hit lists shared by 8 warps)
+    // unless the caller fixes W; the cooperative kernel then uses the same W
+    if (pg->wcfg.kernel && o.words_per_tile <= 0) o.words_per_tile = 8;
     const size_t budget = pg->smem_optin;
     const size_t fixed1 = fixed_smem(hp, 1), fixed2 = fixed_smem(hp, 2);
     auto frame = [&](int W) { return frame_smem_bytes(hp.num_qubits, W); };
@@ -101,6 +132,7 @@ static void choose_layout(pfs_program* pg) {
     if (o.words_per_tile > 0) {
         W = o.words_per_tile;
         G = o.groups > 0 ? o.groups : (fits(W, 2, false) ? 2 : 1);
+        if (pg->wcfg.kernel && !fits(W, G, false)) G = 1;
         if (o.ring_in_smem == 1) rs = true;
         else if (o.ring_in_smem == 0) rs = false;
         else rs = fits(W, G, true);
@@ -128,6 +160,11 @@ static void choose_layout(pfs_program* pg) {
     int threads = o.threads > 0 ? std::min(o.threads, FRAME_MAX_THREADS) : FRAME_MAX_THREADS;
     threads = (threads / (32 * G)) * 32 * G;  // whole warps per group
     pg->cfg.threads = threads;
+    pg->cfg.kernel = KERNEL_COOP;
+    if (pg->wcfg.kernel) {
+        pg->wcfg.W = W;
+        if (!fits(W, G, rs)) pg->cfg.kernel = 0;  // counts mode runs on the warp kernel too
+    }
 }
 
 extern "C" {
@@ -168,14 +205,16 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
     }
     choose_layout(pg);
     if (pg->opts.schedule_only && pg->cfg.W < 1) pg->cfg.W = pg->opts.words_per_tile > 0 ? pg->opts.words_per_tile : 1;
-    if (!pg->opts.schedule_only && (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget)) {
+    if (!pg->opts.schedule_only && !pg->wcfg.kernel && (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget)) {
         delete pg;
         return fail(PFS_E_INVALID, "frame table of " + std::to_string(num_qubits) +
                                        " qubits does not fit one CTA's shared memory");
     }
     const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 1.0;
     try {
-        reorder_for_banks(pg->hp, pg->cfg.W);
+        // warp kernel: 8-byte x/z rows, 16 lanes per shared-memory wavefront
+        reorder_for_banks(pg->hp, pg->wcfg.kernel ? 2 : pg->cfg.W);
+        dedup_operands(pg->hp);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
         assign_staging(pg->hp);
     } catch (const std::invalid_argument& e) {
@@ -193,10 +232,18 @@ int pfs_program_info(const pfs_program* pg, pfs_info* o) {
     o->num_qubits = hp.num_qubits;
     o->words_per_tile = pg->cfg.W;
     o->groups = pg->cfg.groups;
+    o->kernel = pg->wcfg.kernel ? KERNEL_WARP : KERNEL_COOP;
+    o->warps_per_cta = pg->wcfg.kernel ? pg->wcfg.threads / 32 : 0;
     o->tile_shots = 32 * pg->cfg.W;
     o->threads = pg->cfg.threads;
     o->ring_in_smem = pg->cfg.ring_smem ? 1 : 0;
     o->smem_bytes = (int32_t)pg->cfg.smem_bytes;
+    if (pg->wcfg.kernel) {  // row-producing modes run the warp-private kernel
+        o->threads = pg->wcfg.threads;
+        o->ring_in_smem = 1;
+        o->smem_bytes = (int32_t)pg->wcfg.smem_bytes;
+        o->groups = 1;
+    }
     o->num_measurements = hp.num_meas;
     o->num_columns = hp.num_cols;
     o->num_observables = hp.num_obs;
@@ -276,8 +323,11 @@ static int ensure_device(pfs_program* pg, int device) {
     if (prop.major != 10) return fail(PFS_E_NODEVICE, "libpfs is built for sm_100a (B200) only");
     pg->num_sms = prop.multiProcessorCount;
     pg->smem_optin = prop.sharedMemPerBlockOptin;
-    if (pg->cfg.smem_bytes > pg->smem_optin || pg->opts.schedule_only)
-        return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory (or schedule-only program)");
+    if (pg->opts.schedule_only)
+        return fail(PFS_E_INVALID, "schedule-only program");
+    if (pg->wcfg.kernel ? pg->wcfg.smem_bytes > pg->smem_optin
+                        : pg->cfg.smem_bytes > pg->smem_optin)
+        return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory");
     const HostProgram& hp = pg->hp;
     CUDA_TRY(upload(pg->d_ops, hp.ops));
     CUDA_TRY(upload(pg->d_targets, hp.targets));
@@ -288,14 +338,25 @@ static int ensure_device(pfs_program* pg, int device) {
     CUDA_TRY(upload(pg->d_pregen, hp.pregen_ops));
     CUDA_TRY(upload(pg->d_noise_off, hp.noise_off));
     CUDA_TRY(upload(pg->d_noise_ch, hp.noise_ch));
-    CUDA_TRY(set_frame_kernel_smem(pg->cfg));
-    int per_sm = pg->opts.ctas_per_sm;
-    if (per_sm <= 0) {
-        size_t per = pg->cfg.smem_bytes + 1024;
-        per_sm = (int)std::max<size_t>(1, (prop.sharedMemPerMultiprocessor) / per);
-        per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / pg->cfg.threads));
+    auto grid_of = [&](const LaunchCfg& c) {
+        int per_sm = pg->opts.ctas_per_sm;
+        if (per_sm <= 0) {
+            size_t per = c.smem_bytes + 1024;
+            per_sm = (int)std::max<size_t>(1, (prop.sharedMemPerMultiprocessor) / per);
+            per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / c.threads));
+        }
+        return pg->num_sms * per_sm;
+    };
+    if (pg->cfg.kernel && pg->cfg.smem_bytes <= pg->smem_optin) {
+        CUDA_TRY(set_frame_kernel_smem(pg->cfg));
+        pg->cfg.grid = grid_of(pg->cfg);
+    } else {
+        pg->cfg.kernel = 0;
     }
-    pg->cfg.grid = pg->num_sms * per_sm;
+    if (pg->wcfg.kernel) {
+        CUDA_TRY(set_frame_warp_kernel_smem(pg->wcfg));
+        pg->wcfg.grid = grid_of(pg->wcfg);
+    }
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
     for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
     pg->device = device;
@@ -349,9 +410,15 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
             pg->last_launches++;
         }
         LaunchCfg lc = cfg;
-        lc.grid = (int)std::min<int64_t>(cfg.grid, (ns + cfg.groups - 1) / cfg.groups);
         k2.groups = cfg.groups;
-        CUDA_TRY(launch_frame_kernel(lc, k2, st));
+        if (cfg.kernel == KERNEL_WARP) {
+            const int64_t nw = cfg.threads / 32;
+            lc.grid = (int)std::min<int64_t>(cfg.grid, (ns * W + nw - 1) / nw);
+            CUDA_TRY(launch_frame_warp_kernel(lc, k2, st));
+        } else {
+            lc.grid = (int)std::min<int64_t>(cfg.grid, (ns + cfg.groups - 1) / cfg.groups);
+            CUDA_TRY(launch_frame_kernel(lc, k2, st));
+        }
         pg->last_launches++;
     }
     return PFS_OK;
@@ -458,17 +525,21 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.num_cols = (int32_t)hp.num_cols;
     kp.do_dets = rows_meas ? 0 : 1;
     kp.debug_skip = pg->opts.debug_skip;
+    // frame kernel: warp-private when eligible (counts mode keeps the cooperative
+    // kernel's shared-memory counters when it has one)
+    const bool coop_counts = mode == PFS_MODE_COUNTS && pg->cfg.kernel && pg->opts.kernel != KERNEL_WARP;
+    LaunchCfg cfg = (!pg->wcfg.kernel || coop_counts) ? pg->cfg : pg->wcfg;
+    const bool warpk = cfg.kernel == KERNEL_WARP;
     kp.stage = (pg->opts.debug_skip & 1024) ? 0 : 1;  // bit 10: profiling ablation, no staging
-    kp.desc_in_smem = desc_fits(hp) ? 1 : 0;
-    CUDA_TRY(pg->d_nscratch.reserve((size_t)pg->cfg.grid * pg->cfg.threads * NZ_MAX_LIST));
+    kp.desc_in_smem = warpk ? pg->warp_desc_smem : (desc_fits(hp) ? 1 : 0);
+    CUDA_TRY(pg->d_nscratch.reserve((size_t)cfg.grid * cfg.threads * NZ_MAX_LIST));
     kp.noise_scratch = pg->d_nscratch.p;
     if (pg->opts.debug_skip & 64) {  // op-boundary clock trace of the first tile
         CUDA_TRY(pg->d_clock.reserve(hp.ops.size() * 9 + 1));
         kp.op_clock = pg->d_clock.p;
     }
 
-    LaunchCfg cfg = pg->cfg;
-    if (!cfg.ring_smem) {
+    if (!warpk && !cfg.ring_smem) {
         CUDA_TRY(pg->d_ring.reserve((size_t)std::max<int64_t>(hp.num_slots, 1) * W * cfg.grid * cfg.groups));
         kp.ring_global = pg->d_ring.p;
     }
@@ -480,7 +551,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (hp.num_cols > 0) CUDA_TRY(cudaMemsetAsync(cptr, 0, hp.num_cols * 8, st));
         kp.counts = cptr;
         const size_t extra = (size_t)hp.num_cols * 4;
-        kp.counts_in_smem = (cfg.smem_bytes + extra <= pg->smem_optin) ? 1 : 0;
+        kp.counts_in_smem = (!warpk && cfg.smem_bytes + extra <= pg->smem_optin) ? 1 : 0;
         if (kp.counts_in_smem) {
             cfg.smem_bytes += extra;
             CUDA_TRY(set_frame_kernel_smem(cfg));
@@ -528,7 +599,9 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     const int nbuf = dev_out ? 1 : std::min(2, n_chunks);
     const int64_t chunk_words = chunk_tiles * W;
     for (int b = 0; b < nbuf; b++) {
-        if (!direct_rows) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * chunk_words));
+        // (+ padding to whole 8-word groups: the word-major transpose reads
+        // narrow tiles in groups of 8 words)
+        if (!direct_rows) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * ((chunk_words + 7) & ~7ll)));
         if (b8 && !dev_out) CUDA_TRY(pg->d_b8[b].reserve((size_t)chunk_tiles * T * dev_pitch));
     }
     if (timing) CUDA_TRY(cudaEventRecord(pg->ev[1], st));
@@ -542,7 +615,9 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (!dev_out && ci >= 2) CUDA_TRY(cudaStreamWaitEvent(st, pg->ev[6 + b], 0));  // buffer free
         uint32_t* rows = direct_rows ? (uint32_t*)out : pg->d_rows[b].p;
         const int64_t row_words = direct_rows ? used_words : chunk_words;
-        kp.out_row_stride = b8 ? W : row_words;         // b8: tile-major scratch
+        // b8: tile-major scratch ([tile][row][W]; warp kernel [tile][W][row])
+        kp.out_row_stride = b8 ? (warpk ? 1 : W) : row_words;
+        kp.out_word_stride = (b8 && warpk) ? R : 1;
         kp.out_tile_stride = b8 ? R * W : W;
         kp.rec_out = rows_meas ? rows : nullptr;
         kp.ev_out = rows_meas ? nullptr : rows;
@@ -555,6 +630,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             CUDA_TRY(pg->d_rows[0].reserve((size_t)std::max<int64_t>(R, 1) * chunk_words));
             rows = pg->d_rows[0].p;
             kp.out_row_stride = chunk_words;
+            kp.out_word_stride = 1;
             kp.out_tile_stride = W;
             kp.rec_out = rows_meas ? rows : nullptr;
             kp.ev_out = rows_meas ? nullptr : rows;
@@ -568,8 +644,12 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (b8) {
             uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
             const int64_t pitch = dev_out ? out_pitch : dev_pitch;
-            CUDA_TRY(launch_tiles_to_b8(rows, R, W, nt, nshots,
-                                        mode == PFS_MODE_SAMPLES ? d_ref : nullptr, dst, pitch, st));
+            // word-major tiles narrower than 8 words are contiguous word columns:
+            // transpose them as 8-word tiles (256-shot blocks per CTA)
+            const int tw = (warpk && W < 8) ? 8 : W;
+            const int64_t ntw = (nt * W + tw - 1) / tw;
+            CUDA_TRY(launch_tiles_to_b8(rows, R, tw, ntw, nshots,
+                                        mode == PFS_MODE_SAMPLES ? d_ref : nullptr, dst, pitch, st, warpk));
             pg->last_launches++;
             if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
         } else if (direct_rows && rows != (uint32_t*)out) {

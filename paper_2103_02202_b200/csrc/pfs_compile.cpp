@@ -20,6 +20,7 @@
 #include <cmath>
 #include <stdexcept>
 #include <string>
+#include <unordered_map>
 
 #include "pfs_internal.h"
 
@@ -383,6 +384,45 @@ void reorder_for_banks(HostProgram& hp, int W) {
     }
 }
 
+// Operand blocks repeat across the rounds of a REPEAT body (same qubits, and
+// with LIFO slot reuse usually the same record slots): point every op at the
+// first identical block, so the operand stream a kernel walks (and keeps in
+// L1) is one round long.  Blocks stay in place; only offsets move.
+void dedup_operands(HostProgram& hp) {
+    auto fnv = [](const uint32_t* p, size_t n) {
+        uint64_t h = 1469598103934665603ull ^ n;
+        for (size_t i = 0; i < n; i++) { h ^= p[i]; h *= 1099511628211ull; }
+        return h;
+    };
+    std::unordered_map<uint64_t, std::vector<uint32_t>> seen_t, seen_d;
+    auto canon = [&](std::unordered_map<uint64_t, std::vector<uint32_t>>& seen,
+                     const std::vector<uint32_t>& arr, uint32_t off, size_t n) -> uint32_t {
+        if (n == 0) return off;
+        const uint64_t h = fnv(arr.data() + off, n);
+        auto& lst = seen[h];
+        for (uint32_t o : lst)
+            if (std::equal(arr.begin() + o, arr.begin() + o + n, arr.begin() + off)) return o;
+        lst.push_back(off);
+        return off;
+    };
+    for (DOp& o : hp.ops) {
+        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
+        switch (kind) {
+            case K_GATE: o.off = canon(seen_t, hp.targets, o.off, (size_t)o.count * rule_arity(code)); break;
+            case K_M: case K_MR: o.off = canon(seen_t, hp.targets, o.off, 2 * (size_t)o.count); break;
+            case K_R: case K_OBS: o.off = canon(seen_t, hp.targets, o.off, o.count); break;
+            case K_NOISE:
+                o.off = canon(seen_t, hp.targets, o.off, (size_t)o.count * (code == CH_DEP2 ? 2 : 1));
+                hp.noise_off[o.b] = o.off;
+                break;
+            case K_DET:
+                if (code) o.off = canon(seen_d, hp.det_terms, o.off, (size_t)o.count * code);
+                break;
+            default: break;
+        }
+    }
+}
+
 // Binomial(n, p) inverse-CDF thresholds in 64-bit fixed point:
 // X = min{m : u < t[m]} for u uniform on [0, 2^64), X = len(t) if u >= every
 // entry.  Upper-tail thresholds are built from the tail sum so their absolute
@@ -456,7 +496,9 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
         const double E = (double)N * p;
         if (p < 0.25 && E <= 16384.0 && N < (1ull << 28)) {
             np.flags |= NZ_PREGEN;
-            np.cap = (uint32_t)std::ceil(E + 8.0 * std::sqrt(E) + 16.0);
+            // overflow (Poisson tail beyond ~6 sigma + 10, < 1e-9 per list) falls
+            // back to inline sampling, so the slack only trades memory for speed
+            np.cap = (uint32_t)std::ceil(E + 6.0 * std::sqrt(E) + 10.0);
             np.cap_base = (uint32_t)hp.hit_capacity;
             hp.hit_capacity += np.cap;
             // pre-pass work items are 32-chunk blocks (one warp each)
@@ -477,6 +519,8 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
         o.kcf &= ~(F_PREGEN << 16);
         if (np.flags & NZ_PREGEN) o.kcf |= F_PREGEN << 16;
         o.c = np.cap_base;
+        o.d = next_of[o.b];
+        o.e = o.d != NO_SLOT ? hp.noise[o.d].cap_base : 0u;
     }
 }
 
@@ -495,9 +539,10 @@ void assign_staging(HostProgram& hp) {
             case K_DET: if (code) { words = (uint64_t)o.count * code; arr = 1; } break;
             default: break;
         }
+        if (kind == K_NOISE) continue;  // d/e: next noise op (build_noise_schedule)
         o.d = 0;
         o.e = 0;
-        if (kind == K_NOISE || words == 0) continue;
+        if (words == 0) continue;
         const uint64_t lo = o.off & ~3u;
         const uint64_t bytes = ((o.off + words - lo) * 4 + 15) & ~15ull;
         if (bytes > (uint64_t)STAGE_BYTES) continue;

@@ -7,7 +7,7 @@
 #include <string>
 #include <vector>
 
-#include "../../include/pfs.h"
+#include "pfs.h"
 
 namespace pfs {
 
@@ -33,6 +33,8 @@ constexpr int NZ_MAX_LIST = 8;
 // frame kernel CTA size cap (launch bounds): 768 threads leaves 85 registers per
 // thread, enough for the noise sampler without spills
 constexpr int FRAME_MAX_THREADS = 768;
+constexpr int WARP_KERNEL_MAX_THREADS = 1024;
+constexpr int KERNEL_COOP = 1, KERNEL_WARP = 2;  // frame_warp_kernel: one word column per warp
 // per-group TMA staging buffer (x2, double-buffered) for an op's operand block
 constexpr int STAGE_BYTES = 8192;
 // op descriptors are copied to shared memory when they take at most this much
@@ -43,7 +45,8 @@ constexpr int DESC_SMEM_MAX = 16384;      // distinct-position list; larger coun
 //   M/MR : count = targets, off -> (qubit, slot) pairs, a = rec_base, b = coin_base
 //   R    : count = targets, off -> qubits, b = coin_base
 //   NOISE: count = apps, off -> targets, a = noise_row_base, b = noise ordinal,
-//          c = hit-list base
+//          c = hit-list base, d/e = ordinal/hit-list base of the next
+//          pre-generated noise op (NO_SLOT: none), for prefetching its hits
 //   all but NOISE: d/e = TMA staging block of the op's operands (assign_staging)
 //   DET  : count = columns, a = first column (terms via det_ptr/det_terms)
 //   OBS  : count = terms, off -> record slots, a = accumulator slot
@@ -119,6 +122,7 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
 
 void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits);
 void reorder_for_banks(HostProgram& hp, int W);
+void dedup_operands(HostProgram& hp);
 void assign_staging(HostProgram& hp);
 
 // Kernel launch plumbing (pfs_kernels.cu)
@@ -145,6 +149,7 @@ struct KParams {
     int64_t inject_words;
     int64_t out_row_stride;      // output word address = row * out_row_stride
     int64_t out_tile_stride;     //                     + tile * out_tile_stride + word
+    int64_t out_word_stride;     // frame_warp_kernel: word w adds w * out_word_stride
     int64_t n_tiles;
     int64_t num_shots;           // shots of this launch (for tail masking)
     int64_t hit_capacity;
@@ -169,6 +174,7 @@ struct KParams {
 };
 
 struct LaunchCfg {
+    int kernel;  // KERNEL_COOP (frame_kernel) or KERNEL_WARP (frame_warp_kernel)
     int W;
     int groups;
     bool ring_smem;
@@ -181,6 +187,9 @@ size_t frame_smem_bytes(int num_qubits, int W);
 cudaError_t launch_frame_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStream_t stream);
 cudaError_t launch_noise_kernel(int W, const KParams& kp, int64_t n_tiles, cudaStream_t stream);
 cudaError_t set_frame_kernel_smem(const LaunchCfg& cfg);
+cudaError_t launch_frame_warp_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStream_t stream);
+cudaError_t set_frame_warp_kernel_smem(const LaunchCfg& cfg);
+size_t warp_kernel_smem_per_warp(int num_qubits, int64_t num_slots, int64_t num_noise);
 cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t row_words,
                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
                               int64_t pitch, cudaStream_t stream);
@@ -189,9 +198,10 @@ cudaError_t launch_detector_events(const uint8_t* flips, int64_t in_pitch, int64
                                    int64_t num_results, const int64_t* ptr, const int64_t* idx,
                                    int64_t num_dets, uint32_t* rows, uint32_t* ev, uint8_t* out,
                                    int64_t out_pitch, cudaStream_t st);
-// tile-major [tile][row][W] bit tables -> shot-major b8 rows of `pitch` bytes
+// tile-major [tile][row][W] (word_major: [tile][W][row]) bit tables -> shot-major
+// b8 rows of `pitch` bytes
 cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, int64_t n_tiles,
                                int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
-                               int64_t pitch, cudaStream_t stream);
+                               int64_t pitch, cudaStream_t stream, bool word_major = false);
 
 }  // namespace pfs

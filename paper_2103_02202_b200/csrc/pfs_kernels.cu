@@ -83,23 +83,52 @@ template <> __device__ __forceinline__ VW<2> vldg<2>(const uint32_t* p) {
 }
 template <> __device__ __forceinline__ VW<1> vldg<1>(const uint32_t* p) { return VW<1>{{__ldg(p)}}; }
 
-// coin words c*V .. c*V+V-1 of coin row e for global tile g
-template <int W, int V>
-__device__ __forceinline__ VW<V> coin_words(const KParams& kp, uint32_t e, int c, uint32_t g,
-                                            int64_t tile) {
-    if (kp.coins != nullptr)
-        return vldg<V>(kp.coins + (int64_t)e * kp.inject_words + tile * W + c * V);
-#if PFS_PROFILE
-    if (kp.debug_skip & 4) return vzero<V>();
-#endif
-    const int word = c * V;
-    uint32_t c0 = e, c1 = (uint32_t)(word >> 2), c2 = g, c3 = DOMAIN_COIN;
-    philox4x32_10(c0, c1, c2, c3, (uint32_t)kp.seed, (uint32_t)(kp.seed >> 32));
-    const uint32_t o[4] = {c0, c1, c2, c3};
-    VW<V> r;
+// Coin rows come in windows of 128: coin row e of word w of
+// global tile g is word (e >> 5) & 3 of Philox(((e >> 7) << 5) | (e & 31), w, g,
+// DOMAIN_COIN), so one block serves rows e0, e0+32, e0+64, e0+96 of one word
+// (e0 = "coin group" k: ((k >> 5) << 7) | (k & 31)).  coin_group fills o[r] with
+// the word of row e0 + 32 r (injected mode: loaded, rows outside [lo, hi) skipped).
+__device__ __forceinline__ uint32_t coin_row0(uint32_t k) { return ((k >> 5) << 7) | (k & 31u); }
+
+template <int W>
+__device__ __forceinline__ void coin_group(const KParams& kp, uint32_t k, uint32_t w, uint32_t g,
+                                           int64_t tile, uint32_t lo, uint32_t hi, uint32_t o[4]) {
+    if (kp.coins != nullptr) {
+        const uint32_t e0 = coin_row0(k);
 #pragma unroll
-    for (int j = 0; j < V; j++) r.w[j] = o[(word & 3) + j];
-    return r;
+        for (int r = 0; r < 4; r++) {
+            const uint32_t e = e0 + 32u * r;
+            o[r] = (e >= lo && e < hi) ? __ldg(kp.coins + (int64_t)e * kp.inject_words + tile * W + w) : 0u;
+        }
+        return;
+    }
+#if PFS_PROFILE
+    if (kp.debug_skip & 4) { o[0] = o[1] = o[2] = o[3] = 0u; return; }
+#endif
+    uint32_t c0 = k, c1 = w, c2 = g, c3 = DOMAIN_COIN;
+    philox4x32_10(c0, c1, c2, c3, (uint32_t)kp.seed, (uint32_t)(kp.seed >> 32));
+    o[0] = c0; o[1] = c1; o[2] = c2; o[3] = c3;
+}
+
+// coin groups covering coin rows [lo, hi): k in [k0, k1), k0 a multiple of 32
+__device__ __forceinline__ uint32_t coin_k0(uint32_t lo) { return (lo >> 7) << 5; }
+__device__ __forceinline__ uint32_t coin_k1(uint32_t hi) { return ((hi + 127u) >> 7) << 5; }
+__device__ __forceinline__ bool coin_group_live(uint32_t k, uint32_t lo, uint32_t hi) {
+    const uint32_t e0 = coin_row0(k);
+    return e0 + 96u >= lo && e0 < hi;
+}
+
+// words c*V .. c*V+V-1 of the four rows of coin group k (V Philox blocks)
+template <int W, int V>
+__device__ __forceinline__ void coin_group_vec(const KParams& kp, uint32_t k, int c, uint32_t g, int64_t tile,
+                                               uint32_t lo, uint32_t hi, VW<V> o[4]) {
+#pragma unroll
+    for (int j = 0; j < V; j++) {
+        uint32_t b[4];
+        coin_group<W>(kp, k, (uint32_t)(c * V + j), g, tile, lo, hi, b);
+#pragma unroll
+        for (int r = 0; r < 4; r++) o[r].w[j] = b[r];
+    }
 }
 
 __device__ __forceinline__ void pattern_of(uint32_t ch, uint32_t pick, uint32_t& xm, uint32_t& zm) {
@@ -427,8 +456,11 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
 // lists and per-op hit counts to global memory (L2-resident for a chunk).
 // grid = (ceil(items / (8 * NZ_ITEMS_PER_WARP)), tiles), 256 threads.
 constexpr int NZ_ITEMS_PER_WARP = 4;
+#ifndef NZ_MIN_BLOCKS
+#define NZ_MIN_BLOCKS 5
+#endif
 template <int W>
-__global__ void __launch_bounds__(256) noise_kernel(const __grid_constant__ KParams kp) {
+__global__ void __launch_bounds__(256, NZ_MIN_BLOCKS) noise_kernel(const __grid_constant__ KParams kp) {
     __shared__ uint32_t wscr_all[8][256 + 32 * NZ_MAX_LIST];
     const int warp = threadIdx.x >> 5;
     const int64_t tile = blockIdx.y;
@@ -590,7 +622,21 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             for (int i = tid; i < (n << LC); i += nth) {
                 const int q = i >> LC, c = i & (C - 1);
                 vst<V>(X + (size_t)q * W + c * V, vzero<V>());
-                vst<V>(Z + (size_t)q * W + c * V, coin_words<W, V>(kp, (uint32_t)q, c, g, tile));
+            }
+            {  // z = coin rows 0..n-1: items = (coin group, V-word chunk)
+                const int items = (int)coin_k1((uint32_t)n) << LC;
+                for (int i = tid; i < items; i += nth) {
+                    const uint32_t k = (uint32_t)(i >> LC);
+                    const int c = i & (C - 1);
+                    if (!coin_group_live(k, 0u, (uint32_t)n)) continue;
+                    VW<V> o[4];
+                    coin_group_vec<W, V>(kp, k, c, g, tile, 0u, (uint32_t)n, o);
+#pragma unroll
+                    for (int r = 0; r < 4; r++) {
+                        const uint32_t e = coin_row0(k) + 32u * r;
+                        if (e < (uint32_t)n) vst<V>(Z + (size_t)e * W + c * V, o[r]);
+                    }
+                }
             }
             for (int i = tid; i < (kp.num_obs << LC); i += nth) {
                 const int k = i >> LC, c = i & (C - 1);
@@ -709,36 +755,53 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     }
                     break;
                 }
-                case K_M: case K_MR: {
-                    const int items = (int)(count << LC);
-                    batched_items<2>(tid, nth, items,
-                        [&](int i) { return reinterpret_cast<const uint2*>(tg)[i >> LC]; },
-                        [&](int i, uint2 qs) {
-                            const int j = i >> LC, c = i & (C - 1);
-                            const size_t p = (size_t)qs.x * W + c * V;
+                case K_M: case K_MR: case K_R: {
+                    // items = (coin group, V-word chunk): V Philox blocks, up to four rows
+                    const uint32_t lo = ob, hi = ob + (kind == K_MR ? 2u : 1u) * count;
+                    const uint32_t k0 = coin_k0(lo);
+                    const int items = (int)(coin_k1(hi) - k0) << LC;
+                    for (int i = tid; i < items; i += nth) {
+                        const uint32_t k = k0 + (uint32_t)(i >> LC);
+                        const int c = i & (C - 1);
+                        if (!coin_group_live(k, lo, hi)) continue;
+                        uint2 qsv[4];  // operands load while the coin blocks compute
+#pragma unroll
+                        for (int r = 0; r < 4; r++) {
+                            const uint32_t e = coin_row0(k) + 32u * r;
+                            qsv[r] = make_uint2(0u, NO_SLOT);
+                            if (e < lo || e >= hi) continue;
+                            const uint32_t rel = e - lo;
+                            if (kind == K_R) qsv[r].x = tg[rel];
+                            else if (kind == K_M || (rel & 1u))
+                                qsv[r] = reinterpret_cast<const uint2*>(tg)[kind == K_MR ? rel >> 1 : rel];
+                        }
+                        VW<V> o[4];
+                        coin_group_vec<W, V>(kp, k, c, g, tile, lo, hi, o);
+#pragma unroll
+                        for (int r = 0; r < 4; r++) {
+                            const uint32_t e = coin_row0(k) + 32u * r;
+                            if (e < lo || e >= hi) continue;
+                            const uint32_t rel = e - lo;
+                            const size_t p = (size_t)qsv[r].x * W + c * V;
+                            if (kind == K_R) {
+                                vst<V>(X + p, vzero<V>());
+                                vst<V>(Z + p, o[r]);
+                                continue;
+                            }
+                            if (kind == K_MR && !(rel & 1u)) continue;  // the measure's coin row is overwritten
+                            const uint32_t j = kind == K_MR ? rel >> 1 : rel;
                             const VW<V> xv = vld<V>(X + p);
-                            if (kp.do_dets && qs.y != NO_SLOT) vst<V>(ring + (size_t)qs.y * W + c * V, xv);
+                            if (kp.do_dets && qsv[r].y != NO_SLOT) vst<V>(ring + (size_t)qsv[r].y * W + c * V, xv);
                             if (kp.rec_out != nullptr)
-                                vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_row_stride +
-                                           tile * kp.out_tile_stride + c * V, xv);
+                                vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, xv);
                             if (kind == K_M) {
-                                vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_words<W, V>(kp, ob + j, c, g, tile)));
+                                vst<V>(Z + p, vxor<V>(vld<V>(Z + p), o[r]));
                             } else {
                                 vst<V>(X + p, vzero<V>());
-                                vst<V>(Z + p, coin_words<W, V>(kp, ob + 2 * j + 1, c, g, tile));
+                                vst<V>(Z + p, o[r]);
                             }
-                        });
-                    break;
-                }
-                case K_R: {
-                    const int items = (int)(count << LC);
-                    batched_items<4>(tid, nth, items, [&](int i) { return tg[i >> LC]; },
-                        [&](int i, uint32_t q) {
-                            const int j = i >> LC, c = i & (C - 1);
-                            const size_t p = (size_t)q * W + c * V;
-                            vst<V>(X + p, vzero<V>());
-                            vst<V>(Z + p, coin_words<W, V>(kp, ob + j, c, g, tile));
-                        });
+                        }
+                    }
                     break;
                 }
                 case K_NOISE: {
@@ -865,6 +928,351 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
         for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x)
             if (cnt[i]) atomicAdd(kp.counts + i, (unsigned long long)cnt[i]);
     }
+}
+
+// ------------------------------------------------------- warp-private kernel
+// Each warp owns one 32-shot word column (word w of tile t) for the whole
+// circuit: its frame is x/z interleaved per qubit (uint2 XZ[q], 8 bytes) plus
+// its record ring, all in shared memory.  Lanes take the applications of an op
+// (at most one per qubit, so lanes never collide) and warps never wait for
+// each other: no CTA barriers, only __syncwarp between ops.  The CTA's warps
+// run the same op stream on different words, so operand loads (targets,
+// detector terms, hit lists) hit L1 for all but the leading warp.
+template <int W>
+__device__ __forceinline__ void warp_apply_entry(uint32_t* xz, uint64_t e, uint32_t w) {
+    if (((uint32_t)(e >> 40) & 31u) != w) return;
+    const uint32_t q0 = (uint32_t)e & 0xFFFFFu, q1 = (uint32_t)(e >> 20) & 0xFFFFFu;
+    const uint32_t bit = 1u << ((uint32_t)(e >> 45) & 31u);
+    const uint32_t xm = (uint32_t)(e >> 50) & 3u, zm = (uint32_t)(e >> 52) & 3u;
+    if (xm & 1u) atomicXor(xz + 2 * q0, bit);
+    if (zm & 1u) atomicXor(xz + 2 * q0 + 1, bit);
+    if (xm & 2u) atomicXor(xz + 2 * q1, bit);
+    if (zm & 2u) atomicXor(xz + 2 * q1 + 1, bit);
+}
+
+template <int W>
+__global__ void __launch_bounds__(WARP_KERNEL_MAX_THREADS, 1) frame_warp_kernel(const __grid_constant__ KParams kp) {
+    constexpr uint32_t T = 32 * W;
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int n = kp.num_qubits;
+    const size_t dwords = kp.desc_in_smem ? (size_t)kp.n_ops * 8 : 0;
+    const size_t per_warp = ((size_t)2 * n + kp.num_slots + kp.num_noise + 1) & ~(size_t)1;
+    uint32_t* const xz = smem + dwords + (size_t)warp * per_warp;  // x = xz[2q], z = xz[2q+1]
+    uint2* const XZ = reinterpret_cast<uint2*>(xz);
+    uint32_t* const ring = xz + 2 * n;
+    uint32_t* const ncnt = ring + kp.num_slots;
+    const uint4* const dsc = kp.desc_in_smem ? reinterpret_cast<const uint4*>(smem)
+                                             : reinterpret_cast<const uint4*>(kp.ops);
+    uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
+    const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
+    if (kp.desc_in_smem) {
+        uint4* d = reinterpret_cast<uint4*>(smem);
+        for (int i = threadIdx.x; i < 2 * kp.n_ops; i += blockDim.x)
+            d[i] = __ldg(reinterpret_cast<const uint4*>(kp.ops) + i);
+        __syncthreads();
+    }
+    const int64_t units = kp.n_tiles * W;
+    for (int64_t u = (int64_t)blockIdx.x * NW + warp; u < units; u += (int64_t)gridDim.x * NW) {
+        const int64_t tile = u / W;
+        const uint32_t w = (uint32_t)(u % W);
+        if (tile * T + 32 * (int64_t)w >= kp.num_shots) continue;  // no live shot in this word
+        const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
+        const uint64_t* const hits = kp.hits_global + tile * kp.hit_capacity;
+        const int64_t obase = tile * kp.out_tile_stride + (int64_t)w * kp.out_word_stride;
+        // ---- FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39) ----
+        for (uint32_t k = (uint32_t)lane; k < coin_k1((uint32_t)n); k += 32) {
+            uint32_t o[4];
+            coin_group<W>(kp, k, w, g, tile, 0u, (uint32_t)n, o);
+#pragma unroll
+            for (int r = 0; r < 4; r++) {
+                const uint32_t e = coin_row0(k) + 32u * r;
+                if (e < (uint32_t)n) XZ[e] = make_uint2(0u, o[r]);
+            }
+        }
+        for (int i = lane; i < kp.num_obs; i += 32) ring[i] = 0u;
+        if (pregen)
+            for (int i = lane; i < kp.num_noise; i += 32) {
+                const uint32_t c = kp.ncnt_global[tile * kp.num_noise + i];
+                ncnt[i] = c <= __ldg(&kp.noise[i].cap) ? c : NO_SLOT;  // overflow -> inline resampling
+            }
+        __syncwarp();
+        // the next pre-generated noise op's first 32*NZ_PF hits ride in
+        // registers from the previous noise op on, so a noise op never waits
+        // for its hit list
+        constexpr int NZ_PF = 4;
+        uint64_t pf[NZ_PF];
+        auto prefetch_hits = [&](uint32_t ord, uint32_t base) {
+            uint32_t nh = ord != NO_SLOT && pregen ? ncnt[ord] : 0u;
+            if (nh == NO_SLOT) nh = 0u;
+#pragma unroll
+            for (int t = 0; t < NZ_PF; t++) {
+                const uint32_t i = (uint32_t)lane + 32u * t;
+                pf[t] = i < nh ? __ldg(hits + base + i) : 0ull;
+            }
+        };
+        prefetch_hits(kp.first_pregen, kp.first_cap_base);
+        for (int oi = 0; oi < kp.n_ops; oi++) {
+            const uint4 h0 = dsc[2 * oi], h1 = dsc[2 * oi + 1];
+            const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
+            const uint32_t count = h0.y, off = h0.z, oa = h0.w, ob = h1.x, oc = h1.y;
+            const uint32_t* const tg = kp.targets + off;
+#if PFS_PROFILE
+            if (kp.debug_skip) {
+                const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
+                                   : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
+                if (kp.debug_skip & bit) continue;
+            }
+            if (kp.op_clock != nullptr && blockIdx.x == 0 && warp == 0 && lane == 0 && u == 0)
+                kp.op_clock[oi] = clock64();
+#endif
+            switch (kind) {
+            case K_GATE: {
+                // U applications per lane in flight: all operand and frame loads
+                // before any store (an op's applications touch distinct qubits)
+                constexpr int U = 4;
+                if (code <= R_XXORZ) {
+                    for (uint32_t i0 = lane; i0 < count; i0 += 32 * U) {
+                        uint32_t q[U];
+                        uint2 v[U];
+#pragma unroll
+                        for (int t = 0; t < U; t++) {
+                            const uint32_t i = i0 + 32u * t;
+                            q[t] = i < count ? __ldg(tg + i) : 0u;
+                        }
+#pragma unroll
+                        for (int t = 0; t < U; t++)
+                            if (i0 + 32u * t < count) v[t] = XZ[q[t]];
+#pragma unroll
+                        for (int t = 0; t < U; t++) {
+                            if (i0 + 32u * t >= count) continue;
+                            uint2 a = v[t];
+                            if (code == R_SWAPXZ) a = make_uint2(a.y, a.x);
+                            else if (code == R_ZXORX) a.y ^= a.x;
+                            else a.x ^= a.y;
+                            XZ[q[t]] = a;
+                        }
+                    }
+                } else {
+                    const uint2* tg2 = reinterpret_cast<const uint2*>(tg);
+                    for (uint32_t i0 = lane; i0 < count; i0 += 32 * U) {
+                        uint2 qq[U], va[U], vb[U];
+#pragma unroll
+                        for (int t = 0; t < U; t++) {
+                            const uint32_t i = i0 + 32u * t;
+                            qq[t] = i < count ? __ldg(tg2 + i) : make_uint2(0u, 0u);
+                        }
+#pragma unroll
+                        for (int t = 0; t < U; t++)
+                            if (i0 + 32u * t < count) { va[t] = XZ[qq[t].x]; vb[t] = XZ[qq[t].y]; }
+#pragma unroll
+                        for (int t = 0; t < U; t++) {
+                            if (i0 + 32u * t >= count) continue;
+                            uint2 a = va[t], b = vb[t];
+                            switch (code) {
+                            case R_CX: b.x ^= a.x; a.y ^= b.y; break;
+                            case R_CZ: { const uint32_t az = a.y ^ b.x, bz = b.y ^ a.x; a.y = az; b.y = bz; break; }
+                            case R_CY: { const uint32_t az = a.y ^ b.x ^ b.y, bz = b.y ^ a.x;
+                                         b.x ^= a.x; a.y = az; b.y = bz; break; }
+                            default: { const uint2 t2 = a; a = b; b = t2; break; }  // SWAP
+                            }
+                            XZ[qq[t].x] = a;
+                            XZ[qq[t].y] = b;
+                        }
+                    }
+                }
+                break;
+            }
+            case K_M: case K_MR: case K_R: {
+                const uint32_t lo = ob, hi = ob + (kind == K_MR ? 2u : 1u) * count;
+                for (uint32_t k = coin_k0(lo) + lane; k < coin_k1(hi); k += 32) {
+                    if (!coin_group_live(k, lo, hi)) continue;
+                    // the four rows' operands load while the coin block computes
+                    uint2 qsv[4];
+#pragma unroll
+                    for (int r = 0; r < 4; r++) {
+                        const uint32_t e = coin_row0(k) + 32u * r;
+                        qsv[r] = make_uint2(0u, NO_SLOT);
+                        if (e < lo || e >= hi) continue;
+                        const uint32_t rel = e - lo;
+                        if (kind == K_R) qsv[r].x = __ldg(tg + rel);
+                        else if (kind == K_M || (rel & 1u))
+                            qsv[r] = __ldg(reinterpret_cast<const uint2*>(tg) + (kind == K_MR ? rel >> 1 : rel));
+                    }
+                    uint32_t o[4];
+                    coin_group<W>(kp, k, w, g, tile, lo, hi, o);
+#pragma unroll
+                    for (int r = 0; r < 4; r++) {
+                        const uint32_t e = coin_row0(k) + 32u * r;
+                        if (e < lo || e >= hi) continue;
+                        const uint32_t rel = e - lo;
+                        if (kind == K_R) { XZ[qsv[r].x] = make_uint2(0u, o[r]); continue; }
+                        if (kind == K_MR && !(rel & 1u)) continue;  // the measure's coin row is overwritten
+                        const uint32_t j = kind == K_MR ? rel >> 1 : rel;
+                        const uint2 qs = qsv[r];
+                        const uint32_t xv = xz[2 * qs.x];
+                        if (kp.do_dets && qs.y != NO_SLOT) ring[qs.y] = xv;
+                        if (kp.rec_out != nullptr) kp.rec_out[obase + (int64_t)(oa + j) * kp.out_row_stride] = xv;
+                        if (kind == K_M) xz[2 * qs.x + 1] ^= o[r];
+                        else XZ[qs.x] = make_uint2(0u, o[r]);
+                    }
+                }
+                break;
+            }
+            case K_NOISE: {
+                const int ar = code == CH_DEP2 ? 2 : 1;
+                if (kp.masks != nullptr) {
+                    // injected masks: per target, x row then z row
+                    for (uint32_t j = lane; j < count * ar; j += 32) {
+                        const uint32_t q = __ldg(tg + j);
+                        const uint32_t* mrow = kp.masks + (int64_t)(oa + 2 * j) * kp.inject_words + tile * W + w;
+                        const uint32_t mx = __ldg(mrow), mz = __ldg(mrow + kp.inject_words);
+                        if (flags & F_DUP) {
+                            if (mx) atomicXor(xz + 2 * q, mx);
+                            if (mz) atomicXor(xz + 2 * q + 1, mz);
+                        } else {
+                            uint2 v = XZ[q];
+                            v.x ^= mx; v.y ^= mz;
+                            XZ[q] = v;
+                        }
+                    }
+                    break;
+                }
+                if ((flags & F_PREGEN) && pregen) {
+                    const uint32_t nh = ncnt[ob];
+                    uint64_t cur[NZ_PF];
+#pragma unroll
+                    for (int t = 0; t < NZ_PF; t++) cur[t] = pf[t];
+                    prefetch_hits(h1.z, h1.w);  // the next noise op's hits
+                    if (nh != NO_SLOT) {
+#pragma unroll
+                        for (int t = 0; t < NZ_PF; t++) warp_apply_entry<W>(xz, cur[t], w);
+                        const uint64_t* hl = hits + oc;
+                        constexpr int U = 4;
+                        for (uint32_t i0 = lane + 32 * NZ_PF; i0 < nh; i0 += 32 * U) {
+                            uint64_t ent[U];
+#pragma unroll
+                            for (int t = 0; t < U; t++) {
+                                const uint32_t i = i0 + 32u * t;
+                                ent[t] = i < nh ? __ldg(hl + i) : 0ull;
+                            }
+#pragma unroll
+                            for (int t = 0; t < U; t++) warp_apply_entry<W>(xz, ent[t], w);
+                        }
+                        break;
+                    }
+                } else if (kp.debug_skip & 2) {
+                    break;
+                }
+                // inline sampling (large-p ops, hit-list overflow): this warp draws
+                // every chunk of the tile and keeps the hits in its word
+                const NoiseParam np = kp.noise[ob];
+                if (np.flags & NZ_NONE) break;
+                for (uint32_t r = lane; r < np.nchunks; r += 32)
+                    noise_chunk(kp, np, ob, r, g, sl, 1, [&](uint32_t trial, uint32_t pick) {
+                        const uint32_t app = trial / T, s = trial % T;
+                        if ((s >> 5) != w) return;
+                        uint32_t xm, zm;
+                        pattern_of(code, pick, xm, zm);
+                        const uint32_t bit = 1u << (s & 31);
+                        for (int a = 0; a < ar; a++) {
+                            const uint32_t q = __ldg(tg + app * ar + a);
+                            if ((xm >> a) & 1u) atomicXor(xz + 2 * q, bit);
+                            if ((zm >> a) & 1u) atomicXor(xz + 2 * q + 1, bit);
+                        }
+                    });
+                break;
+            }
+            case K_DET: {
+                if (!kp.do_dets) break;
+                auto det_word = [&](uint32_t col, uint32_t acc) {
+                    if (kp.ev_out != nullptr) kp.ev_out[obase + (int64_t)col * kp.out_row_stride] = acc;
+                    if (kp.counts != nullptr) {
+                        const int64_t rem = kp.num_shots - (tile * (int64_t)T + 32 * (int64_t)w);
+                        const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : ((1u << rem) - 1u);
+                        const uint32_t tot = __popc(acc & m);
+                        if (tot) atomicAdd(kp.counts + col, (unsigned long long)tot);
+                    }
+                };
+                if (code == 2) {  // the common two-term detector: 4 columns per lane in flight
+                    constexpr int U = 4;
+                    for (uint32_t i0 = lane; i0 < count; i0 += 32 * U) {
+                        uint32_t s0[U], s1[U];
+#pragma unroll
+                        for (int t = 0; t < U; t++) {
+                            const uint32_t i = i0 + 32u * t;
+                            s0[t] = i < count ? __ldg(kp.det_terms + off + 2 * i) : NO_SLOT;
+                            s1[t] = i < count ? __ldg(kp.det_terms + off + 2 * i + 1) : NO_SLOT;
+                        }
+#pragma unroll
+                        for (int t = 0; t < U; t++) {
+                            const uint32_t i = i0 + 32u * t;
+                            if (i >= count) continue;
+                            const uint32_t acc = (s0[t] != NO_SLOT ? ring[s0[t]] : 0u) ^
+                                                 (s1[t] != NO_SLOT ? ring[s1[t]] : 0u);
+                            det_word(oa + i, acc);
+                        }
+                    }
+                    break;
+                }
+                for (uint32_t i = lane; i < count; i += 32) {
+                    const uint32_t col = oa + i;
+                    uint32_t e0, e1;
+                    if (code) { e0 = off + i * code; e1 = e0 + code; }
+                    else { e0 = __ldg(kp.det_ptr + col); e1 = __ldg(kp.det_ptr + col + 1); }
+                    uint32_t acc = 0u;
+                    for (uint32_t e = e0; e < e1; e++) {
+                        const uint32_t sidx = __ldg(kp.det_terms + e);
+                        if (sidx != NO_SLOT) acc ^= ring[sidx];
+                    }
+                    det_word(col, acc);
+                }
+                break;
+            }
+            case K_OBS: {
+                if (!kp.do_dets) break;
+                uint32_t acc = 0u;
+                for (uint32_t j = lane; j < count; j += 32) {
+                    const uint32_t sidx = __ldg(tg + j);
+                    if (sidx != NO_SLOT) acc ^= ring[sidx];
+                }
+                acc = __reduce_xor_sync(0xFFFFFFFFu, acc);
+                if (lane == 0) ring[oa] ^= acc;
+                break;
+            }
+            default: break;
+            }
+            __syncwarp();
+        }
+    }
+}
+
+template <int W>
+static cudaError_t launch_w(const LaunchCfg& cfg, const KParams& kp, cudaStream_t st) {
+    frame_warp_kernel<W><<<cfg.grid, cfg.threads, cfg.smem_bytes, st>>>(kp);
+    return cudaGetLastError();
+}
+template <int W>
+static cudaError_t smem_w(const LaunchCfg& cfg) {
+    return cudaFuncSetAttribute(frame_warp_kernel<W>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)cfg.smem_bytes);
+}
+#define PFS_DISPATCH_W(FN, ...)                          \
+    switch (cfg.W) {                                     \
+        case 1: return FN<1>(__VA_ARGS__);               \
+        case 2: return FN<2>(__VA_ARGS__);               \
+        case 4: return FN<4>(__VA_ARGS__);               \
+        case 8: return FN<8>(__VA_ARGS__);               \
+        case 16: return FN<16>(__VA_ARGS__);             \
+        case 32: return FN<32>(__VA_ARGS__);             \
+        default: return cudaErrorInvalidValue;           \
+    }
+cudaError_t launch_frame_warp_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStream_t stream) {
+    PFS_DISPATCH_W(launch_w, cfg, kp, stream)
+}
+cudaError_t set_frame_warp_kernel_smem(const LaunchCfg& cfg) { PFS_DISPATCH_W(smem_w, cfg) }
+size_t warp_kernel_smem_per_warp(int num_qubits, int64_t num_slots, int64_t num_noise) {
+    return (((size_t)2 * num_qubits + num_slots + num_noise + 1) & ~(size_t)1) * 4;
 }
 
 size_t frame_smem_bytes(int num_qubits, int W) { return (size_t)2 * num_qubits * W * 4; }
@@ -1004,7 +1412,7 @@ __global__ void __launch_bounds__(256) rows_to_b8_kernel(const uint32_t* __restr
 // 256 W words, so loads are fully coalesced; each shot's 32 output bytes are
 // one aligned sector when the pitch allows.
 // TW = tile words, W = words handled per CTA (TW > 16 splits a tile in parts)
-template <int TW, int W>
+template <int TW, int W, bool WM>
 __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __restrict__ tiles,
                                                           int64_t num_rows, int64_t num_shots,
                                                           const uint8_t* __restrict__ xor_bits,
@@ -1014,18 +1422,27 @@ __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __rest
     __shared__ uint32_t tin[256 * Wp];
     __shared__ uint32_t tout[32 * W * 9];
     const int t = threadIdx.x;
-    const int64_t tile = blockIdx.x / PARTS;
-    const int part = (int)(blockIdx.x % PARTS);
-    const int64_t r0 = (int64_t)blockIdx.y * 256;
+    // row block fastest: the CTAs writing one shot's consecutive 32-byte runs
+    // run together, so their sectors merge into whole lines in L2
+    const int64_t nrb = (num_rows + 255) >> 8;
+    const int64_t rest = (int64_t)blockIdx.x / nrb;
+    const int64_t tile = rest / PARTS;
+    const int part = (int)(rest % PARTS);
+    const int64_t r0 = ((int64_t)blockIdx.x % nrb) * 256;
     const int rows = (int)((num_rows - r0) < 256 ? (num_rows - r0) : 256);
-    const uint32_t* src = tiles + tile * num_rows * TW + r0 * TW + part * W;
+    const uint32_t* src = WM ? tiles + tile * num_rows * TW + (int64_t)part * W * num_rows + r0
+                             : tiles + tile * num_rows * TW + r0 * TW + part * W;
     // thread t owns row t of the block: its W words are contiguous (16-byte
-    // vector loads when W >= 4), all issued before use
+    // vector loads when W >= 4), all issued before use; word-major input: one
+    // coalesced 1 KB run per word
     const int r = t;
     uint32_t v[W];
     if (r < rows) {
         const uint32_t* rp = src + (size_t)r * TW;
-        if constexpr (W >= 4) {
+        if constexpr (WM) {
+#pragma unroll
+            for (int k = 0; k < W; k++) v[k] = __ldg(src + (int64_t)k * num_rows + r);
+        } else if constexpr (W >= 4) {
 #pragma unroll
             for (int k = 0; k < W / 4; k++) {
                 const uint4 q = __ldg(reinterpret_cast<const uint4*>(rp) + k);
@@ -1078,23 +1495,31 @@ __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __rest
     }
 }
 
-cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, int64_t n_tiles,
-                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
-                               int64_t pitch, cudaStream_t stream) {
+template <bool WM>
+static cudaError_t tiles_to_b8_t(const uint32_t* tiles, int64_t num_rows, int W, int64_t n_tiles,
+                                 int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
+                                 int64_t pitch, cudaStream_t stream) {
     if (num_rows <= 0 || num_shots <= 0 || n_tiles <= 0) return cudaSuccess;
-    const unsigned parts = W > 16 ? (unsigned)(W / 16) : 1u;
-    dim3 grid((unsigned)n_tiles * parts, (unsigned)((num_rows + 255) / 256));
-    if (grid.y > 65535u) return cudaErrorInvalidConfiguration;
+    const int64_t parts = W > 16 ? W / 16 : 1;
+    const int64_t nblk = n_tiles * parts * ((num_rows + 255) / 256);
+    if (nblk > 0x7FFFFFFFll) return cudaErrorInvalidConfiguration;
+    const dim3 grid((unsigned)nblk);
     switch (W) {
-        case 1: tiles_to_b8_kernel<1, 1><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
-        case 2: tiles_to_b8_kernel<2, 2><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
-        case 4: tiles_to_b8_kernel<4, 4><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
-        case 8: tiles_to_b8_kernel<8, 8><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
-        case 16: tiles_to_b8_kernel<16, 16><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
-        case 32: tiles_to_b8_kernel<32, 16><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 1: tiles_to_b8_kernel<1, 1, WM><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 2: tiles_to_b8_kernel<2, 2, WM><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 4: tiles_to_b8_kernel<4, 4, WM><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 8: tiles_to_b8_kernel<8, 8, WM><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 16: tiles_to_b8_kernel<16, 16, WM><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
+        case 32: tiles_to_b8_kernel<32, 16, WM><<<grid, 256, 0, stream>>>(tiles, num_rows, num_shots, xor_bits, out, pitch); break;
         default: return cudaErrorInvalidValue;
     }
     return cudaGetLastError();
+}
+cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, int64_t n_tiles,
+                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
+                               int64_t pitch, cudaStream_t stream, bool word_major) {
+    return word_major ? tiles_to_b8_t<true>(tiles, num_rows, W, n_tiles, num_shots, xor_bits, out, pitch, stream)
+                      : tiles_to_b8_t<false>(tiles, num_rows, W, n_tiles, num_shots, xor_bits, out, pitch, stream);
 }
 
 // ------------------------------------------------------------ detector_events

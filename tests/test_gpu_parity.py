@@ -27,20 +27,27 @@ def need_gpu():
     build()
 
 
-# (words_per_tile, ring_in_smem, groups) layouts exercising every kernel
-# instantiation, one and two tiles in flight per CTA
-LAYOUTS = [(0, -1, 0), (1, 0, 1), (2, 1, 2), (4, 0, 0), (8, 1, 1), (16, 0, 2), (32, 1, 0),
-           (16, 0, 1)]
+# (words_per_tile, ring_in_smem, groups, kernel) layouts exercising every
+# kernel instantiation: cooperative (kernel 1; one and two tiles in flight per
+# CTA) and warp-private (kernel 2; one word column per warp), 0 = auto
+LAYOUTS = [(0, -1, 0, 0), (1, 0, 1, 1), (2, 1, 2, 1), (4, 0, 0, 1), (8, 1, 1, 1), (16, 0, 2, 1),
+           (32, 1, 0, 1), (16, 0, 1, 1), (1, -1, 0, 2), (2, -1, 0, 2), (4, -1, 0, 2),
+           (16, -1, 0, 2), (32, -1, 0, 2)]
 
 
-def _fits(text, W, ring, groups=0):
+def _opts(layout):
+    W, ring, groups, kernel = layout
+    return dict(words_per_tile=W, ring_in_smem=ring, groups=groups, kernel=kernel)
+
+
+def _fits(text, layout):
     from paper_2103_02202_b200._native import NativeProgram
     from paper_2103_02202_b200.program import flatten
     try:
-        NativeProgram(flatten(text), words_per_tile=W, ring_in_smem=ring, groups=groups)
-        return True
+        p = NativeProgram(flatten(text), **_opts(layout))
     except ValueError:
         return False
+    return layout[3] == 0 or p.info["kernel"] == layout[3]
 
 
 @pytest.mark.parametrize("name", inject_cases())
@@ -49,13 +56,12 @@ def test_injected_bit_exact_vs_reference(name, layout):
     from paper_2103_02202_b200.sampler import compile_detector_sampler, compile_sampler
 
     text, B, coins, masks, flips_ref, events_ref = load_inject(name)
-    W, ring, groups = layout
-    if not _fits(text, W, ring, groups):
+    if not _fits(text, layout):
         pytest.skip("layout does not fit")
-    ds = compile_detector_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
+    ds = compile_detector_sampler(text, **_opts(layout))
     ev = ds.sample(B, coins=coins, masks=masks)
     assert np.array_equal(ev, events_ref)
-    ms = compile_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
+    ms = compile_sampler(text, **_opts(layout))
     fl = ms.sample_flips(B, coins=coins, masks=masks)
     assert np.array_equal(fl, flips_ref)
     # counts mode sees the same events
@@ -76,21 +82,21 @@ def _philox_cases():
 
 
 @pytest.mark.parametrize("case", list(_philox_cases()))
-@pytest.mark.parametrize("layout", [(0, -1, 0), (1, 1, 1), (4, 0, 2), (16, 1, 1), (8, 0, 2)])
+@pytest.mark.parametrize("layout", [(0, -1, 0, 0), (1, 1, 1, 1), (4, 0, 2, 1), (16, 1, 1, 1),
+                                    (8, 0, 2, 1), (2, -1, 0, 2), (8, -1, 0, 2), (32, -1, 0, 2)])
 def test_philox_bit_exact_vs_oracle(oracle_lib, case, layout):
     from paper_2103_02202_b200.sampler import compile_detector_sampler, compile_sampler
 
     text = _philox_cases()[case]
-    W, ring, groups = layout
-    if not _fits(text, W, ring, groups):
+    if not _fits(text, layout):
         pytest.skip("layout does not fit")
-    ds = compile_detector_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
+    ds = compile_detector_sampler(text, **_opts(layout))
     T = ds.tile_shots
     shots = 3 * T + 37
     seed = 0xC0FFEE
     offset = 5 * T
     ev_rows = ds.sample_rows(shots, seed=seed, shot_offset=offset)
-    ms = compile_sampler(text, words_per_tile=W, ring_in_smem=ring, groups=groups)
+    ms = compile_sampler(text, **_opts(layout))
     fl_rows = ms.sample_flip_rows(shots, seed=seed, shot_offset=offset)
     ofl, oev = oracle_lib.sample(ds.flat, shots, T, seed=seed, tile_offset=offset // T,
                                  nthreads=4, schedule=ds.native.noise_schedule())
@@ -101,6 +107,26 @@ def test_philox_bit_exact_vs_oracle(oracle_lib, case, layout):
     assert np.array_equal(b8_unpack(ev_b8, ds.num_columns), rows_unpack(oev, shots))
     fl_b8 = ms.sample_flips(shots, seed=seed, shot_offset=offset)
     assert np.array_equal(b8_unpack(fl_b8, ms.num_measurements), rows_unpack(ofl, shots))
+
+
+@pytest.mark.parametrize("W", [1, 8, 32])
+def test_warp_and_cooperative_kernels_agree(W):
+    """Both frame kernels make the same counter-based draws for one tile width:
+    b8 events, flips and counts agree bit for bit (d=7 surface code, tail tile)."""
+    from paper_2103_02202_b200 import generators as gen
+    from paper_2103_02202_b200.sampler import compile_detector_sampler, compile_sampler
+
+    text = gen.surface_code_memory(7, 7, 2e-3)
+    a = compile_detector_sampler(text, words_per_tile=W, kernel=1)
+    b = compile_detector_sampler(text, words_per_tile=W, kernel=2)
+    assert a.native.info["kernel"] == 1 and b.native.info["kernel"] == 2
+    shots = 37 * 32 * W + 11
+    assert np.array_equal(a.sample(shots, seed=5), b.sample(shots, seed=5))
+    assert np.array_equal(a.sample_counts(shots, seed=5), b.sample_counts(shots, seed=5))
+    ma = compile_sampler(text, words_per_tile=W, kernel=1)
+    mb = compile_sampler(text, words_per_tile=W, kernel=2)
+    assert np.array_equal(ma.sample_flips(shots, seed=6), mb.sample_flips(shots, seed=6))
+    assert np.array_equal(ma.sample_flip_rows(shots, seed=6), mb.sample_flip_rows(shots, seed=6))
 
 
 def test_shard_invariance():

@@ -55,9 +55,18 @@ def test_d25_layout():
     p = N.NativeProgram(f)
     assert p.info["bframe_bits"] == 518500
     assert p.info["smem_bytes"] <= 227 * 1024
+    assert p.info["kernel"] == 1 and p.info["words_per_tile"] == 8
+    # warp-private kernel (opt-in): one 32-shot word column per warp, 8-word tiles
+    pw = N.NativeProgram(f, kernel=2)
+    assert pw.info["kernel"] == 2 and pw.info["words_per_tile"] == 8
+    assert pw.info["warps_per_cta"] >= 12 and pw.info["threads"] == 32 * pw.info["warps_per_cta"]
     for W in (1, 2, 4, 8, 16):
-        q = N.NativeProgram(f, words_per_tile=W, ring_in_smem=0)
+        q = N.NativeProgram(f, words_per_tile=W, ring_in_smem=0, kernel=1)
+        assert q.info["kernel"] == 1
         assert q.info["tile_shots"] == 32 * W and q.info["ring_in_smem"] == 0
+    # d=100: a word column (20k qubits) exceeds shared memory -> cooperative kernel
+    big = N.NativeProgram(flatten(gen.surface_code_memory(100, 2, 1e-3)))
+    assert big.info["kernel"] == 1 and big.info["warps_per_cta"] == 0
 
 
 def test_binomial_thresholds_match_scipy():

@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--words", type=int, default=0)
     ap.add_argument("--debug", type=int, default=0)
+    ap.add_argument("--kernel", type=int, default=0)
     a = ap.parse_args()
     import numpy as np
     import torch
@@ -26,7 +27,7 @@ def main():
     from paper_2103_02202_b200.sampler import compile_detector_sampler
 
     ds = compile_detector_sampler(gen.config_circuit(a.config), debug_skip=64 | a.debug, groups=a.groups,
-                                  words_per_tile=a.words)
+                                  words_per_tile=a.words, kernel=a.kernel)
     out = torch.empty((ds.num_columns, (a.shots + 31) // 32), dtype=torch.int32, device="cuda")
     for i in range(3):
         ds.sample_rows(a.shots, seed=i, out=out)
