@@ -74,6 +74,15 @@ struct pfs_program {
     DevBuf<uint32_t> d_coins, d_masks;
     DevBuf<uint8_t> d_ref;
     DevBuf<unsigned long long> d_counts;
+    // column kernel (KERNEL_COL): op-block stream, block table, packed reference bits
+    bool colk = false;
+    int col_nw = 0;
+    size_t col_smem = 0;
+    int col_grid = 0;
+    ColStream cs;
+    DevBuf<uint32_t> d_cstream;
+    DevBuf<uint2> d_binfo;
+    DevBuf<uint32_t> d_refw;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev[10] = {};
     double last_ms[6] = {0, 0, 0, 0, 0, 0};
@@ -113,9 +122,71 @@ static void choose_warp_layout(pfs_program* pg) {
     pg->wcfg.smem_bytes = (ds ? desc : 0) + (size_t)nw * per;
 }
 
+// Column kernel: staged op blocks up to kColSlotCap bytes; every consumer warp
+// holds 2n + slots + 64 words.  Chosen automatically when at least
+// kColMinWarps word columns fit one CTA (or forced with options.kernel = 3).
+constexpr uint32_t kColSlotCap = 16384;
+constexpr int kColMinWarps = 4;
+constexpr bool kColAuto = false;  // auto layout picks the column kernel
+
+static uint32_t col_max_block_bytes(const HostProgram& hp) {
+    uint32_t mx = 16;
+    for (const DOp& o : hp.ops) {
+        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
+        uint64_t w = COL_HEAD_WORDS;
+        switch (kind) {
+            case K_GATE: w += (uint64_t)o.count * (code >= R_CX ? 2 : 1); break;
+            case K_M: case K_MR: w += 2ull * o.count; break;
+            case K_R: case K_OBS: w += o.count; break;
+            case K_NOISE: w += COL_NP_WORDS + (uint64_t)o.count * (code == CH_DEP2 ? 2 : 1); break;
+            case K_DET:
+                w += code ? (uint64_t)o.count * code
+                          : (uint64_t)o.count + 1 + (hp.det_ptr[o.a + o.count] - hp.det_ptr[o.a]);
+                break;
+            default: break;
+        }
+        uint64_t b = (w * 4 + 15) & ~15ull;
+        if (b > kColSlotCap) b = ((uint64_t)(COL_HEAD_WORDS + (kind == K_NOISE ? COL_NP_WORDS : 0)) * 4 + 15) & ~15ull;
+        mx = std::max<uint32_t>(mx, (uint32_t)b);
+    }
+    return mx;
+}
+
+static bool choose_col_layout(pfs_program* pg) {
+    const HostProgram& hp = pg->hp;
+    const pfs_options& o = pg->opts;
+    pg->colk = false;
+    if (o.kernel != 0 && o.kernel != KERNEL_COL) return false;
+    if (o.kernel == 0 && (!kColAuto || o.words_per_tile > 1)) return false;
+    if (o.words_per_tile > 1) return false;
+    const size_t ww = col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1));
+    const uint32_t sb = col_max_block_bytes(hp);
+    const size_t fixed = col_smem_bytes(0, ww, sb, 0);
+    if (fixed >= pg->smem_optin) return false;
+    int nw = (int)std::min<size_t>(COL_MAX_WARPS, (pg->smem_optin - fixed) / (ww * 4));
+    if (o.threads > 0) nw = std::min(nw, std::max(1, o.threads / 32 - 1));
+    if (nw < (o.kernel == KERNEL_COL ? 1 : kColMinWarps)) return false;
+    pg->colk = true;
+    pg->col_nw = nw;
+    pg->col_smem = col_smem_bytes(nw, ww, sb, 0);
+    return true;
+}
+
 static void choose_layout(pfs_program* pg) {
     const HostProgram& hp = pg->hp;
     pfs_options o = pg->opts;
+    if (choose_col_layout(pg)) {
+        // the program's tile is one word: RNG counters per 32-shot column
+        pg->wcfg = LaunchCfg{};
+        pg->cfg = LaunchCfg{};
+        pg->cfg.W = 1;
+        pg->cfg.groups = 1;
+        pg->cfg.threads = 32 * (pg->col_nw + 1);
+        pg->cfg.ring_smem = true;
+        pg->cfg.smem_bytes = pg->col_smem;
+        pg->cfg.kernel = 0;
+        return;
+    }
     choose_warp_layout(pg);
     // the warp-private kernel takes 8-word tiles (hit lists shared by 8 warps)
     // unless the caller fixes W; the cooperative kernel then uses the same W
@@ -205,7 +276,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
     }
     choose_layout(pg);
     if (pg->opts.schedule_only && pg->cfg.W < 1) pg->cfg.W = pg->opts.words_per_tile > 0 ? pg->opts.words_per_tile : 1;
-    if (!pg->opts.schedule_only && !pg->wcfg.kernel && (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget)) {
+    if (!pg->opts.schedule_only && !pg->wcfg.kernel && !pg->colk && (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget)) {
         delete pg;
         return fail(PFS_E_INVALID, "frame table of " + std::to_string(num_qubits) +
                                        " qubits does not fit one CTA's shared memory");
@@ -217,6 +288,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         dedup_operands(pg->hp);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
         assign_staging(pg->hp);
+        if (pg->colk) pg->cs = build_col_stream(pg->hp, kColSlotCap);
     } catch (const std::invalid_argument& e) {
         delete pg;
         return fail(PFS_E_INVALID, e.what());
@@ -232,8 +304,8 @@ int pfs_program_info(const pfs_program* pg, pfs_info* o) {
     o->num_qubits = hp.num_qubits;
     o->words_per_tile = pg->cfg.W;
     o->groups = pg->cfg.groups;
-    o->kernel = pg->wcfg.kernel ? KERNEL_WARP : KERNEL_COOP;
-    o->warps_per_cta = pg->wcfg.kernel ? pg->wcfg.threads / 32 : 0;
+    o->kernel = pg->colk ? KERNEL_COL : pg->wcfg.kernel ? KERNEL_WARP : KERNEL_COOP;
+    o->warps_per_cta = pg->colk ? pg->col_nw : pg->wcfg.kernel ? pg->wcfg.threads / 32 : 0;
     o->tile_shots = 32 * pg->cfg.W;
     o->threads = pg->cfg.threads;
     o->ring_in_smem = pg->cfg.ring_smem ? 1 : 0;
@@ -294,6 +366,7 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_nscratch.release(); pg->d_clock.release();
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
+        pg->d_cstream.release(); pg->d_binfo.release(); pg->d_refw.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
         for (auto& e : pg->ev) if (e) cudaEventDestroy(e);
         if (prev >= 0) cudaSetDevice(prev);
@@ -325,8 +398,9 @@ static int ensure_device(pfs_program* pg, int device) {
     pg->smem_optin = prop.sharedMemPerBlockOptin;
     if (pg->opts.schedule_only)
         return fail(PFS_E_INVALID, "schedule-only program");
-    if (pg->wcfg.kernel ? pg->wcfg.smem_bytes > pg->smem_optin
-                        : pg->cfg.smem_bytes > pg->smem_optin)
+    if (pg->colk ? pg->col_smem > pg->smem_optin
+                 : pg->wcfg.kernel ? pg->wcfg.smem_bytes > pg->smem_optin
+                                   : pg->cfg.smem_bytes > pg->smem_optin)
         return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory");
     const HostProgram& hp = pg->hp;
     CUDA_TRY(upload(pg->d_ops, hp.ops));
@@ -357,6 +431,19 @@ static int ensure_device(pfs_program* pg, int device) {
         CUDA_TRY(set_frame_warp_kernel_smem(pg->wcfg));
         pg->wcfg.grid = grid_of(pg->wcfg);
     }
+    if (pg->colk) {
+        CUDA_TRY(upload(pg->d_cstream, pg->cs.words));
+        std::vector<uint2> bi(pg->cs.n_blocks);
+        for (int64_t i = 0; i < pg->cs.n_blocks; i++) bi[i] = make_uint2(pg->cs.binfo[2 * i], pg->cs.binfo[2 * i + 1]);
+        CUDA_TRY(upload(pg->d_binfo, bi));
+        CUDA_TRY(set_frame_col_kernel_smem(pg->smem_optin));
+        int per_sm = pg->opts.ctas_per_sm;
+        if (per_sm <= 0) {
+            per_sm = (int)std::max<size_t>(1, prop.sharedMemPerMultiprocessor / (pg->col_smem + 1024));
+            per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / (32 * (pg->col_nw + 1))));
+        }
+        pg->col_grid = pg->num_sms * per_sm;
+    }
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
     for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
     pg->device = device;
@@ -376,8 +463,25 @@ static bool is_device_ptr(const void* p) {
 // sub-chunks bounded by the hit-list buffer budget.  kp describes tile 0 of
 // the range (tile_offset, output and inject pointers, num_shots).
 static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64_t nt, bool injected,
-                        cudaStream_t st, bool time_noise) {
+                        cudaStream_t st, bool time_noise, ColParams cp = ColParams{}) {
     const HostProgram& hp = pg->hp;
+    if (pg->colk) {
+        // column kernel: one launch, noise sampled inline, outputs written directly
+        cp.stream = pg->d_cstream.p;
+        cp.binfo = pg->d_binfo.p;
+        cp.n_blocks = (int32_t)pg->cs.n_blocks;
+        cp.slot_bytes = (int32_t)std::max<uint32_t>(pg->cs.slot_bytes, 16u);
+        cp.nw = pg->col_nw;
+        cp.warp_words = (int32_t)col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1));
+        cp.n_units = nt;
+        kp.n_tiles = nt;
+        const size_t smem = col_smem_bytes(cp.nw, cp.warp_words, cp.slot_bytes,
+                                           kp.counts_in_smem ? hp.num_cols : 0);
+        const int grid = (int)std::min<int64_t>(pg->col_grid, (nt + cp.nw - 1) / cp.nw);
+        CUDA_TRY(launch_frame_col_kernel(kp, cp, grid, smem, st));
+        pg->last_launches++;
+        return PFS_OK;
+    }
     const int W = cfg.W;
     const int64_t T = 32 * W;
     const bool pregen = !injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2);
@@ -494,6 +598,17 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         CUDA_TRY(cudaMemcpyAsync(pg->d_ref.p, ref_bits, hp.num_meas,
                                  is_device_ptr(ref_bits) ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
         d_ref = pg->d_ref.p;
+        if (pg->colk) {
+            // reference bits packed LSB-first into words (XORed per 32-column block)
+            std::vector<uint32_t> rw((hp.num_meas + 31) / 32, 0u);
+            std::vector<uint8_t> rb(hp.num_meas);
+            if (is_device_ptr(ref_bits)) CUDA_TRY(cudaMemcpy(rb.data(), ref_bits, hp.num_meas, cudaMemcpyDeviceToHost));
+            else std::memcpy(rb.data(), ref_bits, hp.num_meas);
+            for (int64_t m = 0; m < hp.num_meas; m++) if (rb[m] & 1) rw[m >> 5] |= 1u << (m & 31);
+            CUDA_TRY(pg->d_refw.reserve(rw.size()));
+            CUDA_TRY(cudaMemcpyAsync(pg->d_refw.p, rw.data(), rw.size() * 4, cudaMemcpyHostToDevice, st));
+            CUDA_TRY(cudaStreamSynchronize(st));
+        }
     }
     if (timing) CUDA_TRY(cudaEventRecord(pg->ev[1], st));
 
@@ -532,14 +647,15 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     const bool warpk = cfg.kernel == KERNEL_WARP;
     kp.stage = (pg->opts.debug_skip & 1024) ? 0 : 1;  // bit 10: profiling ablation, no staging
     kp.desc_in_smem = warpk ? pg->warp_desc_smem : (desc_fits(hp) ? 1 : 0);
-    CUDA_TRY(pg->d_nscratch.reserve((size_t)cfg.grid * cfg.threads * NZ_MAX_LIST));
+    CUDA_TRY(pg->d_nscratch.reserve(pg->colk ? (size_t)pg->col_grid * 32 * (pg->col_nw + 1) * NZ_MAX_LIST
+                                              : (size_t)cfg.grid * cfg.threads * NZ_MAX_LIST));
     kp.noise_scratch = pg->d_nscratch.p;
     if (pg->opts.debug_skip & 64) {  // op-boundary clock trace of the first tile
         CUDA_TRY(pg->d_clock.reserve(hp.ops.size() * 9 + 1));
         kp.op_clock = pg->d_clock.p;
     }
 
-    if (!warpk && !cfg.ring_smem) {
+    if (!warpk && !cfg.ring_smem && !pg->colk) {
         CUDA_TRY(pg->d_ring.reserve((size_t)std::max<int64_t>(hp.num_slots, 1) * W * cfg.grid * cfg.groups));
         kp.ring_global = pg->d_ring.p;
     }
@@ -552,12 +668,16 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         kp.counts = cptr;
         const size_t extra = (size_t)hp.num_cols * 4;
         kp.counts_in_smem = (!warpk && cfg.smem_bytes + extra <= pg->smem_optin) ? 1 : 0;
-        if (kp.counts_in_smem) {
+        if (pg->colk) {
+            kp.counts_in_smem = col_smem_bytes(pg->col_nw, col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1)),
+                                               std::max<uint32_t>(pg->cs.slot_bytes, 16u), hp.num_cols) <= pg->smem_optin;
+        } else if (kp.counts_in_smem) {
             cfg.smem_bytes += extra;
             CUDA_TRY(set_frame_kernel_smem(cfg));
         }
         // per-CTA u32 counters: bound shots per launch so no counter can overflow
-        const int64_t max_tiles = std::max<int64_t>(1, ((int64_t)1 << 30) / T) * cfg.grid;
+        const int64_t max_tiles = std::max<int64_t>(1, ((int64_t)1 << 30) / T) *
+                                  (pg->colk ? pg->col_grid : cfg.grid);
         for (int64_t t0 = 0; t0 < n_tiles_all; t0 += max_tiles) {
             const int64_t nt = std::min(max_tiles, n_tiles_all - t0);
             kp.n_tiles = nt;
@@ -588,10 +708,11 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     const int64_t dev_pitch = b8 ? ((nbytes + 31) / 32) * 32 : 0;
     int64_t chunk_tiles = n_tiles_all;
     if (!dev_out) {
-        const int64_t bytes_per_tile = R * W * 4 + (b8 ? T * dev_pitch : 0);
+        const int64_t bytes_per_tile = (pg->colk && b8 ? 0 : R * W * 4) + (b8 ? T * dev_pitch : 0);
         const int64_t target = (int64_t)256 << 20;
         chunk_tiles = std::max<int64_t>(1, target / std::max<int64_t>(bytes_per_tile, 1));
-        chunk_tiles = std::max<int64_t>(chunk_tiles, cfg.grid);  // keep every SM busy
+        chunk_tiles = std::max<int64_t>(chunk_tiles, pg->colk ? (int64_t)pg->col_grid * pg->col_nw
+                                                                  : (int64_t)cfg.grid);  // keep every SM busy
         chunk_tiles = std::min(chunk_tiles, n_tiles_all);
     }
     const bool direct_rows = dev_out && !b8;  // *_ROWS into the caller's buffer
@@ -601,7 +722,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     for (int b = 0; b < nbuf; b++) {
         // (+ padding to whole 8-word groups: the word-major transpose reads
         // narrow tiles in groups of 8 words)
-        if (!direct_rows) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * ((chunk_words + 7) & ~7ll)));
+        if (!direct_rows && !(pg->colk && b8)) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * ((chunk_words + 7) & ~7ll)));
         if (b8 && !dev_out) CUDA_TRY(pg->d_b8[b].reserve((size_t)chunk_tiles * T * dev_pitch));
     }
     if (timing) CUDA_TRY(cudaEventRecord(pg->ev[1], st));
@@ -625,7 +746,22 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         kp.tile_offset = shot_offset / T + t0;
         kp.num_shots = nshots;
         if (injected) { kp.coins = pg->d_coins.p + t0 * W; kp.masks = pg->d_masks.p + t0 * W; }
-        if (direct_rows && (used_words % W) != 0) {
+        ColParams cpx{};
+        if (pg->colk) {
+            cpx.records = rows_meas ? 1 : 0;
+            cpx.ncols_out = (int32_t)R;
+            if (b8) {
+                cpx.b8_out = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
+                cpx.b8_pitch = dev_out ? out_pitch : dev_pitch;
+                cpx.b8_bytes = nbytes;
+                cpx.b8_aligned = ((reinterpret_cast<uintptr_t>(cpx.b8_out) | (uintptr_t)cpx.b8_pitch) & 3u) == 0;
+                cpx.ref_words = mode == PFS_MODE_SAMPLES ? pg->d_refw.p : nullptr;
+            } else {
+                cpx.rows_out = rows;
+                cpx.rows_stride = row_words;
+            }
+        }
+        if (!pg->colk && direct_rows && (used_words % W) != 0) {
             // the last tile would write past the caller's rows: stage through scratch
             CUDA_TRY(pg->d_rows[0].reserve((size_t)std::max<int64_t>(R, 1) * chunk_words));
             rows = pg->d_rows[0].p;
@@ -637,11 +773,13 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         }
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[2], st));
         {
-            int rc2 = launch_tiles(pg, kp, cfg, nt, injected, st, timing && ci == 0);
+            int rc2 = launch_tiles(pg, kp, cfg, nt, injected, st, timing && ci == 0, cpx);
             if (rc2) return rc2;
         }
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[3], st));
-        if (b8) {
+        if (b8 && pg->colk) {
+            if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
+        } else if (b8) {
             uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
             const int64_t pitch = dev_out ? out_pitch : dev_pitch;
             // word-major tiles narrower than 8 words are contiguous word columns:
@@ -659,7 +797,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (timing && ci == 0) {
             CUDA_TRY(cudaStreamSynchronize(st));
             cudaEventElapsedTime(&frame_ms, pg->ev[2], pg->ev[3]);
-            if (!injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2)) {
+            if (!pg->colk && !injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2)) {
                 float nz = 0;
                 cudaEventElapsedTime(&nz, pg->ev[8], pg->ev[9]);
                 pg->last_ms[5] = nz;

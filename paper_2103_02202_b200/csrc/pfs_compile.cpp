@@ -551,4 +551,63 @@ void assign_staging(HostProgram& hp) {
     }
 }
 
+// Column-kernel op stream: one self-describing block per device op (header,
+// the NoiseParam of a noise op, then the op's operands), 16-byte aligned so the
+// producer warp can bulk-copy a block into a shared-memory slot in one
+// transaction.  Operands larger than slot_cap stay in global memory
+// (F_GLOBALP); only their header is staged.
+ColStream build_col_stream(const HostProgram& hp, uint32_t slot_cap) {
+    ColStream cs;
+    std::vector<uint32_t> pay;
+    for (const DOp& o : hp.ops) {
+        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
+        pay.clear();
+        auto take = [&](const std::vector<uint32_t>& arr, size_t off, size_t n) {
+            pay.insert(pay.end(), arr.begin() + off, arr.begin() + off + n);
+        };
+        switch (kind) {
+            case K_GATE: take(hp.targets, o.off, (size_t)o.count * rule_arity(code)); break;
+            case K_M: case K_MR: take(hp.targets, o.off, 2 * (size_t)o.count); break;
+            case K_R: case K_OBS: take(hp.targets, o.off, o.count); break;
+            case K_NOISE: take(hp.targets, o.off, (size_t)o.count * (code == CH_DEP2 ? 2 : 1)); break;
+            case K_DET:
+                if (code) {
+                    take(hp.det_terms, o.off, (size_t)o.count * code);
+                } else {
+                    const uint32_t base = hp.det_ptr[o.a];
+                    for (uint32_t c = 0; c <= o.count; c++) pay.push_back(hp.det_ptr[o.a + c] - base);
+                    take(hp.det_terms, base, hp.det_ptr[o.a + o.count] - base);
+                }
+                break;
+            default: break;
+        }
+        while (cs.words.size() & 3) cs.words.push_back(0u);
+        const size_t start = cs.words.size();
+        const uint32_t hw = COL_HEAD_WORDS + (kind == K_NOISE ? COL_NP_WORDS : 0u);
+        const bool globalp = ((size_t)hw + pay.size()) * 4 > slot_cap;
+        CHead h{};
+        h.kcf = o.kcf | (globalp ? (F_GLOBALP << 16) : 0u);
+        h.count = o.count;
+        h.a = o.a;
+        h.b = o.b;
+        h.pwords = (uint32_t)pay.size();
+        h.goff = (uint32_t)(start + hw);
+        const uint32_t* hp32 = reinterpret_cast<const uint32_t*>(&h);
+        cs.words.insert(cs.words.end(), hp32, hp32 + COL_HEAD_WORDS);
+        if (kind == K_NOISE) {
+            const uint32_t* np32 = reinterpret_cast<const uint32_t*>(&hp.noise[o.b]);
+            cs.words.insert(cs.words.end(), np32, np32 + COL_NP_WORDS);
+        }
+        cs.words.insert(cs.words.end(), pay.begin(), pay.end());
+        const uint32_t staged = (uint32_t)((((globalp ? hw : hw + pay.size()) * 4) + 15) & ~(size_t)15);
+        if (start / 4 > 0xFFFFFFFFull) bad("op stream too large");
+        cs.binfo.push_back((uint32_t)(start / 4));
+        cs.binfo.push_back(staged);
+        cs.slot_bytes = std::max(cs.slot_bytes, staged);
+    }
+    while (cs.words.size() & 3) cs.words.push_back(0u);
+    cs.n_blocks = (int64_t)hp.ops.size();
+    return cs;
+}
+
 }  // namespace pfs

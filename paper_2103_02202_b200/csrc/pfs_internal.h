@@ -204,4 +204,69 @@ cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, i
                                int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
                                int64_t pitch, cudaStream_t stream, bool word_major = false);
 
+// ---------------------------------------------------------------- column kernel
+// frame_col_kernel (pfs_colkernel.cu): every consumer warp owns one 32-shot
+// word column (its own x/z planes and record ring in shared memory) for the
+// whole circuit, so warps never wait for each other; the op stream is a byte
+// stream of self-describing blocks that one producer warp bulk-copies (TMA)
+// into a ring of shared-memory slots shared by the CTA's warps.
+constexpr int KERNEL_COL = 3;
+constexpr int COL_MAX_WARPS = 15;     // consumer warps per CTA (+1 producer; 128 registers per thread)
+constexpr int COL_SLOTS = 4;          // op-block ring depth
+constexpr uint32_t F_GLOBALP = 8u;    // block payload left in global memory (too big to stage)
+constexpr uint32_t COL_HEAD_WORDS = 8;   // block header (CHead)
+constexpr uint32_t COL_NP_WORDS = 12;    // NoiseParam after a noise op's header
+
+// Block header, 32 bytes; payload words follow (after a NoiseParam for noise ops).
+//   GATE: count apps, payload targets (1 or 2 per app)
+//   M/MR: count targets, a = first record, b = first coin row, payload (qubit, slot) pairs
+//   R   : count targets, b = first coin row, payload qubits
+//   NOISE: count apps, a = first noise-mask row, b = noise ordinal, payload targets
+//   DET : count columns, a = first column; code = k > 0: payload k slots per column;
+//         code = 0: payload = count + 1 column offsets, then the slot terms
+//   OBS : count terms, a = accumulator slot, payload slots
+struct CHead {
+    uint32_t kcf;
+    uint32_t count;
+    uint32_t a;
+    uint32_t b;
+    uint32_t pwords;   // payload words
+    uint32_t goff;     // word offset of the payload in the global stream
+    uint32_t r0, r1;
+};
+static_assert(sizeof(CHead) == 32, "CHead is 32 bytes");
+
+struct ColStream {
+    std::vector<uint32_t> words;     // blocks, each 16-byte aligned
+    std::vector<uint32_t> binfo;     // per block: (16-byte offset, staged bytes) pairs
+    uint32_t slot_bytes = 0;         // largest staged block
+    int64_t n_blocks = 0;
+};
+ColStream build_col_stream(const HostProgram& hp, uint32_t slot_cap);
+
+struct ColParams {
+    const uint32_t* stream;
+    const uint2* binfo;
+    uint8_t* b8_out;             // shot-major output (b8 modes) or null
+    int64_t b8_pitch;
+    int64_t b8_bytes;            // ceil(R / 8)
+    const uint32_t* ref_words;   // SAMPLES: reference bits packed LSB-first in words, or null
+    uint32_t* rows_out;          // *_ROWS modes: [R][rows_stride] words, or null
+    int64_t rows_stride;
+    int64_t n_units;             // 32-shot words of this launch
+    int32_t n_blocks;
+    int32_t slot_bytes;
+    int32_t nw;                  // consumer warps per CTA
+    int32_t warp_words;          // shared-memory words per consumer warp
+    int32_t records;             // 1: the output columns are measurement records
+    int32_t ncols_out;           // R: output columns (records or detector columns)
+    int32_t b8_aligned;          // b8 pitch and base allow 32-bit stores
+};
+
+size_t col_warp_words(int num_qubits, int64_t num_slots);
+size_t col_smem_bytes(int nw, size_t warp_words, uint32_t slot_bytes, int64_t counts_words);
+cudaError_t launch_frame_col_kernel(const KParams& kp, const ColParams& cp, int grid, size_t smem,
+                                    cudaStream_t stream);
+cudaError_t set_frame_col_kernel_smem(size_t smem);
+
 }  // namespace pfs

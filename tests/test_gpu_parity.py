@@ -29,10 +29,11 @@ def need_gpu():
 
 # (words_per_tile, ring_in_smem, groups, kernel) layouts exercising every
 # kernel instantiation: cooperative (kernel 1; one and two tiles in flight per
-# CTA) and warp-private (kernel 2; one word column per warp), 0 = auto
+# CTA), warp-private (kernel 2; one word column per warp, 8-word tiles) and
+# word-column (kernel 3; one-word tiles, staged op-block stream), 0 = auto
 LAYOUTS = [(0, -1, 0, 0), (1, 0, 1, 1), (2, 1, 2, 1), (4, 0, 0, 1), (8, 1, 1, 1), (16, 0, 2, 1),
            (32, 1, 0, 1), (16, 0, 1, 1), (1, -1, 0, 2), (2, -1, 0, 2), (4, -1, 0, 2),
-           (16, -1, 0, 2), (32, -1, 0, 2)]
+           (16, -1, 0, 2), (32, -1, 0, 2), (0, -1, 0, 3)]
 
 
 def _opts(layout):
