@@ -42,8 +42,9 @@ def parse_args():
     ap.add_argument("--words", type=int, default=0, help="override W (32-shot words per tile)")
     ap.add_argument("--ring", type=int, default=-1)
     ap.add_argument("--threads", type=int, default=0)
-    ap.add_argument("--kernel", type=int, default=0, help="frame kernel: 0 auto, 1 cooperative, 2 warp-private")
+    ap.add_argument("--kernel", type=int, default=0, help="frame kernel: 0 auto, 1 cooperative, 2 warp-private, 3 word-column")
     ap.add_argument("--target-hits", type=float, default=0.0)
+    ap.add_argument("--groups", type=int, default=0, help="cooperative kernel: tiles in flight per CTA")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
@@ -212,7 +213,7 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     flat = flatten(config_text(cfg))
     compile_s = time.perf_counter() - t0
     kw = dict(words_per_tile=args.words, ring_in_smem=args.ring, threads=args.threads,
-              noise_target_hits=args.target_hits, kernel=args.kernel)
+              noise_target_hits=args.target_hits, kernel=args.kernel, groups=args.groups)
     ds = DetectorSampler.__new__(DetectorSampler)
     ds.circuit, ds.flat, ds.device = None, flat, local_rank
     ds._seeds = np.random.default_rng(0)

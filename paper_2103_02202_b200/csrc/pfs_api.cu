@@ -76,6 +76,8 @@ struct pfs_program {
     DevBuf<unsigned long long> d_counts;
     // column kernel (KERNEL_COL): op-block stream, block table, packed reference bits
     bool colk = false;
+    bool col_ring_smem = true;
+    int col_v = 1;      // words per lane (tile = 32 col_v shots)
     int col_nw = 0;
     size_t col_smem = 0;
     int col_grid = 0;
@@ -91,11 +93,13 @@ struct pfs_program {
 
 static bool desc_fits(const HostProgram& hp) { return hp.ops.size() * sizeof(DOp) <= (size_t)DESC_SMEM_MAX; }
 
-// per-group hit counts, TMA staging buffers + mbarriers, descriptor copy
+// per-group hit counts, descriptor copy
 static size_t fixed_smem(const HostProgram& hp, int groups) {
-    return (size_t)hp.num_noise * 4 * groups + 16 + (size_t)groups * 2 * STAGE_BYTES + groups * 16 +
-           (desc_fits(hp) ? hp.ops.size() * sizeof(DOp) : 0);
+    return (size_t)hp.num_noise * 4 * groups + 16 + (desc_fits(hp) ? hp.ops.size() * sizeof(DOp) : 0);
 }
+
+// Cooperative-kernel groups per CTA (named barriers 1..kMaxGroups).
+constexpr int kMaxGroups = 8;
 
 // Warp-private kernel: a warp's word column (x/z per qubit, record ring, hit
 // counts) must fit shared memory several times over; descriptors join it when
@@ -145,8 +149,8 @@ static uint32_t col_max_block_bytes(const HostProgram& hp) {
                 break;
             default: break;
         }
-        uint64_t b = (w * 4 + 15) & ~15ull;
-        if (b > kColSlotCap) b = ((uint64_t)(COL_HEAD_WORDS + (kind == K_NOISE ? COL_NP_WORDS : 0)) * 4 + 15) & ~15ull;
+        const uint64_t b = (w * 4 + 15) & ~15ull;
+        if (b > kColSlotCap) return 0;  // an op too large to stage: not eligible
         mx = std::max<uint32_t>(mx, (uint32_t)b);
     }
     return mx;
@@ -157,18 +161,41 @@ static bool choose_col_layout(pfs_program* pg) {
     const pfs_options& o = pg->opts;
     pg->colk = false;
     if (o.kernel != 0 && o.kernel != KERNEL_COL) return false;
-    if (o.kernel == 0 && (!kColAuto || o.words_per_tile > 1)) return false;
-    if (o.words_per_tile > 1) return false;
-    const size_t ww = col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1));
+    if (o.kernel == 0 && !kColAuto) return false;
+    if (o.words_per_tile != 0 && o.words_per_tile != 1 && o.words_per_tile != 2 && o.words_per_tile != 4)
+        return false;
     const uint32_t sb = col_max_block_bytes(hp);
-    const size_t fixed = col_smem_bytes(0, ww, sb, 0);
-    if (fixed >= pg->smem_optin) return false;
-    int nw = (int)std::min<size_t>(COL_MAX_WARPS, (pg->smem_optin - fixed) / (ww * 4));
-    if (o.threads > 0) nw = std::min(nw, std::max(1, o.threads / 32 - 1));
-    if (nw < (o.kernel == KERNEL_COL ? 1 : kColMinWarps)) return false;
+    if (sb == 0) return false;
+    // candidates (V words per lane, record ring in shared or global memory):
+    // most shots in flight per SM (columns x 32 V), preferring wider lanes (fewer
+    // instructions per shot) and a shared-memory ring on ties
+    int best_nw = 0, best_v = 1;
+    bool best_rs = true;
+    int64_t best_score = -1;
+    for (int V = 4; V >= 1; V >>= 1) {
+        if (o.words_per_tile > 0 && V != o.words_per_tile) continue;
+        for (int rs = 1; rs >= 0; rs--) {
+            if (o.ring_in_smem == 0 && rs) continue;
+            if (o.ring_in_smem == 1 && !rs) continue;
+            const size_t ww = col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1), rs != 0, V);
+            const size_t fixed = col_smem_bytes(0, ww, sb, 0);
+            if (fixed >= pg->smem_optin) continue;
+            int nw = (int)std::min<size_t>(col_max_warps(V, rs != 0), (pg->smem_optin - fixed) / (ww * 4));
+            if (o.threads > 0) nw = std::min(nw, std::max(1, o.threads / 32 - 1));
+            if (nw < 1) continue;
+            // warps keep latency hidden: below kColMinWarps a column counts half
+            const int64_t eff = nw >= kColMinWarps ? nw : nw / 2;
+            const int64_t score = eff * 32 * V * 16 + V * 2 + rs;
+            if (score > best_score) { best_score = score; best_nw = nw; best_v = V; best_rs = rs != 0; }
+        }
+    }
+    if (best_nw < (o.kernel == KERNEL_COL ? 1 : kColMinWarps)) return false;
     pg->colk = true;
-    pg->col_nw = nw;
-    pg->col_smem = col_smem_bytes(nw, ww, sb, 0);
+    pg->col_nw = best_nw;
+    pg->col_v = best_v;
+    pg->col_ring_smem = best_rs;
+    pg->col_smem = col_smem_bytes(best_nw, col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1), best_rs, best_v),
+                                  sb, 0);
     return true;
 }
 
@@ -179,10 +206,10 @@ static void choose_layout(pfs_program* pg) {
         // the program's tile is one word: RNG counters per 32-shot column
         pg->wcfg = LaunchCfg{};
         pg->cfg = LaunchCfg{};
-        pg->cfg.W = 1;
+        pg->cfg.W = pg->col_v;
         pg->cfg.groups = 1;
         pg->cfg.threads = 32 * (pg->col_nw + 1);
-        pg->cfg.ring_smem = true;
+        pg->cfg.ring_smem = pg->col_ring_smem;
         pg->cfg.smem_bytes = pg->col_smem;
         pg->cfg.kernel = 0;
         return;
@@ -192,12 +219,12 @@ static void choose_layout(pfs_program* pg) {
     // unless the caller fixes W; the cooperative kernel then uses the same W
     if (pg->wcfg.kernel && o.words_per_tile <= 0) o.words_per_tile = 8;
     const size_t budget = pg->smem_optin;
-    const size_t fixed1 = fixed_smem(hp, 1), fixed2 = fixed_smem(hp, 2);
     auto frame = [&](int W) { return frame_smem_bytes(hp.num_qubits, W); };
     auto ring = [&](int W) { return (size_t)hp.num_slots * W * 4; };
-    auto fits = [&](int W, int G, bool rs) {
-        return G * (frame(W) + (rs ? ring(W) : 0)) + (G == 1 ? fixed1 : fixed2) <= budget;
+    auto need = [&](int W, int G, bool rs) {
+        return G * (frame(W) + (rs ? ring(W) : 0)) + fixed_smem(hp, G);
     };
+    auto fits = [&](int W, int G, bool rs) { return need(W, G, rs) <= budget; };
     int W = 0, G = 1;
     bool rs = false;
     if (o.words_per_tile > 0) {
@@ -224,10 +251,11 @@ static void choose_layout(pfs_program* pg) {
             }
         }
     }
+    G = std::min(G, kMaxGroups);
     pg->cfg.W = W;
     pg->cfg.groups = G;
     pg->cfg.ring_smem = rs;
-    pg->cfg.smem_bytes = W > 0 ? G * (frame(W) + (rs ? ring(W) : 0)) + (G == 1 ? fixed1 : fixed2) : 0;
+    pg->cfg.smem_bytes = W > 0 ? need(W, G, rs) : 0;
     int threads = o.threads > 0 ? std::min(o.threads, FRAME_MAX_THREADS) : FRAME_MAX_THREADS;
     threads = (threads / (32 * G)) * 32 * G;  // whole warps per group
     pg->cfg.threads = threads;
@@ -287,7 +315,6 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         reorder_for_banks(pg->hp, pg->wcfg.kernel ? 2 : pg->cfg.W);
         dedup_operands(pg->hp);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
-        assign_staging(pg->hp);
         if (pg->colk) pg->cs = build_col_stream(pg->hp, kColSlotCap);
     } catch (const std::invalid_argument& e) {
         delete pg;
@@ -472,13 +499,18 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
         cp.n_blocks = (int32_t)pg->cs.n_blocks;
         cp.slot_bytes = (int32_t)std::max<uint32_t>(pg->cs.slot_bytes, 16u);
         cp.nw = pg->col_nw;
-        cp.warp_words = (int32_t)col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1));
+        cp.warp_words = (int32_t)col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1), pg->col_ring_smem,
+                                                pg->col_v);
+        if (!pg->col_ring_smem) {
+            CUDA_TRY(pg->d_ring.reserve((size_t)std::max<int64_t>(hp.num_slots, 1) * pg->col_grid * cp.nw * pg->col_v));
+            kp.ring_global = pg->d_ring.p;
+        }
         cp.n_units = nt;
         kp.n_tiles = nt;
         const size_t smem = col_smem_bytes(cp.nw, cp.warp_words, cp.slot_bytes,
                                            kp.counts_in_smem ? hp.num_cols : 0);
         const int grid = (int)std::min<int64_t>(pg->col_grid, (nt + cp.nw - 1) / cp.nw);
-        CUDA_TRY(launch_frame_col_kernel(kp, cp, grid, smem, st));
+        CUDA_TRY(launch_frame_col_kernel(kp, cp, pg->col_v, pg->col_ring_smem, grid, smem, st));
         pg->last_launches++;
         return PFS_OK;
     }
@@ -645,7 +677,6 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     const bool coop_counts = mode == PFS_MODE_COUNTS && pg->cfg.kernel && pg->opts.kernel != KERNEL_WARP;
     LaunchCfg cfg = (!pg->wcfg.kernel || coop_counts) ? pg->cfg : pg->wcfg;
     const bool warpk = cfg.kernel == KERNEL_WARP;
-    kp.stage = (pg->opts.debug_skip & 1024) ? 0 : 1;  // bit 10: profiling ablation, no staging
     kp.desc_in_smem = warpk ? pg->warp_desc_smem : (desc_fits(hp) ? 1 : 0);
     CUDA_TRY(pg->d_nscratch.reserve(pg->colk ? (size_t)pg->col_grid * 32 * (pg->col_nw + 1) * NZ_MAX_LIST
                                               : (size_t)cfg.grid * cfg.threads * NZ_MAX_LIST));
@@ -669,7 +700,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         const size_t extra = (size_t)hp.num_cols * 4;
         kp.counts_in_smem = (!warpk && cfg.smem_bytes + extra <= pg->smem_optin) ? 1 : 0;
         if (pg->colk) {
-            kp.counts_in_smem = col_smem_bytes(pg->col_nw, col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1)),
+            kp.counts_in_smem = col_smem_bytes(pg->col_nw, col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1), pg->col_ring_smem, pg->col_v),
                                                std::max<uint32_t>(pg->cs.slot_bytes, 16u), hp.num_cols) <= pg->smem_optin;
         } else if (kp.counts_in_smem) {
             cfg.smem_bytes += extra;

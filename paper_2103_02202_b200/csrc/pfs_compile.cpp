@@ -524,33 +524,6 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
     }
 }
 
-// Static operand blocks (targets, uniform detector terms) staged by TMA:
-// d = 16-byte aligned word offset of the block in its array, e = valid | array |
-// first-operand word offset | size in 16-byte units.
-void assign_staging(HostProgram& hp) {
-    for (DOp& o : hp.ops) {
-        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
-        uint64_t words = 0;
-        uint32_t arr = 0;
-        switch (kind) {
-            case K_GATE: words = (uint64_t)o.count * (rule_arity(code) == 2 ? 2 : 1); break;
-            case K_M: case K_MR: words = 2ull * o.count; break;
-            case K_R: case K_OBS: words = o.count; break;
-            case K_DET: if (code) { words = (uint64_t)o.count * code; arr = 1; } break;
-            default: break;
-        }
-        if (kind == K_NOISE) continue;  // d/e: next noise op (build_noise_schedule)
-        o.d = 0;
-        o.e = 0;
-        if (words == 0) continue;
-        const uint64_t lo = o.off & ~3u;
-        const uint64_t bytes = ((o.off + words - lo) * 4 + 15) & ~15ull;
-        if (bytes > (uint64_t)STAGE_BYTES) continue;
-        o.d = (uint32_t)lo;
-        o.e = 0x80000000u | (arr << 30) | ((o.off - (uint32_t)lo) << 16) | (uint32_t)(bytes / 16);
-    }
-}
-
 // Column-kernel op stream: one self-describing block per device op (header,
 // the NoiseParam of a noise op, then the op's operands), 16-byte aligned so the
 // producer warp can bulk-copy a block into a shared-memory slot in one

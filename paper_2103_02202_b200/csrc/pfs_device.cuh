@@ -178,6 +178,32 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                  ::"r"(smem_addr(dst)), "l"(src), "r"(bytes), "r"(smem_addr(mbar)) : "memory");
 }
+// wait with a suspend-time hint: the waiting warp sleeps instead of spinning
+// on the issue slots its neighbours need
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* mbar, uint32_t parity) {
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_addr(mbar)), "r"(parity), "r"(1000000u) : "memory");
+    }
+}
+
+// wait polling with a nanosleep backoff (a lone producer thread whose latency
+// does not matter: the slot ring is normally full)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* mbar, uint32_t parity) {
+    uint32_t done = 0;
+    for (;;) {
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(done) : "r"(smem_addr(mbar)), "r"(parity) : "memory");
+        if (done) return;
+        __nanosleep(256);
+    }
+}
+
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
     uint32_t done = 0;
     while (!done) {

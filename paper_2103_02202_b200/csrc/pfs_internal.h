@@ -35,8 +35,6 @@ constexpr int NZ_MAX_LIST = 8;
 constexpr int FRAME_MAX_THREADS = 768;
 constexpr int WARP_KERNEL_MAX_THREADS = 1024;
 constexpr int KERNEL_COOP = 1, KERNEL_WARP = 2;  // frame_warp_kernel: one word column per warp
-// per-group TMA staging buffer (x2, double-buffered) for an op's operand block
-constexpr int STAGE_BYTES = 8192;
 // op descriptors are copied to shared memory when they take at most this much
 constexpr int DESC_SMEM_MAX = 16384;      // distinct-position list; larger counts use selection sampling
 
@@ -47,7 +45,6 @@ constexpr int DESC_SMEM_MAX = 16384;      // distinct-position list; larger coun
 //   NOISE: count = apps, off -> targets, a = noise_row_base, b = noise ordinal,
 //          c = hit-list base, d/e = ordinal/hit-list base of the next
 //          pre-generated noise op (NO_SLOT: none), for prefetching its hits
-//   all but NOISE: d/e = TMA staging block of the op's operands (assign_staging)
 //   DET  : count = columns, a = first column (terms via det_ptr/det_terms)
 //   OBS  : count = terms, off -> record slots, a = accumulator slot
 struct DOp {
@@ -123,7 +120,6 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
 void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits);
 void reorder_for_banks(HostProgram& hp, int W);
 void dedup_operands(HostProgram& hp);
-void assign_staging(HostProgram& hp);
 
 // Kernel launch plumbing (pfs_kernels.cu)
 struct KParams {
@@ -167,7 +163,6 @@ struct KParams {
     int32_t do_dets;             // evaluate DET/OBS ops
     int32_t debug_skip;          // profiling ablations (pfs_options.debug_skip)
     int32_t groups;              // independent thread groups (tiles in flight) per CTA
-    int32_t stage;               // stage operand blocks through shared memory (TMA)
     int32_t desc_in_smem;        // op descriptors copied to shared memory
     uint32_t first_pregen;       // first pre-generated noise ordinal (NO_SLOT: none)
     uint32_t first_cap_base;
@@ -212,7 +207,12 @@ cudaError_t launch_tiles_to_b8(const uint32_t* tiles, int64_t num_rows, int W, i
 // into a ring of shared-memory slots shared by the CTA's warps.
 constexpr int KERNEL_COL = 3;
 constexpr int COL_MAX_WARPS = 15;     // consumer warps per CTA (+1 producer; 128 registers per thread)
-constexpr int COL_SLOTS = 4;          // op-block ring depth
+// one-word columns with the record ring in global memory: more, lighter warps
+constexpr int col_max_warps(int V, bool ring_smem) { return (V == 1 && !ring_smem) ? 19 : COL_MAX_WARPS; }
+#ifndef PFS_COL_SLOTS
+#define PFS_COL_SLOTS 4
+#endif
+constexpr int COL_SLOTS = PFS_COL_SLOTS;  // op-block ring depth
 constexpr uint32_t F_GLOBALP = 8u;    // block payload left in global memory (too big to stage)
 constexpr uint32_t COL_HEAD_WORDS = 8;   // block header (CHead)
 constexpr uint32_t COL_NP_WORDS = 12;    // NoiseParam after a noise op's header
@@ -263,10 +263,10 @@ struct ColParams {
     int32_t b8_aligned;          // b8 pitch and base allow 32-bit stores
 };
 
-size_t col_warp_words(int num_qubits, int64_t num_slots);
+size_t col_warp_words(int num_qubits, int64_t num_slots, bool ring_smem, int V);
 size_t col_smem_bytes(int nw, size_t warp_words, uint32_t slot_bytes, int64_t counts_words);
-cudaError_t launch_frame_col_kernel(const KParams& kp, const ColParams& cp, int grid, size_t smem,
-                                    cudaStream_t stream);
+cudaError_t launch_frame_col_kernel(const KParams& kp, const ColParams& cp, int V, bool ring_smem, int grid,
+                                    size_t smem, cudaStream_t stream);
 cudaError_t set_frame_col_kernel_smem(size_t smem);
 
 }  // namespace pfs

@@ -329,40 +329,6 @@ __global__ void __launch_bounds__(256, NZ_MIN_BLOCKS) noise_kernel(const __grid_
                      kp.hits_global + tile * kp.hit_capacity, b, e, wscr_all[warp]);
 }
 
-// Operand block of an op: static blocks (targets, uniform detector terms) come
-// precomputed in the descriptor (h1.z = aligned word offset, h1.w = valid |
-// array | word offset | 16-byte units); a pre-sampled noise op's block is this
-// tile's hit list, sized at run time.  bytes 0 = read from global memory.
-struct StageBlock { const char* src; uint32_t bytes; uint32_t woff; };
-__device__ __forceinline__ StageBlock stage_block(const KParams& kp, uint32_t kcf, uint4 h1, bool pregen,
-                                                  const uint32_t* ncnt, const uint64_t* hits) {
-    StageBlock b{nullptr, 0u, 0u};
-    if ((kcf & 0xFFu) == K_NOISE) {
-        if (pregen && ((kcf >> 16) & F_PREGEN)) {
-            const uint32_t nh = ncnt[h1.x];
-            if (nh != NO_SLOT && nh) {
-                const uintptr_t src = reinterpret_cast<uintptr_t>(hits + h1.y);
-                const uintptr_t lo = src & ~(uintptr_t)15;
-                const uint32_t sz = (uint32_t)((src + nh * 8u - lo + 15) & ~(uintptr_t)15);
-                if (sz <= (uint32_t)STAGE_BYTES) {
-                    b.src = reinterpret_cast<const char*>(lo);
-                    b.bytes = sz;
-                    b.woff = (uint32_t)((src - lo) >> 2);
-                }
-            }
-        }
-        return b;
-    }
-    const uint32_t e = h1.w;
-    if (e >> 31) {
-        const uint32_t* arr = (e & 0x40000000u) ? kp.det_terms : kp.targets;
-        b.src = reinterpret_cast<const char*>(arr + h1.z);
-        b.bytes = (e & 0xFFFFu) * 16u;
-        b.woff = (e >> 16) & 3u;
-    }
-    return b;
-}
-
 // Items of one op, U per thread per batch: all U operand loads (L2-resident
 // target indices) are issued before any of the dependent shared-memory work.
 template <int U, typename Load, typename Work>
@@ -409,41 +375,25 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     uint32_t* const cnt = smem + G * fw + (RING_SMEM ? (size_t)G * kp.num_slots * W : 0);
     uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);
     uint32_t* const ncnt = ncnt0 + grp * kp.num_noise;  // this tile's hits per op
-    // 16-byte aligned tail: per-group TMA staging buffers, mbarriers, descriptors
-    char* const tail = reinterpret_cast<char*>(
+    // 16-byte aligned tail: the op descriptors (when they fit)
+    uint4* const dsc_s = reinterpret_cast<uint4*>(
         (reinterpret_cast<uintptr_t>(ncnt0 + G * kp.num_noise) + 15) & ~(uintptr_t)15);
-    uint32_t* const stg = reinterpret_cast<uint32_t*>(tail) + (size_t)grp * 2 * (STAGE_BYTES / 4);
-    uint64_t* const mbar = reinterpret_cast<uint64_t*>(tail + (size_t)G * 2 * STAGE_BYTES) + grp * 2;
-    const uint4* const dsc = kp.desc_in_smem
-        ? reinterpret_cast<const uint4*>(tail + (size_t)G * 2 * STAGE_BYTES + G * 16)
-        : reinterpret_cast<const uint4*>(kp.ops);
+    const uint4* const dsc_g = reinterpret_cast<const uint4*>(kp.ops);
+    const bool dsm = kp.desc_in_smem != 0;
+    auto ldesc = [&](int i) -> uint4 { return dsm ? dsc_s[i] : __ldg(dsc_g + i); };
     // per-lane scratch of the inline noise sampler (large-p ops / list overflow), global
     uint32_t* const sl = kp.noise_scratch +
                          ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
     const int ss = 1;
     const bool pregen = kp.masks == nullptr && kp.num_pregen > 0 && !(kp.debug_skip & 2);
-    const bool staging = kp.stage != 0;
-    // with staging, the group's last warp is a dedicated TMA issuer: it only
-    // issues the next op's bulk copy, so its latency never delays item work
-    const int nthw = (staging && gsz >= 64) ? gsz - 32 : gsz;  // item workers
-    const int issuer = staging ? (gsz >= 64 ? gsz - 32 : 0) : -1;
     const uint32_t bar_id = 1u + (uint32_t)grp;
     auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gsz) : "memory"); };
 
     if (kp.counts_in_smem)
         for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
-    if (kp.desc_in_smem) {
-        uint4* d = const_cast<uint4*>(dsc);
-        for (int i = threadIdx.x; i < 2 * kp.n_ops; i += blockDim.x)
-            d[i] = __ldg(reinterpret_cast<const uint4*>(kp.ops) + i);
-    }
-    if (staging && tid == 0) {
-        mbar_init(mbar, 1);
-        mbar_init(mbar + 1, 1);
-        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    }
+    if (dsm)
+        for (int i = threadIdx.x; i < 2 * kp.n_ops; i += blockDim.x) dsc_s[i] = __ldg(dsc_g + i);
     __syncthreads();
-    uint32_t phase = 0;  // parity bit per staging buffer
 
     for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
         const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
@@ -490,45 +440,25 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                                      ::"l"(lo), "r"(sz) : "memory");
                     }
                 }
-            group_sync();  // counts visible, previous tile's staging buffers free
-            if (tid == issuer && kp.n_ops > 0) {
-                const StageBlock b = stage_block(kp, dsc[0].x, dsc[1], pregen, ncnt, hits);
-                if (b.bytes) bulk_load(stg, b.src, b.bytes, mbar);
-            }
+            group_sync();  // counts visible
 
-            uint4 h0 = kp.n_ops > 0 ? dsc[0] : make_uint4(0, 0, 0, 0);
+            // descriptors run one op ahead in registers
+            uint4 h0 = kp.n_ops > 0 ? ldesc(0) : make_uint4(0, 0, 0, 0);
+            uint4 h1n = kp.n_ops > 0 ? ldesc(1) : make_uint4(0, 0, 0, 0);
             for (int oi = 0; oi < kp.n_ops; oi++) {
                 const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
                 const uint32_t count = h0.y, off = h0.z, oa = h0.w;
-                const uint4 h1 = dsc[2 * oi + 1];
-                // the next op's first half (an L1/L2 load when descriptors stay global)
-                if (oi + 1 < kp.n_ops) h0 = dsc[2 * oi + 2];
+                const uint4 h1 = h1n;
+                if (oi + 1 < kp.n_ops) { h0 = ldesc(2 * oi + 2); h1n = ldesc(2 * oi + 3); }
                 const uint32_t ob = h1.x, oc = h1.y;
-                if ((flags & F_BARRIER) || staging) group_sync();
-                const uint32_t buf = (uint32_t)oi & 1u;
-                // TMA: stage the next op's operand block into the other buffer
-                // (free: every thread has passed this op's barrier)
-                if (tid == issuer && oi + 1 < kp.n_ops) {
-                    const StageBlock b = stage_block(kp, h0.x, dsc[2 * oi + 3], pregen, ncnt, hits);
-                    if (b.bytes) bulk_load(stg + (buf ^ 1u) * (STAGE_BYTES / 4), b.src, b.bytes, mbar + (buf ^ 1u));
-                }
-                // this op's operands: staged copy (wait for its bulk transaction) or global
-                const uint32_t* ops32 = nullptr;
-                if (staging) {
-                    const StageBlock b = stage_block(kp, kind | (code << 8) | (flags << 16), h1, pregen, ncnt, hits);
-                    if (b.bytes) {
-                        if (tid < nthw) mbar_wait(mbar + buf, (phase >> buf) & 1u);
-                        phase ^= 1u << buf;
-                        ops32 = stg + buf * (STAGE_BYTES / 4) + b.woff;
-                    }
-                }
+                if (flags & F_BARRIER) group_sync();
 #if PFS_PROFILE
                 if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
                     tile == 0)  // profiling: op-boundary timestamps of the first tile
                     kp.op_clock[oi] = clock64();
 #endif
-                const uint32_t* const tgg = kp.targets + off;  // global targets
-                const uint32_t* const tg = (ops32 != nullptr && kind != K_NOISE && kind != K_DET) ? ops32 : tgg;
+                const uint32_t* const tgg = kp.targets + off;  // operands (L1/L2-resident)
+                const uint32_t* const tg = tgg;
 #if PFS_PROFILE
                 if (kp.debug_skip) {
                     const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
@@ -536,8 +466,6 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     if (kp.debug_skip & bit) continue;
                 }
 #endif
-                if (tid >= nthw) continue;  // the issuer warp does no item work
-                const int nth = nthw;       // items are spread over the worker threads
                 switch (kind) {
                 case K_GATE: {
                     const int items = (int)(count << LC);
@@ -661,8 +589,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     if ((flags & F_PREGEN) && pregen) {
                         const uint32_t nh = ncnt[ob];  // NO_SLOT: the hit list overflowed
                         if (nh != NO_SLOT) {
-                            const uint64_t* hl = ops32 != nullptr ? reinterpret_cast<const uint64_t*>(ops32)
-                                                                  : hits + oc;
+                            const uint64_t* hl = hits + oc;
                             for (uint32_t i = tid; i < nh; i += nth) apply_entry<W>(X, Z, hl[i]);
                         } else {
                             const NoiseParam* npp = kp.noise + ob;
@@ -695,8 +622,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                             uint32_t e0, e1;
                             if (code) { e0 = off + ci * code; e1 = e0 + code; }
                             else { e0 = __ldg(kp.det_ptr + col); e1 = __ldg(kp.det_ptr + col + 1); }
-                            // staged uniform terms live at ops32[e - off]
-                            const uint32_t* tb = (code && ops32 != nullptr) ? ops32 - off : kp.det_terms;
+                            const uint32_t* tb = kp.det_terms;
                             const uint32_t s0 = e0 < e1 ? tb[e0] : NO_SLOT;
                             const uint32_t s1 = e0 + 1 < e1 ? tb[e0 + 1] : NO_SLOT;
                             return make_uint4(e0, e1, s0, s1);

@@ -33,7 +33,8 @@ def need_gpu():
 # word-column (kernel 3; one-word tiles, staged op-block stream), 0 = auto
 LAYOUTS = [(0, -1, 0, 0), (1, 0, 1, 1), (2, 1, 2, 1), (4, 0, 0, 1), (8, 1, 1, 1), (16, 0, 2, 1),
            (32, 1, 0, 1), (16, 0, 1, 1), (1, -1, 0, 2), (2, -1, 0, 2), (4, -1, 0, 2),
-           (16, -1, 0, 2), (32, -1, 0, 2), (0, -1, 0, 3)]
+           (16, -1, 0, 2), (32, -1, 0, 2), (0, -1, 0, 3), (1, 0, 0, 3), (2, 1, 0, 3),
+           (4, 0, 0, 3), (4, 1, 0, 3)]
 
 
 def _opts(layout):

@@ -58,7 +58,7 @@ def test_d25_layout():
     assert p.info["kernel"] == 1 and p.info["words_per_tile"] == 8
     # word-column kernel (one 32-shot word per warp, tile = 1 word)
     pc = N.NativeProgram(f, kernel=3)
-    assert pc.info["kernel"] == 3 and pc.info["words_per_tile"] == 1
+    assert pc.info["kernel"] == 3 and pc.info["words_per_tile"] in (1, 2, 4)
     assert pc.info["warps_per_cta"] >= 8 and pc.info["threads"] == 32 * (pc.info["warps_per_cta"] + 1)
     # warp-private kernel (opt-in): one 32-shot word column per warp, 8-word tiles
     pw = N.NativeProgram(f, kernel=2)

@@ -61,6 +61,18 @@ def main():
         ("prod128", {"producer_threads": 128}),
         ("prod384", {"producer_threads": 384}),
         ("thr512_prod128", {"threads": 512, "producer_threads": 128}),
+        ("no_stage", {"debug_skip": 1024}),
+        ("no_stage_no_noise", {"debug_skip": 1024 | 3}),
+        ("no_gates_collapse_dets", {"debug_skip": 8 | 16 | 32}),
+        ("noise_only", {"debug_skip": 4 | 8 | 16 | 32}),
+        ("dets_only", {"debug_skip": 1 | 2 | 4 | 16 | 32}),
+        ("gates_only", {"debug_skip": 1 | 2 | 4 | 8 | 32}),
+        ("collapse_only", {"debug_skip": 1 | 2 | 8 | 16}),
+        ("nothing", {"debug_skip": 1 | 2 | 4 | 8 | 16 | 32}),
+        ("nothing_no_stage", {"debug_skip": 1 | 2 | 4 | 8 | 16 | 32 | 1024}),
+        ("nothing_G1", {"debug_skip": 1 | 2 | 4 | 8 | 16 | 32, "groups": 1}),
+        ("nothing_256", {"debug_skip": 1 | 2 | 4 | 8 | 16 | 32, "threads": 256}),
+        ("gates_only_no_stage", {"debug_skip": 1 | 2 | 4 | 8 | 32 | 1024}),
     ]
     if a.variants:
         keep = set(a.variants.split(","))
