@@ -4,6 +4,7 @@
 
 #include <algorithm>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <new>
 #include <stdexcept>
@@ -64,7 +65,7 @@ struct pfs_program {
     DevBuf<uint32_t> d_targets, d_det_ptr, d_det_terms, d_ring;
     DevBuf<NoiseParam> d_noise;
     DevBuf<uint64_t> d_noise_tab;
-    DevBuf<uint32_t> d_pregen, d_noise_off, d_noise_ch;
+    DevBuf<uint32_t> d_pregen, d_noise_off, d_noise_ch, d_init_dead;
     DevBuf<uint64_t> d_hits;
     DevBuf<uint32_t> d_ncnt;
     DevBuf<long long> d_clock;
@@ -389,7 +390,7 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_ops.release(); pg->d_targets.release(); pg->d_det_ptr.release();
         pg->d_det_terms.release(); pg->d_ring.release(); pg->d_noise.release();
         pg->d_noise_tab.release(); pg->d_pregen.release(); pg->d_hits.release();
-        pg->d_noise_off.release(); pg->d_noise_ch.release(); pg->d_ncnt.release();
+        pg->d_noise_off.release(); pg->d_noise_ch.release(); pg->d_ncnt.release(); pg->d_init_dead.release();
         pg->d_nscratch.release(); pg->d_clock.release();
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
@@ -439,6 +440,7 @@ static int ensure_device(pfs_program* pg, int device) {
     CUDA_TRY(upload(pg->d_pregen, hp.pregen_ops));
     CUDA_TRY(upload(pg->d_noise_off, hp.noise_off));
     CUDA_TRY(upload(pg->d_noise_ch, hp.noise_ch));
+    CUDA_TRY(upload(pg->d_init_dead, hp.init_dead));
     auto grid_of = [&](const LaunchCfg& c) {
         int per_sm = pg->opts.ctas_per_sm;
         if (per_sm <= 0) {
@@ -658,6 +660,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.pregen_chunks = (int32_t)hp.pregen_chunks;
     kp.noise_off = pg->d_noise_off.p;
     kp.noise_ch = pg->d_noise_ch.p;
+    kp.init_dead = pg->d_init_dead.p;
     kp.first_pregen = hp.first_pregen;
     kp.first_cap_base = hp.first_cap_base;
 

@@ -372,16 +372,20 @@ frame_col_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Col
                 for (uint32_t kb = 0; kb < k1; kb += 32) {
                     const uint32_t k = kb + (uint32_t)lane;
                     if (k >= k1 || !coin_group_live(k, 0u, (uint32_t)n)) continue;
+                    const uint32_t live = init_live_rows(kp, k, (uint32_t)n);
                     uint32_t o[V][4];
 #pragma unroll
-                    for (int w = 0; w < V; w++) coin_group<V>(kp, k, (uint32_t)w, g, u, 0u, (uint32_t)n, o[w]);
+                    for (int w = 0; w < V; w++) {
+                        o[w][0] = o[w][1] = o[w][2] = o[w][3] = 0u;
+                        if (live) coin_group<V>(kp, k, (uint32_t)w, g, u, 0u, (uint32_t)n, o[w]);
+                    }
 #pragma unroll
                     for (int r = 0; r < 4; r++) {
                         const uint32_t e = coin_row0(k) + 32u * r;
                         if (e >= (uint32_t)n) continue;
                         VV<V> zv;
 #pragma unroll
-                        for (int w = 0; w < V; w++) zv.w[w] = o[w][r];
+                        for (int w = 0; w < V; w++) zv.w[w] = ((live >> r) & 1u) ? o[w][r] : 0u;
                         vstore<V>(X + e * V, vzero<V>());
                         vstore<V>(Z + e * V, zv);
                     }
@@ -421,6 +425,7 @@ frame_col_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Col
                             const uint32_t k = kb + (uint32_t)lane;
                             const bool kl = k < k1 && coin_group_live(k, lo, hi);
                             uint2 qsv[4];
+                            uint32_t live = 0u;
 #pragma unroll
                             for (int r = 0; r < 4; r++) {
                                 const uint32_t e = coin_row0(k) + 32u * r;
@@ -430,12 +435,15 @@ frame_col_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Col
                                 if (kind == K_R) qsv[r].x = P[rel];
                                 else if (kind == K_M || (rel & 1u))
                                     qsv[r] = reinterpret_cast<const uint2*>(P)[kind == K_MR ? rel >> 1 : rel];
+                                else continue;
+                                if (!(qsv[r].x & COIN_DEAD)) live |= 1u << r;  // dead rows: z never read
+                                qsv[r].x &= ~COIN_DEAD;
                             }
                             uint32_t o[V][4];
 #pragma unroll
                             for (int w = 0; w < V; w++) {
                                 o[w][0] = o[w][1] = o[w][2] = o[w][3] = 0u;
-                                if (kl) coin_group<V>(kp, k, (uint32_t)w, g, u, lo, hi, o[w]);
+                                if (live) coin_group<V>(kp, k, (uint32_t)w, g, u, lo, hi, o[w]);
                             }
 #pragma unroll
                             for (int r = 0; r < 4; r++) {
@@ -446,7 +454,7 @@ frame_col_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Col
                                 const uint32_t j = kind == K_MR ? rel >> 1 : rel;
                                 VV<V> cv, xv = vzero<V>();
 #pragma unroll
-                                for (int w = 0; w < V; w++) cv.w[w] = o[w][r];
+                                for (int w = 0; w < V; w++) cv.w[w] = ((live >> r) & 1u) ? o[w][r] : 0u;
                                 if (in) {
                                     const uint32_t qv = qsv[r].x * V;
                                     if (kind == K_R) {
@@ -456,7 +464,7 @@ frame_col_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Col
                                         xv = vload<V>(X + qv);
                                         if (kp.do_dets && qsv[r].y != NO_SLOT) vstore<V>(ring + (size_t)qsv[r].y * V, xv);
                                         if (kind == K_M) {
-                                            vstore<V>(Z + qv, vxor<V>(vload<V>(Z + qv), cv));
+                                            if ((live >> r) & 1u) vstore<V>(Z + qv, vxor<V>(vload<V>(Z + qv), cv));
                                         } else {
                                             vstore<V>(X + qv, vzero<V>());
                                             vstore<V>(Z + qv, cv);

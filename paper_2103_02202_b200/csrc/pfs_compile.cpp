@@ -289,6 +289,57 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
         if (uniform) o.kcf = (o.kcf & ~0xFF00u) | (k << 8);
     }
 
+    // ---- pass 2b: dead collapse coins ----
+    // A coin row sets z_q (FrameBatch.__init__, R, MR: z = coin; M: z ^= coin,
+    // frame_sim.py:36-39, 74-90).  If z_q is overwritten by a later R / MR (or
+    // the circuit ends) before any gate reads it, that coin can never reach a
+    // measurement: the kernels skip its Philox draw.  Gates conservatively count
+    // as reads of every operand; noise only XORs into z and DET/OBS touch no
+    // frame rows.  Flag = bit 31 of the M/MR/R target word (COIN_DEAD).
+    {
+        std::vector<std::vector<uint32_t>> pending(num_qubits);  // target-word indices
+        std::vector<char> init_pending(num_qubits, 1);
+        hp.init_dead.assign(((size_t)num_qubits + 31) / 32, 0u);
+        auto kill = [&](uint32_t q) {
+            for (uint32_t w : pending[q]) hp.targets[w] |= COIN_DEAD;
+            pending[q].clear();
+            if (init_pending[q]) { hp.init_dead[q >> 5] |= 1u << (q & 31); init_pending[q] = 0; }
+        };
+        for (const DOp& o : hp.ops) {
+            const uint32_t kind = o.kcf & 0xFF;
+            switch (kind) {
+            case K_GATE: {
+                const int ar = rule_arity((o.kcf >> 8) & 0xFF);
+                for (uint32_t j = 0; j < o.count * ar; j++) {
+                    const uint32_t q = hp.targets[o.off + j];
+                    pending[q].clear();
+                    init_pending[q] = 0;
+                }
+                break;
+            }
+            case K_M:
+                for (uint32_t j = 0; j < o.count; j++) pending[hp.targets[o.off + 2 * j]].push_back(o.off + 2 * j);
+                break;
+            case K_MR:
+                for (uint32_t j = 0; j < o.count; j++) {
+                    const uint32_t q = hp.targets[o.off + 2 * j];
+                    kill(q);
+                    pending[q].push_back(o.off + 2 * j);
+                }
+                break;
+            case K_R:
+                for (uint32_t j = 0; j < o.count; j++) {
+                    const uint32_t q = hp.targets[o.off + j];
+                    kill(q);
+                    pending[q].push_back(o.off + j);
+                }
+                break;
+            default: break;
+            }
+        }
+        for (int32_t q = 0; q < num_qubits; q++) kill((uint32_t)q);  // end of circuit
+    }
+
     // ---- pass 3: barrier scheduling over qubit rows + record slots ----
     const int64_t nres = (int64_t)num_qubits + hp.num_slots;
     std::vector<int64_t> rstamp(nres, -1);
@@ -306,13 +357,13 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
         }
         case K_M: case K_MR:
             for (uint32_t j = 0; j < o.count; j++) {
-                res.push_back(hp.targets[o.off + 2 * j]);
+                res.push_back(hp.targets[o.off + 2 * j] & ~COIN_DEAD);
                 uint32_t s = hp.targets[o.off + 2 * j + 1];
                 if (s != NO_SLOT) res.push_back(num_qubits + (int64_t)s);
             }
             break;
         case K_R:
-            for (uint32_t j = 0; j < o.count; j++) res.push_back(hp.targets[o.off + j]);
+            for (uint32_t j = 0; j < o.count; j++) res.push_back(hp.targets[o.off + j] & ~COIN_DEAD);
             break;
         case K_NOISE: {
             int ar = ((o.kcf >> 8) & 0xFF) == CH_DEP2 ? 2 : 1;

@@ -228,4 +228,36 @@ __device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
     return v;
 }
 
+// Dead coin rows (compiler pass 2b): rows of coin group k that some gate can
+// read.  init_live_rows: the initial z rows 0..n-1; collapse_rows also loads
+// the (qubit, slot) operands of an M / MR / R op's rows, flags stripped.
+__device__ __forceinline__ uint32_t init_live_rows(const KParams& kp, uint32_t k, uint32_t n) {
+    uint32_t live = 0;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const uint32_t e = coin_row0(k) + 32u * r;
+        if (e < n && !((__ldg(kp.init_dead + (e >> 5)) >> (e & 31u)) & 1u)) live |= 1u << r;
+    }
+    return live;
+}
+
+__device__ __forceinline__ uint32_t collapse_rows(const uint32_t* tg, uint32_t kind, uint32_t k, uint32_t lo,
+                                                  uint32_t hi, uint2 qsv[4]) {
+    uint32_t live = 0;
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+        const uint32_t e = coin_row0(k) + 32u * r;
+        qsv[r] = make_uint2(0u, NO_SLOT);
+        if (e < lo || e >= hi) continue;
+        const uint32_t rel = e - lo;
+        if (kind == K_R) qsv[r].x = tg[rel];
+        else if (kind == K_M || (rel & 1u))
+            qsv[r] = reinterpret_cast<const uint2*>(tg)[kind == K_MR ? rel >> 1 : rel];
+        else continue;  // an MR's measure coin row: never applied
+        if (!(qsv[r].x & COIN_DEAD)) live |= 1u << r;
+        qsv[r].x &= ~COIN_DEAD;
+    }
+    return live;
+}
+
 }  // namespace pfs

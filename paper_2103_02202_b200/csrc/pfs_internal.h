@@ -21,6 +21,7 @@ constexpr uint32_t F_BARRIER = 1u;   // __syncthreads() before this op
 constexpr uint32_t F_DUP = 2u;       // noise op with repeated targets
 constexpr uint32_t F_PREGEN = 4u;    // noise op whose hits come from the producer warps
 constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
+constexpr uint32_t COIN_DEAD = 0x80000000u;  // M/MR/R target word: the op's coin row is never read
 
 constexpr uint32_t DOMAIN_COIN = 0x40000000u;
 constexpr uint32_t DOMAIN_NOISE = 0x80000000u;
@@ -94,6 +95,7 @@ struct HostProgram {
     std::vector<uint32_t> targets;
     std::vector<uint32_t> det_ptr;    // [num_cols + 1] into det_terms
     std::vector<uint32_t> det_terms;  // slots
+    std::vector<uint32_t> init_dead;  // bitmap: qubits whose initial z coin is never read
     std::vector<double> noise_p;
     std::vector<uint32_t> noise_apps; // apps per noise ordinal
     std::vector<uint32_t> noise_arity;
@@ -140,6 +142,7 @@ struct KParams {
     uint32_t* ring_global;       // [grid][slots][W] when the ring is not in smem
     long long* op_clock;         // profiling: per-op clock64 of CTA 0's first tile, or null
     uint32_t* noise_scratch;     // [grid][threads][NZ_MAX_LIST] inline noise sampler scratch
+    const uint32_t* init_dead;   // bitmap of qubits whose initial coin row is dead (skip its draw)
     uint64_t* hits_global;       // [tiles][hit_capacity] pre-sampled noise hits (noise_kernel)
     uint32_t* ncnt_global;       // [tiles][num_noise] hits per noise op
     int64_t inject_words;

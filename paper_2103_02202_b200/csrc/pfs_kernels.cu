@@ -376,8 +376,10 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     uint32_t* const ncnt0 = cnt + (kp.counts_in_smem ? kp.num_cols : 0);
     uint32_t* const ncnt = ncnt0 + grp * kp.num_noise;  // this tile's hits per op
     // 16-byte aligned tail: the op descriptors (when they fit)
-    uint4* const dsc_s = reinterpret_cast<uint4*>(
-        (reinterpret_cast<uintptr_t>(ncnt0 + G * kp.num_noise) + 15) & ~(uintptr_t)15);
+    // (offset arithmetic on the shared array keeps the loads in the shared
+    // address space: LDS, not generic LD)
+    const size_t dsc_word = ((size_t)(ncnt0 + G * kp.num_noise - smem) + 3) & ~(size_t)3;
+    uint4* const dsc_s = reinterpret_cast<uint4*>(smem + dsc_word);
     const uint4* const dsc_g = reinterpret_cast<const uint4*>(kp.ops);
     const bool dsm = kp.desc_in_smem != 0;
     auto ldesc = [&](int i) -> uint4 { return dsm ? dsc_s[i] : __ldg(dsc_g + i); };
@@ -410,12 +412,13 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     const uint32_t k = (uint32_t)(i >> LC);
                     const int c = i & (C - 1);
                     if (!coin_group_live(k, 0u, (uint32_t)n)) continue;
+                    const uint32_t live = init_live_rows(kp, k, (uint32_t)n);
                     VW<V> o[4];
-                    coin_group_vec<W, V>(kp, k, c, g, tile, 0u, (uint32_t)n, o);
+                    if (live) coin_group_vec<W, V>(kp, k, c, g, tile, 0u, (uint32_t)n, o);
 #pragma unroll
                     for (int r = 0; r < 4; r++) {
                         const uint32_t e = coin_row0(k) + 32u * r;
-                        if (e < (uint32_t)n) vst<V>(Z + (size_t)e * W + c * V, o[r]);
+                        if (e < (uint32_t)n) vst<V>(Z + (size_t)e * W + c * V, ((live >> r) & 1u) ? o[r] : vzero<V>());
                     }
                 }
             }
@@ -524,27 +527,19 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                         const int c = i & (C - 1);
                         if (!coin_group_live(k, lo, hi)) continue;
                         uint2 qsv[4];  // operands load while the coin blocks compute
-#pragma unroll
-                        for (int r = 0; r < 4; r++) {
-                            const uint32_t e = coin_row0(k) + 32u * r;
-                            qsv[r] = make_uint2(0u, NO_SLOT);
-                            if (e < lo || e >= hi) continue;
-                            const uint32_t rel = e - lo;
-                            if (kind == K_R) qsv[r].x = tg[rel];
-                            else if (kind == K_M || (rel & 1u))
-                                qsv[r] = reinterpret_cast<const uint2*>(tg)[kind == K_MR ? rel >> 1 : rel];
-                        }
+                        const uint32_t live = collapse_rows(tg, kind, k, lo, hi, qsv);
                         VW<V> o[4];
-                        coin_group_vec<W, V>(kp, k, c, g, tile, lo, hi, o);
+                        if (live) coin_group_vec<W, V>(kp, k, c, g, tile, lo, hi, o);
 #pragma unroll
                         for (int r = 0; r < 4; r++) {
                             const uint32_t e = coin_row0(k) + 32u * r;
                             if (e < lo || e >= hi) continue;
                             const uint32_t rel = e - lo;
+                            const bool lv = (live >> r) & 1u;  // dead coin rows: z is never read
                             const size_t p = (size_t)qsv[r].x * W + c * V;
                             if (kind == K_R) {
                                 vst<V>(X + p, vzero<V>());
-                                vst<V>(Z + p, o[r]);
+                                vst<V>(Z + p, lv ? o[r] : vzero<V>());
                                 continue;
                             }
                             if (kind == K_MR && !(rel & 1u)) continue;  // the measure's coin row is overwritten
@@ -554,10 +549,10 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                             if (kp.rec_out != nullptr)
                                 vst<V>(kp.rec_out + (int64_t)(oa + j) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, xv);
                             if (kind == K_M) {
-                                vst<V>(Z + p, vxor<V>(vld<V>(Z + p), o[r]));
+                                if (lv) vst<V>(Z + p, vxor<V>(vld<V>(Z + p), o[r]));
                             } else {
                                 vst<V>(X + p, vzero<V>());
-                                vst<V>(Z + p, o[r]);
+                                vst<V>(Z + p, lv ? o[r] : vzero<V>());
                             }
                         }
                     }
@@ -633,8 +628,9 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                             VW<V> acc = vzero<V>();
                             if (d.z != NO_SLOT) acc = vld<V>(ring + (size_t)d.z * W + c * V);
                             if (d.w != NO_SLOT) acc = vxor<V>(acc, vld<V>(ring + (size_t)d.w * W + c * V));
+                            const uint32_t* tb = kp.det_terms;
                             for (uint32_t e = d.x + 2; e < d.y; e++) {
-                                const uint32_t s = __ldg(kp.det_terms + e);
+                                const uint32_t s = tb[e];
                                 acc = vxor<V>(acc, vld<V>(ring + (size_t)s * W + c * V));
                             }
                             if (kp.ev_out != nullptr)
@@ -739,12 +735,13 @@ __global__ void __launch_bounds__(WARP_KERNEL_MAX_THREADS, 1) frame_warp_kernel(
         const int64_t obase = tile * kp.out_tile_stride + (int64_t)w * kp.out_word_stride;
         // ---- FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39) ----
         for (uint32_t k = (uint32_t)lane; k < coin_k1((uint32_t)n); k += 32) {
-            uint32_t o[4];
-            coin_group<W>(kp, k, w, g, tile, 0u, (uint32_t)n, o);
+            const uint32_t live = init_live_rows(kp, k, (uint32_t)n);
+            uint32_t o[4] = {0u, 0u, 0u, 0u};
+            if (live) coin_group<W>(kp, k, w, g, tile, 0u, (uint32_t)n, o);
 #pragma unroll
             for (int r = 0; r < 4; r++) {
                 const uint32_t e = coin_row0(k) + 32u * r;
-                if (e < (uint32_t)n) XZ[e] = make_uint2(0u, o[r]);
+                if (e < (uint32_t)n) XZ[e] = make_uint2(0u, ((live >> r) & 1u) ? o[r] : 0u);
             }
         }
         for (int i = lane; i < kp.num_obs; i += 32) ring[i] = 0u;
@@ -846,32 +843,24 @@ __global__ void __launch_bounds__(WARP_KERNEL_MAX_THREADS, 1) frame_warp_kernel(
                     if (!coin_group_live(k, lo, hi)) continue;
                     // the four rows' operands load while the coin block computes
                     uint2 qsv[4];
-#pragma unroll
-                    for (int r = 0; r < 4; r++) {
-                        const uint32_t e = coin_row0(k) + 32u * r;
-                        qsv[r] = make_uint2(0u, NO_SLOT);
-                        if (e < lo || e >= hi) continue;
-                        const uint32_t rel = e - lo;
-                        if (kind == K_R) qsv[r].x = __ldg(tg + rel);
-                        else if (kind == K_M || (rel & 1u))
-                            qsv[r] = __ldg(reinterpret_cast<const uint2*>(tg) + (kind == K_MR ? rel >> 1 : rel));
-                    }
-                    uint32_t o[4];
-                    coin_group<W>(kp, k, w, g, tile, lo, hi, o);
+                    const uint32_t live = collapse_rows(tg, kind, k, lo, hi, qsv);
+                    uint32_t o[4] = {0u, 0u, 0u, 0u};
+                    if (live) coin_group<W>(kp, k, w, g, tile, lo, hi, o);
 #pragma unroll
                     for (int r = 0; r < 4; r++) {
                         const uint32_t e = coin_row0(k) + 32u * r;
                         if (e < lo || e >= hi) continue;
                         const uint32_t rel = e - lo;
-                        if (kind == K_R) { XZ[qsv[r].x] = make_uint2(0u, o[r]); continue; }
+                        const uint32_t cv = ((live >> r) & 1u) ? o[r] : 0u;  // dead rows: z never read
+                        if (kind == K_R) { XZ[qsv[r].x] = make_uint2(0u, cv); continue; }
                         if (kind == K_MR && !(rel & 1u)) continue;  // the measure's coin row is overwritten
                         const uint32_t j = kind == K_MR ? rel >> 1 : rel;
                         const uint2 qs = qsv[r];
                         const uint32_t xv = xz[2 * qs.x];
                         if (kp.do_dets && qs.y != NO_SLOT) ring[qs.y] = xv;
                         if (kp.rec_out != nullptr) kp.rec_out[obase + (int64_t)(oa + j) * kp.out_row_stride] = xv;
-                        if (kind == K_M) xz[2 * qs.x + 1] ^= o[r];
-                        else XZ[qs.x] = make_uint2(0u, o[r]);
+                        if (kind == K_M) xz[2 * qs.x + 1] ^= cv;
+                        else XZ[qs.x] = make_uint2(0u, cv);
                     }
                 }
                 break;
