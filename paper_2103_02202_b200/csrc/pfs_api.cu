@@ -65,7 +65,7 @@ struct pfs_program {
     DevBuf<uint32_t> d_targets, d_det_ptr, d_det_terms, d_ring;
     DevBuf<NoiseParam> d_noise;
     DevBuf<uint64_t> d_noise_tab;
-    DevBuf<uint32_t> d_pregen, d_noise_off, d_noise_ch, d_init_dead;
+    DevBuf<uint32_t> d_pregen, d_noise_off, d_noise_ch, d_init_dead, d_row_of;
     DevBuf<uint64_t> d_hits;
     DevBuf<uint32_t> d_ncnt;
     DevBuf<long long> d_clock;
@@ -313,6 +313,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
     const double th = pg->opts.noise_target_hits > 0 ? pg->opts.noise_target_hits : 1.0;
     try {
         // warp kernel: 8-byte x/z rows, 16 lanes per shared-memory wavefront
+        permute_rows(pg->hp);
         reorder_for_banks(pg->hp, pg->wcfg.kernel ? 2 : pg->cfg.W);
         dedup_operands(pg->hp);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
@@ -391,6 +392,7 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_det_terms.release(); pg->d_ring.release(); pg->d_noise.release();
         pg->d_noise_tab.release(); pg->d_pregen.release(); pg->d_hits.release();
         pg->d_noise_off.release(); pg->d_noise_ch.release(); pg->d_ncnt.release(); pg->d_init_dead.release();
+        pg->d_row_of.release();
         pg->d_nscratch.release(); pg->d_clock.release();
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
@@ -441,6 +443,7 @@ static int ensure_device(pfs_program* pg, int device) {
     CUDA_TRY(upload(pg->d_noise_off, hp.noise_off));
     CUDA_TRY(upload(pg->d_noise_ch, hp.noise_ch));
     CUDA_TRY(upload(pg->d_init_dead, hp.init_dead));
+    CUDA_TRY(upload(pg->d_row_of, hp.row_of));
     auto grid_of = [&](const LaunchCfg& c) {
         int per_sm = pg->opts.ctas_per_sm;
         if (per_sm <= 0) {
@@ -661,6 +664,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.noise_off = pg->d_noise_off.p;
     kp.noise_ch = pg->d_noise_ch.p;
     kp.init_dead = pg->d_init_dead.p;
+    kp.row_of = pg->d_row_of.p;
     kp.first_pregen = hp.first_pregen;
     kp.first_cap_base = hp.first_cap_base;
 

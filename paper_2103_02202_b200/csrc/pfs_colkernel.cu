@@ -386,8 +386,9 @@ frame_col_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Col
                         VV<V> zv;
 #pragma unroll
                         for (int w = 0; w < V; w++) zv.w[w] = ((live >> r) & 1u) ? o[w][r] : 0u;
-                        vstore<V>(X + e * V, vzero<V>());
-                        vstore<V>(Z + e * V, zv);
+                        const uint32_t row = __ldg(kp.row_of + e);  // qubit e's frame row
+                        vstore<V>(X + row * V, vzero<V>());
+                        vstore<V>(Z + row * V, zv);
                     }
                 }
                 for (int i = lane; i < kp.num_obs; i += 32) vstore<V>(ring + (size_t)i * V, vzero<V>());

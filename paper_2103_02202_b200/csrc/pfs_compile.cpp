@@ -390,10 +390,48 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     return hp;
 }
 
+// Frame-row placement.  Which shared-memory row holds qubit q is free (the
+// kernels only ever address rows through the op targets), so rows follow a
+// fixed pseudo-random permutation: circuit generators number qubits in
+// lattice patterns whose residues mod the bank-group count are badly
+// unbalanced (d=25 CX layers: controls mod 4 = {231, 75, 219, 75}), which no
+// reordering of one layer can make conflict-free.  row_of[q] = row of qubit q.
+void permute_rows(HostProgram& hp) {
+    const uint32_t n = (uint32_t)hp.num_qubits;
+    hp.row_of.resize(n);
+    for (uint32_t q = 0; q < n; q++) hp.row_of[q] = q;
+    uint64_t st = 0x9E3779B97F4A7C15ull ^ n;
+    for (uint32_t i = n; i > 1; i--) {  // Fisher-Yates with splitmix64
+        st += 0x9E3779B97F4A7C15ull;
+        uint64_t z = st;
+        z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+        z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+        z ^= z >> 31;
+        std::swap(hp.row_of[i - 1], hp.row_of[z % i]);
+    }
+    auto map = [&](uint32_t& w) { w = hp.row_of[w & ~COIN_DEAD] | (w & COIN_DEAD); };
+    for (const DOp& o : hp.ops) {
+        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
+        uint32_t* t = hp.targets.data() + o.off;
+        switch (kind) {
+            case K_GATE: for (uint32_t j = 0; j < o.count * rule_arity(code); j++) map(t[j]); break;
+            case K_M: case K_MR: for (uint32_t j = 0; j < o.count; j++) map(t[2 * j]); break;
+            case K_R: for (uint32_t j = 0; j < o.count; j++) map(t[j]); break;
+            case K_NOISE:
+                for (uint32_t j = 0; j < o.count * (code == CH_DEP2 ? 2u : 1u); j++) map(t[j]);
+                break;
+            default: break;
+        }
+    }
+}
+
 // Reorder the applications of every gate op so each aligned group of G
 // consecutive applications (the apps one shared-memory wavefront serves: G =
-// 128 B / row bytes) touches G distinct bank groups per operand.  Apps of one
-// op are independent by construction, so any order is the same circuit.
+// 128 B / row bytes) touches G distinct bank groups per operand: apps are
+// classed by (first, second) operand residue mod G and each group takes one
+// app per first residue, choosing among the second residues still unused the
+// fullest class.  Apps of one op are independent by construction, so any
+// order is the same circuit.
 void reorder_for_banks(HostProgram& hp, int W) {
     const int G = W >= 32 ? 1 : 128 / (W * 4);
     if (G <= 1) return;
@@ -403,33 +441,40 @@ void reorder_for_banks(HostProgram& hp, int W) {
         const int ar = rule_arity((o.kcf >> 8) & 0xFF);
         const uint32_t A = o.count;
         uint32_t* tg = hp.targets.data() + o.off;
-        // buckets of app indices by first-operand residue
-        std::vector<std::vector<uint32_t>> bucket(G);
-        for (uint32_t a = 0; a < A; a++) bucket[tg[a * ar] % G].push_back(a);
-        std::vector<size_t> head(G, 0);
+        const int G2 = ar == 2 ? G : 1;
+        std::vector<std::vector<uint32_t>> cls((size_t)G * G2);
+        std::vector<uint32_t> rem0(G, 0);
+        for (uint32_t a = 0; a < A; a++) {
+            const uint32_t r0 = tg[a * ar] % G, r1 = ar == 2 ? tg[a * ar + 1] % G : 0;
+            cls[(size_t)r0 * G2 + r1].push_back(a);
+            rem0[r0]++;
+        }
         scratch.clear();
         scratch.reserve((size_t)A * ar);
         uint32_t left = A;
-        std::vector<char> used1(G);
+        std::vector<char> used1(G2);
+        std::vector<int> order(G);
         while (left) {
             std::fill(used1.begin(), used1.end(), 0);
-            int taken = 0;
-            for (int r = 0; r < G && left; r++) {
-                auto& b = bucket[r];
-                if (head[r] >= b.size()) continue;
-                size_t pick = head[r];
-                if (ar == 2) {  // prefer an app whose second operand residue is unused
-                    for (size_t k = head[r]; k < b.size() && k < head[r] + 8; k++)
-                        if (!used1[tg[b[k] * 2 + 1] % G]) { pick = k; break; }
-                    std::swap(b[head[r]], b[pick]);
-                    used1[tg[b[head[r]] * 2 + 1] % G] = 1;
+            // fullest first residues first: they are the ones that run out last
+            for (int r = 0; r < G; r++) order[r] = r;
+            std::sort(order.begin(), order.end(), [&](int x, int y) { return rem0[x] > rem0[y]; });
+            for (int r0 : order) {
+                if (!rem0[r0] || !left) continue;
+                int best = -1;
+                for (int r1 = 0; r1 < G2; r1++) {
+                    const size_t c = cls[(size_t)r0 * G2 + r1].size();
+                    if (!c) continue;
+                    if (best < 0 || (!used1[r1] && (used1[best] || c > cls[(size_t)r0 * G2 + best].size()))) best = r1;
                 }
-                const uint32_t a = b[head[r]++];
+                auto& v = cls[(size_t)r0 * G2 + best];
+                const uint32_t a = v.back();
+                v.pop_back();
+                rem0[r0]--;
+                used1[best] = 1;
                 for (int s2 = 0; s2 < ar; s2++) scratch.push_back(tg[a * ar + s2]);
                 left--;
-                taken++;
             }
-            (void)taken;
         }
         std::copy(scratch.begin(), scratch.end(), tg);
     }

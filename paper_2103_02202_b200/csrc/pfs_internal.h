@@ -96,6 +96,7 @@ struct HostProgram {
     std::vector<uint32_t> det_ptr;    // [num_cols + 1] into det_terms
     std::vector<uint32_t> det_terms;  // slots
     std::vector<uint32_t> init_dead;  // bitmap: qubits whose initial z coin is never read
+    std::vector<uint32_t> row_of;     // frame row of each qubit (permute_rows)
     std::vector<double> noise_p;
     std::vector<uint32_t> noise_apps; // apps per noise ordinal
     std::vector<uint32_t> noise_arity;
@@ -120,6 +121,7 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
                             int64_t num_coin_rows, int64_t num_noise_rows);
 
 void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits);
+void permute_rows(HostProgram& hp);
 void reorder_for_banks(HostProgram& hp, int W);
 void dedup_operands(HostProgram& hp);
 
@@ -143,6 +145,7 @@ struct KParams {
     long long* op_clock;         // profiling: per-op clock64 of CTA 0's first tile, or null
     uint32_t* noise_scratch;     // [grid][threads][NZ_MAX_LIST] inline noise sampler scratch
     const uint32_t* init_dead;   // bitmap of qubits whose initial coin row is dead (skip its draw)
+    const uint32_t* row_of;      // frame row of qubit q (initial coin row q goes to z row row_of[q])
     uint64_t* hits_global;       // [tiles][hit_capacity] pre-sampled noise hits (noise_kernel)
     uint32_t* ncnt_global;       // [tiles][num_noise] hits per noise op
     int64_t inject_words;

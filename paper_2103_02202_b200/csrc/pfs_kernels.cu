@@ -418,7 +418,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
 #pragma unroll
                     for (int r = 0; r < 4; r++) {
                         const uint32_t e = coin_row0(k) + 32u * r;
-                        if (e < (uint32_t)n) vst<V>(Z + (size_t)e * W + c * V, ((live >> r) & 1u) ? o[r] : vzero<V>());
+                        if (e < (uint32_t)n)  // coin row e is qubit e's initial z (frame_sim.py:38-39)
+                            vst<V>(Z + (size_t)__ldg(kp.row_of + e) * W + c * V, ((live >> r) & 1u) ? o[r] : vzero<V>());
                     }
                 }
             }
@@ -741,7 +742,7 @@ __global__ void __launch_bounds__(WARP_KERNEL_MAX_THREADS, 1) frame_warp_kernel(
 #pragma unroll
             for (int r = 0; r < 4; r++) {
                 const uint32_t e = coin_row0(k) + 32u * r;
-                if (e < (uint32_t)n) XZ[e] = make_uint2(0u, ((live >> r) & 1u) ? o[r] : 0u);
+                if (e < (uint32_t)n) XZ[__ldg(kp.row_of + e)] = make_uint2(0u, ((live >> r) & 1u) ? o[r] : 0u);
             }
         }
         for (int i = lane; i < kp.num_obs; i += 32) ring[i] = 0u;
