@@ -74,7 +74,7 @@ typedef struct {
 } orc_noise;
 #define NZ_NONE 1u
 #define NZ_ALL 2u
-#define NZ_MAX_LIST 8
+#define NZ_MAX_LIST 16
 
 typedef struct {
     const orc_instr* ins; int64_t n_ins;

@@ -128,7 +128,7 @@ __device__ __forceinline__ void sink_put(const ColParams& cp, Sink<V>& sk, bool 
 // hits are compacted across lanes (prefix sum) and each lane produces one hit
 // position per round.  A chunk whose positions collide, or whose count exceeds
 // NZ_MAX_LIST, is redrawn serially by noise_chunk — so the hits are exactly
-// noise_chunk's for every chunk.  wscr: 256 words of per-warp shared scratch.
+// noise_chunk's for every chunk.  wscr: 32 NZ_MAX_LIST words of per-warp shared scratch.
 template <typename Apply>
 __device__ __forceinline__ void noise_op_warp(const KParams& kp, const NoiseParam& np, uint32_t ordinal,
                                               uint32_t g, uint32_t* wscr, uint32_t* sl, int lane,
@@ -609,7 +609,8 @@ frame_col_kernel(const __grid_constant__ KParams kp, const __grid_constant__ Col
 }
 
 size_t col_warp_words(int num_qubits, int64_t num_slots, bool ring_smem, int V) {
-    return ((size_t)V * (2 * (size_t)num_qubits + (ring_smem ? (size_t)num_slots : 0) + 64) + 256 + 3) & ~(size_t)3;
+    return ((size_t)V * (2 * (size_t)num_qubits + (ring_smem ? (size_t)num_slots : 0) + 64) + 32 * NZ_MAX_LIST + 3) &
+           ~(size_t)3;
 }
 
 size_t col_smem_bytes(int nw, size_t warp_words, uint32_t slot_bytes, int64_t counts_words) {

@@ -30,7 +30,7 @@ constexpr uint32_t DOMAIN_NOISE = 0x80000000u;
 constexpr uint32_t NZ_NONE = 1u;     // p == 0: no hits
 constexpr uint32_t NZ_ALL = 2u;      // p == 1: every trial hits
 constexpr uint32_t NZ_PREGEN = 4u;   // hits generated in the tile's pre-pass into a hit list
-constexpr int NZ_MAX_LIST = 8;
+constexpr int NZ_MAX_LIST = 16;
 // frame kernel CTA size cap (launch bounds): 768 threads leaves 85 registers per
 // thread, enough for the noise sampler without spills
 constexpr int FRAME_MAX_THREADS = 768;

@@ -260,14 +260,12 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
         __syncwarp();
         // duplicate positions within a chunk (probability ~count^2 / 2L)
         bool dup = false;
-        if (c > 1) {
-            for (uint32_t h = 1; h < c; h++)
-                for (uint32_t q = 0; q < h; q++) dup |= wscr[excl + h] == wscr[excl + q];
-        }
+        for (uint32_t h = 1; h < c; h++)
+            for (uint32_t q = 0; q < h; q++) dup |= wscr[excl + h] == wscr[excl + q];
         __syncwarp();
         if (dup) {  // redraw every position of this chunk (attempts >= 1), same slots
             const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
-            uint32_t* sl = wscr + 256 + lane * NZ_MAX_LIST;
+            uint32_t* sl = wscr + 32 * NZ_MAX_LIST + lane * NZ_MAX_LIST;
             for (uint32_t attempt = 1; dup; attempt++) {
                 dup = false;
                 uint32_t blk = 0xFFFFFFFFu, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
@@ -318,7 +316,7 @@ constexpr int NZ_ITEMS_PER_WARP = 4;
 #endif
 template <int W>
 __global__ void __launch_bounds__(256, NZ_MIN_BLOCKS) noise_kernel(const __grid_constant__ KParams kp) {
-    __shared__ uint32_t wscr_all[8][256 + 32 * NZ_MAX_LIST];
+    __shared__ uint32_t wscr_all[8][64 * NZ_MAX_LIST];
     const int warp = threadIdx.x >> 5;
     const int64_t tile = blockIdx.y;
     const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
