@@ -171,6 +171,26 @@ void pfs_program_destroy(struct pfs_program* prog);
 const char* pfs_last_error(void);
 int pfs_version(void);
 
+/* ---- native reference sample (stabsim/tableau_sim.py:326-329) ----------
+ * Noiseless inverse-tableau simulation of a circuit lowered to rows
+ * (gate code, n_targets, target offset) x int32; noise and annotations are
+ * dropped by the caller.  Random measurement / reset collapses consume one
+ * coin each from `coins`, in circuit order (the reference draws
+ * rng.integers(2) per collapse, tableau_sim.py:177).  Writes one bit per
+ * measurement to out_bits and, when non-null, 1/0 to out_determined
+ * (SimState.determined_record).  Host-only: needs no GPU. */
+enum pfs_tableau_gate {
+    PFS_TG_I = 0, PFS_TG_X = 1, PFS_TG_Y = 2, PFS_TG_Z = 3, PFS_TG_H = 4, PFS_TG_S = 5,
+    PFS_TG_S_DAG = 6, PFS_TG_SQRT_X = 7, PFS_TG_SQRT_X_DAG = 8, PFS_TG_SQRT_Y = 9,
+    PFS_TG_SQRT_Y_DAG = 10, PFS_TG_CX = 11, PFS_TG_CY = 12, PFS_TG_CZ = 13, PFS_TG_SWAP = 14,
+    PFS_TG_M = 15, PFS_TG_R = 16, PFS_TG_MR = 17
+};
+int pfs_reference_sample(const int32_t* ops, int64_t n_ops, const int32_t* targets,
+                         int64_t n_targets, int32_t num_qubits, const uint8_t* coins,
+                         int64_t n_coins, uint8_t* out_bits, uint8_t* out_determined,
+                         int64_t n_out, int64_t* n_written);
+const char* pfs_reference_sample_error(void);
+
 #ifdef __cplusplus
 }
 #endif

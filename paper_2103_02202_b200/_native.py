@@ -56,7 +56,8 @@ class Info(ctypes.Structure):
 EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_schedule", "pfs_run",
            "pfs_program_last_timing", "pfs_program_last_launches", "pfs_program_destroy",
            "pfs_last_error", "pfs_version", "pfs_measure_smem_bandwidth",
-           "pfs_detector_events", "pfs_program_op_clock", "pfs_program_ops")
+           "pfs_detector_events", "pfs_program_op_clock", "pfs_program_ops",
+           "pfs_reference_sample", "pfs_reference_sample_error")
 
 _lib = None
 
@@ -95,6 +96,10 @@ def lib():
     L.pfs_program_op_clock.restype = ctypes.c_int
     L.pfs_program_ops.argtypes = [P, P, i64]
     L.pfs_program_ops.restype = ctypes.c_int
+    L.pfs_reference_sample.argtypes = [P, i64, P, i64, i32, P, i64, P, P, i64, ctypes.POINTER(i64)]
+    L.pfs_reference_sample.restype = ctypes.c_int
+    L.pfs_reference_sample_error.argtypes = []
+    L.pfs_reference_sample_error.restype = ctypes.c_char_p
     L.pfs_version.argtypes = []
     L.pfs_version.restype = ctypes.c_int
     _lib = L

@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libpfs.so")
 PROFILE_LIB = os.path.join(LIB_DIR, "libpfs_profile.so")  # PFS_PROFILE=1: traces, ablations
-SOURCES = ["pfs_compile.cpp", "pfs_kernels.cu", "pfs_colkernel.cu", "pfs_api.cu"]
+SOURCES = ["pfs_compile.cpp", "pfs_tableau.cpp", "pfs_kernels.cu", "pfs_colkernel.cu", "pfs_api.cu"]
 HEADERS = ["pfs_internal.h", "pfs_device.cuh", os.path.join("..", "..", "include", "pfs.h")]
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -50,14 +50,14 @@ def build(force: bool = False, verbose: bool = False, profile: bool = False,
     os.makedirs(LIB_DIR, exist_ok=True)
     tmp = lib + ".tmp"
     cmd = [nvcc(), *ARCH, "-O3", "-lineinfo", "-std=c++17", "--threads", "0",
-           "-Xcompiler", "-fPIC,-O3", "-shared", "-I", INCLUDE, "-o", tmp]
+           "-Xcompiler", "-fPIC,-O3,-fopenmp", "-shared", "-I", INCLUDE, "-o", tmp]
     if profile:
         cmd += ["-DPFS_PROFILE=1"]
     cmd += [f"-D{d}" for d in defines]
     if verbose:
         cmd += ["-Xptxas", "-v"]
     cmd += [os.path.join(csrc, f) for f in SOURCES]
-    cmd += ["-lcudart"]
+    cmd += ["-lcudart", "-lgomp"]
     res = subprocess.run(cmd, capture_output=True, text=True)
     if res.returncode != 0:
         raise RuntimeError(f"nvcc failed ({res.returncode}):\n{res.stdout}\n{res.stderr}")

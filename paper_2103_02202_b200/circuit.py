@@ -372,8 +372,8 @@ def as_circuit(circuit_or_text) -> Circuit:
 def to_reference_dialect(circuit) -> str:
     """Lower superset text to the reference dialect.
 
-    TICK is dropped; SQRT_X -> H S H and SQRT_X_DAG -> H S_DAG H (same frame
-    rule x ^= z); OBSERVABLE_INCLUDE is removed and each observable becomes one
+    TICK is dropped; SQRT_X -> H S H and SQRT_X_DAG -> H S_DAG H per target
+    (same frame rule x ^= z, same tableau); OBSERVABLE_INCLUDE is removed and each observable becomes one
     trailing DETECTOR whose lookbacks are relative to the end of the circuit.
     """
     circuit = as_circuit(circuit)
@@ -394,10 +394,12 @@ def to_reference_dialect(circuit) -> str:
                 continue
             if name in ("SQRT_X", "SQRT_X_DAG"):
                 mid = "S" if name == "SQRT_X" else "S_DAG"
-                tg = " ".join(str(t) for t in e.targets)
-                out.append(f"{pad}H {tg}")
-                out.append(f"{pad}{mid} {tg}")
-                out.append(f"{pad}H {tg}")
+                # per target, in order: a repeated target (SQRT_X 2 2) must
+                # stay two sequential SQRT_X, which H 2 2 / S 2 2 / H 2 2 is not
+                for t in e.targets:
+                    out.append(f"{pad}H {t}")
+                    out.append(f"{pad}{mid} {t}")
+                    out.append(f"{pad}H {t}")
                 continue
             assert name in REFERENCE_GATE_NAMES, name
             out.append(pad + str(e))

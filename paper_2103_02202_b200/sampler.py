@@ -165,10 +165,13 @@ class MeasurementSampler(_Compiled):
 
     def sample(self, shots: int, *, seed=None, out=None, shot_offset: int = 0, coins=None,
                masks=None, stream: int = 0):
-        """Shot-major b8 measurement samples (needs the reference sample)."""
+        """Shot-major b8 measurement samples (flips XOR the reference sample;
+        without one, the native inverse-tableau reference sample is computed
+        once, as the paper's compile_sampler does)."""
         if self.reference is None:
-            raise ValueError("measurement sampling needs a reference sample "
-                             "(compile_sampler(circuit, reference=...))")
+            from .tableau_sim import reference_sample
+            ref = reference_sample(self.circuit, np.random.default_rng(self._seeds.integers(2 ** 63)))
+            self.reference = np.ascontiguousarray(np.asarray(ref, dtype=np.uint8))
         return self._run_b8(N.MODE_SAMPLES, self.num_measurements, shots, seed, out,
                             shot_offset, ref=self.reference, coins=coins, masks=masks,
                             stream=stream)

@@ -23,6 +23,10 @@ Fixtures (all derived from `stabsim` at /root/reference/pkg/src):
                         `collect_flips` + `detector_events` (reference RNG).
 * exact_*.json       — `oracle.enumerate_distribution` of tiny noisy circuits
                         with the reference sample used to sample them.
+* refsample_*.npz    — `tableau_sim.SimState.run(skip_noise=True)` (the body of
+                        `reference_sample`, tableau_sim.py:326-329) driven by a
+                        supplied collapse-coin stream: circuit text, coins,
+                        measurement bits and `determined_record`.
 """
 
 from __future__ import annotations
@@ -354,6 +358,46 @@ def gen_exact():
     print("exact_tiny.json", len(out))
 
 
+class _CoinStream:
+    """Stands in for the numpy Generator of SimState: `integers(2)` returns
+    the next supplied coin (one per random collapse, tableau_sim.py:177)."""
+
+    def __init__(self, coins):
+        self.coins = coins
+        self.k = 0
+
+    def integers(self, n, *a, **kw):
+        assert n == 2, n
+        c = int(self.coins[self.k])
+        self.k += 1
+        return c
+
+
+def refsample_cases():
+    cases = [("d3", gen.surface_code_memory(3, 3, 1e-3)),
+             ("d5", gen.surface_code_memory(5, 5, 5e-3)),
+             ("d9", gen.surface_code_memory(9, 4, 1e-3)),
+             ("c1", gen.random_clifford(64, 200, 0.01, 0)),
+             ("c1b", gen.random_clifford(24, 60, 0.0, 3))]
+    cases += [(name, text) for name, text, _, _, _ in mixed_cases()]
+    return cases
+
+
+def gen_refsample():
+    _, rcircuit, _, _, _, _, tableau_sim = _ref()
+    for i, (name, text) in enumerate(refsample_cases()):
+        rc = rcircuit.parse(mc.to_reference_dialect(text))
+        n_coll = sum(len(ins.targets) for ins in rcircuit.iter_flat(rc)
+                     if ins.gate.name in ("M", "R", "MR"))
+        coins = np.random.default_rng(300 + i).integers(0, 2, size=max(n_coll, 1), dtype=np.uint8)
+        st = tableau_sim.SimState(rc.num_qubits, rng=_CoinStream(coins))
+        bits = st.run(rc, skip_noise=True)
+        np.savez_compressed(os.path.join(HERE, f"refsample_{name}.npz"), text=np.array(text),
+                            coins=coins, used=st.rng.k, bits=np.array(bits, dtype=np.uint8),
+                            determined=np.array(st.determined_record, dtype=np.uint8))
+        print(f"refsample {name}: M={len(bits)} collapses={st.rng.k}", flush=True)
+
+
 if __name__ == "__main__":
     if len(sys.argv) == 3 and sys.argv[1] == "_statjob":
         import pickle
@@ -362,7 +406,9 @@ if __name__ == "__main__":
         with open(sys.argv[2] + ".out", "wb") as f:
             pickle.dump(_stat_worker(job), f)
         sys.exit(0)
-    which = set(sys.argv[1:]) or {"plans", "inject", "noiseless", "stats", "exact"}
+    which = set(sys.argv[1:]) or {"plans", "inject", "noiseless", "stats", "exact", "refsample"}
+    if "refsample" in which:
+        gen_refsample()
     if "plans" in which:
         gen_frame_plans()
     if "exact" in which:

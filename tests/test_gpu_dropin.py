@@ -81,3 +81,24 @@ def test_reference_circuit_objects_accepted():
     c = rc.parse("H 0\nCNOT 0 1\nM 0 1\nDETECTOR rec[-1] rec[-2]\n")
     ev = frame_sim.sample_detection_events(c, 500, np.random.default_rng(0))
     assert not ev.to_numpy().any()
+
+
+def test_compile_sampler_native_reference():
+    # compile_sampler without a reference computes the native inverse-tableau
+    # reference sample (tableau_sim.py): noiseless samples equal it at every
+    # deterministic measurement, and every detector parity vanishes
+    from paper_2103_02202_b200 import generators as gen
+    from paper_2103_02202_b200 import tableau_sim as T
+    from paper_2103_02202_b200.circuit import as_circuit, detector_sets
+    from paper_2103_02202_b200.sampler import compile_sampler
+
+    text = gen.surface_code_memory(5, 5, 0.0)
+    c = as_circuit(text)
+    s = compile_sampler(c, seed=3)
+    smp = b8_unpack(s.sample(2048, seed=9), c.num_measurements)
+    ref = s.reference
+    _, det, _ = T.reference_sample_with_coins(c, np.zeros(c.num_measurements, np.uint8))
+    d = det.astype(bool)
+    assert np.all(smp[:, d] == ref[d][None, :])
+    for ds in detector_sets(c):
+        assert not np.any(smp[:, list(ds)].sum(axis=1) % 2)
