@@ -374,6 +374,7 @@ def run_ours(args, rank, world, local_rank):
              "value": extra["value"], "unit": "shots/s", "shots_per_gpu_per_step": extra["shots"],
              "ms_per_step": 1e3 * extra["elapsed"] / extra["steps"], "steps": extra["steps"],
              "host_compile_s": extra["compile_s"],
+             "host_reference_sample_s": reference_sample_seconds(config_text(4)),
              "roofline": roofline_of(extra, smem_peak, hbm), "clocks": extra["clocks"],
              "W": extra["info"]["words_per_tile"], "gpu_launches": extra["launches"]}
         if "e2e" in extra:
@@ -387,6 +388,15 @@ def run_ours(args, rank, world, local_rank):
                                           f"{dt:.1f}s on {cores} threads ({cpu_model()}); C "
                                           "restatement of stabsim frame_sim+detector_events+b8"}
     print(json.dumps(line), flush=True)
+
+
+def reference_sample_seconds(text) -> float:
+    """Host time of the native inverse-tableau reference sample (the step
+    before measurement sampling, reported separately per BASELINE.json C4)."""
+    from paper_2103_02202_b200 import tableau_sim as T
+    t0 = time.perf_counter()
+    T.reference_sample(text, np.random.default_rng(1))
+    return time.perf_counter() - t0
 
 
 def smem_peak_gbs():
