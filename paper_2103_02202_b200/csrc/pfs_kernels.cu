@@ -443,6 +443,17 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     }
                 }
             group_sync();  // counts visible
+            // the next pre-sampled noise op's first hit (one per thread) rides in
+            // a register from the previous noise op on, so applying it does not
+            // put an L2 round trip on the op chain
+            uint64_t pf_hit = 0;
+            auto prefetch_hit = [&](uint32_t ord, uint32_t base) {
+                pf_hit = 0;
+                if (!pregen || ord == NO_SLOT) return;
+                const uint32_t nh = ncnt[ord];
+                if (nh != NO_SLOT && (uint32_t)tid < nh) pf_hit = __ldcg(hits + base + tid);
+            };
+            prefetch_hit(kp.first_pregen, kp.first_cap_base);
 
             // descriptors run one op ahead in registers
             uint4 h0 = kp.n_ops > 0 ? ldesc(0) : make_uint4(0, 0, 0, 0);
@@ -582,9 +593,12 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                     }
                     if ((flags & F_PREGEN) && pregen) {
                         const uint32_t nh = ncnt[ob];  // NO_SLOT: the hit list overflowed
+                        const uint64_t cur = pf_hit;
+                        prefetch_hit(h1.z, h1.w);  // the next pre-sampled noise op
                         if (nh != NO_SLOT) {
                             const uint64_t* hl = hits + oc;
-                            for (uint32_t i = tid; i < nh; i += nth) apply_entry<W>(X, Z, hl[i]);
+                            if ((uint32_t)tid < nh) apply_entry<W>(X, Z, cur);
+                            for (uint32_t i = tid + nth; i < nh; i += nth) apply_entry<W>(X, Z, hl[i]);
                         } else {
                             const NoiseParam* npp = kp.noise + ob;
                             for (uint32_t r = tid; r < __ldg(&npp->nchunks); r += nth)
