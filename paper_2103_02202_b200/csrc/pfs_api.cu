@@ -77,6 +77,11 @@ struct pfs_program {
     DevBuf<unsigned long long> d_counts;
     // column kernel (KERNEL_COL): op-block stream, block table, packed reference bits
     bool colk = false;
+    // error-model detector sampler (KERNEL_DEM)
+    bool demk = false;
+    DemModel dem;
+    DevBuf<uint32_t> d_comp_base, d_comp_ptr, d_cols;
+    int dem_grid = 0;
     bool col_ring_smem = true;
     int col_v = 1;      // words per lane (tile = 32 col_v shots)
     int col_nw = 0;
@@ -133,6 +138,7 @@ static void choose_warp_layout(pfs_program* pg) {
 constexpr uint32_t kColSlotCap = 16384;
 constexpr int kColMinWarps = 4;
 constexpr bool kColAuto = false;  // auto layout picks the column kernel
+constexpr int DEM_WARPS_HOST = 16;  // dem_kernel's warps (DEM_WARPS)
 
 static uint32_t col_max_block_bytes(const HostProgram& hp) {
     uint32_t mx = 16;
@@ -203,6 +209,18 @@ static bool choose_col_layout(pfs_program* pg) {
 static void choose_layout(pfs_program* pg) {
     const HostProgram& hp = pg->hp;
     pfs_options o = pg->opts;
+    if (pg->opts.kernel == KERNEL_DEM) {
+        // error-model sampler: RNG tiles of one word (32 shots), no frame
+        pg->demk = true;
+        pg->wcfg = LaunchCfg{};
+        pg->cfg = LaunchCfg{};
+        pg->cfg.W = 1;
+        pg->cfg.groups = 1;
+        pg->cfg.threads = 32 * DEM_WARPS_HOST;
+        pg->cfg.smem_bytes = dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, false);
+        pg->cfg.kernel = 0;
+        return;
+    }
     if (choose_col_layout(pg)) {
         // the program's tile is one word: RNG counters per 32-shot column
         pg->wcfg = LaunchCfg{};
@@ -305,7 +323,26 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
     }
     choose_layout(pg);
     if (pg->opts.schedule_only && pg->cfg.W < 1) pg->cfg.W = pg->opts.words_per_tile > 0 ? pg->opts.words_per_tile : 1;
-    if (!pg->opts.schedule_only && !pg->wcfg.kernel && !pg->colk && (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget)) {
+    if (pg->demk) {
+        try {
+            pg->dem = build_dem(instrs, n_instrs, targets, det_ptr, det_idx, n_columns, num_qubits,
+                                num_measurements, n_noise);
+        } catch (const std::invalid_argument& e) {
+            delete pg;
+            return fail(PFS_E_INVALID, e.what());
+        }
+        if (!pg->dem.coin_dependent.empty()) {
+            const std::string why = pg->dem.coin_dependent;
+            delete pg;
+            return fail(PFS_E_INVALID, "error-model sampler: " + why + " (use the frame sampler)");
+        }
+        if (pg->cfg.smem_bytes > kSmemBudget) {
+            delete pg;
+            return fail(PFS_E_INVALID, "error-model sampler: too many output columns for one CTA");
+        }
+    }
+    if (!pg->opts.schedule_only && !pg->wcfg.kernel && !pg->colk && !pg->demk &&
+        (pg->cfg.W < 1 || pg->cfg.smem_bytes > kSmemBudget)) {
         delete pg;
         return fail(PFS_E_INVALID, "frame table of " + std::to_string(num_qubits) +
                                        " qubits does not fit one CTA's shared memory");
@@ -335,7 +372,7 @@ int pfs_program_info(const pfs_program* pg, pfs_info* o) {
     o->num_qubits = hp.num_qubits;
     o->words_per_tile = pg->cfg.W;
     o->groups = pg->cfg.groups;
-    o->kernel = pg->colk ? KERNEL_COL : pg->wcfg.kernel ? KERNEL_WARP : KERNEL_COOP;
+    o->kernel = pg->demk ? KERNEL_DEM : pg->colk ? KERNEL_COL : pg->wcfg.kernel ? KERNEL_WARP : KERNEL_COOP;
     o->warps_per_cta = pg->colk ? pg->col_nw : pg->wcfg.kernel ? pg->wcfg.threads / 32 : 0;
     o->tile_shots = 32 * pg->cfg.W;
     o->threads = pg->cfg.threads;
@@ -399,6 +436,7 @@ void pfs_program_destroy(pfs_program* pg) {
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         pg->d_cstream.release(); pg->d_binfo.release(); pg->d_refw.release();
+        pg->d_comp_base.release(); pg->d_comp_ptr.release(); pg->d_cols.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
         for (auto& e : pg->ev) if (e) cudaEventDestroy(e);
         if (prev >= 0) cudaSetDevice(prev);
@@ -430,7 +468,7 @@ static int ensure_device(pfs_program* pg, int device) {
     pg->smem_optin = prop.sharedMemPerBlockOptin;
     if (pg->opts.schedule_only)
         return fail(PFS_E_INVALID, "schedule-only program");
-    if (pg->colk ? pg->col_smem > pg->smem_optin
+    if (pg->demk ? pg->cfg.smem_bytes > pg->smem_optin : pg->colk ? pg->col_smem > pg->smem_optin
                  : pg->wcfg.kernel ? pg->wcfg.smem_bytes > pg->smem_optin
                                    : pg->cfg.smem_bytes > pg->smem_optin)
         return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory");
@@ -464,6 +502,18 @@ static int ensure_device(pfs_program* pg, int device) {
     if (pg->wcfg.kernel) {
         CUDA_TRY(set_frame_warp_kernel_smem(pg->wcfg));
         pg->wcfg.grid = grid_of(pg->wcfg);
+    }
+    if (pg->demk) {
+        CUDA_TRY(upload(pg->d_comp_base, pg->dem.comp_base));
+        CUDA_TRY(upload(pg->d_comp_ptr, pg->dem.comp_ptr));
+        CUDA_TRY(upload(pg->d_cols, pg->dem.cols));
+        CUDA_TRY(set_dem_kernel_smem(pg->smem_optin));
+        int per_sm = pg->opts.ctas_per_sm;
+        if (per_sm <= 0) {
+            per_sm = (int)std::max<size_t>(1, prop.sharedMemPerMultiprocessor / (pg->cfg.smem_bytes + 1024));
+            per_sm = std::min(per_sm, std::max(1, prop.maxThreadsPerMultiProcessor / (32 * DEM_WARPS_HOST)));
+        }
+        pg->dem_grid = pg->num_sms * per_sm;
     }
     if (pg->colk) {
         CUDA_TRY(upload(pg->d_cstream, pg->cs.words));
@@ -499,6 +549,25 @@ static bool is_device_ptr(const void* p) {
 static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64_t nt, bool injected,
                         cudaStream_t st, bool time_noise, ColParams cp = ColParams{}) {
     const HostProgram& hp = pg->hp;
+    if (pg->demk) {
+        // error-model sampler: noise hits XOR their output signatures, one launch
+        DemParams dp{};
+        dp.comp_base = pg->d_comp_base.p;
+        dp.comp_ptr = pg->d_comp_ptr.p;
+        dp.cols = pg->d_cols.p;
+        dp.b8_out = cp.b8_out;
+        dp.b8_pitch = cp.b8_pitch;
+        dp.b8_bytes = cp.b8_bytes;
+        dp.rows_out = cp.rows_out;
+        dp.rows_stride = cp.rows_stride;
+        dp.warps = DEM_WARPS_HOST;
+        kp.n_tiles = nt;
+        const size_t smem = dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, kp.counts_in_smem != 0);
+        const int grid = (int)std::min<int64_t>(pg->dem_grid, nt);
+        CUDA_TRY(launch_dem_kernel(kp, dp, grid, smem, st));
+        pg->last_launches++;
+        return PFS_OK;
+    }
     if (pg->colk) {
         // column kernel: one launch, noise sampled inline, outputs written directly
         cp.stream = pg->d_cstream.p;
@@ -600,6 +669,11 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     else need = R * used_words * 4;
     if (out_bytes < need) return fail(PFS_E_INVALID, "output buffer too small: need " + std::to_string(need) + " bytes");
 
+    if (pg->demk && injected)
+        return fail(PFS_E_INVALID, "the error-model sampler draws its own noise (no injected masks)");
+    if (pg->demk && rows_meas)
+        return fail(PFS_E_INVALID, "the error-model sampler produces detection events only (use the frame sampler "
+                                   "for measurement records)");
     int rc = ensure_device(pg, device);
     if (rc) return rc;
     cudaStream_t st = (cudaStream_t)stream_v;
@@ -687,15 +761,16 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     LaunchCfg cfg = (!pg->wcfg.kernel || coop_counts) ? pg->cfg : pg->wcfg;
     const bool warpk = cfg.kernel == KERNEL_WARP;
     kp.desc_in_smem = warpk ? pg->warp_desc_smem : (desc_fits(hp) ? 1 : 0);
-    CUDA_TRY(pg->d_nscratch.reserve(pg->colk ? (size_t)pg->col_grid * 32 * (pg->col_nw + 1) * NZ_MAX_LIST
-                                              : (size_t)cfg.grid * cfg.threads * NZ_MAX_LIST));
+    CUDA_TRY(pg->d_nscratch.reserve(pg->demk ? (size_t)pg->dem_grid * 32 * DEM_WARPS_HOST * NZ_MAX_LIST
+                                    : pg->colk ? (size_t)pg->col_grid * 32 * (pg->col_nw + 1) * NZ_MAX_LIST
+                                               : (size_t)cfg.grid * cfg.threads * NZ_MAX_LIST));
     kp.noise_scratch = pg->d_nscratch.p;
     if (pg->opts.debug_skip & 64) {  // op-boundary clock trace of the first tile
         CUDA_TRY(pg->d_clock.reserve(hp.ops.size() * 9 + 1));
         kp.op_clock = pg->d_clock.p;
     }
 
-    if (!warpk && !cfg.ring_smem && !pg->colk) {
+    if (!warpk && !cfg.ring_smem && !pg->colk && !pg->demk) {
         CUDA_TRY(pg->d_ring.reserve((size_t)std::max<int64_t>(hp.num_slots, 1) * W * cfg.grid * cfg.groups));
         kp.ring_global = pg->d_ring.p;
     }
@@ -708,7 +783,9 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         kp.counts = cptr;
         const size_t extra = (size_t)hp.num_cols * 4;
         kp.counts_in_smem = (!warpk && cfg.smem_bytes + extra <= pg->smem_optin) ? 1 : 0;
-        if (pg->colk) {
+        if (pg->demk) {
+            kp.counts_in_smem = dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, true) <= pg->smem_optin;
+        } else if (pg->colk) {
             kp.counts_in_smem = col_smem_bytes(pg->col_nw, col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1), pg->col_ring_smem, pg->col_v),
                                                std::max<uint32_t>(pg->cs.slot_bytes, 16u), hp.num_cols) <= pg->smem_optin;
         } else if (kp.counts_in_smem) {
@@ -717,7 +794,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         }
         // per-CTA u32 counters: bound shots per launch so no counter can overflow
         const int64_t max_tiles = std::max<int64_t>(1, ((int64_t)1 << 30) / T) *
-                                  (pg->colk ? pg->col_grid : cfg.grid);
+                                  (pg->demk ? pg->dem_grid : pg->colk ? pg->col_grid : cfg.grid);
         for (int64_t t0 = 0; t0 < n_tiles_all; t0 += max_tiles) {
             const int64_t nt = std::min(max_tiles, n_tiles_all - t0);
             kp.n_tiles = nt;
@@ -748,10 +825,11 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     const int64_t dev_pitch = b8 ? ((nbytes + 31) / 32) * 32 : 0;
     int64_t chunk_tiles = n_tiles_all;
     if (!dev_out) {
-        const int64_t bytes_per_tile = (pg->colk && b8 ? 0 : R * W * 4) + (b8 ? T * dev_pitch : 0);
+        const int64_t bytes_per_tile = ((pg->colk || pg->demk) && b8 ? 0 : R * W * 4) + (b8 ? T * dev_pitch : 0);
         const int64_t target = (int64_t)256 << 20;
         chunk_tiles = std::max<int64_t>(1, target / std::max<int64_t>(bytes_per_tile, 1));
-        chunk_tiles = std::max<int64_t>(chunk_tiles, pg->colk ? (int64_t)pg->col_grid * pg->col_nw
+        chunk_tiles = std::max<int64_t>(chunk_tiles, pg->demk ? (int64_t)pg->dem_grid * 2
+                                                   : pg->colk ? (int64_t)pg->col_grid * pg->col_nw
                                                                   : (int64_t)cfg.grid);  // keep every SM busy
         chunk_tiles = std::min(chunk_tiles, n_tiles_all);
     }
@@ -762,7 +840,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     for (int b = 0; b < nbuf; b++) {
         // (+ padding to whole 8-word groups: the word-major transpose reads
         // narrow tiles in groups of 8 words)
-        if (!direct_rows && !(pg->colk && b8)) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * ((chunk_words + 7) & ~7ll)));
+        if (!direct_rows && !((pg->colk || pg->demk) && b8)) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * ((chunk_words + 7) & ~7ll)));
         if (b8 && !dev_out) CUDA_TRY(pg->d_b8[b].reserve((size_t)chunk_tiles * T * dev_pitch));
     }
     if (timing) CUDA_TRY(cudaEventRecord(pg->ev[1], st));
@@ -787,7 +865,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         kp.num_shots = nshots;
         if (injected) { kp.coins = pg->d_coins.p + t0 * W; kp.masks = pg->d_masks.p + t0 * W; }
         ColParams cpx{};
-        if (pg->colk) {
+        if (pg->colk || pg->demk) {
             cpx.records = rows_meas ? 1 : 0;
             cpx.ncols_out = (int32_t)R;
             if (b8) {
@@ -801,7 +879,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
                 cpx.rows_stride = row_words;
             }
         }
-        if (!pg->colk && direct_rows && (used_words % W) != 0) {
+        if (!pg->colk && !pg->demk && direct_rows && (used_words % W) != 0) {
             // the last tile would write past the caller's rows: stage through scratch
             CUDA_TRY(pg->d_rows[0].reserve((size_t)std::max<int64_t>(R, 1) * chunk_words));
             rows = pg->d_rows[0].p;
@@ -817,7 +895,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             if (rc2) return rc2;
         }
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[3], st));
-        if (b8 && pg->colk) {
+        if (b8 && (pg->colk || pg->demk)) {
             if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
         } else if (b8) {
             uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
@@ -837,7 +915,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         if (timing && ci == 0) {
             CUDA_TRY(cudaStreamSynchronize(st));
             cudaEventElapsedTime(&frame_ms, pg->ev[2], pg->ev[3]);
-            if (!pg->colk && !injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2)) {
+            if (!pg->colk && !pg->demk && !injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2)) {
                 float nz = 0;
                 cudaEventElapsedTime(&nz, pg->ev[8], pg->ev[9]);
                 pg->last_ms[5] = nz;

@@ -123,95 +123,6 @@ __device__ __forceinline__ void sink_put(const ColParams& cp, Sink<V>& sk, bool 
     }
 }
 
-// One noise op's draws for word g (DESIGN.md §4 with T = 32), warp-cooperative:
-// lane l draws chunk r0 + l's Binomial count from Philox block 0; the warp's
-// hits are compacted across lanes (prefix sum) and each lane produces one hit
-// position per round.  A chunk whose positions collide, or whose count exceeds
-// NZ_MAX_LIST, is redrawn serially by noise_chunk — so the hits are exactly
-// noise_chunk's for every chunk.  wscr: 32 NZ_MAX_LIST words of per-warp shared scratch.
-template <typename Apply>
-__device__ __forceinline__ void noise_op_warp(const KParams& kp, const NoiseParam& np, uint32_t ordinal,
-                                              uint32_t g, uint32_t* wscr, uint32_t* sl, int lane,
-                                              Apply apply) {
-    if (np.flags & NZ_ALL) {
-        for (uint32_t r = (uint32_t)lane; r < np.nchunks; r += 32)
-            noise_chunk(kp, np, ordinal, r, g, sl, 1, apply);
-        return;
-    }
-    const uint32_t L = np.L;
-    const uint32_t lg = 31u - __clz(L);
-    const uint32_t sh = 32u - lg;
-    const unsigned long long* tab = reinterpret_cast<const unsigned long long*>(kp.noise_tab) + np.tab_full;
-    const uint32_t len = np.len_full;
-    const unsigned long long t0 = len > 0 ? __ldg(tab) : 0ull;
-    const unsigned long long t1 = len > 1 ? __ldg(tab + 1) : 0ull;
-    for (uint32_t r0 = 0; r0 < np.nchunks; r0 += 32) {
-        const uint32_t r = r0 + (uint32_t)lane;
-        const bool valid = r < np.nchunks;
-        uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, count = 0;
-        if (valid) {
-            noise_block(0u, r, g, ordinal, kp.seed, w0, w1, w2, w3);
-            const unsigned long long uu = ((unsigned long long)w1 << 32) | w0;
-            if (len > 0 && uu >= t0) {
-                count = 1;
-                if (len > 1 && uu >= t1) {
-                    count = 2;
-                    while (count < len && uu >= __ldg(tab + count)) count++;
-                }
-            }
-        }
-        const bool big = count > (uint32_t)NZ_MAX_LIST;
-        const uint32_t c = big ? 0u : count;
-        uint32_t pre = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pre, d);
-            if (lane >= d) pre += v;
-        }
-        const uint32_t H = __shfl_sync(0xFFFFFFFFu, pre, 31);
-        if (H == 0 && !__any_sync(0xFFFFFFFFu, big)) continue;
-        const uint32_t excl = pre - c;
-        for (uint32_t j0 = 0; j0 < H; j0 += 32) {
-            const uint32_t j = j0 + (uint32_t)lane;
-            uint32_t lo = 0;  // owner chunk: smallest lane q with pre[q] > j
-#pragma unroll
-            for (int st = 16; st > 0; st >>= 1) {
-                const uint32_t pv = __shfl_sync(0xFFFFFFFFu, pre, (int)(lo + st - 1));
-                if (pv <= j) lo += st;
-            }
-            const uint32_t owner = lo > 31u ? 31u : lo;
-            const uint32_t oexcl = __shfl_sync(0xFFFFFFFFu, excl, (int)owner);
-            uint32_t x = __shfl_sync(0xFFFFFFFFu, w2, (int)owner);
-            uint32_t y = __shfl_sync(0xFFFFFFFFu, w3, (int)owner);
-            if (j < H) {
-                const uint32_t h = j - oexcl;
-                if (h > 0) {
-                    uint32_t b0, b1, b2, b3;
-                    noise_block((h + 1) >> 1, r0 + owner, g, ordinal, kp.seed, b0, b1, b2, b3);
-                    x = (h & 1u) ? b0 : b2;
-                    y = (h & 1u) ? b1 : b3;
-                }
-                const uint32_t pos = lg ? (x >> sh) : 0u;
-                wscr[j] = (pos << 4) | (np.npat > 1 ? __umulhi(y, np.npat) : 0u);
-            }
-        }
-        __syncwarp();
-        bool dup = false;
-        for (uint32_t h = 1; h < c; h++)
-            for (uint32_t q = 0; q < h; q++) dup |= (wscr[excl + h] >> 4) == (wscr[excl + q] >> 4);
-        if (dup || big) {
-            noise_chunk(kp, np, ordinal, r, g, sl, 1, apply);  // rare: serial redraw
-        } else {
-            const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
-            for (uint32_t h = 0; h < c; h++) {
-                const uint32_t e = wscr[excl + h];
-                if ((e >> 4) < vlen) apply(r * L + (e >> 4), e & 15u);
-            }
-        }
-        __syncwarp();
-    }
-}
-
 // Gate rules on a word column's frame: x plane X[q*V..], z plane Z[q*V..]
 // (stabsim/frame_sim.py:64-72, rules gates.py:326-348; all XORs read old values).
 template <uint32_t CODE, int V>

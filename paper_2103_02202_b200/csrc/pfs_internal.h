@@ -275,4 +275,37 @@ cudaError_t launch_frame_col_kernel(const KParams& kp, const ColParams& cp, int 
                                     size_t smem, cudaStream_t stream);
 cudaError_t set_frame_col_kernel_smem(size_t smem);
 
+// ---------------------------------------------------------------- error model
+// Detector error model (pfs_dem.cpp): per noise ordinal o, application a and
+// component k (x slot 0, z slot 0, x slot 1, z slot 1) the output columns a
+// frame flip there reaches: cols[comp_ptr[i] .. comp_ptr[i + 1]) with
+// i = comp_base[o] + 4 a + k.  coin_dependent != "": some collapse coin reaches
+// an output, so the events are not a function of the noise draws alone.
+constexpr int KERNEL_DEM = 4;
+struct DemModel {
+    std::vector<uint32_t> comp_base;
+    std::vector<uint32_t> comp_ptr;
+    std::vector<uint32_t> cols;
+    std::string coin_dependent;
+    double mean_cols_per_comp = 0.0;
+};
+DemModel build_dem(const pfs_instr* ins, int64_t n_ins, const int32_t* targets, const int64_t* det_ptr,
+                   const int64_t* det_idx, int64_t n_cols, int32_t num_qubits, int64_t num_meas,
+                   int64_t n_noise);
+
+struct DemParams {
+    const uint32_t* comp_base;
+    const uint32_t* comp_ptr;
+    const uint32_t* cols;
+    uint8_t* b8_out;             // shot-major detection events, or null
+    int64_t b8_pitch;
+    int64_t b8_bytes;
+    uint32_t* rows_out;          // DETECTORS_ROWS: [cols][rows_stride], or null
+    int64_t rows_stride;
+    int32_t warps;
+};
+cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, int grid, size_t smem, cudaStream_t st);
+cudaError_t set_dem_kernel_smem(size_t smem);
+size_t dem_smem_bytes(int warps, int64_t num_cols, bool counts);
+
 }  // namespace pfs

@@ -239,3 +239,49 @@ def test_c2_full_size_properties():
         assert five_sigma(counts, shots, counts_ref, n_ref) < 5.0
     except FileNotFoundError:
         pass
+
+
+@pytest.mark.parametrize("case", ["d3_p1e-2", "d5", "d9_highp"])
+def test_error_model_sampler_equals_frame_sampler(oracle_lib, case):
+    """The error-model sampler (kernel 4: detection events = XOR of the noise
+    hits' output signatures) makes the frame sampler's own draws with one-word
+    tiles: events (b8, rows) and counts agree bit for bit with the frame
+    kernel and with the C oracle."""
+    from paper_2103_02202_b200.sampler import compile_detector_sampler
+
+    text = _philox_cases()[case]
+    dem = compile_detector_sampler(text, kernel=4)
+    frm = compile_detector_sampler(text, kernel=1, words_per_tile=1)
+    assert dem.native.info["kernel"] == 4 and dem.tile_shots == 32 == frm.tile_shots
+    for shots, off in ((4096, 0), (1000 + 7, 32 * 37)):
+        a = dem.sample(shots, seed=11, shot_offset=off)
+        assert np.array_equal(a, frm.sample(shots, seed=11, shot_offset=off))
+        assert np.array_equal(dem.sample_rows(shots, seed=11, shot_offset=off),
+                              frm.sample_rows(shots, seed=11, shot_offset=off))
+        assert np.array_equal(dem.sample_counts(shots, seed=11, shot_offset=off),
+                              b8_unpack(a, dem.num_columns).sum(axis=0))
+    shots = 3 * 32 + 5
+    _, oev = oracle_lib.sample(dem.flat, shots, 32, seed=3, tile_offset=2, nthreads=4, flips=False,
+                               schedule=dem.native.noise_schedule())
+    assert np.array_equal(b8_unpack(dem.sample(shots, seed=3, shot_offset=64), dem.num_columns),
+                          rows_unpack(oev, shots))
+
+
+def test_error_model_sampler_full_size_d25():
+    """Config 2 at 2^20 shots through the error-model sampler: identical to the
+    frame sampler on one-word tiles."""
+    from paper_2103_02202_b200 import generators as gen
+    from paper_2103_02202_b200.sampler import compile_detector_sampler
+    import torch
+
+    text = gen.config_circuit(2)
+    dem = compile_detector_sampler(text, kernel=4)
+    frm = compile_detector_sampler(text, kernel=1, words_per_tile=1)
+    shots = 1 << 20
+    nb = (dem.num_columns + 7) // 8
+    a = torch.empty((shots, nb), dtype=torch.uint8, device="cuda")
+    b = torch.empty((shots, nb), dtype=torch.uint8, device="cuda")
+    dem.sample(shots, seed=21, out=a)
+    frm.sample(shots, seed=21, out=b)
+    torch.cuda.synchronize()
+    assert torch.equal(a, b)

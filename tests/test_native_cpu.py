@@ -126,3 +126,13 @@ def test_oracle_not_reachable_from_product():
                     src = f.read()
                 assert "import oracle" not in src and "from oracle" not in src, fn
                 assert "pfs_oracle" not in src, fn
+
+
+def test_error_model_sampler_scope():
+    # the error-model sampler needs coin-independent outputs (QEC memories) and
+    # produces detection events only
+    from paper_2103_02202_b200 import generators as gen2
+    p = N.NativeProgram(flatten(gen2.surface_code_memory(5, 5, 1e-3)), kernel=4)
+    assert p.info["kernel"] == 4 and p.info["tile_shots"] == 32
+    with pytest.raises(ValueError, match="measurement randomness"):
+        N.NativeProgram(flatten(gen2.random_clifford(16, 20, 0.01, 1)), kernel=4)
