@@ -80,7 +80,7 @@ struct pfs_program {
     // error-model detector sampler (KERNEL_DEM)
     bool demk = false;
     DemModel dem;
-    DevBuf<uint32_t> d_comp_base, d_comp_ptr, d_cols;
+    DevBuf<uint32_t> d_comp_base, d_comp_ptr, d_cols, d_items;
     int dem_grid = 0;
     bool col_ring_smem = true;
     int col_v = 1;      // words per lane (tile = 32 col_v shots)
@@ -357,6 +357,14 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         dedup_operands(pg->hp);
         build_noise_schedule(pg->hp, 32 * pg->cfg.W, th);
         if (pg->colk) pg->cs = build_col_stream(pg->hp, kColSlotCap);
+        if (pg->demk) {  // every tile's noise chunks as (ordinal, chunk) work items
+            pg->dem.items.clear();
+            for (int64_t o = 0; o < pg->hp.num_noise; o++) {
+                const NoiseParam& np = pg->hp.noise[o];
+                if (np.flags & NZ_NONE) continue;
+                for (uint32_t r = 0; r < np.nchunks; r++) { pg->dem.items.push_back((uint32_t)o); pg->dem.items.push_back(r); }
+            }
+        }
     } catch (const std::invalid_argument& e) {
         delete pg;
         return fail(PFS_E_INVALID, e.what());
@@ -436,7 +444,7 @@ void pfs_program_destroy(pfs_program* pg) {
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         pg->d_cstream.release(); pg->d_binfo.release(); pg->d_refw.release();
-        pg->d_comp_base.release(); pg->d_comp_ptr.release(); pg->d_cols.release();
+        pg->d_comp_base.release(); pg->d_comp_ptr.release(); pg->d_cols.release(); pg->d_items.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
         for (auto& e : pg->ev) if (e) cudaEventDestroy(e);
         if (prev >= 0) cudaSetDevice(prev);
@@ -507,6 +515,7 @@ static int ensure_device(pfs_program* pg, int device) {
         CUDA_TRY(upload(pg->d_comp_base, pg->dem.comp_base));
         CUDA_TRY(upload(pg->d_comp_ptr, pg->dem.comp_ptr));
         CUDA_TRY(upload(pg->d_cols, pg->dem.cols));
+        CUDA_TRY(upload(pg->d_items, pg->dem.items));
         CUDA_TRY(set_dem_kernel_smem(pg->smem_optin));
         int per_sm = pg->opts.ctas_per_sm;
         if (per_sm <= 0) {
@@ -560,6 +569,8 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
         dp.b8_bytes = cp.b8_bytes;
         dp.rows_out = cp.rows_out;
         dp.rows_stride = cp.rows_stride;
+        dp.items = reinterpret_cast<const uint2*>(pg->d_items.p);
+        dp.n_items = (int32_t)(pg->dem.items.size() / 2);
         dp.warps = DEM_WARPS_HOST;
         kp.n_tiles = nt;
         const size_t smem = dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, kp.counts_in_smem != 0);

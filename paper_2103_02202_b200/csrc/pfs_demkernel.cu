@@ -1,9 +1,10 @@
 // dem_kernel — detection events from the detector error model (pfs_dem.cpp).
 //
 // A CTA owns a tile of 32 shots at a time (the RNG tile of DESIGN.md §4 with
-// W = 1): its warps take the tile's noise instructions, draw each one's hits
-// with the frame sampler's own counter-based schedule (noise_op_warp, the same
-// draws as noise_chunk / noise_kernel), and XOR every hit's component
+// W = 1): its warps take the tile's noise chunks, 32 (instruction, chunk) work
+// items per pass, draw each one's hits with the frame sampler's own
+// counter-based schedule (the same draws as noise_chunk / noise_kernel), and
+// XOR every hit's component
 // signatures into one shared-memory word per output column (bit s = shot s).
 // The column words are then transposed in 32x32 blocks and stored as the
 // shot-major b8 rows (stabsim/io_formats.py:94-96, 208-227), or popcounted
@@ -18,6 +19,89 @@
 namespace pfs {
 
 constexpr int DEM_WARPS = 16;
+
+// The tile's noise chunks of ALL instructions, 32 per warp pass: lane l takes
+// work item (ordinal o, chunk r) and draws exactly what noise_chunk draws for
+// it — block 0 gives the Binomial count and the first hit, the
+// warp compacts the hits and each lane makes one position per round (owner's
+// ordinal and chunk shuffled in), duplicates / oversize counts are redrawn
+// serially.  Packing chunks of different instructions keeps all lanes busy
+// when an instruction has fewer than 32 chunks per 32-shot tile.
+template <typename Apply>
+__device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2* items, uint32_t n_items,
+                                                 uint32_t first, uint32_t g, uint32_t* wscr, uint32_t* sl,
+                                                 int lane, Apply apply) {
+    const uint32_t it = first + (uint32_t)lane;
+    const bool valid = it < n_items;
+    const uint2 oc = valid ? __ldg(items + it) : make_uint2(0u, 0u);
+    const uint32_t o = oc.x, r = oc.y;
+    NoiseParam np{};
+    if (valid) np = kp.noise[o];
+    const bool all = valid && (np.flags & NZ_ALL);
+    const uint32_t L = valid ? np.L : 1u;
+    const uint32_t lg = 31u - __clz(L);
+    const uint32_t sh = 32u - lg;
+    uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, count = 0;
+    if (valid && !all) {
+        noise_block(0u, r, g, o, kp.seed, w0, w1, w2, w3);
+        const unsigned long long uu = ((unsigned long long)w1 << 32) | w0;
+        const unsigned long long* tab = reinterpret_cast<const unsigned long long*>(kp.noise_tab) + np.tab_full;
+        while (count < np.len_full && uu >= __ldg(tab + count)) count++;
+    }
+    const bool big = count > (uint32_t)NZ_MAX_LIST;
+    const uint32_t c = big ? 0u : count;
+    uint32_t pre = c;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+        if (lane >= d) pre += v;
+    }
+    const uint32_t H = __shfl_sync(0xFFFFFFFFu, pre, 31);
+    const uint32_t excl = pre - c;
+    for (uint32_t j0 = 0; j0 < H; j0 += 32) {
+        const uint32_t j = j0 + (uint32_t)lane;
+        uint32_t lo = 0;  // owner lane: smallest q with pre[q] > j
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+            const uint32_t pv = __shfl_sync(0xFFFFFFFFu, pre, (int)(lo + st - 1));
+            if (pv <= j) lo += st;
+        }
+        const int owner = (int)(lo > 31u ? 31u : lo);
+        const uint32_t oexcl = __shfl_sync(0xFFFFFFFFu, excl, owner);
+        const uint32_t oo = __shfl_sync(0xFFFFFFFFu, o, owner);
+        const uint32_t orr = __shfl_sync(0xFFFFFFFFu, r, owner);
+        const uint32_t osh = __shfl_sync(0xFFFFFFFFu, sh, owner);
+        const uint32_t olg = __shfl_sync(0xFFFFFFFFu, lg, owner);
+        const uint32_t onp = __shfl_sync(0xFFFFFFFFu, np.npat, owner);
+        uint32_t x = __shfl_sync(0xFFFFFFFFu, w2, owner);
+        uint32_t y = __shfl_sync(0xFFFFFFFFu, w3, owner);
+        if (j < H) {
+            const uint32_t h = j - oexcl;
+            if (h > 0) {
+                uint32_t b0, b1, b2, b3;
+                noise_block((h + 1) >> 1, orr, g, oo, kp.seed, b0, b1, b2, b3);
+                x = (h & 1u) ? b0 : b2;
+                y = (h & 1u) ? b1 : b3;
+            }
+            const uint32_t pos = olg ? (x >> osh) : 0u;
+            wscr[j] = (pos << 4) | (onp > 1 ? __umulhi(y, onp) : 0u);
+        }
+    }
+    __syncwarp();
+    bool dup = false;
+    for (uint32_t h = 1; h < c; h++)
+        for (uint32_t q = 0; q < h; q++) dup |= (wscr[excl + h] >> 4) == (wscr[excl + q] >> 4);
+    if (dup || big || all) {
+        noise_chunk(kp, np, o, r, g, sl, 1, [&](uint32_t trial, uint32_t pick) { apply(o, trial, pick); });
+    } else if (c) {
+        const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
+        for (uint32_t h = 0; h < c; h++) {
+            const uint32_t e = wscr[excl + h];
+            if ((e >> 4) < vlen) apply(o, r * L + (e >> 4), e & 15u);
+        }
+    }
+    __syncwarp();
+}
 
 __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_constant__ KParams kp,
                                                                 const __grid_constant__ DemParams dp) {
@@ -35,21 +119,18 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_con
         const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
         for (int i = threadIdx.x; i < ncols; i += blockDim.x) ev[i] = 0u;
         __syncthreads();
-        for (int o = warp; o < kp.num_noise; o += NW) {
-            const NoiseParam np = kp.noise[o];
-            if (np.flags & NZ_NONE) continue;
-            const uint32_t ch = __ldg(kp.noise_ch + o);
-            const uint32_t cb = __ldg(dp.comp_base + o);
-            noise_op_warp(kp, np, (uint32_t)o, g, wscr, sl, lane, [&](uint32_t trial, uint32_t pick) {
+        for (uint32_t first = 32u * warp; first < (uint32_t)dp.n_items; first += 32u * NW) {
+            noise_items_warp(kp, dp.items, (uint32_t)dp.n_items, first, g, wscr, sl, lane,
+                             [&](uint32_t o, uint32_t trial, uint32_t pick) {
                 const uint32_t app = trial >> 5, bit = 1u << (trial & 31u);
                 uint32_t xm, zm;
-                pattern_of(ch, pick, xm, zm);
+                pattern_of(__ldg(kp.noise_ch + o), pick, xm, zm);
                 const uint32_t mask = (xm & 1u) | ((zm & 1u) << 1) | ((xm & 2u) << 1) | ((zm & 2u) << 2);
+                const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
                 for (uint32_t k = 0; k < 4; k++) {
                     if (!((mask >> k) & 1u)) continue;
-                    const uint32_t ci = cb + app * 4 + k;
-                    const uint32_t e1 = __ldg(dp.comp_ptr + ci + 1);
-                    for (uint32_t e = __ldg(dp.comp_ptr + ci); e < e1; e++) atomicXor(ev + __ldg(dp.cols + e), bit);
+                    const uint32_t e1 = __ldg(dp.comp_ptr + cb + k + 1);
+                    for (uint32_t e = __ldg(dp.comp_ptr + cb + k); e < e1; e++) atomicXor(ev + __ldg(dp.cols + e), bit);
                 }
             });
         }

@@ -288,6 +288,7 @@ struct DemModel {
     std::vector<uint32_t> cols;
     std::string coin_dependent;
     double mean_cols_per_comp = 0.0;
+    std::vector<uint32_t> items;     // (ordinal, chunk) pairs of one tile (set once the schedule is built)
 };
 DemModel build_dem(const pfs_instr* ins, int64_t n_ins, const int32_t* targets, const int64_t* det_ptr,
                    const int64_t* det_idx, int64_t n_cols, int32_t num_qubits, int64_t num_meas,
@@ -302,6 +303,8 @@ struct DemParams {
     int64_t b8_bytes;
     uint32_t* rows_out;          // DETECTORS_ROWS: [cols][rows_stride], or null
     int64_t rows_stride;
+    const uint2* items;          // (noise ordinal, chunk) work items of one tile
+    int32_t n_items;
     int32_t warps;
 };
 cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, int grid, size_t smem, cudaStream_t st);
