@@ -146,18 +146,26 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_con
                 }
             }
         } else if (dp.b8_out != nullptr) {
+            // whole 32-column blocks store one aligned word per shot; the last,
+            // partial block (and unaligned outputs) go bytewise
             const int nblk = (ncols + 31) >> 5;
             const int64_t shot = tile * 32 + lane;
-            for (int B = warp; B < nblk; B += NW) {
+            const bool live = shot < kp.num_shots;
+            const bool aligned = ((dp.b8_pitch | reinterpret_cast<uintptr_t>(dp.b8_out)) & 3) == 0;
+            const int nfull = aligned ? (int)(dp.b8_bytes >> 2) : 0;  // blocks with 4 whole bytes
+            uint32_t* const row32 = reinterpret_cast<uint32_t*>(dp.b8_out + (live ? shot : 0) * dp.b8_pitch);
+            for (int B = warp; B < nfull && B < nblk; B += NW) {
+                const int col = B * 32 + lane;  // bits past the last column stay 0
+                const uint32_t t = transpose32_lane(col < ncols ? ev[col] : 0u, lane);
+                if (live) row32[B] = t;
+            }
+            for (int B = nfull + ((warp - nfull % NW + NW) % NW); B < nblk; B += NW) {
                 const int col = B * 32 + lane;
-                uint32_t t = transpose32_lane(col < ncols ? ev[col] : 0u, lane);
-                if (shot < kp.num_shots) {
+                const uint32_t t = transpose32_lane(col < ncols ? ev[col] : 0u, lane);
+                if (live) {
                     uint8_t* p = dp.b8_out + shot * dp.b8_pitch + (int64_t)B * 4;
                     const int64_t nb = dp.b8_bytes - (int64_t)B * 4;
-                    if (((dp.b8_pitch | reinterpret_cast<uintptr_t>(dp.b8_out)) & 3) == 0 && nb >= 4)
-                        *reinterpret_cast<uint32_t*>(p) = t;
-                    else
-                        for (int j = 0; j < 4 && j < nb; j++) p[j] = (uint8_t)(t >> (8 * j));
+                    for (int j = 0; j < 4 && j < nb; j++) p[j] = (uint8_t)(t >> (8 * j));
                 }
             }
         } else if (dp.rows_out != nullptr) {
