@@ -49,6 +49,7 @@ def parse_args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-d100", action="store_true", help="skip the config 4 (d=100) extra line")
+    ap.add_argument("--no-dem", action="store_true", help="skip the error-model sampler extra line")
     return ap.parse_args()
 
 
@@ -332,6 +333,14 @@ def run_ours(args, rank, world, local_rank):
     shots = args.shots or gen.CONFIGS[args.config]["shots"]
     main = measure(args, args.config, shots, args.steps, args.warmup, rank, world, local_rank,
                    0 if args.no_e2e else max(2, args.steps // 4))
+    dem = None
+    if args.config == 2 and not args.no_dem and args.kernel == 0:
+        # the error-model detector sampler (kernel 4) on the same workload
+        import copy
+        a2 = copy.copy(args)
+        a2.kernel, a2.words, a2.ring, a2.threads, a2.groups = 4, 0, -1, 0, 0
+        dem = measure(a2, args.config, shots, max(3, args.steps // 2), args.warmup, rank, world,
+                      local_rank, 0)
     extra = None
     if args.config == 2 and not args.no_d100:
         s4 = gen.CONFIGS[4]["shots"]
@@ -380,6 +389,14 @@ def run_ours(args, rank, world, local_rank):
         if "e2e" in extra:
             x["e2e"] = extra["e2e"]
         line["d100"] = x
+    if dem is not None:
+        line["error_model_sampler"] = {
+            "workload": "config2 through the error-model detector sampler (kernel 4): every noise hit "
+                        "XORs its precomputed detector signature; the frame sampler's own Philox draws, "
+                        "bit-exact with the frame kernel on 32-shot tiles (tests/test_gpu_parity.py)",
+            "value": dem["value"], "unit": "shots/s", "ms_per_step": 1e3 * dem["elapsed"] / dem["steps"],
+            "steps": dem["steps"], "kernel_ms": dem["frame_ms"], "gpu_launches": dem["launches"],
+            "clocks": dem["clocks"]}
     if not args.no_cpu_baseline:
         cores = host_cores()
         rate, s_shots, dt = cpu_port_rate(config_text(args.config), args.cpu_seconds, cores)
