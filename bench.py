@@ -346,6 +346,11 @@ def run_ours(args, rank, world, local_rank):
         s4 = gen.CONFIGS[4]["shots"]
         extra = measure(args, 4, s4, max(3, args.steps // 4), 3, rank, world, local_rank,
                         0 if args.no_e2e else 2)
+        if not args.no_dem and args.kernel == 0:
+            import copy
+            a4 = copy.copy(args)
+            a4.kernel, a4.words, a4.ring, a4.threads, a4.groups = 4, 0, -1, 0, 0
+            extra["dem"] = measure(a4, 4, s4, max(3, args.steps // 4), 3, rank, world, local_rank, 0)
     if rank != 0:
         return
     peaks = measured_peaks()
@@ -388,6 +393,12 @@ def run_ours(args, rank, world, local_rank):
              "W": extra["info"]["words_per_tile"], "gpu_launches": extra["launches"]}
         if "e2e" in extra:
             x["e2e"] = extra["e2e"]
+        if "dem" in extra:
+            dm = extra["dem"]
+            x["error_model_sampler"] = {
+                "value": dm["value"], "unit": "shots/s", "ms_per_step": 1e3 * dm["elapsed"] / dm["steps"],
+                "steps": dm["steps"], "kernel_ms": dm["frame_ms"], "transpose_kernel_ms": dm["transpose_ms"],
+                "note": "kernel 4 with the column words in global memory (1M columns), then tiles_to_b8"}
         line["d100"] = x
     if dem is not None:
         line["error_model_sampler"] = {

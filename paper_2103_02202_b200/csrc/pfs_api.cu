@@ -79,6 +79,7 @@ struct pfs_program {
     bool colk = false;
     // error-model detector sampler (KERNEL_DEM)
     bool demk = false;
+    bool dem_global = false;  // output column words in global memory (too many for shared)
     DemModel dem;
     DevBuf<uint32_t> d_comp_base, d_comp_ptr, d_cols, d_items;
     int dem_grid = 0;
@@ -218,6 +219,10 @@ static void choose_layout(pfs_program* pg) {
         pg->cfg.groups = 1;
         pg->cfg.threads = 32 * DEM_WARPS_HOST;
         pg->cfg.smem_bytes = dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, false);
+        if (pg->cfg.smem_bytes > kSmemBudget) {  // d=100: a million columns
+            pg->dem_global = true;
+            pg->cfg.smem_bytes = dem_smem_bytes(DEM_WARPS_HOST, 0, false);
+        }
         pg->cfg.kernel = 0;
         return;
     }
@@ -573,9 +578,22 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
         dp.n_items = (int32_t)(pg->dem.items.size() / 2);
         dp.warps = DEM_WARPS_HOST;
         kp.n_tiles = nt;
-        const size_t smem = dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, kp.counts_in_smem != 0);
+        const size_t smem = pg->dem_global ? dem_smem_bytes(DEM_WARPS_HOST, 0, false)
+                                           : dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, kp.counts_in_smem != 0);
         const int grid = (int)std::min<int64_t>(pg->dem_grid, nt);
-        CUDA_TRY(launch_dem_kernel(kp, dp, grid, smem, st));
+        if (pg->dem_global) {
+            // column words of every tile accumulate in the tile-major scratch
+            // [tile][col] (kp.ev_out), transposed afterwards like the frame path
+            if (!kp.ev_out) return fail(PFS_E_INVALID, "error-model sampler at this size: b8 / rows outputs only");
+            if (kp.out_row_stride == 1)
+                CUDA_TRY(cudaMemsetAsync(kp.ev_out, 0, (size_t)nt * hp.num_cols * 4, st));
+            else
+                CUDA_TRY(cudaMemset2DAsync(kp.ev_out, (size_t)kp.out_row_stride * 4, 0, (size_t)nt * 4,
+                                           (size_t)hp.num_cols, st));
+            dp.b8_out = nullptr;
+            dp.rows_out = nullptr;
+        }
+        CUDA_TRY(launch_dem_kernel(kp, dp, pg->dem_global, grid, smem, st));
         pg->last_launches++;
         return PFS_OK;
     }
@@ -682,6 +700,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
 
     if (pg->demk && injected)
         return fail(PFS_E_INVALID, "the error-model sampler draws its own noise (no injected masks)");
+    if (pg->demk && pg->dem_global && mode == PFS_MODE_COUNTS)
+        return fail(PFS_E_INVALID, "error-model sampler: counts need the output columns in shared memory");
     if (pg->demk && rows_meas)
         return fail(PFS_E_INVALID, "the error-model sampler produces detection events only (use the frame sampler "
                                    "for measurement records)");
@@ -836,7 +856,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     const int64_t dev_pitch = b8 ? ((nbytes + 31) / 32) * 32 : 0;
     int64_t chunk_tiles = n_tiles_all;
     if (!dev_out) {
-        const int64_t bytes_per_tile = ((pg->colk || pg->demk) && b8 ? 0 : R * W * 4) + (b8 ? T * dev_pitch : 0);
+        const bool fused = pg->colk || (pg->demk && !pg->dem_global);  // no tile-major scratch
+        const int64_t bytes_per_tile = (fused && b8 ? 0 : R * W * 4) + (b8 ? T * dev_pitch : 0);
         const int64_t target = (int64_t)256 << 20;
         chunk_tiles = std::max<int64_t>(1, target / std::max<int64_t>(bytes_per_tile, 1));
         chunk_tiles = std::max<int64_t>(chunk_tiles, pg->demk ? (int64_t)pg->dem_grid * 2
@@ -851,7 +872,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     for (int b = 0; b < nbuf; b++) {
         // (+ padding to whole 8-word groups: the word-major transpose reads
         // narrow tiles in groups of 8 words)
-        if (!direct_rows && !((pg->colk || pg->demk) && b8)) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * ((chunk_words + 7) & ~7ll)));
+        if (!direct_rows && !((pg->colk || (pg->demk && !pg->dem_global)) && b8)) CUDA_TRY(pg->d_rows[b].reserve((size_t)std::max<int64_t>(R, 1) * ((chunk_words + 7) & ~7ll)));
         if (b8 && !dev_out) CUDA_TRY(pg->d_b8[b].reserve((size_t)chunk_tiles * T * dev_pitch));
     }
     if (timing) CUDA_TRY(cudaEventRecord(pg->ev[1], st));
@@ -906,7 +927,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             if (rc2) return rc2;
         }
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[3], st));
-        if (b8 && (pg->colk || pg->demk)) {
+        if (b8 && (pg->colk || (pg->demk && !pg->dem_global))) {
             if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
         } else if (b8) {
             uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;

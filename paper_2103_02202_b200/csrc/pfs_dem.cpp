@@ -62,8 +62,9 @@ DemModel build_dem(const pfs_instr* ins, int64_t n_ins, const int32_t* targets, 
             if (m >= 0 && m < num_meas) xor_into(rec_cols[m], Set{(uint32_t)c});
         }
     std::vector<Set> sx(num_qubits), sz(num_qubits);
-    // per noise ordinal: apps x 4 component signatures, filled backwards
-    std::vector<std::vector<Set>> comps(n_noise);
+    // per noise ordinal: apps x 4 component signatures (flat CSR per ordinal),
+    // filled backwards
+    std::vector<std::vector<uint32_t>> cptr(n_noise), ccols(n_noise);
     auto coin = [&](int32_t q, const char* what) {
         if (!sz[q].empty() && dm.coin_dependent.empty())
             dm.coin_dependent = std::string("the ") + what + " coin of qubit " + std::to_string(q) +
@@ -125,13 +126,18 @@ DemModel build_dem(const pfs_instr* ins, int64_t n_ins, const int32_t* targets, 
         case K_NOISE: {
             const int ar = in.code == CH_DEP2 ? 2 : 1;
             const int apps = in.n_targets / ar;
-            std::vector<Set>& cv = comps[in.aux];
-            cv.assign((size_t)apps * 4, Set{});
+            std::vector<uint32_t>& pp = cptr[in.aux];
+            std::vector<uint32_t>& cc = ccols[in.aux];
+            pp.assign(1, 0u);
+            cc.clear();
             for (int a2 = 0; a2 < apps; a2++)
-                for (int s = 0; s < ar; s++) {
-                    const int32_t q = tg[a2 * ar + s];
-                    cv[(size_t)a2 * 4 + 2 * s] = sx[q];
-                    cv[(size_t)a2 * 4 + 2 * s + 1] = sz[q];
+                for (int s = 0; s < 2; s++) {
+                    const bool has = s < ar;
+                    const int32_t q = has ? tg[a2 * ar + s] : 0;
+                    if (has) cc.insert(cc.end(), sx[q].begin(), sx[q].end());
+                    pp.push_back((uint32_t)cc.size());
+                    if (has) cc.insert(cc.end(), sz[q].begin(), sz[q].end());
+                    pp.push_back((uint32_t)cc.size());
                 }
             break;
         }
@@ -145,12 +151,13 @@ DemModel build_dem(const pfs_instr* ins, int64_t n_ins, const int32_t* targets, 
     uint64_t total = 0;
     for (int64_t o = 0; o < n_noise; o++) {
         dm.comp_base[o] = (uint32_t)(dm.comp_ptr.size() - 1);
-        for (const Set& st : comps[o]) {
-            dm.cols.insert(dm.cols.end(), st.begin(), st.end());
-            total += st.size();
-            if (dm.cols.size() > 0xFFFFFFFFull) throw std::invalid_argument("error model too large");
-            dm.comp_ptr.push_back((uint32_t)dm.cols.size());
-        }
+        const uint64_t base = dm.cols.size();
+        if (base + ccols[o].size() > 0xFFFFFFFFull) throw std::invalid_argument("error model too large");
+        dm.cols.insert(dm.cols.end(), ccols[o].begin(), ccols[o].end());
+        total += ccols[o].size();
+        for (size_t k = 1; k < cptr[o].size(); k++) dm.comp_ptr.push_back((uint32_t)(base + cptr[o][k]));
+        std::vector<uint32_t>().swap(ccols[o]);
+        std::vector<uint32_t>().swap(cptr[o]);
     }
     dm.comp_base[n_noise] = (uint32_t)(dm.comp_ptr.size() - 1);
     dm.mean_cols_per_comp = dm.comp_ptr.size() > 1 ? (double)total / (double)(dm.comp_ptr.size() - 1) : 0.0;

@@ -103,22 +103,31 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
     __syncwarp();
 }
 
+// GC: the column words live in the tile-major global scratch kp.ev_out
+// ([tile][col], zeroed by the host, transposed by tiles_to_b8 afterwards)
+template <bool GC>
 __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_constant__ KParams kp,
                                                                 const __grid_constant__ DemParams dp) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const int ncols = kp.num_cols;
-    const int ncw = (ncols + 3) & ~3;
-    uint32_t* const ev = sm;                                    // [ncols] column words of the tile
-    uint32_t* const cnt = ev + ncw;                             // [ncols] (counts mode)
+    const int ncw = GC ? 0 : (ncols + 3) & ~3;
+    uint32_t* const cnt = sm + ncw;                             // [ncols] (counts mode)
     uint32_t* const wscr = cnt + (kp.counts_in_smem ? ncw : 0) + (size_t)warp * 32 * NZ_MAX_LIST;
     uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
     if (kp.counts_in_smem)
         for (int i = threadIdx.x; i < ncols; i += blockDim.x) cnt[i] = 0u;
     for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x) {
         const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
-        for (int i = threadIdx.x; i < ncols; i += blockDim.x) ev[i] = 0u;
-        __syncthreads();
+        // column words of the tile: shared, or the global output rows at
+        // ev_out + col * out_row_stride + tile * out_tile_stride (b8 scratch
+        // [tile][col], or the caller's column-major rows)
+        uint32_t* const ev = GC ? kp.ev_out + (size_t)tile * kp.out_tile_stride : sm;
+        const int64_t cs = GC ? kp.out_row_stride : 1;
+        if (!GC) {
+            for (int i = threadIdx.x; i < ncols; i += blockDim.x) ev[i] = 0u;
+            __syncthreads();
+        }
         for (uint32_t first = 32u * warp; first < (uint32_t)dp.n_items; first += 32u * NW) {
             noise_items_warp(kp, dp.items, (uint32_t)dp.n_items, first, g, wscr, sl, lane,
                              [&](uint32_t o, uint32_t trial, uint32_t pick) {
@@ -130,10 +139,12 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_con
                 for (uint32_t k = 0; k < 4; k++) {
                     if (!((mask >> k) & 1u)) continue;
                     const uint32_t e1 = __ldg(dp.comp_ptr + cb + k + 1);
-                    for (uint32_t e = __ldg(dp.comp_ptr + cb + k); e < e1; e++) atomicXor(ev + __ldg(dp.cols + e), bit);
+                    for (uint32_t e = __ldg(dp.comp_ptr + cb + k); e < e1; e++)
+                        atomicXor(ev + (int64_t)__ldg(dp.cols + e) * cs, bit);
                 }
             });
         }
+        if (GC) continue;  // transposed by tiles_to_b8
         __syncthreads();
         const int64_t rem = kp.num_shots - tile * 32;
         const uint32_t tail = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
@@ -186,11 +197,15 @@ size_t dem_smem_bytes(int warps, int64_t num_cols, bool counts) {
 }
 
 cudaError_t set_dem_kernel_smem(size_t smem) {
-    return cudaFuncSetAttribute(dem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    const cudaError_t e = cudaFuncSetAttribute(dem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    return cudaFuncSetAttribute(dem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
-cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, int grid, size_t smem, cudaStream_t st) {
-    dem_kernel<<<grid, 32 * dp.warps, smem, st>>>(kp, dp);
+cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, bool global_cols, int grid, size_t smem,
+                              cudaStream_t st) {
+    if (global_cols) dem_kernel<true><<<grid, 32 * dp.warps, smem, st>>>(kp, dp);
+    else dem_kernel<false><<<grid, 32 * dp.warps, smem, st>>>(kp, dp);
     return cudaGetLastError();
 }
 

@@ -307,7 +307,8 @@ struct DemParams {
     int32_t n_items;
     int32_t warps;
 };
-cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, int grid, size_t smem, cudaStream_t st);
+cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, bool global_cols, int grid, size_t smem,
+                              cudaStream_t st);
 cudaError_t set_dem_kernel_smem(size_t smem);
 size_t dem_smem_bytes(int warps, int64_t num_cols, bool counts);
 
