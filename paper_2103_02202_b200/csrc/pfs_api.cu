@@ -934,10 +934,13 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             const int64_t pitch = dev_out ? out_pitch : dev_pitch;
             // word-major tiles narrower than 8 words are contiguous word columns:
             // transpose them as 8-word tiles (256-shot blocks per CTA)
-            const int tw = (warpk && W < 8) ? 8 : W;
+            // one-word tiles ([tile][row][1] = [tile][1][row]) are word-major too:
+            // transpose them as 8-word tiles, like the warp kernel's
+            const bool wm = warpk || W == 1;
+            const int tw = (wm && W < 8) ? 8 : W;
             const int64_t ntw = (nt * W + tw - 1) / tw;
             CUDA_TRY(launch_tiles_to_b8(rows, R, tw, ntw, nshots,
-                                        mode == PFS_MODE_SAMPLES ? d_ref : nullptr, dst, pitch, st, warpk));
+                                        mode == PFS_MODE_SAMPLES ? d_ref : nullptr, dst, pitch, st, wm));
             pg->last_launches++;
             if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
         } else if (direct_rows && rows != (uint32_t*)out) {
