@@ -57,6 +57,7 @@ def parse_args():
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-d100", action="store_true", help="skip the config 4 (d=100) extra line")
     ap.add_argument("--no-dem", action="store_true", help="skip the error-model sampler extra line")
+    ap.add_argument("--no-c3", action="store_true", help="skip the config 3 counts extra line")
     return ap.parse_args()
 
 
@@ -311,6 +312,50 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     return res
 
 
+def measure_counts(args, kernel: int, shots: int, steps: int, warmup: int, rank: int, world: int,
+                   local_rank: int):
+    """Config 3 (BASELINE.json): d=5, 5 rounds, p=5e-3, on-device per-column
+    event counts only (no event I/O), `shots` per GPU per step; the per-rank
+    u64 counts are summed with one NCCL all-reduce at the end."""
+    import torch
+
+    from paper_2103_02202_b200.sampler import compile_detector_sampler
+
+    dist = world > 1
+    if dist:
+        import torch.distributed as tdist
+    dev = torch.device("cuda", local_rank)
+    ds = compile_detector_sampler(config_text(3), device=local_rank, kernel=kernel)
+    T = ds.tile_shots
+    counts = torch.zeros(ds.num_columns, dtype=torch.int64, device=dev)
+    base = rank * ((shots + T - 1) // T) * T
+    stream = torch.cuda.current_stream(dev)
+    for i in range(warmup):
+        ds.sample_counts(shots, seed=99 + i, out=counts, shot_offset=base, stream=stream.cuda_stream)
+    torch.cuda.synchronize()
+    if dist:
+        tdist.barrier()
+    torch.cuda.synchronize()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record(stream)
+    for i in range(steps):
+        ds.sample_counts(shots, seed=7 + i, out=counts, shot_offset=base, stream=stream.cuda_stream)
+    if dist:
+        tdist.all_reduce(counts)
+    ev1.record(stream)
+    torch.cuda.synchronize()
+    elapsed = ev0.elapsed_time(ev1) / 1e3
+    if dist:
+        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
+        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
+        elapsed = float(tt.item())
+    rate = float(counts.sum().item()) / max(1, shots * world * steps)  # mean events per shot (last step x world)
+    return {"value": shots * world * steps / elapsed, "unit": "shots/s", "ms_per_step": 1e3 * elapsed / steps,
+            "steps": steps, "shots_per_gpu_per_step": shots, "kernel": ds.info["kernel"],
+            "mean_events_per_shot_last_step": rate * steps}
+
+
 def roofline_of(res, smem_peak, hbm):
     info = res["info"]
     bframe_bytes = info["bframe_bits"] / 8.0
@@ -349,6 +394,14 @@ def run_ours(args, rank, world, local_rank):
         a2.kernel, a2.words, a2.ring, a2.threads, a2.groups = 4, 0, -1, 0, 0
         dem = measure(a2, args.config, shots, max(3, args.steps // 2), args.warmup, rank, world,
                       local_rank, 0)
+    c3 = None
+    if args.config == 2 and not args.no_c3 and args.kernel == 0:
+        c3 = {"workload": WORKLOADS[3] + ", per-column event counts on device (no event I/O), "
+                                        "one u64 all-reduce over ranks",
+              "frame_sampler": measure_counts(args, 1, 1 << 24, max(3, args.steps // 4), 2, rank, world,
+                                              local_rank),
+              "error_model_sampler": measure_counts(args, 4, 1 << 24, max(3, args.steps // 4), 2, rank,
+                                                    world, local_rank)}
     extra = None
     if args.config == 2 and not args.no_d100:
         s4 = gen.CONFIGS[4]["shots"]
@@ -412,6 +465,8 @@ def run_ours(args, rank, world, local_rank):
             "value": dem["value"], "unit": "shots/s", "ms_per_step": 1e3 * dem["elapsed"] / dem["steps"],
             "steps": dem["steps"], "kernel_ms": dem["frame_ms"], "gpu_launches": dem["launches"],
             "clocks": dem["clocks"]}
+    if c3 is not None:
+        line["config3_counts"] = c3
     if not args.no_cpu_baseline:
         cores = host_cores()
         rate, s_shots, dt = cpu_port_rate(config_text(args.config), args.cpu_seconds, cores)

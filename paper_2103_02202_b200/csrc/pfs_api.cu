@@ -80,6 +80,7 @@ struct pfs_program {
     // error-model detector sampler (KERNEL_DEM)
     bool demk = false;
     bool dem_global = false;  // output column words in global memory (too many for shared)
+    bool dem_per_warp = false;  // dem_warp_kernel
     DemModel dem;
     DevBuf<uint32_t> d_comp_base, d_comp_ptr, d_cols, d_items;
     int dem_grid = 0;
@@ -222,6 +223,9 @@ static void choose_layout(pfs_program* pg) {
         if (pg->cfg.smem_bytes > kSmemBudget) {  // d=100: a million columns
             pg->dem_global = true;
             pg->cfg.smem_bytes = dem_smem_bytes(DEM_WARPS_HOST, 0, false);
+        } else if (dem_warp_smem_bytes(DEM_WARPS_HOST, hp.num_cols, true) <= 96 * 1024) {
+            pg->dem_per_warp = true;  // small circuits: a tile per warp
+            pg->cfg.smem_bytes = dem_warp_smem_bytes(DEM_WARPS_HOST, hp.num_cols, false);
         }
         pg->cfg.kernel = 0;
         return;
@@ -578,9 +582,12 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
         dp.n_items = (int32_t)(pg->dem.items.size() / 2);
         dp.warps = DEM_WARPS_HOST;
         kp.n_tiles = nt;
+        dp.per_warp = pg->dem_per_warp ? 1 : 0;
         const size_t smem = pg->dem_global ? dem_smem_bytes(DEM_WARPS_HOST, 0, false)
-                                           : dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, kp.counts_in_smem != 0);
-        const int grid = (int)std::min<int64_t>(pg->dem_grid, nt);
+                          : pg->dem_per_warp ? dem_warp_smem_bytes(DEM_WARPS_HOST, hp.num_cols, kp.counts_in_smem != 0)
+                                             : dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, kp.counts_in_smem != 0);
+        const int grid = (int)std::min<int64_t>(pg->dem_grid,
+                                                pg->dem_per_warp ? (nt + DEM_WARPS_HOST - 1) / DEM_WARPS_HOST : nt);
         if (pg->dem_global) {
             // column words of every tile accumulate in the tile-major scratch
             // [tile][col] (kp.ev_out), transposed afterwards like the frame path
@@ -815,7 +822,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         const size_t extra = (size_t)hp.num_cols * 4;
         kp.counts_in_smem = (!warpk && cfg.smem_bytes + extra <= pg->smem_optin) ? 1 : 0;
         if (pg->demk) {
-            kp.counts_in_smem = dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, true) <= pg->smem_optin;
+            kp.counts_in_smem = (pg->dem_per_warp ? dem_warp_smem_bytes(DEM_WARPS_HOST, hp.num_cols, true)
+                                                  : dem_smem_bytes(DEM_WARPS_HOST, hp.num_cols, true)) <= pg->smem_optin;
         } else if (pg->colk) {
             kp.counts_in_smem = col_smem_bytes(pg->col_nw, col_warp_words(hp.num_qubits, std::max<int64_t>(hp.num_slots, 1), pg->col_ring_smem, pg->col_v),
                                                std::max<uint32_t>(pg->cs.slot_bytes, 16u), hp.num_cols) <= pg->smem_optin;
@@ -860,7 +868,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         const int64_t bytes_per_tile = (fused && b8 ? 0 : R * W * 4) + (b8 ? T * dev_pitch : 0);
         const int64_t target = (int64_t)256 << 20;
         chunk_tiles = std::max<int64_t>(1, target / std::max<int64_t>(bytes_per_tile, 1));
-        chunk_tiles = std::max<int64_t>(chunk_tiles, pg->demk ? (int64_t)pg->dem_grid * 2
+        chunk_tiles = std::max<int64_t>(chunk_tiles, pg->demk ? (int64_t)pg->dem_grid * 2 * (pg->dem_per_warp ? DEM_WARPS_HOST : 1)
                                                    : pg->colk ? (int64_t)pg->col_grid * pg->col_nw
                                                                   : (int64_t)cfg.grid);  // keep every SM busy
         chunk_tiles = std::min(chunk_tiles, n_tiles_all);

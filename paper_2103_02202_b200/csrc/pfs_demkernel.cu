@@ -191,20 +191,98 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_con
     }
 }
 
+// Small circuits (a few hundred output columns): every warp owns its own
+// 32-shot tile and column words, so tiles need no CTA barrier at all.
+__global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_warp_kernel(const __grid_constant__ KParams kp,
+                                                                     const __grid_constant__ DemParams dp) {
+    extern __shared__ __align__(16) uint32_t sm[];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    const int ncols = kp.num_cols;
+    const int ncw = (ncols + 3) & ~3;
+    uint32_t* const cnt = sm;  // [ncols] CTA counts (counts mode)
+    uint32_t* const ev = sm + (kp.counts_in_smem ? ncw : 0) + (size_t)warp * (ncw + 32 * NZ_MAX_LIST);
+    uint32_t* const wscr = ev + ncw;
+    uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
+    if (kp.counts_in_smem)
+        for (int i = threadIdx.x; i < ncols; i += blockDim.x) cnt[i] = 0u;
+    __syncthreads();
+    for (int64_t tile = (int64_t)blockIdx.x * NW + warp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * NW) {
+        const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
+        for (int i = lane; i < ncols; i += 32) ev[i] = 0u;
+        __syncwarp();
+        for (uint32_t first = 0; first < (uint32_t)dp.n_items; first += 32u) {
+            noise_items_warp(kp, dp.items, (uint32_t)dp.n_items, first, g, wscr, sl, lane,
+                             [&](uint32_t o, uint32_t trial, uint32_t pick) {
+                const uint32_t app = trial >> 5, bit = 1u << (trial & 31u);
+                uint32_t xm, zm;
+                pattern_of(__ldg(kp.noise_ch + o), pick, xm, zm);
+                const uint32_t mask = (xm & 1u) | ((zm & 1u) << 1) | ((xm & 2u) << 1) | ((zm & 2u) << 2);
+                const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
+                for (uint32_t k = 0; k < 4; k++) {
+                    if (!((mask >> k) & 1u)) continue;
+                    const uint32_t e1 = __ldg(dp.comp_ptr + cb + k + 1);
+                    for (uint32_t e = __ldg(dp.comp_ptr + cb + k); e < e1; e++) atomicXor(ev + __ldg(dp.cols + e), bit);
+                }
+            });
+        }
+        __syncwarp();
+        const int64_t rem = kp.num_shots - tile * 32;
+        const uint32_t tail = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+        if (kp.counts != nullptr) {
+            for (int c = lane; c < ncols; c += 32) {
+                const uint32_t n = __popc(ev[c] & tail);
+                if (n) {
+                    if (kp.counts_in_smem) atomicAdd(cnt + c, n);
+                    else atomicAdd(kp.counts + c, (unsigned long long)n);
+                }
+            }
+        } else if (dp.b8_out != nullptr) {
+            const int64_t shot = tile * 32 + lane;
+            const bool live = shot < kp.num_shots;
+            const bool aligned = ((dp.b8_pitch | reinterpret_cast<uintptr_t>(dp.b8_out)) & 3) == 0;
+            for (int B = 0; B * 32 < ncols; B++) {
+                const int col = B * 32 + lane;
+                const uint32_t t = transpose32_lane(col < ncols ? ev[col] : 0u, lane);
+                if (!live) continue;
+                uint8_t* p = dp.b8_out + shot * dp.b8_pitch + (int64_t)B * 4;
+                const int64_t nb = dp.b8_bytes - (int64_t)B * 4;
+                if (aligned && nb >= 4) *reinterpret_cast<uint32_t*>(p) = t;
+                else for (int j = 0; j < 4 && j < nb; j++) p[j] = (uint8_t)(t >> (8 * j));
+            }
+        } else if (dp.rows_out != nullptr) {
+            for (int c = lane; c < ncols; c += 32) dp.rows_out[(int64_t)c * dp.rows_stride + tile] = ev[c];
+        }
+        __syncwarp();
+    }
+    if (kp.counts_in_smem) {
+        __syncthreads();
+        for (int i = threadIdx.x; i < ncols; i += blockDim.x)
+            if (cnt[i]) atomicAdd(kp.counts + i, (unsigned long long)cnt[i]);
+    }
+}
+
+size_t dem_warp_smem_bytes(int warps, int64_t num_cols, bool counts) {
+    const size_t ncw = ((size_t)num_cols + 3) & ~(size_t)3;
+    return ((counts ? ncw : 0) + (size_t)warps * (ncw + 32 * NZ_MAX_LIST)) * 4;
+}
+
 size_t dem_smem_bytes(int warps, int64_t num_cols, bool counts) {
     const size_t ncw = ((size_t)num_cols + 3) & ~(size_t)3;
     return (ncw * (counts ? 2 : 1) + (size_t)warps * 32 * NZ_MAX_LIST) * 4;
 }
 
 cudaError_t set_dem_kernel_smem(size_t smem) {
-    const cudaError_t e = cudaFuncSetAttribute(dem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaError_t e = cudaFuncSetAttribute(dem_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    e = cudaFuncSetAttribute(dem_warp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     return cudaFuncSetAttribute(dem_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
 }
 
 cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, bool global_cols, int grid, size_t smem,
                               cudaStream_t st) {
-    if (global_cols) dem_kernel<true><<<grid, 32 * dp.warps, smem, st>>>(kp, dp);
+    if (dp.per_warp) dem_warp_kernel<<<grid, 32 * dp.warps, smem, st>>>(kp, dp);
+    else if (global_cols) dem_kernel<true><<<grid, 32 * dp.warps, smem, st>>>(kp, dp);
     else dem_kernel<false><<<grid, 32 * dp.warps, smem, st>>>(kp, dp);
     return cudaGetLastError();
 }

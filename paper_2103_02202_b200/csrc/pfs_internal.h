@@ -306,10 +306,12 @@ struct DemParams {
     const uint2* items;          // (noise ordinal, chunk) work items of one tile
     int32_t n_items;
     int32_t warps;
+    int32_t per_warp;            // dem_warp_kernel: one 32-shot tile per warp (small circuits)
 };
 cudaError_t launch_dem_kernel(const KParams& kp, const DemParams& dp, bool global_cols, int grid, size_t smem,
                               cudaStream_t st);
 cudaError_t set_dem_kernel_smem(size_t smem);
 size_t dem_smem_bytes(int warps, int64_t num_cols, bool counts);
+size_t dem_warp_smem_bytes(int warps, int64_t num_cols, bool counts);
 
 }  // namespace pfs
