@@ -171,6 +171,14 @@ void pfs_program_destroy(struct pfs_program* prog);
 const char* pfs_last_error(void);
 int pfs_version(void);
 
+/* write_table on the GPU (stabsim/io_formats.py:66-201): shot-major b8 rows
+ * (host or device, in_pitch bytes apart) -> fmt 0 "01", 2 "hits", 3 "r8",
+ * byte-exact with the reference writers.  out == NULL (or too small): only
+ * *out_len is set (the bytes needed).  b8 needs no writer (it is the input). */
+int pfs_write_format(int device, const uint8_t* b8, int64_t in_pitch, int64_t num_shots,
+                     int64_t num_results, int fmt, uint8_t* out, int64_t out_capacity,
+                     int64_t* out_len, void* stream);
+
 /* ---- native reference sample (stabsim/tableau_sim.py:326-329) ----------
  * Noiseless inverse-tableau simulation of a circuit lowered to rows
  * (gate code, n_targets, target offset) x int32; noise and annotations are

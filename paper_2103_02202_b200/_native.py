@@ -57,7 +57,7 @@ EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_schedule
            "pfs_program_last_timing", "pfs_program_last_launches", "pfs_program_destroy",
            "pfs_last_error", "pfs_version", "pfs_measure_smem_bandwidth",
            "pfs_detector_events", "pfs_program_op_clock", "pfs_program_ops",
-           "pfs_reference_sample", "pfs_reference_sample_error")
+           "pfs_reference_sample", "pfs_reference_sample_error", "pfs_write_format")
 
 _lib = None
 
@@ -96,6 +96,8 @@ def lib():
     L.pfs_program_op_clock.restype = ctypes.c_int
     L.pfs_program_ops.argtypes = [P, P, i64]
     L.pfs_program_ops.restype = ctypes.c_int
+    L.pfs_write_format.argtypes = [ctypes.c_int, P, i64, i64, i64, ctypes.c_int, P, i64, ctypes.POINTER(i64), P]
+    L.pfs_write_format.restype = ctypes.c_int
     L.pfs_reference_sample.argtypes = [P, i64, P, i64, i32, P, i64, P, P, i64, ctypes.POINTER(i64)]
     L.pfs_reference_sample.restype = ctypes.c_int
     L.pfs_reference_sample_error.argtypes = []

@@ -1060,6 +1060,50 @@ extern "C" int pfs_detector_events(int device, const uint8_t* flips_b8, int64_t 
     return PFS_OK;
 }
 
+// write_table (stabsim/io_formats.py:198-201) on the GPU for 01 / hits / r8.
+extern "C" int pfs_write_format(int device, const uint8_t* b8, int64_t in_pitch, int64_t num_shots,
+                                int64_t num_results, int fmt, uint8_t* out, int64_t out_capacity,
+                                int64_t* out_len, void* stream_v) {
+    if (!out_len) return fail(PFS_E_INVALID, "out_len is null");
+    *out_len = 0;
+    if (fmt != 0 && fmt != 2 && fmt != 3) return fail(PFS_E_INVALID, "device writers: fmt 0 (01), 2 (hits), 3 (r8)");
+    if (num_shots < 0 || num_results < 0) return fail(PFS_E_INVALID, "negative size");
+    const int64_t nb = (num_results + 7) / 8;
+    if (in_pitch == 0) in_pitch = nb;
+    if (in_pitch < nb) return fail(PFS_E_INVALID, "pitch too small");
+    if (num_shots == 0) return PFS_OK;
+    if (!b8) return fail(PFS_E_INVALID, "null input");
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) return fail(PFS_E_NODEVICE, "no CUDA device available");
+    CUDA_TRY(cudaSetDevice(device));
+    cudaStream_t st = (cudaStream_t)stream_v;
+    const bool in_dev = is_device_ptr(b8);
+    const uint8_t* d_in = b8;
+    uint8_t* tmp_in = nullptr;
+    if (!in_dev) {
+        CUDA_TRY(cudaMalloc(&tmp_in, (size_t)num_shots * in_pitch));
+        CUDA_TRY(cudaMemcpyAsync(tmp_in, b8, (size_t)(num_shots - 1) * in_pitch + nb, cudaMemcpyHostToDevice, st));
+        d_in = tmp_in;
+    }
+    int64_t len = 0;
+    cudaError_t e = write_format(d_in, in_pitch, num_shots, num_results, fmt, nullptr, 0, &len, st);
+    uint8_t* d_out = nullptr;
+    if (e == cudaSuccess && out && out_capacity >= len && len > 0) {
+        const bool out_dev = is_device_ptr(out);
+        if (out_dev) d_out = out;
+        else e = cudaMalloc(&d_out, (size_t)len);
+        if (e == cudaSuccess) e = write_format(d_in, in_pitch, num_shots, num_results, fmt, d_out, len, &len, st);
+        if (e == cudaSuccess && !out_dev) e = cudaMemcpyAsync(out, d_out, (size_t)len, cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        if (!out_dev && d_out) cudaFree(d_out);
+    }
+    if (tmp_in) { cudaStreamSynchronize(st); cudaFree(tmp_in); }
+    CUDA_TRY(e);
+    *out_len = len;
+    if (out && out_capacity < len) return fail(PFS_E_INVALID, "output buffer too small: need " + std::to_string(len) + " bytes");
+    return PFS_OK;
+}
+
 // Profiling: the per-op clock64 trace recorded by the last pfs_run with
 // options.debug_skip bit 6 (CTA 0, group 0, first tile).
 extern "C" int pfs_program_op_clock(pfs_program* pg, long long* out, int64_t n) {

@@ -314,4 +314,8 @@ cudaError_t set_dem_kernel_smem(size_t smem);
 size_t dem_smem_bytes(int warps, int64_t num_cols, bool counts);
 size_t dem_warp_smem_bytes(int warps, int64_t num_cols, bool counts);
 
+// output writers (pfs_writers.cu): device b8 -> 01 (fmt 0), hits (2), r8 (3)
+cudaError_t write_format(const uint8_t* in, int64_t pitch, int64_t shots, int64_t R, int fmt, uint8_t* out,
+                         int64_t capacity, int64_t* out_len, cudaStream_t st);
+
 }  // namespace pfs

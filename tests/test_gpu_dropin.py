@@ -102,3 +102,34 @@ def test_compile_sampler_native_reference():
     assert np.array_equal(smp[0, fixed], ref[fixed])
     for ds in detector_sets(c):
         assert not np.any(smp[:, list(ds)].sum(axis=1) % 2)
+
+
+@pytest.mark.parametrize("R", [1, 7, 8, 31, 33, 255, 256, 300, 1023, 2000])
+@pytest.mark.parametrize("density", [0.0, 0.002, 0.05, 0.5, 1.0])
+def test_device_writers_match_reference_formats(R, density):
+    # write_table on the GPU (01 / hits / r8) equals the host writers, which are
+    # byte-exact with the reference's (io_formats.py:66-187)
+    from paper_2103_02202_b200.io_formats import SampleTable, write_table, write_table_device
+
+    rng = np.random.default_rng(R * 7 + int(density * 1000))
+    shots = 97
+    mat = (rng.random((shots, R)) < density).astype(np.uint8)
+    t = SampleTable.from_numpy(mat)
+    for fmt in ("01", "hits", "r8", "b8"):
+        assert write_table_device(t.b8, R, fmt) == write_table(t, fmt), fmt
+
+
+def test_device_writers_on_sampled_events():
+    import torch
+    from paper_2103_02202_b200 import generators as gen
+    from paper_2103_02202_b200.io_formats import SampleTable, write_table, write_table_device
+    from paper_2103_02202_b200.sampler import compile_detector_sampler
+
+    ds = compile_detector_sampler(gen.surface_code_memory(9, 9, 5e-3))
+    nb = (ds.num_columns + 7) // 8
+    dev = torch.empty((5000, nb), dtype=torch.uint8, device="cuda")
+    ds.sample(5000, seed=1, out=dev)
+    host = dev.cpu().numpy()
+    t = SampleTable.from_b8(host, ds.num_columns)
+    for fmt in ("hits", "r8", "01"):
+        assert write_table_device(dev, ds.num_columns, fmt) == write_table(t, fmt)
