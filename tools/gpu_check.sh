@@ -1,0 +1,11 @@
+# Round-end style GPU validation: gpu tests, default bench, launch list (helper).
+set -x
+mkdir -p gpurun_out
+timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+tail -3 gpurun_out/gpu_tests.log
+timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"
+tail -1 gpurun_out/bench_default.log
+timeout 300 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/bench_ref.log 2>&1; echo "ref rc=$?"
+tail -1 gpurun_out/bench_ref.log
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv \
+  python bench.py --steps 3 --warmup 3 --no-e2e --no-d100 --no-cpu-baseline --no-c3 > gpurun_out/ncu.log 2>&1; echo "ncu rc=$?"
