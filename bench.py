@@ -58,6 +58,7 @@ def parse_args():
     ap.add_argument("--no-d100", action="store_true", help="skip the config 4 (d=100) extra line")
     ap.add_argument("--no-dem", action="store_true", help="skip the error-model sampler extra line")
     ap.add_argument("--no-c3", action="store_true", help="skip the config 3 counts extra line")
+    ap.add_argument("--pipeline", type=int, default=0, help="noise/frame pipeline sub-chunks (0 auto, 1 off)")
     return ap.parse_args()
 
 
@@ -223,7 +224,7 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     flat = flatten(config_text(cfg))
     compile_s = time.perf_counter() - t0
     kw = dict(words_per_tile=args.words, ring_in_smem=args.ring, threads=args.threads,
-              noise_target_hits=args.target_hits, kernel=args.kernel, groups=args.groups)
+              noise_target_hits=args.target_hits, kernel=args.kernel, groups=args.groups, pipeline=args.pipeline)
     ds = DetectorSampler.__new__(DetectorSampler)
     ds.circuit, ds.flat, ds.device = None, flat, local_rank
     ds._seeds = np.random.default_rng(0)

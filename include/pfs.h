@@ -56,7 +56,10 @@ typedef struct pfs_options {
     int32_t kernel;           /* frame kernel: 0 auto, 1 cooperative (a CTA's threads
                                  share one tile), 2 warp-private (a warp owns one
                                  32-shot word column, no CTA barriers)               */
-    int32_t reserved[2];
+    int32_t pipeline;         /* noise/frame pipeline: sub-chunks per launch whose
+                                 noise_kernel overlaps the previous sub-chunk's
+                                 frame kernel (0 = auto, 1 = off)                   */
+    int32_t reserved[1];
 } pfs_options;
 
 typedef struct pfs_info {

@@ -95,6 +95,13 @@ struct pfs_program {
     DevBuf<uint32_t> d_refw;
     cudaStream_t copy_stream = nullptr;
     cudaEvent_t ev[10] = {};
+    // noise/frame pipeline: noise_kernel of sub-chunk i+1 on noise_stream while
+    // frame_kernel of sub-chunk i runs; two hit-list buffers
+    cudaStream_t noise_stream = nullptr;
+    int pipe_default = 1;
+    cudaEvent_t pev[5] = {};  // [0] entry, [1..2] noise done, [3..4] frame done
+    DevBuf<uint64_t> d_hits2;
+    DevBuf<uint32_t> d_ncnt2;
     double last_ms[6] = {0, 0, 0, 0, 0, 0};
     int64_t last_launches = 0;
 };
@@ -140,6 +147,11 @@ static void choose_warp_layout(pfs_program* pg) {
 constexpr uint32_t kColSlotCap = 16384;
 constexpr int kColMinWarps = 4;
 constexpr bool kColAuto = false;  // auto layout picks the column kernel
+// noise/frame pipeline sub-chunks per launch (pfs_options.pipeline overrides):
+// noise_kernel of sub-chunk i+1 (16 KB shared, 8 warps) runs in the room a
+// 640-thread frame CTA leaves on its SM while frame_kernel works on sub-chunk i
+constexpr int kPipeChunks = 6;
+constexpr int kPipeFrameThreads = 640;
 constexpr int DEM_WARPS_HOST = 16;  // dem_kernel's warps (DEM_WARPS)
 
 static uint32_t col_max_block_bytes(const HostProgram& hp) {
@@ -284,7 +296,15 @@ static void choose_layout(pfs_program* pg) {
     pg->cfg.groups = G;
     pg->cfg.ring_smem = rs;
     pg->cfg.smem_bytes = W > 0 ? need(W, G, rs) : 0;
-    int threads = o.threads > 0 ? std::min(o.threads, FRAME_MAX_THREADS) : FRAME_MAX_THREADS;
+    // default threads: all 768 without sampled noise; with it, 640 so that a
+    // noise_kernel CTA fits beside the frame CTA (pipelined launch_tiles)
+    // (measured: d=25, two groups, 12.46 -> 11.83 ms per 2^20 shots; a one-group
+    // layout loses more frame-kernel speed with 640 threads than it hides:
+    // d=100 80.8 -> 87.1 ms, so it keeps 768 threads and no pipeline)
+    const bool pipelined = hp.num_noise > 0 && (o.pipeline > 1 || (o.pipeline == 0 && G >= 2));
+    pg->pipe_default = pipelined ? kPipeChunks : 1;
+    int threads = o.threads > 0 ? std::min(o.threads, FRAME_MAX_THREADS)
+                                : (pipelined ? kPipeFrameThreads : FRAME_MAX_THREADS);
     threads = (threads / (32 * G)) * 32 * G;  // whole warps per group
     pg->cfg.threads = threads;
     pg->cfg.kernel = KERNEL_COOP;
@@ -454,8 +474,11 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         pg->d_cstream.release(); pg->d_binfo.release(); pg->d_refw.release();
         pg->d_comp_base.release(); pg->d_comp_ptr.release(); pg->d_cols.release(); pg->d_items.release();
+        pg->d_hits2.release(); pg->d_ncnt2.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
+        if (pg->noise_stream) cudaStreamDestroy(pg->noise_stream);
         for (auto& e : pg->ev) if (e) cudaEventDestroy(e);
+        for (auto& e : pg->pev) if (e) cudaEventDestroy(e);
         if (prev >= 0) cudaSetDevice(prev);
     }
     delete pg;
@@ -547,7 +570,9 @@ static int ensure_device(pfs_program* pg, int device) {
         pg->col_grid = pg->num_sms * per_sm;
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&pg->noise_stream, cudaStreamNonBlocking));
     for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
+    for (auto& e : pg->pev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pg->device = device;
     return PFS_OK;
 }
@@ -630,15 +655,28 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
     const int64_t T = 32 * W;
     const bool pregen = !injected && !hp.pregen_ops.empty() && !(pg->opts.debug_skip & 2);
     int64_t sub = nt;
+    // pipeline depth: sub-chunks per launch_tiles call (1 = noise, then frame)
+    const int pipe = pg->opts.pipeline > 0 ? pg->opts.pipeline : cfg.kernel == KERNEL_COOP ? pg->pipe_default : 1;
+    const int64_t per_wave = (int64_t)cfg.grid * std::max(cfg.groups, 1);
+    const bool piped = pregen && !time_noise && pipe > 1 && nt >= 2 * per_wave;
     if (pregen) {
         const int64_t per_tile = hp.hit_capacity * 8 + hp.num_noise * 4;
-        const int64_t budget = (int64_t)1536 << 20;
+        const int64_t budget = (int64_t)(piped ? 768 : 1536) << 20;
         sub = std::max<int64_t>(cfg.grid, budget / std::max<int64_t>(per_tile, 1));
+        if (piped)  // whole waves of tiles per sub-chunk
+            sub = std::min(sub, ((nt + pipe - 1) / pipe + per_wave - 1) / per_wave * per_wave);
         sub = std::min(sub, nt);
         CUDA_TRY(pg->d_hits.reserve((size_t)std::max<int64_t>(hp.hit_capacity, 1) * sub));
         CUDA_TRY(pg->d_ncnt.reserve((size_t)std::max<int64_t>(hp.num_noise, 1) * sub));
+        if (piped) {
+            CUDA_TRY(pg->d_hits2.reserve((size_t)std::max<int64_t>(hp.hit_capacity, 1) * sub));
+            CUDA_TRY(pg->d_ncnt2.reserve((size_t)std::max<int64_t>(hp.num_noise, 1) * sub));
+            CUDA_TRY(cudaEventRecord(pg->pev[0], st));  // everything before this call
+            CUDA_TRY(cudaStreamWaitEvent(pg->noise_stream, pg->pev[0], 0));
+        }
     }
-    for (int64_t s0 = 0; s0 < nt; s0 += sub) {
+    int64_t it = 0;
+    for (int64_t s0 = 0; s0 < nt; s0 += sub, it++) {
         const int64_t ns = std::min(sub, nt - s0);
         KParams k2 = kp;
         k2.n_tiles = ns;
@@ -648,7 +686,18 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
         if (k2.ev_out) k2.ev_out += s0 * kp.out_tile_stride;
         if (k2.coins) k2.coins += s0 * W;
         if (k2.masks) k2.masks += s0 * W;
-        if (pregen) {
+        if (piped) {
+            const int b = (int)(it & 1);
+            cudaStream_t nst = pg->noise_stream;
+            k2.hits_global = b ? pg->d_hits2.p : pg->d_hits.p;
+            k2.ncnt_global = b ? pg->d_ncnt2.p : pg->d_ncnt.p;
+            if (it >= 2) CUDA_TRY(cudaStreamWaitEvent(nst, pg->pev[3 + b], 0));  // buffer b consumed
+            CUDA_TRY(cudaMemsetAsync(k2.ncnt_global, 0, (size_t)hp.num_noise * ns * 4, nst));
+            CUDA_TRY(launch_noise_kernel(W, k2, ns, nst));
+            CUDA_TRY(cudaEventRecord(pg->pev[1 + b], nst));
+            CUDA_TRY(cudaStreamWaitEvent(st, pg->pev[1 + b], 0));
+            pg->last_launches++;
+        } else if (pregen) {
             k2.hits_global = pg->d_hits.p;
             k2.ncnt_global = pg->d_ncnt.p;
             CUDA_TRY(cudaMemsetAsync(pg->d_ncnt.p, 0, (size_t)hp.num_noise * ns * 4, st));
@@ -667,6 +716,7 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
             lc.grid = (int)std::min<int64_t>(cfg.grid, (ns + cfg.groups - 1) / cfg.groups);
             CUDA_TRY(launch_frame_kernel(lc, k2, st));
         }
+        if (piped) CUDA_TRY(cudaEventRecord(pg->pev[3 + (it & 1)], st));
         pg->last_launches++;
     }
     return PFS_OK;

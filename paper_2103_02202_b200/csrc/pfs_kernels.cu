@@ -265,7 +265,7 @@ __device__ __forceinline__ void noise_prepass(const KParams& kp, uint32_t g, uin
         __syncwarp();
         if (dup) {  // redraw every position of this chunk (attempts >= 1), same slots
             const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
-            uint32_t* sl = wscr + 32 * NZ_MAX_LIST + lane * NZ_MAX_LIST;
+            uint32_t sl[NZ_MAX_LIST];  // rare path: per-lane local memory
             for (uint32_t attempt = 1; dup; attempt++) {
                 dup = false;
                 uint32_t blk = 0xFFFFFFFFu, b0 = 0, b1 = 0, b2 = 0, b3 = 0;
@@ -316,7 +316,7 @@ constexpr int NZ_ITEMS_PER_WARP = 4;
 #endif
 template <int W>
 __global__ void __launch_bounds__(256, NZ_MIN_BLOCKS) noise_kernel(const __grid_constant__ KParams kp) {
-    __shared__ uint32_t wscr_all[8][64 * NZ_MAX_LIST];
+    __shared__ uint32_t wscr_all[8][32 * NZ_MAX_LIST];  // 16 KB: fits beside a frame CTA
     const int warp = threadIdx.x >> 5;
     const int64_t tile = blockIdx.y;
     const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
