@@ -97,9 +97,11 @@ struct pfs_program {
     cudaEvent_t ev[10] = {};
     // noise/frame pipeline: noise_kernel of sub-chunk i+1 on noise_stream while
     // frame_kernel of sub-chunk i runs; two hit-list buffers
-    cudaStream_t noise_stream = nullptr;
+    cudaStream_t noise_stream = nullptr;   // low priority
+    cudaStream_t frame_stream = nullptr;   // high priority: frame CTAs claim freed SMs first
+    cudaStream_t tr_stream = nullptr;      // low priority: per-sub-chunk transposes
     int pipe_default = 1;
-    cudaEvent_t pev[5] = {};  // [0] entry, [1..2] noise done, [3..4] frame done
+    cudaEvent_t pev[7] = {};  // [0] entry, [1..2] noise done, [3..4] frame done, [5] frame end, [6] transposes end
     DevBuf<uint64_t> d_hits2;
     DevBuf<uint32_t> d_ncnt2;
     double last_ms[6] = {0, 0, 0, 0, 0, 0};
@@ -477,6 +479,8 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_hits2.release(); pg->d_ncnt2.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
         if (pg->noise_stream) cudaStreamDestroy(pg->noise_stream);
+        if (pg->frame_stream) cudaStreamDestroy(pg->frame_stream);
+        if (pg->tr_stream) cudaStreamDestroy(pg->tr_stream);
         for (auto& e : pg->ev) if (e) cudaEventDestroy(e);
         for (auto& e : pg->pev) if (e) cudaEventDestroy(e);
         if (prev >= 0) cudaSetDevice(prev);
@@ -570,7 +574,13 @@ static int ensure_device(pfs_program* pg, int device) {
         pg->col_grid = pg->num_sms * per_sm;
     }
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
-    CUDA_TRY(cudaStreamCreateWithFlags(&pg->noise_stream, cudaStreamNonBlocking));
+    {
+        int least = 0, greatest = 0;
+        CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+        CUDA_TRY(cudaStreamCreateWithPriority(&pg->noise_stream, cudaStreamNonBlocking, least));
+        CUDA_TRY(cudaStreamCreateWithPriority(&pg->tr_stream, cudaStreamNonBlocking, least));
+        CUDA_TRY(cudaStreamCreateWithPriority(&pg->frame_stream, cudaStreamNonBlocking, greatest));
+    }
     for (auto& e : pg->ev) CUDA_TRY(cudaEventCreate(&e));
     for (auto& e : pg->pev) CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     pg->device = device;
@@ -589,8 +599,21 @@ static bool is_device_ptr(const void* p) {
 // Run nt tiles: noise_kernel (per-tile hit lists) then frame_kernel, in
 // sub-chunks bounded by the hit-list buffer budget.  kp describes tile 0 of
 // the range (tile_offset, output and inject pointers, num_shots).
+// Shot-major b8 transposition of the launch's tile-major scratch, handed to a
+// pipelined launch_tiles so that each sub-chunk's transpose overlaps the next
+// sub-chunk's frame kernel (done = true when it was issued there).
+struct TransposeJob {
+    const uint32_t* rows = nullptr;  // [tile][row][W] scratch of tile 0 of the launch
+    int64_t R = 0;
+    const uint8_t* xor_bits = nullptr;
+    uint8_t* dst = nullptr;          // row of shot 0 of the launch
+    int64_t pitch = 0;
+    bool done = false;
+};
+
 static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64_t nt, bool injected,
-                        cudaStream_t st, bool time_noise, ColParams cp = ColParams{}) {
+                        cudaStream_t st, bool time_noise, ColParams cp = ColParams{},
+                        TransposeJob* tj = nullptr) {
     const HostProgram& hp = pg->hp;
     if (pg->demk) {
         // error-model sampler: noise hits XOR their output signatures, one launch
@@ -673,8 +696,11 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
             CUDA_TRY(pg->d_ncnt2.reserve((size_t)std::max<int64_t>(hp.num_noise, 1) * sub));
             CUDA_TRY(cudaEventRecord(pg->pev[0], st));  // everything before this call
             CUDA_TRY(cudaStreamWaitEvent(pg->noise_stream, pg->pev[0], 0));
+            CUDA_TRY(cudaStreamWaitEvent(pg->frame_stream, pg->pev[0], 0));
+            if (tj) CUDA_TRY(cudaStreamWaitEvent(pg->tr_stream, pg->pev[0], 0));
         }
     }
+    cudaStream_t fst = piped ? pg->frame_stream : st;
     int64_t it = 0;
     for (int64_t s0 = 0; s0 < nt; s0 += sub, it++) {
         const int64_t ns = std::min(sub, nt - s0);
@@ -695,7 +721,7 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
             CUDA_TRY(cudaMemsetAsync(k2.ncnt_global, 0, (size_t)hp.num_noise * ns * 4, nst));
             CUDA_TRY(launch_noise_kernel(W, k2, ns, nst));
             CUDA_TRY(cudaEventRecord(pg->pev[1 + b], nst));
-            CUDA_TRY(cudaStreamWaitEvent(st, pg->pev[1 + b], 0));
+            CUDA_TRY(cudaStreamWaitEvent(fst, pg->pev[1 + b], 0));
             pg->last_launches++;
         } else if (pregen) {
             k2.hits_global = pg->d_hits.p;
@@ -711,13 +737,31 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
         if (cfg.kernel == KERNEL_WARP) {
             const int64_t nw = cfg.threads / 32;
             lc.grid = (int)std::min<int64_t>(cfg.grid, (ns * W + nw - 1) / nw);
-            CUDA_TRY(launch_frame_warp_kernel(lc, k2, st));
+            CUDA_TRY(launch_frame_warp_kernel(lc, k2, fst));
         } else {
             lc.grid = (int)std::min<int64_t>(cfg.grid, (ns + cfg.groups - 1) / cfg.groups);
-            CUDA_TRY(launch_frame_kernel(lc, k2, st));
+            CUDA_TRY(launch_frame_kernel(lc, k2, fst));
         }
-        if (piped) CUDA_TRY(cudaEventRecord(pg->pev[3 + (it & 1)], st));
         pg->last_launches++;
+        if (piped) {
+            CUDA_TRY(cudaEventRecord(pg->pev[3 + (it & 1)], fst));
+            if (tj) {
+                CUDA_TRY(cudaStreamWaitEvent(pg->tr_stream, pg->pev[3 + (it & 1)], 0));
+                CUDA_TRY(launch_tiles_to_b8(tj->rows + s0 * kp.out_tile_stride, tj->R, W, ns, k2.num_shots,
+                                            tj->xor_bits, tj->dst + s0 * T * tj->pitch, tj->pitch,
+                                            pg->tr_stream, false));
+                pg->last_launches++;
+            }
+        }
+    }
+    if (piped) {  // the caller's stream resumes after the last frame launch and transpose
+        CUDA_TRY(cudaEventRecord(pg->pev[5], fst));
+        CUDA_TRY(cudaStreamWaitEvent(st, pg->pev[5], 0));
+        if (tj) {
+            CUDA_TRY(cudaEventRecord(pg->pev[6], pg->tr_stream));
+            CUDA_TRY(cudaStreamWaitEvent(st, pg->pev[6], 0));
+            tj->done = true;
+        }
     }
     return PFS_OK;
 }
@@ -980,12 +1024,24 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             kp.ev_out = rows_meas ? nullptr : rows;
         }
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[2], st));
+        TransposeJob tj;
+        const bool wm = warpk || W == 1;
+        const bool tj_ok = b8 && !pg->colk && !pg->demk && !wm && kp.out_row_stride == W;
+        if (tj_ok) {
+            tj.rows = rows;
+            tj.R = R;
+            tj.xor_bits = mode == PFS_MODE_SAMPLES ? d_ref : nullptr;
+            tj.dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
+            tj.pitch = dev_out ? out_pitch : dev_pitch;
+        }
         {
-            int rc2 = launch_tiles(pg, kp, cfg, nt, injected, st, timing && ci == 0, cpx);
+            int rc2 = launch_tiles(pg, kp, cfg, nt, injected, st, timing && ci == 0, cpx, tj_ok ? &tj : nullptr);
             if (rc2) return rc2;
         }
         if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[3], st));
         if (b8 && (pg->colk || (pg->demk && !pg->dem_global))) {
+            if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
+        } else if (b8 && tj.done) {
             if (timing && ci == 0) CUDA_TRY(cudaEventRecord(pg->ev[5], st));
         } else if (b8) {
             uint8_t* dst = dev_out ? (uint8_t*)out + shots0 * out_pitch : pg->d_b8[b].p;
@@ -994,7 +1050,6 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
             // transpose them as 8-word tiles (256-shot blocks per CTA)
             // one-word tiles ([tile][row][1] = [tile][1][row]) are word-major too:
             // transpose them as 8-word tiles, like the warp kernel's
-            const bool wm = warpk || W == 1;
             const int tw = (wm && W < 8) ? 8 : W;
             const int64_t ntw = (nt * W + tw - 1) / tw;
             CUDA_TRY(launch_tiles_to_b8(rows, R, tw, ntw, nshots,

@@ -1166,8 +1166,12 @@ __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __rest
                                                           uint8_t* __restrict__ out, int64_t pitch) {
     constexpr int Wp = W + 1;
     constexpr int PARTS = TW / W;
-    __shared__ uint32_t tin[256 * Wp];
-    __shared__ uint32_t tout[32 * W * 9];
+    // tin and tout share one buffer (the transposed words wait in registers
+    // across a barrier): ~9 KB at W = 8, so a CTA fits beside a frame CTA
+    constexpr int TIN = 256 * Wp, TOUT = 32 * W * 9;
+    __shared__ uint32_t tbuf[TIN > TOUT ? TIN : TOUT];
+    uint32_t* const tin = tbuf;
+    uint32_t* const tout = tbuf;
     const int t = threadIdx.x;
     // row block fastest: the CTAs writing one shot's consecutive 32-byte runs
     // run together, so their sectors merge into whole lines in L2
@@ -1211,12 +1215,17 @@ __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __rest
     for (int k = 0; k < W; k++) tin[r * Wp + k] = v[k];
     __syncthreads();
     const int warp = t >> 5, lane = t & 31;
+    uint32_t xt[W];  // pairs warp, warp + 8, ... (8 W pairs over 8 warps)
 #pragma unroll
-    for (int pair = warp; pair < 8 * W; pair += 8) {
-        const int rb = pair / W, w = pair % W;
-        uint32_t x = tin[(rb * 32 + lane) * Wp + w];
-        x = transpose32_lane(x, lane);
-        tout[(w * 32 + lane) * 9 + rb] = x;
+    for (int k = 0; k < W; k++) {
+        const int pair = warp + 8 * k, rb = pair / W, w = pair % W;
+        xt[k] = transpose32_lane(tin[(rb * 32 + lane) * Wp + w], lane);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < W; k++) {
+        const int pair = warp + 8 * k, rb = pair / W, w = pair % W;
+        tout[(w * 32 + lane) * 9 + rb] = xt[k];
     }
     __syncthreads();
     const int64_t nbytes = (num_rows + 7) >> 3;
