@@ -1,6 +1,7 @@
 import csv,sys,subprocess
 rep=sys.argv[1]
-out=subprocess.run(['ncu','-i',rep,'--page','source','--csv','--print-source','sass'],capture_output=True,text=True).stdout
+extra=sys.argv[3:] if len(sys.argv)>3 else []
+out=subprocess.run(['ncu','-i',rep,'--page','source','--csv','--print-source','sass']+extra,capture_output=True,text=True).stdout
 rows=list(csv.reader(out.splitlines()))
 hdr=rows[1]; c={k:j for j,k in enumerate(hdr)}
 data=[r for r in rows[2:] if len(r)==len(hdr)]
