@@ -204,16 +204,6 @@ __device__ __forceinline__ void mbar_wait_backoff(uint64_t* mbar, uint32_t parit
     }
 }
 
-__device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile("{\n\t.reg .pred p;\n\t"
-                     "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-                     "selp.u32 %0, 1, 0, p;\n\t}"
-                     : "=r"(done) : "r"(smem_addr(mbar)), "r"(parity) : "memory");
-    }
-}
-
 
 __device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
     // lane l holds row l (bit b = column b); afterwards lane l holds column l.

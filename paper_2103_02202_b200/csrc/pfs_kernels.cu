@@ -133,10 +133,6 @@ __device__ __forceinline__ void apply_entry(uint32_t* X, uint32_t* Z, uint64_t e
     if (zm & 2u) atomicXor(Z + (size_t)q1 * W + w, bit);
 }
 
-__device__ __forceinline__ void consumer_sync(int nthreads) {
-    asm volatile("bar.sync 1, %0;" ::"r"(nthreads) : "memory");
-}
-
 // Sample the pre-generated noise ops of global tile g into hit lists.
 // Data-parallel per warp: a work item is 32 consecutive chunks of one op (lane
 // l owns chunk 32*item + l).  (1) every lane draws its chunk's Philox block 0
