@@ -135,8 +135,8 @@ def test_device_writers_on_sampled_events():
         assert write_table_device(dev, ds.num_columns, fmt) == write_table(t, fmt)
 
 
-@pytest.mark.parametrize("d,shots", [(5, 1 << 21), (25, 1 << 19)])
-def test_noise_frame_pipeline_bit_exact(d, shots):
+@pytest.mark.parametrize("d,shots,offset_tiles", [(5, 1 << 21, 0), (25, 1 << 19, 0), (25, (1 << 19) + 12345, 3)])
+def test_noise_frame_pipeline_bit_exact(d, shots, offset_tiles):
     """The pipelined launch (noise_kernel of sub-chunk i+1 on a second stream,
     two hit-list buffers) gives the same events as noise-then-frame per launch,
     also across the layout change it brings (640 vs 768 threads)."""
@@ -147,18 +147,19 @@ def test_noise_frame_pipeline_bit_exact(d, shots):
     text = gen.surface_code_memory(d, d, 2e-3)
     s1 = compile_detector_sampler(text, pipeline=1)
     nb = (s1.num_columns + 7) // 8
+    off = offset_tiles * s1.info["tile_shots"]
     dev = torch.empty((shots, nb), dtype=torch.uint8, device="cuda")
-    s1.sample(shots, seed=77, out=dev)
+    s1.sample(shots, seed=77, out=dev, shot_offset=off)
     torch.cuda.synchronize()
     ref = dev.cpu().numpy()
     for pipe in (0, 3, 7):
         dev.zero_()
-        compile_detector_sampler(text, pipeline=pipe).sample(shots, seed=77, out=dev)
+        compile_detector_sampler(text, pipeline=pipe).sample(shots, seed=77, out=dev, shot_offset=off)
         torch.cuda.synchronize()
         assert np.array_equal(dev.cpu().numpy(), ref), (pipe, d)
     # host output (chunked D2H) and counts over the same launch path
-    assert np.array_equal(compile_detector_sampler(text).sample(shots, seed=77), ref)
-    cr = s1.sample_counts(shots, seed=77)
-    cp = compile_detector_sampler(text, pipeline=4).sample_counts(shots, seed=77)
+    assert np.array_equal(compile_detector_sampler(text).sample(shots, seed=77, shot_offset=off), ref)
+    cr = s1.sample_counts(shots, seed=77, shot_offset=off)
+    cp = compile_detector_sampler(text, pipeline=4).sample_counts(shots, seed=77, shot_offset=off)
     assert np.array_equal(np.asarray(cp), np.asarray(cr))
     assert int(np.asarray(cr, dtype=np.int64).sum()) == int(np.unpackbits(ref, axis=1).sum())
