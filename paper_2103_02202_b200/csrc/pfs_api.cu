@@ -82,7 +82,8 @@ struct pfs_program {
     bool dem_global = false;  // output column words in global memory (too many for shared)
     bool dem_per_warp = false;  // dem_warp_kernel
     DemModel dem;
-    DevBuf<uint32_t> d_comp_base, d_comp_ptr, d_cols, d_items;
+    DevBuf<uint32_t> d_comp_base, d_cols, d_items;
+    DevBuf<unsigned long long> d_comp_words;
     int dem_grid = 0;
     bool col_ring_smem = true;
     int col_v = 1;      // words per lane (tile = 32 col_v shots)
@@ -475,7 +476,8 @@ void pfs_program_destroy(pfs_program* pg) {
         for (int i = 0; i < 2; i++) { pg->d_rows[i].release(); pg->d_b8[i].release(); }
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         pg->d_cstream.release(); pg->d_binfo.release(); pg->d_refw.release();
-        pg->d_comp_base.release(); pg->d_comp_ptr.release(); pg->d_cols.release(); pg->d_items.release();
+        pg->d_comp_base.release(); pg->d_cols.release(); pg->d_items.release();
+        pg->d_comp_words.release();
         pg->d_hits2.release(); pg->d_ncnt2.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
         if (pg->noise_stream) cudaStreamDestroy(pg->noise_stream);
@@ -549,8 +551,8 @@ static int ensure_device(pfs_program* pg, int device) {
     }
     if (pg->demk) {
         CUDA_TRY(upload(pg->d_comp_base, pg->dem.comp_base));
-        CUDA_TRY(upload(pg->d_comp_ptr, pg->dem.comp_ptr));
         CUDA_TRY(upload(pg->d_cols, pg->dem.cols));
+        CUDA_TRY(upload(pg->d_comp_words, pg->dem.comp_words));
         CUDA_TRY(upload(pg->d_items, pg->dem.items));
         CUDA_TRY(set_dem_kernel_smem(pg->smem_optin));
         int per_sm = pg->opts.ctas_per_sm;
@@ -619,8 +621,8 @@ static int launch_tiles(pfs_program* pg, KParams kp, const LaunchCfg& cfg, int64
         // error-model sampler: noise hits XOR their output signatures, one launch
         DemParams dp{};
         dp.comp_base = pg->d_comp_base.p;
-        dp.comp_ptr = pg->d_comp_ptr.p;
         dp.cols = pg->d_cols.p;
+        dp.comp_words = pg->d_comp_words.p;
         dp.b8_out = cp.b8_out;
         dp.b8_pitch = cp.b8_pitch;
         dp.b8_bytes = cp.b8_bytes;

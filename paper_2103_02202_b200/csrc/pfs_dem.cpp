@@ -160,6 +160,23 @@ DemModel build_dem(const pfs_instr* ins, int64_t n_ins, const int32_t* targets, 
         std::vector<uint32_t>().swap(cptr[o]);
     }
     dm.comp_base[n_noise] = (uint32_t)(dm.comp_ptr.size() - 1);
+    // packed component words: a hit's columns in one load (most components of a
+    // QEC memory reach 1-2 detectors)
+    const bool inline_ok = n_cols < (1ll << 20);
+    const size_t ncomp = dm.comp_ptr.size() - 1;
+    dm.comp_words.resize(ncomp);
+    for (size_t k = 0; k < ncomp; k++) {
+        const uint32_t b = dm.comp_ptr[k], n = dm.comp_ptr[k + 1] - b;
+        unsigned long long w;
+        if (inline_ok && n <= 3) {
+            w = (unsigned long long)n << 62;
+            for (uint32_t j = 0; j < n; j++) w |= (unsigned long long)dm.cols[b + j] << (20 * j);
+        } else {
+            if (n >= (1u << 30)) throw std::invalid_argument("error model component too large");
+            w = (unsigned long long)b | ((unsigned long long)n << 32);
+        }
+        dm.comp_words[k] = w;
+    }
     dm.mean_cols_per_comp = dm.comp_ptr.size() > 1 ? (double)total / (double)(dm.comp_ptr.size() - 1) : 0.0;
     return dm;
 }

@@ -103,10 +103,25 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
     __syncwarp();
 }
 
+// XOR `bit` into the column words of component k's signature (one packed
+// word load; long signatures through the CSR columns)
+__device__ __forceinline__ void xor_component(const DemParams& dp, uint32_t k, uint32_t* ev, int64_t cs, uint32_t bit) {
+    const unsigned long long w = __ldg(dp.comp_words + k);
+    const uint32_t n = (uint32_t)(w >> 62);
+    if (n) {
+        atomicXor(ev + (int64_t)(uint32_t)(w & 0xFFFFFu) * cs, bit);
+        if (n > 1) atomicXor(ev + (int64_t)(uint32_t)((w >> 20) & 0xFFFFFu) * cs, bit);
+        if (n > 2) atomicXor(ev + (int64_t)(uint32_t)((w >> 40) & 0xFFFFFu) * cs, bit);
+        return;
+    }
+    const uint32_t b = (uint32_t)w, e1 = b + ((uint32_t)(w >> 32) & 0x3FFFFFFFu);
+    for (uint32_t e = b; e < e1; e++) atomicXor(ev + (int64_t)__ldg(dp.cols + e) * cs, bit);
+}
+
 // GC: the column words live in the tile-major global scratch kp.ev_out
 // ([tile][col], zeroed by the host, transposed by tiles_to_b8 afterwards)
 template <bool GC>
-__global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_constant__ KParams kp,
+__global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_constant__ KParams kp,
                                                                 const __grid_constant__ DemParams dp) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
@@ -136,12 +151,8 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_con
                 pattern_of(__ldg(kp.noise_ch + o), pick, xm, zm);
                 const uint32_t mask = (xm & 1u) | ((zm & 1u) << 1) | ((xm & 2u) << 1) | ((zm & 2u) << 2);
                 const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
-                for (uint32_t k = 0; k < 4; k++) {
-                    if (!((mask >> k) & 1u)) continue;
-                    const uint32_t e1 = __ldg(dp.comp_ptr + cb + k + 1);
-                    for (uint32_t e = __ldg(dp.comp_ptr + cb + k); e < e1; e++)
-                        atomicXor(ev + (int64_t)__ldg(dp.cols + e) * cs, bit);
-                }
+                for (uint32_t k = 0; k < 4; k++)
+                    if ((mask >> k) & 1u) xor_component(dp, cb + k, ev, cs, bit);
             });
         }
         if (GC) continue;  // transposed by tiles_to_b8
@@ -193,7 +204,7 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_kernel(const __grid_con
 
 // Small circuits (a few hundred output columns): every warp owns its own
 // 32-shot tile and column words, so tiles need no CTA barrier at all.
-__global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_warp_kernel(const __grid_constant__ KParams kp,
+__global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_warp_kernel(const __grid_constant__ KParams kp,
                                                                      const __grid_constant__ DemParams dp) {
     extern __shared__ __align__(16) uint32_t sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
@@ -218,11 +229,8 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 1) dem_warp_kernel(const __gri
                 pattern_of(__ldg(kp.noise_ch + o), pick, xm, zm);
                 const uint32_t mask = (xm & 1u) | ((zm & 1u) << 1) | ((xm & 2u) << 1) | ((zm & 2u) << 2);
                 const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
-                for (uint32_t k = 0; k < 4; k++) {
-                    if (!((mask >> k) & 1u)) continue;
-                    const uint32_t e1 = __ldg(dp.comp_ptr + cb + k + 1);
-                    for (uint32_t e = __ldg(dp.comp_ptr + cb + k); e < e1; e++) atomicXor(ev + __ldg(dp.cols + e), bit);
-                }
+                for (uint32_t k = 0; k < 4; k++)
+                    if ((mask >> k) & 1u) xor_component(dp, cb + k, ev, 1, bit);
             });
         }
         __syncwarp();

@@ -286,6 +286,9 @@ struct DemModel {
     std::vector<uint32_t> comp_base;
     std::vector<uint32_t> comp_ptr;
     std::vector<uint32_t> cols;
+    // one 64-bit word per component: up to 3 columns inline (20 bits each,
+    // count in bits 62-63), else count 0 and (offset into cols, n) = bits 0-31, 32-61
+    std::vector<unsigned long long> comp_words;
     std::string coin_dependent;
     double mean_cols_per_comp = 0.0;
     std::vector<uint32_t> items;     // (ordinal, chunk) pairs of one tile (set once the schedule is built)
@@ -295,9 +298,9 @@ DemModel build_dem(const pfs_instr* ins, int64_t n_ins, const int32_t* targets, 
                    int64_t n_noise);
 
 struct DemParams {
-    const uint32_t* comp_base;
-    const uint32_t* comp_ptr;
-    const uint32_t* cols;
+    const uint32_t* comp_base;             // first component of each noise ordinal
+    const uint32_t* cols;                  // CSR columns of long signatures
+    const unsigned long long* comp_words;  // DemModel::comp_words
     uint8_t* b8_out;             // shot-major detection events, or null
     int64_t b8_pitch;
     int64_t b8_bytes;
