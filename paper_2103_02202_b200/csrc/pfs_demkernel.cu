@@ -103,19 +103,20 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
     __syncwarp();
 }
 
-// XOR `bit` into the column words of component k's signature (one packed
-// word load; long signatures through the CSR columns)
-__device__ __forceinline__ void xor_component(const DemParams& dp, uint32_t k, uint32_t* ev, int64_t cs, uint32_t bit) {
+// Visit the columns of component k's signature (one packed word load; long
+// signatures through the CSR columns)
+template <typename F>
+__device__ __forceinline__ void for_component(const DemParams& dp, uint32_t k, F f) {
     const unsigned long long w = __ldg(dp.comp_words + k);
     const uint32_t n = (uint32_t)(w >> 62);
     if (n) {
-        atomicXor(ev + (int64_t)(uint32_t)(w & 0xFFFFFu) * cs, bit);
-        if (n > 1) atomicXor(ev + (int64_t)(uint32_t)((w >> 20) & 0xFFFFFu) * cs, bit);
-        if (n > 2) atomicXor(ev + (int64_t)(uint32_t)((w >> 40) & 0xFFFFFu) * cs, bit);
+        f((uint32_t)(w & 0xFFFFFu));
+        if (n > 1) f((uint32_t)((w >> 20) & 0xFFFFFu));
+        if (n > 2) f((uint32_t)((w >> 40) & 0xFFFFFu));
         return;
     }
     const uint32_t b = (uint32_t)w, e1 = b + ((uint32_t)(w >> 32) & 0x3FFFFFFFu);
-    for (uint32_t e = b; e < e1; e++) atomicXor(ev + (int64_t)__ldg(dp.cols + e) * cs, bit);
+    for (uint32_t e = b; e < e1; e++) f(__ldg(dp.cols + e));
 }
 
 // GC: the column words live in the tile-major global scratch kp.ev_out
@@ -126,12 +127,17 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_con
     extern __shared__ __align__(16) uint32_t sm[];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     const int ncols = kp.num_cols;
-    const int ncw = GC ? 0 : (ncols + 3) & ~3;
+    const int ncw = GC ? 0 : 32 * ((((ncols + 31) >> 5) + 3) & ~3);  // also 32 shot rows (16-byte aligned)
     uint32_t* const cnt = sm + ncw;                             // [ncols] (counts mode)
     uint32_t* const wscr = cnt + (kp.counts_in_smem ? ncw : 0) + (size_t)warp * 32 * NZ_MAX_LIST;
     uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
     if (kp.counts_in_smem)
         for (int i = threadIdx.x; i < ncols; i += blockDim.x) cnt[i] = 0u;
+    // b8 output from shared memory: the tile is kept shot-major (32 rows of
+    // rw words, bit c of row s = column c of shot s), so each row already is
+    // the shot's b8 row and is stored without a transpose
+    const bool shot_major = !GC && dp.b8_out != nullptr && kp.counts == nullptr;
+    const int rw = (((ncols + 31) >> 5) + 3) & ~3;  // words per shot row (16-byte multiple)
     for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x) {
         const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
         // column words of the tile: shared, or the global output rows at
@@ -140,7 +146,7 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_con
         uint32_t* const ev = GC ? kp.ev_out + (size_t)tile * kp.out_tile_stride : sm;
         const int64_t cs = GC ? kp.out_row_stride : 1;
         if (!GC) {
-            for (int i = threadIdx.x; i < ncols; i += blockDim.x) ev[i] = 0u;
+            for (int i = threadIdx.x; i < (shot_major ? 32 * rw : ncols); i += blockDim.x) ev[i] = 0u;
             __syncthreads();
         }
         for (uint32_t first = 32u * warp; first < (uint32_t)dp.n_items; first += 32u * NW) {
@@ -151,8 +157,16 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_con
                 pattern_of(__ldg(kp.noise_ch + o), pick, xm, zm);
                 const uint32_t mask = (xm & 1u) | ((zm & 1u) << 1) | ((xm & 2u) << 1) | ((zm & 2u) << 2);
                 const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
-                for (uint32_t k = 0; k < 4; k++)
-                    if ((mask >> k) & 1u) xor_component(dp, cb + k, ev, cs, bit);
+                if (shot_major) {
+                    uint32_t* const row = ev + (trial & 31u) * rw;
+                    for (uint32_t k = 0; k < 4; k++)
+                        if ((mask >> k) & 1u)
+                            for_component(dp, cb + k, [&](uint32_t col) { atomicXor(row + (col >> 5), 1u << (col & 31u)); });
+                } else {
+                    for (uint32_t k = 0; k < 4; k++)
+                        if ((mask >> k) & 1u)
+                            for_component(dp, cb + k, [&](uint32_t col) { atomicXor(ev + (int64_t)col * cs, bit); });
+                }
             });
         }
         if (GC) continue;  // transposed by tiles_to_b8
@@ -166,6 +180,23 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_con
                     if (kp.counts_in_smem) cnt[c] += n;  // one thread per column
                     else atomicAdd(kp.counts + c, (unsigned long long)n);
                 }
+            }
+        } else if (shot_major) {
+            // row s -> b8 row of shot tile*32+s: 16-byte stores when aligned
+            const int nb = (int)dp.b8_bytes;
+            const bool a16 = ((dp.b8_pitch | reinterpret_cast<uintptr_t>(dp.b8_out)) & 15) == 0;
+            const int nv = a16 ? nb >> 4 : 0;  // whole 16-byte vectors per row
+            const int nrow = rem >= 32 ? 32 : (rem <= 0 ? 0 : (int)rem);
+            for (int i = threadIdx.x; i < nrow * nv; i += blockDim.x) {
+                const int sr = i / nv, v = i - sr * nv;
+                const uint4 q = *reinterpret_cast<const uint4*>(ev + sr * rw + 4 * v);
+                *reinterpret_cast<uint4*>(dp.b8_out + (tile * 32 + sr) * dp.b8_pitch + 16 * v) = q;
+            }
+            const int tb = nb - 16 * nv;  // remaining bytes per row
+            for (int i = threadIdx.x; i < nrow * tb; i += blockDim.x) {
+                const int sr = i / tb, bI = 16 * nv + (i - sr * tb);
+                dp.b8_out[(tile * 32 + sr) * dp.b8_pitch + bI] =
+                    (uint8_t)(ev[sr * rw + (bI >> 2)] >> (8 * (bI & 3)));
             }
         } else if (dp.b8_out != nullptr) {
             // whole 32-column blocks store one aligned word per shot; the last,
@@ -230,7 +261,7 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_warp_kernel(const __gri
                 const uint32_t mask = (xm & 1u) | ((zm & 1u) << 1) | ((xm & 2u) << 1) | ((zm & 2u) << 2);
                 const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
                 for (uint32_t k = 0; k < 4; k++)
-                    if ((mask >> k) & 1u) xor_component(dp, cb + k, ev, 1, bit);
+                    if ((mask >> k) & 1u) for_component(dp, cb + k, [&](uint32_t col) { atomicXor(ev + col, bit); });
             });
         }
         __syncwarp();
@@ -275,7 +306,7 @@ size_t dem_warp_smem_bytes(int warps, int64_t num_cols, bool counts) {
 }
 
 size_t dem_smem_bytes(int warps, int64_t num_cols, bool counts) {
-    const size_t ncw = ((size_t)num_cols + 3) & ~(size_t)3;
+    const size_t ncw = 32 * (((((size_t)num_cols + 31) >> 5) + 3) & ~(size_t)3);  // 32 shot rows, 16-byte multiples
     return (ncw * (counts ? 2 : 1) + (size_t)warps * 32 * NZ_MAX_LIST) * 4;
 }
 

@@ -267,6 +267,29 @@ def test_error_model_sampler_equals_frame_sampler(oracle_lib, case):
                           rows_unpack(oev, shots))
 
 
+def test_error_model_sampler_shot_major_rows():
+    """dem_kernel keeps a tile's events shot-major in shared memory and stores
+    each shot's row directly: 16-byte vector path (host output through the
+    32-byte-pitch scratch), bytewise path (device output with an odd pitch),
+    ragged tail tile and a shot offset — bit-exact with the frame kernel."""
+    from paper_2103_02202_b200 import generators as gen
+    from paper_2103_02202_b200.sampler import compile_detector_sampler
+    import torch
+
+    text = gen.surface_code_memory(25, 5, 2e-3)
+    dem = compile_detector_sampler(text, kernel=4)
+    frm = compile_detector_sampler(text, kernel=1, words_per_tile=1)
+    assert dem.native.info["kernel"] == 4
+    shots, off = 5000 + 13, 32 * 5
+    ref = frm.sample(shots, seed=8, shot_offset=off)
+    assert np.array_equal(dem.sample(shots, seed=8, shot_offset=off), ref)
+    nb = (dem.num_columns + 7) // 8
+    dev = torch.zeros((shots, nb + 1), dtype=torch.uint8, device="cuda")[:, 1:]  # odd base, pitch nb + 1
+    dem.sample(shots, seed=8, shot_offset=off, out=dev)
+    torch.cuda.synchronize()
+    assert np.array_equal(dev.cpu().numpy(), ref)
+
+
 def test_error_model_sampler_full_size_d25():
     """Config 2 at 2^20 shots through the error-model sampler: identical to the
     frame sampler on one-word tiles."""
