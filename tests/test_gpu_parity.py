@@ -288,6 +288,11 @@ def test_error_model_sampler_shot_major_rows():
     dem.sample(shots, seed=8, shot_offset=off, out=dev)
     torch.cuda.synchronize()
     assert np.array_equal(dev.cpu().numpy(), ref)
+    # counts and column-major rows keep the column-word layout
+    assert np.array_equal(dem.sample_rows(shots, seed=8, shot_offset=off),
+                          frm.sample_rows(shots, seed=8, shot_offset=off))
+    assert np.array_equal(dem.sample_counts(shots, seed=8, shot_offset=off),
+                          b8_unpack(ref, dem.num_columns).sum(axis=0))
 
 
 def test_error_model_sampler_full_size_d25():
