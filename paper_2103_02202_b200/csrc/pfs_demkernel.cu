@@ -103,11 +103,10 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
     __syncwarp();
 }
 
-// Visit the columns of component k's signature (one packed word load; long
+// Visit the columns of a packed component word (up to 3 inline; long
 // signatures through the CSR columns)
 template <typename F>
-__device__ __forceinline__ void for_component(const DemParams& dp, uint32_t k, F f) {
-    const unsigned long long w = __ldg(dp.comp_words + k);
+__device__ __forceinline__ void for_word(const DemParams& dp, unsigned long long w, F f) {
     const uint32_t n = (uint32_t)(w >> 62);
     if (n) {
         f((uint32_t)(w & 0xFFFFFu));
@@ -117,6 +116,18 @@ __device__ __forceinline__ void for_component(const DemParams& dp, uint32_t k, F
     }
     const uint32_t b = (uint32_t)w, e1 = b + ((uint32_t)(w >> 32) & 0x3FFFFFFFu);
     for (uint32_t e = b; e < e1; e++) f(__ldg(dp.cols + e));
+}
+
+// A hit's components (mask bit k: x / z on slot 0 / 1): all signature words are
+// loaded before any column is touched, so their L2 round trips overlap
+template <typename F>
+__device__ __forceinline__ void for_hit_columns(const DemParams& dp, uint32_t cb, uint32_t mask, F f) {
+    unsigned long long w[4];
+#pragma unroll
+    for (int k = 0; k < 4; k++) w[k] = ((mask >> k) & 1u) ? __ldg(dp.comp_words + cb + k) : 0ull;
+#pragma unroll
+    for (int k = 0; k < 4; k++)
+        if ((mask >> k) & 1u) for_word(dp, w[k], f);
 }
 
 // GC: the column words live in the tile-major global scratch kp.ev_out
@@ -159,13 +170,9 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_con
                 const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
                 if (shot_major) {
                     uint32_t* const row = ev + (trial & 31u) * rw;
-                    for (uint32_t k = 0; k < 4; k++)
-                        if ((mask >> k) & 1u)
-                            for_component(dp, cb + k, [&](uint32_t col) { atomicXor(row + (col >> 5), 1u << (col & 31u)); });
+                    for_hit_columns(dp, cb, mask, [&](uint32_t col) { atomicXor(row + (col >> 5), 1u << (col & 31u)); });
                 } else {
-                    for (uint32_t k = 0; k < 4; k++)
-                        if ((mask >> k) & 1u)
-                            for_component(dp, cb + k, [&](uint32_t col) { atomicXor(ev + (int64_t)col * cs, bit); });
+                    for_hit_columns(dp, cb, mask, [&](uint32_t col) { atomicXor(ev + (int64_t)col * cs, bit); });
                 }
             });
         }
@@ -260,8 +267,7 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_warp_kernel(const __gri
                 pattern_of(__ldg(kp.noise_ch + o), pick, xm, zm);
                 const uint32_t mask = (xm & 1u) | ((zm & 1u) << 1) | ((xm & 2u) << 1) | ((zm & 2u) << 2);
                 const uint32_t cb = __ldg(dp.comp_base + o) + app * 4;
-                for (uint32_t k = 0; k < 4; k++)
-                    if ((mask >> k) & 1u) for_component(dp, cb + k, [&](uint32_t col) { atomicXor(ev + col, bit); });
+                for_hit_columns(dp, cb, mask, [&](uint32_t col) { atomicXor(ev + col, bit); });
             });
         }
         __syncwarp();
