@@ -2,6 +2,7 @@
 set -x
 mkdir -p gpurun_out
 timeout 1200 python -m pytest tests -m gpu -x -q > gpurun_out/gpu_tests.log 2>&1; echo "tests rc=$?"
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 tail -3 gpurun_out/gpu_tests.log
 timeout 600 python bench.py > gpurun_out/bench_default.log 2>&1; echo "bench rc=$?"
 tail -1 gpurun_out/bench_default.log
