@@ -364,7 +364,7 @@ def roofline_of(res, smem_peak, hbm):
     achieved = bframe_bytes * res["shots"] / (fr / 1e3) / 1e9
     return {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
             "frac": achieved / smem_peak,
-            "traffic": profile_traffic(res["shots"]) if res["cfg"] == 2 else None,
+            "traffic": profile_traffic(res["shots"], res["cfg"]),
             "traffic_source": "profiles/frame_kernel_traffic.json (ncu --set full, per shot)",
             "peak_source": "measured live: pfs_measure_smem_bandwidth (LDS.128/STS.128 CX mix, "
                            "all SMs)",
@@ -496,13 +496,18 @@ def smem_peak_gbs():
         return None
 
 
-def profile_traffic(shots=None):
+def profile_traffic(shots=None, cfg=2):
     """DRAM bytes per frame-kernel launch from the committed ncu capture
-    (profiles/frame_kernel_traffic.json, per shot x this launch's shots)."""
+    (profiles/frame_kernel_traffic.json, per shot x this launch's shots);
+    config 4 reads its own d=100 capture."""
     p = os.path.join(REPO, "profiles", "frame_kernel_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
+        if cfg == 4:
+            d = d["config4"]
+        elif cfg != 2:
+            return None
         return float(d["dram_bytes_per_shot"]) * shots if shots else None
     except Exception:
         return None
