@@ -4,20 +4,23 @@
 Workload (BASELINE.json configs[2]): rotated surface code Z-memory, d=25,
 25 rounds, p=1e-3 circuit noise, 2^20 shots per GPU per step, detection
 events (+ the logical observable) shot-major bit-packed (b8).  One step = one
-full pass of the hot path: frame program kernel over all shots + the
-shot-major transpose, outputs resident in HBM.
+full pass of the hot path: frame program kernel over all shots (noise sampled
+inline) + the shot-major transpose, outputs resident in HBM.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 N>1 runs under torchrun, one process per GPU; shots are sharded by global shot
 offset (weak scaling: every rank samples its own 2^20 shots), no collective on
-the data path; the timing is the max over ranks.
+the data path; the timing is the max over ranks.  --impl reference times the
+reference algorithm on the host cores (the C restatement in oracle/, all
+threads) on the same workload; rank 0 only.
 """
 
 from __future__ import annotations
 
 import argparse
 import json
+import multiprocessing
 import os
 import statistics
 import subprocess
@@ -49,16 +52,18 @@ def parse_args():
     ap.add_argument("--words", type=int, default=0, help="override W (32-shot words per tile)")
     ap.add_argument("--ring", type=int, default=-1)
     ap.add_argument("--threads", type=int, default=0)
-    ap.add_argument("--kernel", type=int, default=0, help="frame kernel: 0 auto, 1 cooperative, 2 warp-private, 3 word-column")
+    ap.add_argument("--kernel", type=int, default=0, help="0 auto / 1 frame sampler, 4 error-model sampler")
     ap.add_argument("--target-hits", type=float, default=0.0)
-    ap.add_argument("--groups", type=int, default=0, help="cooperative kernel: tiles in flight per CTA")
+    ap.add_argument("--fused-hits", type=float, default=0.0)
+    ap.add_argument("--groups", type=int, default=0, help="tiles in flight per CTA")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-d100", action="store_true", help="skip the config 4 (d=100) extra line")
     ap.add_argument("--no-dem", action="store_true", help="skip the error-model sampler extra line")
     ap.add_argument("--no-c3", action="store_true", help="skip the config 3 counts extra line")
-    ap.add_argument("--pipeline", type=int, default=0, help="noise/frame pipeline sub-chunks (0 auto, 1 off)")
+    ap.add_argument("--no-pyref", action="store_true", help="skip timing the Python reference package")
+    ap.add_argument("--pipeline", type=int, default=0, help="frame/transpose pipeline sub-chunks (0 auto, 1 off)")
     return ap.parse_args()
 
 
@@ -128,31 +133,6 @@ def config_text(cfg: int):
     return gen.config_circuit(cfg)
 
 
-def cpu_port_rate(text: str, seconds: float, nthreads: int):
-    """The C oracle (CPU restatement of the reference's algorithm) on host
-    cores: detection events + shot-major b8, shots/s over a bounded sample."""
-    from oracle import oracle as O
-    from paper_2103_02202_b200.program import flatten
-
-    O.build()
-    prog = flatten(text)
-    T = 512
-    # calibrate: one tile per thread
-    shots = max(T * nthreads, 1)
-    t0 = time.perf_counter()
-    _, ev = O.sample(prog, shots, T, seed=1, flips=False, nthreads=nthreads)
-    O.rows_to_b8(ev, shots)
-    dt = time.perf_counter() - t0
-    rate = shots / dt
-    shots = int(min(max(rate * seconds, shots), 1 << 22))
-    shots = max(T, (shots // T) * T)
-    t0 = time.perf_counter()
-    _, ev = O.sample(prog, shots, T, seed=2, flips=False, nthreads=nthreads)
-    O.rows_to_b8(ev, shots)
-    dt = time.perf_counter() - t0
-    return shots / dt, shots, dt
-
-
 def host_cores():
     try:
         return len(os.sched_getaffinity(0))
@@ -171,41 +151,133 @@ def cpu_model():
     return "unknown"
 
 
+def workload_config(cfg: int, shots: int, world: int) -> dict:
+    """The `config` object both arms print (same workload, same keys)."""
+    return {"workload": WORKLOADS.get(cfg, f"config{cfg}") + ", detection events + observable, shot-major b8",
+            "shots_per_gpu_per_step": shots,
+            "parallelism": f"shots sharded x{world} (global shot offsets)"}
+
+
+# ----------------------------------------------------------------- CPU arms
+class PortTimer:
+    """The reference algorithm restated in C (oracle/pfs_oracle.c) on the host
+    cores: frame simulation of every tile (every coin and noise draw), detector
+    XORs, then the shot-major b8 transpose — all host threads.  Setup (circuit
+    lowering, oracle build, the RNG layout) is done once, outside the timing."""
+
+    T = 256
+
+    def __init__(self, cfg: int, threads: int):
+        from oracle import oracle as O
+        from paper_2103_02202_b200.program import flatten
+
+        O.build()
+        self.O = O
+        self.prog = flatten(config_text(cfg))
+        self.threads = threads
+        # layout of the draws (chunk length per noise instruction): it fixes the
+        # draw order, not the work, so any valid one times the algorithm
+        self.chunk_L = np.full(self.prog.num_noise, 512, dtype=np.uint32)
+
+    def run(self, shots: int, seed: int) -> float:
+        t0 = time.perf_counter()
+        _, ev = self.O.sample(self.prog, shots, self.T, seed=seed, flips=False, nthreads=self.threads,
+                              chunk_L=self.chunk_L, vector_shots=128)
+        self.O.rows_to_b8(ev, shots, nthreads=self.threads)
+        return time.perf_counter() - t0
+
+    def rate(self, seconds: float, seed: int = 1):
+        """(shots/s, shots, seconds) of one bounded sample of about `seconds`."""
+        shots = self.T * self.threads
+        dt = self.run(shots, seed)  # calibration (also warms the threads)
+        shots = int(min(max(shots / dt * seconds, shots), 1 << 22))
+        shots = max(self.T, (shots // self.T) * self.T)
+        dt = self.run(shots, seed + 1)
+        return shots / dt, shots, dt
+
+
+def _pyref_worker(args):
+    """One process of the unmodified Python reference (stabsim, pip-installed
+    into baseline/_ref): collect_flips + detector_events on its own shots."""
+    ref_path, text, shots, seed, batch = args
+    sys.path.insert(0, ref_path)
+    from stabsim import circuit, frame_sim, io_formats
+
+    c = circuit.parse(text)
+    dets = circuit.detector_sets(c)
+    t0 = time.perf_counter()
+    flips = frame_sim.collect_flips(c, shots, np.random.default_rng(seed), batch)
+    io_formats.detector_events(flips, dets)
+    return time.perf_counter() - t0
+
+
+def python_reference_rate(cfg: int, procs: int, batch: int = 8192):
+    """the reference package itself on `procs` worker
+    processes, one batch each (bounded sample); None when baseline/_ref is
+    absent.  Circuits are lowered to the reference dialect."""
+    ref_path = os.path.join(REPO, "baseline", "_ref")
+    if not os.path.isdir(os.path.join(ref_path, "stabsim")):
+        return None
+    from paper_2103_02202_b200.circuit import to_reference_dialect
+
+    text = to_reference_dialect(config_text(cfg))
+    ctx = multiprocessing.get_context("spawn")
+    with ctx.Pool(procs) as pool:
+        t0 = time.perf_counter()
+        times = pool.map(_pyref_worker, [(ref_path, text, batch, 1000 + i, batch) for i in range(procs)])
+        wall = time.perf_counter() - t0
+    shots = procs * batch
+    return {"value": shots / max(times), "unit": "shots/s", "cores": procs, "kind": "reference",
+            "sample": f"{shots} shots of config {cfg}: {procs} processes x collect_flips(batch_size={batch}) + "
+                      f"detector_events of the unmodified stabsim package (baseline/_ref), timed inside each "
+                      f"worker after parsing; pool wall {wall:.1f}s ({cpu_model()})"}
+
+
 # ----------------------------------------------------------------- reference arm
 def run_reference(args, rank, world):
     if rank != 0:
         return
-    text = config_text(args.config)
     cores = host_cores()
-    per_step = []
-    sample_shots = 0
+    pt = PortTimer(args.config, cores)
+    shots_cfg = args.shots or __import__("paper_2103_02202_b200.generators", fromlist=["CONFIGS"]).CONFIGS[
+        args.config]["shots"]
+    per_step_s = max(2.0, min(args.cpu_seconds, 60.0) / max(1, args.steps))
+    rates, sample_shots = [], 0
     for i in range(args.warmup + args.steps):
-        rate, shots, dt = cpu_port_rate(text, min(args.cpu_seconds, 20.0) / max(1, args.steps),
-                                        cores)
+        rate, shots, dt = pt.rate(per_step_s, seed=10 + 2 * i)
         if i >= args.warmup:
-            per_step.append(rate)
+            rates.append(rate)
             sample_shots = shots
-    value = float(np.median(per_step))
+    value = float(np.median(rates))
     line = {
         "impl": "reference",
         "metric": METRIC,
         "value": value, "unit": "shots/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": 1e3 * sample_shots / value,
+        "warmup": args.warmup, "ms_per_step": 1e3 * shots_cfg / value,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded circuit-level noise, Philox)",
-        "config": {"workload": WORKLOADS.get(args.config, f"config{args.config}") +
-                               ", detection events + observable, shot-major b8",
-                   "shots_per_step": sample_shots},
+        "config": workload_config(args.config, shots_cfg, world),
         "cpu_baseline": {"value": value, "unit": "shots/s", "cores": cores, "kind": "port",
-                         "sample": f"{sample_shots} shots per step of config {args.config} "
-                                   f"on {cores} threads ({cpu_model()})"},
-        "e2e": {"value": value, "unit": "shots/s", "h2d_bytes_per_step": 0,
-                "d2h_bytes_per_step": 0},
+                         "sample": f"per step a bounded sample of {sample_shots} of the {shots_cfg} shots "
+                                   f"(ms_per_step extrapolates to the full step) of config {args.config}: C "
+                                   f"restatement of stabsim frame_sim + detector_events + b8 transpose on "
+                                   f"{cores} threads ({cpu_model()})"},
+        "e2e": {"value": value, "unit": "shots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
+    if not args.no_pyref:
+        py = python_reference_rate(args.config, min(cores, 8))
+        if py is not None:
+            line["python_reference"] = py
     print(json.dumps(line), flush=True)
 
 
 # ----------------------------------------------------------------- our arm
+def native_opts(args):
+    return dict(words_per_tile=args.words, ring_in_smem=args.ring, threads=args.threads,
+                noise_target_hits=args.target_hits, kernel=args.kernel, groups=args.groups,
+                pipeline=args.pipeline, fused_target_hits=args.fused_hits)
+
+
 def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, world: int,
             local_rank: int, e2e_steps: int):
     """Time `steps` sampling steps of config `cfg` (device-resident b8 output),
@@ -213,6 +285,7 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     import torch
 
     from paper_2103_02202_b200 import _native as N
+    from paper_2103_02202_b200.parallel import rank_offset, reduce_max
     from paper_2103_02202_b200.program import flatten
     from paper_2103_02202_b200.sampler import DetectorSampler, pinned_empty
 
@@ -222,13 +295,12 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     dev = torch.device("cuda", local_rank)
     t0 = time.perf_counter()
     flat = flatten(config_text(cfg))
-    compile_s = time.perf_counter() - t0
-    kw = dict(words_per_tile=args.words, ring_in_smem=args.ring, threads=args.threads,
-              noise_target_hits=args.target_hits, kernel=args.kernel, groups=args.groups, pipeline=args.pipeline)
+    kw = native_opts(args)
     ds = DetectorSampler.__new__(DetectorSampler)
     ds.circuit, ds.flat, ds.device = None, flat, local_rank
     ds._seeds = np.random.default_rng(0)
     ds.native = N.NativeProgram(flat, **kw)
+    compile_s = time.perf_counter() - t0
     info = ds.info
     T = ds.tile_shots
     nb = (ds.num_columns + 7) // 8
@@ -237,7 +309,7 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     pitch = (nb + 31) // 32 * 32  # 32-byte aligned shot rows on device (b8 bytes + zero pad)
     out_full = torch.empty((shots, pitch), dtype=torch.uint8, device=dev)
     out = out_full[:, :nb]
-    base_offset = rank * ((shots + T - 1) // T) * T
+    base_offset = rank_offset(shots, world, rank, T)
     seed = 20260214
 
     def step(sampler, i):
@@ -259,11 +331,7 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
             launches += ds.native.last_launches()
         ev1.record(stream)
         torch.cuda.synchronize()
-    elapsed = ev0.elapsed_time(ev1) / 1e3
-    if dist:
-        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        elapsed = float(tt.item())
+    elapsed = reduce_max(ev0.elapsed_time(ev1) / 1e3, dev)
     res = {"cfg": cfg, "shots": shots, "steps": steps, "elapsed": elapsed,
            "value": shots * world * steps / elapsed, "clocks": clk.summary(),
            "launches": launches, "info": info, "nb": nb, "compile_s": compile_s}
@@ -273,17 +341,15 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     dt.circuit, dt.flat, dt.device = None, flat, local_rank
     dt._seeds = np.random.default_rng(0)
     dt.native = N.NativeProgram(flat, timing=True, **kw)
-    fr, tr, nz = [], [], []
+    fr, tr = [], []
     for i in range(max(3, min(steps, 10))):
         step(dt, i)
         t = dt.native.last_timing()
         if i:
             fr.append(t[0])
             tr.append(t[1])
-            nz.append(t[5])
     res["frame_ms"] = float(np.mean(fr))
     res["transpose_ms"] = float(np.mean(tr))
-    res["noise_ms"] = float(np.mean(nz))
     del dt
 
     if e2e_steps > 0:
@@ -296,11 +362,7 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
         for i in range(e2e_steps):
             ds.sample(shots, seed=seed + i, out=host, shot_offset=base_offset)
         torch.cuda.synchronize()
-        e_el = time.perf_counter() - t0
-        if dist:
-            tt = torch.tensor([e_el], device=dev, dtype=torch.float64)
-            tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-            e_el = float(tt.item())
+        e_el = reduce_max(time.perf_counter() - t0, dev)
         res["e2e"] = {"value": shots * world * e2e_steps / e_el, "unit": "shots/s",
                       "h2d_bytes_per_step": 0, "d2h_bytes_per_step": int(shots * nb * world),
                       "steps": e2e_steps,
@@ -317,9 +379,11 @@ def measure_counts(args, kernel: int, shots: int, steps: int, warmup: int, rank:
                    local_rank: int):
     """Config 3 (BASELINE.json): d=5, 5 rounds, p=5e-3, on-device per-column
     event counts only (no event I/O), `shots` per GPU per step; the per-rank
-    u64 counts are summed with one NCCL all-reduce at the end."""
+    u64 counts are summed with one NCCL all-reduce at the end
+    — parallel.counts_steps, the helper the gloo test drives."""
     import torch
 
+    from paper_2103_02202_b200.parallel import counts_steps, reduce_max
     from paper_2103_02202_b200.sampler import compile_detector_sampler
 
     dist = world > 1
@@ -329,10 +393,12 @@ def measure_counts(args, kernel: int, shots: int, steps: int, warmup: int, rank:
     ds = compile_detector_sampler(config_text(3), device=local_rank, kernel=kernel)
     T = ds.tile_shots
     counts = torch.zeros(ds.num_columns, dtype=torch.int64, device=dev)
-    base = rank * ((shots + T - 1) // T) * T
     stream = torch.cuda.current_stream(dev)
-    for i in range(warmup):
-        ds.sample_counts(shots, seed=99 + i, out=counts, shot_offset=base, stream=stream.cuda_stream)
+
+    def sample_counts(n, s, off, out):
+        ds.sample_counts(n, seed=s, out=out, shot_offset=off, stream=stream.cuda_stream)
+
+    counts_steps(sample_counts, counts, shots, T, 1, 0, warmup, 99)  # warm-up, no reduction
     torch.cuda.synchronize()
     if dist:
         tdist.barrier()
@@ -340,21 +406,14 @@ def measure_counts(args, kernel: int, shots: int, steps: int, warmup: int, rank:
     ev0 = torch.cuda.Event(enable_timing=True)
     ev1 = torch.cuda.Event(enable_timing=True)
     ev0.record(stream)
-    for i in range(steps):
-        ds.sample_counts(shots, seed=7 + i, out=counts, shot_offset=base, stream=stream.cuda_stream)
-    if dist:
-        tdist.all_reduce(counts)
+    counts_steps(sample_counts, counts, shots, T, world, rank, steps, 7)
     ev1.record(stream)
     torch.cuda.synchronize()
-    elapsed = ev0.elapsed_time(ev1) / 1e3
-    if dist:
-        tt = torch.tensor([elapsed], device=dev, dtype=torch.float64)
-        tdist.all_reduce(tt, op=tdist.ReduceOp.MAX)
-        elapsed = float(tt.item())
-    rate = float(counts.sum().item()) / max(1, shots * world * steps)  # mean events per shot (last step x world)
+    elapsed = reduce_max(ev0.elapsed_time(ev1) / 1e3, dev)
+    rate = float(counts.sum().item()) / max(1, shots * world)  # mean events per shot (last step, all ranks)
     return {"value": shots * world * steps / elapsed, "unit": "shots/s", "ms_per_step": 1e3 * elapsed / steps,
             "steps": steps, "shots_per_gpu_per_step": shots, "kernel": ds.info["kernel"],
-            "mean_events_per_shot_last_step": rate * steps}
+            "mean_events_per_shot_last_step": rate}
 
 
 def roofline_of(res, smem_peak, hbm):
@@ -365,12 +424,12 @@ def roofline_of(res, smem_peak, hbm):
     return {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
             "frac": achieved / smem_peak,
             "traffic": profile_traffic(res["shots"], res["cfg"]),
-            "traffic_source": "profiles/frame_kernel_traffic.json (ncu --set full, per shot)",
+            "traffic_source": "profiles/frame_kernel_traffic.json (ncu --set full, DRAM bytes per shot "
+                              "of the frame kernel)",
             "peak_source": "measured live: pfs_measure_smem_bandwidth (LDS.128/STS.128 CX mix, "
                            "all SMs)",
-            "kernel": "frame_kernel (frame table resident in shared memory)",
+            "kernel": "frame_kernel (frame table resident in shared memory, noise sampled inline)",
             "frame_kernel_ms": fr, "transpose_kernel_ms": res["transpose_ms"],
-            "noise_kernel_ms": res["noise_ms"],
             "bytes_per_shot": bframe_bytes,
             "hbm_equiv": {"achieved_gbs": achieved, "peak_gbs": hbm, "frac": achieved / hbm,
                           "note": "frame-update GB/s vs measured HBM copy peak (BASELINE.json "
@@ -378,6 +437,8 @@ def roofline_of(res, smem_peak, hbm):
 
 
 def run_ours(args, rank, world, local_rank):
+    import copy
+
     import torch
 
     from paper_2103_02202_b200 import generators as gen
@@ -390,7 +451,6 @@ def run_ours(args, rank, world, local_rank):
     dem = None
     if args.config == 2 and not args.no_dem and args.kernel == 0:
         # the error-model detector sampler (kernel 4) on the same workload
-        import copy
         a2 = copy.copy(args)
         a2.kernel, a2.words, a2.ring, a2.threads, a2.groups = 4, 0, -1, 0, 0
         dem = measure(a2, args.config, shots, max(3, args.steps // 2), args.warmup, rank, world,
@@ -406,13 +466,14 @@ def run_ours(args, rank, world, local_rank):
     extra = None
     if args.config == 2 and not args.no_d100:
         s4 = gen.CONFIGS[4]["shots"]
-        extra = measure(args, 4, s4, max(3, args.steps // 4), 3, rank, world, local_rank,
+        a4 = copy.copy(args)
+        a4.words, a4.groups, a4.threads = 0, 0, 0
+        extra = measure(a4, 4, s4, max(3, args.steps // 4), 3, rank, world, local_rank,
                         0 if args.no_e2e else 2)
         if not args.no_dem and args.kernel == 0:
-            import copy
-            a4 = copy.copy(args)
-            a4.kernel, a4.words, a4.ring, a4.threads, a4.groups = 4, 0, -1, 0, 0
-            extra["dem"] = measure(a4, 4, s4, max(3, args.steps // 4), 3, rank, world, local_rank, 0)
+            a5 = copy.copy(args)
+            a5.kernel, a5.words, a5.ring, a5.threads, a5.groups = 4, 0, -1, 0, 0
+            extra["dem"] = measure(a5, 4, s4, max(3, args.steps // 4), 3, rank, world, local_rank, 0)
     if rank != 0:
         return
     peaks = measured_peaks()
@@ -420,21 +481,19 @@ def run_ours(args, rank, world, local_rank):
     smem_peak = measure_smem_bandwidth(local_rank)
     info = main["info"]
     T = info["tile_shots"]
-    workloads = WORKLOADS
+    cfgd = workload_config(args.config, main["shots"], world)
+    cfgd.update({"columns": info["num_columns"], "W": info["words_per_tile"], "tile_shots": T,
+                 "groups": info["groups"], "ring_in_smem": info["ring_in_smem"], "threads": info["threads"],
+                 "device_ops": info["num_ops"], "barriers_per_tile": info["num_barriers"],
+                 "fused_noise_instructions": f"{info['fused_noise']}/{info['num_noise']}",
+                 "l2": f"outputs {main['shots'] * main['nb'] / 1e9:.2f} GB/step > 126 MB L2 (no flush needed)"})
     line = {
         "metric": METRIC,
         "value": main["value"], "unit": "shots/s", "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * main["elapsed"] / args.steps,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u32",
         "data": "synthetic (seeded circuit-level noise, counter-based Philox)",
-        "config": {"workload": workloads.get(args.config, f"config{args.config}") +
-                   ", detection events + observable, shot-major b8 in HBM",
-                   "shots_per_gpu_per_step": main["shots"], "columns": info["num_columns"],
-                   "W": info["words_per_tile"], "tile_shots": T,
-                   "ring_in_smem": info["ring_in_smem"], "threads": info["threads"],
-                   "l2": f"outputs {main['shots'] * main['nb'] / 1e9:.2f} GB/step > 126 MB L2 "
-                         "(no flush needed)",
-                   "parallelism": f"shots sharded x{world} (global shot offsets)"},
+        "config": cfgd,
         "roofline": roofline_of(main, smem_peak, hbm),
         "clocks": main["clocks"],
         "gpu_launches": main["launches"],
@@ -442,13 +501,14 @@ def run_ours(args, rank, world, local_rank):
     if "e2e" in main:
         line["e2e"] = main["e2e"]
     if extra is not None:
-        x = {"workload": workloads[4] + ", detection events + observable, shot-major b8 in HBM",
+        x = {"workload": WORKLOADS[4] + ", detection events + observable, shot-major b8 in HBM",
              "value": extra["value"], "unit": "shots/s", "shots_per_gpu_per_step": extra["shots"],
              "ms_per_step": 1e3 * extra["elapsed"] / extra["steps"], "steps": extra["steps"],
              "host_compile_s": extra["compile_s"],
              "host_reference_sample_s": reference_sample_seconds(config_text(4)),
              "roofline": roofline_of(extra, smem_peak, hbm), "clocks": extra["clocks"],
-             "W": extra["info"]["words_per_tile"], "gpu_launches": extra["launches"]}
+             "W": extra["info"]["words_per_tile"], "ring_in_smem": extra["info"]["ring_in_smem"],
+             "gpu_launches": extra["launches"]}
         if "e2e" in extra:
             x["e2e"] = extra["e2e"]
         if "dem" in extra:
@@ -461,8 +521,8 @@ def run_ours(args, rank, world, local_rank):
     if dem is not None:
         line["error_model_sampler"] = {
             "workload": "config2 through the error-model detector sampler (kernel 4): every noise hit "
-                        "XORs its precomputed detector signature; the frame sampler's own Philox draws, "
-                        "bit-exact with the frame kernel on 32-shot tiles (tests/test_gpu_parity.py)",
+                        "XORs its precomputed detector signature; the same counter-based draws, "
+                        "bit-exact with the oracle (tests/test_gpu_parity.py)",
             "value": dem["value"], "unit": "shots/s", "ms_per_step": 1e3 * dem["elapsed"] / dem["steps"],
             "steps": dem["steps"], "kernel_ms": dem["frame_ms"], "gpu_launches": dem["launches"],
             "clocks": dem["clocks"]}
@@ -470,11 +530,11 @@ def run_ours(args, rank, world, local_rank):
         line["config3_counts"] = c3
     if not args.no_cpu_baseline:
         cores = host_cores()
-        rate, s_shots, dt = cpu_port_rate(config_text(args.config), args.cpu_seconds, cores)
+        rate, s_shots, dt = PortTimer(args.config, cores).rate(args.cpu_seconds)
         line["cpu_baseline"] = {"value": rate, "unit": "shots/s", "cores": cores, "kind": "port",
-                                "sample": f"{s_shots} shots of config {args.config} in "
-                                          f"{dt:.1f}s on {cores} threads ({cpu_model()}); C "
-                                          "restatement of stabsim frame_sim+detector_events+b8"}
+                                "sample": f"{s_shots} shots of config {args.config} in {dt:.1f}s on {cores} "
+                                          f"threads ({cpu_model()}); C restatement of stabsim frame_sim + "
+                                          "detector_events + b8 transpose (same timer as --impl reference)"}
     print(json.dumps(line), flush=True)
 
 
@@ -487,28 +547,15 @@ def reference_sample_seconds(text) -> float:
     return time.perf_counter() - t0
 
 
-def smem_peak_gbs():
-    p = os.path.join(REPO, "profiles", "smem_peak.json")
-    try:
-        with open(p) as f:
-            return float(json.load(f)["smem_gbs"])
-    except Exception:
-        return None
-
-
 def profile_traffic(shots=None, cfg=2):
     """DRAM bytes per frame-kernel launch from the committed ncu capture
-    (profiles/frame_kernel_traffic.json, per shot x this launch's shots);
-    config 4 reads its own d=100 capture."""
+    (profiles/frame_kernel_traffic.json, per shot x this launch's shots)."""
     p = os.path.join(REPO, "profiles", "frame_kernel_traffic.json")
     try:
         with open(p) as f:
             d = json.load(f)
-        if cfg == 4:
-            d = d["config4"]
-        elif cfg != 2:
-            return None
-        return float(d["dram_bytes_per_shot"]) * shots if shots else None
+        d = d.get(f"config{cfg}")
+        return float(d["dram_bytes_per_shot"]) * shots if (d and shots) else None
     except Exception:
         return None
 

@@ -49,17 +49,19 @@ typedef struct pfs_options {
     int32_t debug_skip;       /* profiling ablations only (wrong results!): bit0 noise
                                  apply, bit1 noise pre-pass, bit2 coin RNG, bit3 detectors,
                                  bit4 gates, bit5 collapses */
-    int32_t producer_threads; /* threads sampling the next tile's noise (0 = auto)   */
+    int32_t producer_threads; /* reserved (0)                                        */
     int32_t schedule_only;    /* 1: compile without the shared-memory fit check (the
                                  program exposes info / noise schedule, cannot run)  */
     int32_t groups;           /* independent tiles in flight per CTA (0 = auto)     */
-    int32_t kernel;           /* frame kernel: 0 auto, 1 cooperative (a CTA's threads
-                                 share one tile), 2 warp-private (a warp owns one
-                                 32-shot word column, no CTA barriers)               */
-    int32_t pipeline;         /* noise/frame pipeline: sub-chunks per launch whose
-                                 noise_kernel overlaps the previous sub-chunk's
-                                 frame kernel (0 = auto, 1 = off)                   */
-    int32_t reserved[1];
+    int32_t kernel;           /* 0 auto = 1: frame sampler (frame_kernel, a CTA's
+                                 threads share one tile); 4: error-model detector
+                                 sampler (dem_kernel, detection events only)        */
+    int32_t pipeline;         /* frame / transpose pipeline: sub-chunks per launch
+                                 whose shot-major transpose overlaps the next
+                                 sub-chunk's frame kernel (0 = auto, 1 = off)        */
+    int32_t fused_target_milli; /* expected hits x 1000 per noise chunk of a noise
+                                 instruction fused into its gate / collapse op
+                                 (0 = 500)                                          */
 } pfs_options;
 
 typedef struct pfs_info {
@@ -80,11 +82,12 @@ typedef struct pfs_info {
     int64_t num_coin_rows;
     int64_t num_noise_rows;
     int64_t noise_tab_len;    /* uint64 entries of the Binomial threshold tables   */
-    int64_t hit_capacity;     /* pre-generated noise hit-list entries per CTA       */
-    int64_t pregen_chunks;    /* noise work items (32 chunks each) per tile         */
+    int64_t live_coin_rows;   /* coin rows that reach an output (event program)      */
+    int64_t record_ops;       /* device ops of the measurement-record program        */
     int64_t groups;           /* independent tiles in flight per CTA                */
-    int64_t kernel;           /* frame kernel of row-producing modes: 1 cooperative, 2 warp */
-    int64_t warps_per_cta;    /* warp-private kernel: word columns per CTA (0: unused) */
+    int64_t kernel;           /* 1 frame sampler, 4 error-model sampler              */
+    int64_t warps_per_cta;    /* reserved (0)                                        */
+    int64_t fused_noise;      /* noise instructions applied inside gate / collapse ops */
 } pfs_info;
 
 enum pfs_mode {

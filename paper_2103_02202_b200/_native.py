@@ -33,7 +33,8 @@ class Options(ctypes.Structure):
                 ("noise_target_hits", ctypes.c_double), ("timing", ctypes.c_int32),
                 ("debug_skip", ctypes.c_int32), ("producer_threads", ctypes.c_int32),
                 ("schedule_only", ctypes.c_int32), ("groups", ctypes.c_int32),
-                ("kernel", ctypes.c_int32), ("pipeline", ctypes.c_int32), ("reserved", ctypes.c_int32 * 1)]
+                ("kernel", ctypes.c_int32), ("pipeline", ctypes.c_int32),
+                ("fused_target_milli", ctypes.c_int32)]
 
 
 class Info(ctypes.Structure):
@@ -45,12 +46,13 @@ class Info(ctypes.Structure):
                 ("num_barriers", ctypes.c_int64), ("num_slots", ctypes.c_int64),
                 ("num_noise", ctypes.c_int64), ("bframe_bits", ctypes.c_int64),
                 ("num_coin_rows", ctypes.c_int64), ("num_noise_rows", ctypes.c_int64),
-                ("noise_tab_len", ctypes.c_int64), ("hit_capacity", ctypes.c_int64),
-                ("pregen_chunks", ctypes.c_int64), ("groups", ctypes.c_int64),
-                ("kernel", ctypes.c_int64), ("warps_per_cta", ctypes.c_int64)]
+                ("noise_tab_len", ctypes.c_int64), ("live_coin_rows", ctypes.c_int64),
+                ("record_ops", ctypes.c_int64), ("groups", ctypes.c_int64),
+                ("kernel", ctypes.c_int64), ("warps_per_cta", ctypes.c_int64),
+                ("fused_noise", ctypes.c_int64)]
 
     def as_dict(self) -> dict:
-        return {k: getattr(self, k) for k, _ in self._fields_ if k != "reserved"}
+        return {k: getattr(self, k) for k, _ in self._fields_}
 
 
 EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_schedule", "pfs_run",
@@ -159,7 +161,7 @@ class NativeProgram:
                  threads: int = 0, ctas_per_sm: int = 0, noise_target_hits: float = 0.0,
                  timing: bool = False, debug_skip: int = 0, producer_threads: int = 0,
                  schedule_only: bool = False, groups: int = 0, kernel: int = 0,
-                 pipeline: int = 0):
+                 pipeline: int = 0, fused_target_hits: float = 0.0):
         L = lib()
         self.flat = prog
         self._keep = [np.ascontiguousarray(prog.instrs, dtype=np.int32),
@@ -170,7 +172,7 @@ class NativeProgram:
         ins, tg, p, dp, di = self._keep
         opts = Options(words_per_tile, ring_in_smem, threads, ctas_per_sm, noise_target_hits,
                        1 if timing else 0, debug_skip, producer_threads, 1 if schedule_only else 0,
-                       groups, kernel, pipeline)
+                       groups, kernel, pipeline, int(round(fused_target_hits * 1000)))
         h = ctypes.c_void_p()
         _check(L.pfs_program_create(_p(ins), ins.shape[0], _p(tg), tg.shape[0], _p(p), p.shape[0],
                                     _p(dp), _p(di), prog.num_columns, prog.num_observables,
@@ -189,7 +191,9 @@ class NativeProgram:
             self._h = None
 
     def noise_schedule(self):
-        """(params uint32 [num_noise, 12], tables uint64) — the noise RNG schedule."""
+        """(params uint32 [num_noise, 12], tables uint64) — the noise RNG schedule:
+        per instruction L, cs, ca, nchunks, apps, table offset, table length,
+        zone, npat, channel, fused, 0."""
         params = np.zeros((self.flat.num_noise, 12), dtype=np.uint32)
         tab = np.zeros(self.info["noise_tab_len"], dtype=np.uint64)
         _check(lib().pfs_program_noise_schedule(self._h, _p(params) if params.size else None,

@@ -18,7 +18,7 @@ CSRC = os.path.join(PKG, "csrc")
 LIB_DIR = os.path.join(PKG, "_lib")
 LIB = os.path.join(LIB_DIR, "libpfs.so")
 PROFILE_LIB = os.path.join(LIB_DIR, "libpfs_profile.so")  # PFS_PROFILE=1: traces, ablations
-SOURCES = ["pfs_compile.cpp", "pfs_tableau.cpp", "pfs_dem.cpp", "pfs_kernels.cu", "pfs_colkernel.cu", "pfs_demkernel.cu", "pfs_writers.cu", "pfs_api.cu"]
+SOURCES = ["pfs_compile.cpp", "pfs_tableau.cpp", "pfs_dem.cpp", "pfs_kernels.cu", "pfs_demkernel.cu", "pfs_writers.cu", "pfs_api.cu"]
 HEADERS = ["pfs_internal.h", "pfs_device.cuh", os.path.join("..", "..", "include", "pfs.h")]
 INCLUDE = os.path.join(os.path.dirname(PKG), "include")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]

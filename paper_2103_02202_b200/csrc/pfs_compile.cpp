@@ -7,20 +7,33 @@
 //     a set of independent applications (the reference applies an
 //     instruction's applications sequentially, frame_sim.py:61-62, 196-197 —
 //     `CX 0 1 1 2` must stay two steps);
+//   * fuse a noise instruction into its neighbour when both act on the same
+//     target list: gate / reset then noise (DEPOLARIZE2 after CX, DEPOLARIZE1
+//     after H or R), noise then measurement (X_ERROR before M) — one kernel
+//     item applies both to its rows in registers, no barrier between them;
 //   * merge consecutive instructions of the same frame rule / collapse kind
 //     when they touch disjoint qubits (fewer ops, fewer barriers);
-//   * allocate measurement-record ring slots by liveness: a record lives from
-//     its M until the last DETECTOR / OBSERVABLE_INCLUDE that reads it
-//     (detector sets: stabsim/circuit.py:247-256);
-//   * schedule __syncthreads: a barrier goes before an op only if it touches a
-//     qubit row or record slot already touched since the previous barrier.
+//   * detection-event programs keep a measurement record in the measured
+//     qubit's x row (frame_sim.py:74-80: the record IS x at M) until an op
+//     rewrites that row, and only then spill it to a ring slot (fused into the
+//     reset that rewrites it); slots live until the last DETECTOR /
+//     OBSERVABLE_INCLUDE reading them (stabsim/circuit.py:247-256);
+//   * coin relevance: a collapse coin (z row of FrameBatch.__init__, M, R, MR,
+//     frame_sim.py:36-39, 74-90) whose effect reaches no output is never
+//     drawn (decided by a backward pass over random 128-bit projections of the
+//     output columns);
+//   * schedule group barriers: one goes before an op only if it touches a
+//     qubit row or ring slot already touched since the previous barrier
+//     (standalone noise ops commute with each other: their XORs are atomic).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <map>
 #include <stdexcept>
 #include <string>
 #include <unordered_map>
+#include <utility>
 
 #include "pfs_internal.h"
 
@@ -41,7 +54,34 @@ int64_t rule_bits(int32_t rule) {
     }
 }
 
+// does the frame rule (stabsim/gates.py:70-92) write the x row of slot s?
+bool rule_writes_x(int32_t rule, int s) {
+    switch (rule) {
+        case R_SWAPXZ: case R_XXORZ: case R_SWAP: return true;
+        case R_CX: case R_CY: return s == 1;
+        default: return false;  // R_ZXORX, R_CZ write z only
+    }
+}
+
+int channel_arity(int32_t ch) { return ch == CH_DEP2 ? 2 : 1; }
+// noise XORs x rows (injected masks may carry x bits for any channel)
+bool channel_writes_x(int32_t) { return true; }
+
 [[noreturn]] void bad(const std::string& msg) { throw std::invalid_argument(msg); }
+
+uint64_t splitmix64(uint64_t x) {
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+
+// 128-bit random projection of a set of output columns (GF(2) linear)
+struct H128 {
+    uint64_t a = 0, b = 0;
+    void x(const H128& o) { a ^= o.a; b ^= o.b; }
+    bool zero() const { return (a | b) == 0; }
+};
 
 }  // namespace
 
@@ -49,13 +89,16 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
                             int64_t n_targets, const double* noise_p, int64_t n_noise,
                             const int64_t* det_ptr, const int64_t* det_idx, int64_t n_cols,
                             int64_t n_obs, int32_t num_qubits, int64_t num_meas,
-                            int64_t num_coin_rows, int64_t num_noise_rows) {
+                            int64_t num_coin_rows, int64_t num_noise_rows, int mode) {
     if (num_qubits < 0 || num_meas < 0 || n_cols < 0 || n_obs < 0 || n_obs > n_cols)
         bad("negative sizes");
     if (n_ins > 0 && (!ins || (n_targets > 0 && !targets))) bad("null instruction arrays");
     if (n_cols > 0 && (!det_ptr)) bad("null detector arrays");
+    if (num_qubits >= (1 << 30)) bad("too many qubits");
+    const bool events = mode == PM_EVENTS;
     const int64_t n_det = n_cols - n_obs;
     HostProgram hp;
+    hp.mode = mode;
     hp.num_qubits = num_qubits;
     hp.num_meas = num_meas;
     hp.num_cols = n_cols;
@@ -65,17 +108,19 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
     hp.num_noise_rows = num_noise_rows;
     hp.noise_p.assign(noise_p, noise_p + n_noise);
     hp.noise_apps.assign(n_noise, 0);
-    hp.noise_arity.assign(n_noise, 1);
-    hp.noise_off.assign(n_noise, 0);
     hp.noise_ch.assign(n_noise, 0);
-    hp.noise.assign(n_noise, NoiseParam{});
+    hp.noise_fused.assign(n_noise, 0);
+    hp.noise_rowb.assign(n_noise, 0);
+    if (num_noise_rows >= (1ll << 32)) bad("too many noise rows");
     for (int64_t i = 0; i < n_noise; i++) {
         double p = noise_p[i];
         if (!(p >= 0.0 && p <= 1.0)) bad("noise probability must be in [0, 1], got " + std::to_string(p));
     }
 
-    // ---- pass 1: validate and compute record liveness ----
+    // ---- pass 1: validate, record liveness, distinct-target instructions ----
     std::vector<int64_t> last_use(num_meas, -1);
+    std::vector<char> distinct(n_ins, 1);
+    std::vector<int64_t> qstamp(num_qubits, -1);
     {
         int64_t rec = 0, coin = num_qubits, nrow = 0, col = 0;
         for (int64_t i = 0; i < n_ins; i++) {
@@ -83,21 +128,25 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
             if (in.n_targets < 0 || in.tgt_off < 0 || (int64_t)in.tgt_off + in.n_targets > n_targets)
                 bad("instruction " + std::to_string(i) + ": target range out of bounds");
             const int32_t* tg = targets + in.tgt_off;
+            auto check_qubits = [&]() {
+                for (int j = 0; j < in.n_targets; j++) {
+                    if (tg[j] < 0 || tg[j] >= num_qubits)
+                        bad("qubit " + std::to_string(tg[j]) + " out of range [0, " + std::to_string(num_qubits) + ")");
+                    if (qstamp[tg[j]] == i) distinct[i] = 0;
+                    qstamp[tg[j]] = i;
+                }
+            };
             switch (in.kind) {
             case K_GATE:
                 if (in.code <= R_NONE || in.code > R_SWAP) bad("unknown frame rule");
                 if (in.n_targets % rule_arity(in.code)) bad("gate target count not a multiple of arity");
-                for (int j = 0; j < in.n_targets; j++)
-                    if (tg[j] < 0 || tg[j] >= num_qubits)
-                        bad("qubit " + std::to_string(tg[j]) + " out of range [0, " + std::to_string(num_qubits) + ")");
+                check_qubits();
                 for (int j = 0; j + 1 < in.n_targets && rule_arity(in.code) == 2; j += 2)
                     if (tg[j] == tg[j + 1]) bad("two-qubit gate targets a qubit pair twice");
                 hp.bframe_bits += rule_bits(in.code) * (in.n_targets / rule_arity(in.code));
                 break;
             case K_M: case K_R: case K_MR:
-                for (int j = 0; j < in.n_targets; j++)
-                    if (tg[j] < 0 || tg[j] >= num_qubits)
-                        bad("qubit " + std::to_string(tg[j]) + " out of range [0, " + std::to_string(num_qubits) + ")");
+                check_qubits();
                 if (in.kind != K_R && in.rec_base != rec) bad("record numbering is not contiguous");
                 if (in.coin_base != coin) bad("coin row numbering is not contiguous");
                 if (in.kind != K_R) rec += in.n_targets;
@@ -106,16 +155,14 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
                 break;
             case K_NOISE: {
                 if (in.code < CH_XERR || in.code > CH_DEP2) bad("unknown noise channel");
-                int ar = in.code == CH_DEP2 ? 2 : 1;
+                const int ar = channel_arity(in.code);
                 if (in.n_targets % ar) bad("noise target count not a multiple of arity");
-                for (int j = 0; j < in.n_targets; j++)
-                    if (tg[j] < 0 || tg[j] >= num_qubits)
-                        bad("qubit " + std::to_string(tg[j]) + " out of range [0, " + std::to_string(num_qubits) + ")");
+                check_qubits();
                 if (in.aux < 0 || in.aux >= n_noise) bad("noise ordinal out of range");
                 if (in.noise_row_base != nrow) bad("noise row numbering is not contiguous");
                 hp.noise_apps[in.aux] = (uint32_t)(in.n_targets / ar);
-                hp.noise_arity[in.aux] = (uint32_t)ar;
-                hp.noise[in.aux].npat = in.code == CH_DEP1 ? 3u : (in.code == CH_DEP2 ? 15u : 1u);
+                hp.noise_ch[in.aux] = (uint32_t)in.code;
+                hp.noise_rowb[in.aux] = (uint32_t)in.noise_row_base;
                 nrow += 2 * (int64_t)in.n_targets;
                 break;
             }
@@ -149,32 +196,181 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
         if (nrow != num_noise_rows) bad("noise row count mismatch");
     }
 
-    // ---- pass 2: emit device ops, allocating record slots ----
+    // ---- pass 1b: noise fusion plan ----
+    // fuse_post[i]: noise instruction i+1 is applied inside gate / reset i;
+    // fuse_pre[i]: noise instruction i is applied inside measurement i+1.
+    std::vector<char> fuse_post(n_ins, 0), fuse_pre(n_ins, 0), fused_noise(n_ins, 0);
+    auto same_targets = [&](const pfs_instr& a, const pfs_instr& b) {
+        return a.n_targets == b.n_targets &&
+               std::equal(targets + a.tgt_off, targets + a.tgt_off + a.n_targets, targets + b.tgt_off);
+    };
+    for (int64_t i = 0; i + 1 < n_ins; i++) {
+        const pfs_instr& a = ins[i];
+        const pfs_instr& b = ins[i + 1];
+        if (!distinct[i] || a.n_targets == 0 || fused_noise[i]) continue;
+        if ((a.kind == K_GATE || a.kind == K_R) && b.kind == K_NOISE &&
+            (a.kind == K_R ? 1 : rule_arity(a.code)) == channel_arity(b.code) && same_targets(a, b)) {
+            fuse_post[i] = 1;
+            fused_noise[i + 1] = 1;
+        } else if (a.kind == K_NOISE && (b.kind == K_M || b.kind == K_MR) && channel_arity(a.code) == 1 &&
+                   same_targets(a, b)) {
+            fuse_pre[i] = 1;
+            fused_noise[i] = 1;
+        }
+    }
+
+    // ---- pass 1c: coin relevance ----
+    // Backward over the program with a random 128-bit projection h(S) of the
+    // output-column set S each frame component would flip (the transposed
+    // frame rules; gates.py:70-92): a coin is relevant iff the projection of
+    // its z component at the collapse is non-zero (a relevant coin is missed
+    // with probability 2^-128).  Outputs: detector / observable columns for
+    // event programs, every measurement record for record programs.
+    std::vector<char> coin_live(num_coin_rows, 1);
+    {
+        std::vector<H128> rech(num_meas);
+        auto rnd = [](uint64_t salt, uint64_t k) {
+            H128 h;
+            h.a = splitmix64(k * 2 + 0x51A7 + salt);
+            h.b = splitmix64(k * 2 + 1 + 0xC0FFEE00ull + salt);
+            return h;
+        };
+        if (events) {
+            for (int64_t c = 0; c < n_cols; c++) {
+                const H128 h = rnd(1, (uint64_t)c);
+                for (int64_t e = det_ptr[c]; e < det_ptr[c + 1]; e++) rech[det_idx[e]].x(h);
+            }
+        } else {
+            for (int64_t m = 0; m < num_meas; m++) rech[m] = rnd(2, (uint64_t)m);
+        }
+        std::vector<H128> sx(num_qubits), sz(num_qubits);
+        for (int64_t i = n_ins - 1; i >= 0; i--) {
+            const pfs_instr& in = ins[i];
+            const int32_t* tg = targets + in.tgt_off;
+            switch (in.kind) {
+            case K_GATE: {
+                const int ar = rule_arity(in.code);
+                for (int j = in.n_targets - ar; j >= 0; j -= ar) {
+                    const int32_t a = tg[j], b = ar == 2 ? tg[j + 1] : -1;
+                    switch (in.code) {
+                        case R_SWAPXZ: std::swap(sx[a], sz[a]); break;
+                        case R_ZXORX: sx[a].x(sz[a]); break;
+                        case R_XXORZ: sz[a].x(sx[a]); break;
+                        case R_CX: sx[a].x(sx[b]); sz[b].x(sz[a]); break;
+                        case R_CZ: sx[a].x(sz[b]); sx[b].x(sz[a]); break;
+                        case R_CY: {
+                            H128 x0 = sx[a];
+                            x0.x(sx[b]);
+                            x0.x(sz[b]);
+                            sx[b].x(sz[a]);
+                            sz[b].x(sz[a]);
+                            sx[a] = x0;
+                            break;
+                        }
+                        default: std::swap(sx[a], sx[b]); std::swap(sz[a], sz[b]); break;
+                    }
+                }
+                break;
+            }
+            case K_M:
+                for (int j = in.n_targets - 1; j >= 0; j--) {
+                    const int32_t q = tg[j];
+                    coin_live[in.coin_base + j] = !sz[q].zero();
+                    sx[q].x(rech[in.rec_base + j]);
+                }
+                break;
+            case K_MR:
+                for (int j = in.n_targets - 1; j >= 0; j--) {
+                    const int32_t q = tg[j];
+                    coin_live[in.coin_base + 2 * j + 1] = !sz[q].zero();
+                    coin_live[in.coin_base + 2 * j] = 0;  // overwritten by the reset's coin
+                    sx[q] = H128{};
+                    sz[q] = H128{};
+                    sx[q].x(rech[in.rec_base + j]);
+                }
+                break;
+            case K_R:
+                for (int j = in.n_targets - 1; j >= 0; j--) {
+                    const int32_t q = tg[j];
+                    coin_live[in.coin_base + j] = !sz[q].zero();
+                    sx[q] = H128{};
+                    sz[q] = H128{};
+                }
+                break;
+            default: break;
+            }
+        }
+        for (int32_t q = 0; q < num_qubits; q++) coin_live[q] = !sz[q].zero();
+        hp.init_dead.assign(((size_t)num_qubits + 31) / 32, 0u);
+        for (int32_t q = 0; q < num_qubits; q++)
+            if (!coin_live[q]) hp.init_dead[q >> 5] |= 1u << (q & 31);
+        for (char c : coin_live) hp.live_coin_rows += c ? 1 : 0;
+    }
+
+    // ---- pass 2: emit device ops ----
     std::vector<uint32_t> slot_of(num_meas, NO_SLOT);
+    std::vector<int32_t> home_of(num_meas, -1);            // record homed in this qubit's x row
+    std::vector<std::vector<uint32_t>> xrec(num_qubits);    // live records homed in x_q
     std::vector<uint32_t> free_slots;
-    uint32_t next_slot = (uint32_t)n_obs;  // [0, n_obs) = observable accumulators
+    uint32_t next_slot = (uint32_t)(events ? n_obs : 0);   // [0, n_obs) = observable accumulators
     std::vector<int64_t> stamp(num_qubits, -1);
     int64_t cur = -1;  // open (mergeable) op index
     auto open_op = [&](uint32_t kind, uint32_t code) {
-        // ops read their targets as uint2 pairs (two-qubit rules, (qubit, slot)
-        // pairs of M/MR): keep every op's target list 8-byte aligned
+        // ops read their targets as uint2 pairs (two-qubit rules, (row, slot)
+        // pairs): keep every op's target list 8-byte aligned
         if (hp.targets.size() & 1) hp.targets.push_back(0u);
         DOp op{};
         op.kcf = kind | (code << 8);
         op.off = (uint32_t)hp.targets.size();
+        op.c = NO_SLOT;
         hp.ops.push_back(op);
         cur = (int64_t)hp.ops.size() - 1;
     };
     auto kind_of = [&](int64_t k) { return hp.ops[k].kcf & 0xFF; };
     auto code_of = [&](int64_t k) { return (hp.ops[k].kcf >> 8) & 0xFF; };
+    auto mergeable = [&](int64_t k) { return !((hp.ops[k].kcf >> 16) & F_NOISE); };
     auto alloc = [&]() -> uint32_t {
         if (!free_slots.empty()) { uint32_t s = free_slots.back(); free_slots.pop_back(); return s; }
         return next_slot++;
     };
-    hp.det_ptr.assign(1, 0);
-    auto release_after = [&](int64_t i, int64_t m) {
-        if (last_use[m] == i && slot_of[m] != NO_SLOT) { free_slots.push_back(slot_of[m]); slot_of[m] = NO_SLOT; }
+    // records homed in x_q that are still needed at or after instruction i move
+    // to slots: one through `first` (fused into a reset), the rest via a SPILL op
+    std::vector<std::pair<uint32_t, uint32_t>> spills;  // (qubit, slot) pairs of the pending SPILL op
+    auto take_homes = [&](int32_t q, int64_t i, uint32_t* first) {
+        std::vector<uint32_t>& v = xrec[q];
+        for (uint32_t m : v) {
+            if (last_use[m] < i || home_of[m] != q) continue;
+            const uint32_t s = alloc();
+            slot_of[m] = s;
+            home_of[m] = -1;
+            if (first && *first == NO_SLOT) *first = s;
+            else spills.emplace_back((uint32_t)q, s);
+        }
+        v.clear();
     };
+    auto flush_spills = [&]() {
+        if (spills.empty()) return;
+        open_op(K_SPILL, 0);
+        for (auto& ps : spills) { hp.targets.push_back(ps.first); hp.targets.push_back(ps.second); }
+        hp.ops[cur].count = (uint32_t)spills.size();
+        spills.clear();
+        cur = -1;
+    };
+    auto release = [&](int64_t i, int64_t m) {
+        if (last_use[m] != i) return;
+        if (slot_of[m] != NO_SLOT) { free_slots.push_back(slot_of[m]); slot_of[m] = NO_SLOT; }
+        if (home_of[m] >= 0) {
+            std::vector<uint32_t>& v = xrec[home_of[m]];
+            v.erase(std::remove(v.begin(), v.end(), (uint32_t)m), v.end());
+            home_of[m] = -1;
+        }
+    };
+    auto term_of = [&](int64_t m) -> uint32_t {
+        if (slot_of[m] != NO_SLOT) return slot_of[m];
+        if (home_of[m] >= 0) return XROW | (uint32_t)home_of[m];
+        bad("internal: record " + std::to_string(m) + " has no location");
+    };
+    hp.det_ptr.assign(1, 0);
 
     for (int64_t i = 0; i < n_ins; i++) {
         const pfs_instr& in = ins[i];
@@ -182,8 +378,28 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
         switch (in.kind) {
         case K_GATE: {
             const int ar = rule_arity(in.code);
+            const bool fz = fuse_post[i] != 0;
+            const pfs_instr* nz = fz ? &ins[i + 1] : nullptr;
+            if (events) {  // records homed in rows this op rewrites move to slots first
+                for (int j = 0; j < in.n_targets; j++)
+                    if (rule_writes_x(in.code, j % ar) || (nz && channel_writes_x(nz->code)))
+                        if (!xrec[tg[j]].empty()) take_homes(tg[j], i, nullptr);
+                flush_spills();
+            }
+            if (fz) {
+                open_op(K_GATE, in.code);
+                DOp& o = hp.ops[cur];
+                o.kcf |= F_NOISE << 16;
+                o.count = (uint32_t)(in.n_targets / ar);
+                o.c = (uint32_t)nz->aux;
+                hp.noise_fused[nz->aux] = 1;
+                for (int j = 0; j < in.n_targets; j++) hp.targets.push_back((uint32_t)tg[j]);
+                cur = -1;
+                break;
+            }
             for (int j = 0; j < in.n_targets; j += ar) {
-                bool conflict = cur < 0 || kind_of(cur) != K_GATE || code_of(cur) != (uint32_t)in.code;
+                bool conflict = cur < 0 || kind_of(cur) != K_GATE || code_of(cur) != (uint32_t)in.code ||
+                                !mergeable(cur);
                 for (int s = 0; s < ar && !conflict; s++) conflict = stamp[tg[j + s]] == cur;
                 if (conflict) open_op(K_GATE, in.code);
                 for (int s = 0; s < ar; s++) { hp.targets.push_back((uint32_t)tg[j + s]); stamp[tg[j + s]] = cur; }
@@ -194,77 +410,107 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
         case K_M: case K_MR: case K_R: {
             const bool records = in.kind != K_R;
             const int coin_per = in.kind == K_MR ? 2 : 1;
+            // pre-noise: noise instruction i-1 applied inside this op
+            const pfs_instr* pre = (i > 0 && fuse_pre[i - 1]) ? &ins[i - 1] : nullptr;
+            const pfs_instr* nz = (in.kind == K_R && fuse_post[i]) ? &ins[i + 1] : pre;
+            std::vector<uint32_t> rspill;  // R: slot each target's homed record moves to
+            if (events) {
+                for (int j = 0; j < in.n_targets; j++) {
+                    const int32_t q = tg[j];
+                    if (xrec[q].empty()) continue;
+                    if (in.kind == K_M && !(pre && channel_writes_x(pre->code))) continue;  // M keeps x
+                    if (in.kind == K_R) {
+                        if (rspill.empty()) rspill.assign(in.n_targets, NO_SLOT);
+                        take_homes(q, i, &rspill[j]);
+                    } else {
+                        take_homes(q, i, nullptr);
+                    }
+                }
+                flush_spills();
+            }
+            const bool fused = nz != nullptr;
             for (int j = 0; j < in.n_targets; j++) {
                 const int64_t q = tg[j];
                 const uint32_t rec = (uint32_t)(in.rec_base + j);
                 const uint32_t coin = (uint32_t)(in.coin_base + (int64_t)coin_per * j);
-                bool conflict = cur < 0 || kind_of(cur) != in.kind || stamp[q] == cur;
+                bool conflict = cur < 0 || kind_of(cur) != in.kind || stamp[q] == cur || !mergeable(cur);
                 if (!conflict) {
                     const DOp& o = hp.ops[cur];
                     if (records && o.a + o.count != rec) conflict = true;
                     if (o.b + (uint32_t)coin_per * o.count != coin) conflict = true;
                 }
+                if (fused) conflict = j == 0;  // one op holds the whole fused instruction
                 if (conflict) {
                     open_op(in.kind, 0);
                     hp.ops[cur].a = records ? rec : 0;
                     hp.ops[cur].b = coin;
+                    if (fused) {
+                        hp.ops[cur].kcf |= F_NOISE << 16;
+                        hp.ops[cur].c = (uint32_t)nz->aux;
+                        hp.noise_fused[nz->aux] = 1;
+                    }
                 }
-                hp.targets.push_back((uint32_t)q);
-                if (records) {
-                    uint32_t s = NO_SLOT;
-                    if (last_use[rec] >= 0) { s = alloc(); slot_of[rec] = s; }
-                    hp.targets.push_back(s);
+                const bool live = coin_live[coin + (in.kind == K_MR ? 1 : 0)] != 0;
+                hp.targets.push_back((uint32_t)q | (live ? 0u : COIN_DEAD));
+                uint32_t s = NO_SLOT;
+                if (in.kind == K_R) {
+                    s = rspill.empty() ? NO_SLOT : rspill[j];
+                } else if (events && last_use[rec] >= 0) {
+                    if (in.kind == K_MR) { s = alloc(); slot_of[rec] = s; }  // the reset rewrites x
+                    else { home_of[rec] = (int32_t)q; xrec[q].push_back(rec); }
                 }
+                hp.targets.push_back(s);
                 stamp[q] = cur;
                 hp.ops[cur].count++;
             }
+            if (fused) cur = -1;
             break;
         }
         case K_NOISE: {
-            const int ar = in.code == CH_DEP2 ? 2 : 1;
+            if (fused_noise[i]) break;  // emitted inside its gate / collapse op
+            const int ar = channel_arity(in.code);
+            if (events && channel_writes_x(in.code)) {
+                for (int j = 0; j < in.n_targets; j++)
+                    if (!xrec[tg[j]].empty()) take_homes(tg[j], i, nullptr);
+                flush_spills();
+            }
             open_op(K_NOISE, in.code);
             DOp& o = hp.ops[cur];
             o.count = (uint32_t)(in.n_targets / ar);
-            o.a = (uint32_t)in.noise_row_base;
-            o.b = (uint32_t)in.aux;
-            hp.noise_off[in.aux] = o.off;
-            hp.noise_ch[in.aux] = (uint32_t)in.code;
-            bool dup = false;
-            for (int j = 0; j < in.n_targets; j++) {
-                if (stamp[tg[j]] == cur) dup = true;
-                stamp[tg[j]] = cur;
-                hp.targets.push_back((uint32_t)tg[j]);
-            }
-            if (dup) o.kcf |= F_DUP << 16;
+            o.c = (uint32_t)in.aux;
+            if (!distinct[i]) o.kcf |= F_DUP << 16;
+            for (int j = 0; j < in.n_targets; j++) hp.targets.push_back((uint32_t)tg[j]);
             cur = -1;  // never merge noise ops (one RNG domain per instruction)
             break;
         }
         case K_DET: {
+            if (!events) break;
             const int64_t col = in.aux;
             if (cur < 0 || kind_of(cur) != K_DET || hp.ops[cur].a + hp.ops[cur].count != (uint32_t)col) {
                 open_op(K_DET, 0);
                 hp.ops[cur].a = (uint32_t)col;
             }
             hp.ops[cur].count++;
-            for (int64_t e = det_ptr[col]; e < det_ptr[col + 1]; e++) hp.det_terms.push_back(slot_of[det_idx[e]]);
+            for (int64_t e = det_ptr[col]; e < det_ptr[col + 1]; e++) hp.det_terms.push_back(term_of(det_idx[e]));
             hp.det_ptr.push_back((uint32_t)hp.det_terms.size());
-            for (int64_t e = det_ptr[col]; e < det_ptr[col + 1]; e++) release_after(i, det_idx[e]);
+            for (int64_t e = det_ptr[col]; e < det_ptr[col + 1]; e++) release(i, det_idx[e]);
             break;
         }
         case K_OBS: {
+            if (!events) break;
             open_op(K_OBS, 0);
             DOp& o = hp.ops[cur];
             o.count = (uint32_t)in.n_targets;
             o.a = (uint32_t)(in.aux - n_det);  // accumulator slot
-            for (int j = 0; j < in.n_targets; j++) hp.targets.push_back(slot_of[tg[j]]);
-            for (int j = 0; j < in.n_targets; j++) release_after(i, tg[j]);
+            for (int j = 0; j < in.n_targets; j++) hp.targets.push_back(term_of(tg[j]));
+            for (int j = 0; j < in.n_targets; j++) release(i, tg[j]);
             cur = -1;
             break;
         }
         }
     }
     // observable columns: one term each, the accumulator slot
-    if (n_obs > 0) {
+    if (events && n_obs > 0) {
         open_op(K_DET, 0);
         hp.ops[cur].a = (uint32_t)n_det;
         hp.ops[cur].count = (uint32_t)n_obs;
@@ -274,6 +520,20 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
         }
     }
     hp.num_slots = next_slot;
+
+    // event programs: a measurement that keeps its records in x rows, draws no
+    // coin and carries no noise does nothing — drop it
+    if (events) {
+        std::vector<DOp> kept;
+        kept.reserve(hp.ops.size());
+        for (const DOp& o : hp.ops) {
+            bool noop = (o.kcf & 0xFF) == K_M && !((o.kcf >> 16) & F_NOISE);
+            for (uint32_t j = 0; noop && j < o.count; j++)
+                noop = (hp.targets[o.off + 2 * j] & COIN_DEAD) && hp.targets[o.off + 2 * j + 1] == NO_SLOT;
+            if (!noop) kept.push_back(o);
+        }
+        hp.ops.swap(kept);
+    }
 
     // DET ops whose columns all have the same term count k get direct term
     // addressing: terms of column a+i at det_terms[off + i*k] (off = term base,
@@ -289,102 +549,59 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
         if (uniform) o.kcf = (o.kcf & ~0xFF00u) | (k << 8);
     }
 
-    // ---- pass 2b: dead collapse coins ----
-    // A coin row sets z_q (FrameBatch.__init__, R, MR: z = coin; M: z ^= coin,
-    // frame_sim.py:36-39, 74-90).  If z_q is overwritten by a later R / MR (or
-    // the circuit ends) before any gate reads it, that coin can never reach a
-    // measurement: the kernels skip its Philox draw.  Gates conservatively count
-    // as reads of every operand; noise only XORs into z and DET/OBS touch no
-    // frame rows.  Flag = bit 31 of the M/MR/R target word (COIN_DEAD).
-    {
-        std::vector<std::vector<uint32_t>> pending(num_qubits);  // target-word indices
-        std::vector<char> init_pending(num_qubits, 1);
-        hp.init_dead.assign(((size_t)num_qubits + 31) / 32, 0u);
-        auto kill = [&](uint32_t q) {
-            for (uint32_t w : pending[q]) hp.targets[w] |= COIN_DEAD;
-            pending[q].clear();
-            if (init_pending[q]) { hp.init_dead[q >> 5] |= 1u << (q & 31); init_pending[q] = 0; }
-        };
-        for (const DOp& o : hp.ops) {
-            const uint32_t kind = o.kcf & 0xFF;
-            switch (kind) {
-            case K_GATE: {
-                const int ar = rule_arity((o.kcf >> 8) & 0xFF);
-                for (uint32_t j = 0; j < o.count * ar; j++) {
-                    const uint32_t q = hp.targets[o.off + j];
-                    pending[q].clear();
-                    init_pending[q] = 0;
-                }
-                break;
-            }
-            case K_M:
-                for (uint32_t j = 0; j < o.count; j++) pending[hp.targets[o.off + 2 * j]].push_back(o.off + 2 * j);
-                break;
-            case K_MR:
-                for (uint32_t j = 0; j < o.count; j++) {
-                    const uint32_t q = hp.targets[o.off + 2 * j];
-                    kill(q);
-                    pending[q].push_back(o.off + 2 * j);
-                }
-                break;
-            case K_R:
-                for (uint32_t j = 0; j < o.count; j++) {
-                    const uint32_t q = hp.targets[o.off + j];
-                    kill(q);
-                    pending[q].push_back(o.off + j);
-                }
-                break;
-            default: break;
-            }
-        }
-        for (int32_t q = 0; q < num_qubits; q++) kill((uint32_t)q);  // end of circuit
-    }
-
-    // ---- pass 3: barrier scheduling over qubit rows + record slots ----
+    // ---- pass 3: barrier scheduling over qubit rows + ring slots ----
     const int64_t nres = (int64_t)num_qubits + hp.num_slots;
     std::vector<int64_t> rstamp(nres, -1);
+    std::vector<char> rnoise(nres, 0);  // touched only by standalone noise ops in this segment
     int64_t seg = 0;
     std::vector<int64_t> res;
     for (size_t k = 0; k < hp.ops.size(); k++) {
         DOp& o = hp.ops[k];
         const uint32_t kind = o.kcf & 0xFF;
         res.clear();
+        auto row = [&](uint32_t w) { res.push_back((int64_t)(w & ~COIN_DEAD)); };
+        auto slot = [&](uint32_t s) { if (s != NO_SLOT) res.push_back(num_qubits + (int64_t)s); };
+        auto term = [&](uint32_t t) {
+            if (t == NO_SLOT) return;
+            if (t & XROW) res.push_back((int64_t)(t & ~XROW));
+            else res.push_back(num_qubits + (int64_t)t);
+        };
         switch (kind) {
         case K_GATE: {
-            int ar = rule_arity((o.kcf >> 8) & 0xFF);
-            for (uint32_t j = 0; j < o.count * ar; j++) res.push_back(hp.targets[o.off + j]);
+            const int ar = rule_arity((o.kcf >> 8) & 0xFF);
+            for (uint32_t j = 0; j < o.count * ar; j++) row(hp.targets[o.off + j]);
             break;
         }
-        case K_M: case K_MR:
+        case K_M: case K_MR: case K_R: case K_SPILL:
             for (uint32_t j = 0; j < o.count; j++) {
-                res.push_back(hp.targets[o.off + 2 * j] & ~COIN_DEAD);
-                uint32_t s = hp.targets[o.off + 2 * j + 1];
-                if (s != NO_SLOT) res.push_back(num_qubits + (int64_t)s);
+                row(hp.targets[o.off + 2 * j]);
+                slot(hp.targets[o.off + 2 * j + 1]);
             }
             break;
-        case K_R:
-            for (uint32_t j = 0; j < o.count; j++) res.push_back(hp.targets[o.off + j] & ~COIN_DEAD);
-            break;
         case K_NOISE: {
-            int ar = ((o.kcf >> 8) & 0xFF) == CH_DEP2 ? 2 : 1;
-            for (uint32_t j = 0; j < o.count * ar; j++) res.push_back(hp.targets[o.off + j]);
+            const int ar = channel_arity((o.kcf >> 8) & 0xFF);
+            for (uint32_t j = 0; j < o.count * ar; j++) row(hp.targets[o.off + j]);
             break;
         }
         case K_DET:
             for (uint32_t c = o.a; c < o.a + o.count; c++)
-                for (uint32_t e = hp.det_ptr[c]; e < hp.det_ptr[c + 1]; e++)
-                    if (hp.det_terms[e] != NO_SLOT) res.push_back(num_qubits + (int64_t)hp.det_terms[e]);
+                for (uint32_t e = hp.det_ptr[c]; e < hp.det_ptr[c + 1]; e++) term(hp.det_terms[e]);
             break;
         case K_OBS:
-            res.push_back(num_qubits + (int64_t)o.a);
-            for (uint32_t j = 0; j < o.count; j++)
-                if (hp.targets[o.off + j] != NO_SLOT) res.push_back(num_qubits + (int64_t)hp.targets[o.off + j]);
+            slot(o.a);
+            for (uint32_t j = 0; j < o.count; j++) term(hp.targets[o.off + j]);
             break;
         }
+        const bool nz = kind == K_NOISE;
         bool conflict = false;
-        for (int64_t r : res) if (rstamp[r] == seg) { conflict = true; break; }
+        for (int64_t r : res)
+            if (rstamp[r] == seg && !(nz && rnoise[r])) { conflict = true; break; }
         if (conflict && k > 0) { seg++; o.kcf |= F_BARRIER << 16; }
-        for (int64_t r : res) rstamp[r] = seg;
+        for (int64_t r : res) {
+            if (rstamp[r] != seg) rnoise[r] = nz ? 1 : 0;
+            else rnoise[r] = rnoise[r] && nz;
+            rstamp[r] = seg;
+        }
     }
     hp.num_barriers = seg;
     return hp;
@@ -410,34 +627,37 @@ void permute_rows(HostProgram& hp) {
         std::swap(hp.row_of[i - 1], hp.row_of[z % i]);
     }
     auto map = [&](uint32_t& w) { w = hp.row_of[w & ~COIN_DEAD] | (w & COIN_DEAD); };
+    auto map_term = [&](uint32_t& t) { if (t != NO_SLOT && (t & XROW)) t = XROW | hp.row_of[t & ~XROW]; };
     for (const DOp& o : hp.ops) {
         const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
         uint32_t* t = hp.targets.data() + o.off;
         switch (kind) {
             case K_GATE: for (uint32_t j = 0; j < o.count * rule_arity(code); j++) map(t[j]); break;
-            case K_M: case K_MR: for (uint32_t j = 0; j < o.count; j++) map(t[2 * j]); break;
-            case K_R: for (uint32_t j = 0; j < o.count; j++) map(t[j]); break;
+            case K_M: case K_MR: case K_R: case K_SPILL: for (uint32_t j = 0; j < o.count; j++) map(t[2 * j]); break;
             case K_NOISE:
-                for (uint32_t j = 0; j < o.count * (code == CH_DEP2 ? 2u : 1u); j++) map(t[j]);
+                for (uint32_t j = 0; j < o.count * channel_arity(code); j++) map(t[j]);
                 break;
+            case K_OBS: for (uint32_t j = 0; j < o.count; j++) map_term(t[j]); break;
             default: break;
         }
     }
+    for (uint32_t& t : hp.det_terms) map_term(t);
 }
 
-// Reorder the applications of every gate op so each aligned group of G
-// consecutive applications (the apps one shared-memory wavefront serves: G =
+// Reorder the applications of every unfused gate op so each aligned group of
+// G consecutive applications (the apps one shared-memory wavefront serves: G =
 // 128 B / row bytes) touches G distinct bank groups per operand: apps are
 // classed by (first, second) operand residue mod G and each group takes one
 // app per first residue, choosing among the second residues still unused the
 // fullest class.  Apps of one op are independent by construction, so any
-// order is the same circuit.
+// order is the same circuit.  (A fused op keeps its noise instruction's
+// application order: it defines the noise trials.)
 void reorder_for_banks(HostProgram& hp, int W) {
     const int G = W >= 32 ? 1 : 128 / (W * 4);
     if (G <= 1) return;
     std::vector<uint32_t> scratch;
     for (DOp& o : hp.ops) {
-        if ((o.kcf & 0xFF) != K_GATE || o.count < 2) continue;
+        if ((o.kcf & 0xFF) != K_GATE || o.count < 2 || ((o.kcf >> 16) & F_NOISE)) continue;
         const int ar = rule_arity((o.kcf >> 8) & 0xFF);
         const uint32_t A = o.count;
         uint32_t* tg = hp.targets.data() + o.off;
@@ -505,12 +725,11 @@ void dedup_operands(HostProgram& hp) {
         const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
         switch (kind) {
             case K_GATE: o.off = canon(seen_t, hp.targets, o.off, (size_t)o.count * rule_arity(code)); break;
-            case K_M: case K_MR: o.off = canon(seen_t, hp.targets, o.off, 2 * (size_t)o.count); break;
-            case K_R: case K_OBS: o.off = canon(seen_t, hp.targets, o.off, o.count); break;
-            case K_NOISE:
-                o.off = canon(seen_t, hp.targets, o.off, (size_t)o.count * (code == CH_DEP2 ? 2 : 1));
-                hp.noise_off[o.b] = o.off;
+            case K_M: case K_MR: case K_R: case K_SPILL:
+                o.off = canon(seen_t, hp.targets, o.off, 2 * (size_t)o.count);
                 break;
+            case K_OBS: o.off = canon(seen_t, hp.targets, o.off, o.count); break;
+            case K_NOISE: o.off = canon(seen_t, hp.targets, o.off, (size_t)o.count * channel_arity(code)); break;
             case K_DET:
                 if (code) o.off = canon(seen_d, hp.det_terms, o.off, (size_t)o.count * code);
                 break;
@@ -551,132 +770,74 @@ static std::vector<uint64_t> binomial_thresholds(uint64_t n, double p) {
     return t;
 }
 
-void build_noise_schedule(HostProgram& hp, int tile_shots, double target_hits) {
+static uint32_t ilog2(uint64_t v) {
+    uint32_t l = 0;
+    while ((1ull << l) < v) l++;
+    return l;
+}
+
+// Chunk geometry and Binomial tables of every noise instruction (DESIGN.md
+// §4).  L = the power of two nearest (in ratio) to target / p trials (fused
+// instructions use their own, smaller target: one kernel item owns a chunk's
+// ca applications), cs = min(L, S) shots, ca = L / cs applications.
+void build_noise_schedule(HostProgram& hp, int tile_shots, int vector_shots, double target_hits,
+                          double fused_target_hits) {
     hp.noise_tab.clear();
-    hp.pregen_ops.clear();
-    hp.pregen_chunks = 0;
-    hp.hit_capacity = 0;
+    hp.noise.assign(hp.num_noise, NoiseParam{});
+    std::map<std::pair<uint32_t, double>, std::pair<uint32_t, uint32_t>> tabs;  // (L, p) -> (offset, len)
+    const uint64_t T = (uint64_t)tile_shots;
     for (int64_t j = 0; j < hp.num_noise; j++) {
         NoiseParam& np = hp.noise[j];
-        const uint32_t npat = np.npat ? np.npat : 1u;
-        np = NoiseParam{};
-        np.npat = npat;
-        const uint64_t N = (uint64_t)hp.noise_apps[j] * (uint64_t)tile_shots;
+        const uint32_t ch = hp.noise_ch[j];
+        np.ch = ch;
+        np.npat = ch == CH_DEP1 ? 3u : (ch == CH_DEP2 ? 15u : 1u);
+        np.apps = hp.noise_apps[j];
+        np.fused = hp.noise_fused[j];
+        const uint64_t N = (uint64_t)np.apps * T;
         const double p = hp.noise_p[j];
-        if (N == 0 || p <= 0.0) { np.flags = NZ_NONE; continue; }
-        if (N >= (1ull << 31)) bad("noise instruction too large for one tile");
-        uint64_t L;
-        if (p >= 1.0) {
-            np.flags = NZ_ALL;
-            L = 1;
+        uint64_t L = 1;
+        if (N == 0 || p <= 0.0) {
+            np.zone = NZONE_NONE;
+        } else if (p >= 1.0) {
+            np.zone = NZONE_ALL;
             while (L < N && L < 1024) L *= 2;  // power of two; positions stay below 2^28
         } else {
-            // power of two nearest (in ratio) to target_hits / p trials
-            double want = target_hits / p;
-            L = 1;
+            np.zone = NZONE_TAB;
+            const double want = (np.fused ? fused_target_hits : target_hits) / p;
             while ((double)(L * 2) <= want * 1.41421356 && L < (1ull << 27)) L *= 2;
             while (L > 1 && L / 2 >= N) L /= 2;  // no chunk longer than needed
         }
+        if (N >= (1ull << 31)) bad("noise instruction too large for one tile");
+        const uint64_t cs = std::min<uint64_t>(L, (uint64_t)vector_shots);
         np.L = (uint32_t)L;
-        np.nchunks = (uint32_t)((N + L - 1) / L);
-        np.last_len = (uint32_t)(N - (uint64_t)(np.nchunks - 1) * L);  // real trials in the last chunk
-        if (!(np.flags & NZ_ALL)) {
-            // every chunk draws from Binomial(L, p): trials past N are virtual and dropped
-            auto tf = binomial_thresholds(L, p);
-            np.tab_full = (uint32_t)hp.noise_tab.size();
-            np.len_full = (uint32_t)tf.size();
-            np.tab_last = np.tab_full;
-            np.len_last = np.len_full;
-            hp.noise_tab.insert(hp.noise_tab.end(), tf.begin(), tf.end());
-        }
-        const double E = (double)N * p;
-        if (p < 0.25 && E <= 16384.0 && N < (1ull << 28)) {
-            np.flags |= NZ_PREGEN;
-            // overflow (Poisson tail beyond ~6 sigma + 10, < 1e-9 per list) falls
-            // back to inline sampling, so the slack only trades memory for speed
-            np.cap = (uint32_t)std::ceil(E + 6.0 * std::sqrt(E) + 10.0);
-            np.cap_base = (uint32_t)hp.hit_capacity;
-            hp.hit_capacity += np.cap;
-            // pre-pass work items are 32-chunk blocks (one warp each)
-            np.chunk_base = (uint32_t)hp.pregen_chunks;
-            hp.pregen_chunks += (np.nchunks + 31) / 32;
-            hp.pregen_ops.push_back((uint32_t)j);
+        np.cs = (uint32_t)cs;
+        np.ca = (uint32_t)(L / cs);
+        const uint64_t nA = (np.apps + (uint64_t)np.ca - 1) / np.ca;
+        const uint64_t nch = nA * (T / cs);
+        if (nch >= (1ull << 31)) bad("noise instruction too large for one tile");
+        np.nchunks = (uint32_t)nch;
+        if (np.zone == NZONE_TAB) {
+            // every chunk draws from Binomial(L, p): trials past the end are virtual and dropped
+            auto key = std::make_pair((uint32_t)L, p);
+            auto it = tabs.find(key);
+            if (it == tabs.end()) {
+                auto tf = binomial_thresholds(L, p);
+                if (tf.size() > 255) bad("noise threshold table too long");
+                it = tabs.emplace(key, std::make_pair((uint32_t)hp.noise_tab.size(), (uint32_t)tf.size())).first;
+                hp.noise_tab.insert(hp.noise_tab.end(), tf.begin(), tf.end());
+            }
+            np.tab = it->second.first;
+            np.len = it->second.second;
         }
     }
-    // noise ops learn their hit-list base and the next pre-generated op, so
-    // consumer threads can prefetch the next op's hits while other ops run
-    std::vector<uint32_t> next_of(hp.num_noise, NO_SLOT);
-    for (size_t k = 0; k + 1 < hp.pregen_ops.size(); k++) next_of[hp.pregen_ops[k]] = hp.pregen_ops[k + 1];
-    hp.first_pregen = hp.pregen_ops.empty() ? NO_SLOT : hp.pregen_ops[0];
-    hp.first_cap_base = hp.pregen_ops.empty() ? 0 : hp.noise[hp.pregen_ops[0]].cap_base;
+    if (hp.noise_tab.size() >= (1u << 24)) bad("noise threshold tables too large");
     for (DOp& o : hp.ops) {
-        if ((o.kcf & 0xFF) != K_NOISE) continue;
-        const NoiseParam& np = hp.noise[o.b];
-        o.kcf &= ~(F_PREGEN << 16);
-        if (np.flags & NZ_PREGEN) o.kcf |= F_PREGEN << 16;
-        o.c = np.cap_base;
-        o.d = next_of[o.b];
-        o.e = o.d != NO_SLOT ? hp.noise[o.d].cap_base : 0u;
+        const uint32_t kind = o.kcf & 0xFF, flags = o.kcf >> 16;
+        if (!(kind == K_NOISE || (flags & F_NOISE))) continue;
+        const NoiseParam& np = hp.noise[o.c];
+        o.d = ilog2(np.L) | (ilog2(np.cs) << 5) | (np.npat << 10) | (np.ch << 14) | (np.zone << 17);
+        o.e = np.tab | (np.len << 24);
     }
-}
-
-// Column-kernel op stream: one self-describing block per device op (header,
-// the NoiseParam of a noise op, then the op's operands), 16-byte aligned so the
-// producer warp can bulk-copy a block into a shared-memory slot in one
-// transaction.  Operands larger than slot_cap stay in global memory
-// (F_GLOBALP); only their header is staged.
-ColStream build_col_stream(const HostProgram& hp, uint32_t slot_cap) {
-    ColStream cs;
-    std::vector<uint32_t> pay;
-    for (const DOp& o : hp.ops) {
-        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF;
-        pay.clear();
-        auto take = [&](const std::vector<uint32_t>& arr, size_t off, size_t n) {
-            pay.insert(pay.end(), arr.begin() + off, arr.begin() + off + n);
-        };
-        switch (kind) {
-            case K_GATE: take(hp.targets, o.off, (size_t)o.count * rule_arity(code)); break;
-            case K_M: case K_MR: take(hp.targets, o.off, 2 * (size_t)o.count); break;
-            case K_R: case K_OBS: take(hp.targets, o.off, o.count); break;
-            case K_NOISE: take(hp.targets, o.off, (size_t)o.count * (code == CH_DEP2 ? 2 : 1)); break;
-            case K_DET:
-                if (code) {
-                    take(hp.det_terms, o.off, (size_t)o.count * code);
-                } else {
-                    const uint32_t base = hp.det_ptr[o.a];
-                    for (uint32_t c = 0; c <= o.count; c++) pay.push_back(hp.det_ptr[o.a + c] - base);
-                    take(hp.det_terms, base, hp.det_ptr[o.a + o.count] - base);
-                }
-                break;
-            default: break;
-        }
-        while (cs.words.size() & 3) cs.words.push_back(0u);
-        const size_t start = cs.words.size();
-        const uint32_t hw = COL_HEAD_WORDS + (kind == K_NOISE ? COL_NP_WORDS : 0u);
-        const bool globalp = ((size_t)hw + pay.size()) * 4 > slot_cap;
-        CHead h{};
-        h.kcf = o.kcf | (globalp ? (F_GLOBALP << 16) : 0u);
-        h.count = o.count;
-        h.a = o.a;
-        h.b = o.b;
-        h.pwords = (uint32_t)pay.size();
-        h.goff = (uint32_t)(start + hw);
-        const uint32_t* hp32 = reinterpret_cast<const uint32_t*>(&h);
-        cs.words.insert(cs.words.end(), hp32, hp32 + COL_HEAD_WORDS);
-        if (kind == K_NOISE) {
-            const uint32_t* np32 = reinterpret_cast<const uint32_t*>(&hp.noise[o.b]);
-            cs.words.insert(cs.words.end(), np32, np32 + COL_NP_WORDS);
-        }
-        cs.words.insert(cs.words.end(), pay.begin(), pay.end());
-        const uint32_t staged = (uint32_t)((((globalp ? hw : hw + pay.size()) * 4) + 15) & ~(size_t)15);
-        if (start / 4 > 0xFFFFFFFFull) bad("op stream too large");
-        cs.binfo.push_back((uint32_t)(start / 4));
-        cs.binfo.push_back(staged);
-        cs.slot_bytes = std::max(cs.slot_bytes, staged);
-    }
-    while (cs.words.size() & 3) cs.words.push_back(0u);
-    cs.n_blocks = (int64_t)hp.ops.size();
-    return cs;
 }
 
 }  // namespace pfs

@@ -3,7 +3,7 @@
 // A CTA owns a tile of 32 shots at a time (the RNG tile of DESIGN.md §4 with
 // W = 1): its warps take the tile's noise chunks, 32 (instruction, chunk) work
 // items per pass, draw each one's hits with the frame sampler's own
-// counter-based schedule (the same draws as noise_chunk / noise_kernel), and
+// counter-based schedule (the same draws as noise_chunk), and
 // XOR every hit's component
 // signatures into one shared-memory word per output column (bit s = shot s).
 // The column words are then transposed in 32x32 blocks and stored as the
@@ -27,9 +27,22 @@ constexpr int DEM_WARPS = 16;
 // ordinal and chunk shuffled in), duplicates / oversize counts are redrawn
 // serially.  Packing chunks of different instructions keeps all lanes busy
 // when an instruction has fewer than 32 chunks per 32-shot tile.
+__device__ __forceinline__ NoiseOp noise_op_of(const NoiseParam& np, uint32_t ordinal) {
+    NoiseOp n;
+    n.ordinal = ordinal;
+    n.lgL = 31u - __clz(np.L);
+    n.lgcs = 31u - __clz(np.cs);
+    n.npat = np.npat;
+    n.ch = np.ch;
+    n.zone = np.zone;
+    n.tab_off = np.tab;
+    n.tab_len = np.len;
+    return n;
+}
+
 template <typename Apply>
 __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2* items, uint32_t n_items,
-                                                 uint32_t first, uint32_t g, uint32_t* wscr, uint32_t* sl,
+                                                 uint32_t first, const TileKey& tk, uint32_t* wscr, uint32_t* sl,
                                                  int lane, Apply apply) {
     const uint32_t it = first + (uint32_t)lane;
     const bool valid = it < n_items;
@@ -37,16 +50,20 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
     const uint32_t o = oc.x, r = oc.y;
     NoiseParam np{};
     if (valid) np = kp.noise[o];
-    const bool all = valid && (np.flags & NZ_ALL);
+    const bool all = valid && np.zone == NZONE_ALL;
     const uint32_t L = valid ? np.L : 1u;
     const uint32_t lg = 31u - __clz(L);
     const uint32_t sh = 32u - lg;
+    // valid positions of chunk r (T = 32 shots, cs = min(L, 32): trial = r L + pos)
+    uint32_t vlen = 0;
+    if (valid) {
+        const uint32_t nS = 32u / np.cs, k = r / nS;
+        vlen = min(np.ca, np.apps - k * np.ca) * np.cs;
+    }
     uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, count = 0;
     if (valid && !all) {
-        noise_block(0u, r, g, o, kp.seed, w0, w1, w2, w3);
-        const unsigned long long uu = ((unsigned long long)w1 << 32) | w0;
-        const unsigned long long* tab = reinterpret_cast<const unsigned long long*>(kp.noise_tab) + np.tab_full;
-        while (count < np.len_full && uu >= __ldg(tab + count)) count++;
+        noise_block(tk, 0u, r, o, w0, w1, w2, w3);
+        count = chunk_count(kp.noise_tab + np.tab, np.len, w0, w1);
     }
     const bool big = count > (uint32_t)NZ_MAX_LIST;
     const uint32_t c = big ? 0u : count;
@@ -79,7 +96,7 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
             const uint32_t h = j - oexcl;
             if (h > 0) {
                 uint32_t b0, b1, b2, b3;
-                noise_block((h + 1) >> 1, orr, g, oo, kp.seed, b0, b1, b2, b3);
+                noise_block(tk, (h + 1) >> 1, orr, oo, b0, b1, b2, b3);
                 x = (h & 1u) ? b0 : b2;
                 y = (h & 1u) ? b1 : b3;
             }
@@ -92,9 +109,10 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
     for (uint32_t h = 1; h < c; h++)
         for (uint32_t q = 0; q < h; q++) dup |= (wscr[excl + h] >> 4) == (wscr[excl + q] >> 4);
     if (dup || big || all) {
-        noise_chunk(kp, np, o, r, g, sl, 1, [&](uint32_t trial, uint32_t pick) { apply(o, trial, pick); });
+        const NoiseOp nz = noise_op_of(np, o);
+        noise_chunk(tk, nz, kp.noise_tab, r, vlen, sl,
+                    [&](uint32_t pos, uint32_t pick) { apply(o, r * L + pos, pick); });
     } else if (c) {
-        const uint32_t vlen = (r + 1 == np.nchunks) ? np.last_len : L;
         for (uint32_t h = 0; h < c; h++) {
             const uint32_t e = wscr[excl + h];
             if ((e >> 4) < vlen) apply(o, r * L + (e >> 4), e & 15u);
@@ -150,7 +168,7 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_con
     const bool shot_major = !GC && dp.b8_out != nullptr && kp.counts == nullptr;
     const int rw = (((ncols + 31) >> 5) + 3) & ~3;  // words per shot row (16-byte multiple)
     for (int64_t tile = blockIdx.x; tile < kp.n_tiles; tile += gridDim.x) {
-        const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
+        const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
         // column words of the tile: shared, or the global output rows at
         // ev_out + col * out_row_stride + tile * out_tile_stride (b8 scratch
         // [tile][col], or the caller's column-major rows)
@@ -161,7 +179,7 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_kernel(const __grid_con
             __syncthreads();
         }
         for (uint32_t first = 32u * warp; first < (uint32_t)dp.n_items; first += 32u * NW) {
-            noise_items_warp(kp, dp.items, (uint32_t)dp.n_items, first, g, wscr, sl, lane,
+            noise_items_warp(kp, dp.items, (uint32_t)dp.n_items, first, tk, wscr, sl, lane,
                              [&](uint32_t o, uint32_t trial, uint32_t pick) {
                 const uint32_t app = trial >> 5, bit = 1u << (trial & 31u);
                 uint32_t xm, zm;
@@ -256,11 +274,11 @@ __global__ void __launch_bounds__(32 * DEM_WARPS, 2) dem_warp_kernel(const __gri
         for (int i = threadIdx.x; i < ncols; i += blockDim.x) cnt[i] = 0u;
     __syncthreads();
     for (int64_t tile = (int64_t)blockIdx.x * NW + warp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * NW) {
-        const uint32_t g = (uint32_t)(kp.tile_offset + (uint64_t)tile);
+        const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
         for (int i = lane; i < ncols; i += 32) ev[i] = 0u;
         __syncwarp();
         for (uint32_t first = 0; first < (uint32_t)dp.n_items; first += 32u) {
-            noise_items_warp(kp, dp.items, (uint32_t)dp.n_items, first, g, wscr, sl, lane,
+            noise_items_warp(kp, dp.items, (uint32_t)dp.n_items, first, tk, wscr, sl, lane,
                              [&](uint32_t o, uint32_t trial, uint32_t pick) {
                 const uint32_t app = trial >> 5, bit = 1u << (trial & 31u);
                 uint32_t xm, zm;

@@ -72,3 +72,39 @@ def gather_shards(local: np.ndarray, group=None, device=None) -> np.ndarray | No
     if rank != 0:
         return None
     return np.concatenate([o.cpu().numpy()[:s] for o, s in zip(outs, sizes)], axis=0)
+
+
+def rank_offset(shots_per_rank: int, world: int, rank: int, tile_shots: int) -> int:
+    """Global shot offset of `rank` under weak scaling (bench.py: every rank
+    samples `shots_per_rank` shots of its own, tile-aligned, disjoint)."""
+    return shard(shots_per_rank, world, rank, tile_shots, weak=True)[0]
+
+
+def reduce_max(value: float, device=None) -> float:
+    """Max of a per-rank scalar (device-timed seconds) over all ranks; the
+    value itself when torch.distributed is not initialised."""
+    import torch
+    import torch.distributed as dist
+
+    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size() == 1:
+        return float(value)
+    t = torch.tensor([float(value)], dtype=torch.float64, device=device)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def counts_steps(sample_counts, counts, shots_per_rank: int, tile_shots: int, world: int, rank: int,
+                 steps: int, seed0: int):
+    """The config-3 step loop of bench.py: `steps` weak-scaled sampling steps of
+    per-column event counts on this rank (`sample_counts(shots, seed, offset,
+    out)` overwrites `counts`, a torch int64 tensor), then one in-place sum
+    over ranks (NCCL for CUDA tensors, gloo for CPU ones).  Returns `counts`:
+    the last step's counts summed over all ranks."""
+    import torch.distributed as dist
+
+    off = rank_offset(shots_per_rank, world, rank, tile_shots)
+    for i in range(steps):
+        sample_counts(shots_per_rank, seed0 + i, off, counts)
+    if world > 1:
+        dist.all_reduce(counts, op=dist.ReduceOp.SUM)
+    return counts

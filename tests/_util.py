@@ -64,3 +64,50 @@ def five_sigma(count_a, n_a, count_b, n_b, sigmas=5.0):
 def pair_counts(bits: np.ndarray, pairs: np.ndarray) -> np.ndarray:
     b = bits.astype(np.int64)
     return (b[:, pairs[:, 0]] & b[:, pairs[:, 1]]).sum(axis=0)
+
+
+# ---------------------------------------------------------------- RNG layout
+def rule_chunk_length(p: float, apps: int, tile_shots: int, target: float) -> int:
+    """the power of two nearest (in ratio) to target / p trials,
+    halved while half of it still covers the instruction's trials (p == 1:
+    up to 1024, p == 0: 1)."""
+    N = apps * tile_shots
+    L = 1
+    if N == 0 or p <= 0.0:
+        return L
+    if p >= 1.0:
+        while L < N and L < 1024:
+            L *= 2
+        return L
+    want = target / p
+    while L * 2 <= want * 1.41421356 and L < (1 << 27):
+        L *= 2
+    while L > 1 and L // 2 >= N:
+        L //= 2
+    return L
+
+
+def rule_chunk_lengths(prog, tile_shots: int, target: float = 2.0) -> np.ndarray:
+    """Chunk length of every noise instruction of a FlatProgram by the rule."""
+    out = np.ones(prog.num_noise, dtype=np.uint32)
+    for row in prog.instrs:
+        if row[0] == 4:  # K_NOISE
+            ar = 2 if row[1] == 4 else 1
+            out[row[7]] = rule_chunk_length(float(prog.noise_p[row[7]]), int(row[2]) // ar, tile_shots, target)
+    return out
+
+
+def product_layout(sampler):
+    """(T, S, chunk_L): the RNG layout a compiled sampler draws with."""
+    params, _ = sampler.native.noise_schedule()
+    T = sampler.tile_shots
+    S = 32 if sampler.native.info["kernel"] == 4 else 32 * min(T // 32, 4)
+    return T, S, params[:, 0].copy()
+
+
+def oracle_run(oracle, sampler, shots: int, seed: int, shot_offset: int = 0, **kw):
+    """The oracle's draws with the sampler's layout: (flip rows, event rows)."""
+    T, S, L = product_layout(sampler)
+    assert shot_offset % T == 0
+    return oracle.sample(sampler.flat, shots, T, seed=seed, tile_offset=shot_offset // T, chunk_L=L,
+                         vector_shots=S, **kw)

@@ -277,9 +277,13 @@ def _stat_worker(args):
     _, rcircuit, frame_sim, _, io_formats, _, _ = _ref()
     rc = rcircuit.parse(mc.to_reference_dialect(text))
     fl = frame_sim.collect_flips(rc, shots, np.random.default_rng(seed), B)
-    ev = io_formats.detector_events(fl, rcircuit.detector_sets(rc)).to_numpy().astype(np.int64)
-    counts = ev.sum(axis=0)
-    pc = (ev[:, pairs[:, 0]] & ev[:, pairs[:, 1]]).sum(axis=0)
+    ev = io_formats.detector_events(fl, rcircuit.detector_sets(rc)).to_numpy().astype(np.uint8)
+    del fl
+    counts = ev.sum(axis=0, dtype=np.int64)
+    pc = np.zeros(len(pairs), dtype=np.int64)
+    for i in range(0, len(pairs), 1024):  # bounded temporaries (d=25: 16k columns)
+        pp = pairs[i:i + 1024]
+        pc[i:i + 1024] = (ev[:, pp[:, 0]] & ev[:, pp[:, 1]]).sum(axis=0, dtype=np.int64)
     return counts, pc
 
 
@@ -313,7 +317,7 @@ def gen_stats(procs: int, only=None):
         ("d3", gen.surface_code_memory(3, 3, 1e-2), 1 << 16, 1024, 8),
         ("d5", gen.surface_code_memory(5, 5, 5e-3), 1 << 16, 4096, 24),
         ("c1", gen.random_clifford(64, 200, 0.01, 0), 1 << 15, 1024, 6),
-        ("d25", gen.surface_code_memory(25, 25, 1e-3), 1 << 16, 8192, 624),
+        ("d25", gen.surface_code_memory(25, 25, 1e-3), 1 << 20, 8192, 624),
     ]
     for name, text, shots, B, per_round in cases:
         if only and name not in only:
@@ -322,17 +326,19 @@ def gen_stats(procs: int, only=None):
         c = mc.parse(text)
         nd = len(mc.detector_and_observable_sets(c))
         pairs = make_pairs(nd, per_round, 3)
-        per = shots // procs
-        jobs = [(text, per, 1000 + i, B, pairs) for i in range(procs)]
+        # shards of at most 8192 shots keep each worker's event matrix small
+        n_jobs = max(procs, shots // 8192)
+        per = shots // n_jobs
+        jobs = [(text, per, 1000 + i, B, pairs) for i in range(n_jobs)]
         from concurrent.futures import ThreadPoolExecutor
         with ThreadPoolExecutor(procs) as pool:
             res = list(pool.map(_stat_subprocess, jobs))
         counts = sum(r[0] for r in res)
         pc = sum(r[1] for r in res)
         np.savez_compressed(os.path.join(HERE, f"stats_{name}.npz"), text=np.array(text),
-                            shots=per * procs, counts=counts, pairs=pairs, pair_counts=pc)
-        print(f"stats {name}: shots={per * procs} det={nd} mean rate="
-              f"{counts.mean() / (per * procs):.4g} {time.time() - t0:.1f}s", flush=True)
+                            shots=per * n_jobs, counts=counts, pairs=pairs, pair_counts=pc)
+        print(f"stats {name}: shots={per * n_jobs} det={nd} mean rate="
+              f"{counts.mean() / (per * n_jobs):.4g} {time.time() - t0:.1f}s", flush=True)
 
 
 TINY = [

@@ -29,7 +29,7 @@ def test_exports_match_header():
     L = ctypes.CDLL(N.LIB_PATH)
     for name in declared:
         assert hasattr(L, name), name
-    assert N.lib().pfs_version() == 1
+    assert N.lib().pfs_version() == 2
 
 
 @pytest.mark.parametrize("cfg", [0, 1, 3])
@@ -45,32 +45,29 @@ def test_program_info_matches_survey_counts(cfg):
     assert params.shape == (f.num_noise, 12)
     # every table is non-decreasing (inverse-CDF thresholds)
     for row in params:
-        for off, ln in ((row[3], row[4]), (row[5], row[6])):
-            t = tab[off:off + ln]
-            assert np.all(t[1:] >= t[:-1])
+        t = tab[row[5]:row[5] + row[6]]
+        assert np.all(t[1:] >= t[:-1])
 
 
 def test_d25_layout():
     f = flatten(gen.surface_code_memory(25, 25, 1e-3))
     p = N.NativeProgram(f)
-    assert p.info["bframe_bits"] == 518500
-    assert p.info["smem_bytes"] <= 227 * 1024
-    assert p.info["kernel"] == 1 and p.info["words_per_tile"] == 8
-    # word-column kernel (one 32-shot word per warp, tile = 1 word)
-    pc = N.NativeProgram(f, kernel=3)
-    assert pc.info["kernel"] == 3 and pc.info["words_per_tile"] in (1, 2, 4)
-    assert pc.info["warps_per_cta"] >= 8 and pc.info["threads"] == 32 * (pc.info["warps_per_cta"] + 1)
-    # warp-private kernel (opt-in): one 32-shot word column per warp, 8-word tiles
-    pw = N.NativeProgram(f, kernel=2)
-    assert pw.info["kernel"] == 2 and pw.info["words_per_tile"] == 8
-    assert pw.info["warps_per_cta"] >= 12 and pw.info["threads"] == 32 * pw.info["warps_per_cta"]
+    info = p.info
+    assert info["bframe_bits"] == 518500
+    assert info["smem_bytes"] <= 227 * 1024
+    assert info["kernel"] == 1 and info["words_per_tile"] == 8 and info["groups"] == 2
+    # every noise instruction rides inside its gate / collapse op; records stay
+    # in x rows until the next reset spills them to the shared-memory ring
+    assert info["fused_noise"] == f.num_noise and info["ring_in_smem"] == 1
+    assert info["num_slots"] == 625  # one per measure qubit + the observable
+    assert info["live_coin_rows"] == 0  # no coin reaches a detector of a Z memory
+    assert info["num_ops"] < 250
     for W in (1, 2, 4, 8, 16):
         q = N.NativeProgram(f, words_per_tile=W, ring_in_smem=0, kernel=1)
         assert q.info["kernel"] == 1
         assert q.info["tile_shots"] == 32 * W and q.info["ring_in_smem"] == 0
-    # d=100: a word column (20k qubits) exceeds shared memory -> cooperative kernel
     big = N.NativeProgram(flatten(gen.surface_code_memory(100, 2, 1e-3)))
-    assert big.info["kernel"] == 1 and big.info["warps_per_cta"] == 0
+    assert big.info["kernel"] == 1 and big.info["words_per_tile"] == 1 and big.info["ring_in_smem"] == 1
 
 
 def test_binomial_thresholds_match_scipy():
@@ -80,20 +77,58 @@ def test_binomial_thresholds_match_scipy():
     f = flatten("X_ERROR(0.001) " + " ".join(map(str, range(64))) + "\n")
     p = N.NativeProgram(f, words_per_tile=8, ring_in_smem=0)
     params, tab = p.noise_schedule()
-    L, nch, last, tf, lf = (int(v) for v in params[0, :5])
-    assert L * (nch - 1) + last == 64 * 256
+    L, cs, ca, nch, apps, tf, lf = (int(v) for v in params[0, :7])
+    assert cs == min(L, 128) and ca == L // cs and nch == -(-apps // ca) * (256 // cs) and apps == 64
     cdf = binom.cdf(np.arange(lf), L, 0.001)
     got = tab[tf:tf + lf].astype(np.float64) / 2.0 ** 64
     assert np.allclose(got, cdf, rtol=1e-9, atol=1e-15)
+
+
+@pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
+def test_noise_schedule_matches_oracle_restatement(oracle_lib, cfg):
+    """The product's chunk lengths follow the rule of DESIGN.md §4 (target 0.5
+    hits for fused instructions, 2 otherwise); its geometry and Binomial tables
+    equal the oracle's own (oracle/pfs_oracle.c computes them independently)."""
+    from tests._util import rule_chunk_length
+
+    f = flatten(gen.config_circuit(cfg))
+    p = N.NativeProgram(f)
+    params, tab = p.noise_schedule()
+    params = params.astype(np.int64)
+    T = p.tile_shots
+    S = 32 * min(T // 32, 4)
+    for row in f.instrs:
+        if row[0] != 4:
+            continue
+        o = int(row[7])
+        ar = 2 if row[1] == 4 else 1
+        apps = int(row[2]) // ar
+        mine = params[o]
+        assert mine[0] == rule_chunk_length(float(f.noise_p[o]), apps, T, 0.5 if mine[10] else 2.0)
+        ref, rtab = oracle_lib.noise_schedule_one(apps, int(row[1]), float(f.noise_p[o]), int(mine[0]), T, S)
+        assert list(mine[[0, 1, 2, 3, 4, 6, 7, 8, 9]]) == list(ref[[0, 1, 2, 3, 4, 6, 7, 8, 9]])
+        assert np.array_equal(tab[mine[5]:mine[5] + mine[6]], rtab)
 
 
 def test_conflicting_instruction_is_split():
     # CX 0 1 1 2 must stay two sequential steps (frame_sim.py:61-62)
     f = flatten("CX 0 1 1 2\nM 0 1 2\n")
     p = N.NativeProgram(f)
-    assert p.info["num_ops"] == 3
+    assert p.info["record_ops"] == 3
+    assert p.info["num_ops"] == 2  # no detector reads the records: the event program drops M
     f2 = flatten("CX 0 1 2 3\nCX 4 5\nM 0 1 2 3 4 5\n")
-    assert N.NativeProgram(f2).info["num_ops"] == 2  # merged CX, one M
+    assert N.NativeProgram(f2).info["record_ops"] == 2  # merged CX, one M
+
+
+def test_records_stay_in_x_rows_until_rewritten():
+    # the M records live in x rows; R spills the one a later detector needs;
+    # H rewrites x, so its record is spilled by a SPILL op before it
+    f = flatten("R 0 1\nH 0\nCX 0 1\nM 0 1\nR 0\nH 1\nM 0 1\nDETECTOR rec[-2] rec[-4]\nDETECTOR rec[-1] rec[-3]\n")
+    p = N.NativeProgram(f)
+    assert p.info["num_slots"] == 2
+    ops = p.ops()
+    kinds = [int(k & 0xFF) for k in ops[:, 0]]
+    assert 7 in kinds  # K_SPILL before the H on qubit 1
 
 
 def test_errors_are_value_errors():

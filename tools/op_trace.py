@@ -38,7 +38,7 @@ def main():
     ops = ds.native.ops()
     dt = np.diff(clk)
     work = ends[:, :-1] - clk[None, :-1]  # per warp: op start (barrier exit) -> own work done
-    names = {0: "GATE", 1: "M", 2: "R", 3: "MR", 4: "NOISE", 5: "DET", 6: "OBS"}
+    names = {0: "GATE", 1: "M", 2: "R", 3: "MR", 4: "NOISE", 5: "DET", 6: "OBS", 7: "SPILL"}
     agg = collections.defaultdict(lambda: [0, 0])
     for i, d in enumerate(dt):
         k = int(ops[i, 0] & 0xFF)

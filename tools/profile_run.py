@@ -19,7 +19,7 @@ def main():
     ap.add_argument("--mode", default="b8")
     ap.add_argument("--reps", type=int, default=2)
     ap.add_argument("--debug-skip", type=int, default=0)
-    ap.add_argument("--producers", type=int, default=0)
+    ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0)
     a = ap.parse_args()
     import torch
@@ -29,8 +29,7 @@ def main():
 
     ds = compile_detector_sampler(gen.config_circuit(a.config), words_per_tile=a.words,
                                   ring_in_smem=a.ring, threads=a.threads,
-                                  debug_skip=a.debug_skip, producer_threads=a.producers,
-                                  kernel=a.kernel)
+                                  debug_skip=a.debug_skip, groups=a.groups, kernel=a.kernel)
     nb = (ds.num_columns + 7) // 8
     pitch = (nb + 31) // 32 * 32
     if a.mode == "b8":
