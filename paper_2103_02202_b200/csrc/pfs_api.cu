@@ -110,15 +110,16 @@ constexpr int kPipeChunks = 6;
 constexpr int kPipeFrameThreads = FRAME_MAX_THREADS;
 constexpr int DEM_WARPS_HOST = 16;  // dem_kernel's warps (DEM_WARPS)
 constexpr double kStandaloneHits = 2.0;  // mean hits per noise chunk (standalone / error-model)
-constexpr double kFusedHits = 0.5;       // mean hits per fused noise chunk (one kernel item)
+constexpr double kFusedHits = 1.0;       // mean hits per fused noise chunk (one kernel item)
 
 static bool desc_fits(const HostProgram& hp) {
     return hp.ops.size() * sizeof(DOp) + hp.noise_tab.size() * 8 <= (size_t)DESC_SMEM_MAX;
 }
 
-// descriptors + threshold tables (when they fit), alignment slack
+// per-warp noise scratch, descriptors + threshold tables (when they fit), alignment slack
 static size_t fixed_smem(const HostProgram& hp) {
-    return 16 + (desc_fits(hp) ? hp.ops.size() * sizeof(DOp) + hp.noise_tab.size() * 8 : 0);
+    return 16 + (size_t)(FRAME_MAX_THREADS / 32) * WSCR * 4 +
+           (desc_fits(hp) ? hp.ops.size() * sizeof(DOp) + hp.noise_tab.size() * 8 : 0);
 }
 
 // Outputs of the kernels that write final layouts directly (dem_kernel).
@@ -283,6 +284,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
             dedup_operands(hp);
             // the error-model kernel's chunks span whole 32-shot tiles
             build_noise_schedule(hp, 32 * W, dem ? 32 : 32 * V, th, dem ? th : thf);
+            if (!dem) bank_order_fused(hp, W, cfg.threads / std::max(1, cfg.groups) / 32);
             Flavour& f = pg->fl[m];
             if (m == PM_RECORDS) f.cfg = cfg, f.cfg.ring_smem = true;
             f.desc_smem = desc_fits(hp);

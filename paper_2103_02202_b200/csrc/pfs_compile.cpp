@@ -644,59 +644,101 @@ void permute_rows(HostProgram& hp) {
     for (uint32_t& t : hp.det_terms) map_term(t);
 }
 
-// Reorder the applications of every unfused gate op so each aligned group of
-// G consecutive applications (the apps one shared-memory wavefront serves: G =
-// 128 B / row bytes) touches G distinct bank groups per operand: apps are
-// classed by (first, second) operand residue mod G and each group takes one
-// app per first residue, choosing among the second residues still unused the
-// fullest class.  Apps of one op are independent by construction, so any
-// order is the same circuit.  (A fused op keeps its noise instruction's
-// application order: it defines the noise trials.)
+// Bank-aware order of A applications (ar targets each) in place: each
+// aligned group of G consecutive applications (the apps one shared-memory
+// wavefront serves: G = 128 B / row bytes) touches G distinct bank groups per
+// operand: apps are classed by (first, second) operand residue mod G and each
+// group takes one app per first residue, choosing among the second residues
+// still unused the fullest class.
+static void bank_reorder(uint32_t* tg, uint32_t A, int ar, int G, std::vector<uint32_t>& scratch) {
+    if (G <= 1 || A < 2) return;
+    const int G2 = ar == 2 ? G : 1;
+    std::vector<std::vector<uint32_t>> cls((size_t)G * G2);
+    std::vector<uint32_t> rem0(G, 0);
+    for (uint32_t a = 0; a < A; a++) {
+        const uint32_t r0 = tg[a * ar] % G, r1 = ar == 2 ? tg[a * ar + 1] % G : 0;
+        cls[(size_t)r0 * G2 + r1].push_back(a);
+        rem0[r0]++;
+    }
+    scratch.clear();
+    scratch.reserve((size_t)A * ar);
+    uint32_t left = A;
+    std::vector<char> used1(G2);
+    std::vector<int> order(G);
+    while (left) {
+        std::fill(used1.begin(), used1.end(), 0);
+        // fullest first residues first: they are the ones that run out last
+        for (int r = 0; r < G; r++) order[r] = r;
+        std::sort(order.begin(), order.end(), [&](int x, int y) { return rem0[x] > rem0[y]; });
+        for (int r0 : order) {
+            if (!rem0[r0] || !left) continue;
+            int best = -1;
+            for (int r1 = 0; r1 < G2; r1++) {
+                const size_t c = cls[(size_t)r0 * G2 + r1].size();
+                if (!c) continue;
+                if (best < 0 || (!used1[r1] && (used1[best] || c > cls[(size_t)r0 * G2 + best].size()))) best = r1;
+            }
+            auto& v = cls[(size_t)r0 * G2 + best];
+            const uint32_t a = v.back();
+            v.pop_back();
+            rem0[r0]--;
+            used1[best] = 1;
+            for (int s2 = 0; s2 < ar; s2++) scratch.push_back(tg[a * ar + s2]);
+            left--;
+        }
+    }
+    std::copy(scratch.begin(), scratch.end(), tg);
+}
+
+static int bank_groups(int W) { return W >= 32 ? 1 : 128 / (W * 4); }
+
+// Reorder the applications of every unfused gate op for distinct bank groups
+// (apps of one op are independent by construction, so any order is the same
+// circuit).  A fused op keeps its noise instruction's application order — it
+// defines the noise trials; see bank_order_fused.
 void reorder_for_banks(HostProgram& hp, int W) {
-    const int G = W >= 32 ? 1 : 128 / (W * 4);
+    const int G = bank_groups(W);
     if (G <= 1) return;
     std::vector<uint32_t> scratch;
     for (DOp& o : hp.ops) {
         if ((o.kcf & 0xFF) != K_GATE || o.count < 2 || ((o.kcf >> 16) & F_NOISE)) continue;
+        bank_reorder(hp.targets.data() + o.off, o.count, rule_arity((o.kcf >> 8) & 0xFF), G, scratch);
+    }
+}
+
+// Fused gate ops: the kernel gives each warp of a group a chunk-aligned range
+// of K applications (noise chunks of ca applications); the
+// warp's gate work may visit its range in any order, so a bank-ordered copy of
+// each range's targets is appended (op.a = its offset, op.b = K) while the
+// noise draws keep addressing the instruction order at op.off.
+void bank_order_fused(HostProgram& hp, int W, int warps_per_group) {
+    const int G = bank_groups(W);
+    const uint32_t nw = (uint32_t)std::max(1, warps_per_group);
+    std::vector<uint32_t> scratch, copy;
+    std::unordered_map<uint64_t, std::vector<uint32_t>> seen;
+    for (DOp& o : hp.ops) {
+        if ((o.kcf & 0xFF) != K_GATE || !((o.kcf >> 16) & F_NOISE)) continue;
         const int ar = rule_arity((o.kcf >> 8) & 0xFF);
-        const uint32_t A = o.count;
-        uint32_t* tg = hp.targets.data() + o.off;
-        const int G2 = ar == 2 ? G : 1;
-        std::vector<std::vector<uint32_t>> cls((size_t)G * G2);
-        std::vector<uint32_t> rem0(G, 0);
-        for (uint32_t a = 0; a < A; a++) {
-            const uint32_t r0 = tg[a * ar] % G, r1 = ar == 2 ? tg[a * ar + 1] % G : 0;
-            cls[(size_t)r0 * G2 + r1].push_back(a);
-            rem0[r0]++;
+        const uint32_t ca = std::max<uint32_t>(1u, hp.noise[o.c].ca);
+        const uint32_t K = ((o.count + nw - 1) / nw + ca - 1) / ca * ca;
+        copy.assign(hp.targets.begin() + o.off, hp.targets.begin() + o.off + (size_t)o.count * ar);
+        for (uint32_t a0 = 0; a0 < o.count; a0 += K)
+            bank_reorder(copy.data() + (size_t)a0 * ar, std::min(K, o.count - a0), ar, G, scratch);
+        // rounds of a REPEAT body produce identical copies: share them
+        uint64_t h = 1469598103934665603ull ^ copy.size();
+        for (uint32_t v : copy) { h ^= v; h *= 1099511628211ull; }
+        auto& lst = seen[h];
+        uint32_t where = NO_SLOT;
+        for (uint32_t cand : lst)
+            if (std::equal(copy.begin(), copy.end(), hp.targets.begin() + cand)) { where = cand; break; }
+        if (where == NO_SLOT) {
+            if (hp.targets.size() & 1) hp.targets.push_back(0u);
+            where = (uint32_t)hp.targets.size();
+            hp.targets.insert(hp.targets.end(), copy.begin(), copy.end());
+            lst.push_back(where);
         }
-        scratch.clear();
-        scratch.reserve((size_t)A * ar);
-        uint32_t left = A;
-        std::vector<char> used1(G2);
-        std::vector<int> order(G);
-        while (left) {
-            std::fill(used1.begin(), used1.end(), 0);
-            // fullest first residues first: they are the ones that run out last
-            for (int r = 0; r < G; r++) order[r] = r;
-            std::sort(order.begin(), order.end(), [&](int x, int y) { return rem0[x] > rem0[y]; });
-            for (int r0 : order) {
-                if (!rem0[r0] || !left) continue;
-                int best = -1;
-                for (int r1 = 0; r1 < G2; r1++) {
-                    const size_t c = cls[(size_t)r0 * G2 + r1].size();
-                    if (!c) continue;
-                    if (best < 0 || (!used1[r1] && (used1[best] || c > cls[(size_t)r0 * G2 + best].size()))) best = r1;
-                }
-                auto& v = cls[(size_t)r0 * G2 + best];
-                const uint32_t a = v.back();
-                v.pop_back();
-                rem0[r0]--;
-                used1[best] = 1;
-                for (int s2 = 0; s2 < ar; s2++) scratch.push_back(tg[a * ar + s2]);
-                left--;
-            }
-        }
-        std::copy(scratch.begin(), scratch.end(), tg);
+        o.a = where;
+        o.b = K;
     }
 }
 

@@ -33,6 +33,7 @@ constexpr uint32_t NZONE_TAB = 0u;   // Binomial(L, p) count by table inversion
 constexpr uint32_t NZONE_NONE = 1u;  // p == 0: no hits
 constexpr uint32_t NZONE_ALL = 2u;   // p == 1: every trial hits
 constexpr int NZ_MAX_LIST = 16;      // distinct-position list; larger counts use selection sampling
+constexpr int WSCR = 64;             // per-warp shared scratch of the warp-cooperative noise draws (words)
 // frame kernel CTA size cap (launch bounds): 512 threads leave 128 registers per
 // thread — the fused gate + noise items need ~124 without spilling
 #ifndef PFS_FRAME_MAX_THREADS
@@ -50,7 +51,8 @@ constexpr int DESC_SMEM_MAX = 24576;
 enum ProgMode : int { PM_EVENTS = 0, PM_RECORDS = 1 };
 
 // One device op (32 bytes).  See DESIGN.md §3.
-//   GATE : count = apps, off -> targets (1 or 2 per app)
+//   GATE : count = apps, off -> targets (1 or 2 per app); fused: a -> the
+//          targets again, bank-ordered within each warp range of b applications
 //   R    : count = targets, off -> (row, spill slot) pairs, b = first coin row
 //   M/MR : count = targets, off -> (row, record slot) pairs, a = first record,
 //          b = first coin row (MR: two per target, the second is the reset's)
@@ -136,6 +138,7 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, int vector_shots, dou
                           double fused_target_hits);
 void permute_rows(HostProgram& hp);
 void reorder_for_banks(HostProgram& hp, int W);
+void bank_order_fused(HostProgram& hp, int W, int warps_per_group);
 void dedup_operands(HostProgram& hp);
 
 // Kernel launch plumbing (pfs_kernels.cu)

@@ -191,8 +191,8 @@ __device__ __noinline__ void chunk_hits_slow(const TileKey tk, const NoiseOp nz,
     });
 }
 
-// The noise of one chunk into the frame: one Philox block in the common
-// case (at most two hits, distinct), else the general path
+// The noise of one chunk into the frame, one thread: one Philox block in the
+// common case (at most two hits, distinct), else the general path
 template <int W, bool ATOMIC>
 __device__ __forceinline__ void chunk_hits(const TileKey& tk, const NoiseOp& nz, const unsigned long long* tab,
                                            uint32_t r, uint32_t a0, uint32_t na, uint32_t s0, const uint32_t* tg,
@@ -212,20 +212,110 @@ __device__ __forceinline__ void chunk_hits(const TileKey& tk, const NoiseOp& nz,
                              s0 + ((h1 >> 4) & msk));
 }
 
-// The fused noise of item (application chunk k, vector c): applications
-// [a0, a0 + na), the vector's S shots (one chunk when cs = S, else S / cs
-// chunks of one application).  The item's thread owns these rows in this op:
-// plain read-modify-write.  Injected mode: each application's mask rows.
+// Warp-cooperative noise: lane l draws one chunk r (valid lanes) — block 0
+// gives the Binomial count and the first position pair — the warp compacts the
+// hits (prefix sum), each lane resolves one hit per round (extra Philox blocks
+// for hits h >= 1) into the warp scratch, then each lane XORs one
+// hit into the frame (shared-memory atomics: hits of a chunk may share a word).
+// Chunks whose positions collide, counts above NZ_MAX_LIST, p == 1, or a warp
+// total above WSCR take the general path, lane by lane.  The chunk covers
+// applications [a0, a0 + na) and shots [s0, s0 + cs).  Every lane of the warp
+// must call this (shuffles).
 template <int W>
-__device__ __forceinline__ void item_noise(const KParams& kp, const TileKey& tk, const NoiseOp& nz,
-                                           const unsigned long long* tab, uint32_t k, int c, uint32_t a0,
-                                           uint32_t na, const uint32_t* tg, int ar, bool pairs, uint32_t* X,
-                                           uint32_t* Z, uint32_t* sl, uint32_t rowb, int64_t tile) {
+__device__ __forceinline__ void warp_chunks(const TileKey& tk, const NoiseOp& nz, const unsigned long long* tab,
+                                            bool valid, uint32_t r, uint32_t a0, uint32_t na, uint32_t s0,
+                                            const uint32_t* tg, int ar, bool pairs, uint32_t* X, uint32_t* Z,
+                                            uint32_t* sl, uint32_t* wscr, int lane) {
+    if (nz.zone == NZONE_NONE) return;
+    const uint32_t sh = 32u - nz.lgL, msk = (1u << nz.lgcs) - 1;
+    uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, count = 0;
+    if (valid && nz.zone == NZONE_TAB) {
+        noise_block(tk, 0u, r, nz.ordinal, w0, w1, w2, w3);
+        count = chunk_count(tab + nz.tab_off, nz.tab_len, w0, w1);
+    }
+    bool slow = valid && (nz.zone == NZONE_ALL || count > (uint32_t)NZ_MAX_LIST);
+    uint32_t c = slow ? 0u : count;
+    uint32_t pre = c;  // inclusive prefix of the warp's hit counts
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+        if (lane >= d) pre += v;
+    }
+    uint32_t H = __shfl_sync(0xFFFFFFFFu, pre, 31);
+    if (H > (uint32_t)WSCR) {  // rare: too many hits for the scratch
+        slow |= c > 0;
+        c = 0;
+        pre = 0;
+        H = 0;
+    }
+    const uint32_t excl = pre - c;
+    auto owner_of = [&](uint32_t j) {  // smallest lane q with pre[q] > j
+        uint32_t lo = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+            const uint32_t pv = __shfl_sync(0xFFFFFFFFu, pre, (int)(lo + st - 1));
+            if (pv <= j) lo += st;
+        }
+        return (int)(lo > 31u ? 31u : lo);
+    };
+    for (uint32_t j0 = 0; j0 < H; j0 += 32) {
+        const uint32_t j = j0 + (uint32_t)lane;
+        const int ow = owner_of(j);
+        const uint32_t oexcl = __shfl_sync(0xFFFFFFFFu, excl, ow);
+        const uint32_t orr = __shfl_sync(0xFFFFFFFFu, r, ow);
+        uint32_t x = __shfl_sync(0xFFFFFFFFu, w2, ow);
+        uint32_t y = __shfl_sync(0xFFFFFFFFu, w3, ow);
+        if (j < H) {
+            const uint32_t h = j - oexcl;
+            if (h > 0) {
+                uint32_t b0, b1, b2, b3;
+                noise_block(tk, (h + 1) >> 1, orr, nz.ordinal, b0, b1, b2, b3);
+                x = (h & 1u) ? b0 : b2;
+                y = (h & 1u) ? b1 : b3;
+            }
+            wscr[j] = ((nz.lgL ? (x >> sh) : 0u) << 4) | (nz.npat > 1 ? __umulhi(y, nz.npat) : 0u);
+        }
+    }
+    __syncwarp();
+    for (uint32_t h = 1; h < c; h++)  // positions of one chunk must be distinct
+        for (uint32_t q = 0; q < h; q++) slow |= (wscr[excl + h] >> 4) == (wscr[excl + q] >> 4);
+    const uint32_t slowm = __ballot_sync(0xFFFFFFFFu, slow);
+    for (uint32_t j0 = 0; j0 < H; j0 += 32) {
+        const uint32_t j = j0 + (uint32_t)lane;
+        const int ow = owner_of(j);
+        const uint32_t oa0 = __shfl_sync(0xFFFFFFFFu, a0, ow);
+        const uint32_t os0 = __shfl_sync(0xFFFFFFFFu, s0, ow);
+        const uint32_t ovl = __shfl_sync(0xFFFFFFFFu, na, ow) << nz.lgcs;
+        if (j < H && !((slowm >> ow) & 1u)) {
+            const uint32_t e = wscr[j], pos = e >> 4;
+            if (pos < ovl)
+                xor_pauli<W, true>(X, Z, app_rows(tg, oa0 + (pos >> nz.lgcs), ar, pairs), ar, nz.ch, e & 15u,
+                                   os0 + (pos & msk));
+        }
+    }
+    if (slow) chunk_hits_slow<W, true>(tk, nz, tab, r, a0, na, s0, tg, ar, pairs, X, Z, sl);
+    __syncwarp();  // the scratch is reused by the next call
+}
+
+// Fused noise of the applications [A0, A1) a warp owns in this op (A0 a
+// multiple of ca): every chunk (k, vector c, sub-chunk u) of those
+// applications, 32 per warp-cooperative pass.  Injected mode: each
+// application's mask rows.  Every lane must call this.
+template <int W>
+__device__ __forceinline__ void warp_range_noise(const KParams& kp, const TileKey& tk, const NoiseOp& nz,
+                                                 const unsigned long long* tab, uint32_t count, uint32_t A0,
+                                                 uint32_t A1, const uint32_t* tg, int ar, bool pairs, uint32_t* X,
+                                                 uint32_t* Z, uint32_t* sl, uint32_t* wscr, int lane, uint32_t rowb,
+                                                 int64_t tile) {
     constexpr int V = W >= 4 ? 4 : W;
+    constexpr int C = W / V;
+    constexpr int LC = Log2<C>::v;
     constexpr uint32_t S = 32u * V;
+    __syncwarp();  // the warp's row updates are visible to the lanes applying hits
     if (kp.masks != nullptr) {
-        for (uint32_t j = 0; j < na; j++) {
-            const uint32_t app = a0 + j;
+        for (uint32_t j = (uint32_t)lane; j < ((A1 - A0) << LC); j += 32) {
+            const uint32_t app = A0 + (j >> LC);
+            const int c = (int)(j & (C - 1));
             const AppRows rr = app_rows(tg, app, ar, pairs);
             for (int sl2 = 0; sl2 < ar; sl2++) {
                 const uint32_t* m = kp.masks + (int64_t)(rowb + 2u * (app * ar + sl2)) * kp.inject_words + tile * W + c * V;
@@ -234,14 +324,40 @@ __device__ __forceinline__ void item_noise(const KParams& kp, const TileKey& tk,
                 vst<V>(Z + p, vxor<V>(vld<V>(Z + p), vldg<V>(m + kp.inject_words)));
             }
         }
+        __syncwarp();
         return;
     }
+#if PFS_PROFILE
+    if (kp.debug_skip & 2) return;  // profiling ablation: no noise draws (wrong results)
+#endif
     if (nz.zone == NZONE_NONE) return;
+    const uint32_t lgca = nz.lgL - nz.lgcs;
     const uint32_t cs = 1u << nz.lgcs;
     const uint32_t nS = (32u * W) >> nz.lgcs;
-    const uint32_t m = cs >= S ? 1u : S / cs;
-    for (uint32_t u = 0; u < m; u++)
-        chunk_hits<W, false>(tk, nz, tab, k * nS + c * m + u, a0, na, c * S + u * cs, tg, ar, pairs, X, Z, sl);
+    const uint32_t m = cs >= S ? 1u : S / cs;      // chunks per vector
+    const uint32_t per_k = (uint32_t)C * m;         // chunks per application block
+    const uint32_t k0 = A0 >> lgca;
+    const uint32_t nch = ((A1 - A0 + (1u << lgca) - 1) >> lgca) * per_k;
+    for (uint32_t q0 = 0; q0 < nch; q0 += 32) {
+        const uint32_t q = q0 + (uint32_t)lane;
+        const bool valid = q < nch;
+        const uint32_t k = k0 + q / per_k, rem = q % per_k;
+        const uint32_t c = rem / m, u = rem - c * m;
+        const uint32_t a0 = k << lgca;
+        warp_chunks<W>(tk, nz, tab, valid, k * nS + c * m + u, a0, valid ? min(1u << lgca, count - a0) : 0u,
+                       c * S + u * cs, tg, ar, pairs, X, Z, sl, wscr, lane);
+    }
+}
+
+// The application range of a warp in a fused op: ceil(count / warps), rounded
+// up to whole noise chunks (ca applications), so each chunk has one owner warp
+__device__ __forceinline__ void warp_range(uint32_t count, uint32_t lgca, int tid, int nth, uint32_t& A0,
+                                           uint32_t& A1) {
+    const uint32_t nw = (uint32_t)nth >> 5, w = (uint32_t)tid >> 5;
+    const uint32_t ca = 1u << lgca;
+    const uint32_t K = ((count + nw - 1) / nw + ca - 1) & ~(ca - 1);
+    A0 = min(count, w * K);
+    A1 = min(count, A0 + K);
 }
 
 // One gate op (frame rule RULE) without fused noise: (application, vector)
@@ -278,109 +394,117 @@ __device__ __forceinline__ void gate_plain(uint32_t* X, uint32_t* Z, const uint3
     }
 }
 
-// Gate + its noise instruction: item (chunk k, vector c) owns the chunk's ca
-// applications — the rule on each (operands four at a time), then the chunk's hits
+// Gate + its noise instruction: each warp owns a chunk-aligned range of
+// applications — its lanes apply the rule to (application, vector) items of
+// the range (four operand loads in flight), then the warp draws the range's
+// noise chunks.  No group barrier between the rule and its noise.
 template <int W>
 __device__ __forceinline__ void gate_fused(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
-                                           const uint32_t* tg, uint32_t code, uint32_t count, const NoiseOp& nz,
-                                           uint32_t rowb, const unsigned long long* tab, uint32_t* sl, int tid,
-                                           int nth, int64_t tile) {
+                                           const uint32_t* tg, const uint32_t* tgp, uint32_t K, uint32_t code,
+                                           uint32_t count, const NoiseOp& nz,
+                                           uint32_t rowb, const unsigned long long* tab, uint32_t* sl,
+                                           uint32_t* wscr, int tid, int nth, int64_t tile) {
     constexpr int V = W >= 4 ? 4 : W;
     constexpr int C = W / V;
     constexpr int LC = Log2<C>::v;
+    const int lane = tid & 31;
     const int ar = code >= R_CX ? 2 : 1;
-    const uint32_t lgca = nz.lgL - nz.lgcs;
-    const uint32_t nA = (count + (1u << lgca) - 1) >> lgca;
-    const int items = (int)(nA << LC);
-    for (int i = tid; i < items; i += nth) {
-        const uint32_t k = (uint32_t)i >> LC;
-        const int c = i & (C - 1);
-        const uint32_t a0 = k << lgca;
-        const uint32_t na = min(1u << lgca, count - a0);
-        for (uint32_t j0 = 0; j0 < na; j0 += 4) {
-            uint2 qq[4];
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                const uint32_t app = a0 + j0 + u;
-                qq[u] = j0 + u >= na ? make_uint2(0u, 0u)
-                      : ar == 2 ? reinterpret_cast<const uint2*>(tg)[app] : make_uint2(tg[app], 0u);
-            }
-#pragma unroll
-            for (int u = 0; u < 4; u++) {
-                if (j0 + u >= na) break;
-                const size_t p0 = (size_t)qq[u].x * W + c * V, p1 = (size_t)qq[u].y * W + c * V;
-                VW<V> x0 = vld<V>(X + p0), z0 = vld<V>(Z + p0), x1 = vzero<V>(), z1 = vzero<V>();
-                if (ar == 2) { x1 = vld<V>(X + p1); z1 = vld<V>(Z + p1); }
-                apply_rule<V>(code, x0, z0, x1, z1);
-                vst<V>(X + p0, x0);
-                vst<V>(Z + p0, z0);
-                if (ar == 2) { vst<V>(X + p1, x1); vst<V>(Z + p1, z1); }
-            }
-        }
-        item_noise<W>(kp, tk, nz, tab, k, c, a0, na, tg, ar, false, X, Z, sl, rowb, tile);
+    // this warp's chunk-aligned range of K applications (host-computed, op.b);
+    // its gate work walks the bank-ordered copy of the range (op.a)
+    const uint32_t A0 = min(count, ((uint32_t)tid >> 5) * K), A1 = min(count, A0 + K);
+    if (A0 >= A1) return;  // warp-uniform
+    const int items = (int)((A1 - A0) << LC);
+    const uint32_t* const tga = tgp + (size_t)A0 * ar;
+    if (ar == 1) {
+        batched_items<4>(lane, 32, items, [&](int i) { return tga[i >> LC]; }, [&](int i, uint32_t q) {
+            const size_t p = (size_t)q * W + (i & (C - 1)) * V;
+            VW<V> x0 = vld<V>(X + p), z0 = vld<V>(Z + p), x1, z1;
+            apply_rule<V>(code, x0, z0, x1, z1);
+            if (code != R_ZXORX) vst<V>(X + p, x0);
+            if (code != R_XXORZ) vst<V>(Z + p, z0);
+        });
+    } else {
+        batched_items<4>(lane, 32, items, [&](int i) { return reinterpret_cast<const uint2*>(tga)[i >> LC]; },
+                         [&](int i, uint2 qq) {
+            const int cv = (i & (C - 1)) * V;
+            const size_t p0 = (size_t)qq.x * W + cv, p1 = (size_t)qq.y * W + cv;
+            VW<V> x0 = vld<V>(X + p0), x1 = vld<V>(X + p1);
+            VW<V> z0 = vld<V>(Z + p0), z1 = vld<V>(Z + p1);
+            apply_rule<V>(code, x0, z0, x1, z1);
+            if (code != R_CZ) vst<V>(X + p1, x1);
+            if (code == R_SWAP) vst<V>(X + p0, x0);
+            vst<V>(Z + p0, z0);
+            if (code != R_CX) vst<V>(Z + p1, z1);
+        });
     }
+    warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, ar, false, X, Z, sl, wscr, lane, rowb, tile);
 }
 
-// M / R / MR (+ fused noise: after a reset, before a measurement) over items
-// (chunk k, vector c) of ca targets each (ca = 1 without fused noise)
+// M / R / MR (+ fused noise: after a reset, before a measurement).  With
+// fused noise each warp owns a chunk-aligned target range (noise, then the
+// collapses of its (target, vector) items — or the reverse for a reset);
+// without, (target, vector) items over the whole group.
 template <int W>
 __device__ __forceinline__ void collapse_op(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
                                             uint32_t* ring, const uint32_t* tg, uint32_t kind, uint32_t count,
                                             bool fz, const NoiseOp& nz, uint32_t rowb, uint32_t rec0, uint32_t coin0,
-                                            const unsigned long long* tab, uint32_t* sl, int tid, int nth,
-                                            int64_t tile) {
+                                            const unsigned long long* tab, uint32_t* sl, uint32_t* wscr, int tid,
+                                            int nth, int64_t tile) {
     constexpr int V = W >= 4 ? 4 : W;
     constexpr int C = W / V;
     constexpr int LC = Log2<C>::v;
-    const uint32_t lgca = fz ? nz.lgL - nz.lgcs : 0u;
-    const uint32_t nA = (count + (1u << lgca) - 1) >> lgca;
-    const int items = (int)(nA << LC);
-    const uint2* const tp = reinterpret_cast<const uint2*>(tg);  // (row | COIN_DEAD, slot)
-    for (int i = tid; i < items; i += nth) {
-        const uint32_t k = (uint32_t)i >> LC;
-        const int c = i & (C - 1);
-        const uint32_t a0 = k << lgca;
-        const uint32_t na = min(1u << lgca, count - a0);
+    const int lane = tid & 31;
+    uint32_t A0 = 0, A1 = count;
+    int first = tid, stride = nth;
+    if (fz) {
+        warp_range(count, nz.lgL - nz.lgcs, tid, nth, A0, A1);
+        if (A0 >= A1) return;  // warp-uniform
+        first = lane;
+        stride = 32;
         // the fused noise precedes a measurement (X_ERROR before M)
-        if (fz && kind != K_R) item_noise<W>(kp, tk, nz, tab, k, c, a0, na, tg, 1, true, X, Z, sl, rowb, tile);
-        for (uint32_t j = 0; j < na; j++) {
-            const uint32_t app = a0 + j;
-            const uint2 rs = tp[app];
-            const bool live = !(rs.x & COIN_DEAD);
-            const size_t p = (size_t)(rs.x & ~COIN_DEAD) * W + c * V;
-            if (kind == K_R) {
-                // spill the record homed in x, then reset
-                if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, vld<V>(X + p));
-                vst<V>(X + p, vzero<V>());
-                vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + app, c, tile) : vzero<V>());
-                continue;
-            }
-            const VW<V> x = vld<V>(X + p);
-            if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, x);
-            if (kp.rec_out != nullptr)
-                vst<V>(kp.rec_out + (int64_t)(rec0 + app) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, x);
-            if (kind == K_M) {
-                if (live) vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_vec<W, V>(kp, tk, coin0 + app, c, tile)));
-            } else {  // MR: the measure's coin row (coin0 + 2 app) is overwritten by the reset's
-                vst<V>(X + p, vzero<V>());
-                vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + 2 * app + 1, c, tile) : vzero<V>());
-            }
-        }
-        if (fz && kind == K_R) item_noise<W>(kp, tk, nz, tab, k, c, a0, na, tg, 1, true, X, Z, sl, rowb, tile);
+        if (kind != K_R) warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile);
     }
+    const uint2* const tp = reinterpret_cast<const uint2*>(tg);  // (row | COIN_DEAD, slot)
+    batched_items<4>(first, stride, (int)((A1 - A0) << LC), [&](int i) { return tp[A0 + (i >> LC)]; },
+                     [&](int i, uint2 rs) {
+        const uint32_t app = A0 + (uint32_t)(i >> LC);
+        const int c = i & (C - 1);
+        const bool live = !(rs.x & COIN_DEAD);
+        const size_t p = (size_t)(rs.x & ~COIN_DEAD) * W + c * V;
+        if (kind == K_R) {
+            // spill the record homed in x, then reset
+            if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, vld<V>(X + p));
+            vst<V>(X + p, vzero<V>());
+            vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + app, c, tile) : vzero<V>());
+            return;
+        }
+        const VW<V> x = vld<V>(X + p);
+        if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, x);
+        if (kp.rec_out != nullptr)
+            vst<V>(kp.rec_out + (int64_t)(rec0 + app) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, x);
+        if (kind == K_M) {
+            if (live) vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_vec<W, V>(kp, tk, coin0 + app, c, tile)));
+        } else {  // MR: the measure's coin row (coin0 + 2 app) is overwritten by the reset's
+            vst<V>(X + p, vzero<V>());
+            vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + 2 * app + 1, c, tile) : vzero<V>());
+        }
+    });
+    if (fz && kind == K_R) warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile);
 }
 
-// A standalone noise instruction: one chunk per item, hits XORed with
-// shared-memory atomics (consecutive noise ops commute: no barrier between them)
+// A standalone noise instruction: one chunk per lane, warp-cooperative draws,
+// hits XORed with shared-memory atomics (consecutive noise ops commute: no
+// barrier between them)
 template <int W>
 __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
                                          const uint32_t* tg, uint32_t code, uint32_t count, const NoiseOp& nz,
-                                         uint32_t rowb, const unsigned long long* tab, uint32_t* sl, int tid,
-                                         int nth, int64_t tile) {
+                                         uint32_t rowb, const unsigned long long* tab, uint32_t* sl, uint32_t* wscr,
+                                         int tid, int nth, int64_t tile) {
     constexpr int V = W >= 4 ? 4 : W;
     constexpr int C = W / V;
     constexpr int LC = Log2<C>::v;
     const int ar = code == CH_DEP2 ? 2 : 1;
+    const int lane = tid & 31;
     if (kp.masks != nullptr) {
         // injected masks: per target, x row then z row
         const int items = (int)((count * ar) << LC);
@@ -398,13 +522,19 @@ __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, u
         return;
     }
     if (nz.zone == NZONE_NONE) return;
+#if PFS_PROFILE
+    if (kp.debug_skip & 2) return;
+#endif
     const uint32_t lgca = nz.lgL - nz.lgcs;
     const uint32_t nS = (32u * W) >> nz.lgcs;
     const uint32_t nch = ((count + (1u << lgca) - 1) >> lgca) * nS;
-    for (uint32_t r = tid; r < nch; r += nth) {
+    for (uint32_t rb = (uint32_t)(tid - lane); rb < nch; rb += nth) {
+        const uint32_t r = rb + (uint32_t)lane;
+        const bool valid = r < nch;
         const uint32_t k = r / nS, cc = r - k * nS;
         const uint32_t a0 = k << lgca;
-        chunk_hits<W, true>(tk, nz, tab, r, a0, min(1u << lgca, count - a0), cc << nz.lgcs, tg, ar, false, X, Z, sl);
+        warp_chunks<W>(tk, nz, tab, valid, r, a0, valid ? min(1u << lgca, count - a0) : 0u, cc << nz.lgcs, tg, ar,
+                       false, X, Z, sl, wscr, lane);
     }
 }
 
@@ -435,10 +565,12 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     uint32_t* const ring = RING_SMEM ? (smem + G * fw + (size_t)grp * kp.num_slots * W)
                                      : (kp.ring_global + ((size_t)blockIdx.x * G + grp) * kp.num_slots * W);
     uint32_t* const cnt = smem + G * fw + (RING_SMEM ? (size_t)G * kp.num_slots * W : 0);
-    // 16-byte aligned tail: the op descriptors, then the threshold tables
-    // (offset arithmetic on the shared array keeps the loads in the shared
-    // address space: LDS, not generic LD)
-    const size_t dsc_word = ((size_t)(cnt + (kp.counts_in_smem ? kp.num_cols : 0) - smem) + 3) & ~(size_t)3;
+    // then the per-warp noise scratch, and a 16-byte aligned tail: the op
+    // descriptors, then the threshold tables (offset arithmetic on the shared
+    // array keeps the loads in the shared address space: LDS, not generic LD)
+    const size_t wscr_word = (size_t)(cnt + (kp.counts_in_smem ? kp.num_cols : 0) - smem);
+    uint32_t* const wscr = smem + wscr_word + (size_t)(threadIdx.x >> 5) * WSCR;
+    const size_t dsc_word = (wscr_word + (size_t)(blockDim.x >> 5) * WSCR + 3) & ~(size_t)3;
     uint4* const dsc_s = reinterpret_cast<uint4*>(smem + dsc_word);
     unsigned long long* const tab_s = reinterpret_cast<unsigned long long*>(dsc_s + 2 * kp.n_ops);
     const uint4* const dsc_g = reinterpret_cast<const uint4*>(kp.ops);
@@ -484,6 +616,29 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             const uint4 h1 = h1n;
             if (oi + 1 < kp.n_ops) { h0 = ldesc(2 * oi + 2); h1n = ldesc(2 * oi + 3); }
             const uint32_t ob = h1.x;
+            if (oi + 1 < kp.n_ops) {
+                // pull the next op's operand block into L1 while this op runs:
+                // the frame and ring leave ~20 KB of L1, not a whole round of
+                // operands, and an L2 round trip per operand load would sit on
+                // every op's critical path
+                const uint32_t nk = h0.x & 0xFFu, nc = (h0.x >> 8) & 0xFFu, ncount = h0.y;
+                const uint32_t* base;
+                uint32_t words;
+                if (nk == K_DET) {
+                    base = kp.det_terms + h0.z;
+                    words = nc ? ncount * nc : 0u;
+                } else {
+                    // (a fused gate's gate work walks its bank-ordered copy)
+                    base = kp.targets + ((nk == K_GATE && ((h0.x >> 16) & F_NOISE)) ? h0.w : h0.z);
+                    const uint32_t per = (nk == K_GATE) ? (nc >= R_CX ? 2u : 1u)
+                                       : (nk == K_NOISE) ? (nc == CH_DEP2 ? 2u : 1u)
+                                       : (nk == K_OBS) ? 1u : 2u;
+                    words = ncount * per;
+                }
+                const uint32_t lines = (words * 4u + 127u) >> 7;
+                for (uint32_t l = (uint32_t)tid; l < lines; l += (uint32_t)nth)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(base + 32u * l));
+            }
             if (flags & F_BARRIER) group_sync();
 #if PFS_PROFILE
             if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
@@ -506,7 +661,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             switch (kind) {
             case K_GATE: {
                 if (fz) {
-                    gate_fused<W>(kp, tk, X, Z, tg, code, count, nz, rowb, tab, sl, tid, nth, tile);
+                    gate_fused<W>(kp, tk, X, Z, tg, kp.targets + oa, ob, code, count, nz, rowb, tab, sl, wscr, tid, nth, tile);
                     break;
                 }
                 switch (code) {
@@ -522,7 +677,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 break;
             }
             case K_R: case K_M: case K_MR:
-                collapse_op<W>(kp, tk, X, Z, ring, tg, kind, count, fz, nz, rowb, oa, ob, tab, sl, tid, nth, tile);
+                collapse_op<W>(kp, tk, X, Z, ring, tg, kind, count, fz, nz, rowb, oa, ob, tab, sl, wscr, tid, nth, tile);
                 break;
             case K_SPILL: {
                 const uint2* const tp = reinterpret_cast<const uint2*>(tg);
@@ -534,7 +689,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 break;
             }
             case K_NOISE:
-                noise_op<W>(kp, tk, X, Z, tg, code, count, nz, rowb, tab, sl, tid, nth, tile);
+                noise_op<W>(kp, tk, X, Z, tg, code, count, nz, rowb, tab, sl, wscr, tid, nth, tile);
                 break;
             case K_DET: {
                 const int items = (int)(count << LC);
