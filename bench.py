@@ -62,6 +62,8 @@ def parse_args():
     ap.add_argument("--no-d100", action="store_true", help="skip the config 4 (d=100) extra line")
     ap.add_argument("--no-dem", action="store_true", help="skip the error-model sampler extra line")
     ap.add_argument("--no-c3", action="store_true", help="skip the config 3 counts extra line")
+    ap.add_argument("--presample", type=int, default=0,
+                    help="fused noise pre-sampled by noise_kernel (0 auto/on, -1 drawn inline)")
     ap.add_argument("--no-pyref", action="store_true", help="skip timing the Python reference package")
     ap.add_argument("--pipeline", type=int, default=0, help="frame/transpose pipeline sub-chunks (0 auto, 1 off)")
     return ap.parse_args()
@@ -275,7 +277,8 @@ def run_reference(args, rank, world):
 def native_opts(args):
     return dict(words_per_tile=args.words, ring_in_smem=args.ring, threads=args.threads,
                 noise_target_hits=args.target_hits, kernel=args.kernel, groups=args.groups,
-                pipeline=args.pipeline, fused_target_hits=args.fused_hits)
+                pipeline=args.pipeline, fused_target_hits=args.fused_hits,
+                presample_noise=args.presample)
 
 
 def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, world: int,
@@ -341,15 +344,17 @@ def measure(args, cfg: int, shots: int, steps: int, warmup: int, rank: int, worl
     dt.circuit, dt.flat, dt.device = None, flat, local_rank
     dt._seeds = np.random.default_rng(0)
     dt.native = N.NativeProgram(flat, timing=True, **kw)
-    fr, tr = [], []
+    fr, tr, nz = [], [], []
     for i in range(max(3, min(steps, 10))):
         step(dt, i)
         t = dt.native.last_timing()
         if i:
             fr.append(t[0])
             tr.append(t[1])
+            nz.append(t[5])
     res["frame_ms"] = float(np.mean(fr))
     res["transpose_ms"] = float(np.mean(tr))
+    res["noise_ms"] = float(np.mean(nz))
     del dt
 
     if e2e_steps > 0:
@@ -430,6 +435,7 @@ def roofline_of(res, smem_peak, hbm):
                            "all SMs)",
             "kernel": "frame_kernel (frame table resident in shared memory, noise sampled inline)",
             "frame_kernel_ms": fr, "transpose_kernel_ms": res["transpose_ms"],
+            "noise_kernel_ms": res["noise_ms"],
             "bytes_per_shot": bframe_bytes,
             "hbm_equiv": {"achieved_gbs": achieved, "peak_gbs": hbm, "frac": achieved / hbm,
                           "note": "frame-update GB/s vs measured HBM copy peak (BASELINE.json "

@@ -49,7 +49,9 @@ typedef struct pfs_options {
     int32_t debug_skip;       /* profiling ablations only (wrong results!): bit0 noise
                                  apply, bit1 noise pre-pass, bit2 coin RNG, bit3 detectors,
                                  bit4 gates, bit5 collapses */
-    int32_t producer_threads; /* reserved (0)                                        */
+    int32_t presample_noise;  /* fused noise drawn by noise_kernel into per-warp hit
+                                 lists ahead of the frame kernel: 0 auto (on), -1 off
+                                 (drawn inline by the frame kernel)                 */
     int32_t schedule_only;    /* 1: compile without the shared-memory fit check (the
                                  program exposes info / noise schedule, cannot run)  */
     int32_t groups;           /* independent tiles in flight per CTA (0 = auto)     */
@@ -61,7 +63,7 @@ typedef struct pfs_options {
                                  sub-chunk's frame kernel (0 = auto, 1 = off)        */
     int32_t fused_target_milli; /* expected hits x 1000 per noise chunk of a noise
                                  instruction fused into its gate / collapse op
-                                 (0 = 500)                                          */
+                                 (0 = 1000)                                         */
 } pfs_options;
 
 typedef struct pfs_info {

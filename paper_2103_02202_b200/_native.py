@@ -31,7 +31,7 @@ class Options(ctypes.Structure):
     _fields_ = [("words_per_tile", ctypes.c_int32), ("ring_in_smem", ctypes.c_int32),
                 ("threads", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("noise_target_hits", ctypes.c_double), ("timing", ctypes.c_int32),
-                ("debug_skip", ctypes.c_int32), ("producer_threads", ctypes.c_int32),
+                ("debug_skip", ctypes.c_int32), ("presample_noise", ctypes.c_int32),
                 ("schedule_only", ctypes.c_int32), ("groups", ctypes.c_int32),
                 ("kernel", ctypes.c_int32), ("pipeline", ctypes.c_int32),
                 ("fused_target_milli", ctypes.c_int32)]
@@ -159,7 +159,7 @@ class NativeProgram:
 
     def __init__(self, prog: FlatProgram, words_per_tile: int = 0, ring_in_smem: int = -1,
                  threads: int = 0, ctas_per_sm: int = 0, noise_target_hits: float = 0.0,
-                 timing: bool = False, debug_skip: int = 0, producer_threads: int = 0,
+                 timing: bool = False, debug_skip: int = 0, presample_noise: int = 0,
                  schedule_only: bool = False, groups: int = 0, kernel: int = 0,
                  pipeline: int = 0, fused_target_hits: float = 0.0):
         L = lib()
@@ -171,7 +171,7 @@ class NativeProgram:
                       np.ascontiguousarray(prog.det_idx, dtype=np.int64)]
         ins, tg, p, dp, di = self._keep
         opts = Options(words_per_tile, ring_in_smem, threads, ctas_per_sm, noise_target_hits,
-                       1 if timing else 0, debug_skip, producer_threads, 1 if schedule_only else 0,
+                       1 if timing else 0, debug_skip, presample_noise, 1 if schedule_only else 0,
                        groups, kernel, pipeline, int(round(fused_target_hits * 1000)))
         h = ctypes.c_void_p()
         _check(L.pfs_program_create(_p(ins), ins.shape[0], _p(tg), tg.shape[0], _p(p), p.shape[0],

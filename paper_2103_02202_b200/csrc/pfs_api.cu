@@ -62,10 +62,11 @@ struct Flavour {
     DevBuf<uint32_t> targets, det_ptr, det_terms, ring, init_dead, row_of, noise_ch, noise_rowb;
     DevBuf<NoiseParam> noise;
     DevBuf<unsigned long long> noise_tab;
+    DevBuf<uint32_t> fused, hit_items;  // pre-sampled fused noise (noise_kernel)
     void release() {
         ops.release(); targets.release(); det_ptr.release(); det_terms.release(); ring.release();
         init_dead.release(); row_of.release(); noise_ch.release(); noise_rowb.release();
-        noise.release(); noise_tab.release();
+        noise.release(); noise_tab.release(); fused.release(); hit_items.release();
     }
 };
 }  // namespace
@@ -83,6 +84,10 @@ struct pfs_program {
     DevBuf<uint32_t> d_coins, d_masks;
     DevBuf<uint8_t> d_ref;
     DevBuf<unsigned long long> d_counts;
+    DevBuf<unsigned long long> d_hits;  // noise_kernel hit entries of one sub-chunk of tiles
+    DevBuf<uint32_t> d_spans;           // their per-warp spans (uint2) and per-tile fill counters
+    DevBuf<uint32_t> d_fill;
+    int noise_grid = 0;
     // error-model detector sampler (KERNEL_DEM)
     bool demk = false;
     bool dem_global = false;    // output column words in global memory (too many for shared)
@@ -111,6 +116,7 @@ constexpr int kPipeFrameThreads = FRAME_MAX_THREADS;
 constexpr int DEM_WARPS_HOST = 16;  // dem_kernel's warps (DEM_WARPS)
 constexpr double kStandaloneHits = 2.0;  // mean hits per noise chunk (standalone / error-model)
 constexpr double kFusedHits = 1.0;       // mean hits per fused noise chunk (one kernel item)
+constexpr int64_t kHitBufBytes = (int64_t)256 << 20;  // hit lists of one sub-chunk of tiles
 
 static bool desc_fits(const HostProgram& hp) {
     return hp.ops.size() * sizeof(DOp) + hp.noise_tab.size() * 8 <= (size_t)DESC_SMEM_MAX;
@@ -284,7 +290,11 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
             dedup_operands(hp);
             // the error-model kernel's chunks span whole 32-shot tiles
             build_noise_schedule(hp, 32 * W, dem ? 32 : 32 * V, th, dem ? th : thf);
-            if (!dem) bank_order_fused(hp, W, cfg.threads / std::max(1, cfg.groups) / 32);
+            if (!dem) {
+                const int wpg = cfg.threads / std::max(1, cfg.groups) / 32;
+                bank_order_fused(hp, W, wpg);
+                if (pg->opts.presample_noise >= 0) build_hit_lists(hp, 32 * W, wpg);
+            }
             Flavour& f = pg->fl[m];
             if (m == PM_RECORDS) f.cfg = cfg, f.cfg.ring_smem = true;
             f.desc_smem = desc_fits(hp);
@@ -373,6 +383,7 @@ void pfs_program_destroy(pfs_program* pg) {
         pg->d_coins.release(); pg->d_masks.release(); pg->d_ref.release(); pg->d_counts.release();
         pg->d_comp_base.release(); pg->d_cols.release(); pg->d_items.release();
         pg->d_comp_words.release();
+        pg->d_hits.release(); pg->d_spans.release(); pg->d_fill.release();
         if (pg->copy_stream) cudaStreamDestroy(pg->copy_stream);
         if (pg->frame_stream) cudaStreamDestroy(pg->frame_stream);
         if (pg->tr_stream) cudaStreamDestroy(pg->tr_stream);
@@ -424,6 +435,8 @@ static int ensure_device(pfs_program* pg, int device) {
         CUDA_TRY(upload(f.noise_rowb, hp.noise_rowb));
         CUDA_TRY(upload(f.init_dead, hp.init_dead));
         CUDA_TRY(upload(f.row_of, hp.row_of));
+        CUDA_TRY(upload(f.fused, hp.fused_info));
+        CUDA_TRY(upload(f.hit_items, hp.hit_items));
         if (!pg->demk) {
             // the attribute is per kernel instance, shared by both flavours and
             // counts mode: allow the device maximum once
@@ -451,6 +464,7 @@ static int ensure_device(pfs_program* pg, int device) {
         }
         pg->dem_grid = pg->num_sms * per_sm;
     }
+    pg->noise_grid = pg->num_sms * std::max(1, prop.maxThreadsPerMultiProcessor / (NK_WARPS * 32));
     CUDA_TRY(cudaStreamCreateWithFlags(&pg->copy_stream, cudaStreamNonBlocking));
     {
         int least = 0, greatest = 0;
@@ -535,9 +549,24 @@ static int launch_tiles(pfs_program* pg, const Flavour& f, KParams kp, const Lau
     const int pipe = pg->opts.pipeline > 0 ? pg->opts.pipeline : pg->pipe_default;
     const int64_t per_wave = (int64_t)cfg.grid * std::max(cfg.groups, 1);
     const bool piped = tj != nullptr && !serial && pipe > 1 && nt >= 2 * per_wave;
+    // pre-sampled fused noise: noise_kernel fills the hit lists of a sub-chunk
+    // of tiles ahead of its frame kernel (same stream), lists bounded by kHitBufBytes
+    const bool lists = !hp.hit_items.empty() && kp.masks == nullptr && !(pg->opts.debug_skip & 2);
     int64_t sub = nt;
+    if (lists) {
+        const int64_t cap_tiles = std::max<int64_t>(per_wave, kHitBufBytes / (hp.hit_block * 8) / per_wave * per_wave);
+        sub = std::min(nt, cap_tiles);
+        CUDA_TRY(pg->d_hits.reserve((size_t)sub * hp.hit_block));
+        CUDA_TRY(pg->d_spans.reserve((size_t)sub * hp.num_noise * hp.list_warps * 2));
+        CUDA_TRY(pg->d_fill.reserve((size_t)sub));
+        kp.fused = reinterpret_cast<const uint4*>(f.fused.p);
+        kp.hit_items = reinterpret_cast<const uint2*>(f.hit_items.p);
+        kp.hit_block = hp.hit_block;
+        kp.list_warps = hp.list_warps;
+        kp.n_items = (int32_t)(hp.hit_items.size() / 2);
+    }
     if (piped) {
-        sub = ((nt + pipe - 1) / pipe + per_wave - 1) / per_wave * per_wave;  // whole waves per sub-chunk
+        sub = std::min(sub, ((nt + pipe - 1) / pipe + per_wave - 1) / per_wave * per_wave);  // whole waves per sub-chunk
         CUDA_TRY(cudaEventRecord(pg->pev[0], st));  // everything before this call
         CUDA_TRY(cudaStreamWaitEvent(pg->frame_stream, pg->pev[0], 0));
         CUDA_TRY(cudaStreamWaitEvent(pg->tr_stream, pg->pev[0], 0));
@@ -556,6 +585,25 @@ static int launch_tiles(pfs_program* pg, const Flavour& f, KParams kp, const Lau
         LaunchCfg lc = cfg;
         k2.groups = cfg.groups;
         lc.grid = (int)std::min<int64_t>(cfg.grid, (ns + cfg.groups - 1) / cfg.groups);
+        if (lists) {
+            const bool tm = serial && pg->opts.timing;
+            k2.hits_global = pg->d_hits.p;
+            k2.spans_global = reinterpret_cast<uint2*>(pg->d_spans.p);
+            k2.fill_global = pg->d_fill.p;
+            if (tm) CUDA_TRY(cudaEventRecord(pg->ev[8], fst));
+            CUDA_TRY(cudaMemsetAsync(pg->d_fill.p, 0, (size_t)ns * 4, fst));
+            const int64_t items = ns * k2.n_items;
+            const int ng = (int)std::min<int64_t>(pg->noise_grid, (items + NK_WARPS - 1) / NK_WARPS);
+            CUDA_TRY(launch_noise_kernel(W, k2, ng, fst));
+            pg->last_launches++;
+            if (tm) {
+                CUDA_TRY(cudaEventRecord(pg->ev[9], fst));
+                CUDA_TRY(cudaEventSynchronize(pg->ev[9]));
+                float ms = 0;
+                cudaEventElapsedTime(&ms, pg->ev[8], pg->ev[9]);
+                pg->last_ms[5] += ms;
+            }
+        }
         CUDA_TRY(launch_frame_kernel(lc, k2, fst));
         pg->last_launches++;
         if (piped) {
@@ -861,7 +909,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
         float h2d = 0, tot = 0;
         cudaEventElapsedTime(&h2d, pg->ev[0], pg->ev[1]);
         cudaEventElapsedTime(&tot, pg->ev[0], pg->ev[4]);
-        pg->last_ms[0] = frame_ms;
+        pg->last_ms[0] = frame_ms - pg->last_ms[5];  // frame kernels only (noise_kernel: [5])
         pg->last_ms[1] = tr_ms;
         pg->last_ms[2] = h2d;
         pg->last_ms[4] = tot;

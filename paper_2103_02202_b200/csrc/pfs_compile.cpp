@@ -742,6 +742,47 @@ void bank_order_fused(HostProgram& hp, int W, int warps_per_group) {
     }
 }
 
+// Pre-sampled fused noise (noise_kernel): a fused op's consumer warp w owns
+// applications [w K, w K + K) (K = ceil(apps / warps) rounded up to whole
+// chunks, the kernel's warp_range), and reads its hits from a fixed-capacity
+// list filled by noise_kernel (capacity = mean + 6 sigma + 8; a fuller list,
+// or a chunk needing the general path, is left to the consumer to draw).
+void build_hit_lists(HostProgram& hp, int tile_shots, int warps_per_group) {
+    const uint32_t nw = (uint32_t)std::max(1, warps_per_group);
+    hp.list_warps = (int32_t)nw;
+    hp.fused_info.assign((size_t)hp.num_noise * 4, 0u);
+    hp.hit_items.clear();
+    double mean_all = 0.0;
+    for (const DOp& o : hp.ops) {
+        const uint32_t kind = o.kcf & 0xFF;
+        if (!((o.kcf >> 16) & F_NOISE) || o.c == NO_SLOT) continue;
+        const NoiseParam& np = hp.noise[o.c];
+        if (np.zone != NZONE_TAB) continue;  // p == 0 / p == 1: drawn by the consumer
+        const uint32_t ca = std::max<uint32_t>(1u, np.ca);
+        const uint32_t K = ((np.apps + nw - 1) / nw + ca - 1) / ca * ca;
+        const double p = hp.noise_p[o.c];
+        // consumer warps per noise_kernel item: as many as keep the item's hits
+        // (mean + 6 sigma + slack) within one warp's staging buffer
+        const double per_warp = (double)K * tile_shots * p;
+        uint32_t wpi = nw;
+        while (wpi > 0 && per_warp * wpi + 6.0 * std::sqrt(per_warp * wpi) + 16.0 > (double)NK_SCR) wpi--;
+        if (wpi == 0) continue;  // heavy noise: drawn by the consumer
+        uint32_t* fi = &hp.fused_info[(size_t)o.c * 4];
+        fi[0] = K;
+        fi[1] = 1u;
+        fi[3] = o.off | (kind == K_GATE ? 0u : FUSED_PAIRS);
+        for (uint32_t wb = 0; wb < nw; wb += wpi) {
+            hp.hit_items.push_back(o.c);
+            hp.hit_items.push_back(wb | (std::min(nw, wb + wpi) << 16));
+        }
+        mean_all += (double)np.apps * tile_shots * p;
+    }
+    // a tile's entries; an item that finds the block full leaves its warps to
+    // draw inline (still exact), so the bound only sets how rare that is
+    hp.hit_block = hp.hit_items.empty() ? 0 : (int64_t)std::ceil(mean_all + 8.0 * std::sqrt(mean_all) + 256.0);
+    if (hp.hit_block >= (1ll << 31)) bad("noise hit lists too large");
+}
+
 // Operand blocks repeat across the rounds of a REPEAT body (same qubits, and
 // with LIFO slot reuse usually the same record slots): point every op at the
 // first identical block, so the operand stream a kernel walks (and keeps in

@@ -27,19 +27,6 @@ constexpr int DEM_WARPS = 16;
 // ordinal and chunk shuffled in), duplicates / oversize counts are redrawn
 // serially.  Packing chunks of different instructions keeps all lanes busy
 // when an instruction has fewer than 32 chunks per 32-shot tile.
-__device__ __forceinline__ NoiseOp noise_op_of(const NoiseParam& np, uint32_t ordinal) {
-    NoiseOp n;
-    n.ordinal = ordinal;
-    n.lgL = 31u - __clz(np.L);
-    n.lgcs = 31u - __clz(np.cs);
-    n.npat = np.npat;
-    n.ch = np.ch;
-    n.zone = np.zone;
-    n.tab_off = np.tab;
-    n.tab_len = np.len;
-    return n;
-}
-
 template <typename Apply>
 __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2* items, uint32_t n_items,
                                                  uint32_t first, const TileKey& tk, uint32_t* wscr, uint32_t* sl,

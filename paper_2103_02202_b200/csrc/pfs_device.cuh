@@ -16,10 +16,9 @@
 namespace pfs {
 
 // ---------------------------------------------------------------- Philox
-// Out of line: one copy of the 10 unrolled rounds serves every call site (the
-// interpreter kernel is instruction-cache bound when each site inlines it).
-static __device__ __noinline__ uint4 philox4x32_10_block(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
-                                                  uint32_t k1) {
+// The 10 rounds inline (the hottest draw site uses this directly) ...
+__device__ __forceinline__ void philox_rounds(uint32_t& c0, uint32_t& c1, uint32_t& c2, uint32_t& c3, uint32_t k0,
+                                              uint32_t k1) {
 #pragma unroll
     for (int r = 0; r < 10; r++) {
         const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
@@ -29,6 +28,11 @@ static __device__ __noinline__ uint4 philox4x32_10_block(uint32_t c0, uint32_t c
         c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
         k0 += 0x9E3779B9u; k1 += 0xBB67AE85u;
     }
+}
+// ... and out of line: one copy serves the other call sites (code size)
+static __device__ __noinline__ uint4 philox4x32_10_block(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, uint32_t k0,
+                                                  uint32_t k1) {
+    philox_rounds(c0, c1, c2, c3, k0, k1);
     return make_uint4(c0, c1, c2, c3);
 }
 __device__ __forceinline__ void philox4x32_10(uint32_t& c0, uint32_t& c1, uint32_t& c2,
@@ -115,6 +119,19 @@ __device__ __forceinline__ NoiseOp decode_noise(uint32_t c, uint32_t d, uint32_t
     n.zone = (d >> 17) & 3u;
     n.tab_off = e & 0xFFFFFFu;
     n.tab_len = e >> 24;
+    return n;
+}
+
+__device__ __forceinline__ NoiseOp noise_op_of(const NoiseParam& np, uint32_t ordinal) {
+    NoiseOp n;
+    n.ordinal = ordinal;
+    n.lgL = 31u - __clz(np.L);
+    n.lgcs = 31u - __clz(np.cs);
+    n.npat = np.npat;
+    n.ch = np.ch;
+    n.zone = np.zone;
+    n.tab_off = np.tab;
+    n.tab_len = np.len;
     return n;
 }
 

@@ -121,7 +121,17 @@ struct HostProgram {
     // filled by build_noise_schedule once the tile geometry is known
     std::vector<NoiseParam> noise;
     std::vector<uint64_t> noise_tab;
+    // pre-sampled hit lists of fused noise (build_hit_lists): per ordinal
+    // (K = applications per consumer warp, 1 = pre-sampled, 0, targets
+    // offset | PAIRS), and the noise_kernel work items of one tile
+    std::vector<uint32_t> fused_info;   // 4 per ordinal (zeros: drawn by the frame kernel)
+    std::vector<uint32_t> hit_items;    // 2 per item: ordinal, first | last consumer warp << 16
+    int64_t hit_block = 0;              // hit-entry capacity of one tile
+    int32_t list_warps = 0;             // consumer warps per group
 };
+constexpr uint32_t FUSED_PAIRS = 0x80000000u;  // fused_info[3]: targets are (row, slot) pairs
+constexpr int NK_WARPS = 8;                    // noise_kernel warps per CTA
+constexpr int NK_SCR = 384;                    // noise_kernel hit entries staged per warp
 
 // Host compiler: flat program -> device ops (splitting, noise fusion, merging,
 // record homes and ring-slot liveness, coin relevance, barrier scheduling).
@@ -139,6 +149,7 @@ void build_noise_schedule(HostProgram& hp, int tile_shots, int vector_shots, dou
 void permute_rows(HostProgram& hp);
 void reorder_for_banks(HostProgram& hp, int W);
 void bank_order_fused(HostProgram& hp, int W, int warps_per_group);
+void build_hit_lists(HostProgram& hp, int tile_shots, int warps_per_group);
 void dedup_operands(HostProgram& hp);
 
 // Kernel launch plumbing (pfs_kernels.cu)
@@ -179,6 +190,16 @@ struct KParams {
     int32_t groups;              // independent thread groups (tiles in flight) per CTA
     int32_t desc_in_smem;        // op descriptors + threshold tables copied to shared memory
     int32_t tab_len;             // threshold table entries
+    // pre-sampled fused noise (noise_kernel): per ordinal (K, 1, 0, off | PAIRS)
+    const uint4* fused;
+    unsigned long long* hits_global;  // [tiles][hit_block] entries
+    uint2* spans_global;              // [tiles][num_noise][list_warps] (begin, end) in the tile's
+                                      // block (begin NO_SLOT: the warp draws inline)
+    uint32_t* fill_global;            // [tiles] entries used (noise_kernel allocation)
+    const uint2* hit_items;           // noise_kernel items of one tile
+    int64_t hit_block;
+    int32_t list_warps;
+    int32_t n_items;
 };
 
 struct LaunchCfg {
@@ -194,6 +215,7 @@ struct LaunchCfg {
 size_t frame_smem_bytes(int num_qubits, int W);
 cudaError_t launch_frame_kernel(const LaunchCfg& cfg, const KParams& kp, cudaStream_t stream);
 cudaError_t set_frame_kernel_smem(const LaunchCfg& cfg);
+cudaError_t launch_noise_kernel(int W, const KParams& kp, int grid, cudaStream_t stream);
 cudaError_t launch_rows_to_b8(const uint32_t* rows, int64_t num_rows, int64_t row_words,
                               int64_t num_shots, const uint8_t* xor_bits, uint8_t* out,
                               int64_t pitch, cudaStream_t stream);

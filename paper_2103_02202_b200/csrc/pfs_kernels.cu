@@ -221,17 +221,43 @@ __device__ __forceinline__ void chunk_hits(const TileKey& tk, const NoiseOp& nz,
 // total above WSCR take the general path, lane by lane.  The chunk covers
 // applications [a0, a0 + na) and shots [s0, s0 + cs).  Every lane of the warp
 // must call this (shuffles).
+// Hit entry of a pre-sampled noise list (noise_kernel -> frame kernel): frame
+// rows q0 | q1 (20 bits each) | word (5) | bit (5) | x mask (2) | z mask (2)
+__device__ __forceinline__ unsigned long long make_hit(const AppRows& rr, uint32_t ch, uint32_t pick, uint32_t s) {
+    uint32_t xm, zm;
+    pattern_of(ch, pick, xm, zm);
+    return (unsigned long long)rr.r0 | ((unsigned long long)rr.r1 << 20) | ((unsigned long long)(s >> 5) << 40) |
+           ((unsigned long long)(s & 31u) << 45) | ((unsigned long long)xm << 50) | ((unsigned long long)zm << 52);
+}
+template <int W>
+__device__ __forceinline__ void apply_hit_entry(uint32_t* X, uint32_t* Z, unsigned long long e) {
+    const uint32_t q0 = (uint32_t)e & 0xFFFFFu, q1 = (uint32_t)(e >> 20) & 0xFFFFFu;
+    const uint32_t w = (uint32_t)(e >> 40) & 31u, bit = 1u << ((uint32_t)(e >> 45) & 31u);
+    const uint32_t xm = (uint32_t)(e >> 50) & 3u, zm = (uint32_t)(e >> 52) & 3u;
+    if (xm & 1u) atomicXor(X + (size_t)q0 * W + w, bit);
+    if (zm & 1u) atomicXor(Z + (size_t)q0 * W + w, bit);
+    if (xm & 2u) atomicXor(X + (size_t)q1 * W + w, bit);
+    if (zm & 2u) atomicXor(Z + (size_t)q1 * W + w, bit);
+}
+
 template <int W>
 __device__ __forceinline__ void warp_chunks(const TileKey& tk, const NoiseOp& nz, const unsigned long long* tab,
-                                            bool valid, uint32_t r, uint32_t a0, uint32_t na, uint32_t s0,
-                                            const uint32_t* tg, int ar, bool pairs, uint32_t* X, uint32_t* Z,
-                                            uint32_t* sl, uint32_t* wscr, int lane) {
+                                            unsigned long long t0, unsigned long long t1, bool valid, uint32_t r,
+                                            uint32_t a0, uint32_t na, uint32_t s0, const uint32_t* tg, int ar,
+                                            bool pairs, uint32_t* X, uint32_t* Z, uint32_t* sl, uint32_t* wscr,
+                                            int lane) {
     if (nz.zone == NZONE_NONE) return;
     const uint32_t sh = 32u - nz.lgL, msk = (1u << nz.lgcs) - 1;
     uint32_t w0 = 0, w1 = 0, w2 = 0, w3 = 0, count = 0;
     if (valid && nz.zone == NZONE_TAB) {
-        noise_block(tk, 0u, r, nz.ordinal, w0, w1, w2, w3);
-        count = chunk_count(tab + nz.tab_off, nz.tab_len, w0, w1);
+        w0 = 0u; w1 = r; w2 = tk.g; w3 = DOMAIN_NOISE | nz.ordinal;  // block 0, inline
+        philox_rounds(w0, w1, w2, w3, tk.k0, tk.k1);
+        // count = min{m : u < t[m]}: the first two thresholds come from
+        // registers (uniform per op), the rare tail from the table
+        const unsigned long long u = ((unsigned long long)w1 << 32) | w0;
+        count = (nz.tab_len > 0 && u >= t0) ? ((nz.tab_len > 1 && u >= t1) ? 2u : 1u) : 0u;
+        if (count == 2u)
+            while (count < nz.tab_len && u >= tab[nz.tab_off + count]) count++;
     }
     bool slow = valid && (nz.zone == NZONE_ALL || count > (uint32_t)NZ_MAX_LIST);
     uint32_t c = slow ? 0u : count;
@@ -258,14 +284,22 @@ __device__ __forceinline__ void warp_chunks(const TileKey& tk, const NoiseOp& nz
         }
         return (int)(lo > 31u ? 31u : lo);
     };
-    for (uint32_t j0 = 0; j0 < H; j0 += 32) {
-        const uint32_t j = j0 + (uint32_t)lane;
+    if (H <= 32u) {
+        // one hit per lane: its position, pick and frame rows are resolved in a
+        // single round (the operand loads overlap the collision check)
+        const uint32_t j = (uint32_t)lane;
         const int ow = owner_of(j);
         const uint32_t oexcl = __shfl_sync(0xFFFFFFFFu, excl, ow);
         const uint32_t orr = __shfl_sync(0xFFFFFFFFu, r, ow);
+        const uint32_t oa0 = __shfl_sync(0xFFFFFFFFu, a0, ow);
+        const uint32_t os0 = __shfl_sync(0xFFFFFFFFu, s0, ow);
+        const uint32_t ovl = __shfl_sync(0xFFFFFFFFu, na, ow) << nz.lgcs;
         uint32_t x = __shfl_sync(0xFFFFFFFFu, w2, ow);
         uint32_t y = __shfl_sync(0xFFFFFFFFu, w3, ow);
-        if (j < H) {
+        uint32_t pos = 0, pick = 0;
+        AppRows rr{0u, 0u};
+        const bool mine = j < H;
+        if (mine) {
             const uint32_t h = j - oexcl;
             if (h > 0) {
                 uint32_t b0, b1, b2, b3;
@@ -273,24 +307,59 @@ __device__ __forceinline__ void warp_chunks(const TileKey& tk, const NoiseOp& nz
                 x = (h & 1u) ? b0 : b2;
                 y = (h & 1u) ? b1 : b3;
             }
-            wscr[j] = ((nz.lgL ? (x >> sh) : 0u) << 4) | (nz.npat > 1 ? __umulhi(y, nz.npat) : 0u);
+            pos = nz.lgL ? (x >> sh) : 0u;
+            pick = nz.npat > 1 ? __umulhi(y, nz.npat) : 0u;
+            wscr[j] = pos;
+            if (pos < ovl) rr = app_rows(tg, oa0 + (pos >> nz.lgcs), ar, pairs);
         }
-    }
-    __syncwarp();
-    for (uint32_t h = 1; h < c; h++)  // positions of one chunk must be distinct
-        for (uint32_t q = 0; q < h; q++) slow |= (wscr[excl + h] >> 4) == (wscr[excl + q] >> 4);
-    const uint32_t slowm = __ballot_sync(0xFFFFFFFFu, slow);
-    for (uint32_t j0 = 0; j0 < H; j0 += 32) {
-        const uint32_t j = j0 + (uint32_t)lane;
-        const int ow = owner_of(j);
-        const uint32_t oa0 = __shfl_sync(0xFFFFFFFFu, a0, ow);
-        const uint32_t os0 = __shfl_sync(0xFFFFFFFFu, s0, ow);
-        const uint32_t ovl = __shfl_sync(0xFFFFFFFFu, na, ow) << nz.lgcs;
-        if (j < H && !((slowm >> ow) & 1u)) {
-            const uint32_t e = wscr[j], pos = e >> 4;
-            if (pos < ovl)
-                xor_pauli<W, true>(X, Z, app_rows(tg, oa0 + (pos >> nz.lgcs), ar, pairs), ar, nz.ch, e & 15u,
-                                   os0 + (pos & msk));
+        // positions of one chunk must be distinct: two hits compare by
+        // shuffle, more through the scratch
+        const uint32_t p0 = __shfl_sync(0xFFFFFFFFu, pos, (int)(excl & 31u));
+        const uint32_t p1 = __shfl_sync(0xFFFFFFFFu, pos, (int)((excl + 1) & 31u));
+        if (c == 2) slow |= p0 == p1;
+        if (__any_sync(0xFFFFFFFFu, c > 2)) {
+            __syncwarp();
+            for (uint32_t h = 1; h < c; h++)
+                for (uint32_t q = 0; q < h; q++) slow |= wscr[excl + h] == wscr[excl + q];
+        }
+        const uint32_t slowm = __ballot_sync(0xFFFFFFFFu, slow);
+        if (mine && pos < ovl && !((slowm >> ow) & 1u))
+            xor_pauli<W, true>(X, Z, rr, ar, nz.ch, pick, os0 + (pos & msk));
+    } else {
+        for (uint32_t j0 = 0; j0 < H; j0 += 32) {
+            const uint32_t j = j0 + (uint32_t)lane;
+            const int ow = owner_of(j);
+            const uint32_t oexcl = __shfl_sync(0xFFFFFFFFu, excl, ow);
+            const uint32_t orr = __shfl_sync(0xFFFFFFFFu, r, ow);
+            uint32_t x = __shfl_sync(0xFFFFFFFFu, w2, ow);
+            uint32_t y = __shfl_sync(0xFFFFFFFFu, w3, ow);
+            if (j < H) {
+                const uint32_t h = j - oexcl;
+                if (h > 0) {
+                    uint32_t b0, b1, b2, b3;
+                    noise_block(tk, (h + 1) >> 1, orr, nz.ordinal, b0, b1, b2, b3);
+                    x = (h & 1u) ? b0 : b2;
+                    y = (h & 1u) ? b1 : b3;
+                }
+                wscr[j] = ((nz.lgL ? (x >> sh) : 0u) << 4) | (nz.npat > 1 ? __umulhi(y, nz.npat) : 0u);
+            }
+        }
+        __syncwarp();
+        for (uint32_t h = 1; h < c; h++)  // positions of one chunk must be distinct
+            for (uint32_t q = 0; q < h; q++) slow |= (wscr[excl + h] >> 4) == (wscr[excl + q] >> 4);
+        const uint32_t slowm = __ballot_sync(0xFFFFFFFFu, slow);
+        for (uint32_t j0 = 0; j0 < H; j0 += 32) {
+            const uint32_t j = j0 + (uint32_t)lane;
+            const int ow = owner_of(j);
+            const uint32_t oa0 = __shfl_sync(0xFFFFFFFFu, a0, ow);
+            const uint32_t os0 = __shfl_sync(0xFFFFFFFFu, s0, ow);
+            const uint32_t ovl = __shfl_sync(0xFFFFFFFFu, na, ow) << nz.lgcs;
+            if (j < H && !((slowm >> ow) & 1u)) {
+                const uint32_t e = wscr[j], pos = e >> 4;
+                if (pos < ovl)
+                    xor_pauli<W, true>(X, Z, app_rows(tg, oa0 + (pos >> nz.lgcs), ar, pairs), ar, nz.ch, e & 15u,
+                                       os0 + (pos & msk));
+            }
         }
     }
     if (slow) chunk_hits_slow<W, true>(tk, nz, tab, r, a0, na, s0, tg, ar, pairs, X, Z, sl);
@@ -338,15 +407,51 @@ __device__ __forceinline__ void warp_range_noise(const KParams& kp, const TileKe
     const uint32_t per_k = (uint32_t)C * m;         // chunks per application block
     const uint32_t k0 = A0 >> lgca;
     const uint32_t nch = ((A1 - A0 + (1u << lgca) - 1) >> lgca) * per_k;
+    const unsigned long long t0 = nz.tab_len > 0 ? tab[nz.tab_off] : ~0ull;
+    const unsigned long long t1 = nz.tab_len > 1 ? tab[nz.tab_off + 1] : ~0ull;
     for (uint32_t q0 = 0; q0 < nch; q0 += 32) {
         const uint32_t q = q0 + (uint32_t)lane;
         const bool valid = q < nch;
         const uint32_t k = k0 + q / per_k, rem = q % per_k;
         const uint32_t c = rem / m, u = rem - c * m;
         const uint32_t a0 = k << lgca;
-        warp_chunks<W>(tk, nz, tab, valid, k * nS + c * m + u, a0, valid ? min(1u << lgca, count - a0) : 0u,
+        warp_chunks<W>(tk, nz, tab, t0, t1, valid, k * nS + c * m + u, a0, valid ? min(1u << lgca, count - a0) : 0u,
                        c * S + u * cs, tg, ar, pairs, X, Z, sl, wscr, lane);
     }
+}
+
+// Where noise_kernel left warp `w`'s hits of fused op `ordinal` in tile
+// `tile`: its (begin, end) span in the tile's block (nullptr: not pre-sampled)
+__device__ __forceinline__ const uint2* hit_span(const KParams& kp, uint32_t ordinal, int64_t tile, int tid) {
+    if (kp.hits_global == nullptr || __ldg(&kp.fused[ordinal].y) == 0u) return nullptr;
+    return kp.spans_global + (tile * kp.num_noise + ordinal) * kp.list_warps + ((uint32_t)tid >> 5);
+}
+
+// Op start: pull the warp's span toward L1 (no registers held across the op's
+// frame work)
+__device__ __forceinline__ void prefetch_span(const KParams& kp, uint32_t ordinal, int64_t tile, int tid) {
+    const uint2* sp = hit_span(kp, ordinal, tile, tid);
+    if (sp != nullptr && (tid & 31) == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
+}
+
+// The fused noise of a warp's range [A0, A1): its pre-sampled hits when
+// noise_kernel wrote them (span begin != NO_SLOT), else drawn here
+template <int W>
+__device__ __forceinline__ void range_noise(const KParams& kp, const TileKey& tk, const NoiseOp& nz,
+                                            const unsigned long long* tab, uint32_t count, uint32_t A0, uint32_t A1,
+                                            const uint32_t* tg, int ar, bool pairs, uint32_t* X, uint32_t* Z,
+                                            uint32_t* sl, uint32_t* wscr, int lane, uint32_t rowb, int64_t tile,
+                                            int tid) {
+    const uint2* sp = kp.masks == nullptr ? hit_span(kp, nz.ordinal, tile, tid) : nullptr;
+    const uint2 span = sp != nullptr ? __ldg(sp) : make_uint2(NO_SLOT, 0u);
+    if (span.x == NO_SLOT) {
+        warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, ar, pairs, X, Z, sl, wscr, lane, rowb, tile);
+        return;
+    }
+    const unsigned long long* hits = kp.hits_global + tile * kp.hit_block;
+    __syncwarp();  // the warp's row updates are visible to the lanes applying hits
+    for (uint32_t j = span.x + (uint32_t)lane; j < span.y; j += 32) apply_hit_entry<W>(X, Z, __ldg(hits + j));
+    __syncwarp();
 }
 
 // The application range of a warp in a fused op: ceil(count / warps), rounded
@@ -437,7 +542,7 @@ __device__ __forceinline__ void gate_fused(const KParams& kp, const TileKey& tk,
             if (code != R_CX) vst<V>(Z + p1, z1);
         });
     }
-    warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, ar, false, X, Z, sl, wscr, lane, rowb, tile);
+    range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, ar, false, X, Z, sl, wscr, lane, rowb, tile, tid);
 }
 
 // M / R / MR (+ fused noise: after a reset, before a measurement).  With
@@ -462,7 +567,8 @@ __device__ __forceinline__ void collapse_op(const KParams& kp, const TileKey& tk
         first = lane;
         stride = 32;
         // the fused noise precedes a measurement (X_ERROR before M)
-        if (kind != K_R) warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile);
+        if (kind != K_R)
+            range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile, tid);
     }
     const uint2* const tp = reinterpret_cast<const uint2*>(tg);  // (row | COIN_DEAD, slot)
     batched_items<4>(first, stride, (int)((A1 - A0) << LC), [&](int i) { return tp[A0 + (i >> LC)]; },
@@ -489,7 +595,8 @@ __device__ __forceinline__ void collapse_op(const KParams& kp, const TileKey& tk
             vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + 2 * app + 1, c, tile) : vzero<V>());
         }
     });
-    if (fz && kind == K_R) warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile);
+    if (fz && kind == K_R)
+        range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile, tid);
 }
 
 // A standalone noise instruction: one chunk per lane, warp-cooperative draws,
@@ -528,14 +635,167 @@ __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, u
     const uint32_t lgca = nz.lgL - nz.lgcs;
     const uint32_t nS = (32u * W) >> nz.lgcs;
     const uint32_t nch = ((count + (1u << lgca) - 1) >> lgca) * nS;
+    const unsigned long long t0 = nz.tab_len > 0 ? tab[nz.tab_off] : ~0ull;
+    const unsigned long long t1 = nz.tab_len > 1 ? tab[nz.tab_off + 1] : ~0ull;
     for (uint32_t rb = (uint32_t)(tid - lane); rb < nch; rb += nth) {
         const uint32_t r = rb + (uint32_t)lane;
         const bool valid = r < nch;
         const uint32_t k = r / nS, cc = r - k * nS;
         const uint32_t a0 = k << lgca;
-        warp_chunks<W>(tk, nz, tab, valid, r, a0, valid ? min(1u << lgca, count - a0) : 0u, cc << nz.lgcs, tg, ar,
-                       false, X, Z, sl, wscr, lane);
+        warp_chunks<W>(tk, nz, tab, t0, t1, valid, r, a0, valid ? min(1u << lgca, count - a0) : 0u, cc << nz.lgcs,
+                       tg, ar, false, X, Z, sl, wscr, lane);
     }
+}
+
+// ------------------------------------------------------------ noise kernel
+// Pre-samples the fused noise of a launch's tiles (DESIGN.md §4 draws, exactly
+// the ones the frame kernel would make inline).  Work item = (tile, fused op,
+// consumer warps [wb, we) of the frame kernel): a warp walks the chunks of
+// those warps' applications, one chunk per lane per pass (Binomial count from
+// block 0, positions from the pairs, distinctness by redraw, the general path
+// for long chunks), stages the resolved hit entries (tagged with the consumer
+// warp) in shared memory, allocates room in the tile's block with one global
+// atomic, and scatters them into one contiguous span per consumer warp.  An
+// item whose hits do not fit leaves its warps to draw inline.
+template <int W>
+__global__ void __launch_bounds__(NK_WARPS * 32, 4) noise_kernel(const __grid_constant__ KParams kp) {
+    constexpr int V = W >= 4 ? 4 : W;
+    constexpr int C = W / V;
+    constexpr uint32_t S = 32u * V;
+    __shared__ unsigned long long ent_all[NK_WARPS][NK_SCR];
+    __shared__ uint32_t sl_all[NK_WARPS * 32][NZ_MAX_LIST];
+    __shared__ uint32_t wc_all[NK_WARPS][2][16];
+    __shared__ uint32_t wn_all[NK_WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    unsigned long long* const ent = ent_all[warp];
+    uint32_t* const sl = sl_all[threadIdx.x];
+    uint32_t* const wcnt = wc_all[warp][0];
+    uint32_t* const wfill = wc_all[warp][1];
+    uint32_t* const wn = &wn_all[warp];
+    const int64_t items = kp.n_tiles * (int64_t)kp.n_items;
+    for (int64_t it = (int64_t)blockIdx.x * NK_WARPS + warp; it < items; it += (int64_t)gridDim.x * NK_WARPS) {
+        const int64_t tile = it / kp.n_items;
+        const uint2 item = __ldg(kp.hit_items + (it - tile * kp.n_items));
+        const uint32_t o = item.x, wb = item.y & 0xFFFFu, we = item.y >> 16;
+        const uint4 fi = __ldg(kp.fused + o);
+        const NoiseParam np = kp.noise[o];
+        const NoiseOp nz = noise_op_of(np, o);
+        const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
+        const uint32_t K = fi.x;
+        const uint32_t A0 = min(np.apps, wb * K), A1 = min(np.apps, we * K);
+        const bool pairs = (fi.w & FUSED_PAIRS) != 0;
+        const uint32_t* tg = kp.targets + (fi.w & ~FUSED_PAIRS);
+        const int ar = np.ch == CH_DEP2 ? 2 : 1;
+        if (lane < 16) { wcnt[lane] = 0u; wfill[lane] = 0u; }
+        if (lane == 0) *wn = 0u;
+        __syncwarp();
+        bool over = false;
+        if (A0 < A1) {
+            const unsigned long long* tab = kp.noise_tab + nz.tab_off;
+            const unsigned long long t0 = nz.tab_len > 0 ? tab[0] : ~0ull;
+            const unsigned long long t1 = nz.tab_len > 1 ? tab[1] : ~0ull;
+            const uint32_t lgca = nz.lgL - nz.lgcs, cs = 1u << nz.lgcs, msk = cs - 1u;
+            const uint32_t nS = (32u * W) >> nz.lgcs;
+            const uint32_t m = cs >= S ? 1u : S / cs;
+            const uint32_t per_k = (uint32_t)C * m;
+            const uint32_t k0 = A0 >> lgca;
+            const uint32_t nch = ((A1 - A0 + (1u << lgca) - 1) >> lgca) * per_k;
+            const uint32_t sh = 32u - nz.lgL;
+            for (uint32_t q0 = 0; q0 < nch; q0 += 32) {
+                const uint32_t q = q0 + (uint32_t)lane;
+                if (q < nch) {
+                    const uint32_t k = k0 + q / per_k, rem = q % per_k;
+                    const uint32_t c = rem / m, u = rem - c * m;
+                    const uint32_t r = k * nS + c * m + u;
+                    const uint32_t a0 = k << lgca;
+                    const uint32_t vl = min(1u << lgca, np.apps - a0) << nz.lgcs;
+                    const uint32_t s0 = c * S + u * cs;
+                    const uint32_t wl = a0 / K - wb;  // consumer warp (item-local)
+                    uint32_t w0 = 0u, w1 = r, w2 = tk.g, w3 = DOMAIN_NOISE | nz.ordinal;  // block 0
+                    philox_rounds(w0, w1, w2, w3, tk.k0, tk.k1);
+                    const unsigned long long uu = ((unsigned long long)w1 << 32) | w0;
+                    uint32_t cnt = (nz.tab_len > 0 && uu >= t0) ? ((nz.tab_len > 1 && uu >= t1) ? 2u : 1u) : 0u;
+                    if (cnt == 2u)
+                        while (cnt < nz.tab_len && uu >= tab[cnt]) cnt++;
+                    auto put = [&](uint32_t pos, uint32_t pick) {
+                        const uint32_t slot = atomicAdd(wn, 1u);
+                        if (slot < (uint32_t)NK_SCR) {
+                            ent[slot] = make_hit(app_rows(tg, a0 + (pos >> nz.lgcs), ar, pairs), nz.ch, pick,
+                                                 s0 + (pos & msk)) |
+                                        ((unsigned long long)wl << 56);
+                            atomicAdd(&wcnt[wl], 1u);
+                        }
+                    };
+                    bool general = cnt > (uint32_t)NZ_MAX_LIST;
+                    if (cnt > 0u && !general) {
+                        // attempt 0: hit h takes pair h (block (h + 1) >> 1)
+                        uint32_t b0 = 0, b1 = 0, b2 = w2, b3 = w3;
+                        bool dup = false;
+                        for (uint32_t h = 0; h < cnt; h++) {
+                            if (h > 0 && (h & 1u)) noise_block(tk, (h + 1) >> 1, r, nz.ordinal, b0, b1, b2, b3);
+                            const uint32_t x = (h & 1u) ? b0 : b2, y = (h & 1u) ? b1 : b3;
+                            const uint32_t pos = nz.lgL ? (x >> sh) : 0u;
+                            for (uint32_t j = 0; j < h; j++) dup |= (sl[j] >> 4) == pos;
+                            sl[h] = (pos << 4) | (nz.npat > 1 ? __umulhi(y, nz.npat) : 0u);
+                        }
+                        if (dup) general = true;
+                        else
+                            for (uint32_t h = 0; h < cnt; h++) {
+                                const uint32_t e = sl[h];
+                                if ((e >> 4) < vl) put(e >> 4, e & 15u);
+                            }
+                    }
+                    if (general)  // redraws / selection sampling: the reference path
+                        noise_chunk(tk, nz, kp.noise_tab, r, vl, sl, put);
+                }
+            }
+            __syncwarp();
+            over = *wn > (uint32_t)NK_SCR;
+        }
+        const uint32_t n = over ? 0u : *wn;
+        uint2* spans = kp.spans_global + (tile * kp.num_noise + o) * kp.list_warps;
+        uint32_t base = 0u;
+        if (lane == 0 && !over && n > 0u) base = atomicAdd(kp.fill_global + tile, n);
+        base = __shfl_sync(0xFFFFFFFFu, base, 0);
+        over |= (int64_t)base + n > kp.hit_block;
+        // consumer warp spans: exclusive prefix of the per-warp counts
+        const uint32_t nwl = we - wb;
+        uint32_t v = (uint32_t)lane < nwl ? wcnt[lane] : 0u, pre = v;
+#pragma unroll
+        for (int d = 1; d < 16; d <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+            if (lane >= d) pre += t;
+        }
+        if ((uint32_t)lane < nwl) {
+            const uint32_t beg = base + pre - v;
+            spans[wb + lane] = over ? make_uint2(NO_SLOT, 0u) : make_uint2(beg, beg + v);
+            wfill[lane] = beg;
+        }
+        __syncwarp();
+        if (!over) {
+            unsigned long long* hits = kp.hits_global + tile * kp.hit_block;
+            for (uint32_t i = (uint32_t)lane; i < n; i += 32) {
+                const unsigned long long e = ent[i];
+                const uint32_t slot = atomicAdd(&wfill[(uint32_t)(e >> 56) & 15u], 1u);
+                hits[slot] = e & ((1ull << 56) - 1);
+            }
+        }
+        __syncwarp();  // staging reused by the next item
+    }
+}
+
+cudaError_t launch_noise_kernel(int W, const KParams& kp, int grid, cudaStream_t st) {
+    if (kp.n_tiles <= 0 || kp.n_items <= 0) return cudaSuccess;
+    switch (W) {
+        case 1: noise_kernel<1><<<grid, NK_WARPS * 32, 0, st>>>(kp); break;
+        case 2: noise_kernel<2><<<grid, NK_WARPS * 32, 0, st>>>(kp); break;
+        case 4: noise_kernel<4><<<grid, NK_WARPS * 32, 0, st>>>(kp); break;
+        case 8: noise_kernel<8><<<grid, NK_WARPS * 32, 0, st>>>(kp); break;
+        case 16: noise_kernel<16><<<grid, NK_WARPS * 32, 0, st>>>(kp); break;
+        case 32: noise_kernel<32><<<grid, NK_WARPS * 32, 0, st>>>(kp); break;
+        default: return cudaErrorInvalidValue;
+    }
+    return cudaGetLastError();
 }
 
 // ------------------------------------------------------------ frame kernel
@@ -657,11 +917,13 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             const bool fz = (flags & F_NOISE) != 0;
             const NoiseOp nz = decode_noise(h1.y, h1.z, h1.w);
             const uint32_t rowb = (injected && (fz || kind == K_NOISE)) ? __ldg(kp.noise_rowb + nz.ordinal) : 0u;
+            if (fz && !injected) prefetch_span(kp, nz.ordinal, tile, tid);
 
             switch (kind) {
             case K_GATE: {
                 if (fz) {
-                    gate_fused<W>(kp, tk, X, Z, tg, kp.targets + oa, ob, code, count, nz, rowb, tab, sl, wscr, tid, nth, tile);
+                    gate_fused<W>(kp, tk, X, Z, tg, kp.targets + oa, ob, code, count, nz, rowb, tab, sl, wscr, tid, nth,
+                                  tile);
                     break;
                 }
                 switch (code) {
