@@ -59,12 +59,14 @@ struct Flavour {
     LaunchCfg cfg{};
     bool desc_smem = false;
     DevBuf<DOp> ops;
+    DevBuf<SOp> sops;
+    DevBuf<uint32_t> arena;
     DevBuf<uint32_t> targets, det_ptr, det_terms, ring, init_dead, row_of, noise_ch, noise_rowb;
     DevBuf<NoiseParam> noise;
     DevBuf<unsigned long long> noise_tab;
     DevBuf<uint32_t> fused, hit_items;  // pre-sampled fused noise (noise_kernel)
     void release() {
-        ops.release(); targets.release(); det_ptr.release(); det_terms.release(); ring.release();
+        ops.release(); sops.release(); arena.release(); targets.release(); det_ptr.release(); det_terms.release(); ring.release();
         init_dead.release(); row_of.release(); noise_ch.release(); noise_rowb.release();
         noise.release(); noise_tab.release(); fused.release(); hit_items.release();
     }
@@ -119,13 +121,13 @@ constexpr double kFusedHits = 1.0;       // mean hits per fused noise chunk (one
 constexpr int64_t kHitBufBytes = (int64_t)256 << 20;  // hit lists of one sub-chunk of tiles
 
 static bool desc_fits(const HostProgram& hp) {
-    return hp.ops.size() * sizeof(DOp) + hp.noise_tab.size() * 8 <= (size_t)DESC_SMEM_MAX;
+    return hp.ops.size() * sizeof(SOp) + hp.noise_tab.size() * 8 <= (size_t)DESC_SMEM_MAX;
 }
 
 // per-warp noise scratch, descriptors + threshold tables (when they fit), alignment slack
 static size_t fixed_smem(const HostProgram& hp) {
     return 16 + (size_t)(FRAME_MAX_THREADS / 32) * WSCR * 4 +
-           (desc_fits(hp) ? hp.ops.size() * sizeof(DOp) + hp.noise_tab.size() * 8 : 0);
+           (desc_fits(hp) ? hp.ops.size() * sizeof(SOp) + hp.noise_tab.size() * 8 : 0);
 }
 
 // Outputs of the kernels that write final layouts directly (dem_kernel).
@@ -286,14 +288,13 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         for (int m = 0; m < (dem ? 1 : 2); m++) {
             HostProgram& hp = pg->fl[m].hp;
             permute_rows(hp);
-            reorder_for_banks(hp, W);
             dedup_operands(hp);
             // the error-model kernel's chunks span whole 32-shot tiles
             build_noise_schedule(hp, 32 * W, dem ? 32 : 32 * V, th, dem ? th : thf);
             if (!dem) {
                 const int wpg = cfg.threads / std::max(1, cfg.groups) / 32;
-                bank_order_fused(hp, W, wpg);
                 if (pg->opts.presample_noise >= 0) build_hit_lists(hp, 32 * W, wpg);
+                lower_stream(hp, W, wpg);
             }
             Flavour& f = pg->fl[m];
             if (m == PM_RECORDS) f.cfg = cfg, f.cfg.ring_smem = true;
@@ -426,6 +427,8 @@ static int ensure_device(pfs_program* pg, int device) {
             return fail(PFS_E_INVALID, "frame tile exceeds this device's shared memory");
         const HostProgram& hp = f.hp;
         CUDA_TRY(upload(f.ops, hp.ops));
+        CUDA_TRY(upload(f.sops, hp.sops));
+        CUDA_TRY(upload(f.arena, hp.arena));
         CUDA_TRY(upload(f.targets, hp.targets));
         CUDA_TRY(upload(f.det_ptr, hp.det_ptr));
         CUDA_TRY(upload(f.det_terms, hp.det_terms));
@@ -703,6 +706,9 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
 
     KParams kp{};
     kp.ops = fl.ops.p;
+    kp.sops = fl.sops.p;
+    kp.arena = fl.arena.p;
+    kp.first_span = hp.first_span;
     kp.targets = fl.targets.p;
     kp.det_ptr = fl.det_ptr.p;
     kp.det_terms = fl.det_terms.p;

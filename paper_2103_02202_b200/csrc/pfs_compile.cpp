@@ -692,54 +692,104 @@ static void bank_reorder(uint32_t* tg, uint32_t A, int ar, int G, std::vector<ui
 
 static int bank_groups(int W) { return W >= 32 ? 1 : 128 / (W * 4); }
 
-// Reorder the applications of every unfused gate op for distinct bank groups
-// (apps of one op are independent by construction, so any order is the same
-// circuit).  A fused op keeps its noise instruction's application order — it
-// defines the noise trials; see bank_order_fused.
-void reorder_for_banks(HostProgram& hp, int W) {
-    const int G = bank_groups(W);
-    if (G <= 1) return;
-    std::vector<uint32_t> scratch;
-    for (DOp& o : hp.ops) {
-        if ((o.kcf & 0xFF) != K_GATE || o.count < 2 || ((o.kcf >> 16) & F_NOISE)) continue;
-        bank_reorder(hp.targets.data() + o.off, o.count, rule_arity((o.kcf >> 8) & 0xFF), G, scratch);
-    }
+// Applications per warp of a group for an op of `apps` applications: an even
+// split rounded up to whole noise chunks (ca applications), so every chunk of
+// a fused noise instruction has one owner warp.
+static uint32_t warp_share(uint32_t apps, uint32_t nw, uint32_t ca) {
+    ca = std::max<uint32_t>(1u, ca);
+    return ((apps + nw - 1) / nw + ca - 1) / ca * ca;
 }
 
-// Fused gate ops: the kernel gives each warp of a group a chunk-aligned range
-// of K applications (noise chunks of ca applications); the
-// warp's gate work may visit its range in any order, so a bank-ordered copy of
-// each range's targets is appended (op.a = its offset, op.b = K) while the
-// noise draws keep addressing the instruction order at op.off.
-void bank_order_fused(HostProgram& hp, int W, int warps_per_group) {
-    const int G = bank_groups(W);
+// Stream form of the device ops for tiles of W words run by groups of
+// `warps_per_group` warps (SOp, pfs_internal.h).  Every gate op becomes one
+// block of packed operand words per warp: the warp's (chunk-aligned) range of
+// applications in bank order, padded to whole warp passes, so the kernel's
+// item loop is a coalesced word load, two shifts and the row work.  Collapses,
+// detectors and observables get a copy of their operand lists; identical
+// blocks (the rounds of a REPEAT body) are stored once.
+void lower_stream(HostProgram& hp, int W, int warps_per_group) {
+    const int V = W >= 4 ? 4 : W, C = W / V;
+    const uint32_t PI = 32u / (uint32_t)C;  // applications per warp pass
     const uint32_t nw = (uint32_t)std::max(1, warps_per_group);
-    std::vector<uint32_t> scratch, copy;
-    std::unordered_map<uint64_t, std::vector<uint32_t>> seen;
-    for (DOp& o : hp.ops) {
-        if ((o.kcf & 0xFF) != K_GATE || !((o.kcf >> 16) & F_NOISE)) continue;
-        const int ar = rule_arity((o.kcf >> 8) & 0xFF);
-        const uint32_t ca = std::max<uint32_t>(1u, hp.noise[o.c].ca);
-        const uint32_t K = ((o.count + nw - 1) / nw + ca - 1) / ca * ca;
-        copy.assign(hp.targets.begin() + o.off, hp.targets.begin() + o.off + (size_t)o.count * ar);
-        for (uint32_t a0 = 0; a0 < o.count; a0 += K)
-            bank_reorder(copy.data() + (size_t)a0 * ar, std::min(K, o.count - a0), ar, G, scratch);
-        // rounds of a REPEAT body produce identical copies: share them
-        uint64_t h = 1469598103934665603ull ^ copy.size();
-        for (uint32_t v : copy) { h ^= v; h *= 1099511628211ull; }
+    const int G = bank_groups(W);
+    if (hp.num_qubits >= 65536) bad("frame rows exceed the 16-bit operand format");
+    hp.sops.assign(hp.ops.size(), SOp{});
+    hp.arena.clear();
+    hp.first_span = NO_SLOT;
+    std::unordered_map<uint64_t, std::vector<std::pair<uint32_t, uint32_t>>> seen;
+    auto add_block = [&](const std::vector<uint32_t>& blk) -> uint32_t {
+        if (blk.empty()) return 0u;
+        uint64_t h = 1469598103934665603ull ^ blk.size();
+        for (uint32_t v : blk) { h ^= v; h *= 1099511628211ull; }
         auto& lst = seen[h];
-        uint32_t where = NO_SLOT;
-        for (uint32_t cand : lst)
-            if (std::equal(copy.begin(), copy.end(), hp.targets.begin() + cand)) { where = cand; break; }
-        if (where == NO_SLOT) {
-            if (hp.targets.size() & 1) hp.targets.push_back(0u);
-            where = (uint32_t)hp.targets.size();
-            hp.targets.insert(hp.targets.end(), copy.begin(), copy.end());
-            lst.push_back(where);
+        for (auto& c : lst)
+            if (c.second == blk.size() && std::equal(blk.begin(), blk.end(), hp.arena.begin() + c.first)) return c.first;
+        while (hp.arena.size() & 31) hp.arena.push_back(STREAM_NOP);  // 128-byte aligned blocks
+        const uint32_t where = (uint32_t)hp.arena.size();
+        hp.arena.insert(hp.arena.end(), blk.begin(), blk.end());
+        lst.emplace_back(where, (uint32_t)blk.size());
+        return where;
+    };
+    std::vector<uint32_t> blk, range, scratch;
+    for (size_t i = 0; i < hp.ops.size(); i++) {
+        const DOp& o = hp.ops[i];
+        SOp& s = hp.sops[i];
+        const uint32_t kind = o.kcf & 0xFF, code = (o.kcf >> 8) & 0xFF, flags = o.kcf >> 16;
+        s.kcf = o.kcf;
+        s.count = o.count;
+        s.a = o.a;
+        s.b = o.b;
+        s.span = s.next_span = NO_SLOT;
+        s.ordinal = (kind == K_NOISE || (flags & F_NOISE)) ? o.c : NO_SLOT;
+        const bool fz = (flags & F_NOISE) != 0;
+        const uint32_t ca = fz ? hp.noise[o.c].ca : 1u;
+        if (fz && !hp.fused_info.empty() && hp.fused_info[(size_t)o.c * 4 + 1] == 1u) {
+            s.kcf |= F_PRESAMPLED << 16;
+            s.span = o.c * (uint32_t)hp.list_warps;
         }
-        o.a = where;
-        o.b = K;
+        blk.clear();
+        switch (kind) {
+        case K_GATE: {
+            const int ar = rule_arity(code);
+            const uint32_t Kc = warp_share(o.count, nw, ca);
+            const uint32_t passes = (Kc + PI - 1) / PI;
+            blk.assign((size_t)nw * passes * PI, STREAM_NOP);
+            for (uint32_t w = 0; w < nw; w++) {
+                const uint32_t A0 = std::min(o.count, w * Kc), A1 = std::min(o.count, A0 + Kc);
+                if (A0 >= A1) continue;
+                range.assign(hp.targets.begin() + o.off + (size_t)A0 * ar, hp.targets.begin() + o.off + (size_t)A1 * ar);
+                bank_reorder(range.data(), A1 - A0, ar, G, scratch);
+                for (uint32_t j = 0; j < A1 - A0; j++)
+                    blk[(size_t)w * passes * PI + j] = range[(size_t)j * ar] | (ar == 2 ? range[(size_t)j * ar + 1] << 16 : 0u);
+            }
+            s.K = passes;
+            s.r0 = Kc;
+            break;
+        }
+        case K_M: case K_MR: case K_R: case K_SPILL:
+            blk.assign(hp.targets.begin() + o.off, hp.targets.begin() + o.off + 2 * (size_t)o.count);
+            s.K = warp_share(o.count, nw, ca);
+            break;
+        case K_DET:
+            if (code) blk.assign(hp.det_terms.begin() + o.off, hp.det_terms.begin() + o.off + (size_t)o.count * code);
+            break;
+        case K_OBS:
+            blk.assign(hp.targets.begin() + o.off, hp.targets.begin() + o.off + o.count);
+            break;
+        default: break;  // standalone noise reads its DOp
+        }
+        s.off = blk.empty() ? o.off : add_block(blk);
+        s.pf_words = (uint32_t)blk.size();
     }
+    uint32_t next = NO_SLOT;
+    for (size_t i = hp.sops.size(); i-- > 0;) {
+        SOp& s = hp.sops[i];
+        if (!((s.kcf >> 16) & F_PRESAMPLED)) continue;
+        s.next_span = next == NO_SLOT ? s.span : next;
+        next = s.span;
+    }
+    hp.first_span = next;
+    if (hp.arena.size() >= (1ull << 31)) bad("operand arena too large");
 }
 
 // Pre-sampled fused noise (noise_kernel): a fused op's consumer warp w owns
@@ -758,8 +808,7 @@ void build_hit_lists(HostProgram& hp, int tile_shots, int warps_per_group) {
         if (!((o.kcf >> 16) & F_NOISE) || o.c == NO_SLOT) continue;
         const NoiseParam& np = hp.noise[o.c];
         if (np.zone != NZONE_TAB) continue;  // p == 0 / p == 1: drawn by the consumer
-        const uint32_t ca = std::max<uint32_t>(1u, np.ca);
-        const uint32_t K = ((np.apps + nw - 1) / nw + ca - 1) / ca * ca;
+        const uint32_t K = warp_share(np.apps, nw, np.ca);
         const double p = hp.noise_p[o.c];
         // consumer warps per noise_kernel item: as many as keep the item's hits
         // (mean + 6 sigma + slack) within one warp's staging buffer

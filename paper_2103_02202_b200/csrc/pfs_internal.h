@@ -21,6 +21,7 @@ enum Channel : uint32_t { CH_XERR = 0, CH_YERR = 1, CH_ZERR = 2, CH_DEP1 = 3, CH
 constexpr uint32_t F_BARRIER = 1u;   // group barrier before this op
 constexpr uint32_t F_DUP = 2u;       // noise op with repeated targets
 constexpr uint32_t F_NOISE = 4u;     // fused noise (after a gate / reset, before a measurement)
+constexpr uint32_t F_PRESAMPLED = 8u;  // stream op: the fused noise comes from noise_kernel's hit lists
 constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
 constexpr uint32_t COIN_DEAD = 0x80000000u;  // M/MR/R target word: the op's coin row reaches no output
 constexpr uint32_t XROW = 0x80000000u;       // DET/OBS term: the record is the x row of this frame row
@@ -41,7 +42,7 @@ constexpr int WSCR = 64;             // per-warp shared scratch of the warp-coop
 #endif
 constexpr int FRAME_MAX_THREADS = PFS_FRAME_MAX_THREADS;
 constexpr int KERNEL_COOP = 1;
-// op descriptors (+ threshold tables) are copied to shared memory when they take at most this much
+// stream ops (+ threshold tables) are copied to shared memory when they take at most this much
 constexpr int DESC_SMEM_MAX = 24576;
 
 // Program flavours: detection events (DETECTORS / COUNTS / DETECTORS_ROWS) keep
@@ -75,6 +76,33 @@ struct DOp {
     uint32_t e;
 };
 static_assert(sizeof(DOp) == 32, "DOp is 32 bytes");
+
+// Stream op (48 bytes): what frame_kernel reads per op (lower_stream, DESIGN.md
+// §3).  Same index as the DOp it was lowered from (the rare general paths —
+// inline noise draws, injected masks, CSR detectors — read the DOp).
+//   GATE : arena[off ..]: one block of K * PI words per warp of the group
+//          (PI = applications per warp pass = 32 / vectors per row); word =
+//          row of target 0 | row of target 1 << 16, bank-ordered within the
+//          warp's application range, STREAM_NOP padding
+//   M / MR / R / SPILL: arena[off ..] = the (row | COIN_DEAD, slot) pairs; warp w
+//          owns targets [w K, w K + K)
+//   DET  : code = k > 0: arena[off + k i ..] = the k terms of column a + i
+//   OBS  : arena[off ..] = terms
+struct SOp {
+    uint32_t kcf;        // kind | code << 8 | flags << 16 (DOp flags + F_PRESAMPLED)
+    uint32_t count;
+    uint32_t off;        // operand block in the arena (words)
+    uint32_t K;          // GATE: passes per warp; collapses: targets per warp
+    uint32_t a, b;       // as in DOp (first record / column / accumulator, first coin row)
+    uint32_t span;       // F_PRESAMPLED: ordinal * list_warps (index of warp 0's span)
+    uint32_t next_span;  // span index of the next F_PRESAMPLED op (this op's when it is the last)
+    uint32_t pf_words;   // operand block length in words (prefetched one op ahead)
+    uint32_t ordinal;    // noise ordinal (fused or standalone), else NO_SLOT
+    uint32_t r0;         // GATE: applications per warp (the warp's share)
+    uint32_t r1;
+};
+static_assert(sizeof(SOp) == 48, "SOp is 48 bytes");
+constexpr uint32_t STREAM_NOP = 0xFFFFFFFFu;
 
 // Per noise instruction sampling schedule for one tile, also
 // exported to the parity oracle through pfs_program_noise_schedule.
@@ -126,6 +154,10 @@ struct HostProgram {
     // offset | PAIRS), and the noise_kernel work items of one tile
     std::vector<uint32_t> fused_info;   // 4 per ordinal (zeros: drawn by the frame kernel)
     std::vector<uint32_t> hit_items;    // 2 per item: ordinal, first | last consumer warp << 16
+    // stream form of the ops for one tile geometry (lower_stream)
+    std::vector<SOp> sops;
+    std::vector<uint32_t> arena;
+    uint32_t first_span = NO_SLOT;      // span index of the first F_PRESAMPLED op
     int64_t hit_block = 0;              // hit-entry capacity of one tile
     int32_t list_warps = 0;             // consumer warps per group
 };
@@ -147,14 +179,16 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
 void build_noise_schedule(HostProgram& hp, int tile_shots, int vector_shots, double target_hits,
                           double fused_target_hits);
 void permute_rows(HostProgram& hp);
-void reorder_for_banks(HostProgram& hp, int W);
-void bank_order_fused(HostProgram& hp, int W, int warps_per_group);
 void build_hit_lists(HostProgram& hp, int tile_shots, int warps_per_group);
+void lower_stream(HostProgram& hp, int W, int warps_per_group);
 void dedup_operands(HostProgram& hp);
 
 // Kernel launch plumbing (pfs_kernels.cu)
 struct KParams {
     const DOp* ops;
+    const SOp* sops;             // stream ops (same indices as ops)
+    const uint32_t* arena;       // their operand blocks
+    uint32_t first_span;         // span index of the first pre-sampled op (NO_SLOT: none)
     const uint32_t* targets;
     const uint32_t* det_ptr;
     const uint32_t* det_terms;

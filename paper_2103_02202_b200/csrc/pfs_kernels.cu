@@ -420,185 +420,6 @@ __device__ __forceinline__ void warp_range_noise(const KParams& kp, const TileKe
     }
 }
 
-// Where noise_kernel left warp `w`'s hits of fused op `ordinal` in tile
-// `tile`: its (begin, end) span in the tile's block (nullptr: not pre-sampled)
-__device__ __forceinline__ const uint2* hit_span(const KParams& kp, uint32_t ordinal, int64_t tile, int tid) {
-    if (kp.hits_global == nullptr || __ldg(&kp.fused[ordinal].y) == 0u) return nullptr;
-    return kp.spans_global + (tile * kp.num_noise + ordinal) * kp.list_warps + ((uint32_t)tid >> 5);
-}
-
-// Op start: pull the warp's span toward L1 (no registers held across the op's
-// frame work)
-__device__ __forceinline__ void prefetch_span(const KParams& kp, uint32_t ordinal, int64_t tile, int tid) {
-    const uint2* sp = hit_span(kp, ordinal, tile, tid);
-    if (sp != nullptr && (tid & 31) == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(sp));
-}
-
-// The fused noise of a warp's range [A0, A1): its pre-sampled hits when
-// noise_kernel wrote them (span begin != NO_SLOT), else drawn here
-template <int W>
-__device__ __forceinline__ void range_noise(const KParams& kp, const TileKey& tk, const NoiseOp& nz,
-                                            const unsigned long long* tab, uint32_t count, uint32_t A0, uint32_t A1,
-                                            const uint32_t* tg, int ar, bool pairs, uint32_t* X, uint32_t* Z,
-                                            uint32_t* sl, uint32_t* wscr, int lane, uint32_t rowb, int64_t tile,
-                                            int tid) {
-    const uint2* sp = kp.masks == nullptr ? hit_span(kp, nz.ordinal, tile, tid) : nullptr;
-    const uint2 span = sp != nullptr ? __ldg(sp) : make_uint2(NO_SLOT, 0u);
-    if (span.x == NO_SLOT) {
-        warp_range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, ar, pairs, X, Z, sl, wscr, lane, rowb, tile);
-        return;
-    }
-    const unsigned long long* hits = kp.hits_global + tile * kp.hit_block;
-    __syncwarp();  // the warp's row updates are visible to the lanes applying hits
-    for (uint32_t j = span.x + (uint32_t)lane; j < span.y; j += 32) apply_hit_entry<W>(X, Z, __ldg(hits + j));
-    __syncwarp();
-}
-
-// The application range of a warp in a fused op: ceil(count / warps), rounded
-// up to whole noise chunks (ca applications), so each chunk has one owner warp
-__device__ __forceinline__ void warp_range(uint32_t count, uint32_t lgca, int tid, int nth, uint32_t& A0,
-                                           uint32_t& A1) {
-    const uint32_t nw = (uint32_t)nth >> 5, w = (uint32_t)tid >> 5;
-    const uint32_t ca = 1u << lgca;
-    const uint32_t K = ((count + nw - 1) / nw + ca - 1) & ~(ca - 1);
-    A0 = min(count, w * K);
-    A1 = min(count, A0 + K);
-}
-
-// One gate op (frame rule RULE) without fused noise: (application, vector)
-// items, four operand loads in flight per thread
-template <int W, uint32_t RULE>
-__device__ __forceinline__ void gate_plain(uint32_t* X, uint32_t* Z, const uint32_t* tg, uint32_t count, int tid,
-                                           int nth) {
-    constexpr int V = W >= 4 ? 4 : W;
-    constexpr int C = W / V;
-    constexpr int LC = Log2<C>::v;
-    constexpr int ar = RULE >= R_CX ? 2 : 1;
-    const int items = (int)(count << LC);
-    if (ar == 1) {
-        batched_items<4>(tid, nth, items, [&](int i) { return tg[i >> LC]; }, [&](int i, uint32_t q) {
-            const size_t p = (size_t)q * W + (i & (C - 1)) * V;
-            VW<V> x0 = vld<V>(X + p), z0 = vld<V>(Z + p), x1, z1;
-            apply_rule<V>(RULE, x0, z0, x1, z1);
-            if (RULE != R_ZXORX) vst<V>(X + p, x0);
-            if (RULE != R_XXORZ) vst<V>(Z + p, z0);
-        });
-    } else {
-        batched_items<4>(tid, nth, items, [&](int i) { return reinterpret_cast<const uint2*>(tg)[i >> LC]; },
-                         [&](int i, uint2 qq) {
-            const int cv = (i & (C - 1)) * V;
-            const size_t p0 = (size_t)qq.x * W + cv, p1 = (size_t)qq.y * W + cv;
-            VW<V> x0 = vld<V>(X + p0), x1 = vld<V>(X + p1);
-            VW<V> z0 = vld<V>(Z + p0), z1 = vld<V>(Z + p1);
-            apply_rule<V>(RULE, x0, z0, x1, z1);
-            if (RULE != R_CZ) vst<V>(X + p1, x1);
-            if (RULE == R_SWAP) vst<V>(X + p0, x0);
-            vst<V>(Z + p0, z0);
-            if (RULE != R_CX) vst<V>(Z + p1, z1);
-        });
-    }
-}
-
-// Gate + its noise instruction: each warp owns a chunk-aligned range of
-// applications — its lanes apply the rule to (application, vector) items of
-// the range (four operand loads in flight), then the warp draws the range's
-// noise chunks.  No group barrier between the rule and its noise.
-template <int W>
-__device__ __forceinline__ void gate_fused(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
-                                           const uint32_t* tg, const uint32_t* tgp, uint32_t K, uint32_t code,
-                                           uint32_t count, const NoiseOp& nz,
-                                           uint32_t rowb, const unsigned long long* tab, uint32_t* sl,
-                                           uint32_t* wscr, int tid, int nth, int64_t tile) {
-    constexpr int V = W >= 4 ? 4 : W;
-    constexpr int C = W / V;
-    constexpr int LC = Log2<C>::v;
-    const int lane = tid & 31;
-    const int ar = code >= R_CX ? 2 : 1;
-    // this warp's chunk-aligned range of K applications (host-computed, op.b);
-    // its gate work walks the bank-ordered copy of the range (op.a)
-    const uint32_t A0 = min(count, ((uint32_t)tid >> 5) * K), A1 = min(count, A0 + K);
-    if (A0 >= A1) return;  // warp-uniform
-    const int items = (int)((A1 - A0) << LC);
-    const uint32_t* const tga = tgp + (size_t)A0 * ar;
-    if (ar == 1) {
-        batched_items<4>(lane, 32, items, [&](int i) { return tga[i >> LC]; }, [&](int i, uint32_t q) {
-            const size_t p = (size_t)q * W + (i & (C - 1)) * V;
-            VW<V> x0 = vld<V>(X + p), z0 = vld<V>(Z + p), x1, z1;
-            apply_rule<V>(code, x0, z0, x1, z1);
-            if (code != R_ZXORX) vst<V>(X + p, x0);
-            if (code != R_XXORZ) vst<V>(Z + p, z0);
-        });
-    } else {
-        batched_items<4>(lane, 32, items, [&](int i) { return reinterpret_cast<const uint2*>(tga)[i >> LC]; },
-                         [&](int i, uint2 qq) {
-            const int cv = (i & (C - 1)) * V;
-            const size_t p0 = (size_t)qq.x * W + cv, p1 = (size_t)qq.y * W + cv;
-            VW<V> x0 = vld<V>(X + p0), x1 = vld<V>(X + p1);
-            VW<V> z0 = vld<V>(Z + p0), z1 = vld<V>(Z + p1);
-            apply_rule<V>(code, x0, z0, x1, z1);
-            if (code != R_CZ) vst<V>(X + p1, x1);
-            if (code == R_SWAP) vst<V>(X + p0, x0);
-            vst<V>(Z + p0, z0);
-            if (code != R_CX) vst<V>(Z + p1, z1);
-        });
-    }
-    range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, ar, false, X, Z, sl, wscr, lane, rowb, tile, tid);
-}
-
-// M / R / MR (+ fused noise: after a reset, before a measurement).  With
-// fused noise each warp owns a chunk-aligned target range (noise, then the
-// collapses of its (target, vector) items — or the reverse for a reset);
-// without, (target, vector) items over the whole group.
-template <int W>
-__device__ __forceinline__ void collapse_op(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
-                                            uint32_t* ring, const uint32_t* tg, uint32_t kind, uint32_t count,
-                                            bool fz, const NoiseOp& nz, uint32_t rowb, uint32_t rec0, uint32_t coin0,
-                                            const unsigned long long* tab, uint32_t* sl, uint32_t* wscr, int tid,
-                                            int nth, int64_t tile) {
-    constexpr int V = W >= 4 ? 4 : W;
-    constexpr int C = W / V;
-    constexpr int LC = Log2<C>::v;
-    const int lane = tid & 31;
-    uint32_t A0 = 0, A1 = count;
-    int first = tid, stride = nth;
-    if (fz) {
-        warp_range(count, nz.lgL - nz.lgcs, tid, nth, A0, A1);
-        if (A0 >= A1) return;  // warp-uniform
-        first = lane;
-        stride = 32;
-        // the fused noise precedes a measurement (X_ERROR before M)
-        if (kind != K_R)
-            range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile, tid);
-    }
-    const uint2* const tp = reinterpret_cast<const uint2*>(tg);  // (row | COIN_DEAD, slot)
-    batched_items<4>(first, stride, (int)((A1 - A0) << LC), [&](int i) { return tp[A0 + (i >> LC)]; },
-                     [&](int i, uint2 rs) {
-        const uint32_t app = A0 + (uint32_t)(i >> LC);
-        const int c = i & (C - 1);
-        const bool live = !(rs.x & COIN_DEAD);
-        const size_t p = (size_t)(rs.x & ~COIN_DEAD) * W + c * V;
-        if (kind == K_R) {
-            // spill the record homed in x (DESIGN.md §2), then reset
-            if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, vld<V>(X + p));
-            vst<V>(X + p, vzero<V>());
-            vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + app, c, tile) : vzero<V>());
-            return;
-        }
-        const VW<V> x = vld<V>(X + p);
-        if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, x);
-        if (kp.rec_out != nullptr)
-            vst<V>(kp.rec_out + (int64_t)(rec0 + app) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, x);
-        if (kind == K_M) {
-            if (live) vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_vec<W, V>(kp, tk, coin0 + app, c, tile)));
-        } else {  // MR: the measure's coin row (coin0 + 2 app) is overwritten by the reset's
-            vst<V>(X + p, vzero<V>());
-            vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + 2 * app + 1, c, tile) : vzero<V>());
-        }
-    });
-    if (fz && kind == K_R)
-        range_noise<W>(kp, tk, nz, tab, count, A0, A1, tg, 1, true, X, Z, sl, wscr, lane, rowb, tile, tid);
-}
-
 // A standalone noise instruction: one chunk per lane, warp-cooperative draws,
 // hits XORed with shared-memory atomics (consecutive noise ops commute: no
 // barrier between them)
@@ -646,6 +467,134 @@ __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, u
                        tg, ar, false, X, Z, sl, wscr, lane);
     }
 }
+
+// ------------------------------------------------------------ stream executor
+// One gate op in stream form (SOp, lower_stream): the warp's block of packed
+// operand words, one word per application (row of target 0 | row of target 1
+// << 16), PI = 32 / C applications per warp pass; the C lanes that share an
+// application take one V-word vector of its rows each.  XB = the group's x
+// plane + this lane's vector offset, zoff = words from the x to the z plane.
+// Four operand words are in flight per lane.
+template <int W, uint32_t RULE>
+__device__ __forceinline__ void gate_stream(uint32_t* XB, uint32_t zoff, const uint32_t* blk, uint32_t K) {
+    constexpr int V = W >= 4 ? 4 : W;
+    constexpr int PI = 32 / (W / V);
+    constexpr int ar = RULE >= R_CX ? 2 : 1;
+    for (uint32_t k0 = 0; k0 < K; k0 += 4) {
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; u++) w[u] = (k0 + u < K) ? __ldg(blk + (k0 + u) * PI) : STREAM_NOP;
+#pragma unroll
+        for (int u = 0; u < 4; u++) {
+            if (w[u] == STREAM_NOP) continue;
+            uint32_t* const pa = XB + (w[u] & 0xFFFFu) * W;
+            if (ar == 1) {
+                VW<V> x0 = vld<V>(pa), z0 = vld<V>(pa + zoff), x1, z1;
+                apply_rule<V>(RULE, x0, z0, x1, z1);
+                if (RULE != R_ZXORX) vst<V>(pa, x0);
+                if (RULE != R_XXORZ) vst<V>(pa + zoff, z0);
+            } else {
+                uint32_t* const pb = XB + (w[u] >> 16) * W;
+                VW<V> x0 = vld<V>(pa), x1 = vld<V>(pb);
+                VW<V> z0 = vld<V>(pa + zoff), z1 = vld<V>(pb + zoff);
+                apply_rule<V>(RULE, x0, z0, x1, z1);
+                if (RULE != R_CZ) vst<V>(pb, x1);
+                if (RULE == R_SWAP) vst<V>(pa, x0);
+                vst<V>(pa + zoff, z0);
+                if (RULE != R_CX) vst<V>(pb + zoff, z1);
+            }
+        }
+    }
+}
+
+// The warp's share [A0, A1) of an op's applications (SOp.K / SOp.r0 per warp)
+__device__ __forceinline__ void warp_share_of(uint32_t count, uint32_t Kc, int warp, uint32_t& A0, uint32_t& A1) {
+    A0 = min(count, (uint32_t)warp * Kc);
+    A1 = min(count, A0 + Kc);
+}
+
+// General path of an op's fused noise for this warp's applications (rare, out
+// of line): injected mask rows, or the draws made here when noise_kernel did
+// not pre-sample the op (p == 0 / 1, heavy noise) or its hits did not fit.
+// Reads the op's DOp.  Every lane of the warp must call this.
+template <int W>
+__device__ __noinline__ void fused_noise_general(const KParams& kp, const TileKey tk, int oi, uint32_t Kc,
+                                                 uint32_t* X, uint32_t* Z, uint32_t* sl, uint32_t* wscr, int warp,
+                                                 int lane, int64_t tile) {
+    const DOp o = kp.ops[oi];
+    const uint32_t kind = o.kcf & 0xFFu, code = (o.kcf >> 8) & 0xFFu;
+    const bool pairs = kind != K_GATE;
+    const int ar = (kind == K_GATE && code >= R_CX) ? 2 : 1;
+    const NoiseOp nz = decode_noise(o.c, o.d, o.e);
+    const uint32_t rowb = kp.masks != nullptr ? __ldg(kp.noise_rowb + nz.ordinal) : 0u;
+    uint32_t A0, A1;
+    warp_share_of(o.count, Kc, warp, A0, A1);
+    if (A0 >= A1) return;
+    warp_range_noise<W>(kp, tk, nz, kp.noise_tab, o.count, A0, A1, kp.targets + o.off, ar, pairs, X, Z, sl, wscr, lane,
+                        rowb, tile);
+}
+
+// A standalone noise op (reads its DOp), out of line
+template <int W>
+__device__ __noinline__ void noise_general(const KParams& kp, const TileKey tk, int oi, uint32_t* X, uint32_t* Z,
+                                           uint32_t* sl, uint32_t* wscr, int tid, int nth, int64_t tile) {
+    const DOp o = kp.ops[oi];
+    const NoiseOp nz = decode_noise(o.c, o.d, o.e);
+    const uint32_t rowb = kp.masks != nullptr ? __ldg(kp.noise_rowb + nz.ordinal) : 0u;
+    noise_op<W>(kp, tk, X, Z, kp.targets + o.off, (o.kcf >> 8) & 0xFFu, o.count, nz, rowb, kp.noise_tab, sl, wscr, tid,
+                nth, tile);
+}
+
+// Pre-sampled hit lists (noise_kernel): the span and first hit entry of the
+// next pre-sampled op travel in registers, loaded while the current op runs
+struct HitPipe {
+    uint2 nsp;                // the next pre-sampled op's span of this warp
+    unsigned long long e0n;   // its entry for this lane (0: none)
+};
+__device__ __forceinline__ unsigned long long first_entry(const unsigned long long* hits, const uint2 sp, int lane) {
+    const uint32_t j = sp.x + (uint32_t)lane;
+    return (sp.x != NO_SLOT && j < sp.y) ? __ldg(hits + j) : 0ull;
+}
+
+// M / R / MR / SPILL items of this warp's targets [A0, A1): (target, vector)
+// items over the warp's lanes, four operand pairs in flight
+template <int W>
+__device__ __forceinline__ void collapse_stream(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
+                                                uint32_t* ring, const uint2* tp, uint32_t kind, uint32_t A0,
+                                                uint32_t A1, uint32_t rec0, uint32_t coin0, int lane, int64_t tile) {
+    constexpr int V = W >= 4 ? 4 : W;
+    constexpr int C = W / V;
+    constexpr int LC = Log2<C>::v;
+    batched_items<4>(lane, 32, (int)((A1 - A0) << LC), [&](int i) { return __ldg(tp + A0 + (i >> LC)); },
+                     [&](int i, uint2 rs) {
+        const uint32_t app = A0 + (uint32_t)(i >> LC);
+        const int c = i & (C - 1);
+        const bool live = !(rs.x & COIN_DEAD);
+        const size_t p = (size_t)(rs.x & ~COIN_DEAD) * W + c * V;
+        if (kind == K_SPILL) {
+            vst<V>(ring + (size_t)rs.y * W + c * V, vld<V>(X + p));
+            return;
+        }
+        if (kind == K_R) {
+            // spill the record homed in x (DESIGN.md §2), then reset
+            if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, vld<V>(X + p));
+            vst<V>(X + p, vzero<V>());
+            vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + app, c, tile) : vzero<V>());
+            return;
+        }
+        const VW<V> x = vld<V>(X + p);
+        if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, x);
+        if (kp.rec_out != nullptr)
+            vst<V>(kp.rec_out + (int64_t)(rec0 + app) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, x);
+        if (kind == K_M) {
+            if (live) vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_vec<W, V>(kp, tk, coin0 + app, c, tile)));
+        } else {  // MR: the measure's coin row (coin0 + 2 app) is overwritten by the reset's
+            vst<V>(X + p, vzero<V>());
+            vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + 2 * app + 1, c, tile) : vzero<V>());
+        }
+    });
+}
+
 
 // ------------------------------------------------------------ noise kernel
 // Pre-samples the fused noise of a launch's tiles (DESIGN.md §4 draws, exactly
@@ -799,60 +748,65 @@ cudaError_t launch_noise_kernel(int W, const KParams& kp, int grid, cudaStream_t
 }
 
 // ------------------------------------------------------------ frame kernel
-// Persistent kernel: each thread group runs the op stream over its tiles with
-// the frame in shared memory.  Items of an op are (application chunk k, vector
-// c): c selects V words (S = 32 V shots) of every row; a fused op's item owns
-// the ca applications of one noise chunk so it can apply that chunk's hits to
-// the rows it holds in registers.
+// Persistent kernel: each thread group runs the stream ops (SOp) over its
+// tiles with the frame in shared memory.  Per op a thread reads three
+// descriptor vectors (one op ahead), prefetches the next op's operand block,
+// passes the group barrier where the compiler found a conflict, and walks its
+// warp's operand words.  Fused noise comes from noise_kernel's per-warp hit
+// spans (span and first entry prefetched one pre-sampled op ahead); the general
+// paths (injected masks, inline draws, standalone noise ops) are out of line.
 template <int W, bool RING_SMEM>
 __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __grid_constant__ KParams kp) {
     constexpr int V = W >= 4 ? 4 : W;  // words per vector access
     constexpr int C = W / V;           // vectors per row
     constexpr int LC = Log2<C>::v;
+    constexpr int PI = 32 / C;         // applications per warp pass
     extern __shared__ __align__(16) uint32_t smem[];
     const int n = kp.num_qubits;
     // kp.groups independent thread groups per CTA, each with its own tile,
-    // frame, record ring and named barrier: one group's op latency overlaps
-    // the other group's work
+    // frame (x plane, z plane), record ring and named barrier: one group's op
+    // latency overlaps the other group's work
     const int G = kp.groups;
     const int gsz = blockDim.x / G;
     const int grp = threadIdx.x / gsz;
     const int tid = threadIdx.x - grp * gsz;  // thread index within the group
     const int nth = gsz;
-    const size_t fw = (size_t)2 * n * W;      // frame words per group
-    uint32_t* const X = smem + grp * fw;
-    uint32_t* const Z = X + (size_t)n * W;
-    uint32_t* const ring = RING_SMEM ? (smem + G * fw + (size_t)grp * kp.num_slots * W)
+    const int lane = tid & 31, warp = tid >> 5;
+    const uint32_t zoff = (uint32_t)n * W;
+    const size_t gw = (size_t)2 * n * W + (RING_SMEM ? (size_t)kp.num_slots * W : 0);  // words per group
+    uint32_t* const X = smem + grp * gw;
+    uint32_t* const Z = X + zoff;
+    uint32_t* const ring = RING_SMEM ? (Z + zoff)
                                      : (kp.ring_global + ((size_t)blockIdx.x * G + grp) * kp.num_slots * W);
-    uint32_t* const cnt = smem + G * fw + (RING_SMEM ? (size_t)G * kp.num_slots * W : 0);
-    // then the per-warp noise scratch, and a 16-byte aligned tail: the op
-    // descriptors, then the threshold tables (offset arithmetic on the shared
-    // array keeps the loads in the shared address space: LDS, not generic LD)
+    uint32_t* const cnt = smem + G * gw;
+    // then the per-warp noise scratch, and a 16-byte aligned tail: the stream
+    // ops, then the threshold tables
     const size_t wscr_word = (size_t)(cnt + (kp.counts_in_smem ? kp.num_cols : 0) - smem);
     uint32_t* const wscr = smem + wscr_word + (size_t)(threadIdx.x >> 5) * WSCR;
     const size_t dsc_word = (wscr_word + (size_t)(blockDim.x >> 5) * WSCR + 3) & ~(size_t)3;
     uint4* const dsc_s = reinterpret_cast<uint4*>(smem + dsc_word);
-    unsigned long long* const tab_s = reinterpret_cast<unsigned long long*>(dsc_s + 2 * kp.n_ops);
-    const uint4* const dsc_g = reinterpret_cast<const uint4*>(kp.ops);
+    const uint4* const dsc_g = reinterpret_cast<const uint4*>(kp.sops);
     const bool dsm = kp.desc_in_smem != 0;
     auto ldesc = [&](int i) -> uint4 { return dsm ? dsc_s[i] : __ldg(dsc_g + i); };
-    const unsigned long long* const tab = dsm ? tab_s : kp.noise_tab;
     // per-thread scratch of the general noise path (global, L1-resident)
     uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
-    const bool injected = kp.masks != nullptr;
+    const bool use_lists = kp.hits_global != nullptr && kp.masks == nullptr;
     const uint32_t bar_id = 1u + (uint32_t)grp;
     auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gsz) : "memory"); };
+    uint32_t* const XB = X + (lane & (C - 1)) * V;  // this lane's vector of every row
 
     if (kp.counts_in_smem)
         for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
-    if (dsm) {
-        for (int i = threadIdx.x; i < 2 * kp.n_ops; i += blockDim.x) dsc_s[i] = __ldg(dsc_g + i);
-        for (int i = threadIdx.x; i < kp.tab_len; i += blockDim.x) tab_s[i] = __ldg(kp.noise_tab + i);
-    }
+    if (dsm)
+        for (int i = threadIdx.x; i < 3 * kp.n_ops; i += blockDim.x) dsc_s[i] = __ldg(dsc_g + i);
     __syncthreads();
 
     for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
         const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
+        const unsigned long long* const hits = kp.hits_global + tile * kp.hit_block;
+        const uint2* const spans = kp.spans_global + (tile * kp.num_noise) * kp.list_warps + warp;
+        HitPipe hp{make_uint2(NO_SLOT, 0u), 0ull};
+        if (use_lists && kp.first_span != NO_SLOT) hp.nsp = __ldg(spans + kp.first_span);
         // ---- FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39) ----
         for (int i = tid; i < (n << LC); i += nth) {
             const int q = i >> LC, c = i & (C - 1);
@@ -865,102 +819,103 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             const int k = i >> LC, c = i & (C - 1);
             vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
         }
+        if (use_lists) hp.e0n = first_entry(hits, hp.nsp, lane);
         group_sync();
 
         // descriptors run one op ahead in registers
-        uint4 h0 = kp.n_ops > 0 ? ldesc(0) : make_uint4(0, 0, 0, 0);
-        uint4 h1n = kp.n_ops > 0 ? ldesc(1) : make_uint4(0, 0, 0, 0);
+        uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0, n2 = n0;
+        if (kp.n_ops > 0) { n0 = ldesc(0); n1 = ldesc(1); n2 = ldesc(2); }
         for (int oi = 0; oi < kp.n_ops; oi++) {
-            const uint32_t kind = h0.x & 0xFFu, code = (h0.x >> 8) & 0xFFu, flags = h0.x >> 16;
-            const uint32_t count = h0.y, off = h0.z, oa = h0.w;
-            const uint4 h1 = h1n;
-            if (oi + 1 < kp.n_ops) { h0 = ldesc(2 * oi + 2); h1n = ldesc(2 * oi + 3); }
-            const uint32_t ob = h1.x;
+            const uint4 d0 = n0, d1 = n1, d2 = n2;
             if (oi + 1 < kp.n_ops) {
-                // pull the next op's operand block into L1 while this op runs:
-                // the frame and ring leave ~20 KB of L1, not a whole round of
-                // operands, and an L2 round trip per operand load would sit on
-                // every op's critical path
-                const uint32_t nk = h0.x & 0xFFu, nc = (h0.x >> 8) & 0xFFu, ncount = h0.y;
-                const uint32_t* base;
-                uint32_t words;
-                if (nk == K_DET) {
-                    base = kp.det_terms + h0.z;
-                    words = nc ? ncount * nc : 0u;
-                } else {
-                    // (a fused gate's gate work walks its bank-ordered copy)
-                    base = kp.targets + ((nk == K_GATE && ((h0.x >> 16) & F_NOISE)) ? h0.w : h0.z);
-                    const uint32_t per = (nk == K_GATE) ? (nc >= R_CX ? 2u : 1u)
-                                       : (nk == K_NOISE) ? (nc == CH_DEP2 ? 2u : 1u)
-                                       : (nk == K_OBS) ? 1u : 2u;
-                    words = ncount * per;
-                }
-                const uint32_t lines = (words * 4u + 127u) >> 7;
+                n0 = ldesc(3 * oi + 3); n1 = ldesc(3 * oi + 4); n2 = ldesc(3 * oi + 5);
+                // pull the next op's operand block into L1 while this op runs
+                const uint32_t lines = (n2.x * 4u + 127u) >> 7;
                 for (uint32_t l = (uint32_t)tid; l < lines; l += (uint32_t)nth)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(base + 32u * l));
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(kp.arena + n0.z + 32u * l));
+            }
+            const uint32_t kind = d0.x & 0xFFu, code = (d0.x >> 8) & 0xFFu, flags = d0.x >> 16;
+            const uint32_t count = d0.y, off = d0.z, K = d0.w;
+            const bool fz = (flags & F_NOISE) != 0;
+            // this op's pre-sampled hits; start the next pre-sampled op's span load
+            const bool pre = use_lists && (flags & F_PRESAMPLED);
+            uint2 sp = make_uint2(NO_SLOT, 0u);
+            unsigned long long e0 = 0ull;
+            if (pre) {
+                sp = hp.nsp;
+                e0 = hp.e0n;
+                hp.nsp = __ldg(spans + d1.w);
             }
             if (flags & F_BARRIER) group_sync();
 #if PFS_PROFILE
             if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
                 tile == 0)  // profiling: op-boundary timestamps of the first tile
                 kp.op_clock[oi] = clock64();
-#endif
-            const uint32_t* const tg = kp.targets + off;  // operands (L1/L2-resident)
-#if PFS_PROFILE
             if (kp.debug_skip) {
                 const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
                                    : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
                 if (kp.debug_skip & bit) continue;
             }
 #endif
-            // fused / standalone noise of this op (F_NOISE or K_NOISE)
-            const bool fz = (flags & F_NOISE) != 0;
-            const NoiseOp nz = decode_noise(h1.y, h1.z, h1.w);
-            const uint32_t rowb = (injected && (fz || kind == K_NOISE)) ? __ldg(kp.noise_rowb + nz.ordinal) : 0u;
-            if (fz && !injected) prefetch_span(kp, nz.ordinal, tile, tid);
+            // the fused noise of this warp's applications (Kc per warp)
+            auto fused_noise = [&](uint32_t Kc) {
+#if PFS_PROFILE
+                if (kp.debug_skip & 2) return;
+#endif
+                if (pre && sp.x != NO_SLOT) {
+                    __syncwarp();  // the warp's row updates are visible to the lanes applying hits
+                    uint32_t j = sp.x + (uint32_t)lane;
+                    if (j < sp.y) apply_hit_entry<W>(X, Z, e0);
+                    for (j += 32u; j < sp.y; j += 32u) apply_hit_entry<W>(X, Z, __ldg(hits + j));
+                    __syncwarp();
+                } else {
+                    fused_noise_general<W>(kp, tk, oi, Kc, X, Z, sl, wscr, warp, lane, tile);
+                }
+            };
 
             switch (kind) {
             case K_GATE: {
-                if (fz) {
-                    gate_fused<W>(kp, tk, X, Z, tg, kp.targets + oa, ob, code, count, nz, rowb, tab, sl, wscr, tid, nth,
-                                  tile);
-                    break;
-                }
+                const uint32_t* const blk = kp.arena + off + (uint32_t)warp * K * PI + (lane >> LC);
                 switch (code) {
-                    case R_SWAPXZ: gate_plain<W, R_SWAPXZ>(X, Z, tg, count, tid, nth); break;
-                    case R_ZXORX: gate_plain<W, R_ZXORX>(X, Z, tg, count, tid, nth); break;
-                    case R_XXORZ: gate_plain<W, R_XXORZ>(X, Z, tg, count, tid, nth); break;
-                    case R_CX: gate_plain<W, R_CX>(X, Z, tg, count, tid, nth); break;
-                    case R_CZ: gate_plain<W, R_CZ>(X, Z, tg, count, tid, nth); break;
-                    case R_CY: gate_plain<W, R_CY>(X, Z, tg, count, tid, nth); break;
-                    case R_SWAP: gate_plain<W, R_SWAP>(X, Z, tg, count, tid, nth); break;
+                    case R_SWAPXZ: gate_stream<W, R_SWAPXZ>(XB, zoff, blk, K); break;
+                    case R_ZXORX: gate_stream<W, R_ZXORX>(XB, zoff, blk, K); break;
+                    case R_XXORZ: gate_stream<W, R_XXORZ>(XB, zoff, blk, K); break;
+                    case R_CX: gate_stream<W, R_CX>(XB, zoff, blk, K); break;
+                    case R_CZ: gate_stream<W, R_CZ>(XB, zoff, blk, K); break;
+                    case R_CY: gate_stream<W, R_CY>(XB, zoff, blk, K); break;
+                    case R_SWAP: gate_stream<W, R_SWAP>(XB, zoff, blk, K); break;
                     default: break;
                 }
+                if (fz) fused_noise(d2.z);
                 break;
             }
-            case K_R: case K_M: case K_MR:
-                collapse_op<W>(kp, tk, X, Z, ring, tg, kind, count, fz, nz, rowb, oa, ob, tab, sl, wscr, tid, nth, tile);
-                break;
-            case K_SPILL: {
-                const uint2* const tp = reinterpret_cast<const uint2*>(tg);
-                for (int i = tid; i < (int)(count << LC); i += nth) {
-                    const uint2 rs = tp[i >> LC];
-                    const int cv = (i & (C - 1)) * V;
-                    vst<V>(ring + (size_t)rs.y * W + cv, vld<V>(X + (size_t)rs.x * W + cv));
-                }
+            case K_R: case K_M: case K_MR: case K_SPILL: {
+                uint32_t A0, A1;
+                warp_share_of(count, K, warp, A0, A1);
+                // fused noise precedes a measurement (X_ERROR before M), follows a reset
+                if (fz && kind != K_R) fused_noise(K);
+                if (A0 < A1)
+                    collapse_stream<W>(kp, tk, X, Z, ring, reinterpret_cast<const uint2*>(kp.arena + off), kind, A0, A1,
+                                       d1.x, d1.y, lane, tile);
+                if (fz && kind == K_R) fused_noise(K);
                 break;
             }
             case K_NOISE:
-                noise_op<W>(kp, tk, X, Z, tg, code, count, nz, rowb, tab, sl, wscr, tid, nth, tile);
+#if PFS_PROFILE
+                if (kp.debug_skip & 2) break;
+#endif
+                noise_general<W>(kp, tk, oi, X, Z, sl, wscr, tid, nth, tile);
                 break;
             case K_DET: {
+                const uint32_t oa = d1.x;
                 const int items = (int)(count << LC);
-                // prefetch each column's term range and first two terms; uniform
-                // ops (code = terms per column) address terms directly.  A term is
-                // a ring slot, or XROW | row: the record still in that x row.
+                // a term is a ring slot, or XROW | row: the record still in that
+                // x row.  Uniform ops (code = terms per column) read their terms
+                // from the arena block, the others through the CSR arrays.
                 auto src = [&](uint32_t t) -> const uint32_t* {
                     return (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
                 };
+                const uint32_t* const tb = code ? kp.arena : kp.det_terms;
                 batched_items<2>(tid, nth, items,
                     [&](int i) {
                         const uint32_t ci = (uint32_t)(i >> LC);
@@ -968,9 +923,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                         uint32_t e0, e1;
                         if (code) { e0 = off + ci * code; e1 = e0 + code; }
                         else { e0 = __ldg(kp.det_ptr + col); e1 = __ldg(kp.det_ptr + col + 1); }
-                        const uint32_t* tb = kp.det_terms;
-                        const uint32_t s0 = e0 < e1 ? tb[e0] : NO_SLOT;
-                        const uint32_t s1 = e0 + 1 < e1 ? tb[e0 + 1] : NO_SLOT;
+                        const uint32_t s0 = e0 < e1 ? __ldg(tb + e0) : NO_SLOT;
+                        const uint32_t s1 = e0 + 1 < e1 ? __ldg(tb + e0 + 1) : NO_SLOT;
                         return make_uint4(e0, e1, s0, s1);
                     },
                     [&](int i, uint4 d) {
@@ -979,8 +933,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                         VW<V> acc = vzero<V>();
                         if (d.z != NO_SLOT) acc = vld<V>(src(d.z) + c * V);
                         if (d.w != NO_SLOT) acc = vxor<V>(acc, vld<V>(src(d.w) + c * V));
-                        const uint32_t* tb = kp.det_terms;
-                        for (uint32_t e = d.x + 2; e < d.y; e++) acc = vxor<V>(acc, vld<V>(src(tb[e]) + c * V));
+                        for (uint32_t e = d.x + 2; e < d.y; e++) acc = vxor<V>(acc, vld<V>(src(__ldg(tb + e)) + c * V));
                         if (kp.ev_out != nullptr)
                             vst<V>(kp.ev_out + (int64_t)col * kp.out_row_stride + tile * kp.out_tile_stride + c * V, acc);
                         if (kp.counts != nullptr) {
@@ -1001,10 +954,12 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
                 break;
             }
             case K_OBS: {
+                const uint32_t oa = d1.x;
+                const uint32_t* const tg = kp.arena + off;
                 for (int c = tid; c < C; c += nth) {
                     VW<V> acc = vld<V>(ring + (size_t)oa * W + c * V);
                     for (uint32_t j = 0; j < count; j++) {
-                        const uint32_t t = tg[j];
+                        const uint32_t t = __ldg(tg + j);
                         const uint32_t* s = (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
                         acc = vxor<V>(acc, vld<V>(s + c * V));
                     }
@@ -1014,6 +969,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             }
             default: break;
             }
+            // the next pre-sampled op's first hit entry (its span has arrived by now)
+            if (pre) hp.e0n = first_entry(hits, hp.nsp, lane);
 #if PFS_PROFILE
             if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tile == 0 &&
                 (tid & 31) == 0 && (tid >> 5) < 8)  // profiling: per-warp end of op work
@@ -1028,6 +985,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             if (cnt[i]) atomicAdd(kp.counts + i, (unsigned long long)cnt[i]);
     }
 }
+
 
 size_t frame_smem_bytes(int num_qubits, int W) { return (size_t)2 * num_qubits * W * 4; }
 
