@@ -121,13 +121,13 @@ constexpr double kFusedHits = 1.0;       // mean hits per fused noise chunk (one
 constexpr int64_t kHitBufBytes = (int64_t)256 << 20;  // hit lists of one sub-chunk of tiles
 
 static bool desc_fits(const HostProgram& hp) {
-    return hp.ops.size() * sizeof(SOp) + hp.noise_tab.size() * 8 <= (size_t)DESC_SMEM_MAX;
+    return hp.ops.size() * sizeof(SOp) <= (size_t)DESC_SMEM_MAX;
 }
 
 // per-warp noise scratch, descriptors + threshold tables (when they fit), alignment slack
 static size_t fixed_smem(const HostProgram& hp) {
     return 16 + (size_t)(FRAME_MAX_THREADS / 32) * WSCR * 4 +
-           (desc_fits(hp) ? hp.ops.size() * sizeof(SOp) + hp.noise_tab.size() * 8 : 0);
+           (desc_fits(hp) ? hp.ops.size() * sizeof(SOp) : 0);
 }
 
 // Outputs of the kernels that write final layouts directly (dem_kernel).
@@ -561,7 +561,7 @@ static int launch_tiles(pfs_program* pg, const Flavour& f, KParams kp, const Lau
         sub = std::min(nt, cap_tiles);
         CUDA_TRY(pg->d_hits.reserve((size_t)sub * hp.hit_block));
         CUDA_TRY(pg->d_spans.reserve((size_t)sub * hp.num_noise * hp.list_warps * 2));
-        CUDA_TRY(pg->d_fill.reserve((size_t)sub));
+        CUDA_TRY(pg->d_fill.reserve((size_t)sub * 2));
         kp.fused = reinterpret_cast<const uint4*>(f.fused.p);
         kp.hit_items = reinterpret_cast<const uint2*>(f.hit_items.p);
         kp.hit_block = hp.hit_block;
@@ -594,7 +594,7 @@ static int launch_tiles(pfs_program* pg, const Flavour& f, KParams kp, const Lau
             k2.spans_global = reinterpret_cast<uint2*>(pg->d_spans.p);
             k2.fill_global = pg->d_fill.p;
             if (tm) CUDA_TRY(cudaEventRecord(pg->ev[8], fst));
-            CUDA_TRY(cudaMemsetAsync(pg->d_fill.p, 0, (size_t)ns * 4, fst));
+            CUDA_TRY(cudaMemsetAsync(pg->d_fill.p, 0, (size_t)ns * 8, fst));
             const int64_t items = ns * k2.n_items;
             const int ng = (int)std::min<int64_t>(pg->noise_grid, (items + NK_WARPS - 1) / NK_WARPS);
             CUDA_TRY(launch_noise_kernel(W, k2, ng, fst));
@@ -709,6 +709,7 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.sops = fl.sops.p;
     kp.arena = fl.arena.p;
     kp.first_span = hp.first_span;
+    kp.all_presampled = hp.all_presampled ? 1 : 0;
     kp.targets = fl.targets.p;
     kp.det_ptr = fl.det_ptr.p;
     kp.det_terms = fl.det_terms.p;

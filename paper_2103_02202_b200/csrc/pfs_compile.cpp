@@ -716,6 +716,7 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
     hp.sops.assign(hp.ops.size(), SOp{});
     hp.arena.clear();
     hp.first_span = NO_SLOT;
+    hp.all_presampled = true;
     std::unordered_map<uint64_t, std::vector<std::pair<uint32_t, uint32_t>>> seen;
     auto add_block = [&](const std::vector<uint32_t>& blk) -> uint32_t {
         if (blk.empty()) return 0u;
@@ -743,6 +744,10 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
         s.ordinal = (kind == K_NOISE || (flags & F_NOISE)) ? o.c : NO_SLOT;
         const bool fz = (flags & F_NOISE) != 0;
         const uint32_t ca = fz ? hp.noise[o.c].ca : 1u;
+        if ((fz || kind == K_NOISE) && hp.noise[o.c].zone != NZONE_NONE &&
+            (!fz || hp.fused_info.empty() || hp.fused_info[(size_t)o.c * 4 + 1] != 1u))
+            hp.all_presampled = false;
+        if (fz && hp.noise[o.c].zone == NZONE_NONE) s.kcf &= ~(F_NOISE << 16);  // p == 0: nothing to apply
         if (fz && !hp.fused_info.empty() && hp.fused_info[(size_t)o.c * 4 + 1] == 1u) {
             s.kcf |= F_PRESAMPLED << 16;
             s.span = o.c * (uint32_t)hp.list_warps;
@@ -779,7 +784,12 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
         default: break;  // standalone noise reads its DOp
         }
         s.off = blk.empty() ? o.off : add_block(blk);
-        s.pf_words = (uint32_t)blk.size();
+        // the block is prefetched while the previous op runs: its extent goes
+        // into that op's descriptor
+        if (i > 0) {
+            hp.sops[i - 1].pf_words = (uint32_t)blk.size();
+            hp.sops[i - 1].r1 = s.off;
+        }
     }
     uint32_t next = NO_SLOT;
     for (size_t i = hp.sops.size(); i-- > 0;) {

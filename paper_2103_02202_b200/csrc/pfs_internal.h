@@ -96,10 +96,10 @@ struct SOp {
     uint32_t a, b;       // as in DOp (first record / column / accumulator, first coin row)
     uint32_t span;       // F_PRESAMPLED: ordinal * list_warps (index of warp 0's span)
     uint32_t next_span;  // span index of the next F_PRESAMPLED op (this op's when it is the last)
-    uint32_t pf_words;   // operand block length in words (prefetched one op ahead)
+    uint32_t pf_words;   // the NEXT op's operand block: length in words (prefetched while this op runs)
     uint32_t ordinal;    // noise ordinal (fused or standalone), else NO_SLOT
     uint32_t r0;         // GATE: applications per warp (the warp's share)
-    uint32_t r1;
+    uint32_t r1;         // the NEXT op's operand block: arena offset
 };
 static_assert(sizeof(SOp) == 48, "SOp is 48 bytes");
 constexpr uint32_t STREAM_NOP = 0xFFFFFFFFu;
@@ -158,6 +158,7 @@ struct HostProgram {
     std::vector<SOp> sops;
     std::vector<uint32_t> arena;
     uint32_t first_span = NO_SLOT;      // span index of the first F_PRESAMPLED op
+    bool all_presampled = false;        // every noise op with p > 0 is fused and pre-sampled
     int64_t hit_block = 0;              // hit-entry capacity of one tile
     int32_t list_warps = 0;             // consumer warps per group
 };
@@ -229,7 +230,8 @@ struct KParams {
     unsigned long long* hits_global;  // [tiles][hit_block] entries
     uint2* spans_global;              // [tiles][num_noise][list_warps] (begin, end) in the tile's
                                       // block (begin NO_SLOT: the warp draws inline)
-    uint32_t* fill_global;            // [tiles] entries used (noise_kernel allocation)
+    uint32_t* fill_global;            // [tiles][2]: entries used (noise_kernel allocation), overflow mark
+    int32_t all_presampled;           // every noise instruction is fused and pre-sampled (hot frame loop)
     const uint2* hit_items;           // noise_kernel items of one tile
     int64_t hit_block;
     int32_t list_warps;

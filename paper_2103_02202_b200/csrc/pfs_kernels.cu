@@ -98,8 +98,10 @@ __device__ __forceinline__ VW<V> coin_vec(const KParams& kp, const TileKey& tk, 
 #if PFS_PROFILE
     if (kp.debug_skip & 4) return vzero<V>();
 #endif
-    uint32_t b[4];
-    coin_block(tk, e, (uint32_t)(c * V) >> 2, b);
+    // word w of coin row e = word (w & 3) of Philox(e, w >> 2, g, DOMAIN_COIN),
+    // inline: a call inside the op loop would spill the loop's live values
+    uint32_t b[4] = {e, (uint32_t)(c * V) >> 2, tk.g, DOMAIN_COIN};
+    philox_rounds(b[0], b[1], b[2], b[3], tk.k0, tk.k1);
 #pragma unroll
     for (int j = 0; j < V; j++) o.w[j] = b[(c * V + j) & 3];
     return o;
@@ -469,6 +471,10 @@ __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, u
 }
 
 // ------------------------------------------------------------ stream executor
+#ifndef PFS_GATE_BATCH
+#define PFS_GATE_BATCH 2
+#endif
+constexpr int GATE_BATCH = PFS_GATE_BATCH;  // operand words in flight per lane
 // One gate op in stream form (SOp, lower_stream): the warp's block of packed
 // operand words, one word per application (row of target 0 | row of target 1
 // << 16), PI = 32 / C applications per warp pass; the C lanes that share an
@@ -480,12 +486,13 @@ __device__ __forceinline__ void gate_stream(uint32_t* XB, uint32_t zoff, const u
     constexpr int V = W >= 4 ? 4 : W;
     constexpr int PI = 32 / (W / V);
     constexpr int ar = RULE >= R_CX ? 2 : 1;
-    for (uint32_t k0 = 0; k0 < K; k0 += 4) {
-        uint32_t w[4];
+    constexpr int U = GATE_BATCH;
+    for (uint32_t k0 = 0; k0 < K; k0 += U) {
+        uint32_t w[U];
 #pragma unroll
-        for (int u = 0; u < 4; u++) w[u] = (k0 + u < K) ? __ldg(blk + (k0 + u) * PI) : STREAM_NOP;
+        for (int u = 0; u < U; u++) w[u] = (k0 + u < K) ? __ldg(blk + (k0 + u) * PI) : STREAM_NOP;
 #pragma unroll
-        for (int u = 0; u < 4; u++) {
+        for (int u = 0; u < U; u++) {
             if (w[u] == STREAM_NOP) continue;
             uint32_t* const pa = XB + (w[u] & 0xFFFFu) * W;
             if (ar == 1) {
@@ -513,36 +520,58 @@ __device__ __forceinline__ void warp_share_of(uint32_t count, uint32_t Kc, int w
     A1 = min(count, A0 + Kc);
 }
 
+// Shared-memory map of frame_kernel (word offsets into the dynamic array): the
+// per-warp scratch of the general noise paths, the stream ops (when they fit),
+// then per group its x plane, z plane and record ring, then the counters.
+struct FrameMap {
+    uint32_t dsc_word, fr0;
+};
+__device__ __forceinline__ FrameMap frame_map(const KParams& kp) {
+    FrameMap m;
+    m.dsc_word = (blockDim.x >> 5) * WSCR;
+    m.fr0 = m.dsc_word + (kp.desc_in_smem ? 12u * (uint32_t)kp.n_ops : 0u);
+    return m;
+}
+
 // General path of an op's fused noise for this warp's applications (rare, out
-// of line): injected mask rows, or the draws made here when noise_kernel did
-// not pre-sample the op (p == 0 / 1, heavy noise) or its hits did not fit.
-// Reads the op's DOp.  Every lane of the warp must call this.
+// of line, few arguments: it rebuilds its context): injected mask rows, or the
+// draws made here when noise_kernel did not pre-sample the op (p == 0 / 1,
+// heavy noise) or its hits did not fit.  Reads the op's DOp; xg = the group's
+// x plane.  Every lane of the warp must call this.
 template <int W>
-__device__ __noinline__ void fused_noise_general(const KParams& kp, const TileKey tk, int oi, uint32_t Kc,
-                                                 uint32_t* X, uint32_t* Z, uint32_t* sl, uint32_t* wscr, int warp,
-                                                 int lane, int64_t tile) {
+__device__ __noinline__ void fused_noise_general(const KParams& kp, int oi, uint32_t Kc, uint32_t xg, int64_t tile) {
+    extern __shared__ __align__(16) uint32_t smem[];
     const DOp o = kp.ops[oi];
     const uint32_t kind = o.kcf & 0xFFu, code = (o.kcf >> 8) & 0xFFu;
     const bool pairs = kind != K_GATE;
     const int ar = (kind == K_GATE && code >= R_CX) ? 2 : 1;
     const NoiseOp nz = decode_noise(o.c, o.d, o.e);
     const uint32_t rowb = kp.masks != nullptr ? __ldg(kp.noise_rowb + nz.ordinal) : 0u;
+    const int gsz = blockDim.x / kp.groups;
+    const int tid = threadIdx.x % gsz;
     uint32_t A0, A1;
-    warp_share_of(o.count, Kc, warp, A0, A1);
+    warp_share_of(o.count, Kc, tid >> 5, A0, A1);
     if (A0 >= A1) return;
-    warp_range_noise<W>(kp, tk, nz, kp.noise_tab, o.count, A0, A1, kp.targets + o.off, ar, pairs, X, Z, sl, wscr, lane,
-                        rowb, tile);
+    const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
+    uint32_t* const X = smem + xg;
+    uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
+    warp_range_noise<W>(kp, tk, nz, kp.noise_tab, o.count, A0, A1, kp.targets + o.off, ar, pairs, X,
+                        X + (size_t)kp.num_qubits * W, sl, smem + (threadIdx.x >> 5) * WSCR, tid & 31, rowb, tile);
 }
 
 // A standalone noise op (reads its DOp), out of line
 template <int W>
-__device__ __noinline__ void noise_general(const KParams& kp, const TileKey tk, int oi, uint32_t* X, uint32_t* Z,
-                                           uint32_t* sl, uint32_t* wscr, int tid, int nth, int64_t tile) {
+__device__ __noinline__ void noise_general(const KParams& kp, int oi, uint32_t xg, int64_t tile) {
+    extern __shared__ __align__(16) uint32_t smem[];
     const DOp o = kp.ops[oi];
     const NoiseOp nz = decode_noise(o.c, o.d, o.e);
     const uint32_t rowb = kp.masks != nullptr ? __ldg(kp.noise_rowb + nz.ordinal) : 0u;
-    noise_op<W>(kp, tk, X, Z, kp.targets + o.off, (o.kcf >> 8) & 0xFFu, o.count, nz, rowb, kp.noise_tab, sl, wscr, tid,
-                nth, tile);
+    const int gsz = blockDim.x / kp.groups;
+    const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
+    uint32_t* const X = smem + xg;
+    uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
+    noise_op<W>(kp, tk, X, X + (size_t)kp.num_qubits * W, kp.targets + o.off, (o.kcf >> 8) & 0xFFu, o.count, nz, rowb,
+                kp.noise_tab, sl, smem + (threadIdx.x >> 5) * WSCR, (int)(threadIdx.x % gsz), gsz, tile);
 }
 
 // Pre-sampled hit lists (noise_kernel): the span and first hit entry of the
@@ -704,9 +733,12 @@ __global__ void __launch_bounds__(NK_WARPS * 32, 4) noise_kernel(const __grid_co
         const uint32_t n = over ? 0u : *wn;
         uint2* spans = kp.spans_global + (tile * kp.num_noise + o) * kp.list_warps;
         uint32_t base = 0u;
-        if (lane == 0 && !over && n > 0u) base = atomicAdd(kp.fill_global + tile, n);
+        if (lane == 0 && !over && n > 0u) base = atomicAdd(kp.fill_global + 2 * tile, n);
         base = __shfl_sync(0xFFFFFFFFu, base, 0);
         over |= (int64_t)base + n > kp.hit_block;
+        // an item whose hits did not fit sends its tile through the general
+        // frame loop (its consumer warps draw inline)
+        if (lane == 0 && over) kp.fill_global[2 * tile + 1] = 1u;
         // consumer warp spans: exclusive prefix of the per-warp counts
         const uint32_t nwl = we - wb;
         uint32_t v = (uint32_t)lane < nwl ? wcnt[lane] : 0u, pre = v;
@@ -748,24 +780,24 @@ cudaError_t launch_noise_kernel(int W, const KParams& kp, int grid, cudaStream_t
 }
 
 // ------------------------------------------------------------ frame kernel
-// Persistent kernel: each thread group runs the stream ops (SOp) over its
-// tiles with the frame in shared memory.  Per op a thread reads three
-// descriptor vectors (one op ahead), prefetches the next op's operand block,
-// passes the group barrier where the compiler found a conflict, and walks its
-// warp's operand words.  Fused noise comes from noise_kernel's per-warp hit
-// spans (span and first entry prefetched one pre-sampled op ahead); the general
-// paths (injected masks, inline draws, standalone noise ops) are out of line.
-template <int W, bool RING_SMEM>
-__global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __grid_constant__ KParams kp) {
+// One tile of one thread group: the stream ops (SOp) over the group's frame in
+// shared memory.  Per op a thread reads three descriptor vectors, prefetches
+// the next op's operand block, passes the group barrier where the compiler
+// found a conflict, and walks its warp's operand words.  Fused noise comes from
+// noise_kernel's per-warp hit spans (span and first entry prefetched one
+// pre-sampled op ahead).  GENERAL = false is the hot instantiation: every noise
+// instruction is fused and pre-sampled and no list overflowed, so the loop
+// makes no calls (a call inside it makes ptxas spill the loop's live values);
+// GENERAL = true adds the out-of-line paths (injected masks, inline draws,
+// standalone noise ops) and runs as one call per tile.
+template <int W, bool RING_SMEM, bool GENERAL>
+__device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t tile) {
     constexpr int V = W >= 4 ? 4 : W;  // words per vector access
     constexpr int C = W / V;           // vectors per row
     constexpr int LC = Log2<C>::v;
     constexpr int PI = 32 / C;         // applications per warp pass
     extern __shared__ __align__(16) uint32_t smem[];
     const int n = kp.num_qubits;
-    // kp.groups independent thread groups per CTA, each with its own tile,
-    // frame (x plane, z plane), record ring and named barrier: one group's op
-    // latency overlaps the other group's work
     const int G = kp.groups;
     const int gsz = blockDim.x / G;
     const int grp = threadIdx.x / gsz;
@@ -773,41 +805,29 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     const int nth = gsz;
     const int lane = tid & 31, warp = tid >> 5;
     const uint32_t zoff = (uint32_t)n * W;
-    const size_t gw = (size_t)2 * n * W + (RING_SMEM ? (size_t)kp.num_slots * W : 0);  // words per group
-    uint32_t* const X = smem + grp * gw;
+    const uint32_t gw = 2u * zoff + (RING_SMEM ? (uint32_t)kp.num_slots * W : 0u);  // words per group
+    const FrameMap fm = frame_map(kp);
+    const uint32_t xg = fm.fr0 + (uint32_t)grp * gw;  // the group's x plane
+    uint32_t* const X = smem + xg;
     uint32_t* const Z = X + zoff;
     uint32_t* const ring = RING_SMEM ? (Z + zoff)
                                      : (kp.ring_global + ((size_t)blockIdx.x * G + grp) * kp.num_slots * W);
-    uint32_t* const cnt = smem + G * gw;
-    // then the per-warp noise scratch, and a 16-byte aligned tail: the stream
-    // ops, then the threshold tables
-    const size_t wscr_word = (size_t)(cnt + (kp.counts_in_smem ? kp.num_cols : 0) - smem);
-    uint32_t* const wscr = smem + wscr_word + (size_t)(threadIdx.x >> 5) * WSCR;
-    const size_t dsc_word = (wscr_word + (size_t)(blockDim.x >> 5) * WSCR + 3) & ~(size_t)3;
-    uint4* const dsc_s = reinterpret_cast<uint4*>(smem + dsc_word);
+    uint32_t* const cnt = smem + fm.fr0 + (uint32_t)G * gw;
+    const uint4* const dsc_s = reinterpret_cast<const uint4*>(smem + fm.dsc_word);
     const uint4* const dsc_g = reinterpret_cast<const uint4*>(kp.sops);
     const bool dsm = kp.desc_in_smem != 0;
-    auto ldesc = [&](int i) -> uint4 { return dsm ? dsc_s[i] : __ldg(dsc_g + i); };
-    // per-thread scratch of the general noise path (global, L1-resident)
-    uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
-    const bool use_lists = kp.hits_global != nullptr && kp.masks == nullptr;
+    const bool use_lists = !GENERAL || (kp.hits_global != nullptr && kp.masks == nullptr);
     const uint32_t bar_id = 1u + (uint32_t)grp;
     auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gsz) : "memory"); };
     uint32_t* const XB = X + (lane & (C - 1)) * V;  // this lane's vector of every row
 
-    if (kp.counts_in_smem)
-        for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
-    if (dsm)
-        for (int i = threadIdx.x; i < 3 * kp.n_ops; i += blockDim.x) dsc_s[i] = __ldg(dsc_g + i);
-    __syncthreads();
-
-    for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
-        const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
-        const unsigned long long* const hits = kp.hits_global + tile * kp.hit_block;
-        const uint2* const spans = kp.spans_global + (tile * kp.num_noise) * kp.list_warps + warp;
-        HitPipe hp{make_uint2(NO_SLOT, 0u), 0ull};
-        if (use_lists && kp.first_span != NO_SLOT) hp.nsp = __ldg(spans + kp.first_span);
+    const unsigned long long* const hits = kp.hits_global + tile * kp.hit_block;
+    const uint2* const spans = kp.spans_global + (tile * kp.num_noise) * kp.list_warps + warp;
+    HitPipe hp{make_uint2(NO_SLOT, 0u), 0ull};
+    if (use_lists && kp.first_span != NO_SLOT) hp.nsp = __ldg(spans + kp.first_span);
+    {
         // ---- FrameBatch.__init__: x = 0, z = coin rows 0..n-1 (frame_sim.py:36-39) ----
+        const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
         for (int i = tid; i < (n << LC); i += nth) {
             const int q = i >> LC, c = i & (C - 1);
             const uint32_t row = __ldg(kp.row_of + q);
@@ -819,165 +839,202 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
             const int k = i >> LC, c = i & (C - 1);
             vst<V>(ring + (size_t)k * W + c * V, vzero<V>());
         }
-        if (use_lists) hp.e0n = first_entry(hits, hp.nsp, lane);
-        group_sync();
+    }
+    if (use_lists) hp.e0n = first_entry(hits, hp.nsp, lane);
+    group_sync();
 
-        // descriptors run one op ahead in registers
-        uint4 n0 = make_uint4(0, 0, 0, 0), n1 = n0, n2 = n0;
-        if (kp.n_ops > 0) { n0 = ldesc(0); n1 = ldesc(1); n2 = ldesc(2); }
-        for (int oi = 0; oi < kp.n_ops; oi++) {
-            const uint4 d0 = n0, d1 = n1, d2 = n2;
-            if (oi + 1 < kp.n_ops) {
-                n0 = ldesc(3 * oi + 3); n1 = ldesc(3 * oi + 4); n2 = ldesc(3 * oi + 5);
-                // pull the next op's operand block into L1 while this op runs
-                const uint32_t lines = (n2.x * 4u + 127u) >> 7;
-                for (uint32_t l = (uint32_t)tid; l < lines; l += (uint32_t)nth)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(kp.arena + n0.z + 32u * l));
-            }
-            const uint32_t kind = d0.x & 0xFFu, code = (d0.x >> 8) & 0xFFu, flags = d0.x >> 16;
-            const uint32_t count = d0.y, off = d0.z, K = d0.w;
-            const bool fz = (flags & F_NOISE) != 0;
-            // this op's pre-sampled hits; start the next pre-sampled op's span load
-            const bool pre = use_lists && (flags & F_PRESAMPLED);
-            uint2 sp = make_uint2(NO_SLOT, 0u);
-            unsigned long long e0 = 0ull;
-            if (pre) {
-                sp = hp.nsp;
-                e0 = hp.e0n;
-                hp.nsp = __ldg(spans + d1.w);
-            }
-            if (flags & F_BARRIER) group_sync();
-#if PFS_PROFILE
-            if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
-                tile == 0)  // profiling: op-boundary timestamps of the first tile
-                kp.op_clock[oi] = clock64();
-            if (kp.debug_skip) {
-                const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
-                                   : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
-                if (kp.debug_skip & bit) continue;
-            }
-#endif
-            // the fused noise of this warp's applications (Kc per warp)
-            auto fused_noise = [&](uint32_t Kc) {
-#if PFS_PROFILE
-                if (kp.debug_skip & 2) return;
-#endif
-                if (pre && sp.x != NO_SLOT) {
-                    __syncwarp();  // the warp's row updates are visible to the lanes applying hits
-                    uint32_t j = sp.x + (uint32_t)lane;
-                    if (j < sp.y) apply_hit_entry<W>(X, Z, e0);
-                    for (j += 32u; j < sp.y; j += 32u) apply_hit_entry<W>(X, Z, __ldg(hits + j));
-                    __syncwarp();
-                } else {
-                    fused_noise_general<W>(kp, tk, oi, Kc, X, Z, sl, wscr, warp, lane, tile);
-                }
-            };
-
-            switch (kind) {
-            case K_GATE: {
-                const uint32_t* const blk = kp.arena + off + (uint32_t)warp * K * PI + (lane >> LC);
-                switch (code) {
-                    case R_SWAPXZ: gate_stream<W, R_SWAPXZ>(XB, zoff, blk, K); break;
-                    case R_ZXORX: gate_stream<W, R_ZXORX>(XB, zoff, blk, K); break;
-                    case R_XXORZ: gate_stream<W, R_XXORZ>(XB, zoff, blk, K); break;
-                    case R_CX: gate_stream<W, R_CX>(XB, zoff, blk, K); break;
-                    case R_CZ: gate_stream<W, R_CZ>(XB, zoff, blk, K); break;
-                    case R_CY: gate_stream<W, R_CY>(XB, zoff, blk, K); break;
-                    case R_SWAP: gate_stream<W, R_SWAP>(XB, zoff, blk, K); break;
-                    default: break;
-                }
-                if (fz) fused_noise(d2.z);
-                break;
-            }
-            case K_R: case K_M: case K_MR: case K_SPILL: {
-                uint32_t A0, A1;
-                warp_share_of(count, K, warp, A0, A1);
-                // fused noise precedes a measurement (X_ERROR before M), follows a reset
-                if (fz && kind != K_R) fused_noise(K);
-                if (A0 < A1)
-                    collapse_stream<W>(kp, tk, X, Z, ring, reinterpret_cast<const uint2*>(kp.arena + off), kind, A0, A1,
-                                       d1.x, d1.y, lane, tile);
-                if (fz && kind == K_R) fused_noise(K);
-                break;
-            }
-            case K_NOISE:
-#if PFS_PROFILE
-                if (kp.debug_skip & 2) break;
-#endif
-                noise_general<W>(kp, tk, oi, X, Z, sl, wscr, tid, nth, tile);
-                break;
-            case K_DET: {
-                const uint32_t oa = d1.x;
-                const int items = (int)(count << LC);
-                // a term is a ring slot, or XROW | row: the record still in that
-                // x row.  Uniform ops (code = terms per column) read their terms
-                // from the arena block, the others through the CSR arrays.
-                auto src = [&](uint32_t t) -> const uint32_t* {
-                    return (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
-                };
-                const uint32_t* const tb = code ? kp.arena : kp.det_terms;
-                batched_items<2>(tid, nth, items,
-                    [&](int i) {
-                        const uint32_t ci = (uint32_t)(i >> LC);
-                        const uint32_t col = oa + ci;
-                        uint32_t e0, e1;
-                        if (code) { e0 = off + ci * code; e1 = e0 + code; }
-                        else { e0 = __ldg(kp.det_ptr + col); e1 = __ldg(kp.det_ptr + col + 1); }
-                        const uint32_t s0 = e0 < e1 ? __ldg(tb + e0) : NO_SLOT;
-                        const uint32_t s1 = e0 + 1 < e1 ? __ldg(tb + e0 + 1) : NO_SLOT;
-                        return make_uint4(e0, e1, s0, s1);
-                    },
-                    [&](int i, uint4 d) {
-                        const uint32_t col = oa + (uint32_t)(i >> LC);
-                        const int c = i & (C - 1);
-                        VW<V> acc = vzero<V>();
-                        if (d.z != NO_SLOT) acc = vld<V>(src(d.z) + c * V);
-                        if (d.w != NO_SLOT) acc = vxor<V>(acc, vld<V>(src(d.w) + c * V));
-                        for (uint32_t e = d.x + 2; e < d.y; e++) acc = vxor<V>(acc, vld<V>(src(__ldg(tb + e)) + c * V));
-                        if (kp.ev_out != nullptr)
-                            vst<V>(kp.ev_out + (int64_t)col * kp.out_row_stride + tile * kp.out_tile_stride + c * V, acc);
-                        if (kp.counts != nullptr) {
-                            uint32_t tot = 0;
-#pragma unroll
-                            for (int jw = 0; jw < V; jw++) {
-                                const int64_t s0 = tile * (int64_t)(32 * W) + 32 * (c * V + jw);
-                                const int64_t rem = kp.num_shots - s0;
-                                const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
-                                tot += __popc(acc.w[jw] & m);
-                            }
-                            if (tot) {
-                                if (kp.counts_in_smem) atomicAdd(cnt + col, tot);
-                                else atomicAdd(kp.counts + col, (unsigned long long)tot);
-                            }
-                        }
-                    });
-                break;
-            }
-            case K_OBS: {
-                const uint32_t oa = d1.x;
-                const uint32_t* const tg = kp.arena + off;
-                for (int c = tid; c < C; c += nth) {
-                    VW<V> acc = vld<V>(ring + (size_t)oa * W + c * V);
-                    for (uint32_t j = 0; j < count; j++) {
-                        const uint32_t t = __ldg(tg + j);
-                        const uint32_t* s = (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
-                        acc = vxor<V>(acc, vld<V>(s + c * V));
-                    }
-                    vst<V>(ring + (size_t)oa * W + c * V, acc);
-                }
-                break;
-            }
-            default: break;
-            }
-            // the next pre-sampled op's first hit entry (its span has arrived by now)
-            if (pre) hp.e0n = first_entry(hits, hp.nsp, lane);
-#if PFS_PROFILE
-            if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tile == 0 &&
-                (tid & 31) == 0 && (tid >> 5) < 8)  // profiling: per-warp end of op work
-                kp.op_clock[(size_t)kp.n_ops * (1 + (tid >> 5)) + oi] = clock64();
-#endif
+    for (int oi = 0; oi < kp.n_ops; oi++) {
+        uint4 d0, d1, d2;
+        if (dsm) { d0 = dsc_s[3 * oi]; d1 = dsc_s[3 * oi + 1]; d2 = dsc_s[3 * oi + 2]; }
+        else {
+            d0 = __ldg(dsc_g + 3 * oi); d1 = __ldg(dsc_g + 3 * oi + 1); d2 = __ldg(dsc_g + 3 * oi + 2);
+            if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(dsc_g + 3 * oi + 6));
         }
-        group_sync();  // the group's frame is reused by its next tile
+        {
+            // pull the next op's operand block (d2.x words at arena + d2.w)
+            // into L1 while this op runs
+            const uint32_t lines = (d2.x * 4u + 127u) >> 7;
+            for (uint32_t l = (uint32_t)tid; l < lines; l += (uint32_t)nth)
+                asm volatile("prefetch.global.L1 [%0];" ::"l"(kp.arena + d2.w + 32u * l));
+        }
+        const uint32_t kind = d0.x & 0xFFu, code = (d0.x >> 8) & 0xFFu, flags = d0.x >> 16;
+        const uint32_t count = d0.y, off = d0.z, K = d0.w;
+        const bool fz = (flags & F_NOISE) != 0;
+        // this op's pre-sampled hits: its span (prefetched); start the next
+        // pre-sampled op's span load
+        const bool pre = GENERAL ? (use_lists && (flags & F_PRESAMPLED)) : fz;
+        uint2 sp = make_uint2(NO_SLOT, 0u);
+        if (pre) {
+            sp = hp.nsp;
+            hp.nsp = __ldg(spans + d1.w);
+        }
+        if (flags & F_BARRIER) group_sync();
+#if PFS_PROFILE
+        if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
+            tile == 0)  // profiling: op-boundary timestamps of the first tile
+            kp.op_clock[oi] = clock64();
+        if (kp.debug_skip) {
+            const uint32_t bit = kind == K_NOISE ? 1u : kind == K_DET ? 8u : kind == K_GATE ? 16u
+                               : (kind == K_M || kind == K_R || kind == K_MR) ? 32u : 0u;
+            if (kp.debug_skip & bit) continue;
+        }
+#endif
+        // the fused noise of this warp's applications (Kc per warp), then
+        // the first entry of the next pre-sampled op (its span has arrived)
+        auto fused_noise = [&](uint32_t Kc) {
+#if PFS_PROFILE
+            if (kp.debug_skip & 2) return;
+#endif
+            if (!GENERAL || (pre && sp.x != NO_SLOT)) {
+                __syncwarp();  // the warp's row updates are visible to the lanes applying hits
+                uint32_t j = sp.x + (uint32_t)lane;
+                if (j < sp.y) apply_hit_entry<W>(X, Z, hp.e0n);
+                for (j += 32u; j < sp.y; j += 32u) apply_hit_entry<W>(X, Z, __ldg(hits + j));
+                __syncwarp();
+            } else if (GENERAL) {
+                fused_noise_general<W>(kp, oi, Kc, xg, tile);
+            }
+            if (pre) hp.e0n = first_entry(hits, hp.nsp, lane);
+        };
+
+        switch (kind) {
+        case K_GATE: {
+            const uint32_t* const blk = kp.arena + off + (uint32_t)warp * K * PI + (lane >> LC);
+            switch (code) {
+                case R_SWAPXZ: gate_stream<W, R_SWAPXZ>(XB, zoff, blk, K); break;
+                case R_ZXORX: gate_stream<W, R_ZXORX>(XB, zoff, blk, K); break;
+                case R_XXORZ: gate_stream<W, R_XXORZ>(XB, zoff, blk, K); break;
+                case R_CX: gate_stream<W, R_CX>(XB, zoff, blk, K); break;
+                case R_CZ: gate_stream<W, R_CZ>(XB, zoff, blk, K); break;
+                case R_CY: gate_stream<W, R_CY>(XB, zoff, blk, K); break;
+                case R_SWAP: gate_stream<W, R_SWAP>(XB, zoff, blk, K); break;
+                default: break;
+            }
+            if (fz) fused_noise(d2.z);
+            break;
+        }
+        case K_R: case K_M: case K_MR: case K_SPILL: {
+            uint32_t A0, A1;
+            warp_share_of(count, K, warp, A0, A1);
+            // fused noise precedes a measurement (X_ERROR before M), follows a reset
+            if (fz && kind != K_R) fused_noise(K);
+            if (A0 < A1) {
+                const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
+                collapse_stream<W>(kp, tk, X, Z, ring, reinterpret_cast<const uint2*>(kp.arena + off), kind, A0, A1,
+                                   d1.x, d1.y, lane, tile);
+            }
+            if (fz && kind == K_R) fused_noise(K);
+            break;
+        }
+        case K_NOISE:
+#if PFS_PROFILE
+            if (kp.debug_skip & 2) break;
+#endif
+            if (GENERAL) noise_general<W>(kp, oi, xg, tile);
+            break;
+        case K_DET: {
+            const uint32_t oa = d1.x;
+            const int items = (int)(count << LC);
+            // a term is a ring slot, or XROW | row: the record still in that
+            // x row.  Uniform ops (code = terms per column) read their terms
+            // from the arena block, the others through the CSR arrays.
+            auto src = [&](uint32_t t) -> const uint32_t* {
+                return (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
+            };
+            const uint32_t* const tb = code ? kp.arena : kp.det_terms;
+            batched_items<2>(tid, nth, items,
+                [&](int i) {
+                    const uint32_t ci = (uint32_t)(i >> LC);
+                    const uint32_t col = oa + ci;
+                    uint32_t e0, e1;
+                    if (code) { e0 = off + ci * code; e1 = e0 + code; }
+                    else { e0 = __ldg(kp.det_ptr + col); e1 = __ldg(kp.det_ptr + col + 1); }
+                    const uint32_t s0 = e0 < e1 ? __ldg(tb + e0) : NO_SLOT;
+                    const uint32_t s1 = e0 + 1 < e1 ? __ldg(tb + e0 + 1) : NO_SLOT;
+                    return make_uint4(e0, e1, s0, s1);
+                },
+                [&](int i, uint4 d) {
+                    const uint32_t col = oa + (uint32_t)(i >> LC);
+                    const int c = i & (C - 1);
+                    VW<V> acc = vzero<V>();
+                    if (d.z != NO_SLOT) acc = vld<V>(src(d.z) + c * V);
+                    if (d.w != NO_SLOT) acc = vxor<V>(acc, vld<V>(src(d.w) + c * V));
+                    for (uint32_t e = d.x + 2; e < d.y; e++) acc = vxor<V>(acc, vld<V>(src(__ldg(tb + e)) + c * V));
+                    if (kp.ev_out != nullptr)
+                        vst<V>(kp.ev_out + (int64_t)col * kp.out_row_stride + tile * kp.out_tile_stride + c * V, acc);
+                    if (kp.counts != nullptr) {
+                        uint32_t tot = 0;
+#pragma unroll
+                        for (int jw = 0; jw < V; jw++) {
+                            const int64_t s0 = tile * (int64_t)(32 * W) + 32 * (c * V + jw);
+                            const int64_t rem = kp.num_shots - s0;
+                            const uint32_t m = rem >= 32 ? 0xFFFFFFFFu : (rem <= 0 ? 0u : ((1u << rem) - 1u));
+                            tot += __popc(acc.w[jw] & m);
+                        }
+                        if (tot) {
+                            if (kp.counts_in_smem) atomicAdd(cnt + col, tot);
+                            else atomicAdd(kp.counts + col, (unsigned long long)tot);
+                        }
+                    }
+                });
+            break;
+        }
+        case K_OBS: {
+            const uint32_t oa = d1.x;
+            const uint32_t* const tg = kp.arena + off;
+            for (int c = tid; c < C; c += nth) {
+                VW<V> acc = vld<V>(ring + (size_t)oa * W + c * V);
+                for (uint32_t j = 0; j < count; j++) {
+                    const uint32_t t = __ldg(tg + j);
+                    const uint32_t* s = (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
+                    acc = vxor<V>(acc, vld<V>(s + c * V));
+                }
+                vst<V>(ring + (size_t)oa * W + c * V, acc);
+            }
+            break;
+        }
+        default: break;
+        }
+#if PFS_PROFILE
+        if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tile == 0 &&
+            (tid & 31) == 0 && (tid >> 5) < 8)  // profiling: per-warp end of op work
+            kp.op_clock[(size_t)kp.n_ops * (1 + (tid >> 5)) + oi] = clock64();
+#endif
+    }
+    group_sync();  // the group's frame is reused by its next tile
+}
+
+template <int W, bool RING_SMEM>
+__device__ __noinline__ void frame_tile_general(const KParams& kp, const int64_t tile) {
+    frame_tile_body<W, RING_SMEM, true>(kp, tile);
+}
+
+// Persistent kernel: kp.groups independent thread groups per CTA, each with
+// its own tile, frame (x plane, z plane), record ring and named barrier — one
+// group's op latency overlaps the other group's work.
+template <int W, bool RING_SMEM>
+__global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __grid_constant__ KParams kp) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    const int G = kp.groups;
+    const int grp = threadIdx.x / (blockDim.x / G);
+    const FrameMap fm = frame_map(kp);
+    const uint32_t gw = 2u * (uint32_t)kp.num_qubits * W + (RING_SMEM ? (uint32_t)kp.num_slots * W : 0u);
+    uint32_t* const cnt = smem + fm.fr0 + (uint32_t)G * gw;
+    if (kp.counts_in_smem)
+        for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
+    if (kp.desc_in_smem) {
+        uint4* const d = reinterpret_cast<uint4*>(smem + fm.dsc_word);
+        const uint4* const dsc_g = reinterpret_cast<const uint4*>(kp.sops);
+        for (int i = threadIdx.x; i < 3 * kp.n_ops; i += blockDim.x) d[i] = __ldg(dsc_g + i);
+    }
+    __syncthreads();
+    for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
+        // the hot loop serves programs whose noise is all fused and pre-sampled,
+        // for tiles whose hit lists all fitted (noise_kernel's overflow mark)
+        const bool fast = kp.all_presampled && kp.hits_global != nullptr && kp.masks == nullptr &&
+                          __ldg(kp.fill_global + 2 * tile + 1) == 0u;
+        if (fast) frame_tile_body<W, RING_SMEM, false>(kp, tile);
+        else frame_tile_general<W, RING_SMEM>(kp, tile);
     }
     if (kp.counts_in_smem) {
         __syncthreads();
