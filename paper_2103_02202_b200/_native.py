@@ -214,9 +214,9 @@ class NativeProgram:
         return list(arr)
 
     def op_clock(self) -> np.ndarray:
-        out = np.zeros(self.info["num_ops"] * 9, dtype=np.int64)
+        out = np.zeros(self.info["num_ops"] * 12, dtype=np.int64)
         _check(lib().pfs_program_op_clock(self._h, _p(out), out.size))
-        return out.reshape(9, self.info["num_ops"])
+        return out.reshape(12, self.info["num_ops"])
 
     def ops(self) -> np.ndarray:
         out = np.zeros((self.info["num_ops"], 2), dtype=np.uint32)

@@ -710,6 +710,10 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.arena = fl.arena.p;
     kp.first_span = hp.first_span;
     kp.all_presampled = hp.all_presampled ? 1 : 0;
+    {
+        const char* e = std::getenv("PFS_STAGGER");  // experiment: group start offset in cycles
+        kp.stagger = e ? std::atoi(e) : 0;
+    }
     kp.targets = fl.targets.p;
     kp.det_ptr = fl.det_ptr.p;
     kp.det_terms = fl.det_terms.p;
@@ -737,7 +741,8 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
                                              : (size_t)cfg.grid * cfg.threads * NZ_MAX_LIST));
     kp.noise_scratch = pg->d_nscratch.p;
     if (pg->opts.debug_skip & 64) {  // op-boundary clock trace of the first tile
-        CUDA_TRY(pg->d_clock.reserve(hp.ops.size() * 9 + 1));
+        CUDA_TRY(pg->d_clock.reserve(hp.ops.size() * 12 + 1));
+        CUDA_TRY(cudaMemsetAsync(pg->d_clock.p, 0, (hp.ops.size() * 12 + 1) * sizeof(long long), st));
         kp.op_clock = pg->d_clock.p;
     }
 
@@ -1035,7 +1040,7 @@ extern "C" int pfs_write_format(int device, const uint8_t* b8, int64_t in_pitch,
 extern "C" int pfs_program_op_clock(pfs_program* pg, long long* out, int64_t n) {
     if (!pg || !out) return fail(PFS_E_INVALID, "null argument");
     if (!pg->d_clock.p) return fail(PFS_E_INVALID, "no clock trace (set debug_skip bit 6)");
-    const int64_t m = std::min<int64_t>(n, (int64_t)pg->fl[PM_EVENTS].hp.ops.size() * 9);
+    const int64_t m = std::min<int64_t>(n, (int64_t)pg->fl[PM_EVENTS].hp.ops.size() * 12);
     CUDA_TRY(cudaMemcpy(out, pg->d_clock.p, m * sizeof(long long), cudaMemcpyDeviceToHost));
     return PFS_OK;
 }

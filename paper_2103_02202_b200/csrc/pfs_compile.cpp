@@ -712,7 +712,7 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
     const uint32_t PI = 32u / (uint32_t)C;  // applications per warp pass
     const uint32_t nw = (uint32_t)std::max(1, warps_per_group);
     const int G = bank_groups(W);
-    if (hp.num_qubits >= 65536) bad("frame rows exceed the 16-bit operand format");
+    if (hp.num_qubits + DUMMY_ROWS >= 65536) bad("frame rows exceed the 16-bit operand format");
     hp.sops.assign(hp.ops.size(), SOp{});
     hp.arena.clear();
     hp.first_span = NO_SLOT;
@@ -758,7 +758,12 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
             const int ar = rule_arity(code);
             const uint32_t Kc = warp_share(o.count, nw, ca);
             const uint32_t passes = (Kc + PI - 1) / PI;
-            blk.assign((size_t)nw * passes * PI, STREAM_NOP);
+            // padding applications act on the group's dummy rows (rows num_qubits ..)
+            blk.resize((size_t)nw * passes * PI);
+            for (size_t j = 0; j < blk.size(); j++) {
+                const uint32_t dr = (uint32_t)hp.num_qubits + (uint32_t)(j % DUMMY_ROWS);
+                blk[j] = dr | (dr << 16);
+            }
             for (uint32_t w = 0; w < nw; w++) {
                 const uint32_t A0 = std::min(o.count, w * Kc), A1 = std::min(o.count, A0 + Kc);
                 if (A0 >= A1) continue;
@@ -823,7 +828,7 @@ void build_hit_lists(HostProgram& hp, int tile_shots, int warps_per_group) {
         // consumer warps per noise_kernel item: as many as keep the item's hits
         // (mean + 6 sigma + slack) within one warp's staging buffer
         const double per_warp = (double)K * tile_shots * p;
-        uint32_t wpi = nw;
+        uint32_t wpi = std::min<uint32_t>(nw, 16u);  // noise_kernel tags a hit's consumer warp in 4 bits
         while (wpi > 0 && per_warp * wpi + 6.0 * std::sqrt(per_warp * wpi) + 16.0 > (double)NK_SCR) wpi--;
         if (wpi == 0) continue;  // heavy noise: drawn by the consumer
         uint32_t* fi = &hp.fused_info[(size_t)o.c * 4];

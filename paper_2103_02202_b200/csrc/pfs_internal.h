@@ -103,6 +103,10 @@ struct SOp {
 };
 static_assert(sizeof(SOp) == 48, "SOp is 48 bytes");
 constexpr uint32_t STREAM_NOP = 0xFFFFFFFFu;
+// Padding words of a gate block name dummy frame rows (rows num_qubits ..):
+// no lane is predicated off; consecutive padding applications take different
+// dummy rows so that they fall into different shared-memory bank groups.
+constexpr int DUMMY_ROWS = 4;
 
 // Per noise instruction sampling schedule for one tile, also
 // exported to the parity oracle through pfs_program_noise_schedule.
@@ -232,6 +236,7 @@ struct KParams {
                                       // block (begin NO_SLOT: the warp draws inline)
     uint32_t* fill_global;            // [tiles][2]: entries used (noise_kernel allocation), overflow mark
     int32_t all_presampled;           // every noise instruction is fused and pre-sampled (hot frame loop)
+    int32_t stagger;                  // cycles group g waits (g * stagger) before its first tile
     const uint2* hit_items;           // noise_kernel items of one tile
     int64_t hit_block;
     int32_t list_warps;

@@ -474,42 +474,111 @@ __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, u
 #ifndef PFS_GATE_BATCH
 #define PFS_GATE_BATCH 2
 #endif
-constexpr int GATE_BATCH = PFS_GATE_BATCH;  // operand words in flight per lane
+constexpr int GATE_BATCH = PFS_GATE_BATCH;  // applications whose rows a lane loads before it stores any
+#ifndef PFS_GATE_AHEAD
+#define PFS_GATE_AHEAD 6
+#endif
+constexpr int GATE_AHEAD = PFS_GATE_AHEAD;   // operand words of the next gate op held in registers
+
+// Shared-memory vectors by 32-bit shared address (gate hot path: explicit
+// address arithmetic, loads of a batch issued before its stores)
+template <int V> __device__ __forceinline__ VW<V> slds(uint32_t a);
+template <> __device__ __forceinline__ VW<4> slds<4>(uint32_t a) {
+    VW<4> v;
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.w[0]), "=r"(v.w[1]), "=r"(v.w[2]), "=r"(v.w[3]) : "r"(a));
+    return v;
+}
+template <> __device__ __forceinline__ VW<2> slds<2>(uint32_t a) {
+    VW<2> v;
+    asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.w[0]), "=r"(v.w[1]) : "r"(a));
+    return v;
+}
+template <> __device__ __forceinline__ VW<1> slds<1>(uint32_t a) {
+    VW<1> v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v.w[0]) : "r"(a));
+    return v;
+}
+template <int V> __device__ __forceinline__ void ssts(uint32_t a, const VW<V>& v);
+template <> __device__ __forceinline__ void ssts<4>(uint32_t a, const VW<4>& v) {
+    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(a), "r"(v.w[0]), "r"(v.w[1]), "r"(v.w[2]), "r"(v.w[3]) : "memory");
+}
+template <> __device__ __forceinline__ void ssts<2>(uint32_t a, const VW<2>& v) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(a), "r"(v.w[0]), "r"(v.w[1]) : "memory");
+}
+template <> __device__ __forceinline__ void ssts<1>(uint32_t a, const VW<1>& v) {
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(a), "r"(v.w[0]) : "memory");
+}
+
+// One batch of gate applications for this lane: operand word = row of target 0
+// | row of target 1 << 16 (padding words name the group's dummy row, so no
+// lane is predicated off); bx / bz = shared addresses of this lane's vector of
+// row 0 in the x / z plane.  All rows of the batch are loaded before any store
+// (the applications of an op are independent).
+template <int W, uint32_t RULE, int U>
+__device__ __forceinline__ void gate_batch(uint32_t bx, uint32_t bz, const uint32_t (&w)[U]) {
+    constexpr int V = W >= 4 ? 4 : W;
+    constexpr int ar = RULE >= R_CX ? 2 : 1;
+    constexpr uint32_t RB = W * 4;  // row bytes
+    uint32_t oa[U], ob[U];
+    VW<V> x0[U], z0[U], x1[U], z1[U];
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        oa[u] = (w[u] & 0xFFFFu) * RB;
+        x0[u] = slds<V>(bx + oa[u]);
+        z0[u] = slds<V>(bz + oa[u]);
+        if (ar == 2) {
+            ob[u] = (w[u] >> 16) * RB;
+            x1[u] = slds<V>(bx + ob[u]);
+            z1[u] = slds<V>(bz + ob[u]);
+        }
+    }
+#pragma unroll
+    for (int u = 0; u < U; u++) {
+        apply_rule<V>(RULE, x0[u], z0[u], x1[u], z1[u]);
+        if (ar == 1) {
+            if (RULE != R_ZXORX) ssts<V>(bx + oa[u], x0[u]);
+            if (RULE != R_XXORZ) ssts<V>(bz + oa[u], z0[u]);
+        } else {
+            if (RULE != R_CZ) ssts<V>(bx + ob[u], x1[u]);
+            if (RULE == R_SWAP) ssts<V>(bx + oa[u], x0[u]);
+            ssts<V>(bz + oa[u], z0[u]);
+            if (RULE != R_CX) ssts<V>(bz + ob[u], z1[u]);
+        }
+    }
+}
+
 // One gate op in stream form (SOp, lower_stream): the warp's block of packed
-// operand words, one word per application (row of target 0 | row of target 1
-// << 16), PI = 32 / C applications per warp pass; the C lanes that share an
-// application take one V-word vector of its rows each.  XB = the group's x
-// plane + this lane's vector offset, zoff = words from the x to the z plane.
-// Four operand words are in flight per lane.
+// operand words, one word per application, PI = 32 / C applications per warp
+// pass; the C lanes that share an application take one V-word vector of its
+// rows each.  The words of the first GATE_AHEAD passes arrive in registers
+// (pw, loaded while the previous op ran); later passes load one batch ahead.
 template <int W, uint32_t RULE>
-__device__ __forceinline__ void gate_stream(uint32_t* XB, uint32_t zoff, const uint32_t* blk, uint32_t K) {
+__device__ __forceinline__ void gate_stream(uint32_t bx, uint32_t bz, const uint32_t* blk, uint32_t K,
+                                            const uint32_t (&pw)[GATE_AHEAD], uint32_t nop) {
     constexpr int V = W >= 4 ? 4 : W;
     constexpr int PI = 32 / (W / V);
-    constexpr int ar = RULE >= R_CX ? 2 : 1;
     constexpr int U = GATE_BATCH;
-    for (uint32_t k0 = 0; k0 < K; k0 += U) {
-        uint32_t w[U];
+    static_assert(GATE_AHEAD % U == 0, "whole batches ahead");
 #pragma unroll
-        for (int u = 0; u < U; u++) w[u] = (k0 + u < K) ? __ldg(blk + (k0 + u) * PI) : STREAM_NOP;
+    for (int k = 0; k < GATE_AHEAD; k += U) {
+        if ((uint32_t)k < K) {
+            uint32_t w[U];
 #pragma unroll
-        for (int u = 0; u < U; u++) {
-            if (w[u] == STREAM_NOP) continue;
-            uint32_t* const pa = XB + (w[u] & 0xFFFFu) * W;
-            if (ar == 1) {
-                VW<V> x0 = vld<V>(pa), z0 = vld<V>(pa + zoff), x1, z1;
-                apply_rule<V>(RULE, x0, z0, x1, z1);
-                if (RULE != R_ZXORX) vst<V>(pa, x0);
-                if (RULE != R_XXORZ) vst<V>(pa + zoff, z0);
-            } else {
-                uint32_t* const pb = XB + (w[u] >> 16) * W;
-                VW<V> x0 = vld<V>(pa), x1 = vld<V>(pb);
-                VW<V> z0 = vld<V>(pa + zoff), z1 = vld<V>(pb + zoff);
-                apply_rule<V>(RULE, x0, z0, x1, z1);
-                if (RULE != R_CZ) vst<V>(pb, x1);
-                if (RULE == R_SWAP) vst<V>(pa, x0);
-                vst<V>(pa + zoff, z0);
-                if (RULE != R_CX) vst<V>(pb + zoff, z1);
-            }
+            for (int u = 0; u < U; u++) w[u] = pw[k + u];
+            gate_batch<W, RULE, U>(bx, bz, w);
+        }
+    }
+    if (K > (uint32_t)GATE_AHEAD) {
+        uint32_t c[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) c[u] = (GATE_AHEAD + u < K) ? __ldg(blk + (GATE_AHEAD + u) * PI) : nop;
+        for (uint32_t k = GATE_AHEAD; k < K; k += U) {
+            uint32_t nx[U];
+#pragma unroll
+            for (int u = 0; u < U; u++) nx[u] = (k + U + u < K) ? __ldg(blk + (k + U + u) * PI) : nop;
+            gate_batch<W, RULE, U>(bx, bz, c);
+#pragma unroll
+            for (int u = 0; u < U; u++) c[u] = nx[u];
         }
     }
 }
@@ -556,7 +625,7 @@ __device__ __noinline__ void fused_noise_general(const KParams& kp, int oi, uint
     uint32_t* const X = smem + xg;
     uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
     warp_range_noise<W>(kp, tk, nz, kp.noise_tab, o.count, A0, A1, kp.targets + o.off, ar, pairs, X,
-                        X + (size_t)kp.num_qubits * W, sl, smem + (threadIdx.x >> 5) * WSCR, tid & 31, rowb, tile);
+                        X + (size_t)(kp.num_qubits + DUMMY_ROWS) * W, sl, smem + (threadIdx.x >> 5) * WSCR, tid & 31, rowb, tile);
 }
 
 // A standalone noise op (reads its DOp), out of line
@@ -570,7 +639,7 @@ __device__ __noinline__ void noise_general(const KParams& kp, int oi, uint32_t x
     const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
     uint32_t* const X = smem + xg;
     uint32_t* const sl = kp.noise_scratch + ((size_t)blockIdx.x * blockDim.x + threadIdx.x) * NZ_MAX_LIST;
-    noise_op<W>(kp, tk, X, X + (size_t)kp.num_qubits * W, kp.targets + o.off, (o.kcf >> 8) & 0xFFu, o.count, nz, rowb,
+    noise_op<W>(kp, tk, X, X + (size_t)(kp.num_qubits + DUMMY_ROWS) * W, kp.targets + o.off, (o.kcf >> 8) & 0xFFu, o.count, nz, rowb,
                 kp.noise_tab, sl, smem + (threadIdx.x >> 5) * WSCR, (int)(threadIdx.x % gsz), gsz, tile);
 }
 
@@ -804,7 +873,8 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
     const int tid = threadIdx.x - grp * gsz;  // thread index within the group
     const int nth = gsz;
     const int lane = tid & 31, warp = tid >> 5;
-    const uint32_t zoff = (uint32_t)n * W;
+    // each plane has n rows and DUMMY_ROWS dummy rows (rows n ..): the targets of padding operand words
+    const uint32_t zoff = (uint32_t)(n + DUMMY_ROWS) * W;
     const uint32_t gw = 2u * zoff + (RING_SMEM ? (uint32_t)kp.num_slots * W : 0u);  // words per group
     const FrameMap fm = frame_map(kp);
     const uint32_t xg = fm.fr0 + (uint32_t)grp * gw;  // the group's x plane
@@ -819,7 +889,11 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
     const bool use_lists = !GENERAL || (kp.hits_global != nullptr && kp.masks == nullptr);
     const uint32_t bar_id = 1u + (uint32_t)grp;
     auto group_sync = [&]() { asm volatile("bar.sync %0, %1;" ::"r"(bar_id), "r"(gsz) : "memory"); };
-    uint32_t* const XB = X + (lane & (C - 1)) * V;  // this lane's vector of every row
+    // shared addresses of this lane's vector of row 0 in the x / z plane
+    const uint32_t bx = (uint32_t)__cvta_generic_to_shared(X + (lane & (C - 1)) * V);
+    const uint32_t bz = bx + zoff * 4u;
+    const uint32_t nop = ((uint32_t)n + ((uint32_t)(lane >> LC) & (DUMMY_ROWS - 1))) * 0x10001u;  // a dummy row
+    auto ldesc = [&](int i) -> uint4 { return dsm ? dsc_s[i] : __ldg(dsc_g + i); };
 
     const unsigned long long* const hits = kp.hits_global + tile * kp.hit_block;
     const uint2* const spans = kp.spans_global + (tile * kp.num_noise) * kp.list_warps + warp;
@@ -843,19 +917,42 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
     if (use_lists) hp.e0n = first_entry(hits, hp.nsp, lane);
     group_sync();
 
-    for (int oi = 0; oi < kp.n_ops; oi++) {
-        uint4 d0, d1, d2;
-        if (dsm) { d0 = dsc_s[3 * oi]; d1 = dsc_s[3 * oi + 1]; d2 = dsc_s[3 * oi + 2]; }
-        else {
-            d0 = __ldg(dsc_g + 3 * oi); d1 = __ldg(dsc_g + 3 * oi + 1); d2 = __ldg(dsc_g + 3 * oi + 2);
-            if (lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(dsc_g + 3 * oi + 6));
+    // the first descriptor vector runs one op ahead; a gate op's first
+    // GATE_AHEAD operand words are loaded while the op before it runs
+    uint4 nd0 = kp.n_ops > 0 ? ldesc(0) : make_uint4(0, 0, 0, 0);
+    uint32_t nw[GATE_AHEAD];
+    auto load_ahead = [&]() {
+        if ((nd0.x & 0xFFu) == K_GATE) {
+            const uint32_t* const nblk = kp.arena + nd0.z + (uint32_t)warp * nd0.w * PI + (lane >> LC);
+#pragma unroll
+            for (int j = 0; j < GATE_AHEAD; j++) nw[j] = (uint32_t)j < nd0.w ? __ldg(nblk + j * PI) : nop;
         }
-        {
-            // pull the next op's operand block (d2.x words at arena + d2.w)
-            // into L1 while this op runs
-            const uint32_t lines = (d2.x * 4u + 127u) >> 7;
-            for (uint32_t l = (uint32_t)tid; l < lines; l += (uint32_t)nth)
-                asm volatile("prefetch.global.L1 [%0];" ::"l"(kp.arena + d2.w + 32u * l));
+    };
+#pragma unroll
+    for (int j = 0; j < GATE_AHEAD; j++) nw[j] = nop;
+    load_ahead();
+    for (int oi = 0; oi < kp.n_ops; oi++) {
+#if PFS_PROFILE
+        const bool stamp = kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 && tile == 0;
+        if (stamp) kp.op_clock[(size_t)kp.n_ops * 9 + oi] = clock64();   // op top (before the header)
+#endif
+        const uint4 d0 = nd0;
+        const uint4 d1 = ldesc(3 * oi + 1), d2 = ldesc(3 * oi + 2);
+        uint32_t pw[GATE_AHEAD];
+#pragma unroll
+        for (int j = 0; j < GATE_AHEAD; j++) pw[j] = nw[j];
+        if (oi + 1 < kp.n_ops) {
+            nd0 = ldesc(3 * oi + 3);
+            if (!dsm && lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(dsc_g + 3 * oi + 6));
+            if ((nd0.x & 0xFFu) == K_GATE) {
+                load_ahead();
+            } else {
+                // pull the next op's operand block (d2.x words at arena + d2.w)
+                // toward L1 while this op runs
+                const uint32_t lines = (d2.x * 4u + 127u) >> 7;
+                for (uint32_t l = (uint32_t)tid; l < lines; l += (uint32_t)nth)
+                    asm volatile("prefetch.global.L1 [%0];" ::"l"(kp.arena + d2.w + 32u * l));
+            }
         }
         const uint32_t kind = d0.x & 0xFFu, code = (d0.x >> 8) & 0xFFu, flags = d0.x >> 16;
         const uint32_t count = d0.y, off = d0.z, K = d0.w;
@@ -868,6 +965,9 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
             sp = hp.nsp;
             hp.nsp = __ldg(spans + d1.w);
         }
+#if PFS_PROFILE
+        if (stamp) kp.op_clock[(size_t)kp.n_ops * 11 + oi] = clock64();  // header done, at the barrier
+#endif
         if (flags & F_BARRIER) group_sync();
 #if PFS_PROFILE
         if (kp.op_clock != nullptr && blockIdx.x == 0 && grp == 0 && tid == 0 &&
@@ -890,7 +990,6 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
                 uint32_t j = sp.x + (uint32_t)lane;
                 if (j < sp.y) apply_hit_entry<W>(X, Z, hp.e0n);
                 for (j += 32u; j < sp.y; j += 32u) apply_hit_entry<W>(X, Z, __ldg(hits + j));
-                __syncwarp();
             } else if (GENERAL) {
                 fused_noise_general<W>(kp, oi, Kc, xg, tile);
             }
@@ -901,15 +1000,18 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
         case K_GATE: {
             const uint32_t* const blk = kp.arena + off + (uint32_t)warp * K * PI + (lane >> LC);
             switch (code) {
-                case R_SWAPXZ: gate_stream<W, R_SWAPXZ>(XB, zoff, blk, K); break;
-                case R_ZXORX: gate_stream<W, R_ZXORX>(XB, zoff, blk, K); break;
-                case R_XXORZ: gate_stream<W, R_XXORZ>(XB, zoff, blk, K); break;
-                case R_CX: gate_stream<W, R_CX>(XB, zoff, blk, K); break;
-                case R_CZ: gate_stream<W, R_CZ>(XB, zoff, blk, K); break;
-                case R_CY: gate_stream<W, R_CY>(XB, zoff, blk, K); break;
-                case R_SWAP: gate_stream<W, R_SWAP>(XB, zoff, blk, K); break;
+                case R_SWAPXZ: gate_stream<W, R_SWAPXZ>(bx, bz, blk, K, pw, nop); break;
+                case R_ZXORX: gate_stream<W, R_ZXORX>(bx, bz, blk, K, pw, nop); break;
+                case R_XXORZ: gate_stream<W, R_XXORZ>(bx, bz, blk, K, pw, nop); break;
+                case R_CX: gate_stream<W, R_CX>(bx, bz, blk, K, pw, nop); break;
+                case R_CZ: gate_stream<W, R_CZ>(bx, bz, blk, K, pw, nop); break;
+                case R_CY: gate_stream<W, R_CY>(bx, bz, blk, K, pw, nop); break;
+                case R_SWAP: gate_stream<W, R_SWAP>(bx, bz, blk, K, pw, nop); break;
                 default: break;
             }
+#if PFS_PROFILE
+            if (stamp) kp.op_clock[(size_t)kp.n_ops * 10 + oi] = clock64();  // gate rows done
+#endif
             if (fz) fused_noise(d2.z);
             break;
         }
@@ -1018,7 +1120,7 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
     const int G = kp.groups;
     const int grp = threadIdx.x / (blockDim.x / G);
     const FrameMap fm = frame_map(kp);
-    const uint32_t gw = 2u * (uint32_t)kp.num_qubits * W + (RING_SMEM ? (uint32_t)kp.num_slots * W : 0u);
+    const uint32_t gw = 2u * (uint32_t)(kp.num_qubits + DUMMY_ROWS) * W + (RING_SMEM ? (uint32_t)kp.num_slots * W : 0u);
     uint32_t* const cnt = smem + fm.fr0 + (uint32_t)G * gw;
     if (kp.counts_in_smem)
         for (int i = threadIdx.x; i < kp.num_cols; i += blockDim.x) cnt[i] = 0u;
@@ -1028,6 +1130,14 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
         for (int i = threadIdx.x; i < 3 * kp.n_ops; i += blockDim.x) d[i] = __ldg(dsc_g + i);
     }
     __syncthreads();
+    // The groups of a CTA run the same op sequence; started together they stay
+    // in phase and their shared-memory bursts (the gate rows) collide while the
+    // latency-bound phases (descriptors, barrier, noise hits) leave the pipe
+    // idle.  A start offset per group keeps them out of phase.
+    if (kp.stagger > 0 && grp > 0) {
+        const long long t0 = clock64();
+        while (clock64() - t0 < (long long)grp * kp.stagger) {}
+    }
     for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
         // the hot loop serves programs whose noise is all fused and pre-sampled,
         // for tiles whose hit lists all fitted (noise_kernel's overflow mark)
@@ -1044,7 +1154,8 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
 }
 
 
-size_t frame_smem_bytes(int num_qubits, int W) { return (size_t)2 * num_qubits * W * 4; }
+// x and z planes of num_qubits rows plus the dummy rows padding operand words name
+size_t frame_smem_bytes(int num_qubits, int W) { return (size_t)2 * (num_qubits + DUMMY_ROWS) * W * 4; }
 
 template <int W, bool RS>
 static cudaError_t launch_t(const LaunchCfg& cfg, const KParams& kp, cudaStream_t st) {

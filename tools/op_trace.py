@@ -18,6 +18,7 @@ def main():
     ap.add_argument("--groups", type=int, default=0)
     ap.add_argument("--words", type=int, default=0)
     ap.add_argument("--debug", type=int, default=0)
+    ap.add_argument("--threads", type=int, default=0)
     ap.add_argument("--kernel", type=int, default=0)
     a = ap.parse_args()
     import numpy as np
@@ -27,14 +28,15 @@ def main():
     from paper_2103_02202_b200.sampler import compile_detector_sampler
 
     ds = compile_detector_sampler(gen.config_circuit(a.config), debug_skip=64 | a.debug, groups=a.groups,
-                                  words_per_tile=a.words, kernel=a.kernel)
+                                  words_per_tile=a.words, kernel=a.kernel, threads=a.threads)
     out = torch.empty((ds.num_columns, (a.shots + 31) // 32), dtype=torch.int32, device="cuda")
     for i in range(3):
         ds.sample_rows(a.shots, seed=i, out=out)
     torch.cuda.synchronize()
     clk9 = ds.native.op_clock()
     clk = clk9[0]
-    ends = clk9[1:]  # per-warp (warps 0..7) end of each op's work
+    ends = clk9[1:9]  # per-warp (warps 0..7) end of each op's work
+    top_t, gate_t, hdr_t = clk9[9], clk9[10], clk9[11]  # warp 0: op top, gate rows done, header done
     ops = ds.native.ops()
     dt = np.diff(clk)
     work = ends[:, :-1] - clk[None, :-1]  # per warp: op start (barrier exit) -> own work done
@@ -67,7 +69,25 @@ def main():
         print(f"  {k[0]:6s} code={k[1]} n={n:4d} avg_cycles={c / n:8.0f} avg_count={cnt / n:8.1f} "
               f"warp0_work={w[:, 0].mean():7.0f} warpmax_work={w.max(axis=1).mean():7.0f} "
               f"warpmin_work={w.min(axis=1).mean():7.0f}")
-    top = np.argsort(dt)[::-1][:15]
+    # warp 0 phases: header (top -> at barrier), barrier wait (-> op start), gate rows, noise / rest
+    print("  warp 0 phases per op kind: header | barrier wait | gate rows | rest (noise, collapses, detectors)")
+    ph = collections.defaultdict(lambda: [0, 0, 0, 0, 0])
+    for i in range(len(dt)):
+        k = int(ops[i, 0] & 0xFF)
+        key = (names.get(k, str(k)), int((ops[i, 0] >> 8) & 0xFF))
+        p = ph[key]
+        p[0] += 1
+        p[1] += int(hdr_t[i] - top_t[i])
+        p[2] += int(clk[i] - hdr_t[i])
+        if gate_t[i] > 0:
+            p[3] += int(gate_t[i] - clk[i])
+            p[4] += int(ends[0, i] - gate_t[i])
+        else:
+            p[4] += int(ends[0, i] - clk[i])
+    for k, p in sorted(ph.items()):
+        n = p[0]
+        print(f"  {k[0]:6s} code={k[1]} n={n:4d} header={p[1] / n:7.0f} barrier={p[2] / n:7.0f} gate={p[3] / n:7.0f} rest={p[4] / n:7.0f}")
+    top = np.argsort(dt)[::-1][:5]
     for i in top:
         print(f"  op {i:4d} kind={names.get(int(ops[i, 0] & 0xFF))} code={(ops[i, 0] >> 8) & 0xFF} "
               f"count={ops[i, 1]} cycles={dt[i]}")
