@@ -188,11 +188,12 @@ class PortTimer:
         self.O.rows_to_b8(ev, shots, nthreads=self.threads)
         return time.perf_counter() - t0
 
-    def rate(self, seconds: float, seed: int = 1):
-        """(shots/s, shots, seconds) of one bounded sample of about `seconds`."""
+    def rate(self, seconds: float, seed: int = 1, max_shots: int = 1 << 22):
+        """(shots/s, shots, seconds) of one bounded sample of about `seconds`
+        (at most `max_shots`: a sample never exceeds the step it stands for)."""
         shots = self.T * self.threads
         dt = self.run(shots, seed)  # calibration (also warms the threads)
-        shots = int(min(max(shots / dt * seconds, shots), 1 << 22))
+        shots = int(min(max(shots / dt * seconds, shots), max_shots))
         shots = max(self.T, (shots // self.T) * self.T)
         dt = self.run(shots, seed + 1)
         return shots / dt, shots, dt
@@ -246,7 +247,7 @@ def run_reference(args, rank, world):
     per_step_s = max(2.0, min(args.cpu_seconds, 60.0) / max(1, args.steps))
     rates, sample_shots = [], 0
     for i in range(args.warmup + args.steps):
-        rate, shots, dt = pt.rate(per_step_s, seed=10 + 2 * i)
+        rate, shots, dt = pt.rate(per_step_s, seed=10 + 2 * i, max_shots=shots_cfg)
         if i >= args.warmup:
             rates.append(rate)
             sample_shots = shots
@@ -260,8 +261,8 @@ def run_reference(args, rank, world):
         "data": "synthetic (seeded circuit-level noise, Philox)",
         "config": workload_config(args.config, shots_cfg, world),
         "cpu_baseline": {"value": value, "unit": "shots/s", "cores": cores, "kind": "port",
-                         "sample": f"per step a bounded sample of {sample_shots} of the {shots_cfg} shots "
-                                   f"(ms_per_step extrapolates to the full step) of config {args.config}: C "
+                         "sample": f"per step {sample_shots} of the {shots_cfg} shots (a bounded sample; "
+                                   f"ms_per_step is scaled to the full step) of config {args.config}: C "
                                    f"restatement of stabsim frame_sim + detector_events + b8 transpose on "
                                    f"{cores} threads ({cpu_model()})"},
         "e2e": {"value": value, "unit": "shots/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},

@@ -175,6 +175,17 @@ int pfs_measure_smem_bandwidth(int device, double* gbs);
 int pfs_program_op_clock(struct pfs_program* prog, long long* out, int64_t n);
 int pfs_program_ops(const struct pfs_program* prog, uint32_t* out, int64_t n);
 
+/* Test tooling: the raw tables of a compiled flavour (0 detection events,
+ * 1 measurement records) as uint32 words, for the static schedule verifier
+ * (tests/test_schedule.py: every pair of ops with no group barrier between
+ * them touches disjoint frame rows and ring slots; every application sits in
+ * exactly one warp's operand block).  what: 0 device ops (8 words each),
+ * 1 targets, 2 det_ptr, 3 det_terms, 4 stream ops (12 words each), 5 operand
+ * arena, 6 fused_info (4 words per noise ordinal), 7 row_of.  Copies
+ * min(n, words) words into out (may be NULL) and returns the table's length
+ * in words, or a negative error. */
+int64_t pfs_program_dump(const struct pfs_program* prog, int flavour, int what, uint32_t* out, int64_t n);
+
 void pfs_program_destroy(struct pfs_program* prog);
 const char* pfs_last_error(void);
 int pfs_version(void);

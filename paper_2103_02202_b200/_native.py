@@ -58,7 +58,7 @@ class Info(ctypes.Structure):
 EXPORTS = ("pfs_program_create", "pfs_program_info", "pfs_program_noise_schedule", "pfs_run",
            "pfs_program_last_timing", "pfs_program_last_launches", "pfs_program_destroy",
            "pfs_last_error", "pfs_version", "pfs_measure_smem_bandwidth",
-           "pfs_detector_events", "pfs_program_op_clock", "pfs_program_ops",
+           "pfs_detector_events", "pfs_program_op_clock", "pfs_program_ops", "pfs_program_dump",
            "pfs_reference_sample", "pfs_reference_sample_error", "pfs_write_format")
 
 _lib = None
@@ -98,6 +98,8 @@ def lib():
     L.pfs_program_op_clock.restype = ctypes.c_int
     L.pfs_program_ops.argtypes = [P, P, i64]
     L.pfs_program_ops.restype = ctypes.c_int
+    L.pfs_program_dump.argtypes = [P, ctypes.c_int, ctypes.c_int, P, i64]
+    L.pfs_program_dump.restype = ctypes.c_int64
     L.pfs_write_format.argtypes = [ctypes.c_int, P, i64, i64, i64, ctypes.c_int, P, i64, ctypes.POINTER(i64), P]
     L.pfs_write_format.restype = ctypes.c_int
     L.pfs_reference_sample.argtypes = [P, i64, P, i64, i32, P, i64, P, P, i64, ctypes.POINTER(i64)]
@@ -222,6 +224,15 @@ class NativeProgram:
         out = np.zeros((self.info["num_ops"], 2), dtype=np.uint32)
         _check(lib().pfs_program_ops(self._h, _p(out), self.info["num_ops"]))
         return out
+
+    def dump(self, what: int, flavour: int = 0) -> np.ndarray:
+        """Raw uint32 table of a compiled flavour (pfs_program_dump; test tooling)."""
+        n = int(lib().pfs_program_dump(self._h, flavour, what, None, 0))
+        if n < 0:
+            raise ValueError(lib().pfs_last_error().decode())
+        out = np.zeros(max(n, 1), dtype=np.uint32)
+        lib().pfs_program_dump(self._h, flavour, what, _p(out), n)
+        return out[:n]
 
     def last_launches(self) -> int:
         return int(lib().pfs_program_last_launches(self._h))

@@ -1053,3 +1053,24 @@ extern "C" int pfs_program_ops(const pfs_program* pg, uint32_t* out, int64_t n) 
     for (int64_t i = 0; i < m; i++) { out[2 * i] = hp.ops[i].kcf; out[2 * i + 1] = hp.ops[i].count; }
     return PFS_OK;
 }
+
+// Test tooling: raw tables of a compiled flavour (include/pfs.h).
+extern "C" int64_t pfs_program_dump(const pfs_program* pg, int flavour, int what, uint32_t* out, int64_t n) {
+    if (!pg || flavour < 0 || flavour > 1) return fail(PFS_E_INVALID, "bad argument");
+    const HostProgram& hp = pg->fl[flavour].hp;
+    const uint32_t* src = nullptr;
+    int64_t words = 0;
+    switch (what) {
+        case 0: src = reinterpret_cast<const uint32_t*>(hp.ops.data()); words = (int64_t)hp.ops.size() * 8; break;
+        case 1: src = hp.targets.data(); words = (int64_t)hp.targets.size(); break;
+        case 2: src = hp.det_ptr.data(); words = (int64_t)hp.det_ptr.size(); break;
+        case 3: src = hp.det_terms.data(); words = (int64_t)hp.det_terms.size(); break;
+        case 4: src = reinterpret_cast<const uint32_t*>(hp.sops.data()); words = (int64_t)hp.sops.size() * 12; break;
+        case 5: src = hp.arena.data(); words = (int64_t)hp.arena.size(); break;
+        case 6: src = hp.fused_info.data(); words = (int64_t)hp.fused_info.size(); break;
+        case 7: src = hp.row_of.data(); words = (int64_t)hp.row_of.size(); break;
+        default: return fail(PFS_E_INVALID, "unknown table");
+    }
+    if (out && n > 0 && words > 0) std::memcpy(out, src, (size_t)std::min(n, words) * 4);
+    return words;
+}

@@ -11,7 +11,7 @@
 //   * at M q (record m): S_x[q] ^= cols(m)    (an X before M flips the record,
 //     stabsim/frame_sim.py:74-80);
 //   * at R / MR: S_x[q] = S_z[q] = {}         (frame_sim.py:82-90);
-//   * at a gate: the transpose of its frame rule (gates.py:326-348), e.g. CX:
+//   * at a gate: the transpose of its frame rule (gates.py:70-92), e.g. CX:
 //     S_x0 ^= S_x1, S_z1 ^= S_z0;
 //   * at a noise instruction: the component signatures (x / z on each slot) of
 //     every application, read off the current sets.

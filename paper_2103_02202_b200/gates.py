@@ -2,13 +2,13 @@
 
 Only the data the Pauli-frame hot path needs is kept here: the per-gate
 frame-update rule (the reference derives it from the gate tableau in
-`stabsim/gates.py:326-348` `GateData.frame_plan`), the noise-channel Pauli
-patterns (`stabsim/gates.py:354-360, 402-408`), and the collapse flags
-(`stabsim/gates.py:296-297, 398-400`).  Tableau / unitary algebra is not on
+`stabsim/gates.py:70-92` `GateData.frame_plan`), the noise-channel Pauli
+patterns (`stabsim/gates.py:98-104, 146-152`), and the collapse flags
+(`stabsim/gates.py:40-41, 142-144`).  Tableau / unitary algebra is not on
 the frame path and is not rebuilt.
 
 The superset dialect adds TICK, OBSERVABLE_INCLUDE, SQRT_X and SQRT_X_DAG,
-which the reference registry lacks (`stabsim/gates.py:363-411`).
+which the reference registry lacks (`stabsim/gates.py:107-156`).
 """
 
 from __future__ import annotations
@@ -54,7 +54,7 @@ RULE_BITS = {RULE_NONE: 0, RULE_SWAPXZ: 4, RULE_ZXORX: 3, RULE_XXORZ: 3,
 
 
 def _depolarize2_patterns():
-    """15 two-qubit Pauli codes in the reference order (gates.py:354-360)."""
+    """15 two-qubit Pauli codes in the reference order (gates.py:98-104)."""
     pats = []
     for code in range(1, 16):
         x = (code & 1) | (((code >> 2) & 1) << 1)
@@ -123,7 +123,7 @@ for _g in GATES:
     for _a in _g.aliases:
         GATE_MAP[_a] = _g
 
-# Gates the reference itself knows (stabsim/gates.py:363-411); the rest need
+# Gates the reference itself knows (stabsim/gates.py:107-156); the rest need
 # lowering before a circuit can be handed to the reference.
 REFERENCE_GATE_NAMES = frozenset(
     ["I", "X", "Y", "Z", "H", "S", "S_DAG", "SQRT_Y", "SQRT_Y_DAG", "CNOT",

@@ -9,7 +9,7 @@ committed files next to this script.  Usage:
 Fixtures (all derived from `stabsim` at /root/reference/pkg/src):
 
 * frame_plans.json   — `GateData.frame_plan` / `noise_patterns` per gate
-                        (stabsim/gates.py:326-348, 354-360).
+                        (stabsim/gates.py:70-92, 354-360).
 * inject_*.npz       — (T2) injected-mask runs of the reference's own
                         `FrameBatch` opcode loop (frame_sim.py:192-205) with
                         the coin stream fed through `.bytes()` and opcode 4
