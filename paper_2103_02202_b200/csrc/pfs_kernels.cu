@@ -743,58 +743,110 @@ __global__ void __launch_bounds__(NK_WARPS * 32, 4) noise_kernel(const __grid_co
             const unsigned long long t1 = nz.tab_len > 1 ? tab[1] : ~0ull;
             const uint32_t lgca = nz.lgL - nz.lgcs, cs = 1u << nz.lgcs, msk = cs - 1u;
             const uint32_t nS = (32u * W) >> nz.lgcs;
-            const uint32_t m = cs >= S ? 1u : S / cs;
-            const uint32_t per_k = (uint32_t)C * m;
+            // chunks per vector m and per application block per_k: powers of two
+            const uint32_t lgm = cs >= S ? 0u : (uint32_t)__ffs(S / cs) - 1u;
+            const uint32_t lgpk = lgm + (uint32_t)Log2<C>::v;
             const uint32_t k0 = A0 >> lgca;
-            const uint32_t nch = ((A1 - A0 + (1u << lgca) - 1) >> lgca) * per_k;
+            const uint32_t nch = ((A1 - A0 + (1u << lgca) - 1) >> lgca) << lgpk;
             const uint32_t sh = 32u - nz.lgL;
+            // consumer warp of chunk row kq = kq / (rows per warp), by reciprocal (exact below 2^16)
+            const uint32_t rpw = K >> lgca;
+            const uint32_t magic = rpw > 1u ? (uint32_t)(0x100000000ull / rpw) + 1u : 0u;
+            // a hit into the staging buffer, tagged with its consumer warp
+            auto put = [&](uint32_t a0, uint32_t s0, uint32_t wl, uint32_t pos, uint32_t pick) {
+                const uint32_t slot = atomicAdd(wn, 1u);
+                if (slot < (uint32_t)NK_SCR) {
+                    ent[slot] = make_hit(app_rows(tg, a0 + (pos >> nz.lgcs), ar, pairs), nz.ch, pick, s0 + (pos & msk)) |
+                                ((unsigned long long)wl << 56);
+                    atomicAdd(&wcnt[wl], 1u);
+                }
+            };
             for (uint32_t q0 = 0; q0 < nch; q0 += 32) {
+                // ---- phase 1, one chunk per lane: Binomial count from Philox block 0
                 const uint32_t q = q0 + (uint32_t)lane;
-                if (q < nch) {
-                    const uint32_t k = k0 + q / per_k, rem = q % per_k;
-                    const uint32_t c = rem / m, u = rem - c * m;
-                    const uint32_t r = k * nS + c * m + u;
-                    const uint32_t a0 = k << lgca;
-                    const uint32_t vl = min(1u << lgca, np.apps - a0) << nz.lgcs;
-                    const uint32_t s0 = c * S + u * cs;
-                    const uint32_t wl = a0 / K - wb;  // consumer warp (item-local)
-                    uint32_t w0 = 0u, w1 = r, w2 = tk.g, w3 = DOMAIN_NOISE | nz.ordinal;  // block 0
+                const bool valid = q < nch;
+                const uint32_t kq = q >> lgpk, rem = q & ((1u << lgpk) - 1u);
+                const uint32_t c = rem >> lgm, u = rem & ((1u << lgm) - 1u);
+                const uint32_t k = k0 + kq;
+                const uint32_t r = k * nS + (c << lgm) + u;
+                const uint32_t a0 = k << lgca;
+                const uint32_t vl = valid ? (min(1u << lgca, np.apps - a0) << nz.lgcs) : 0u;
+                const uint32_t s0 = c * S + u * cs;
+                const uint32_t wl = rpw > 1u ? __umulhi(kq, magic) : kq;  // consumer warp (item-local)
+                uint32_t w2 = 0u, w3 = 0u, cnt = 0u;
+                if (valid) {
+                    uint32_t w0 = 0u, w1 = r;
+                    w2 = tk.g; w3 = DOMAIN_NOISE | nz.ordinal;  // block 0
                     philox_rounds(w0, w1, w2, w3, tk.k0, tk.k1);
                     const unsigned long long uu = ((unsigned long long)w1 << 32) | w0;
-                    uint32_t cnt = (nz.tab_len > 0 && uu >= t0) ? ((nz.tab_len > 1 && uu >= t1) ? 2u : 1u) : 0u;
+                    cnt = (nz.tab_len > 0 && uu >= t0) ? ((nz.tab_len > 1 && uu >= t1) ? 2u : 1u) : 0u;
                     if (cnt == 2u)
                         while (cnt < nz.tab_len && uu >= tab[cnt]) cnt++;
-                    auto put = [&](uint32_t pos, uint32_t pick) {
-                        const uint32_t slot = atomicAdd(wn, 1u);
-                        if (slot < (uint32_t)NK_SCR) {
-                            ent[slot] = make_hit(app_rows(tg, a0 + (pos >> nz.lgcs), ar, pairs), nz.ch, pick,
-                                                 s0 + (pos & msk)) |
-                                        ((unsigned long long)wl << 56);
-                            atomicAdd(&wcnt[wl], 1u);
-                        }
-                    };
-                    bool general = cnt > (uint32_t)NZ_MAX_LIST;
-                    if (cnt > 0u && !general) {
-                        // attempt 0: hit h takes pair h (block (h + 1) >> 1)
-                        uint32_t b0 = 0, b1 = 0, b2 = w2, b3 = w3;
-                        bool dup = false;
-                        for (uint32_t h = 0; h < cnt; h++) {
-                            if (h > 0 && (h & 1u)) noise_block(tk, (h + 1) >> 1, r, nz.ordinal, b0, b1, b2, b3);
-                            const uint32_t x = (h & 1u) ? b0 : b2, y = (h & 1u) ? b1 : b3;
-                            const uint32_t pos = nz.lgL ? (x >> sh) : 0u;
-                            for (uint32_t j = 0; j < h; j++) dup |= (sl[j] >> 4) == pos;
-                            sl[h] = (pos << 4) | (nz.npat > 1 ? __umulhi(y, nz.npat) : 0u);
-                        }
-                        if (dup) general = true;
-                        else
-                            for (uint32_t h = 0; h < cnt; h++) {
-                                const uint32_t e = sl[h];
-                                if ((e >> 4) < vl) put(e >> 4, e & 15u);
-                            }
-                    }
-                    if (general)  // redraws / selection sampling: the reference path
-                        noise_chunk(tk, nz, kp.noise_tab, r, vl, sl, put);
                 }
+                bool general = cnt > (uint32_t)NZ_MAX_LIST;
+                const uint32_t cf = general ? 0u : cnt;  // hits drawn by the hit-parallel phase
+                uint32_t pre = cf;                        // inclusive prefix over the lanes
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const uint32_t v = __shfl_up_sync(0xFFFFFFFFu, pre, d);
+                    if (lane >= d) pre += v;
+                }
+                const uint32_t excl = pre - cf;
+                // ---- phase 2, one hit per lane: runs of whole chunks with at most 32 hits;
+                // hit h of a chunk takes word pair h (block (h + 1) >> 1; pair 0 = block 0's w2, w3)
+                uint32_t regen = 0u;  // chunks whose positions collide: the reference path redraws them
+                for (uint32_t c0 = 0; c0 < 32u;) {
+                    const uint32_t base = __shfl_sync(0xFFFFFFFFu, excl, (int)c0);
+                    const uint32_t inm = __ballot_sync(0xFFFFFFFFu, (uint32_t)lane >= c0 && pre - base <= 32u);
+                    const uint32_t c1 = c0 + (uint32_t)__popc(inm);
+                    const uint32_t Hs = __shfl_sync(0xFFFFFFFFu, pre, (int)c1 - 1) - base;
+                    if (Hs > 0u) {
+                        const uint32_t j = (uint32_t)lane;
+                        const bool mine = j < Hs;
+                        uint32_t lo = c0;  // owner chunk: the first lane in [c0, c1) with pre - base > j
+#pragma unroll
+                        for (int st = 16; st > 0; st >>= 1) {
+                            const uint32_t idx = lo + (uint32_t)st - 1u;
+                            const uint32_t pv = __shfl_sync(0xFFFFFFFFu, pre, (int)min(idx, 31u)) - base;
+                            if (idx < c1 && pv <= j) lo = idx + 1u;
+                        }
+                        const int o = (int)min(lo, c1 - 1u);
+                        const uint32_t h = j - (__shfl_sync(0xFFFFFFFFu, excl, o) - base);
+                        const uint32_t o_cnt = __shfl_sync(0xFFFFFFFFu, cf, o);
+                        const uint32_t o_r = __shfl_sync(0xFFFFFFFFu, r, o);
+                        const uint32_t o_a0 = __shfl_sync(0xFFFFFFFFu, a0, o);
+                        const uint32_t o_vl = __shfl_sync(0xFFFFFFFFu, vl, o);
+                        const uint32_t o_s0 = __shfl_sync(0xFFFFFFFFu, s0, o);
+                        const uint32_t o_wl = __shfl_sync(0xFFFFFFFFu, wl, o);
+                        uint32_t x = __shfl_sync(0xFFFFFFFFu, w2, o);
+                        uint32_t y = __shfl_sync(0xFFFFFFFFu, w3, o);
+                        if (__any_sync(0xFFFFFFFFu, mine && h > 0u)) {
+                            uint32_t b0 = (h + 1u) >> 1, b1 = o_r, b2 = tk.g, b3 = DOMAIN_NOISE | nz.ordinal;
+                            philox_rounds(b0, b1, b2, b3, tk.k0, tk.k1);
+                            if (h > 0u) { x = (h & 1u) ? b0 : b2; y = (h & 1u) ? b1 : b3; }
+                        }
+                        const uint32_t pos = nz.lgL ? (x >> sh) : 0u;
+                        const uint32_t pick = nz.npat > 1 ? __umulhi(y, nz.npat) : 0u;
+                        // the positions of one chunk must be distinct: compare with the earlier siblings
+                        const uint32_t maxh = __reduce_max_sync(0xFFFFFFFFu, mine ? h : 0u);
+                        bool dup = false;
+                        for (uint32_t d = 1; d <= maxh; d++) {
+                            const uint32_t p = __shfl_up_sync(0xFFFFFFFFu, pos, d);
+                            if (mine && h >= d) dup |= p == pos;
+                        }
+                        const uint32_t dupm = __ballot_sync(0xFFFFFFFFu, mine && dup);
+                        const uint32_t sib = (o_cnt >= 32u ? 0xFFFFFFFFu : ((1u << o_cnt) - 1u)) << (j - h);
+                        const bool cdup = mine && (dupm & sib) != 0u;
+                        if (mine && !cdup && pos < o_vl) put(o_a0, o_s0, o_wl, pos, pick);
+                        regen |= __reduce_or_sync(0xFFFFFFFFu, (cdup && h == 0u) ? (1u << o) : 0u);
+                    }
+                    c0 = c1;
+                }
+                // ---- phase 3 (rare): long or colliding chunks through the reference path
+                general |= ((regen >> lane) & 1u) != 0u;
+                if (general)
+                    noise_chunk(tk, nz, kp.noise_tab, r, vl, sl,
+                                [&](uint32_t pos, uint32_t pick) { put(a0, s0, wl, pos, pick); });
             }
             __syncwarp();
             over = *wn > (uint32_t)NK_SCR;
