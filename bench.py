@@ -434,7 +434,8 @@ def roofline_of(res, smem_peak, hbm):
                               "of the frame kernel)",
             "peak_source": "measured live: pfs_measure_smem_bandwidth (LDS.128/STS.128 CX mix, "
                            "all SMs)",
-            "kernel": "frame_kernel (frame table resident in shared memory, noise sampled inline)",
+            "kernel": "frame_kernel (frame table resident in shared memory; fused noise applied from noise_kernel's "
+                      "pre-sampled per-warp hit lists)",
             "frame_kernel_ms": fr, "transpose_kernel_ms": res["transpose_ms"],
             "noise_kernel_ms": res["noise_ms"],
             "bytes_per_shot": bframe_bytes,
@@ -561,7 +562,7 @@ def profile_traffic(shots=None, cfg=2):
     try:
         with open(p) as f:
             d = json.load(f)
-        d = d.get(f"config{cfg}")
+        d = d if cfg == 2 else d.get(f"config{cfg}")  # top level: config 2; "config4": d=100
         return float(d["dram_bytes_per_shot"]) * shots if (d and shots) else None
     except Exception:
         return None
