@@ -758,8 +758,11 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
             const int ar = rule_arity(code);
             const uint32_t Kc = warp_share(o.count, nw, ca);
             const uint32_t passes = (Kc + PI - 1) / PI;
+            // a warp's block holds at least GATE_AHEAD_PASSES passes (the kernel
+            // prefetches that many words per lane without predicates);
             // padding applications act on the group's dummy rows (rows num_qubits ..)
-            blk.resize((size_t)nw * passes * PI);
+            const uint32_t stride = std::max<uint32_t>(passes, GATE_AHEAD_PASSES) * PI;
+            blk.resize((size_t)nw * stride);
             for (size_t j = 0; j < blk.size(); j++) {
                 const uint32_t dr = (uint32_t)hp.num_qubits + (uint32_t)(j % DUMMY_ROWS);
                 blk[j] = dr | (dr << 16);
@@ -770,7 +773,7 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
                 range.assign(hp.targets.begin() + o.off + (size_t)A0 * ar, hp.targets.begin() + o.off + (size_t)A1 * ar);
                 bank_reorder(range.data(), A1 - A0, ar, G, scratch);
                 for (uint32_t j = 0; j < A1 - A0; j++)
-                    blk[(size_t)w * passes * PI + j] = range[(size_t)j * ar] | (ar == 2 ? range[(size_t)j * ar + 1] << 16 : 0u);
+                    blk[(size_t)w * stride + j] = range[(size_t)j * ar] | (ar == 2 ? range[(size_t)j * ar + 1] << 16 : 0u);
             }
             s.K = passes;
             s.r0 = Kc;

@@ -107,6 +107,12 @@ constexpr uint32_t STREAM_NOP = 0xFFFFFFFFu;
 // no lane is predicated off; consecutive padding applications take different
 // dummy rows so that they fall into different shared-memory bank groups.
 constexpr int DUMMY_ROWS = 4;
+// operand words of the next gate op a lane loads ahead (frame kernel GATE_AHEAD):
+// every warp block of a gate op is padded to at least this many passes
+#ifndef PFS_GATE_AHEAD
+#define PFS_GATE_AHEAD 6
+#endif
+constexpr uint32_t GATE_AHEAD_PASSES = PFS_GATE_AHEAD;
 
 // Per noise instruction sampling schedule for one tile, also
 // exported to the parity oracle through pfs_program_noise_schedule.

@@ -223,23 +223,31 @@ __device__ __forceinline__ void chunk_hits(const TileKey& tk, const NoiseOp& nz,
 // total above WSCR take the general path, lane by lane.  The chunk covers
 // applications [a0, a0 + na) and shots [s0, s0 + cs).  Every lane of the warp
 // must call this (shuffles).
-// Hit entry of a pre-sampled noise list (noise_kernel -> frame kernel): frame
-// rows q0 | q1 (20 bits each) | word (5) | bit (5) | x mask (2) | z mask (2)
+// Hit entry of a pre-sampled noise list (noise_kernel -> frame kernel), ready
+// to apply: low word = plane word offset of target 0 (row W + word, 20 bits) |
+// bit index << 20 | x0 z0 x1 z1 flip flags << 25; high word = plane word offset
+// of target 1 (bits 24-31 of the high word are free: noise_kernel's staging
+// keeps the consumer warp there)
+template <int W>
 __device__ __forceinline__ unsigned long long make_hit(const AppRows& rr, uint32_t ch, uint32_t pick, uint32_t s) {
     uint32_t xm, zm;
     pattern_of(ch, pick, xm, zm);
-    return (unsigned long long)rr.r0 | ((unsigned long long)rr.r1 << 20) | ((unsigned long long)(s >> 5) << 40) |
-           ((unsigned long long)(s & 31u) << 45) | ((unsigned long long)xm << 50) | ((unsigned long long)zm << 52);
+    const uint32_t w = s >> 5;
+    const uint32_t lo = (rr.r0 * W + w) | ((s & 31u) << 20) | ((xm & 1u) << 25) | ((zm & 1u) << 26) |
+                        ((xm >> 1) << 27) | ((zm >> 1) << 28);
+    const uint32_t hi = rr.r1 * W + w;
+    return (unsigned long long)lo | ((unsigned long long)hi << 32);
 }
-template <int W>
-__device__ __forceinline__ void apply_hit_entry(uint32_t* X, uint32_t* Z, unsigned long long e) {
-    const uint32_t q0 = (uint32_t)e & 0xFFFFFu, q1 = (uint32_t)(e >> 20) & 0xFFFFFu;
-    const uint32_t w = (uint32_t)(e >> 40) & 31u, bit = 1u << ((uint32_t)(e >> 45) & 31u);
-    const uint32_t xm = (uint32_t)(e >> 50) & 3u, zm = (uint32_t)(e >> 52) & 3u;
-    if (xm & 1u) atomicXor(X + (size_t)q0 * W + w, bit);
-    if (zm & 1u) atomicXor(Z + (size_t)q0 * W + w, bit);
-    if (xm & 2u) atomicXor(X + (size_t)q1 * W + w, bit);
-    if (zm & 2u) atomicXor(Z + (size_t)q1 * W + w, bit);
+// xa = shared address of the group's x plane, zb = bytes from the x to the z
+// plane; fire-and-forget shared-memory XOR reductions (hits may share a word)
+__device__ __forceinline__ void apply_hit_entry(uint32_t xa, uint32_t zb, unsigned long long e) {
+    const uint32_t lo = (uint32_t)e, hi = (uint32_t)(e >> 32);
+    const uint32_t bit = 1u << ((lo >> 20) & 31u);
+    const uint32_t p0 = xa + ((lo & 0xFFFFFu) << 2), p1 = xa + ((hi & 0xFFFFFu) << 2);
+    if (lo & (1u << 25)) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(p0), "r"(bit) : "memory");
+    if (lo & (1u << 26)) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(p0 + zb), "r"(bit) : "memory");
+    if (lo & (1u << 27)) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(p1), "r"(bit) : "memory");
+    if (lo & (1u << 28)) asm volatile("red.shared.xor.b32 [%0], %1;" ::"r"(p1 + zb), "r"(bit) : "memory");
 }
 
 template <int W>
@@ -475,10 +483,7 @@ __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, u
 #define PFS_GATE_BATCH 2
 #endif
 constexpr int GATE_BATCH = PFS_GATE_BATCH;  // applications whose rows a lane loads before it stores any
-#ifndef PFS_GATE_AHEAD
-#define PFS_GATE_AHEAD 6
-#endif
-constexpr int GATE_AHEAD = PFS_GATE_AHEAD;   // operand words of the next gate op held in registers
+constexpr int GATE_AHEAD = (int)GATE_AHEAD_PASSES;   // operand words of the next gate op held in registers
 
 // Shared-memory vectors by 32-bit shared address (gate hot path: explicit
 // address arithmetic, loads of a batch issued before its stores)
@@ -756,7 +761,7 @@ __global__ void __launch_bounds__(NK_WARPS * 32, 4) noise_kernel(const __grid_co
             auto put = [&](uint32_t a0, uint32_t s0, uint32_t wl, uint32_t pos, uint32_t pick) {
                 const uint32_t slot = atomicAdd(wn, 1u);
                 if (slot < (uint32_t)NK_SCR) {
-                    ent[slot] = make_hit(app_rows(tg, a0 + (pos >> nz.lgcs), ar, pairs), nz.ch, pick, s0 + (pos & msk)) |
+                    ent[slot] = make_hit<W>(app_rows(tg, a0 + (pos >> nz.lgcs), ar, pairs), nz.ch, pick, s0 + (pos & msk)) |
                                 ((unsigned long long)wl << 56);
                     atomicAdd(&wcnt[wl], 1u);
                 }
@@ -975,9 +980,10 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
     uint32_t nw[GATE_AHEAD];
     auto load_ahead = [&]() {
         if ((nd0.x & 0xFFu) == K_GATE) {
-            const uint32_t* const nblk = kp.arena + nd0.z + (uint32_t)warp * nd0.w * PI + (lane >> LC);
+            // (a warp's block holds at least GATE_AHEAD passes of words: no predicates)
+            const uint32_t* const nblk = kp.arena + nd0.z + (uint32_t)warp * max(nd0.w, (uint32_t)GATE_AHEAD) * PI + (lane >> LC);
 #pragma unroll
-            for (int j = 0; j < GATE_AHEAD; j++) nw[j] = (uint32_t)j < nd0.w ? __ldg(nblk + j * PI) : nop;
+            for (int j = 0; j < GATE_AHEAD; j++) nw[j] = __ldg(nblk + j * PI);
         }
     };
 #pragma unroll
@@ -1040,8 +1046,9 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
             if (!GENERAL || (pre && sp.x != NO_SLOT)) {
                 __syncwarp();  // the warp's row updates are visible to the lanes applying hits
                 uint32_t j = sp.x + (uint32_t)lane;
-                if (j < sp.y) apply_hit_entry<W>(X, Z, hp.e0n);
-                for (j += 32u; j < sp.y; j += 32u) apply_hit_entry<W>(X, Z, __ldg(hits + j));
+                const uint32_t xa = (uint32_t)__cvta_generic_to_shared(X);
+                if (j < sp.y) apply_hit_entry(xa, zoff * 4u, hp.e0n);
+                for (j += 32u; j < sp.y; j += 32u) apply_hit_entry(xa, zoff * 4u, __ldg(hits + j));
             } else if (GENERAL) {
                 fused_noise_general<W>(kp, oi, Kc, xg, tile);
             }
@@ -1050,7 +1057,7 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
 
         switch (kind) {
         case K_GATE: {
-            const uint32_t* const blk = kp.arena + off + (uint32_t)warp * K * PI + (lane >> LC);
+            const uint32_t* const blk = kp.arena + off + (uint32_t)warp * max(K, (uint32_t)GATE_AHEAD) * PI + (lane >> LC);
             switch (code) {
                 case R_SWAPXZ: gate_stream<W, R_SWAPXZ>(bx, bz, blk, K, pw, nop); break;
                 case R_ZXORX: gate_stream<W, R_ZXORX>(bx, bz, blk, K, pw, nop); break;

@@ -33,6 +33,7 @@ NO_SLOT = 0xFFFFFFFF
 COIN_DEAD = 0x80000000
 XROW = 0x80000000
 DUMMY_ROWS = 4
+GATE_AHEAD = 6
 
 
 def _tables(p, flavour):
@@ -117,7 +118,8 @@ def _check_program(p, flavour, n_qubits, warps_per_group, W):
             count = int(op[1])
             apps = t["targets"][int(op[2]): int(op[2]) + count * ar].reshape(-1, ar)
             want = [tuple(int(x) for x in a) for a in apps]
-            blk = t["arena"][off: off + warps_per_group * K * PI].reshape(warps_per_group, K * PI)
+            stride = max(K, GATE_AHEAD) * PI   # a warp's block: at least GATE_AHEAD passes of words
+            blk = t["arena"][off: off + warps_per_group * stride].reshape(warps_per_group, stride)
             seen = []
             for w in range(warps_per_group):
                 mine = set(want[min(count, w * Kc): min(count, (w + 1) * Kc)])
