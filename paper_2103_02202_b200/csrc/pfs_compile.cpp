@@ -779,10 +779,17 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
             s.r0 = Kc;
             break;
         }
-        case K_M: case K_MR: case K_R: case K_SPILL:
+        case K_M: case K_MR: case K_R: case K_SPILL: {
             blk.assign(hp.targets.begin() + o.off, hp.targets.begin() + o.off + 2 * (size_t)o.count);
             s.K = warp_share(o.count, nw, ca);
+            // an event-program M whose coins are all dead and whose records all
+            // stay in their x rows has no row work (only its fused noise)
+            bool norows = kind == K_M && hp.mode == PM_EVENTS;
+            for (uint32_t j = 0; norows && j < o.count; j++)
+                norows = (blk[2 * j] & COIN_DEAD) && blk[2 * j + 1] == NO_SLOT;
+            if (norows) s.kcf |= F_NOROWS << 16;
             break;
+        }
         case K_DET:
             if (code) blk.assign(hp.det_terms.begin() + o.off, hp.det_terms.begin() + o.off + (size_t)o.count * code);
             break;

@@ -22,6 +22,8 @@ constexpr uint32_t F_BARRIER = 1u;   // group barrier before this op
 constexpr uint32_t F_DUP = 2u;       // noise op with repeated targets
 constexpr uint32_t F_NOISE = 4u;     // fused noise (after a gate / reset, before a measurement)
 constexpr uint32_t F_PRESAMPLED = 8u;  // stream op: the fused noise comes from noise_kernel's hit lists
+constexpr uint32_t F_NOROWS = 16u;     // stream op: a measurement with no row work (dead coins, records stay
+                                       // in their x rows, no record output): only its fused noise runs
 constexpr uint32_t NO_SLOT = 0xFFFFFFFFu;
 constexpr uint32_t COIN_DEAD = 0x80000000u;  // M/MR/R target word: the op's coin row reaches no output
 constexpr uint32_t XROW = 0x80000000u;       // DET/OBS term: the record is the x row of this frame row

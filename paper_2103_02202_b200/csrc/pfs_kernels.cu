@@ -660,11 +660,12 @@ __device__ __forceinline__ unsigned long long first_entry(const unsigned long lo
 }
 
 // M / R / MR / SPILL items of this warp's targets [A0, A1): (target, vector)
-// items over the warp's lanes, four operand pairs in flight
-template <int W>
-__device__ __forceinline__ void collapse_stream(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
-                                                uint32_t* ring, const uint2* tp, uint32_t kind, uint32_t A0,
-                                                uint32_t A1, uint32_t rec0, uint32_t coin0, int lane, int64_t tile) {
+// items over the warp's lanes, four operand pairs in flight.  KIND is a template
+// argument: no per-item dispatch.
+template <int W, uint32_t KIND>
+__device__ __forceinline__ void collapse_kind(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
+                                              uint32_t* ring, const uint2* tp, uint32_t A0, uint32_t A1,
+                                              uint32_t rec0, uint32_t coin0, int lane, int64_t tile) {
     constexpr int V = W >= 4 ? 4 : W;
     constexpr int C = W / V;
     constexpr int LC = Log2<C>::v;
@@ -673,23 +674,26 @@ __device__ __forceinline__ void collapse_stream(const KParams& kp, const TileKey
         const uint32_t app = A0 + (uint32_t)(i >> LC);
         const int c = i & (C - 1);
         const bool live = !(rs.x & COIN_DEAD);
-        const size_t p = (size_t)(rs.x & ~COIN_DEAD) * W + c * V;
-        if (kind == K_SPILL) {
-            vst<V>(ring + (size_t)rs.y * W + c * V, vld<V>(X + p));
+        const uint32_t p = (rs.x & ~COIN_DEAD) * W + c * V;
+        if (KIND == K_SPILL) {
+            vst<V>(ring + rs.y * W + c * V, vld<V>(X + p));
             return;
         }
-        if (kind == K_R) {
+        if (KIND == K_R) {
             // spill the record homed in x, then reset
-            if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, vld<V>(X + p));
+            if (rs.y != NO_SLOT) vst<V>(ring + rs.y * W + c * V, vld<V>(X + p));
             vst<V>(X + p, vzero<V>());
             vst<V>(Z + p, live ? coin_vec<W, V>(kp, tk, coin0 + app, c, tile) : vzero<V>());
             return;
         }
-        const VW<V> x = vld<V>(X + p);
-        if (rs.y != NO_SLOT) vst<V>(ring + (size_t)rs.y * W + c * V, x);
-        if (kp.rec_out != nullptr)
-            vst<V>(kp.rec_out + (int64_t)(rec0 + app) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, x);
-        if (kind == K_M) {
+        // M / MR: the record is the x row
+        if (rs.y != NO_SLOT || kp.rec_out != nullptr || KIND == K_MR) {
+            const VW<V> x = vld<V>(X + p);
+            if (rs.y != NO_SLOT) vst<V>(ring + rs.y * W + c * V, x);
+            if (kp.rec_out != nullptr)
+                vst<V>(kp.rec_out + (int64_t)(rec0 + app) * kp.out_row_stride + tile * kp.out_tile_stride + c * V, x);
+        }
+        if (KIND == K_M) {
             if (live) vst<V>(Z + p, vxor<V>(vld<V>(Z + p), coin_vec<W, V>(kp, tk, coin0 + app, c, tile)));
         } else {  // MR: the measure's coin row (coin0 + 2 app) is overwritten by the reset's
             vst<V>(X + p, vzero<V>());
@@ -697,7 +701,17 @@ __device__ __forceinline__ void collapse_stream(const KParams& kp, const TileKey
         }
     });
 }
-
+template <int W>
+__device__ __forceinline__ void collapse_stream(const KParams& kp, const TileKey& tk, uint32_t* X, uint32_t* Z,
+                                                uint32_t* ring, const uint2* tp, uint32_t kind, uint32_t A0,
+                                                uint32_t A1, uint32_t rec0, uint32_t coin0, int lane, int64_t tile) {
+    switch (kind) {
+        case K_R: collapse_kind<W, K_R>(kp, tk, X, Z, ring, tp, A0, A1, rec0, coin0, lane, tile); break;
+        case K_M: collapse_kind<W, K_M>(kp, tk, X, Z, ring, tp, A0, A1, rec0, coin0, lane, tile); break;
+        case K_MR: collapse_kind<W, K_MR>(kp, tk, X, Z, ring, tp, A0, A1, rec0, coin0, lane, tile); break;
+        default: collapse_kind<W, K_SPILL>(kp, tk, X, Z, ring, tp, A0, A1, rec0, coin0, lane, tile); break;
+    }
+}
 
 // ------------------------------------------------------------ noise kernel
 // Pre-samples the fused noise of a launch's tiles (DESIGN.md §4 draws, exactly
@@ -1079,7 +1093,7 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
             warp_share_of(count, K, warp, A0, A1);
             // fused noise precedes a measurement (X_ERROR before M), follows a reset
             if (fz && kind != K_R) fused_noise(K);
-            if (A0 < A1) {
+            if (A0 < A1 && !(flags & F_NOROWS)) {
                 const TileKey tk = tile_key(kp.seed, kp.tile_offset + (uint64_t)tile);
                 collapse_stream<W>(kp, tk, X, Z, ring, reinterpret_cast<const uint2*>(kp.arena + off), kind, A0, A1,
                                    d1.x, d1.y, lane, tile);
