@@ -483,7 +483,11 @@ __device__ __forceinline__ void noise_op(const KParams& kp, const TileKey& tk, u
 #define PFS_GATE_BATCH 2
 #endif
 constexpr int GATE_BATCH = PFS_GATE_BATCH;  // applications whose rows a lane loads before it stores any
-constexpr int GATE_AHEAD = (int)GATE_AHEAD_PASSES;   // operand words of the next gate op held in registers
+constexpr int GATE_AHEAD = (int)GATE_AHEAD_PASSES;
+#ifndef PFS_DET_BATCH
+#define PFS_DET_BATCH 6
+#endif
+constexpr int DET_BATCH = PFS_DET_BATCH;    // detector columns whose term loads a thread keeps in flight   // operand words of the next gate op held in registers
 
 // Shared-memory vectors by 32-bit shared address (gate hot path: explicit
 // address arithmetic, loads of a batch issued before its stores)
@@ -1117,7 +1121,7 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
                 return (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
             };
             const uint32_t* const tb = code ? kp.arena : kp.det_terms;
-            batched_items<2>(tid, nth, items,
+            batched_items<DET_BATCH>(tid, nth, items,
                 [&](int i) {
                     const uint32_t ci = (uint32_t)(i >> LC);
                     const uint32_t col = oa + ci;
