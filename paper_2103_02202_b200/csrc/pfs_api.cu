@@ -287,7 +287,7 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         const int V = W >= 4 ? 4 : W;
         for (int m = 0; m < (dem ? 1 : 2); m++) {
             HostProgram& hp = pg->fl[m].hp;
-            permute_rows(hp);
+            permute_rows(hp, (dem || W >= 32) ? 1 : 128 / (W * 4));
             dedup_operands(hp);
             // the error-model kernel's chunks span whole 32-shot tiles
             build_noise_schedule(hp, 32 * W, dem ? 32 : 32 * V, th, dem ? th : thf);
@@ -710,10 +710,6 @@ extern "C" int pfs_run(pfs_program* pg, int device, uint64_t seed, uint64_t shot
     kp.arena = fl.arena.p;
     kp.first_span = hp.first_span;
     kp.all_presampled = hp.all_presampled ? 1 : 0;
-    {
-        const char* e = std::getenv("PFS_STAGGER");  // experiment: group start offset in cycles
-        kp.stagger = e ? std::atoi(e) : 0;
-    }
     kp.targets = fl.targets.p;
     kp.det_ptr = fl.det_ptr.p;
     kp.det_terms = fl.det_terms.p;

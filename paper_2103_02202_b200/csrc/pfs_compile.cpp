@@ -613,7 +613,7 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
 // lattice patterns whose residues mod the bank-group count are badly
 // unbalanced (d=25 CX layers: controls mod 4 = {231, 75, 219, 75}), which no
 // reordering of one layer can make conflict-free.  row_of[q] = row of qubit q.
-void permute_rows(HostProgram& hp) {
+void permute_rows(HostProgram& hp, int bank_classes) {
     const uint32_t n = (uint32_t)hp.num_qubits;
     hp.row_of.resize(n);
     for (uint32_t q = 0; q < n; q++) hp.row_of[q] = q;
@@ -625,6 +625,46 @@ void permute_rows(HostProgram& hp) {
         z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
         z ^= z >> 31;
         std::swap(hp.row_of[i - 1], hp.row_of[z % i]);
+    }
+    // Bank classes (row mod G, G = 128 B / row bytes): a warp pass serves G
+    // consecutive applications per shared-memory wavefront, conflict-free when
+    // their rows fall into G distinct classes.  Walk the gate ops in program
+    // order and give every qubit, at its first appearance, the class of its
+    // application's position (j mod G): in circuits whose layers list their
+    // applications in a regular (lattice) order, neighbouring applications then
+    // land in distinct classes in every layer.  Rows are dealt per class from
+    // the random permutation (a full class takes from the emptiest one).
+    const uint32_t G = (uint32_t)std::max(1, bank_classes);
+    if (G > 1 && n >= G) {
+        std::vector<int32_t> cls(n, -1);
+        for (const DOp& o : hp.ops) {
+            if ((o.kcf & 0xFF) != K_GATE) continue;
+            const int ar = rule_arity((o.kcf >> 8) & 0xFF);
+            for (uint32_t j = 0; j < o.count; j++)
+                for (int s2 = 0; s2 < ar; s2++) {
+                    const uint32_t q = hp.targets[o.off + (size_t)j * ar + s2];
+                    if (cls[q] < 0) cls[q] = (int32_t)(j % G);
+                }
+        }
+        // pools: the rows of each class, in the order of the random permutation
+        std::vector<std::vector<uint32_t>> pool(G);
+        for (uint32_t q = 0; q < n; q++) pool[hp.row_of[q] % G].push_back(hp.row_of[q]);
+        std::vector<uint32_t> rest;
+        for (uint32_t q = 0; q < n; q++) {
+            if (cls[q] >= 0 && !pool[cls[q]].empty()) {
+                hp.row_of[q] = pool[cls[q]].back();
+                pool[cls[q]].pop_back();
+            } else {
+                rest.push_back(q);
+            }
+        }
+        for (uint32_t q : rest) {
+            uint32_t best = 0;
+            for (uint32_t c = 1; c < G; c++)
+                if (pool[c].size() > pool[best].size()) best = c;
+            hp.row_of[q] = pool[best].back();
+            pool[best].pop_back();
+        }
     }
     auto map = [&](uint32_t& w) { w = hp.row_of[w & ~COIN_DEAD] | (w & COIN_DEAD); };
     auto map_term = [&](uint32_t& t) { if (t != NO_SLOT && (t & XROW)) t = XROW | hp.row_of[t & ~XROW]; };

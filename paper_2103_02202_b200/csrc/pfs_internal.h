@@ -191,7 +191,7 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
 // chunk of standalone and of fused noise instructions
 void build_noise_schedule(HostProgram& hp, int tile_shots, int vector_shots, double target_hits,
                           double fused_target_hits);
-void permute_rows(HostProgram& hp);
+void permute_rows(HostProgram& hp, int bank_classes);
 void build_hit_lists(HostProgram& hp, int tile_shots, int warps_per_group);
 void lower_stream(HostProgram& hp, int W, int warps_per_group);
 void dedup_operands(HostProgram& hp);
@@ -244,7 +244,6 @@ struct KParams {
                                       // block (begin NO_SLOT: the warp draws inline)
     uint32_t* fill_global;            // [tiles][2]: entries used (noise_kernel allocation), overflow mark
     int32_t all_presampled;           // every noise instruction is fused and pre-sampled (hot frame loop)
-    int32_t stagger;                  // cycles group g waits (g * stagger) before its first tile
     const uint2* hit_items;           // noise_kernel items of one tile
     int64_t hit_block;
     int32_t list_warps;

@@ -1207,14 +1207,6 @@ __global__ void __launch_bounds__(FRAME_MAX_THREADS, 1) frame_kernel(const __gri
         for (int i = threadIdx.x; i < 3 * kp.n_ops; i += blockDim.x) d[i] = __ldg(dsc_g + i);
     }
     __syncthreads();
-    // The groups of a CTA run the same op sequence; started together they stay
-    // in phase and their shared-memory bursts (the gate rows) collide while the
-    // latency-bound phases (descriptors, barrier, noise hits) leave the pipe
-    // idle.  A start offset per group keeps them out of phase.
-    if (kp.stagger > 0 && grp > 0) {
-        const long long t0 = clock64();
-        while (clock64() - t0 < (long long)grp * kp.stagger) {}
-    }
     for (int64_t tile = (int64_t)blockIdx.x * G + grp; tile < kp.n_tiles; tile += (int64_t)gridDim.x * G) {
         // the hot loop serves programs whose noise is all fused and pre-sampled,
         // for tiles whose hit lists all fitted (noise_kernel's overflow mark)
