@@ -117,7 +117,7 @@ constexpr int kPipeChunks = 6;
 constexpr int kPipeFrameThreads = FRAME_MAX_THREADS;
 constexpr int DEM_WARPS_HOST = 16;  // dem_kernel's warps (DEM_WARPS)
 constexpr double kStandaloneHits = 2.0;  // mean hits per noise chunk (standalone / error-model)
-constexpr double kFusedHits = 1.0;       // mean hits per fused noise chunk (one kernel item)
+constexpr double kFusedHits = 2.0;       // mean hits per fused noise chunk (noise_kernel: count per chunk, then hit-parallel)
 constexpr int64_t kHitBufBytes = (int64_t)256 << 20;  // hit lists of one sub-chunk of tiles
 
 static bool desc_fits(const HostProgram& hp) {

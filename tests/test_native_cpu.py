@@ -86,8 +86,8 @@ def test_binomial_thresholds_match_scipy():
 
 @pytest.mark.parametrize("cfg", [0, 1, 2, 3, 4])
 def test_noise_schedule_matches_oracle_restatement(oracle_lib, cfg):
-    """The product's chunk lengths follow the rule of DESIGN.md §4 (target 1
-    hit for fused instructions, 2 otherwise); its geometry and Binomial tables
+    """The product's chunk lengths follow the rule of DESIGN.md §4 (target 2
+    hits per chunk); its geometry and Binomial tables
     equal the oracle's own (oracle/pfs_oracle.c computes them independently)."""
     from tests._util import rule_chunk_length
 
@@ -104,7 +104,7 @@ def test_noise_schedule_matches_oracle_restatement(oracle_lib, cfg):
         ar = 2 if row[1] == 4 else 1
         apps = int(row[2]) // ar
         mine = params[o]
-        assert mine[0] == rule_chunk_length(float(f.noise_p[o]), apps, T, 1.0 if mine[10] else 2.0)
+        assert mine[0] == rule_chunk_length(float(f.noise_p[o]), apps, T, 2.0)
         ref, rtab = oracle_lib.noise_schedule_one(apps, int(row[1]), float(f.noise_p[o]), int(mine[0]), T, S)
         assert list(mine[[0, 1, 2, 3, 4, 6, 7, 8, 9]]) == list(ref[[0, 1, 2, 3, 4, 6, 7, 8, 9]])
         assert np.array_equal(tab[mine[5]:mine[5] + mine[6]], rtab)
