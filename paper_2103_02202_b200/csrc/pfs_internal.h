@@ -37,10 +37,12 @@ constexpr uint32_t NZONE_NONE = 1u;  // p == 0: no hits
 constexpr uint32_t NZONE_ALL = 2u;   // p == 1: every trial hits
 constexpr int NZ_MAX_LIST = 16;      // distinct-position list; larger counts use selection sampling
 constexpr int WSCR = 64;             // per-warp shared scratch of the warp-cooperative noise draws (words)
-// frame kernel CTA size cap (launch bounds): 512 threads leave 128 registers per
-// thread — the fused gate + noise items need ~124 without spilling
+// frame kernel CTA size (launch bounds): 640 threads at 96 registers — the hot
+// tile loop fits without spills, and 20 warps hide more of the op chain than 16
+// at 128 registers (measured at d=25: 512 / 576 / 640 / 704 threads -> 6.83 /
+// 7.85 / 6.55 / 8.08 ms per 2^20 shots)
 #ifndef PFS_FRAME_MAX_THREADS
-#define PFS_FRAME_MAX_THREADS 512
+#define PFS_FRAME_MAX_THREADS 640
 #endif
 constexpr int FRAME_MAX_THREADS = PFS_FRAME_MAX_THREADS;
 constexpr int KERNEL_COOP = 1;

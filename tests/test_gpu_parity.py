@@ -285,7 +285,7 @@ def test_c2_bench_layout_bit_exact_vs_oracle(oracle_lib):
 
     ds = compile_detector_sampler(gen.config_circuit(2))
     info = ds.info
-    assert info["words_per_tile"] == 8 and info["groups"] == 2 and info["threads"] == 512
+    assert info["words_per_tile"] == 8 and info["groups"] == 2 and info["threads"] == 640
     T = ds.tile_shots
     n_tiles = 2 * 148 * 2 + 9
     shots = n_tiles * T - 77
