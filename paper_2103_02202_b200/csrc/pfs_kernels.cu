@@ -968,7 +968,10 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
     const uint32_t bx = (uint32_t)__cvta_generic_to_shared(X + (lane & (C - 1)) * V);
     const uint32_t bz = bx + zoff * 4u;
     const uint32_t nop = ((uint32_t)n + ((uint32_t)(lane >> LC) & (DUMMY_ROWS - 1))) * 0x10001u;  // a dummy row
-    auto ldesc = [&](int i) -> uint4 { return dsm ? dsc_s[i] : __ldg(dsc_g + i); };
+    // one generic load serves both placements (two predicated loads per vector
+    // cost 5 % of the d=25 kernel time; d=100, descriptors in global memory, loses 2 %)
+    const uint4* const dsc_any = dsm ? dsc_s : dsc_g;
+    auto ldesc = [&](int i) -> uint4 { return dsc_any[i]; };
 
     const unsigned long long* const hits = kp.hits_global + tile * kp.hit_block;
     const uint2* const spans = kp.spans_global + (tile * kp.num_noise) * kp.list_warps + warp;
@@ -1020,15 +1023,7 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
         if (oi + 1 < kp.n_ops) {
             nd0 = ldesc(3 * oi + 3);
             if (!dsm && lane == 0) asm volatile("prefetch.global.L1 [%0];" ::"l"(dsc_g + 3 * oi + 6));
-            if ((nd0.x & 0xFFu) == K_GATE) {
-                load_ahead();
-            } else {
-                // pull the next op's operand block (d2.x words at arena + d2.w)
-                // toward L1 while this op runs
-                const uint32_t lines = (d2.x * 4u + 127u) >> 7;
-                for (uint32_t l = (uint32_t)tid; l < lines; l += (uint32_t)nth)
-                    asm volatile("prefetch.global.L1 [%0];" ::"l"(kp.arena + d2.w + 32u * l));
-            }
+            load_ahead();
         }
         const uint32_t kind = d0.x & 0xFFu, code = (d0.x >> 8) & 0xFFu, flags = d0.x >> 16;
         const uint32_t count = d0.y, off = d0.z, K = d0.w;
