@@ -95,15 +95,32 @@ __device__ __forceinline__ void noise_items_warp(const KParams& kp, const uint2*
     bool dup = false;
     for (uint32_t h = 1; h < c; h++)
         for (uint32_t q = 0; q < h; q++) dup |= (wscr[excl + h] >> 4) == (wscr[excl + q] >> 4);
-    if (dup || big || all) {
+    // apply, one hit per lane (converged: a chunk lane walking its own hits left
+    // half the lanes idle): hit j of the pass belongs to the chunk lane found by
+    // the same search; chunks on the reference path are skipped here
+    const bool slow = dup || big || all;
+    const uint32_t slowm = __ballot_sync(0xFFFFFFFFu, slow);
+    for (uint32_t j0 = 0; j0 < H; j0 += 32) {
+        const uint32_t j = j0 + (uint32_t)lane;
+        uint32_t lo = 0;
+#pragma unroll
+        for (int st = 16; st > 0; st >>= 1) {
+            const uint32_t pv = __shfl_sync(0xFFFFFFFFu, pre, (int)(lo + st - 1));
+            if (pv <= j) lo += st;
+        }
+        const int owner = (int)(lo > 31u ? 31u : lo);
+        const uint32_t oo = __shfl_sync(0xFFFFFFFFu, o, owner);
+        const uint32_t obase = __shfl_sync(0xFFFFFFFFu, r * L, owner);
+        const uint32_t ovlen = __shfl_sync(0xFFFFFFFFu, vlen, owner);
+        if (j < H && !((slowm >> owner) & 1u)) {
+            const uint32_t e = wscr[j];
+            if ((e >> 4) < ovlen) apply(oo, obase + (e >> 4), e & 15u);
+        }
+    }
+    if (slow) {
         const NoiseOp nz = noise_op_of(np, o);
         noise_chunk(tk, nz, kp.noise_tab, r, vlen, sl,
                     [&](uint32_t pos, uint32_t pick) { apply(o, r * L + pos, pick); });
-    } else if (c) {
-        for (uint32_t h = 0; h < c; h++) {
-            const uint32_t e = wscr[excl + h];
-            if ((e >> 4) < vlen) apply(o, r * L + (e >> 4), e & 15u);
-        }
     }
     __syncwarp();
 }
