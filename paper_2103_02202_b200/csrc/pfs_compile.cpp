@@ -839,12 +839,6 @@ void lower_stream(HostProgram& hp, int W, int warps_per_group) {
         default: break;  // standalone noise reads its DOp
         }
         s.off = blk.empty() ? o.off : add_block(blk);
-        // the block is prefetched while the previous op runs: its extent goes
-        // into that op's descriptor
-        if (i > 0) {
-            hp.sops[i - 1].pf_words = (uint32_t)blk.size();
-            hp.sops[i - 1].r1 = s.off;
-        }
     }
     uint32_t next = NO_SLOT;
     for (size_t i = hp.sops.size(); i-- > 0;) {

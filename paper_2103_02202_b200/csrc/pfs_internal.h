@@ -100,10 +100,10 @@ struct SOp {
     uint32_t a, b;       // as in DOp (first record / column / accumulator, first coin row)
     uint32_t span;       // F_PRESAMPLED: ordinal * list_warps (index of warp 0's span)
     uint32_t next_span;  // span index of the next F_PRESAMPLED op (this op's when it is the last)
-    uint32_t pf_words;   // the NEXT op's operand block: length in words (prefetched while this op runs)
+    uint32_t r2;         // reserved
     uint32_t ordinal;    // noise ordinal (fused or standalone), else NO_SLOT
     uint32_t r0;         // GATE: applications per warp (the warp's share)
-    uint32_t r1;         // the NEXT op's operand block: arena offset
+    uint32_t r1;         // reserved
 };
 static_assert(sizeof(SOp) == 48, "SOp is 48 bytes");
 constexpr uint32_t STREAM_NOP = 0xFFFFFFFFu;
