@@ -1115,6 +1115,46 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
             auto src = [&](uint32_t t) -> const uint32_t* {
                 return (t & XROW) ? X + (size_t)(t & ~XROW) * W : ring + (size_t)t * W;
             };
+            if (RING_SMEM && code >= 1u && code <= 2u && kp.counts == nullptr && kp.ev_out != nullptr) {
+                // one or two terms per column, events to the scratch table: all
+                // term loads of a batch, then all row loads, then the stores
+                constexpr uint32_t RB = W * 4;
+                constexpr int U = 4;
+                const uint32_t xa = (uint32_t)__cvta_generic_to_shared(X);
+                const uint32_t ra = (uint32_t)__cvta_generic_to_shared(ring);
+                uint32_t* const evt = kp.ev_out + tile * kp.out_tile_stride;
+                const int64_t rs = kp.out_row_stride;
+                for (int i0 = tid; i0 < items; i0 += U * nth) {
+                    uint32_t t0[U], t1[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int i = i0 + u * nth;
+                        t0[u] = t1[u] = NO_SLOT;
+                        if (i < items) {
+                            const uint32_t* const e = kp.arena + off + (uint32_t)(i >> LC) * code;
+                            t0[u] = __ldg(e);
+                            if (code == 2u) t1[u] = __ldg(e + 1);
+                        }
+                    }
+                    VW<V> a[U], b[U];
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const uint32_t cb = (uint32_t)((i0 + u * nth) & (C - 1)) * (V * 4);
+                        a[u] = b[u] = vzero<V>();
+                        if (t0[u] != NO_SLOT)
+                            a[u] = slds<V>(((t0[u] & XROW) ? xa + (t0[u] & ~XROW) * RB : ra + t0[u] * RB) + cb);
+                        if (t1[u] != NO_SLOT)
+                            b[u] = slds<V>(((t1[u] & XROW) ? xa + (t1[u] & ~XROW) * RB : ra + t1[u] * RB) + cb);
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; u++) {
+                        const int i = i0 + u * nth;
+                        if (i < items)
+                            vst<V>(evt + (int64_t)(oa + (uint32_t)(i >> LC)) * rs + (i & (C - 1)) * V, vxor<V>(a[u], b[u]));
+                    }
+                }
+                break;
+            }
             const uint32_t* const tb = code ? kp.arena : kp.det_terms;
             batched_items<DET_BATCH>(tid, nth, items,
                 [&](int i) {
