@@ -50,6 +50,16 @@ template <> __device__ __forceinline__ void vst<2>(uint32_t* p, const VW<2>& v) 
 }
 template <> __device__ __forceinline__ void vst<1>(uint32_t* p, const VW<1>& v) { *p = v.w[0]; }
 
+// streaming (evict-first) global stores
+template <int V> __device__ __forceinline__ void vstcs(uint32_t* p, const VW<V>& v);
+template <> __device__ __forceinline__ void vstcs<4>(uint32_t* p, const VW<4>& v) {
+    __stcs(reinterpret_cast<uint4*>(p), make_uint4(v.w[0], v.w[1], v.w[2], v.w[3]));
+}
+template <> __device__ __forceinline__ void vstcs<2>(uint32_t* p, const VW<2>& v) {
+    __stcs(reinterpret_cast<uint2*>(p), make_uint2(v.w[0], v.w[1]));
+}
+template <> __device__ __forceinline__ void vstcs<1>(uint32_t* p, const VW<1>& v) { __stcs(p, v.w[0]); }
+
 template <int V> __device__ __forceinline__ VW<V> vxor(const VW<V>& a, const VW<V>& b) {
     VW<V> r;
 #pragma unroll
@@ -1149,8 +1159,8 @@ __device__ __forceinline__ void frame_tile_body(const KParams& kp, const int64_t
 #pragma unroll
                     for (int u = 0; u < U; u++) {
                         const int i = i0 + u * nth;
-                        if (i < items)
-                            vst<V>(evt + (int64_t)(oa + (uint32_t)(i >> LC)) * rs + (i & (C - 1)) * V, vxor<V>(a[u], b[u]));
+                        if (i < items)  // streaming store: the scratch must not evict the hit lists from L2
+                            vstcs<V>(evt + (int64_t)(oa + (uint32_t)(i >> LC)) * rs + (i & (C - 1)) * V, vxor<V>(a[u], b[u]));
                     }
                 }
                 break;
