@@ -287,10 +287,14 @@ int pfs_program_create(const pfs_instr* instrs, int64_t n_instrs, const int32_t*
         const int V = W >= 4 ? 4 : W;
         for (int m = 0; m < (dem ? 1 : 2); m++) {
             HostProgram& hp = pg->fl[m].hp;
-            permute_rows(hp, (dem || W >= 32) ? 1 : 128 / (W * 4));
-            dedup_operands(hp);
             // the error-model kernel's chunks span whole 32-shot tiles
             build_noise_schedule(hp, 32 * W, dem ? 32 : 32 * V, th, dem ? th : thf);
+            // row placement needs the warps' application ranges, hence the chunk
+            // geometry; it rewrites every op's targets, so it runs before
+            // identical operand blocks are shared
+            permute_rows(hp, (dem || W >= 32) ? 1 : 128 / (W * 4),
+                         dem ? 0 : cfg.threads / std::max(1, cfg.groups) / 32);
+            dedup_operands(hp);
             if (!dem) {
                 const int wpg = cfg.threads / std::max(1, cfg.groups) / 32;
                 if (pg->opts.presample_noise >= 0) build_hit_lists(hp, 32 * W, wpg);

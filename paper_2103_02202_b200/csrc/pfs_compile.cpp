@@ -29,6 +29,8 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <stdexcept>
 #include <string>
@@ -613,7 +615,88 @@ HostProgram compile_program(const pfs_instr* ins, int64_t n_ins, const int32_t* 
 // lattice patterns whose residues mod the bank-group count are badly
 // unbalanced (d=25 CX layers: controls mod 4 = {231, 75, 219, 75}), which no
 // reordering of one layer can make conflict-free.  row_of[q] = row of qubit q.
-void permute_rows(HostProgram& hp, int bank_classes) {
+static uint32_t warp_share(uint32_t apps, uint32_t nw, uint32_t ca);
+
+// Local search over the bank classes of the qubits.  Cost = for every gate op,
+// every warp's share of its applications (the range one warp walks,
+// lower_stream) and each operand: the applications in excess of an even split
+// over the G classes — with none, the warp's passes can be ordered so that every
+// shared-memory wavefront serves G distinct bank groups (bank_reorder).  Moves
+// swap the classes of two qubits (class sizes stay what the row pools can hold);
+// a move is kept when it does not raise the cost.  Ops with identical target
+// lists (the rounds of a REPEAT body) are counted once, weighted.  Measured with
+// tools/bank_model.py at d=25 (4 classes): CX row wavefronts 1.45x -> 1.08x the
+// conflict-free count.  With 32 classes (one-word tiles, d=100) an even split
+// is not enough for the greedy grouping (2.05x vs 1.85x for the first-appearance
+// classes, whose order is already regular), so the search runs for G <= 8 only;
+// a cost on aligned groups in instruction order converged worse in both cases.
+static void refine_classes(const HostProgram& hp, std::vector<int32_t>& cls, uint32_t G, uint32_t nw) {
+    struct Occ { uint32_t cell; uint32_t w; };
+    const uint32_t n = (uint32_t)hp.num_qubits;
+    std::unordered_map<uint64_t, uint32_t> uniq;   // target-list hash -> unique op
+    std::vector<uint32_t> weight, first_op;
+    for (size_t i = 0; i < hp.ops.size(); i++) {
+        const DOp& o = hp.ops[i];
+        if ((o.kcf & 0xFF) != K_GATE || o.count == 0) continue;
+        const int ar = rule_arity((o.kcf >> 8) & 0xFF);
+        uint64_t h = 1469598103934665603ull ^ ((uint64_t)o.count * 2 + ar);
+        for (uint32_t j = 0; j < o.count * ar; j++) { h ^= hp.targets[o.off + j]; h *= 1099511628211ull; }
+        auto it = uniq.find(h);
+        if (it == uniq.end()) { uniq.emplace(h, (uint32_t)weight.size()); weight.push_back(1); first_op.push_back((uint32_t)i); }
+        else weight[it->second]++;
+    }
+    const size_t U = weight.size();
+    if (U == 0) return;
+    std::vector<std::vector<Occ>> occ(n);
+    std::vector<int32_t> cnt(U * nw * 2 * G, 0), cap(U * nw * 2, 0);
+    for (size_t u = 0; u < U; u++) {
+        const DOp& o = hp.ops[first_op[u]];
+        const int ar = rule_arity((o.kcf >> 8) & 0xFF);
+        const uint32_t ca = ((o.kcf >> 16) & F_NOISE) && o.c != NO_SLOT && o.c < hp.noise.size() ? hp.noise[o.c].ca : 1u;
+        const uint32_t Kc = std::max<uint32_t>(1u, warp_share(o.count, nw, ca));
+        for (uint32_t j = 0; j < o.count; j++) {
+            const uint32_t r = std::min(nw - 1, j / Kc);
+            for (int s2 = 0; s2 < ar; s2++) {
+                const uint32_t q = hp.targets[o.off + (size_t)j * ar + s2];
+                const uint32_t cell = (uint32_t)((u * nw + r) * 2 + s2);
+                occ[q].push_back(Occ{cell, weight[u]});
+                if (cls[q] >= 0) cnt[(size_t)cell * G + cls[q]]++;
+                cap[cell]++;
+            }
+        }
+    }
+    for (int32_t& c : cap) c = (c + (int32_t)G - 1) / (int32_t)G;  // even split
+    std::vector<uint32_t> movable;
+    for (uint32_t q = 0; q < n; q++)
+        if (cls[q] >= 0 && !occ[q].empty()) movable.push_back(q);
+    if (movable.size() < 2) return;
+    auto over = [&](uint32_t cell, int32_t c) { return std::max(0, cnt[(size_t)cell * G + c] - cap[cell]); };
+    auto move = [&](uint32_t q, int32_t from, int32_t to) -> int64_t {  // returns the cost change
+        int64_t d = 0;
+        for (const Occ& oc : occ[q]) {
+            d -= (int64_t)oc.w * (over(oc.cell, from) + over(oc.cell, to));
+            cnt[(size_t)oc.cell * G + from]--;
+            cnt[(size_t)oc.cell * G + to]++;
+            d += (int64_t)oc.w * (over(oc.cell, from) + over(oc.cell, to));
+        }
+        return d;
+    };
+    uint64_t st = 0xD1B54A32D192ED03ull ^ n;
+    auto rnd = [&]() { st += 0x9E3779B97F4A7C15ull; uint64_t z = st; z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+                       z = (z ^ (z >> 27)) * 0x94D049BB133111EBull; return z ^ (z >> 31); };
+    const uint64_t iters = std::min<uint64_t>(6000000ull, 600ull * movable.size());
+    for (uint64_t it = 0; it < iters; it++) {
+        const uint32_t a = movable[rnd() % movable.size()], b = movable[rnd() % movable.size()];
+        const int32_t ca2 = cls[a], cb2 = cls[b];
+        if (ca2 == cb2) continue;
+        int64_t d = move(a, ca2, cb2);
+        d += move(b, cb2, ca2);
+        if (d <= 0) { cls[a] = cb2; cls[b] = ca2; }
+        else { move(b, ca2, cb2); move(a, cb2, ca2); }
+    }
+}
+
+void permute_rows(HostProgram& hp, int bank_classes, int warps_per_group) {
     const uint32_t n = (uint32_t)hp.num_qubits;
     hp.row_of.resize(n);
     for (uint32_t q = 0; q < n; q++) hp.row_of[q] = q;
@@ -646,6 +729,22 @@ void permute_rows(HostProgram& hp, int bank_classes) {
                     if (cls[q] < 0) cls[q] = (int32_t)(j % G);
                 }
         }
+        // class sizes must fit the row pools: move the overflow to the emptiest classes
+        {
+            std::vector<uint32_t> size(G, 0), room(G, 0);
+            for (uint32_t q = 0; q < n; q++) room[hp.row_of[q] % G]++;
+            for (uint32_t q = 0; q < n; q++) if (cls[q] >= 0) size[cls[q]]++;
+            for (uint32_t q = n; q-- > 0;) {
+                if (cls[q] < 0 || size[cls[q]] <= room[cls[q]]) continue;
+                uint32_t best = 0;
+                for (uint32_t c = 1; c < G; c++)
+                    if ((int64_t)room[c] - size[c] > (int64_t)room[best] - size[best]) best = c;
+                size[cls[q]]--;
+                cls[q] = (int32_t)best;
+                size[best]++;
+            }
+        }
+        if (warps_per_group > 0 && G <= 8) refine_classes(hp, cls, G, (uint32_t)warps_per_group);
         // pools: the rows of each class, in the order of the random permutation
         std::vector<std::vector<uint32_t>> pool(G);
         for (uint32_t q = 0; q < n; q++) pool[hp.row_of[q] % G].push_back(hp.row_of[q]);

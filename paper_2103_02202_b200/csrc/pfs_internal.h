@@ -193,7 +193,7 @@ HostProgram compile_program(const pfs_instr* instrs, int64_t n_instrs, const int
 // chunk of standalone and of fused noise instructions
 void build_noise_schedule(HostProgram& hp, int tile_shots, int vector_shots, double target_hits,
                           double fused_target_hits);
-void permute_rows(HostProgram& hp, int bank_classes);
+void permute_rows(HostProgram& hp, int bank_classes, int warps_per_group);
 void build_hit_lists(HostProgram& hp, int tile_shots, int warps_per_group);
 void lower_stream(HostProgram& hp, int W, int warps_per_group);
 void dedup_operands(HostProgram& hp);
