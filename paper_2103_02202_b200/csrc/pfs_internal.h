@@ -114,7 +114,7 @@ constexpr int DUMMY_ROWS = 4;
 // operand words of the next gate op a lane loads ahead (frame kernel GATE_AHEAD):
 // every warp block of a gate op is padded to at least this many passes
 #ifndef PFS_GATE_AHEAD
-#define PFS_GATE_AHEAD 6
+#define PFS_GATE_AHEAD 4
 #endif
 constexpr uint32_t GATE_AHEAD_PASSES = PFS_GATE_AHEAD;
 

@@ -33,7 +33,7 @@ NO_SLOT = 0xFFFFFFFF
 COIN_DEAD = 0x80000000
 XROW = 0x80000000
 DUMMY_ROWS = 4
-GATE_AHEAD = 6
+GATE_AHEAD = 4
 
 
 def _tables(p, flavour):

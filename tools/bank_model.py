@@ -40,7 +40,7 @@ def main():
         code = (int(op[0]) >> 8) & 0xFF
         ar = 2 if code >= 4 else 1
         K = int(so[3])
-        stride = max(K, 6) * PI
+        stride = max(K, 4) * PI
         blk = arena[int(so[2]): int(so[2]) + wpg * stride].reshape(wpg, stride)
         wf = ideal = 0
         for w in range(wpg):
