@@ -514,22 +514,28 @@ static inline uint64_t transpose8x8(uint64_t x) {
 static void* b8_worker(void* arg) {
     const b8_job* j = (const b8_job*)arg;
     const int64_t nb = (j->num_rows + 7) / 8;
-    for (int64_t s8 = j->s0; s8 < j->s1; s8 += 8) {       /* 8 shots */
+    /* 512 shots (one 64-byte line of every row) at a time: the 8 input lines of a
+     * row block are used up before the next block is touched, and the 512 output
+     * lines stay cached while the row blocks fill them byte by byte -- whatever
+     * the row pitch (a power-of-two pitch maps every row to one cache set). */
+    for (int64_t c0 = j->s0; c0 < j->s1; c0 += 512) {
+        const int64_t c1 = c0 + 512 < j->s1 ? c0 + 512 : j->s1;
         for (int64_t rb = 0; rb < nb; rb++) {              /* 8 rows */
-            uint64_t blk = 0;
-            for (int i = 0; i < 8; i++) {
-                const int64_t r = rb * 8 + i;
-                if (r >= j->num_rows) break;
-                const uint32_t* row = j->rows + r * j->row_words;
-                uint32_t byte = (uint32_t)((row[s8 >> 5] >> (s8 & 31)) & 0xFFu);
-                if (j->xor_bits && (j->xor_bits[r] & 1)) byte ^= 0xFFu;
-                blk |= (uint64_t)byte << (8 * i);
-            }
-            blk = transpose8x8(blk);
-            for (int k = 0; k < 8 && s8 + k < j->num_shots; k++) {
-                uint8_t v = (uint8_t)(blk >> (8 * k));
-                if (rb == nb - 1 && (j->num_rows & 7)) v &= (uint8_t)((1u << (j->num_rows & 7)) - 1);
-                j->out[(s8 + k) * j->pitch + rb] = v;
+            const int nr = (int)(j->num_rows - rb * 8 < 8 ? j->num_rows - rb * 8 : 8);
+            const uint8_t last_mask = (rb == nb - 1 && (j->num_rows & 7)) ? (uint8_t)((1u << (j->num_rows & 7)) - 1) : 0xFFu;
+            uint32_t flip[8];
+            for (int i = 0; i < nr; i++)
+                flip[i] = (j->xor_bits && (j->xor_bits[rb * 8 + i] & 1)) ? 0xFFu : 0u;
+            for (int64_t s8 = c0; s8 < c1; s8 += 8) {      /* 8 shots */
+                uint64_t blk = 0;
+                for (int i = 0; i < nr; i++) {
+                    const uint32_t* row = j->rows + (rb * 8 + i) * j->row_words;
+                    uint32_t byte = ((row[s8 >> 5] >> (s8 & 31)) & 0xFFu) ^ flip[i];
+                    blk |= (uint64_t)byte << (8 * i);
+                }
+                blk = transpose8x8(blk);
+                for (int k = 0; k < 8 && s8 + k < j->num_shots; k++)
+                    j->out[(s8 + k) * j->pitch + rb] = (uint8_t)(blk >> (8 * k)) & last_mask;
             }
         }
     }
