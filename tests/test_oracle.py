@@ -177,3 +177,8 @@ def test_oracle_rows_to_b8_threads_agree(oracle_lib):
     ref = np.packbits(rows_unpack(rows, shots) ^ xor[None, :], axis=1, bitorder="little")
     for nt in (1, 3, 8):
         assert np.array_equal(oracle_lib.rows_to_b8(rows, shots, xor, nthreads=nt), ref)
+    # power-of-two row pitch, whole 512-shot chunks, rows a multiple of 8, no xor
+    rows = rng.integers(0, 2 ** 32, size=(64, 64), dtype=np.uint64).astype(np.uint32)
+    ref = np.packbits(rows_unpack(rows, 2048), axis=1, bitorder="little")
+    for nt in (1, 5):
+        assert np.array_equal(oracle_lib.rows_to_b8(rows, 2048, nthreads=nt), ref)
