@@ -1452,13 +1452,14 @@ __global__ void __launch_bounds__(256) tiles_to_b8_kernel(const uint32_t* __rest
     const int64_t s0 = tile * 32 * TW + part * 32 * W;
     const bool full = (pitch & 15) == 0 && ((uintptr_t)out & 15) == 0 && b0 + 32 <= pitch;
     if (full) {
-        for (int sl = t; sl < 32 * W; sl += 256) {
+        // two lanes per shot, 16 bytes each: a store instruction writes 16
+        // whole 32-byte runs instead of 32 half ones
+        for (int i = t; i < 64 * W; i += 256) {
+            const int sl = i >> 1, half = i & 1;
             const int64_t s = s0 + sl;
             if (s >= num_shots) break;
-            const uint32_t* o = tout + sl * 9;
-            uint4* dst = reinterpret_cast<uint4*>(out + s * pitch + b0);
-            dst[0] = make_uint4(o[0], o[1], o[2], o[3]);
-            dst[1] = make_uint4(o[4], o[5], o[6], o[7]);
+            const uint32_t* o = tout + sl * 9 + 4 * half;
+            reinterpret_cast<uint4*>(out + s * pitch + b0)[half] = make_uint4(o[0], o[1], o[2], o[3]);
         }
     } else {
         for (int sl = warp; sl < 32 * W; sl += 8) {
