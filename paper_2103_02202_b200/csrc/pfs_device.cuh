@@ -221,13 +221,22 @@ __device__ __forceinline__ uint32_t chunk_fast(const TileKey& tk, const NoiseOp&
 
 __device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
     // lane l holds row l (bit b = column b); afterwards lane l holds column l.
+    // Stage j swaps, between lanes l and l ^ j, the off-diagonal j-bit blocks.
+    // j = 16, 8 move whole bytes: one PRMT with a per-lane selector.
+    uint32_t o = __shfl_xor_sync(0xFFFFFFFFu, v, 16);
+    v = __byte_perm(v, o, (lane & 16) ? 0x3276u : 0x5410u);
+    o = __shfl_xor_sync(0xFFFFFFFFu, v, 8);
+    v = __byte_perm(v, o, (lane & 8) ? 0x3715u : 0x6240u);
+    // j = 4, 2, 1: rotate the partner's word into place (the bits that wrap
+    // around fall outside the inserted mask), then one bit-select
 #pragma unroll
-    for (int j = 16; j > 0; j >>= 1) {
-        const uint32_t mlo = j == 16 ? 0x0000FFFFu : j == 8 ? 0x00FF00FFu : j == 4 ? 0x0F0F0F0Fu
-                           : j == 2 ? 0x33333333u : 0x55555555u;
-        const uint32_t other = __shfl_xor_sync(0xFFFFFFFFu, v, j);
-        if (lane & j) v = (v & ~mlo) | ((other >> j) & mlo);
-        else v = (v & mlo) | ((other & mlo) << j);
+    for (int j = 4; j > 0; j >>= 1) {
+        const uint32_t mlo = j == 4 ? 0x0F0F0F0Fu : j == 2 ? 0x33333333u : 0x55555555u;
+        const bool hi = (lane & j) != 0;
+        const uint32_t keep = hi ? ~mlo : mlo;
+        o = __shfl_xor_sync(0xFFFFFFFFu, v, j);
+        o = __funnelshift_l(o, o, hi ? 32 - j : j);
+        v = (v & keep) | (o & ~keep);
     }
     return v;
 }
